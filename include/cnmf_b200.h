@@ -1,0 +1,174 @@
+/*
+ * cnmf_b200.h — C ABI of the B200-native compressed-NMF hot path.
+ *
+ * The reference (arxiv/paper_1505_04650, package `cnmf`) is pure Python/numpy;
+ * its FFI for this path would be a ctypes binding of exactly these entry
+ * points (see INTEGRATION.md for the stub). Every pointer argument marked
+ * "device" is CUDA device memory on the current device; `stream` is a
+ * cudaStream_t (NULL = legacy default stream). Calls are stream-ordered unless
+ * they return host-visible results, in which case they synchronise `stream`.
+ *
+ * Layouts
+ *   A        : fp32 row-major m x n, leading dimension lda (elements),
+ *              lda % 4 == 0 and 16-byte aligned base (TMA requirement).
+ *   panel    : a tall-skinny matrix with s logical columns stored row-major
+ *              with leading dimension ldp = cnmf_panel_ld(s) >= s; the
+ *              padding columns are kept zero. Q (m x s), the row-space basis
+ *              R^T (n x s) and the reduced matrix (Q^T A)^T (n x s) are panels.
+ *
+ * Every function returns a cnmf_status; cnmf_last_error() describes the most
+ * recent failure on the calling thread. Error codes map one-to-one onto the
+ * reference's exception classes (errors.py).
+ */
+#ifndef CNMF_B200_H
+#define CNMF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CNMF_OK = 0,
+  CNMF_ERR_ARGUMENT = 1,          /* errors.py:13  ArgumentError */
+  CNMF_ERR_INFEASIBLE_RANK = 2,   /* errors.py:17  InfeasibleRankError */
+  CNMF_ERR_NUMERIC = 3,           /* errors.py:21  NumericError */
+  CNMF_ERR_RANK_DEFICIENCY = 4,   /* errors.py:48  RankDeficiencyError */
+  CNMF_ERR_CONVERGENCE = 5,       /* errors.py:30  ConvergenceError */
+  CNMF_ERR_DIVERGENCE = 6,        /* errors.py:39  DivergenceError */
+  CNMF_ERR_UNDEFINED_METRIC = 7,  /* errors.py:57  UndefinedMetricError */
+  CNMF_ERR_CUDA = 8,              /* device / launch failure (no reference analogue) */
+} cnmf_status;
+
+typedef enum { CNMF_F32 = 0, CNMF_F64 = 1 } cnmf_dtype;
+
+/* ---- library ------------------------------------------------------------ */
+int cnmf_abi_version(void);
+const char* cnmf_last_error(void);
+/* padded leading dimension used for s-column panels (multiple of 32) */
+int cnmf_panel_ld(int s);
+/* instrumentation: kernels launched by this library so far (process-wide),
+ * and optional CUDA-event timing of the streaming passes over A: total
+ * device milliseconds, launch count and algorithmic bytes since enabled. */
+int64_t cnmf_launch_count(void);
+void cnmf_set_pass_profiling(int on);
+int cnmf_pass_stats(double* total_ms, int64_t* launches, double* bytes);
+
+/* ---- RNG (rng.py) --------------------------------------------------------
+ * cnmf_child_seed             replaces rng.py:73 child_seed / rng.py:56 Rng.child
+ * cnmf_gaussian_fill          replaces compress.py:115 _drawn_in_chunks /
+ *                             compress.py:125 draw_test_matrix (chunk_rows=4096)
+ *                             and rng.py:78 gaussian_matrix (chunk_rows=0).
+ *                             Bit-identical to numpy Generator(Philox(key))
+ *                             .standard_normal. out: device, rows x cols, ld.
+ * cnmf_uniform_fill           replaces rng.py:63 Rng.uniform (row-major
+ *                             rows x cols stream); transpose=1 stores the
+ *                             stream transposed (cols x rows, ld=rows).
+ */
+uint64_t cnmf_child_seed(uint64_t seed, const char* tag);
+int cnmf_gaussian_fill(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_rows, int dtype, void* out,
+                       int64_t ld, void* stream);
+int cnmf_uniform_fill(uint64_t seed, int64_t rows, int64_t cols, double low, double high, int dtype,
+                      int transpose, void* out, void* stream);
+
+/* ---- streaming passes over A (store.py:578 matmul_blocked,
+ *      store.py:600 matmul_transposed_blocked) --------------------------------
+ * forward  : Y (m x s panel)  = A X,    X (n x s panel)
+ * transpose: Z (n x s panel)  = A^T W,  W (m x s panel)
+ * Outputs are overwritten (the kernels zero them first).
+ */
+int cnmf_pass_forward(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int s, float* Y,
+                      void* stream);
+int cnmf_pass_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const float* W, int s, float* Z,
+                        void* stream);
+
+/* ---- structured compression (compress.py:156 structured_compress,
+ *      compress.py:202 structured_compress_rows, nmf.py:120 _compression_pair)
+ * side = 0: Q (m x s panel) spans the dominant column space of A.
+ * side = 1: Q (n x s panel) spans the dominant row space (= basis of A^T).
+ * Power passes are re-orthonormalised implicitly (CholeskyQR2 with fp64
+ * Gram matrices); the final basis is sign-canonical (diag(R) > 0).
+ * The Gaussian test matrix is the reference's, drawn from `seed`.
+ * ws: device workspace of cnmf_compress_workspace(m, n, s) bytes.
+ */
+size_t cnmf_compress_workspace(int64_t m, int64_t n, int s);
+int cnmf_structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed,
+                             int side, float* Q, void* ws, size_t ws_bytes, void* stream);
+/* orthonormalise a panel in place (compress.py:136 canonical_qr, Q factor);
+ * R (s x s, fp64, device, may be NULL) receives the triangular factor. */
+int cnmf_orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- separable NMF (snmf.py) ---------------------------------------------
+ * The reduced matrix (Q^T A, s x n) is kept transposed: W (n x ld, fp64,
+ * device) holds column j of the reduced matrix in row j.
+ * cnmf_panel_to_f64     converts an fp32 panel (rows x S) into such a W.
+ * cnmf_select_spa       replaces snmf.py:39 select_columns_spa. W is
+ *                       overwritten by the projected residual. picks: host
+ *                       int64[r]; *n_picks = picks found (also on
+ *                       CNMF_ERR_RANK_DEFICIENCY, errors.py:48 .picks).
+ * cnmf_select_xray      replaces snmf.py:74 select_columns_xray (mass: device
+ *                       s-vector, the column-mass functional).
+ * cnmf_right_factor     replaces snmf.py:129 snmf_right_factor: Ht (n x k) =
+ *                       NNLS coefficients (transposed) of every column over
+ *                       the k picked ones; d_picks: device int64[k].
+ *                       *n_capped = columns that hit the exchange cap.
+ * cnmf_refit_norms      out[0] = ||W - W[:,K] H||^2, out[1] = ||W||^2 (device)
+ *                       (snmf.py:218-221 rel_error_reduced).
+ */
+size_t cnmf_spa_workspace(int64_t n, int s);
+int cnmf_panel_to_f64(const float* src, int64_t rows, int S, double* dst, int64_t ld, void* stream);
+int cnmf_select_spa(double* W, int64_t n, int s, int64_t ld, int r, int64_t* picks, int* n_picks, void* ws,
+                    size_t ws_bytes, void* stream);
+int cnmf_select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const double* mass, double nnls_tol,
+                     int64_t* picks, int* n_picks, void* stream);
+int cnmf_right_factor(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_picks, int k, double tol,
+                      double* Ht, int64_t* n_capped, void* stream);
+int cnmf_refit_norms(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_picks, int k,
+                     const double* Ht, double* out, void* stream);
+/* batched active-set NNLS (nnls.py:21 nnls_solve) on precomputed Gram
+ * products: gram (q x q) = C^T C, target (k x q) = (C^T D)^T, H (k x q) out;
+ * fp64, device. tol / max_exchanges (0 = 3q) as in the reference. */
+int cnmf_nnls_gram(const double* gram, const double* target, int64_t k, int q, double tol, int max_exchanges,
+                   double* H, int64_t* n_capped, void* stream);
+/* out (a x b, fp64, device) = X^T Y for row-aligned fp64 X (p x a), Y (p x b):
+ * the shared Gram products of nnls.py:64-65. */
+int cnmf_gram_f64(const double* X, int64_t p, int a, const double* Y, int b, double* out, void* stream);
+
+/* ---- projections (nmf.py:138 _projected_data, nmf.py:329-332) ------------
+ * out (S x S, fp64, device) = P1^T P2 for row-aligned panels (S = 32, 64). */
+int cnmf_panel_cross(const float* P1, const float* P2, int64_t rows, int S, double* out, void* stream);
+
+/* ---- relative error (nmf.py:53 relative_error) ---------------------------
+ * out[0] = ||A - X Y||_F^2, out[1] = ||A||_F^2 (device, fp64).
+ * X: m x r fp64 row-major, Yt: n x r fp64 row-major (Y transposed).
+ * cols (optional, may be NULL): when given, X is gathered as A[:, cols]
+ * (snmf.py:223-230 full-space error; X must then be NULL). */
+int cnmf_residual_norms(const float* A, int64_t m, int64_t n, int64_t lda, const double* X, const int64_t* cols,
+                        const double* Yt, int r, double* out, void* stream);
+
+/* ---- compressed ADMM NMF (nmf.py:306 nmf_admm) --------------------------
+ * core : s x s fp64 (L^T A R^T), L : m x s panel, Rt : n x s panel (fp32).
+ * u, du: m x r fp64; vt, dvt: n x r fp64 (V and its dual, transposed).
+ * u / vt hold the initial splits on entry; du / dvt are zeroed here.
+ * xc (s x r), yc (r x s) fp64 device. trace / scores: device fp64[max_iter].
+ * Runs up to max_iter iterations with the reference's stopping rule (max KKT
+ * residual < tol) and divergence rule (10x over 50 iterations), checked on
+ * the device; *iterations (host) receives the iteration count.
+ * Returns CNMF_ERR_DIVERGENCE with *iterations = detection iteration + 1.
+ */
+size_t cnmf_admm_workspace(int64_t m, int64_t n, int s, int r);
+/* resume = 0 starts from the initial splits; resume = 1 continues a run
+ * (same workspace). step_limit > 0 runs at most that many iterations in this
+ * call (used to drive the reference's on_iteration callback); 0 = run to
+ * completion. *done (host) = 1 once the run has stopped. */
+int cnmf_admm_run(const double* core, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r,
+                  double* u, double* du, double* vt, double* dvt, double* xc, double* yc, double pu, double pv,
+                  double step, int max_iter, double tol, double* trace, double* scores, int* iterations, int* done,
+                  int resume, int step_limit, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CNMF_B200_H */

@@ -160,14 +160,21 @@ def gaussian_basis(m, s, seed):
 
 
 def projector_distance(q1, q2):
-    """||Q1 Q1^T - Q2 Q2^T||_2 for orthonormal Q1, Q2 (north-star parity metric)."""
-    # the spectral norm of the projector difference equals sin of the largest
-    # principal angle; compute it from the singular values of Q1^T Q2
-    s = np.linalg.svd(q1.T @ q2, compute_uv=False)
-    if q1.shape[1] != q2.shape[1]:
+    """||Q1 Q1^T - Q2 Q2^T||_2 for orthonormal Q1, Q2 of equal width (the
+    north-star parity metric) = sine of the largest principal angle, computed
+    as ||Q2 - Q1 (Q1^T Q2)||_2 (accurate for small angles)."""
+    q1 = np.asarray(q1, dtype=np.float64)
+    q2 = np.asarray(q2, dtype=np.float64)
+    if q1.shape != q2.shape:
         return 1.0
-    c = np.clip(s.min(), -1.0, 1.0)
-    return float(np.sqrt(max(0.0, 1.0 - c * c)))
+    return float(np.linalg.norm(q2 - q1 @ (q1.T @ q2), 2))
+
+
+def dominant_subspace(q, a, k):
+    """Orthonormal basis of the top-k left singular subspace of Q Q^T A: the
+    numerically determined part of a range basis on low-rank + noise data."""
+    u = np.linalg.svd(q.T @ a, full_matrices=False)[0][:, :k]
+    return q @ u
 
 
 # ----------------------------------------------------------------------------

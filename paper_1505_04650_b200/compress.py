@@ -1,0 +1,160 @@
+"""Structured random compression on the B200 (reference compress.py).
+
+Public functions keep the reference's signatures:
+
+* ``structured_compress(a, cfg, reorthogonalize=False, scratch_dir=None)``
+  (compress.py:156-199) — column-space basis, one C-ABI call
+  (``cnmf_structured_compress``) that draws the reference's Gaussian test
+  matrix on the device, streams the 2w+1 passes over A and orthonormalises.
+* ``structured_compress_rows`` (compress.py:202-227) — row-space basis.
+* ``gaussian_compress`` (compress.py:238-247), ``compression_error``
+  (compress.py:250-265), ``adjust_config`` (compress.py:101-112),
+  ``draw_test_matrix`` (compress.py:125-127).
+
+``reorthogonalize`` is accepted for signature compatibility; the device path
+always re-orthonormalises between passes (deferred CholeskyQR, see
+csrc/linalg.cu), which yields the same Q as the reference in exact arithmetic
+and is the numerically stable variant in floating point.
+"""
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import MASK64, DeviceMatrix, as_device64, empty, out, panel_ld, stream, workspace, zeros
+from .errors import ArgumentError, InfeasibleRankError
+from .rng import child_seed
+
+OMEGA_CHUNK = 4096  # compress.py:22
+
+
+@dataclass(frozen=True)
+class CompressionConfig:
+    """Target rank, oversampling, power passes, seed (compress.py:27-51)."""
+
+    r: int
+    r_ov: int = 10
+    w: int = 4
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.r < 1:
+            raise ArgumentError(f"target rank must be >= 1, got {self.r}")
+        if self.r_ov < 0:
+            raise ArgumentError(f"oversampling must be >= 0, got {self.r_ov}")
+        if self.w < 0:
+            raise ArgumentError(f"power exponent must be >= 0, got {self.w}")
+
+    @property
+    def basis_cols(self):
+        return self.r + self.r_ov
+
+
+@dataclass
+class CompressionBasis:
+    """Basis produced by a compression run (compress.py:54-80).
+
+    ``Q`` is an ndarray (host input) or a CUDA tensor view (device input);
+    ``panel`` is the padded device panel the other device kernels consume.
+    """
+
+    Q: object
+    kind: str
+    config: CompressionConfig
+    panel: object = None
+
+    @property
+    def cols(self):
+        return self.Q.shape[1]
+
+    @property
+    def rows(self):
+        return self.Q.shape[0]
+
+    def q_dense(self):
+        return self.Q
+
+
+def adjust_config(cfg, m, n):
+    """min(max(20, r + r_ov), n, m) sizing rule (compress.py:101-112)."""
+    if cfg.r >= min(m, n):
+        raise InfeasibleRankError(f"rank {cfg.r} infeasible for a {m}x{n} matrix (need r < min(m, n))")
+    width = min(max(20, cfg.r + cfg.r_ov), n, m)
+    return replace(cfg, r_ov=width - cfg.r)
+
+
+def _require_feasible(cfg, m, n):
+    s = cfg.basis_cols
+    if s > min(m, n):
+        raise InfeasibleRankError(f"basis width {s} exceeds min(m, n) = {min(m, n)}; adjust_config first")
+
+
+def _compress(a, cfg, side):
+    A = DeviceMatrix(a)
+    _require_feasible(cfg, A.m, A.n)
+    s = cfg.basis_cols
+    S = panel_ld(s)
+    rows = A.m if side == 0 else A.n
+    q = zeros((rows, S))
+    lib = _lib.load()
+    nbytes = lib.cnmf_compress_workspace(A.m, A.n, s)
+    ws = workspace(nbytes)
+    _lib.call("cnmf_structured_compress", A.ptr, A.m, A.n, A.lda, s, cfg.w, cfg.seed & MASK64, side,
+              q.data_ptr(), ws.data_ptr(), nbytes, stream())
+    view = q[:, :s]
+    Q = view.double().cpu().numpy() if A.on_host else view
+    return CompressionBasis(Q=Q, kind="structured", config=cfg, panel=q), A
+
+
+def structured_compress(a, cfg, reorthogonalize=False, scratch_dir=None):
+    """Orthonormal basis for the dominant column space of ``a`` (compress.py:156)."""
+    return _compress(a, cfg, 0)[0]
+
+
+def structured_compress_rows(a, cfg, reorthogonalize=False, scratch_dir=None):
+    """Orthonormal basis for the dominant row space of ``a`` (compress.py:202)."""
+    return _compress(a, cfg, 1)[0]
+
+
+def draw_test_matrix(cfg, rows, dtype=torch.float64):
+    """The seeded Gaussian test matrix, bit-identical to the reference's
+    (compress.py:125-127), generated on the device."""
+    t = empty((rows, cfg.basis_cols), dtype=dtype)
+    _lib.call("cnmf_gaussian_fill", child_seed(cfg.seed, "omega"), rows, cfg.basis_cols, OMEGA_CHUNK,
+              0 if dtype == torch.float32 else 1, t.data_ptr(), cfg.basis_cols, stream())
+    return t
+
+
+def gaussian_compress(m, s, seed):
+    """Q = s^(-1/2) * (m x s Gaussian) (compress.py:238-247), drawn on the device."""
+    if s < 1:
+        raise ArgumentError(f"projection width must be >= 1, got {s}")
+    from .rng import gaussian_matrix
+
+    g = gaussian_matrix(m, s, child_seed(seed, "gaussian-projection"))
+    cfg = CompressionConfig(r=s, r_ov=0, w=0, seed=seed)
+    return CompressionBasis(Q=(g / np.sqrt(s)).cpu().numpy(), kind="gaussian", config=cfg)
+
+
+def compression_error(a, basis, norm="frobenius"):
+    """||A - Q Q^T A||_F (compress.py:250-265) from one transpose pass and one
+    fused residual pass over A."""
+    if norm != "frobenius":
+        raise ArgumentError(f"norm {norm!r} is not supported on the device path (use 'frobenius')")
+    A = DeviceMatrix(a)
+    qd = as_device64(basis.Q if not isinstance(basis.Q, torch.Tensor) else basis.Q, "Q")
+    if qd.shape[0] != A.m:
+        raise ArgumentError(f"basis rows {qd.shape[0]} != matrix rows {A.m}")
+    s = qd.shape[1]
+    S = panel_ld(s)
+    qp = zeros((A.m, S))
+    qp[:, :s] = qd.float()
+    z = zeros((A.n, S))
+    _lib.call("cnmf_pass_transpose", A.ptr, A.m, A.n, A.lda, qp.data_ptr(), s, z.data_ptr(), stream())
+    zt = z[:, :s].double().contiguous()
+    res = zeros((2,), dtype=torch.float64)
+    _lib.call("cnmf_residual_norms", A.ptr, A.m, A.n, A.lda, qd.data_ptr(), None, zt.data_ptr(), s,
+              res.data_ptr(), stream())
+    return float(np.sqrt(max(res[0].item(), 0.0)))

@@ -1,0 +1,169 @@
+// extern "C" entry points (include/cnmf_b200.h). Thin: argument checks and
+// dispatch into the cnmf:: implementations; no torch types cross this line.
+#include "common.cuh"
+
+namespace cnmf {
+const char* last_error();
+int panel_ld(int s);
+int gaussian_fill(uint64_t, int64_t, int64_t, int64_t, int, void*, int64_t, cudaStream_t);
+int uniform_fill(uint64_t, int64_t, int64_t, double, double, int, int, void*, cudaStream_t);
+int pass_forward(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
+int pass_transpose(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
+int panel_cross(const float*, const float*, int64_t, int, double*, cudaStream_t);
+size_t compress_workspace(int64_t, int64_t, int);
+int structured_compress(const float*, int64_t, int64_t, int64_t, int, int, uint64_t, int, float*, void*, size_t,
+                        cudaStream_t);
+int orthonormalize(float*, int64_t, int, double*, void*, size_t, cudaStream_t);
+size_t spa_workspace(int64_t, int);
+int panel_to_f64(const float*, int64_t, int, double*, int64_t, cudaStream_t);
+int select_spa(double*, int64_t, int, int64_t, int, int64_t*, int*, void*, size_t, cudaStream_t);
+int select_xray(const double*, int64_t, int, int64_t, int, const double*, double, int64_t*, int*, cudaStream_t);
+int right_factor(const double*, int64_t, int, int64_t, const int64_t*, int, double, double*, double*, int64_t*,
+                 cudaStream_t);
+int refit_norms(const double*, int64_t, int, int64_t, const int64_t*, int, const double*, double*, double*, double*,
+                cudaStream_t);
+int nnls_gram(const double*, const double*, int64_t, int, double, int, double*, int64_t*, cudaStream_t);
+int residual_norms(const float*, int64_t, int64_t, int64_t, const double*, const int64_t*, const double*, int,
+                   double*, cudaStream_t);
+size_t admm_workspace(int64_t, int64_t, int, int);
+int admm_run(const double*, const float*, int64_t, const float*, int64_t, int, int, double*, double*, double*,
+             double*, double*, double*, double, double, double, int, double, double*, double*, int*, void*, size_t,
+             int, int, cudaStream_t);
+int64_t launch_count();
+void set_pass_profiling(int);
+int pass_stats(double*, int64_t*, double*);
+}  // namespace cnmf
+
+using namespace cnmf;
+
+#define STREAM(s) reinterpret_cast<cudaStream_t>(s)
+
+static int check_a(const float* A, int64_t m, int64_t n, int64_t lda) {
+  if (A == nullptr || m < 1 || n < 1) return fail(CNMF_ERR_ARGUMENT, "A must be a non-empty device matrix");
+  if (lda < n || (lda & 3) || ((uintptr_t)A & 15))
+    return fail(CNMF_ERR_ARGUMENT, "A needs lda >= n, lda % 4 == 0 and a 16-byte aligned base");
+  return CNMF_OK;
+}
+
+extern "C" {
+
+int cnmf_abi_version(void) { return 1; }
+
+const char* cnmf_last_error(void) { return last_error(); }
+
+int cnmf_panel_ld(int s) { return panel_ld(s); }
+
+int64_t cnmf_launch_count(void) { return launch_count(); }
+
+void cnmf_set_pass_profiling(int on) { set_pass_profiling(on); }
+
+int cnmf_pass_stats(double* total_ms, int64_t* launches, double* bytes) {
+  return pass_stats(total_ms, launches, bytes);
+}
+
+uint64_t cnmf_child_seed(uint64_t seed, const char* tag) { return child_seed(seed, tag); }
+
+int cnmf_gaussian_fill(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_rows, int dtype, void* out,
+                       int64_t ld, void* stream) {
+  return gaussian_fill(seed, rows, cols, chunk_rows, dtype, out, ld, STREAM(stream));
+}
+
+int cnmf_uniform_fill(uint64_t seed, int64_t rows, int64_t cols, double low, double high, int dtype, int transpose,
+                      void* out, void* stream) {
+  return uniform_fill(seed, rows, cols, low, high, dtype, transpose, out, STREAM(stream));
+}
+
+int cnmf_pass_forward(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int s, float* Y,
+                      void* stream) {
+  CNMF_TRY(check_a(A, m, n, lda));
+  return pass_forward(A, m, n, lda, X, panel_ld(s), Y, STREAM(stream));
+}
+
+int cnmf_pass_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const float* W, int s, float* Z,
+                        void* stream) {
+  CNMF_TRY(check_a(A, m, n, lda));
+  return pass_transpose(A, m, n, lda, W, panel_ld(s), Z, STREAM(stream));
+}
+
+size_t cnmf_compress_workspace(int64_t m, int64_t n, int s) { return compress_workspace(m, n, s); }
+
+int cnmf_structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed,
+                             int side, float* Q, void* ws, size_t ws_bytes, void* stream) {
+  CNMF_TRY(check_a(A, m, n, lda));
+  if (side != 0 && side != 1) return fail(CNMF_ERR_ARGUMENT, "side must be 0 (columns) or 1 (rows)");
+  return structured_compress(A, m, n, lda, s, w, seed, side, Q, ws, ws_bytes, STREAM(stream));
+}
+
+int cnmf_orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, void* stream) {
+  if (rows < s) return fail(CNMF_ERR_ARGUMENT, "panel must be at least as tall as it is wide");
+  return orthonormalize(P, rows, s, R, ws, ws_bytes, STREAM(stream));
+}
+
+size_t cnmf_spa_workspace(int64_t n, int s) { return spa_workspace(n, s); }
+
+int cnmf_panel_to_f64(const float* src, int64_t rows, int S, double* dst, int64_t ld, void* stream) {
+  return panel_to_f64(src, rows, S, dst, ld, STREAM(stream));
+}
+
+int cnmf_select_spa(double* W, int64_t n, int s, int64_t ld, int r, int64_t* picks, int* n_picks, void* ws,
+                    size_t ws_bytes, void* stream) {
+  return select_spa(W, n, s, ld, r, picks, n_picks, ws, ws_bytes, STREAM(stream));
+}
+
+int cnmf_select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const double* mass, double nnls_tol,
+                     int64_t* picks, int* n_picks, void* stream) {
+  return select_xray(W, n, s, ld, r, mass, nnls_tol, picks, n_picks, STREAM(stream));
+}
+
+int cnmf_right_factor(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_picks, int k, double tol,
+                      double* Ht, int64_t* n_capped, void* stream) {
+  if (k < 1 || k > 64) return fail(CNMF_ERR_ARGUMENT, "right factor supports 1 <= k <= 64");
+  cudaStream_t st = STREAM(stream);
+  double* scratch = nullptr;
+  CNMF_CUDA(cudaMallocAsync((void**)&scratch, ((size_t)k * k + (size_t)n * k) * 8, st));
+  int rc = right_factor(W, n, s, ld, d_picks, k, tol, Ht, scratch, n_capped, st);
+  cudaFreeAsync(scratch, st);
+  return rc;
+}
+
+int cnmf_refit_norms(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_picks, int k, const double* Ht,
+                     double* out, void* stream) {
+  return refit_norms(W, n, s, ld, d_picks, k, Ht, nullptr, nullptr, out, STREAM(stream));
+}
+
+int cnmf_nnls_gram(const double* gram, const double* target, int64_t k, int q, double tol, int max_exchanges,
+                   double* H, int64_t* n_capped, void* stream) {
+  return nnls_gram(gram, target, k, q, tol, max_exchanges, H, n_capped, STREAM(stream));
+}
+
+int cnmf_panel_cross(const float* P1, const float* P2, int64_t rows, int S, double* out, void* stream) {
+  return panel_cross(P1, P2, rows, S, out, STREAM(stream));
+}
+
+int cnmf_residual_norms(const float* A, int64_t m, int64_t n, int64_t lda, const double* X, const int64_t* cols,
+                        const double* Yt, int r, double* out, void* stream) {
+  if (A == nullptr || m < 1 || n < 1 || lda < n) return fail(CNMF_ERR_ARGUMENT, "bad A");
+  return residual_norms(A, m, n, lda, X, cols, Yt, r, out, STREAM(stream));
+}
+
+size_t cnmf_admm_workspace(int64_t m, int64_t n, int s, int r) { return admm_workspace(m, n, s, r); }
+
+int cnmf_admm_run(const double* core, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
+                  double* du, double* vt, double* dvt, double* xc, double* yc, double pu, double pv, double step,
+                  int max_iter, double tol, double* trace, double* scores, int* iterations, int* done, int resume,
+                  int step_limit, void* ws, size_t ws_bytes, void* stream) {
+  if (max_iter < 0) return fail(CNMF_ERR_ARGUMENT, "max_iter must be >= 0");
+  if (max_iter == 0) {
+    if (iterations) *iterations = 0;
+    if (done) *done = 1;
+    return CNMF_OK;
+  }
+  int it = 0;
+  int rc = admm_run(core, L, m, Rt, n, s, r, u, du, vt, dvt, xc, yc, pu, pv, step, max_iter, tol, trace, scores, &it,
+                    ws, ws_bytes, resume, step_limit, STREAM(stream));
+  if (iterations) *iterations = it < 0 ? -it - 1 : it;
+  if (done) *done = it >= 0 ? 1 : 0;
+  return rc;
+}
+
+}  // extern "C"

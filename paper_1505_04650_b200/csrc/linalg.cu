@@ -1,0 +1,275 @@
+// Range finder driver and CholeskyQR machinery.
+//
+// Reference: compress.py:156-199 structured_compress, compress.py:202-227
+// structured_compress_rows, compress.py:136-145 canonical_qr, tsqr.py:65-135.
+//
+// Every pass output is re-orthonormalised on the device by CholeskyQR: the
+// finalize kernel computes the fp64 Gram matrix of the skinny panel while it
+// streams it, one CTA factors G = R^T R (with a shift when G is numerically
+// singular) and inverts R, and the next finalize applies R^{-1} in place. The
+// first sweep runs explicitly (its R^{-1} carries cond(P) ~ sigma_1/sigma_s);
+// the second sweep's near-identity R^{-1} is deferred into the next pass's
+// finalize, because A (P T) = (A P) T. All transforms are upper triangular, so
+// the leading column spans — and therefore the sign-canonical Q of the
+// reference — are those of the reference (its reorthogonalize flag changes
+// nothing in exact arithmetic); numerically this is the stable variant.
+#include <algorithm>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace cnmf {
+
+int panel_ld(int s);
+int pass_forward(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
+int pass_transpose(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
+int panel_finalize(float*, int64_t, int, const double*, double*, cudaStream_t);
+int gaussian_fill(uint64_t, int64_t, int64_t, int64_t, int, void*, int64_t, cudaStream_t);
+
+namespace {
+
+// G (upper triangle valid, S x S) = R^T R; T = R^{-1} written S x S (zero
+// outside the leading s x s block). info[0] |= 1 when a shift was needed,
+// info[1] = min(pass id) whose Gram matrix was not finite. One block.
+__global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict__ G, int s, int S,
+                                                       double* __restrict__ T, double* __restrict__ Rout,
+                                                       int* __restrict__ info, int pass_id) {
+  extern __shared__ double a[];  // s x s
+  __shared__ double s_maxd;
+  __shared__ int s_fail, s_nonfinite;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_maxd = 0.0;
+    s_fail = 0;
+    s_nonfinite = 0;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < s * s; idx += blockDim.x) {
+    const int i = idx / s, j = idx % s;
+    const double v = (i <= j) ? G[i * S + j] : G[j * S + i];
+    a[idx] = v;
+    if (!isfinite(v)) s_nonfinite = 1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double md = 0.0;
+    for (int i = 0; i < s; ++i) md = fmax(md, a[i * s + i]);
+    s_maxd = md;
+  }
+  __syncthreads();
+  if (s_nonfinite || !(s_maxd > 0.0)) {
+    if (tid == 0) atomicMin(&info[1], pass_id);
+    for (int idx = tid; idx < S * S; idx += blockDim.x) T[idx] = 0.0;
+    return;
+  }
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (attempt == 1) {
+      __syncthreads();  // every thread has observed s_fail before it is reset
+      // shifted CholeskyQR: restore G and add a relative shift
+      for (int idx = tid; idx < s * s; idx += blockDim.x) {
+        const int i = idx / s, j = idx % s;
+        double v = (i <= j) ? G[i * S + j] : G[j * S + i];
+        if (i == j) v += 1e-12 * s_maxd;
+        a[idx] = v;
+      }
+      if (tid == 0) {
+        s_fail = 0;
+        info[0] |= 1;
+      }
+      __syncthreads();
+    }
+    const double thr = 1e-15 * s_maxd;
+    for (int k = 0; k < s; ++k) {
+      if (tid == 0) {
+        const double d = a[k * s + k];
+        if (!(d > thr)) s_fail = 1;
+        a[k * s + k] = sqrt(fmax(d, thr));
+      }
+      __syncthreads();
+      if (s_fail) break;
+      const double rkk = a[k * s + k];
+      for (int j = k + 1 + tid; j < s; j += blockDim.x) a[k * s + j] /= rkk;
+      __syncthreads();
+      const int t = s - k - 1;
+      for (int idx = tid; idx < t * t; idx += blockDim.x) {
+        const int i = k + 1 + idx / t, j = k + 1 + idx % t;
+        if (j >= i) a[i * s + j] -= a[k * s + i] * a[k * s + j];
+      }
+      __syncthreads();
+    }
+    if (!s_fail) break;
+  }
+  if (s_fail) {
+    if (tid == 0) atomicMin(&info[1], pass_id);
+    for (int idx = tid; idx < S * S; idx += blockDim.x) T[idx] = 0.0;
+    return;
+  }
+  if (Rout != nullptr)
+    for (int idx = tid; idx < S * S; idx += blockDim.x) {
+      const int i = idx / S, j = idx % S;
+      Rout[idx] = (i < s && j < s && i <= j) ? a[i * s + j] : 0.0;
+    }
+  __syncthreads();
+  // in-place inverse of the upper-triangular factor (column sweep)
+  __shared__ double col[128];
+  for (int j = 0; j < s; ++j) {
+    const double ajj = 1.0 / a[j * s + j];
+    // col[i] = -(T[:j,:j] R[:j,j])_i / R[j,j]   (T already stored in a[:j,:j])
+    for (int i = tid; i < j; i += blockDim.x) {
+      double acc = 0.0;
+      for (int k = i; k < j; ++k) acc += a[i * s + k] * a[k * s + j];
+      col[i] = -acc * ajj;
+    }
+    __syncthreads();
+    for (int i = tid; i < j; i += blockDim.x) a[i * s + j] = col[i];
+    if (tid == 0) a[j * s + j] = ajj;
+    __syncthreads();
+  }
+  for (int idx = tid; idx < S * S; idx += blockDim.x) {
+    const int i = idx / S, j = idx % S;
+    T[idx] = (i < s && j < s && i <= j) ? a[i * s + j] : 0.0;
+  }
+}
+
+__global__ void init_info(int* info) {
+  info[0] = 0;
+  info[1] = 1 << 30;
+}
+
+}  // namespace
+
+int chol_inv(const double* G, int s, int S, double* T, double* R, int* info, int pass_id, cudaStream_t st) {
+  const size_t smem = (size_t)s * s * 8;
+  static bool attr = false;
+  if (!attr) {
+    CNMF_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 8));
+    attr = true;
+  }
+  chol_inv_kernel<<<1, 256, smem, st>>>(G, s, S, T, R, info, pass_id);
+  CNMF_LAUNCH_CHECK();
+  return CNMF_OK;
+}
+
+size_t compress_workspace(int64_t m, int64_t n, int s) {
+  const int S = panel_ld(s);
+  if (S < 0) return 0;
+  return (size_t)std::max(m, n) * S * 4 + 2 * (size_t)S * S * 8 + 256;
+}
+
+struct Scratch {
+  double* G;
+  double* T;
+  int* info;
+};
+
+static Scratch carve_small(void* base, int S) {
+  char* p = (char*)base;
+  Scratch sc;
+  sc.G = (double*)p;
+  sc.T = (double*)(p + (size_t)S * S * 8);
+  sc.info = (int*)(p + 2 * (size_t)S * S * 8);
+  return sc;
+}
+
+// Finish a panel whose Gram-derived transform sc.T is pending: apply it,
+// re-factor, apply again (CholeskyQR2 on an already well-conditioned panel).
+static int finish_basis(float* P, int64_t rows, int s, int S, Scratch sc, double* Rfinal, int first_pass_id,
+                        cudaStream_t st) {
+  CNMF_TRY(panel_finalize(P, rows, S, sc.T, sc.G, st));
+  CNMF_TRY(chol_inv(sc.G, s, S, sc.T, Rfinal, sc.info, first_pass_id, st));
+  CNMF_TRY(panel_finalize(P, rows, S, sc.T, nullptr, st));
+  return CNMF_OK;
+}
+
+static int check_info(const int* d_info, const char* what, cudaStream_t st) {
+  int h[2];
+  CNMF_CUDA(cudaMemcpyAsync(h, d_info, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CNMF_CUDA(cudaStreamSynchronize(st));
+  if (h[1] != (1 << 30)) {
+    return fail(CNMF_ERR_NUMERIC, std::string("non-finite values after pass ") + std::to_string(h[1]) + " (" +
+                                      what + ")");
+  }
+  return CNMF_OK;
+}
+
+int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed, int side,
+                        float* Q, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int S = panel_ld(s);
+  if (S < 0) return fail(CNMF_ERR_ARGUMENT, "basis width must be <= 128");
+  if (s < 1 || w < 0) return fail(CNMF_ERR_ARGUMENT, "bad width or power exponent");
+  if (s > std::min(m, n))
+    return fail(CNMF_ERR_INFEASIBLE_RANK, "basis width " + std::to_string(s) + " exceeds min(m, n) = " +
+                                              std::to_string(std::min(m, n)) + "; adjust_config first");
+  if (ws_bytes < compress_workspace(m, n, s)) return fail(CNMF_ERR_ARGUMENT, "workspace too small");
+  // panels: rows m (B-type) and rows n (C-type); the output side uses Q
+  float* Pm = side == 0 ? Q : (float*)ws;
+  float* Pn = side == 0 ? (float*)ws : Q;
+  Scratch sc = carve_small((char*)ws + (size_t)std::max(m, n) * S * 4, S);
+  init_info<<<1, 1, 0, st>>>(sc.info);
+  CNMF_LAUNCH_CHECK();
+  // Omega: the reference's seeded test matrix (compress.py:125-127), rows =
+  // A.cols for the column basis, A.rows for the row basis.
+  const uint64_t oseed = child_seed(seed, "omega");
+  float* omega = side == 0 ? Pn : Pm;
+  const int64_t orows = side == 0 ? n : m;
+  CNMF_CUDA(cudaMemsetAsync(omega, 0, (size_t)orows * S * 4, st));
+  CNMF_TRY(gaussian_fill(oseed, orows, s, 4096, CNMF_F32, omega, S, st));
+
+  int pass_id = 0;
+  // Every pass output P is orthonormalised explicitly with one CholeskyQR
+  // sweep (Gram in fp64, R^{-1} applied in place); the second sweep's
+  // R^{-1} is well conditioned and is deferred into the next finalize.
+  // Deferring the first (ill-conditioned, cond ~ sigma_1/sigma_s) R^{-1}
+  // instead would amplify the fp32 pass error by that condition number.
+  float* cur;
+  if (side == 0) {
+    CNMF_TRY(pass_forward(A, m, n, lda, Pn, S, Pm, st));
+    cur = Pm;
+  } else {
+    CNMF_TRY(pass_transpose(A, m, n, lda, Pm, S, Pn, st));
+    cur = Pn;
+  }
+  int64_t cur_rows = side == 0 ? m : n;
+  bool pending = false;  // sc.T holds a deferred transform for `cur`
+  auto orth_sweep = [&]() -> int {
+    CNMF_TRY(panel_finalize(cur, cur_rows, S, pending ? sc.T : nullptr, sc.G, st));
+    CNMF_TRY(chol_inv(sc.G, s, S, sc.T, nullptr, sc.info, pass_id, st));
+    CNMF_TRY(panel_finalize(cur, cur_rows, S, sc.T, sc.G, st));
+    CNMF_TRY(chol_inv(sc.G, s, S, sc.T, nullptr, sc.info, pass_id, st));
+    pending = true;
+    return CNMF_OK;
+  };
+  CNMF_TRY(orth_sweep());
+  for (int t = 0; t < 2 * w; ++t) {
+    ++pass_id;
+    const bool to_n = (cur == Pm);  // next output has n rows: transpose pass
+    float* nxt = to_n ? Pn : Pm;
+    if (to_n)
+      CNMF_TRY(pass_transpose(A, m, n, lda, cur, S, nxt, st));
+    else
+      CNMF_TRY(pass_forward(A, m, n, lda, cur, S, nxt, st));
+    // the input's deferred (near-identity) transform commutes with the pass
+    cur = nxt;
+    cur_rows = to_n ? n : m;
+    CNMF_TRY(orth_sweep());
+  }
+  CNMF_TRY(finish_basis(cur, cur_rows, s, S, sc, nullptr, pass_id, st));
+  return check_info(sc.info, side == 0 ? "column basis" : "row basis", st);
+}
+
+int orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int S = panel_ld(s);
+  if (S < 0) return fail(CNMF_ERR_ARGUMENT, "width must be <= 128");
+  if (ws_bytes < 2 * (size_t)S * S * 8 + 256) return fail(CNMF_ERR_ARGUMENT, "workspace too small");
+  Scratch sc = carve_small(ws, S);
+  init_info<<<1, 1, 0, st>>>(sc.info);
+  CNMF_LAUNCH_CHECK();
+  CNMF_TRY(panel_finalize(P, rows, S, nullptr, sc.G, st));
+  CNMF_TRY(chol_inv(sc.G, s, S, sc.T, nullptr, sc.info, 0, st));
+  CNMF_TRY(panel_finalize(P, rows, S, sc.T, sc.G, st));
+  CNMF_TRY(chol_inv(sc.G, s, S, sc.T, nullptr, sc.info, 0, st));
+  CNMF_TRY(finish_basis(P, rows, s, S, sc, R, 0, st));
+  return check_info(sc.info, "orthonormalize", st);
+}
+
+}  // namespace cnmf

@@ -1,0 +1,523 @@
+// Device RNG: numpy-compatible Philox4x64 uniform and ziggurat normal streams.
+//
+// Reference: rng.py:38-98 (Rng over numpy Generator(Philox)), compress.py:115-127
+// (_drawn_in_chunks: fixed 4096-row chunks, child stream per chunk).
+//
+// The normal sampler consumes a variable number of raw 64-bit draws per
+// variate (≈0.75% of draws hit the wedge/tail path), so a stream is decoded in
+// parallel by splitting its raw sequence into fixed segments:
+//   k1  one warp per segment walks the variate chain speculatively from the
+//       segment start (128 raws per warp step, one Philox block per lane) and
+//       records the exit position, the variate count and which of the first
+//       128 positions start a variate;
+//   k2  one CTA per stream re-anchors every segment at the previous segment's
+//       exit (chains merge at the first shared start position, almost always
+//       the entry itself) and prefix-sums the corrected counts;
+//   k3  one warp per segment decodes again from its true entry and writes its
+//       variates at the scanned offset.
+// Any segment whose chain does not merge inside its first window flags the
+// stream, which is then decoded by one warp sequentially (never observed; kept
+// for exactness).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "ziggurat_tables.h"
+
+namespace cnmf {
+namespace {
+
+constexpr int kWin = 128;  // raw positions per warp step (32 lanes x 4 words)
+
+struct StreamDesc {
+  uint64_t key;
+  int64_t count;    // variates in this stream
+  int64_t row0;     // first output row
+  int64_t seg0;     // first segment index (global)
+  int32_t nseg;     // segments of this stream
+  int32_t seglen;   // raw positions per segment (multiple of kWin)
+};
+
+struct SegState {
+  int64_t exit;          // first chain start >= segment end (absolute position)
+  int64_t count;         // variates started in [entry, exit)
+  int64_t entry;         // true entry (after k2)
+  int64_t offset;        // output offset (after k2)
+  uint32_t chain[4];     // chain-start bits for [seg_start, seg_start + 128)
+};
+
+// ---- correctly rounded log(w), w in (0, 1], in double-double arithmetic ----
+struct DD {
+  double hi, lo;
+};
+__device__ __forceinline__ DD two_sum(double a, double b) {
+  const double s = a + b, bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ DD dd_add(DD a, DD b) {
+  DD s = two_sum(a.hi, b.hi);
+  return two_sum(s.hi, s.lo + a.lo + b.lo);
+}
+__device__ __forceinline__ DD dd_mul(DD a, DD b) {
+  const double p = a.hi * b.hi;
+  const double e = fma(a.hi, b.hi, -p) + (a.hi * b.lo + a.lo * b.hi);
+  return two_sum(p, e);
+}
+__device__ DD dd_div(DD a, DD b) {
+  const double q1 = a.hi / b.hi;
+  DD r = dd_add(a, dd_mul(DD{-q1, 0.0}, b));
+  const double q2 = r.hi / b.hi;
+  r = dd_add(r, dd_mul(DD{-q2, 0.0}, b));
+  const double q3 = r.hi / b.hi;
+  return dd_add(two_sum(q1, q2), DD{q3, 0.0});
+}
+// log(w) = e ln2 + 2 atanh((m-1)/(m+1)), m in [sqrt(1/2), sqrt(2)), series to
+// ~2^-110; rounded once at the end.
+__device__ double cr_log(double w) {
+  int e;
+  double m = frexp(w, &e);
+  if (m < 0.7071067811865476) {
+    m *= 2.0;
+    e -= 1;
+  }
+  const DD s = dd_div(DD{m - 1.0, 0.0}, two_sum(m, 1.0));
+  const DD z = dd_mul(s, s);
+  DD p = dd_div(DD{1.0, 0.0}, DD{49.0, 0.0});
+  for (int k = 23; k >= 0; --k) p = dd_add(dd_mul(p, z), dd_div(DD{1.0, 0.0}, DD{2.0 * k + 1, 0.0}));
+  const DD lm = dd_mul(DD{2.0 * s.hi, 2.0 * s.lo}, p);
+  const DD r = dd_add(dd_mul(DD{(double)e, 0.0}, DD{0x1.62e42fefa39efp-1, 0x1.abc9e3b39803fp-56}), lm);
+  return r.hi + r.lo;
+}
+
+// A tail variate (|x| > r) is finished on the host with the C library's
+// log1p, the very call numpy makes: that libm is not correctly rounded (it
+// differs from the exact log in ~7% of arguments), so bit-exactness with the
+// reference needs the same function. The device decides acceptance with a
+// correctly rounded log (a flip needs the two to straddle a rounding
+// boundary of the acceptance test, ~1e-16 per draw).
+struct TailRec {
+  int64_t offset;  // element offset into the output
+  uint64_t u1;     // accepted first uniform (raw)
+  int32_t negative;
+  int32_t pad;
+};
+
+// Slow path of numpy's random_standard_normal starting at raw position `pos`
+// whose first draw `r0` failed the fast acceptance. Returns the variate and
+// sets *next to the position after the last consumed draw.
+__device__ double slow_normal(uint64_t key, int64_t pos, uint64_t r0, int64_t* next, uint64_t* tail_u1 = nullptr,
+                              int* tail_neg = nullptr) {
+  uint64_t r = r0;
+  int64_t p = pos + 1;
+  for (;;) {
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    double x = __dmul_rn((double)rabs, cnmf_zig::kWi[idx]);
+    if (sign) x = -x;
+    if (rabs < cnmf_zig::kKi[idx]) {
+      *next = p;
+      return x;
+    }
+    if (idx == 0) {
+      for (;;) {
+        const uint64_t r1 = philox_raw(key, (uint64_t)p);
+        const double u1 = raw_to_unit(r1);
+        const double u2 = raw_to_unit(philox_raw(key, (uint64_t)(p + 1)));
+        p += 2;
+        // 1 - u is exact for u = k 2^-53, so log1p(-u) = log(1 - u)
+        const double xx = __dmul_rn(-cnmf_zig::kTailInvR, cr_log(1.0 - u1));
+        const double yy = -cr_log(1.0 - u2);
+        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+          *next = p;
+          const int neg = (int)((rabs >> 8) & 1);
+          if (tail_u1) {
+            *tail_u1 = r1;
+            *tail_neg = neg;
+          }
+          return neg ? -(cnmf_zig::kTailR + xx) : cnmf_zig::kTailR + xx;
+        }
+      }
+    }
+    const double u = raw_to_unit(philox_raw(key, (uint64_t)p));
+    p += 1;
+    const double lhs = __dadd_rn(__dmul_rn(__dadd_rn(cnmf_zig::kFi[idx - 1], -cnmf_zig::kFi[idx]), u),
+                                 cnmf_zig::kFi[idx]);
+    if (lhs < exp(__dmul_rn(__dmul_rn(-0.5, x), x))) {
+      *next = p;
+      return x;
+    }
+    r = philox_raw(key, (uint64_t)p);
+    p += 1;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void store_variate(T* out, int64_t ld, int64_t cols, int64_t row0, int64_t k,
+                                              int64_t count, double x) {
+  if (k < count) {
+    const int64_t row = row0 + k / cols;
+    const int64_t col = k - (k / cols) * cols;
+    out[row * ld + col] = (T)x;
+  }
+}
+
+// Walk the chain of one segment from `head` until the head reaches `stop`.
+// When WRITE, variates are stored from output index `k0`. Returns the number
+// of variates started; *exit_pos receives the final head. When chain != null
+// the start bits of the first window [seg_start, seg_start+128) are recorded.
+template <bool WRITE, typename T>
+__device__ int64_t walk(uint64_t key, int64_t head, int64_t stop, int64_t seg_start, uint32_t* chain, T* out,
+                        int64_t ld, int64_t cols, int64_t row0, int64_t k0, int64_t count, int64_t* exit_pos,
+                        TailRec* tails = nullptr, unsigned int* ntails = nullptr, unsigned int tail_cap = 0) {
+  const int lane = threadIdx.x & 31;
+  int64_t k = 0;
+  int64_t base = (head / kWin) * kWin;
+  while (head < stop) {
+    // one Philox block per lane: positions base + 4*lane + {0..3}
+    const U64x4 blk = philox4x64((uint64_t)(base / 4 + lane) + 1, 0, key, 0);
+    uint32_t slow = 0;
+    double xs[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint64_t r = blk.v[j];
+      const int idx = (int)(r & 0xff);
+      r >>= 8;
+      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+      double x = __dmul_rn((double)rabs, cnmf_zig::kWi[idx]);
+      xs[j] = (r & 1) ? -x : x;
+      if (!(rabs < cnmf_zig::kKi[idx])) slow |= 1u << j;
+    }
+    uint32_t m[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      m[q] = __reduce_or_sync(0xffffffffu, (lane >> 3) == q ? (slow << (4 * (lane & 7))) : 0u);
+
+    int p = (int)(head - base);
+    while (p < kWin && base + p < stop) {
+      // first slow position >= p
+      int f = kWin;
+      for (int q = p >> 5; q < 4; ++q) {
+        uint32_t w = m[q] & (q == (p >> 5) ? (0xffffffffu << (p & 31)) : 0xffffffffu);
+        if (w) {
+          f = q * 32 + __ffs(w) - 1;
+          break;
+        }
+      }
+      // fast run [p, f) — but never start a variate at or beyond `stop`
+      int fe = f;
+      if (base + fe > stop) fe = (int)(stop - base);
+      if (chain != nullptr && base == seg_start) {
+        // record chain starts p..fe-1 in the first window
+        for (int q = 0; q < 4; ++q) {
+          const int lo = q * 32, hi = lo + 32;
+          const int a = max(p, lo), b = min(fe, hi);
+          if (a < b) {
+            const uint32_t bits = (b - a == 32) ? 0xffffffffu : (((1u << (b - a)) - 1u) << (a - lo));
+            chain[q] |= bits;
+          }
+        }
+      }
+      if (WRITE) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int pos = 4 * lane + j;
+          if (pos >= p && pos < fe) store_variate(out, ld, cols, row0, k0 + k + (pos - p), count, xs[j]);
+        }
+      }
+      k += fe - p;
+      p = fe;
+      if (fe < f || f == kWin) break;  // reached stop or window end
+      // slow variate starting at base + f (warp-uniform, all lanes compute)
+      const uint64_t r0 = __shfl_sync(0xffffffffu, blk.v[0], f >> 2);
+      const uint64_t r1 = __shfl_sync(0xffffffffu, blk.v[1], f >> 2);
+      const uint64_t r2 = __shfl_sync(0xffffffffu, blk.v[2], f >> 2);
+      const uint64_t r3 = __shfl_sync(0xffffffffu, blk.v[3], f >> 2);
+      const int jj = f & 3;
+      const uint64_t rf = jj == 0 ? r0 : jj == 1 ? r1 : jj == 2 ? r2 : r3;
+      int64_t nxt;
+      uint64_t tu1 = 0;
+      int tneg = -1;
+      const double x = slow_normal(key, base + f, rf, &nxt, &tu1, &tneg);
+      if (chain != nullptr && base == seg_start) chain[f >> 5] |= 1u << (f & 31);
+      if (WRITE && lane == 0) {
+        store_variate(out, ld, cols, row0, k0 + k, count, x);
+        const int64_t kk = k0 + k;
+        if (tneg >= 0 && tails != nullptr && kk < count) {
+          const unsigned int slot = atomicAdd(ntails, 1u);
+          if (slot < tail_cap) {
+            const int64_t row = row0 + kk / cols, col = kk - (kk / cols) * cols;
+            tails[slot] = TailRec{row * ld + col, tu1, tneg, 0};
+          }
+        }
+      }
+      k += 1;
+      p = (int)(nxt - base);
+    }
+    head = base + p;
+    base = (head / kWin) * kWin;
+  }
+  *exit_pos = head;
+  return k;
+}
+
+__global__ void k1_speculate(const StreamDesc* streams, int nstreams, const int32_t* seg_stream, SegState* segs,
+                             int64_t total_segs) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (g >= total_segs) return;
+  const StreamDesc sd = streams[seg_stream[g]];
+  const int64_t w = g - sd.seg0;
+  const int64_t s0 = w * sd.seglen, s1 = s0 + sd.seglen;
+  uint32_t chain[4] = {0, 0, 0, 0};
+  int64_t ex;
+  const int64_t n = walk<false, float>(sd.key, s0, s1, s0, chain, nullptr, 0, 1, 0, 0, 0, &ex);
+  if ((threadIdx.x & 31) == 0) {
+    segs[g].exit = ex;
+    segs[g].count = n;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) segs[g].chain[q] = chain[q];
+  }
+}
+
+// One CTA per stream: re-anchor each segment at its true entry, scan counts.
+__global__ void k2_anchor_scan(const StreamDesc* streams, SegState* segs, int* flags) {
+  const StreamDesc sd = streams[blockIdx.x];
+  __shared__ int64_t s_cnt[1024];
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  for (int w = threadIdx.x; w < sd.nseg; w += blockDim.x) {
+    SegState& st = segs[sd.seg0 + w];
+    const int64_t s0 = (int64_t)w * sd.seglen;
+    const int64_t entry = (w == 0) ? 0 : segs[sd.seg0 + w - 1].exit;
+    int64_t d = 0;
+    int64_t p = entry;
+    bool merged = false;
+    // serial single-thread walk from the entry until hitting a recorded start
+    for (int guard = 0; guard < 64; ++guard) {
+      const int64_t rel = p - s0;
+      if (rel >= 0 && rel < kWin && ((st.chain[rel >> 5] >> (rel & 31)) & 1u)) {
+        merged = true;
+        break;
+      }
+      if (rel >= kWin || rel < 0) break;
+      const uint64_t r = philox_raw(sd.key, (uint64_t)p);
+      uint64_t rr = r >> 8;
+      const int idx = (int)(r & 0xff);
+      const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
+      int64_t nxt = p + 1;
+      if (!(rabs < cnmf_zig::kKi[idx])) (void)slow_normal(sd.key, p, r, &nxt);
+      d += 1;
+      p = nxt;
+    }
+    int64_t cnt = 0;
+    if (merged) {
+      const int64_t rel = p - s0;
+      int64_t below = 0;
+      for (int q = 0; q < 4; ++q) {
+        const int lo = q * 32;
+        if (rel >= lo + 32)
+          below += __popc(st.chain[q]);
+        else if (rel > lo)
+          below += __popc(st.chain[q] & ((1u << (rel - lo)) - 1u));
+      }
+      cnt = d + st.count - below;
+    } else {
+      s_bad = 1;
+    }
+    st.entry = entry;
+    s_cnt[w] = cnt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int w = 0; w < sd.nseg; ++w) {
+      segs[sd.seg0 + w].offset = acc;
+      acc += s_cnt[w];
+    }
+    if (acc < sd.count) s_bad = 1;
+    flags[blockIdx.x] = s_bad;
+  }
+}
+
+template <typename T>
+__global__ void k3_emit(const StreamDesc* streams, const int32_t* seg_stream, const SegState* segs,
+                        int64_t total_segs, const int* flags, T* out, int64_t ld, int64_t cols, TailRec* tails,
+                        unsigned int* ntails, unsigned int tail_cap) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (g >= total_segs) return;
+  const int sid = seg_stream[g];
+  if (flags[sid]) return;
+  const StreamDesc sd = streams[sid];
+  const int64_t w = g - sd.seg0;
+  const SegState st = segs[g];
+  if (st.offset >= sd.count) return;
+  const int64_t s1 = (w + 1) * sd.seglen;
+  int64_t ex;
+  walk<true, T>(sd.key, st.entry, s1, -1, nullptr, out, ld, cols, sd.row0, st.offset, sd.count, &ex, tails, ntails,
+                tail_cap);
+}
+
+// Fallback: one warp decodes a whole stream sequentially.
+template <typename T>
+__global__ void k_serial(const StreamDesc* streams, const int* flags, T* out, int64_t ld, int64_t cols,
+                         TailRec* tails, unsigned int* ntails, unsigned int tail_cap) {
+  const StreamDesc sd = streams[blockIdx.x];
+  if (!flags[blockIdx.x]) return;
+  // walk in windows until `count` variates are produced
+  int64_t head = 0, k = 0;
+  while (k < sd.count) {
+    int64_t ex;
+    k += walk<true, T>(sd.key, head, head + 64 * kWin, -1, nullptr, out, ld, cols, sd.row0, k, sd.count, &ex, tails,
+                       ntails, tail_cap);
+    head = ex;
+  }
+}
+
+template <typename T>
+__global__ void scatter_tail(T* out, const int64_t* offsets, const double* vals, int count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[offsets[i]] = (T)vals[i];
+}
+
+template <typename T>
+__global__ void uniform_kernel(uint64_t key, int64_t rows, int64_t cols, double low, double high, int transpose,
+                               T* out) {
+  const int64_t total = rows * cols;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // Philox block
+  if (b * 4 >= total) return;
+  const U64x4 blk = philox4x64((uint64_t)b + 1, 0, key, 0);
+  const double span = __dadd_rn(high, -low);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t i = b * 4 + j;
+    if (i < total) {
+      const double v = __dadd_rn(low, __dmul_rn(span, raw_to_unit(blk.v[j])));
+      if (transpose) {
+        const int64_t r = i / cols, c = i - (i / cols) * cols;
+        out[c * rows + r] = (T)v;
+      } else {
+        out[i] = (T)v;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// Launch the three-phase decode for a list of streams sharing one output.
+template <typename T>
+static int gaussian_streams(std::vector<StreamDesc>& sd, T* out, int64_t ld, int64_t cols, cudaStream_t stream) {
+  int64_t total = 0;
+  std::vector<int32_t> seg_stream;
+  for (size_t i = 0; i < sd.size(); ++i) {
+    const int64_t need = (int64_t)(sd[i].count * 1.02) + 4 * kWin;
+    int64_t seglen = 16 * kWin;
+    while (ceil_div(need, seglen) > 1024) seglen *= 2;
+    sd[i].seglen = (int32_t)seglen;
+    sd[i].nseg = (int32_t)ceil_div(need, seglen);
+    sd[i].seg0 = total;
+    total += sd[i].nseg;
+    for (int w = 0; w < sd[i].nseg; ++w) seg_stream.push_back((int32_t)i);
+  }
+  const size_t bytes_sd = sd.size() * sizeof(StreamDesc);
+  const size_t bytes_map = seg_stream.size() * sizeof(int32_t);
+  const size_t bytes_seg = (size_t)total * sizeof(SegState);
+  const size_t bytes_flags = sd.size() * sizeof(int);
+  int64_t variates = 0;
+  for (auto& x : sd) variates += x.count;
+  const unsigned int tail_cap = (unsigned int)std::min<int64_t>(variates / 256 + 1024, 1 << 26);
+  const size_t bytes_tail = (size_t)tail_cap * sizeof(TailRec) + 64;
+  char* buf = nullptr;
+  CNMF_CUDA(cudaMallocAsync((void**)&buf, bytes_sd + bytes_map + bytes_seg + bytes_flags + bytes_tail + 256, stream));
+  StreamDesc* d_sd = (StreamDesc*)buf;
+  int32_t* d_map = (int32_t*)(buf + bytes_sd);
+  SegState* d_seg = (SegState*)(((uintptr_t)(buf + bytes_sd + bytes_map) + 15) & ~(uintptr_t)15);
+  int* d_flags = (int*)((char*)d_seg + bytes_seg);
+  unsigned int* d_ntail = (unsigned int*)(((uintptr_t)(d_flags + sd.size()) + 63) & ~(uintptr_t)63);
+  TailRec* d_tail = (TailRec*)(d_ntail + 16);
+  CNMF_CUDA(cudaMemsetAsync(d_ntail, 0, 4, stream));
+  CNMF_CUDA(cudaMemcpyAsync(d_sd, sd.data(), bytes_sd, cudaMemcpyHostToDevice, stream));
+  CNMF_CUDA(cudaMemcpyAsync(d_map, seg_stream.data(), bytes_map, cudaMemcpyHostToDevice, stream));
+  const int wpb = 4;  // warps per block
+  const unsigned grid = (unsigned)ceil_div(total, wpb);
+  k1_speculate<<<grid, 32 * wpb, 0, stream>>>(d_sd, (int)sd.size(), d_map, d_seg, total);
+  CNMF_LAUNCH_CHECK();
+  k2_anchor_scan<<<(unsigned)sd.size(), 256, 0, stream>>>(d_sd, d_seg, d_flags);
+  CNMF_LAUNCH_CHECK();
+  k3_emit<T><<<grid, 32 * wpb, 0, stream>>>(d_sd, d_map, d_seg, total, d_flags, out, ld, cols, d_tail, d_ntail,
+                                            tail_cap);
+  CNMF_LAUNCH_CHECK();
+  k_serial<T><<<(unsigned)sd.size(), 32, 0, stream>>>(d_sd, d_flags, out, ld, cols, d_tail, d_ntail, tail_cap);
+  CNMF_LAUNCH_CHECK();
+  // finish the tail variates with the C library's log1p (see TailRec)
+  unsigned int ntail = 0;
+  CNMF_CUDA(cudaMemcpyAsync(&ntail, d_ntail, 4, cudaMemcpyDeviceToHost, stream));
+  CNMF_CUDA(cudaStreamSynchronize(stream));
+  if (ntail > tail_cap) {
+    cudaFreeAsync(buf, stream);
+    return fail(CNMF_ERR_CUDA, "tail record buffer overflow");
+  }
+  if (ntail > 0) {
+    std::vector<TailRec> rec(ntail);
+    CNMF_CUDA(cudaMemcpyAsync(rec.data(), d_tail, ntail * sizeof(TailRec), cudaMemcpyDeviceToHost, stream));
+    CNMF_CUDA(cudaStreamSynchronize(stream));
+    std::vector<int64_t> off(ntail);
+    std::vector<double> val(ntail);
+    for (unsigned int i = 0; i < ntail; ++i) {
+      const double u1 = (double)(rec[i].u1 >> 11) * (1.0 / 9007199254740992.0);
+      const double xx = -cnmf_zig::kTailInvR * std::log1p(-u1);
+      off[i] = rec[i].offset;
+      val[i] = rec[i].negative ? -(cnmf_zig::kTailR + xx) : cnmf_zig::kTailR + xx;
+    }
+    int64_t* d_off = (int64_t*)d_tail;  // reuse the record buffer
+    double* d_val = (double*)(d_off + ntail);
+    CNMF_CUDA(cudaMemcpyAsync(d_off, off.data(), ntail * 8, cudaMemcpyHostToDevice, stream));
+    CNMF_CUDA(cudaMemcpyAsync(d_val, val.data(), ntail * 8, cudaMemcpyHostToDevice, stream));
+    scatter_tail<T><<<(ntail + 255) / 256, 256, 0, stream>>>(out, d_off, d_val, (int)ntail);
+    CNMF_LAUNCH_CHECK();
+    CNMF_CUDA(cudaStreamSynchronize(stream));
+  }
+  CNMF_CUDA(cudaFreeAsync(buf, stream));
+  return CNMF_OK;
+}
+
+int gaussian_fill(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_rows, int dtype, void* out, int64_t ld,
+                  cudaStream_t stream) {
+  if (rows < 1 || cols < 1) return fail(CNMF_ERR_ARGUMENT, "gaussian_fill needs positive dims");
+  if (ld < cols) return fail(CNMF_ERR_ARGUMENT, "gaussian_fill: ld < cols");
+  std::vector<StreamDesc> sd;
+  if (chunk_rows <= 0) {
+    sd.push_back(StreamDesc{seed, rows * cols, 0, 0, 0, 0});
+  } else {
+    // compress.py:115-122: chunk c is drawn from Rng(seed).child(f"chunk{c}")
+    int64_t c = 0;
+    for (int64_t r0 = 0; r0 < rows; r0 += chunk_rows, ++c) {
+      const int64_t rr = std::min(chunk_rows, rows - r0);
+      const std::string tag = "chunk" + std::to_string(c);
+      sd.push_back(StreamDesc{child_seed(seed, tag.c_str()), rr * cols, r0, 0, 0, 0});
+    }
+  }
+  if (dtype == CNMF_F64) return gaussian_streams(sd, (double*)out, ld, cols, stream);
+  if (dtype == CNMF_F32) return gaussian_streams(sd, (float*)out, ld, cols, stream);
+  return fail(CNMF_ERR_ARGUMENT, "unknown dtype");
+}
+
+int uniform_fill(uint64_t seed, int64_t rows, int64_t cols, double low, double high, int dtype, int transpose,
+                 void* out, cudaStream_t stream) {
+  if (rows < 1 || cols < 1) return fail(CNMF_ERR_ARGUMENT, "uniform_fill needs positive dims");
+  const int64_t blocks = ceil_div(rows * cols, 4);
+  const unsigned grid = (unsigned)ceil_div(blocks, 256);
+  if (dtype == CNMF_F64)
+    uniform_kernel<double><<<grid, 256, 0, stream>>>(seed, rows, cols, low, high, transpose, (double*)out);
+  else if (dtype == CNMF_F32)
+    uniform_kernel<float><<<grid, 256, 0, stream>>>(seed, rows, cols, low, high, transpose, (float*)out);
+  else
+    return fail(CNMF_ERR_ARGUMENT, "unknown dtype");
+  CNMF_LAUNCH_CHECK();
+  return CNMF_OK;
+}
+
+}  // namespace cnmf

@@ -1,0 +1,152 @@
+"""Compressed ADMM NMF on the B200 (reference nmf.py:226-377).
+
+``nmf_admm(a, r, compressed=True, cfg, penalty_u, penalty_v, step_scale,
+max_iter, tol, scratch_dir, on_iteration)`` keeps the reference signature:
+left/right bases from the device range finder (nmf.py:120-135), the core
+L^T A R^T from one transpose pass plus a panel cross product (nmf.py:329-332),
+seeded U[0,1] splits drawn on the device bit-identically to the reference
+(nmf.py:337-339), then the whole iteration on the device (csrc/admm.cu) and
+the true relative error from one fused residual pass over A (nmf.py:53-75).
+"""
+
+import ctypes
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .compress import CompressionConfig, _compress, adjust_config
+from .device import DeviceMatrix, as_device64, out, stream, zeros
+from .errors import ArgumentError, DivergenceError, UndefinedMetricError
+from .rng import Rng, child_seed
+
+
+@dataclass
+class FactorPair:
+    """Nonnegative factors plus run metadata (nmf.py:37-50)."""
+
+    X: object
+    Y: object
+    iterations: int
+    objective_trace: list = field(default_factory=list)
+    rel_error: float = None
+
+
+@dataclass
+class AdmmState:
+    """ADMM iterates (nmf.py:232-244): compressed cores, splits, duals."""
+
+    xc: object
+    yc: object
+    u: object
+    v: object
+    dual_u: object
+    dual_v: object
+    penalty_u: float
+    penalty_v: float
+    step_scale: float
+
+
+def _resolve_config(r, cfg, m, n):
+    """nmf.py:108-117."""
+    if cfg is None:
+        cfg = CompressionConfig(r=r, r_ov=10, w=4, seed=0)
+    if cfg.r != r:
+        raise ArgumentError(f"cfg.r = {cfg.r} disagrees with rank argument {r}")
+    return adjust_config(cfg, m, n)
+
+
+def relative_error(a, x, y):
+    """||A - X Y||_F / ||A||_F from one fused pass over A (nmf.py:53-75)."""
+    A = DeviceMatrix(a)
+    X = as_device64(x, "X")
+    Y = as_device64(y, "Y")
+    if X.shape[0] != A.m or Y.shape[1] != A.n or X.shape[1] != Y.shape[0]:
+        raise ArgumentError(f"shape mismatch: A {A.shape}, X {tuple(X.shape)}, Y {tuple(Y.shape)}")
+    return _rel_error(A, X, Y.t().contiguous())
+
+
+def _rel_error(A, X, Yt):
+    res = zeros((2,), dtype=torch.float64)
+    _lib.call("cnmf_residual_norms", A.ptr, A.m, A.n, A.lda, X.data_ptr(), None, Yt.data_ptr(), X.shape[1],
+              res.data_ptr(), stream())
+    num, den = res.tolist()
+    if den == 0.0:
+        raise UndefinedMetricError("relative error undefined: ||A||_F is zero")
+    return float(np.sqrt(max(num, 0.0) / den))
+
+
+def compressed_problem(A, cfg):
+    """Bases and core for the compressed ADMM (nmf.py:120-135, 327-332)."""
+    left, _ = _compress(A, replace(cfg, seed=child_seed(cfg.seed, "left-basis")), 0)
+    right, _ = _compress(A, replace(cfg, seed=child_seed(cfg.seed, "right-basis")), 1)
+    s = cfg.basis_cols
+    S = left.panel.shape[1]
+    z = zeros((A.n, S))
+    _lib.call("cnmf_pass_transpose", A.ptr, A.m, A.n, A.lda, left.panel.data_ptr(), s, z.data_ptr(), stream())
+    core = zeros((S, S), dtype=torch.float64)
+    _lib.call("cnmf_panel_cross", z.data_ptr(), right.panel.data_ptr(), A.n, S, core.data_ptr(), stream())
+    return left, right, core[:s, :s].contiguous()
+
+
+def nmf_admm(a, r, compressed=True, cfg=None, penalty_u=1.0, penalty_v=1.0, step_scale=1.0, max_iter=500,
+             tol=1e-4, scratch_dir=None, on_iteration=None):
+    """NMF through ADMM on U = L Xc, V = Yc R, U, V >= 0 (nmf.py:306-377)."""
+    if penalty_u <= 0 or penalty_v <= 0:
+        raise ArgumentError("penalties must be positive")
+    A = DeviceMatrix(a)
+    m, n = A.m, A.n
+    if not compressed:
+        raise ArgumentError("the device path implements the compressed ADMM (compressed=True)")
+    cfg = _resolve_config(r, cfg, m, n)
+    s = cfg.basis_cols
+    left, right, core = compressed_problem(A, cfg)
+    rng = Rng(cfg.seed)
+    u = rng.child("init-left").uniform((m, r))
+    vt = rng.child("init-right").uniform((r, n), transpose=True)  # V^T, n x r
+    du = zeros((m, r), dtype=torch.float64)
+    dvt = zeros((n, r), dtype=torch.float64)
+    xc = zeros((s, r), dtype=torch.float64)
+    yc = zeros((r, s), dtype=torch.float64)
+    trace = zeros((max(max_iter, 1),), dtype=torch.float64)
+    scores = zeros((max(max_iter, 1),), dtype=torch.float64)
+    lib = _lib.load()
+    nbytes = lib.cnmf_admm_workspace(m, n, s, r)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=u.device)
+    it = ctypes.c_int(0)
+    done = ctypes.c_int(0)
+    args = lambda resume, limit: (core.data_ptr(), left.panel.data_ptr(), m, right.panel.data_ptr(), n, s, r,
+                                  u.data_ptr(), du.data_ptr(), vt.data_ptr(), dvt.data_ptr(), xc.data_ptr(),
+                                  yc.data_ptr(), float(penalty_u), float(penalty_v), float(step_scale),
+                                  int(max_iter), float(tol), trace.data_ptr(), scores.data_ptr(), ctypes.byref(it),
+                                  ctypes.byref(done), resume, limit, ws.data_ptr(), nbytes, stream())
+
+    def diverged(status):
+        k = it.value
+        return dict(trace=scores[:k].tolist())
+
+    if on_iteration is None:
+        status = lib.cnmf_admm_run(*args(0, 0))
+        _lib.check(status, **diverged(status))
+    else:
+        resume = 0
+        seen = 0
+        while True:
+            status = lib.cnmf_admm_run(*args(resume, 1))
+            _lib.check(status, **diverged(status))
+            resume = 1
+            if it.value > seen:
+                seen = it.value
+                Lh, Rh = left.Q, right.Q
+                st = AdmmState(xc=out(xc.clone(), A.on_host), yc=out(yc.clone(), A.on_host),
+                               u=out(u.clone(), A.on_host), v=out(vt.t().contiguous(), A.on_host),
+                               dual_u=out(du.clone(), A.on_host), dual_v=out(dvt.t().contiguous(), A.on_host),
+                               penalty_u=penalty_u, penalty_v=penalty_v, step_scale=step_scale)
+                on_iteration(seen - 1, st)
+            if done.value:
+                break
+    iters = it.value
+    rel = _rel_error(A, u, vt)
+    return FactorPair(X=out(u, A.on_host), Y=out(vt.t().contiguous(), A.on_host), iterations=iters,
+                      objective_trace=trace[:iters].tolist(), rel_error=rel)
