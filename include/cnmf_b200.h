@@ -96,6 +96,13 @@ int cnmf_pass_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const
 size_t cnmf_compress_workspace(int64_t m, int64_t n, int s);
 int cnmf_structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed,
                              int side, float* Q, void* ws, size_t ws_bytes, void* stream);
+/* Same as cnmf_structured_compress without the final host synchronisation:
+ * the numeric status stays in `ws` until cnmf_compress_check(ws, m, n, s)
+ * reads it (synchronising `stream`). Lets a caller enqueue several range
+ * finders and projections back to back. */
+int cnmf_structured_compress_async(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed,
+                                   int side, float* Q, void* ws, size_t ws_bytes, void* stream);
+int cnmf_compress_check(const void* ws, int64_t m, int64_t n, int s, void* stream);
 /* orthonormalise a panel in place (compress.py:136 canonical_qr, Q factor);
  * R (s x s, fp64, device, may be NULL) receives the triangular factor. */
 int cnmf_orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, void* stream);

@@ -37,6 +37,9 @@ SIGNATURES = {
     "cnmf_pass_transpose": (c_int, [vp, c_i64, c_i64, c_i64, vp, c_int, vp, vp]),
     "cnmf_compress_workspace": (c_size, [c_i64, c_i64, c_int]),
     "cnmf_structured_compress": (c_int, [vp, c_i64, c_i64, c_i64, c_int, c_int, c_u64, c_int, vp, vp, c_size, vp]),
+    "cnmf_structured_compress_async": (c_int, [vp, c_i64, c_i64, c_i64, c_int, c_int, c_u64, c_int, vp, vp, c_size,
+                                               vp]),
+    "cnmf_compress_check": (c_int, [vp, c_i64, c_i64, c_int, vp]),
     "cnmf_orthonormalize": (c_int, [vp, c_i64, c_int, vp, vp, c_size, vp]),
     "cnmf_spa_workspace": (c_size, [c_i64, c_int]),
     "cnmf_panel_to_f64": (c_int, [vp, c_i64, c_int, vp, c_i64, vp]),

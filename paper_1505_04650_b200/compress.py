@@ -91,21 +91,32 @@ def _require_feasible(cfg, m, n):
         raise InfeasibleRankError(f"basis width {s} exceeds min(m, n) = {min(m, n)}; adjust_config first")
 
 
-def _compress(a, cfg, side):
+def _compress(a, cfg, side, check=True):
+    """Device range finder. check=False enqueues without synchronising; the
+    caller must then call ``basis.check()`` before trusting the result."""
     A = DeviceMatrix(a)
     _require_feasible(cfg, A.m, A.n)
     s = cfg.basis_cols
     S = panel_ld(s)
     rows = A.m if side == 0 else A.n
-    q = zeros((rows, S))
+    q = empty((rows, S))
     lib = _lib.load()
     nbytes = lib.cnmf_compress_workspace(A.m, A.n, s)
     ws = workspace(nbytes)
-    _lib.call("cnmf_structured_compress", A.ptr, A.m, A.n, A.lda, s, cfg.w, cfg.seed & MASK64, side,
-              q.data_ptr(), ws.data_ptr(), nbytes, stream())
+    name = "cnmf_structured_compress" if check else "cnmf_structured_compress_async"
+    _lib.call(name, A.ptr, A.m, A.n, A.lda, s, cfg.w, cfg.seed & MASK64, side, q.data_ptr(), ws.data_ptr(), nbytes,
+              stream())
     view = q[:, :s]
-    Q = view.double().cpu().numpy() if A.on_host else view
-    return CompressionBasis(Q=Q, kind="structured", config=cfg, panel=q), A
+    Q = view.double().cpu().numpy() if (A.on_host and check) else view
+    basis = CompressionBasis(Q=Q, kind="structured", config=cfg, panel=q)
+    basis._ws = ws
+    basis._dims = (A.m, A.n, s)
+    return basis, A
+
+
+def _check(basis):
+    m, n, s = basis._dims
+    _lib.call("cnmf_compress_check", basis._ws.data_ptr(), m, n, s, stream())
 
 
 def structured_compress(a, cfg, reorthogonalize=False, scratch_dir=None):

@@ -1,49 +1,108 @@
 // Compressed ADMM NMF (reference nmf.py:306-377, KKT residual nmf.py:281-303).
 //
-// Per iteration two launches:
-//   core kernel (one CTA): finishes the previous iteration's KKT score from
-//     the reduced partials and applies the stopping / divergence rules on the
-//     device, then solves the two r x r ridge systems for Xc and Yc
-//     (Cholesky by one warp, triangular solves by all threads) and records
-//     the compressed objective ||L^T A R^T - Xc Yc||^2;
-//   split kernel (all SMs): one fused sweep over the rows of L and of R^T
-//     that forms L Xc (resp. Yc R), projects onto the nonnegative orthant,
-//     takes the dual step and accumulates every reduction the next core step
-//     needs (L^T U, L^T dU, V R^T, dV R^T, feasibility and complementarity
-//     sums) — U, V, dU, dV are each read and written exactly once.
+// The whole iteration loop is ONE persistent cooperative kernel (one CTA per
+// SM) with a single grid-wide barrier per iteration:
+//
+//   split(k)  every CTA owns a contiguous slice of the rows of L (m x s) or of
+//             R^T (n x s): it forms L Xc_k (resp. Yc_k R), projects onto the
+//             nonnegative orthant, takes the dual step and accumulates every
+//             reduction the next step needs (L^T U, L^T dU, R V^T, R dV^T,
+//             feasibility and complementarity sums) into acc[k % 3];
+//   barrier
+//   score(k)  every CTA redundantly finishes the six KKT residuals from
+//             acc[k % 3] and applies the reference's stopping and divergence
+//             rules — all CTAs reach the same decision without a broadcast;
+//   core(k+1) every CTA redundantly solves the two r x r ridge systems for
+//             Xc_{k+1}, Yc_{k+1} (block Gauss-Jordan inverses) in shared
+//             memory, so the next split needs no global round trip.
+//
+// When a CTA's slice fits in shared memory (configs[1]: ~100 rows per CTA),
+// its rows of the basis, U and dU stay resident there for the whole run: an
+// iteration then touches global memory only for the reduced partials.
+// acc is triple-buffered: a buffer is zeroed (by CTA 0, during split k) two
+// barriers after its last reader, so one barrier per iteration suffices;
+// reads of the reduced partials bypass L1 (ld.global.cg).
+// Sizes are compile-time (s <= SP, r <= RP, zero padded: exact) so every
+// small product is an unrolled register-blocked loop.
 // The state is fp64 (the method is sensitive to roundoff over hundreds of
 // iterations); the bases are the fp32 panels produced by the compression.
-// Batches of iterations are captured once into a CUDA graph and replayed;
-// a device flag turns the remaining kernels into no-ops after convergence, so
-// the iteration count is exactly the reference's.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
 namespace cnmf {
-int64_t launch_count();
 namespace {
 
-constexpr int kAdmmMax = 64;  // s, r <= 64
-constexpr int kTile = 64;     // rows per split-kernel tile
-constexpr int kSplitThreads = 256;
+constexpr int kMax = 64;      // s, r <= 64
+constexpr int kTile = 32;     // rows per streamed split tile
+constexpr int kThreads = 256;
+constexpr size_t kSmemCap = 200 * 1024;
 
 struct Ctrl {
-  int k;         // next iteration index
+  int k;         // next iteration index (resume point)
   int done;
   int iters;     // iterations completed when done
   int diverged;  // iteration index (0-based) that tripped the divergence rule, or -1
+  unsigned int bar_count;
+  unsigned int bar_gen;
 };
 
-// reduced partials written by the split kernel for one iteration
+// reduced partials of one split sweep (stride kMax so every SP/RP fits)
 struct Acc {
-  double LtU[kAdmmMax * kAdmmMax];   // s x r : L^T U
-  double LtDU[kAdmmMax * kAdmmMax];  // s x r : L^T dU
-  double RtV[kAdmmMax * kAdmmMax];   // s x r : R V^T   (= (V R^T)^T)
-  double RtDV[kAdmmMax * kAdmmMax];  // s x r : R dV^T
-  double scal[4];                    // feasL^2, compL^2, feasR^2, compR^2
+  double LtU[kMax * kMax];   // s x r : L^T U
+  double LtDU[kMax * kMax];  // s x r : L^T dU
+  double RtV[kMax * kMax];   // s x r : R V^T   (= (V R^T)^T)
+  double RtDV[kMax * kMax];  // s x r : R dV^T
+  double scal[4];            // feasL^2, compL^2, feasR^2, compR^2
 };
+
+struct Side {
+  const float* P;  // panel (rows x S)
+  int64_t rows;
+  int S;
+  double* U;       // rows x r
+  double* D;       // rows x r
+  double pen;
+};
+
+struct Params {
+  const double* core;
+  Side left, right;
+  int s, r;
+  double pu, pv, step, tol;
+  int max_iter;
+  int step_limit;  // > 0: stop after this many splits (resume later)
+  int fresh;
+  int nblk_left;
+  int64_t rows_left, rows_right;  // rows per CTA slice
+  double* xc_g;
+  double* yc_g;
+  double* trace;
+  double* scores;
+  Ctrl* ctrl;
+  Acc* acc;  // [3]
+  unsigned long long* prof;  // optional: per-iteration phase timestamps (CTA 0)
+};
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void stamp(const Params& p, int k, int slot) {
+  if (p.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && k < 256) p.prof[k * 8 + slot] = gtime();
+}
+
+__device__ unsigned long long* g_prof_ptr;  // CTA 0 phase stamps (profiling only)
+__device__ int g_prof_k;
+__device__ __forceinline__ void sstamp(int slot) {
+  if (g_prof_ptr != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && g_prof_k < 256)
+    g_prof_ptr[g_prof_k * 8 + slot] = gtime();
+}
+
+__device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
 
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
@@ -51,224 +110,281 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-// Cholesky of the r x r SPD matrix M (row-major, stride r) in place (lower
-// factor in the lower triangle) by warp 0.
-__device__ void warp_cholesky(double* M, int r) {
-  const int lane = threadIdx.x & 31;
+__device__ void grid_barrier(Ctrl* c) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = &c->bar_gen;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(&c->bar_count, 1u) == gridDim.x - 1) {
+      c->bar_count = 0;
+      __threadfence();
+      atomicAdd(&c->bar_gen, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// out(i, j) = sum_k a(i, k) b(k, j) for an MO x NO output (MO, NO multiples
+// of 16): a 16 x 16 thread grid, each thread a (MO/16) x (NO/16) register
+// block (i = ti + 16 a, j = tj + 16 b), so per k it loads MO/16 + NO/16
+// operands for (MO/16)(NO/16) FMAs. Operands are read through accessors;
+// callers use odd leading dimensions, so transposed reads are conflict-free.
+template <int MO, int NO, int K, class FA, class FB, class FO>
+__device__ __forceinline__ void bgemm(FA a, FB b, FO o) {
+  static_assert(MO % 16 == 0 && NO % 16 == 0, "bgemm tiles");
+  constexpr int BI = MO / 16, BJ = NO / 16;
+  const int ti = threadIdx.x >> 4, tj = threadIdx.x & 15;
+  double acc[BI][BJ];
+#pragma unroll
+  for (int x = 0; x < BI; ++x)
+#pragma unroll
+    for (int y = 0; y < BJ; ++y) acc[x][y] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < K; ++k) {
+    double av[BI], bv[BJ];
+#pragma unroll
+    for (int x = 0; x < BI; ++x) av[x] = a(ti + 16 * x, k);
+#pragma unroll
+    for (int y = 0; y < BJ; ++y) bv[y] = b(k, tj + 16 * y);
+#pragma unroll
+    for (int x = 0; x < BI; ++x)
+#pragma unroll
+      for (int y = 0; y < BJ; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
+  }
+#pragma unroll
+  for (int x = 0; x < BI; ++x)
+#pragma unroll
+    for (int y = 0; y < BJ; ++y) o(ti + 16 * x, tj + 16 * y, acc[x][y]);
+}
+
+// Gauss-Jordan inverse of the leading r x r block of the RP x RP SPD matrix
+// M by the whole block, ping-ponging between M and T so that each pivot step
+// reads only the previous matrix: one barrier per pivot. The padded block is
+// pen*I and is inverted on the diagonal. The result ends in M.
+template <int RP>
+__device__ void gj_inverse(double* M, double* T, int r) {
+  constexpr int LR = RP + 1;
+  const int tid = threadIdx.x;
+  double* src = M;
+  double* dst = T;
   for (int k = 0; k < r; ++k) {
-    const double d = sqrt(M[k * r + k]);
-    __syncwarp();
-    for (int i = k + 1 + lane; i < r; i += 32) M[i * r + k] /= d;
-    if (lane == 0) M[k * r + k] = d;
-    __syncwarp();
-    for (int i = k + 1 + lane; i < r; i += 32) {
-      const double lik = M[i * r + k];
-      for (int j = k + 1; j <= i; ++j) M[i * r + j] -= lik * M[j * r + k];
-    }
-    __syncwarp();
-  }
-}
-
-// x = M^{-1} b for a lower Cholesky factor (row-major, stride r), in place.
-__device__ void chol_solve_vec(const double* L, int r, double* x, int stride) {
-  for (int i = 0; i < r; ++i) {
-    double v = x[i * stride];
-    for (int j = 0; j < i; ++j) v -= L[i * r + j] * x[j * stride];
-    x[i * stride] = v / L[i * r + i];
-  }
-  for (int i = r - 1; i >= 0; --i) {
-    double v = x[i * stride];
-    for (int j = i + 1; j < r; ++j) v -= L[j * r + i] * x[j * stride];
-    x[i * stride] = v / L[i * r + i];
-  }
-}
-
-__global__ void __launch_bounds__(512)
-    admm_core(const double* __restrict__ core, int s, int r, double pu, double pv, int max_iter, double tol,
-              Ctrl* ctrl, Acc* acc, double* __restrict__ xc_g, double* __restrict__ yc_g, double* __restrict__ trace,
-              double* __restrict__ scores) {
-  extern __shared__ double sm[];
-  double* C = sm;                    // s x s core
-  double* xc = C + s * s;            // s x r
-  double* yc = xc + s * r;           // r x s
-  double* W = yc + r * s;            // s x s scratch (E) / r x s rhs
-  double* M = W + s * s;             // r x r
-  __shared__ double red[16][6];
-  __shared__ int s_stop;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  if (ctrl->done) return;
-  const int k = ctrl->k;
-  for (int i = tid; i < s * s; i += nt) C[i] = core[i];
-  for (int i = tid; i < s * r; i += nt) {
-    xc[i] = xc_g[i];
-    yc[i] = yc_g[i];
-  }
-  if (tid == 0) s_stop = 0;
-  __syncthreads();
-  if (k == 0) {
-    // yc = V R^T (nmf.py:342)
-    for (int i = tid; i < r * s; i += nt) {
-      const int a = i / s, j = i % s;
-      yc[i] = acc->RtV[j * r + a];
-    }
-    __syncthreads();
-  } else {
-    // ---- KKT score of iteration k-1 (nmf.py:281-303, 365-374) ----
-    // E = xc yc - C
-    for (int i = tid; i < s * s; i += nt) {
-      const int a = i / s, b = i % s;
-      double v = -C[i];
-      for (int q = 0; q < r; ++q) v += xc[a * r + q] * yc[q * s + b];
-      W[i] = v;
-    }
-    __syncthreads();
-    double g1 = 0.0, g2 = 0.0;
-    // grad_left = E yc^T + L^T dU  (s x r)
-    for (int i = tid; i < s * r; i += nt) {
-      const int a = i / r, q = i % r;
-      double v = acc->LtDU[a * r + q];
-      for (int b = 0; b < s; ++b) v += W[a * s + b] * yc[q * s + b];
-      g1 += v * v;
-    }
-    // grad_right = xc^T E + dV R^T  (r x s)
-    for (int i = tid; i < r * s; i += nt) {
-      const int q = i / s, b = i % s;
-      double v = acc->RtDV[b * r + q];
-      for (int a = 0; a < s; ++a) v += xc[a * r + q] * W[a * s + b];
-      g2 += v * v;
-    }
-    g1 = wsum(g1);
-    g2 = wsum(g2);
-    if (lane == 0) {
-      red[warp][0] = g1;
-      red[warp][1] = g2;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double a = 0.0, b = 0.0;
-      for (int w = 0; w < nt / 32; ++w) {
-        a += red[w][0];
-        b += red[w][1];
-      }
-      const double score = fmax(fmax(fmax(sqrt(a), sqrt(b)), fmax(sqrt(acc->scal[0]), sqrt(acc->scal[2]))),
-                                fmax(sqrt(acc->scal[1]), sqrt(acc->scal[3])));
-      scores[k - 1] = score;
-      if (score < tol) {
-        s_stop = 1;
-      } else if (k - 1 >= 50 && score > 10.0 * scores[k - 1 - 50]) {
-        s_stop = 1;
-        ctrl->diverged = k - 1;
-      } else if (k >= max_iter) {
-        s_stop = 1;
-      }
-      if (s_stop) {
-        ctrl->done = 1;
-        ctrl->iters = k;
+    const double inv = 1.0 / src[k * LR + k];
+#pragma unroll
+    for (int t = 0; t < (RP * RP + kThreads - 1) / kThreads; ++t) {
+      const int idx = tid + t * kThreads;
+      if (idx < RP * RP) {
+        const int i = idx / RP, j = idx % RP;
+        if (i < r && j < r) {
+          const double nk = ((j == k) ? 1.0 : src[k * LR + j]) * inv;
+          dst[i * LR + j] = (i == k) ? nk : ((j == k) ? 0.0 : src[i * LR + j]) - src[i * LR + k] * nk;
+        }
       }
     }
     __syncthreads();
-    if (s_stop) return;
+    double* tmp = src;
+    src = dst;
+    dst = tmp;
   }
-  // ---- Xc: solve (yc yc^T + pu I) xc^T = rhs^T, rhs = C yc^T + pu L^T U - L^T dU
-  for (int i = tid; i < r * r; i += nt) {
-    const int a = i / r, b = i % r;
-    double v = (a == b) ? pu : 0.0;
-    for (int j = 0; j < s; ++j) v += yc[a * s + j] * yc[b * s + j];
-    M[i] = v;
+  if (src != M) {
+    for (int idx = tid; idx < r * RP; idx += kThreads) {
+      const int i = idx / RP, j = idx % RP;
+      if (j < r) M[i * LR + j] = src[i * LR + j];
+    }
   }
-  for (int i = tid; i < s * r; i += nt) {
-    const int a = i / r, q = i % r;
-    double v = pu * acc->LtU[a * r + q] - acc->LtDU[a * r + q];
-    for (int b = 0; b < s; ++b) v += C[a * s + b] * yc[q * s + b];
-    xc[i] = v;  // rhs, solved in place row by row
+  for (int i = r + tid; i < RP; i += kThreads) M[i * LR + i] = 1.0 / M[i * LR + i];
+  __syncthreads();
+}
+
+// Gauss-Jordan inverse of the leading r x r block by ONE warp (RP <= 32):
+// lane i owns row i in shared memory; per pivot the pivot row is broadcast
+// into registers and each lane updates its own row, so the only
+// synchronisation is __syncwarp. The other warps stay free for independent
+// work meanwhile.
+template <int RP>
+__device__ void gj_warp(double* M, int r) {
+  static_assert(RP <= 32, "one row per lane");
+  constexpr int LR = RP + 1;
+  const int i = threadIdx.x & 31;
+  double row[RP];
+#pragma unroll
+  for (int j = 0; j < RP; ++j) row[j] = (i < RP) ? M[i * LR + j] : 0.0;
+  for (int k = 0; k < r; ++k) {
+    double f = 0.0;
+#pragma unroll
+    for (int j = 0; j < RP; ++j) f = (j == k) ? row[j] : f;  // row_i[k] without dynamic indexing
+    const double inv = 1.0 / __shfl_sync(0xffffffffu, f, k);
+#pragma unroll
+    for (int j = 0; j < RP; ++j) {
+      const double nk = ((j == k) ? 1.0 : __shfl_sync(0xffffffffu, row[j], k)) * inv;
+      row[j] = (i == k) ? nk : ((j == k) ? 0.0 : row[j]) - f * nk;
+    }
   }
-  __syncthreads();
-  if (warp == 0) warp_cholesky(M, r);
-  __syncthreads();
-  for (int a = tid; a < s; a += nt) chol_solve_vec(M, r, xc + a * r, 1);
-  __syncthreads();
-  // ---- Yc: solve (xc^T xc + pv I) yc = xc^T C + pv V R^T - dV R^T
-  for (int i = tid; i < r * r; i += nt) {
-    const int a = i / r, b = i % r;
-    double v = (a == b) ? pv : 0.0;
-    for (int j = 0; j < s; ++j) v += xc[j * r + a] * xc[j * r + b];
-    M[i] = v;
+  if (i < RP) {
+#pragma unroll
+    for (int j = 0; j < RP; ++j) M[i * LR + j] = (j >= r && i == j) ? 1.0 / row[j] : row[j];
   }
-  for (int i = tid; i < r * s; i += nt) {
-    const int q = i / s, b = i % s;
-    double v = pv * acc->RtV[b * r + q] - acc->RtDV[b * r + q];
-    for (int a = 0; a < s; ++a) v += xc[a * r + q] * C[a * s + b];
-    yc[i] = v;
-  }
-  __syncthreads();
-  if (warp == 0) warp_cholesky(M, r);
-  __syncthreads();
-  for (int b = tid; b < s; b += nt) chol_solve_vec(M, r, yc + b, s);
-  __syncthreads();
-  // ---- objective trace ||C - xc yc||^2 (nmf.py:360)
-  double t = 0.0;
-  for (int i = tid; i < s * s; i += nt) {
-    const int a = i / s, b = i % s;
-    double v = C[i];
-    for (int q = 0; q < r; ++q) v -= xc[a * r + q] * yc[q * s + b];
-    t += v * v;
-  }
-  t = wsum(t);
-  if (lane == 0) red[warp][0] = t;
-  for (int i = tid; i < s * r; i += nt) {
-    xc_g[i] = xc[i];
-    yc_g[i] = yc[i];
-  }
-  // reset the partials for this iteration's split sweep
-  double* z = (double*)acc;
-  for (int i = tid; i < (int)(sizeof(Acc) / 8); i += nt) z[i] = 0.0;
-  __syncthreads();
-  if (tid == 0) {
-    double a = 0.0;
-    for (int w = 0; w < nt / 32; ++w) a += red[w][0];
-    trace[k] = a;
-    ctrl->k = k + 1;
+  __syncwarp();
+}
+
+// out(i, j) = sum_k a(i, k) b(k, j) by threads [first, kThreads) (plain
+// strided loop; used for work that overlaps a one-warp inverse).
+template <int MO, int NO, int K, class FA, class FB, class FO>
+__device__ __forceinline__ void sgemm_part(int first, FA a, FB b, FO o) {
+  for (int idx = threadIdx.x - first; idx < MO * NO; idx += kThreads - first) {
+    const int i = idx / NO, j = idx % NO;
+    double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; k += 2) {
+      v0 = fma(a(i, k), b(k, j), v0);
+      v1 = fma(a(i, k + 1), b(k + 1, j), v1);
+    }
+    o(i, j, v0 + v1);
   }
 }
 
-// One side of the split/dual sweep. For the left side P = L (m x S panel),
-// X = xc (s x r); for the right side P = R^T (n x S panel), X = yc^T.
-// mode 0: accumulate P^T U only (initial projection); mode 1: full update.
-struct SideArgs {
-  const float* P;
-  int64_t rows;
-  int S;
-  double* U;
-  double* D;
-  double pen;
-  double* accU;   // s x r
-  double* accD;   // s x r
-  double* scal;   // [feas, comp]
-  int transposeX; // X read as yc (r x s) transposed
+template <int SP, int RP>
+struct Smem {
+  static constexpr int LS = SP + 1, LR = RP + 1;  // odd strides: conflict-free columns
+  double* C;   // SP x SP
+  double* xc;  // SP x RP
+  double* yc;  // RP x SP
+  double* X;   // SP x RP  split operand (xc or yc^T)
+  double* W;   // SP x SP  scratch
+  double* M;   // RP x RP
+  double* T;   // RP x RP  Gauss-Jordan ping-pong buffer
+  double* fold;  // 256 x 16: row-group folding of the split accumulators
+  double* Pt;  // rows x SP   (resident slice or one tile)
+  double* Ut;  // rows x RP
+  double* Dt;  // rows x RP
+  __device__ Smem(double* base, int rows) {
+    C = base;
+    xc = C + SP * LS;
+    yc = xc + SP * LR;
+    X = yc + RP * LS;
+    W = X + SP * LR;
+    M = W + SP * LS;
+    T = M + RP * LR;
+    fold = T + RP * LR;
+    Pt = fold + kThreads * 16;
+    Ut = Pt + (size_t)rows * SP;
+    Dt = Ut + (size_t)rows * RP;
+  }
+  static size_t bytes(int rows) {
+    return ((size_t)2 * SP * LS + 2 * SP * LR + RP * LS + 2 * RP * LR + kThreads * 16 +
+            (size_t)rows * (SP + 2 * RP)) * 8;
+  }
 };
 
-__device__ void split_side(const SideArgs& a, const double* Xg, int s, int r, double step, int mode, int bid,
-                           int nblk, double* sm) {
-  double* X = sm;                          // s x r (padded to 64 x 64)
-  double* Pt = X + kAdmmMax * kAdmmMax;    // kTile x 64
-  double* Ut = Pt + kTile * kAdmmMax;      // kTile x 64
-  double* Dt = Ut + kTile * kAdmmMax;      // kTile x 64
-  __shared__ double red[kSplitThreads / 32][2];
-  const int tid = threadIdx.x;
-  const int rp = (r + 3) & ~3, sp = (s + 3) & ~3;
-  for (int i = tid; i < kAdmmMax * kAdmmMax; i += kSplitThreads) {
-    const int j = i / kAdmmMax, b = i % kAdmmMax;
-    double v = 0.0;
-    if (j < s && b < r) v = a.transposeX ? Xg[b * s + j] : Xg[j * r + b];
-    X[i] = v;
+// KKT score of the state (xc, yc) with the split reductions `a` (nmf.py:281-303).
+template <int SP, int RP>
+__device__ double kkt_score(const Smem<SP, RP>& sm, const Acc* a, double* red, double* objective) {
+  constexpr int LS = SP + 1, LR = RP + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* xc = sm.xc;
+  const double* yc = sm.yc;
+  double* W = sm.W;
+  const double* C = sm.C;
+  // E = xc yc - C
+  double e2 = 0.0;
+  bgemm<SP, SP, RP>([&](int i, int k) { return xc[i * LR + k]; }, [&](int k, int j) { return yc[k * LS + j]; },
+                    [&](int i, int j, double v) {
+                      const double e = v - C[i * LS + j];
+                      W[i * LS + j] = e;
+                      e2 += e * e;
+                    });
+  __syncthreads();
+  double g1 = 0.0, g2 = 0.0;
+  // E yc^T + L^T dU   and   xc^T E + dV R^T
+  bgemm<SP, RP, SP>([&](int i, int k) { return W[i * LS + k]; }, [&](int k, int j) { return yc[j * LS + k]; },
+                    [&](int i, int j, double v) {
+                      const double t = v + ld(&a->LtDU[i * kMax + j]);
+                      g1 += t * t;
+                    });
+  bgemm<RP, SP, SP>([&](int i, int k) { return xc[k * LR + i]; }, [&](int k, int j) { return W[k * LS + j]; },
+                    [&](int i, int j, double v) {
+                      const double t = v + ld(&a->RtDV[j * kMax + i]);
+                      g2 += t * t;
+                    });
+  g1 = wsum(g1);
+  g2 = wsum(g2);
+  e2 = wsum(e2);
+  if (lane == 0) {
+    red[3 * warp] = g1;
+    red[3 * warp + 1] = g2;
+    red[3 * warp + 2] = e2;
   }
-  // accumulator block owned by this thread: rows 4*bj.., cols 4*bb..
-  const int nbb = rp / 4;
-  const int nbj = sp / 4;
-  const int myb = tid;
-  const bool own = myb < nbj * nbb;
-  const int bj = own ? myb / nbb : 0, bb = own ? myb % nbb : 0;
+  __syncthreads();
+  double t1 = 0.0, t2 = 0.0, t3 = 0.0;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) {
+    t1 += red[3 * w];
+    t2 += red[3 * w + 1];
+    t3 += red[3 * w + 2];
+  }
+  *objective = t3;
+  __syncthreads();
+  return fmax(fmax(fmax(sqrt(t1), sqrt(t2)), fmax(sqrt(ld(&a->scal[0])), sqrt(ld(&a->scal[2])))),
+              fmax(sqrt(ld(&a->scal[1])), sqrt(ld(&a->scal[3]))));
+}
+
+// Xc, Yc of the next iteration from the current yc and the split reductions
+// (nmf.py:350-353). For RP <= 32 each r x r inverse runs on warp 0 while the
+// other warps form the matching right-hand side.
+template <int SP, int RP>
+__device__ void core_step(const Smem<SP, RP>& sm, const Acc* a, int s, int r, double pu, double pv) {
+  constexpr int LS = SP + 1, LR = RP + 1;
+  double* xc = sm.xc;
+  double* yc = sm.yc;
+  double* W = sm.W;
+  const double* C = sm.C;
+  double* M = sm.M;
+  // Xc = rhs (yc yc^T + pu I)^{-1},  rhs = C yc^T + pu L^T U - L^T dU
+  bgemm<RP, RP, SP>([&](int i, int k) { return yc[i * LS + k]; }, [&](int k, int j) { return yc[j * LS + k]; },
+                    [&](int i, int j, double v) { M[i * LR + j] = v + (i == j ? pu : 0.0); });
+  __syncthreads();
+  auto rhs1 = [&](int i, int j, double v) {
+    W[i * LS + j] = v + pu * ld(&a->LtU[i * kMax + j]) - ld(&a->LtDU[i * kMax + j]);
+  };
+  bgemm<SP, RP, SP>([&](int i, int k) { return C[i * LS + k]; }, [&](int k, int j) { return yc[j * LS + k]; },
+                    rhs1);
+  gj_inverse<RP>(M, sm.T, r);  // its first barrier also orders the products above
+  sstamp(6);
+  bgemm<SP, RP, RP>([&](int i, int k) { return W[i * LS + k]; }, [&](int k, int j) { return M[k * LR + j]; },
+                    [&](int i, int j, double v) { xc[i * LR + j] = (i < s && j < r) ? v : 0.0; });
+  __syncthreads();
+  // Yc = (xc^T xc + pv I)^{-1} (xc^T C + pv V R^T - dV R^T)
+  bgemm<RP, RP, SP>([&](int i, int k) { return xc[k * LR + i]; }, [&](int k, int j) { return xc[k * LR + j]; },
+                    [&](int i, int j, double v) { M[i * LR + j] = v + (i == j ? pv : 0.0); });
+  __syncthreads();
+  auto rhs2 = [&](int i, int j, double v) {
+    W[i * LS + j] = v + pv * ld(&a->RtV[j * kMax + i]) - ld(&a->RtDV[j * kMax + i]);
+  };
+  bgemm<RP, SP, SP>([&](int i, int k) { return xc[k * LR + i]; }, [&](int k, int j) { return C[k * LS + j]; },
+                    rhs2);
+  gj_inverse<RP>(M, sm.T, r);
+  sstamp(7);
+  bgemm<RP, SP, RP>([&](int i, int k) { return M[i * LR + k]; }, [&](int k, int j) { return W[k * LS + j]; },
+                    [&](int i, int j, double v) { yc[i * LS + j] = (i < r && j < s) ? v : 0.0; });
+  __syncthreads();
+}
+
+// Split sweep of one CTA over its contiguous slice [r0, r1) of a side.
+// mode 0: only accumulate P^T U (initial projection); mode 1: full update.
+// RES: the slice lives in shared memory (loaded when `load`).
+template <int SP, int RP, bool RES>
+__device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, int s, int r, double step, int mode,
+                           int64_t r0, int64_t r1, bool load, double* accU, double* accD, double* scal,
+                           double* red) {
+  const int tid = threadIdx.x;
+  constexpr int NBJ = SP / 4, NBB = RP / 4, NBLK = NBJ * NBB;
+  constexpr int GROUPS = NBLK >= kThreads ? 1 : kThreads / NBLK;
+  const int grp = tid / NBLK, myb = tid - grp * NBLK;
+  const bool own = grp < GROUPS;
+  const int bj = own ? myb / NBB : 0, bb = own ? myb % NBB : 0;
   double au[4][4], ad[4][4];
 #pragma unroll
   for (int x = 0; x < 4; ++x)
@@ -279,50 +395,97 @@ __device__ void split_side(const SideArgs& a, const double* Xg, int s, int r, do
     }
   double feas = 0.0, comp = 0.0;
   const double invpen = 1.0 / a.pen, sp_ = step * a.pen;
-  for (int64_t t0 = (int64_t)bid * kTile; t0 < a.rows; t0 += (int64_t)nblk * kTile) {
-    const int nr = (int)min64(kTile, a.rows - t0);
-    __syncthreads();
-    for (int i = tid; i < kTile * kAdmmMax; i += kSplitThreads) {
-      const int rr = i / kAdmmMax, c = i % kAdmmMax;
-      const bool in = rr < nr;
-      Pt[i] = (in && c < s) ? (double)a.P[(t0 + rr) * a.S + c] : 0.0;
-      if (mode == 0) {
-        Ut[i] = (in && c < r) ? a.U[(t0 + rr) * r + c] : 0.0;
-        Dt[i] = 0.0;
-      } else {
-        Dt[i] = (in && c < r) ? a.D[(t0 + rr) * r + c] : 0.0;
-      }
+  constexpr int LS = SP + 1, LR = RP + 1;
+  // split operand X (SP x RP): xc, or yc^T for the right side
+  if (mode == 1) {
+    for (int i = tid; i < SP * RP; i += kThreads) {
+      const int j = i / RP, b = i % RP;
+      sm.X[j * LR + b] = right ? sm.yc[b * LS + j] : sm.xc[j * LR + b];
     }
+  }
+  const int64_t span = RES ? (r1 - r0) : kTile;
+  for (int64_t t0 = r0; t0 < r1; t0 += span) {
+    const int nr = (int)min64(span, r1 - t0);
     __syncthreads();
-    if (mode == 1) {
-      // lx = P X ; u = max(lx + d/pen, 0) ; d += step*pen*(lx - u)
-      for (int i = tid; i < kTile * r; i += kSplitThreads) {
-        const int rr = i / r, b = i % r;
-        if (rr >= nr) continue;
-        double lx = 0.0;
-        for (int j = 0; j < s; ++j) lx += Pt[rr * kAdmmMax + j] * X[j * kAdmmMax + b];
-        const double d0 = Dt[rr * kAdmmMax + b];
-        const double u = fmax(lx + d0 * invpen, 0.0);
-        const double d1 = d0 + sp_ * (lx - u);
-        Ut[rr * kAdmmMax + b] = u;
-        Dt[rr * kAdmmMax + b] = d1;
-        a.U[(t0 + rr) * r + b] = u;
-        a.D[(t0 + rr) * r + b] = d1;
-        const double fe = lx - u;
-        feas += fe * fe;
-        const double du = d1 * u;
-        comp += du * du + (d1 > 0.0 ? d1 * d1 : 0.0) + (u < 0.0 ? u * u : 0.0);
+    if (!RES || load) {
+      for (int i = tid; i < nr * SP; i += kThreads) {
+        const int rr = i / SP, c = i % SP;
+        sm.Pt[i] = (c < s) ? (double)a.P[(t0 + rr) * a.S + c] : 0.0;
+      }
+      for (int i = tid; i < nr * RP; i += kThreads) {
+        const int rr = i / RP, c = i % RP;
+        if (mode == 0) {
+          sm.Ut[i] = (c < r) ? a.U[(t0 + rr) * r + c] : 0.0;
+          sm.Dt[i] = 0.0;
+        } else {
+          sm.Dt[i] = (c < r) ? a.D[(t0 + rr) * r + c] : 0.0;
+        }
       }
       __syncthreads();
     }
+    if (mode == 1) {
+      // lx = P X ; u = max(lx + d/pen, 0) ; d += step*pen*(lx - u)   (nmf.py:354-357)
+      // 16 threads across b (BJ values each), 16 row groups of BR rows
+      constexpr int BJ = RP / 16, BR = (8 / BJ) > 0 ? 8 / BJ : 1;
+      const int tb = tid & 15, tr = tid >> 4;
+      for (int rbase = 0; rbase < nr; rbase += 16 * BR) {
+        double acc[BR][BJ];
+#pragma unroll
+        for (int x = 0; x < BR; ++x)
+#pragma unroll
+          for (int y = 0; y < BJ; ++y) acc[x][y] = 0.0;
+        int rows[BR];
+#pragma unroll
+        for (int x = 0; x < BR; ++x) rows[x] = min(rbase + tr + 16 * x, nr - 1);
+#pragma unroll 4
+        for (int j = 0; j < SP; ++j) {
+          double pv[BR], xv[BJ];
+#pragma unroll
+          for (int x = 0; x < BR; ++x) pv[x] = sm.Pt[rows[x] * SP + j];
+#pragma unroll
+          for (int y = 0; y < BJ; ++y) xv[y] = sm.X[j * LR + tb + 16 * y];
+#pragma unroll
+          for (int x = 0; x < BR; ++x)
+#pragma unroll
+            for (int y = 0; y < BJ; ++y) acc[x][y] = fma(pv[x], xv[y], acc[x][y]);
+        }
+#pragma unroll
+        for (int x = 0; x < BR; ++x) {
+          const int rr = rbase + tr + 16 * x;
+          if (rr >= nr) continue;
+#pragma unroll
+          for (int y = 0; y < BJ; ++y) {
+            const int b = tb + 16 * y;
+            if (b >= r) continue;
+            const int i = rr * RP + b;
+            const double lx = acc[x][y];
+            const double d0 = sm.Dt[i];
+            const double u = fmax(lx + d0 * invpen, 0.0);
+            const double d1 = d0 + sp_ * (lx - u);
+            sm.Ut[i] = u;
+            sm.Dt[i] = d1;
+            if (!RES) {
+              a.U[(t0 + rr) * r + b] = u;
+              a.D[(t0 + rr) * r + b] = d1;
+            }
+            const double fe = lx - u;
+            feas += fe * fe;
+            const double du = d1 * u;
+            comp += du * du + (d1 > 0.0 ? d1 * d1 : 0.0);  // u >= 0: neg(u) = 0
+          }
+        }
+      }
+      __syncthreads();
+      if (mode == 1) sstamp(4);
+    }
     if (own) {
-      for (int rr = 0; rr < nr; ++rr) {
+      for (int rr = grp; rr < nr; rr += GROUPS) {
         double pv[4], uv[4], dv[4];
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
-          pv[x] = Pt[rr * kAdmmMax + 4 * bj + x];
-          uv[x] = Ut[rr * kAdmmMax + 4 * bb + x];
-          dv[x] = Dt[rr * kAdmmMax + 4 * bb + x];
+          pv[x] = sm.Pt[rr * SP + 4 * bj + x];
+          uv[x] = sm.Ut[rr * RP + 4 * bb + x];
+          dv[x] = sm.Dt[rr * RP + 4 * bb + x];
         }
 #pragma unroll
         for (int x = 0; x < 4; ++x)
@@ -334,48 +497,218 @@ __device__ void split_side(const SideArgs& a, const double* Xg, int s, int r, do
       }
     }
   }
-  if (own) {
+  if (mode == 1) {
+    __syncthreads();
+    sstamp(5);
+  }
+  // fold the row groups through shared memory (the W scratch), then one
+  // atomic per accumulator entry per CTA
+  double* fold = sm.fold;  // GROUPS x NBLK x 16 <= kThreads x 16 doubles
+  for (int half = 0; half < (mode == 1 ? 2 : 1); ++half) {
+    if (GROUPS > 1) {
+      __syncthreads();
+      if (own)
 #pragma unroll
-    for (int x = 0; x < 4; ++x)
+        for (int x = 0; x < 4; ++x)
 #pragma unroll
-      for (int y = 0; y < 4; ++y) {
-        const int j = 4 * bj + x, b = 4 * bb + y;
-        if (j < s && b < r) {
-          atomicAdd(&a.accU[j * r + b], au[x][y]);
-          if (mode == 1) atomicAdd(&a.accD[j * r + b], ad[x][y]);
+          for (int y = 0; y < 4; ++y) fold[(grp * NBLK + myb) * 16 + x * 4 + y] = half ? ad[x][y] : au[x][y];
+      __syncthreads();
+    }
+    if (own && grp == 0) {
+      double* accp = half ? accD : accU;
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          double v = half ? ad[x][y] : au[x][y];
+          if (GROUPS > 1) {
+            v = 0.0;
+            for (int g = 0; g < GROUPS; ++g) v += fold[(g * NBLK + myb) * 16 + x * 4 + y];
+          }
+          const int j = 4 * bj + x, b = 4 * bb + y;
+          if (j < s && b < r) atomicAdd(&accp[j * kMax + b], v);
         }
-      }
+    }
   }
   if (mode == 1) {
     feas = wsum(feas);
     comp = wsum(comp);
     const int lane = tid & 31, warp = tid >> 5;
     if (lane == 0) {
-      red[warp][0] = feas;
-      red[warp][1] = comp;
+      red[2 * warp] = feas;
+      red[2 * warp + 1] = comp;
     }
     __syncthreads();
     if (tid == 0) {
       double f = 0.0, c = 0.0;
-      for (int w = 0; w < kSplitThreads / 32; ++w) {
-        f += red[w][0];
-        c += red[w][1];
+      for (int w = 0; w < kThreads / 32; ++w) {
+        f += red[2 * w];
+        c += red[2 * w + 1];
       }
-      atomicAdd(&a.scal[0], f);
-      atomicAdd(&a.scal[1], c);
+      atomicAdd(&scal[0], f);
+      atomicAdd(&scal[1], c);
     }
+  }
+  __syncthreads();
+}
+
+template <int SP, int RP, bool RES>
+__device__ void split(const Params& p, const Smem<SP, RP>& sm, int mode, bool load, Acc* acc, double* red) {
+  const int b = blockIdx.x;
+  if (b < p.nblk_left) {
+    const int64_t r0 = min64((int64_t)b * p.rows_left, p.left.rows), r1 = min64(r0 + p.rows_left, p.left.rows);
+    split_side<SP, RP, RES>(p.left, sm, false, p.s, p.r, p.step, mode, r0, r1, load, acc->LtU, acc->LtDU,
+                            acc->scal, red);
+  } else {
+    const int64_t bb = b - p.nblk_left;
+    const int64_t r0 = min64(bb * p.rows_right, p.right.rows), r1 = min64(r0 + p.rows_right, p.right.rows);
+    split_side<SP, RP, RES>(p.right, sm, true, p.s, p.r, p.step, mode, r0, r1, load, acc->RtV, acc->RtDV,
+                            acc->scal + 2, red);
   }
 }
 
-__global__ void __launch_bounds__(kSplitThreads)
-    admm_split(SideArgs left, SideArgs right, const double* __restrict__ xc, const double* __restrict__ yc, int s,
-               int r, double step, int mode, int nblk_left, const Ctrl* ctrl) {
-  extern __shared__ double sm[];
-  if (mode == 1 && ctrl->done) return;
-  if ((int)blockIdx.x < nblk_left)
-    split_side(left, xc, s, r, step, mode, blockIdx.x, nblk_left, sm);
-  else
-    split_side(right, yc, s, r, step, mode, blockIdx.x - nblk_left, gridDim.x - nblk_left, sm);
+// write the resident slice of U and dU back to global memory
+template <int SP, int RP>
+__device__ void write_back(const Params& p, const Smem<SP, RP>& sm) {
+  const int b = blockIdx.x;
+  const Side& a = b < p.nblk_left ? p.left : p.right;
+  const int64_t per = b < p.nblk_left ? p.rows_left : p.rows_right;
+  const int64_t bb = b < p.nblk_left ? b : b - p.nblk_left;
+  const int64_t r0 = min64(bb * per, a.rows), r1 = min64(r0 + per, a.rows);
+  const int r = p.r;
+  for (int64_t i = threadIdx.x; i < (r1 - r0) * r; i += kThreads) {
+    const int64_t rr = i / r, c = i - rr * r;
+    a.U[(r0 + rr) * r + c] = sm.Ut[rr * RP + c];
+    a.D[(r0 + rr) * r + c] = sm.Dt[rr * RP + c];
+  }
+}
+
+// clear the used part of a partials buffer
+__device__ void zero_acc(Acc* a, int s, int r) {
+  for (int i = threadIdx.x; i < s * kMax; i += blockDim.x) {
+    if ((i % kMax) < r) {
+      a->LtU[i] = 0.0;
+      a->LtDU[i] = 0.0;
+      a->RtV[i] = 0.0;
+      a->RtDV[i] = 0.0;
+    }
+  }
+  if (threadIdx.x < 4) a->scal[threadIdx.x] = 0.0;
+}
+
+template <int SP, int RP, bool RES>
+__global__ void __launch_bounds__(kThreads, 1) admm_persistent(const Params p) {
+  extern __shared__ double smraw[];
+  __shared__ double red[3 * kThreads / 32];
+  const int s = p.s, r = p.r, tid = threadIdx.x;
+  const Smem<SP, RP> sm(smraw, RES ? (int)max(p.rows_left, p.rows_right) : kTile);
+  Ctrl* c = p.ctrl;
+  if (c->done) return;
+  if (blockIdx.x == 0 && tid == 0) g_prof_ptr = p.prof;
+  constexpr int LS = SP + 1, LR = RP + 1;
+  for (int i = tid; i < SP * SP; i += kThreads) {
+    const int a = i / SP, b = i % SP;
+    sm.C[a * LS + b] = (a < s && b < s) ? p.core[a * s + b] : 0.0;
+  }
+  for (int i = tid; i < SP * RP; i += kThreads) {
+    const int a = i / RP, b = i % RP;
+    sm.xc[a * LR + b] = 0.0;
+    sm.yc[b * LS + a] = 0.0;
+  }
+  __syncthreads();
+  int k = c->k;
+  if (p.fresh) {
+    // initial projections L^T U0 and R V0^T into acc[2] (nmf.py:337-343)
+    split<SP, RP, RES>(p, sm, 0, true, &p.acc[2], red);
+    grid_barrier(c);
+    for (int i = tid; i < r * s; i += kThreads) {  // yc = V0 R^T
+      const int q = i / s, j = i - q * s;
+      sm.yc[q * LS + j] = ld(&p.acc[2].RtV[j * kMax + q]);
+    }
+    __syncthreads();
+    core_step<SP, RP>(sm, &p.acc[2], s, r, p.pu, p.pv);
+    k = 0;
+  } else {
+    for (int i = tid; i < s * r; i += kThreads) {
+      const int a = i / r, b = i - a * r;
+      sm.xc[a * LR + b] = p.xc_g[i];
+      sm.yc[b * LS + a] = p.yc_g[b * s + a];
+    }
+    __syncthreads();
+    // finish the iteration the previous launch stopped after
+    const Acc* a = &p.acc[(k - 1) % 3];
+    double obj;
+    const double score = kkt_score<SP, RP>(sm, a, red, &obj);
+    const bool conv = score < p.tol;
+    const bool div = !conv && k - 1 >= 50 && score > 10.0 * ld(&p.scores[k - 1 - 50]);
+    const bool cap = k >= p.max_iter;
+    if (blockIdx.x == 0 && tid == 0) {
+      p.scores[k - 1] = score;
+      p.trace[k - 1] = obj;
+      if (conv || div || cap) {
+        if (div) c->diverged = k - 1;
+        c->done = 1;
+        c->iters = k;
+      }
+    }
+    if (conv || div || cap) return;
+    core_step<SP, RP>(sm, a, s, r, p.pu, p.pv);
+  }
+  int splits = 0;
+  bool load = !p.fresh;  // fresh runs loaded the slice in the projection sweep
+  for (;;) {
+    // split(k) into acc[k % 3]; CTA 0 clears the buffer split(k+1) will use
+    stamp(p, k, 0);
+    if (blockIdx.x == 0 && tid == 0) g_prof_k = k;
+    if (blockIdx.x == 0) zero_acc(&p.acc[(k + 1) % 3], s, r);
+    split<SP, RP, RES>(p, sm, 1, load, &p.acc[k % 3], red);
+    load = false;
+    ++splits;
+    stamp(p, k, 1);
+    grid_barrier(c);
+    stamp(p, k, 2);
+    if (p.step_limit > 0 && splits >= p.step_limit) {
+      // hand the state to the next launch (which scores iteration k first)
+      if (RES) write_back<SP, RP>(p, sm);
+      if (blockIdx.x == 0) {
+        for (int i = tid; i < s * r; i += kThreads) {
+          const int a = i / r, b = i - a * r;
+          p.xc_g[i] = sm.xc[a * LR + b];
+          p.yc_g[b * s + a] = sm.yc[b * LS + a];
+        }
+        if (tid == 0) c->k = k + 1;
+      }
+      return;
+    }
+    const Acc* a = &p.acc[k % 3];
+    double obj;
+    const double score = kkt_score<SP, RP>(sm, a, red, &obj);
+    stamp(p, k, 3);
+    const bool conv = score < p.tol;
+    // scores[k - 50] was written by CTA 0 at least 50 barriers ago
+    const bool div = !conv && k >= 50 && score > 10.0 * ld(&p.scores[k - 50]);
+    const bool cap = k + 1 >= p.max_iter;
+    if (blockIdx.x == 0 && tid == 0) {
+      p.scores[k] = score;
+      p.trace[k] = obj;  // ||C - xc_k yc_k||^2 (nmf.py:360)
+      if (conv || div || cap) {
+        if (div) c->diverged = k;
+        c->done = 1;
+        c->iters = k + 1;
+        c->k = k + 1;
+      }
+    }
+    if (conv || div || cap) break;
+    core_step<SP, RP>(sm, a, s, r, p.pu, p.pv);
+    ++k;
+  }
+  if (RES) write_back<SP, RP>(p, sm);
+  if (blockIdx.x == 0)
+    for (int i = tid; i < s * r; i += kThreads) {
+      const int a = i / r, b = i - a * r;
+      p.xc_g[i] = sm.xc[a * LR + b];
+      p.yc_g[b * s + a] = sm.yc[b * LS + a];
+    }
 }
 
 __global__ void init_ctrl(Ctrl* c) {
@@ -383,6 +716,34 @@ __global__ void init_ctrl(Ctrl* c) {
   c->done = 0;
   c->iters = 0;
   c->diverged = -1;
+  c->bar_count = 0;
+  c->bar_gen = 0;
+}
+
+template <int SP, int RP, bool RES>
+int launch(Params& p, int grid, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    CNMF_CUDA(cudaFuncSetAttribute(admm_persistent<SP, RP, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kSmemCap));
+    attr = true;
+  }
+  int per_sm = 0;
+  CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, admm_persistent<SP, RP, RES>, kThreads, smem));
+  if (per_sm < 1) return fail(CNMF_ERR_CUDA, "ADMM kernel does not fit on an SM");
+  void* args[] = {(void*)&p};
+  CNMF_CUDA(cudaLaunchCooperativeKernel((void*)admm_persistent<SP, RP, RES>, dim3(grid), dim3(kThreads), args, smem,
+                                        st));
+  CNMF_LAUNCH_CHECK();
+  return CNMF_OK;
+}
+
+template <int SP, int RP>
+int dispatch_res(Params& p, int grid, cudaStream_t st) {
+  const int64_t rows = std::max(p.rows_left, p.rows_right);
+  const size_t res_bytes = Smem<SP, RP>::bytes((int)std::min<int64_t>(rows, 1 << 20));
+  if (res_bytes <= kSmemCap) return launch<SP, RP, true>(p, grid, res_bytes, st);
+  return launch<SP, RP, false>(p, grid, Smem<SP, RP>::bytes(kTile), st);
 }
 
 }  // namespace
@@ -392,90 +753,103 @@ size_t admm_workspace(int64_t m, int64_t n, int s, int r) {
   (void)n;
   (void)s;
   (void)r;
-  return sizeof(Ctrl) + 256 + sizeof(Acc) + 256;
+  return 256 + 3 * sizeof(Acc) + 256;
 }
 
 int admm_run(const double* core, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
              double* du, double* vt, double* dvt, double* xc, double* yc, double pu, double pv, double step,
              int max_iter, double tol, double* trace, double* scores, int* iterations, void* ws, size_t ws_bytes,
              int resume, int step_limit, cudaStream_t st) {
-  if (s < 1 || s > kAdmmMax || r < 1 || r > kAdmmMax)
-    return fail(CNMF_ERR_ARGUMENT, "ADMM supports 1 <= r, s <= 64");
+  if (s < 1 || s > kMax || r < 1 || r > kMax) return fail(CNMF_ERR_ARGUMENT, "ADMM supports 1 <= r, s <= 64");
   if (!(pu > 0) || !(pv > 0)) return fail(CNMF_ERR_ARGUMENT, "penalties must be positive");
   if (ws_bytes < admm_workspace(m, n, s, r)) return fail(CNMF_ERR_ARGUMENT, "workspace too small");
-  int S = s <= 32 ? 32 : 64;
+  const int S = s <= 32 ? 32 : 64;
   Ctrl* ctrl = (Ctrl*)ws;
   Acc* acc = (Acc*)((char*)ws + 256);
-  const size_t core_smem = (size_t)(2 * s * s + 2 * s * r + r * r) * 8;
-  const size_t split_smem = (size_t)(kAdmmMax * kAdmmMax + 3 * kTile * kAdmmMax) * 8;
-  static bool attr = false;
-  if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(admm_core, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CNMF_CUDA(cudaFuncSetAttribute(admm_split, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)split_smem));
-    attr = true;
-  }
-  const int64_t tl = ceil_div(m, kTile), tr = ceil_div(n, kTile);
-  int nbl = (int)std::max<int64_t>(1, std::min<int64_t>(tl, std::max<int64_t>(1, kNumSMs * tl / (tl + tr))));
-  int nbr = (int)std::max<int64_t>(1, std::min<int64_t>(tr, kNumSMs - std::min(nbl, kNumSMs - 1)));
-  SideArgs left{L, m, S, u, du, pu, acc->LtU, acc->LtDU, acc->scal, 0};
-  SideArgs right{Rt, n, S, vt, dvt, pv, acc->RtV, acc->RtDV, acc->scal + 2, 1};
+  int dev = 0, sms = 0;
+  CNMF_CUDA(cudaGetDevice(&dev));
+  CNMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // one CTA per SM; split the CTAs between the two sides by row count
+  const int64_t want = std::max<int64_t>(2, std::min<int64_t>((int64_t)sms, ceil_div(m, 8) + ceil_div(n, 8)));
+  int nbl = (int)std::max<int64_t>(1, std::min<int64_t>(want - 1, (want * m + (m + n) / 2) / (m + n)));
+  const int nbr = (int)std::max<int64_t>(1, want - nbl);
+  const int grid = nbl + nbr;
   if (!resume) {
     init_ctrl<<<1, 1, 0, st>>>(ctrl);
     CNMF_LAUNCH_CHECK();
-    CNMF_CUDA(cudaMemsetAsync(acc, 0, sizeof(Acc), st));
+    CNMF_CUDA(cudaMemsetAsync(acc, 0, 3 * sizeof(Acc), st));
     CNMF_CUDA(cudaMemsetAsync(du, 0, (size_t)m * r * 8, st));
     CNMF_CUDA(cudaMemsetAsync(dvt, 0, (size_t)n * r * 8, st));
-    CNMF_CUDA(cudaMemsetAsync(xc, 0, (size_t)s * r * 8, st));
-    CNMF_CUDA(cudaMemsetAsync(yc, 0, (size_t)s * r * 8, st));
-    // initial projections L^T U0 and R V0^T
-    admm_split<<<nbl + nbr, kSplitThreads, split_smem, st>>>(left, right, xc, yc, s, r, step, 0, nbl, ctrl);
-    CNMF_LAUNCH_CHECK();
   }
-  auto one_iter = [&]() -> int {
-    admm_core<<<1, 512, core_smem, st>>>(core, s, r, pu, pv, max_iter, tol, ctrl, acc, xc, yc, trace, scores);
-    CNMF_LAUNCH_CHECK();
-    admm_split<<<nbl + nbr, kSplitThreads, split_smem, st>>>(left, right, xc, yc, s, r, step, 1, nbl, ctrl);
-    CNMF_LAUNCH_CHECK();
-    return CNMF_OK;
-  };
+  Params p;
+  p.core = core;
+  p.left = Side{L, m, S, u, du, pu};
+  p.right = Side{Rt, n, S, vt, dvt, pv};
+  p.s = s;
+  p.r = r;
+  p.pu = pu;
+  p.pv = pv;
+  p.step = step;
+  p.tol = tol;
+  p.max_iter = max_iter;
+  p.step_limit = step_limit;
+  p.fresh = !resume;
+  p.nblk_left = nbl;
+  p.rows_left = ceil_div(m, nbl);
+  p.rows_right = ceil_div(n, nbr);
+  p.xc_g = xc;
+  p.yc_g = yc;
+  p.trace = trace;
+  p.scores = scores;
+  p.ctrl = ctrl;
+  p.acc = acc;
+  p.prof = nullptr;
+  if (const char* e = getenv("CNMF_ADMM_PROFILE")) {
+    static unsigned long long* buf = nullptr;
+    if (!buf) cudaMalloc(&buf, 256 * 8 * 8);
+    p.prof = buf;
+    (void)e;
+  }
+  int rc;
+  if (s <= 32 && r <= 16)
+    rc = dispatch_res<32, 16>(p, grid, st);
+  else if (s <= 32 && r <= 32)
+    rc = dispatch_res<32, 32>(p, grid, st);
+  else if (r <= 16)
+    rc = dispatch_res<64, 16>(p, grid, st);
+  else if (r <= 32)
+    rc = dispatch_res<64, 32>(p, grid, st);
+  else
+    rc = dispatch_res<64, 64>(p, grid, st);
+  CNMF_TRY(rc);
+  if (p.prof) {
+    unsigned long long h[256 * 8];
+    cudaMemcpyAsync(h, p.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double acc8[8] = {0};
+    int n = 0;
+    for (int k = 5; k < 105 && k + 1 < 256; ++k) {
+      const unsigned long long* t = h + k * 8;
+      const unsigned long long next0 = h[(k + 1) * 8];
+      if (!next0 || !t[3]) break;
+      acc8[0] += t[4] - t[0];  // lx + update
+      acc8[1] += t[5] - t[4];  // accumulate
+      acc8[2] += t[1] - t[5];  // fold + atomics
+      acc8[3] += t[2] - t[1];  // barrier
+      acc8[4] += t[3] - t[2];  // score
+      acc8[5] += t[6] - t[3];  // core up to first inverse done
+      acc8[6] += t[7] - t[6];  // to second inverse done
+      acc8[7] += next0 - t[7];  // rest
+      ++n;
+    }
+    if (n)
+      fprintf(stderr,
+              "[admm profile] ns/iter: lx %.0f acc %.0f fold %.0f | barrier %.0f | score %.0f | core: inv1 %.0f "
+              "inv2 %.0f tail %.0f\n",
+              acc8[0] / n, acc8[1] / n, acc8[2] / n, acc8[3] / n, acc8[4] / n, acc8[5] / n, acc8[6] / n,
+              acc8[7] / n);
+  }
   Ctrl hc;
-  if (step_limit > 0) {
-    for (int i = 0; i < step_limit; ++i) CNMF_TRY(one_iter());
-  } else {
-    // capture a batch of iterations once, replay until the device says done
-    const int batch = 25;
-    cudaGraph_t graph;
-    cudaGraphExec_t exec;
-    cudaStream_t cap;
-    CNMF_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-    CNMF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
-    cudaStream_t saved = st;
-    st = cap;
-    const int64_t before = launch_count();
-    for (int i = 0; i < batch; ++i) {
-      int rc = one_iter();
-      if (rc != CNMF_OK) {
-        cudaStreamEndCapture(cap, &graph);
-        return rc;
-      }
-    }
-    st = saved;
-    count_launches(before - launch_count());  // captured, not launched
-    CNMF_CUDA(cudaStreamEndCapture(cap, &graph));
-    CNMF_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-    for (int done = 0; !done;) {
-      for (int b = 0; b < 4; ++b) {
-        CNMF_CUDA(cudaGraphLaunch(exec, st));
-        count_launches(2 * batch);
-      }
-      CNMF_CUDA(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
-      CNMF_CUDA(cudaStreamSynchronize(st));
-      done = hc.done;
-    }
-    CNMF_CUDA(cudaGraphExecDestroy(exec));
-    CNMF_CUDA(cudaGraphDestroy(graph));
-    CNMF_CUDA(cudaStreamDestroy(cap));
-  }
   CNMF_CUDA(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
   CNMF_CUDA(cudaStreamSynchronize(st));
   if (iterations) *iterations = hc.done ? hc.iters : -hc.k - 1;  // negative: still running

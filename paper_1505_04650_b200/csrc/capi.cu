@@ -12,7 +12,8 @@ int pass_transpose(const float*, int64_t, int64_t, int64_t, const float*, int, f
 int panel_cross(const float*, const float*, int64_t, int, double*, cudaStream_t);
 size_t compress_workspace(int64_t, int64_t, int);
 int structured_compress(const float*, int64_t, int64_t, int64_t, int, int, uint64_t, int, float*, void*, size_t,
-                        cudaStream_t);
+                        cudaStream_t, bool);
+int compress_check(const void*, int64_t, int64_t, int, cudaStream_t);
 int orthonormalize(float*, int64_t, int, double*, void*, size_t, cudaStream_t);
 size_t spa_workspace(int64_t, int);
 int panel_to_f64(const float*, int64_t, int, double*, int64_t, cudaStream_t);
@@ -91,7 +92,18 @@ int cnmf_structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, 
                              int side, float* Q, void* ws, size_t ws_bytes, void* stream) {
   CNMF_TRY(check_a(A, m, n, lda));
   if (side != 0 && side != 1) return fail(CNMF_ERR_ARGUMENT, "side must be 0 (columns) or 1 (rows)");
-  return structured_compress(A, m, n, lda, s, w, seed, side, Q, ws, ws_bytes, STREAM(stream));
+  return structured_compress(A, m, n, lda, s, w, seed, side, Q, ws, ws_bytes, STREAM(stream), true);
+}
+
+int cnmf_structured_compress_async(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed,
+                                   int side, float* Q, void* ws, size_t ws_bytes, void* stream) {
+  CNMF_TRY(check_a(A, m, n, lda));
+  if (side != 0 && side != 1) return fail(CNMF_ERR_ARGUMENT, "side must be 0 (columns) or 1 (rows)");
+  return structured_compress(A, m, n, lda, s, w, seed, side, Q, ws, ws_bytes, STREAM(stream), false);
+}
+
+int cnmf_compress_check(const void* ws, int64_t m, int64_t n, int s, void* stream) {
+  return compress_check(ws, m, n, s, STREAM(stream));
 }
 
 int cnmf_orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, void* stream) {
@@ -119,6 +131,7 @@ int cnmf_right_factor(const double* W, int64_t n, int s, int64_t ld, const int64
                       double* Ht, int64_t* n_capped, void* stream) {
   if (k < 1 || k > 64) return fail(CNMF_ERR_ARGUMENT, "right factor supports 1 <= k <= 64");
   cudaStream_t st = STREAM(stream);
+  keep_pool();
   double* scratch = nullptr;
   CNMF_CUDA(cudaMallocAsync((void**)&scratch, ((size_t)k * k + (size_t)n * k) * 8, st));
   int rc = right_factor(W, n, s, ld, d_picks, k, tol, Ht, scratch, n_capped, st);

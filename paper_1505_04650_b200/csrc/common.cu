@@ -65,6 +65,24 @@ int pass_stats(double* total_ms, int64_t* launches, double* bytes) {
   return CNMF_OK;
 }
 
+// Keep freed stream-ordered allocations in the default pool instead of
+// returning them to the driver at every synchronisation (the default release
+// threshold of 0 makes every cudaMallocAsync remap physical memory).
+void keep_pool() {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 uint64_t fnv1a64(const char* s) {
   uint64_t h = 0xCBF29CE484222325ULL;
   for (const unsigned char* p = (const unsigned char*)s; *p; ++p) h = (h ^ *p) * 0x100000001B3ULL;

@@ -92,6 +92,8 @@ __device__ __forceinline__ double raw_to_unit(uint64_t r) {
   return (double)(r >> 11) * (1.0 / 9007199254740992.0);
 }
 
+void keep_pool();
+
 // host-side seed derivation (rng.py:23-35, 56-58, 73-75)
 uint64_t fnv1a64(const char* s);
 uint64_t splitmix64(uint64_t x);

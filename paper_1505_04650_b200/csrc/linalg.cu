@@ -24,110 +24,113 @@ int panel_ld(int s);
 int pass_forward(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
 int pass_transpose(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
 int panel_finalize(float*, int64_t, int, const double*, double*, cudaStream_t);
-int gaussian_fill(uint64_t, int64_t, int64_t, int64_t, int, void*, int64_t, cudaStream_t);
+int gaussian_fill_ws(uint64_t, int64_t, int64_t, int64_t, int, void*, int64_t, void*, size_t, cudaStream_t);
+size_t gaussian_workspace(int64_t, int64_t, int64_t);
 
 namespace {
 
 // G (upper triangle valid, S x S) = R^T R; T = R^{-1} written S x S (zero
-// outside the leading s x s block). info[0] |= 1 when a shift was needed,
-// info[1] = min(pass id) whose Gram matrix was not finite. One block.
-__global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict__ G, int s, int S,
+// outside the leading s x s block). Symmetric Gaussian elimination of G held
+// in place, LU-style: after step k the upper triangle holds D L^T and the
+// strict lower triangle the accumulated row operations E = L^{-1}; scaling
+// row k by d_k^{-1/2} at the end yields R (upper) and R^{-T} (lower) at once,
+// so the factor and its inverse cost s parallel rank-1 steps (two barriers
+// each) instead of two serial triangular sweeps.
+// info[0] |= 1 when a shift was needed, info[1] = min(pass id) whose Gram
+// matrix was not finite or not factorable. One block.
+// the Gram buffer is consumed here and handed back zeroed for the next sweep
+__device__ __forceinline__ void G_rw_zero(const double* G, int idx) { const_cast<double*>(G)[idx] = 0.0; }
+
+__global__ void __launch_bounds__(512) chol_inv_kernel(const double* G, int s, int S,
                                                        double* __restrict__ T, double* __restrict__ Rout,
                                                        int* __restrict__ info, int pass_id) {
-  extern __shared__ double a[];  // s x s
+  extern __shared__ double a[];  // s x s (+ f[s], rowk[s])
+  double* f = a + s * s;
+  double* rowk = f + s;
   __shared__ double s_maxd;
   __shared__ int s_fail, s_nonfinite;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
   if (tid == 0) {
     s_maxd = 0.0;
     s_fail = 0;
     s_nonfinite = 0;
   }
   __syncthreads();
-  for (int idx = tid; idx < s * s; idx += blockDim.x) {
-    const int i = idx / s, j = idx % s;
+  for (int idx = tid; idx < s * s; idx += nt) {
+    const int i = idx / s, j = idx - i * s;
     const double v = (i <= j) ? G[i * S + j] : G[j * S + i];
-    a[idx] = v;
     if (!isfinite(v)) s_nonfinite = 1;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double md = 0.0;
-    for (int i = 0; i < s; ++i) md = fmax(md, a[i * s + i]);
-    s_maxd = md;
+    if (i == j) atomicMax((unsigned long long*)&s_maxd, __double_as_longlong(fmax(v, 0.0)));
   }
   __syncthreads();
   if (s_nonfinite || !(s_maxd > 0.0)) {
     if (tid == 0) atomicMin(&info[1], pass_id);
-    for (int idx = tid; idx < S * S; idx += blockDim.x) T[idx] = 0.0;
+    __syncthreads();
+    for (int idx = tid; idx < S * S; idx += nt) {
+      T[idx] = 0.0;
+      G_rw_zero(G, idx);
+    }
     return;
   }
+  const double thr = 1e-15 * s_maxd;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    if (attempt == 1) {
-      __syncthreads();  // every thread has observed s_fail before it is reset
-      // shifted CholeskyQR: restore G and add a relative shift
-      for (int idx = tid; idx < s * s; idx += blockDim.x) {
-        const int i = idx / s, j = idx % s;
-        double v = (i <= j) ? G[i * S + j] : G[j * S + i];
-        if (i == j) v += 1e-12 * s_maxd;
-        a[idx] = v;
-      }
-      if (tid == 0) {
-        s_fail = 0;
-        info[0] |= 1;
-      }
-      __syncthreads();
+    const double shift = attempt ? 1e-12 * s_maxd : 0.0;
+    for (int idx = tid; idx < s * s; idx += nt) {
+      const int i = idx / s, j = idx - i * s;
+      a[idx] = ((i <= j) ? G[i * S + j] : G[j * S + i]) + (i == j ? shift : 0.0);
     }
-    const double thr = 1e-15 * s_maxd;
+    if (tid == 0 && attempt) info[0] |= 1;
+    __syncthreads();
     for (int k = 0; k < s; ++k) {
-      if (tid == 0) {
-        const double d = a[k * s + k];
-        if (!(d > thr)) s_fail = 1;
-        a[k * s + k] = sqrt(fmax(d, thr));
+      const double d = a[k * s + k];
+      if (!(d > thr)) break;  // uniform: every thread reads the same value
+      for (int i = tid; i < s; i += nt) {
+        rowk[i] = a[k * s + i];
+        f[i] = (i > k) ? a[i * s + k] / d : 0.0;
       }
       __syncthreads();
-      if (s_fail) break;
-      const double rkk = a[k * s + k];
-      for (int j = k + 1 + tid; j < s; j += blockDim.x) a[k * s + j] /= rkk;
-      __syncthreads();
-      const int t = s - k - 1;
-      for (int idx = tid; idx < t * t; idx += blockDim.x) {
-        const int i = k + 1 + idx / t, j = k + 1 + idx % t;
-        if (j >= i) a[i * s + j] -= a[k * s + i] * a[k * s + j];
+      const int rows = s - k - 1;
+      for (int idx = tid; idx < rows * s; idx += nt) {
+        const int i = k + 1 + idx / s, j = idx % s;
+        a[i * s + j] = (j == k) ? -f[i] : a[i * s + j] - f[i] * rowk[j];
       }
       __syncthreads();
     }
-    if (!s_fail) break;
+    // a pivot below the threshold aborted the sweep (checked uniformly)
+    bool ok = true;
+    for (int k = 0; k < s; ++k)
+      if (!(a[k * s + k] > thr)) ok = false;
+    if (ok) {
+      s_fail = 0;
+      break;
+    }
+    s_fail = 1;
+    __syncthreads();
   }
   if (s_fail) {
     if (tid == 0) atomicMin(&info[1], pass_id);
-    for (int idx = tid; idx < S * S; idx += blockDim.x) T[idx] = 0.0;
+    for (int idx = tid; idx < S * S; idx += nt) {
+      T[idx] = 0.0;
+      G_rw_zero(G, idx);
+    }
     return;
   }
-  if (Rout != nullptr)
-    for (int idx = tid; idx < S * S; idx += blockDim.x) {
-      const int i = idx / S, j = idx % S;
-      Rout[idx] = (i < s && j < s && i <= j) ? a[i * s + j] : 0.0;
-    }
   __syncthreads();
-  // in-place inverse of the upper-triangular factor (column sweep)
-  __shared__ double col[128];
-  for (int j = 0; j < s; ++j) {
-    const double ajj = 1.0 / a[j * s + j];
-    // col[i] = -(T[:j,:j] R[:j,j])_i / R[j,j]   (T already stored in a[:j,:j])
-    for (int i = tid; i < j; i += blockDim.x) {
-      double acc = 0.0;
-      for (int k = i; k < j; ++k) acc += a[i * s + k] * a[k * s + j];
-      col[i] = -acc * ajj;
+  for (int idx = tid; idx < S * S; idx += nt) G_rw_zero(G, idx);
+  for (int idx = tid; idx < S * S; idx += nt) {
+    const int i = idx / S, j = idx - i * S;
+    double t = 0.0, r = 0.0;
+    if (i < s && j < s) {
+      // T[i][j] = R^{-T}[j][i]: row j of E scaled by d_j^{-1/2}
+      if (i <= j) {
+        const double dj = sqrt(a[j * s + j]);
+        t = (i == j) ? 1.0 / dj : a[j * s + i] / dj;
+        const double di = sqrt(a[i * s + i]);
+        r = (i == j) ? di : a[i * s + j] / di;
+      }
     }
-    __syncthreads();
-    for (int i = tid; i < j; i += blockDim.x) a[i * s + j] = col[i];
-    if (tid == 0) a[j * s + j] = ajj;
-    __syncthreads();
-  }
-  for (int idx = tid; idx < S * S; idx += blockDim.x) {
-    const int i = idx / S, j = idx % S;
-    T[idx] = (i < s && j < s && i <= j) ? a[i * s + j] : 0.0;
+    T[idx] = t;
+    if (Rout != nullptr) Rout[idx] = r;
   }
 }
 
@@ -139,21 +142,24 @@ __global__ void init_info(int* info) {
 }  // namespace
 
 int chol_inv(const double* G, int s, int S, double* T, double* R, int* info, int pass_id, cudaStream_t st) {
-  const size_t smem = (size_t)s * s * 8;
+  const size_t smem = ((size_t)s * s + 2 * (size_t)s) * 8;
   static bool attr = false;
   if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 128 * 8));
+    CNMF_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (128 * 128 + 256) * 8));
     attr = true;
   }
-  chol_inv_kernel<<<1, 256, smem, st>>>(G, s, S, T, R, info, pass_id);
+  chol_inv_kernel<<<1, 512, smem, st>>>(G, s, S, T, R, info, pass_id);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }
 
+static size_t small_bytes(int S) { return 2 * (size_t)S * S * 8 + 256; }
+
 size_t compress_workspace(int64_t m, int64_t n, int s) {
   const int S = panel_ld(s);
   if (S < 0) return 0;
-  return (size_t)std::max(m, n) * S * 4 + 2 * (size_t)S * S * 8 + 256;
+  return (size_t)std::max(m, n) * S * 4 + small_bytes(S) + gaussian_workspace(std::max(m, n), s, 4096) + 256;
 }
 
 struct Scratch {
@@ -192,8 +198,17 @@ static int check_info(const int* d_info, const char* what, cudaStream_t st) {
   return CNMF_OK;
 }
 
+// status of an asynchronous compression: reads the device info word it left
+// in its workspace (synchronises the stream)
+int compress_check(const void* ws, int64_t m, int64_t n, int s, cudaStream_t st) {
+  const int S = panel_ld(s);
+  if (S < 0) return fail(CNMF_ERR_ARGUMENT, "basis width must be <= 128");
+  Scratch sc = carve_small((char*)ws + (size_t)std::max(m, n) * S * 4, S);
+  return check_info(sc.info, "range finder", st);
+}
+
 int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed, int side,
-                        float* Q, void* ws, size_t ws_bytes, cudaStream_t st) {
+                        float* Q, void* ws, size_t ws_bytes, cudaStream_t st, bool check) {
   const int S = panel_ld(s);
   if (S < 0) return fail(CNMF_ERR_ARGUMENT, "basis width must be <= 128");
   if (s < 1 || w < 0) return fail(CNMF_ERR_ARGUMENT, "bad width or power exponent");
@@ -205,15 +220,18 @@ int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s
   float* Pm = side == 0 ? Q : (float*)ws;
   float* Pn = side == 0 ? (float*)ws : Q;
   Scratch sc = carve_small((char*)ws + (size_t)std::max(m, n) * S * 4, S);
+  char* rng_ws = (char*)ws + (size_t)std::max(m, n) * S * 4 + small_bytes(S);
+  const size_t rng_bytes = ws_bytes - ((size_t)std::max(m, n) * S * 4 + small_bytes(S));
   init_info<<<1, 1, 0, st>>>(sc.info);
   CNMF_LAUNCH_CHECK();
+  CNMF_CUDA(cudaMemsetAsync(sc.G, 0, (size_t)S * S * 8, st));
   // Omega: the reference's seeded test matrix (compress.py:125-127), rows =
   // A.cols for the column basis, A.rows for the row basis.
   const uint64_t oseed = child_seed(seed, "omega");
   float* omega = side == 0 ? Pn : Pm;
   const int64_t orows = side == 0 ? n : m;
   CNMF_CUDA(cudaMemsetAsync(omega, 0, (size_t)orows * S * 4, st));
-  CNMF_TRY(gaussian_fill(oseed, orows, s, 4096, CNMF_F32, omega, S, st));
+  CNMF_TRY(gaussian_fill_ws(oseed, orows, s, 4096, CNMF_F32, omega, S, rng_ws, rng_bytes, st));
 
   int pass_id = 0;
   // Every pass output P is orthonormalised explicitly with one CholeskyQR
@@ -254,6 +272,7 @@ int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s
     CNMF_TRY(orth_sweep());
   }
   CNMF_TRY(finish_basis(cur, cur_rows, s, S, sc, nullptr, pass_id, st));
+  if (!check) return CNMF_OK;
   return check_info(sc.info, side == 0 ? "column basis" : "row basis", st);
 }
 
@@ -264,6 +283,7 @@ int orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws
   Scratch sc = carve_small(ws, S);
   init_info<<<1, 1, 0, st>>>(sc.info);
   CNMF_LAUNCH_CHECK();
+  CNMF_CUDA(cudaMemsetAsync(sc.G, 0, (size_t)S * S * 8, st));
   CNMF_TRY(panel_finalize(P, rows, S, nullptr, sc.G, st));
   CNMF_TRY(chol_inv(sc.G, s, S, sc.T, nullptr, sc.info, 0, st));
   CNMF_TRY(panel_finalize(P, rows, S, sc.T, sc.G, st));

@@ -327,6 +327,7 @@ int nnls_gram(const double* gram, const double* target, int64_t k, int q, double
     attr = true;
   }
   unsigned long long* d_cap = nullptr;
+  keep_pool();
   CNMF_CUDA(cudaMallocAsync((void**)&d_cap, 8, st));
   CNMF_CUDA(cudaMemsetAsync(d_cap, 0, 8, st));
   const int64_t blocks = std::min<int64_t>(ceil_div(k, wpb), 16 * kNumSMs);

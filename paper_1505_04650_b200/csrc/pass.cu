@@ -51,11 +51,17 @@ __device__ __forceinline__ float f4c(const float4& v, int i) {
   return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
 
-// Y[m x S] (+)= A[m x n] X[n x S]; grid = (ceil(m/BM), nsplit).
+// Y[m x S] = A[m x n] X[n x S]. Work unit = one BM x 32 tile of A (row block
+// rb, k-tile kt), flattened rb-major. Each CTA (one per SM) streams a
+// contiguous range of units — whole row blocks when there are many, else an
+// even split of all units — and flushes its register accumulator whenever
+// the row block changes: a plain store when it owned the whole row block,
+// a red.global.add.v4 into the zeroed output otherwise. Balanced to within
+// one 64 KB tile per SM.
 template <int S>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_ffma(const __grid_constant__ TmaDesc tA, const __grid_constant__ TmaDesc tX, float* __restrict__ Y,
-             int64_t m, int kt_per_split, int nkt, int direct) {
+             int64_t m, int nkt, int64_t mb, int whole_blocks) {
   using C = FwdCfg<S>;
   constexpr int BM = C::BM, BK = 32, ST = C::ST;
   constexpr int ABYTES = BM * BK * 4, XBYTES = BK * S * 4;
@@ -67,10 +73,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp / C::WC, wc = warp % C::WC;
-  const int64_t row0 = (int64_t)blockIdx.x * BM;
-  const int kt0 = blockIdx.y * kt_per_split;
-  const int kt1 = min(nkt, kt0 + kt_per_split);
-  const int ntiles = kt1 - kt0;
+  const int64_t U = mb * nkt, G = gridDim.x, b = blockIdx.x;
+  const int64_t u0 = whole_blocks ? (b * mb / G) * nkt : b * U / G;
+  const int64_t u1 = whole_blocks ? ((b + 1) * mb / G) * nkt : (b + 1) * U / G;
+  const int64_t ntiles = u1 - u0;
   if (ntiles <= 0) return;
 
   if (tid == 0) {
@@ -80,15 +86,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   __syncthreads();
-  auto issue = [&](int stage, int kt) {
+  auto issue = [&](int stage, int64_t u) {
+    const int64_t rb = u / nkt;
+    const int kt = (int)(u - rb * nkt);
     mbar_arrive_expect_tx(&bars[stage], ABYTES + XBYTES);
 #pragma unroll
     for (int h = 0; h < (BM + 255) / 256; ++h)
-      tma_load_2d(sA + stage * ABYTES + h * 256 * 128, &tA, &bars[stage], kt * BK, (int)(row0 + h * 256));
+      tma_load_2d(sA + stage * ABYTES + h * 256 * 128, &tA, &bars[stage], kt * BK, (int)(rb * BM + h * 256));
     tma_load_2d(sX + stage * (BK * S), &tX, &bars[stage], 0, kt * BK);
   };
   if (tid == 0)
-    for (int s = 0; s < ST && s < ntiles; ++s) issue(s, kt0 + s);
+    for (int s = 0; s < ST && s < ntiles; ++s) issue(s, u0 + s);
 
   float acc[C::TM][C::TS];
 #pragma unroll
@@ -96,9 +104,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int j = 0; j < C::TS; ++j) acc[i][j] = 0.f;
 
-  for (int it = 0; it < ntiles; ++it) {
-    const int stage = it % ST;
-    mbar_wait(&bars[stage], (it / ST) & 1);
+  for (int64_t it = 0; it < ntiles; ++it) {
+    const int stage = (int)(it % ST);
+    const int64_t u = u0 + it;
+    mbar_wait(&bars[stage], (uint32_t)((it / ST) & 1));
     const unsigned char* As = sA + stage * ABYTES;
     const float* Xs = sX + stage * (BK * S) + wc * C::TS;
 #pragma unroll 2
@@ -127,21 +136,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncthreads();
-    if (tid == 0 && it + ST < ntiles) issue(stage, kt0 + it + ST);
-  }
-
+    if (tid == 0 && it + ST < ntiles) issue(stage, u + ST);
+    const int64_t rb = u / nkt;
+    if (it == ntiles - 1 || (u + 1) / nkt != rb) {
+      // flush this row block
+      const bool owned = (rb * nkt >= u0) && ((rb + 1) * nkt <= u1);
 #pragma unroll
-  for (int i = 0; i < C::TM; ++i) {
-    const int64_t row = row0 + wr * 32 * C::TM + lane + 32 * i;
-    if (row < m) {
-      float* yr = Y + row * S + wc * C::TS;
+      for (int i = 0; i < C::TM; ++i) {
+        const int64_t row = rb * BM + wr * 32 * C::TM + lane + 32 * i;
+        if (row < m) {
+          float* yr = Y + row * S + wc * C::TS;
 #pragma unroll
-      for (int j4 = 0; j4 < C::TS / 4; ++j4) {
-        if (direct)
-          *(float4*)(yr + 4 * j4) =
-              make_float4(acc[i][4 * j4], acc[i][4 * j4 + 1], acc[i][4 * j4 + 2], acc[i][4 * j4 + 3]);
-        else
-          red_add_v4(yr + 4 * j4, acc[i][4 * j4], acc[i][4 * j4 + 1], acc[i][4 * j4 + 2], acc[i][4 * j4 + 3]);
+          for (int j4 = 0; j4 < C::TS / 4; ++j4) {
+            if (owned)
+              *(float4*)(yr + 4 * j4) =
+                  make_float4(acc[i][4 * j4], acc[i][4 * j4 + 1], acc[i][4 * j4 + 2], acc[i][4 * j4 + 3]);
+            else
+              red_add_v4(yr + 4 * j4, acc[i][4 * j4], acc[i][4 * j4 + 1], acc[i][4 * j4 + 2],
+                         acc[i][4 * j4 + 3]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < C::TS; ++j) acc[i][j] = 0.f;
       }
     }
   }
@@ -168,11 +184,13 @@ constexpr size_t trn_smem() {
   return 1024 + (size_t)C::ST * (C::BN * C::BR * 4 + C::BR * S * 4) + 64;
 }
 
-// Z[n x S] (+)= A[m x n]^T W[m x S]; grid = (ceil(n/BN), rsplit).
+// Z[n x S] = A[m x n]^T W[m x S]. Work unit = one BR x BN tile (column block
+// cb, row tile rt), flattened cb-major; CTAs stream contiguous unit ranges
+// and flush per column block exactly like the forward pass.
 template <int S>
 __global__ void __launch_bounds__(kThreads, 1)
     trn_ffma(const __grid_constant__ TmaDesc tA, const __grid_constant__ TmaDesc tW, float* __restrict__ Z,
-             int64_t n, int rt_per_split, int nrt, int direct) {
+             int64_t n, int nrt, int64_t nb, int whole_blocks) {
   using C = TrnCfg<S>;
   constexpr int BN = C::BN, BR = C::BR, ST = C::ST;
   constexpr int ABYTES = BN * BR * 4, WBYTES = BR * S * 4;
@@ -185,10 +203,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wn = warp / C::WC, wc = warp % C::WC;
-  const int64_t col0 = (int64_t)blockIdx.x * BN;
-  const int rt0 = blockIdx.y * rt_per_split;
-  const int rt1 = min(nrt, rt0 + rt_per_split);
-  const int ntiles = rt1 - rt0;
+  const int64_t U = nb * nrt, G = gridDim.x, b = blockIdx.x;
+  const int64_t u0 = whole_blocks ? (b * nb / G) * nrt : b * U / G;
+  const int64_t u1 = whole_blocks ? ((b + 1) * nb / G) * nrt : (b + 1) * U / G;
+  const int64_t ntiles = u1 - u0;
   if (ntiles <= 0) return;
 
   if (tid == 0) {
@@ -198,15 +216,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   __syncthreads();
-  auto issue = [&](int stage, int rt) {
+  auto issue = [&](int stage, int64_t u) {
+    const int64_t cb = u / nrt;
+    const int rt = (int)(u - cb * nrt);
     mbar_arrive_expect_tx(&bars[stage], ABYTES + WBYTES);
 #pragma unroll
     for (int h = 0; h < NSUB; ++h)
-      tma_load_2d(sA + stage * (BN * BR) + h * (256 * BR), &tA, &bars[stage], (int)(col0 + h * 256), rt * BR);
+      tma_load_2d(sA + stage * (BN * BR) + h * (256 * BR), &tA, &bars[stage], (int)(cb * BN + h * 256), rt * BR);
     tma_load_2d(sW + stage * (BR * S), &tW, &bars[stage], 0, rt * BR);
   };
   if (tid == 0)
-    for (int s = 0; s < ST && s < ntiles; ++s) issue(s, rt0 + s);
+    for (int s = 0; s < ST && s < ntiles; ++s) issue(s, u0 + s);
 
   const int cl = wn * 128 + 4 * lane;  // first of this thread's 4 columns in the tile
   const int sub = cl / 256, cin = cl % 256;
@@ -216,9 +236,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int j = 0; j < C::TS; ++j) acc[i][j] = 0.f;
 
-  for (int it = 0; it < ntiles; ++it) {
-    const int stage = it % ST;
-    mbar_wait(&bars[stage], (it / ST) & 1);
+  for (int64_t it = 0; it < ntiles; ++it) {
+    const int stage = (int)(it % ST);
+    const int64_t u = u0 + it;
+    mbar_wait(&bars[stage], (uint32_t)((it / ST) & 1));
     const float* As = sA + stage * (BN * BR) + sub * (256 * BR) + cin;
     const float* Ws = sW + stage * (BR * S) + wc * C::TS;
 #pragma unroll 4
@@ -238,29 +259,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     __syncthreads();
-    if (tid == 0 && it + ST < ntiles) issue(stage, rt0 + it + ST);
-  }
-
+    if (tid == 0 && it + ST < ntiles) issue(stage, u + ST);
+    const int64_t cb = u / nrt;
+    if (it == ntiles - 1 || (u + 1) / nrt != cb) {
+      const bool owned = (cb * nrt >= u0) && ((cb + 1) * nrt <= u1);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t col = col0 + cl + i;
-    if (col < n) {
-      float* zr = Z + col * S + wc * C::TS;
+      for (int i = 0; i < 4; ++i) {
+        const int64_t col = cb * BN + cl + i;
+        if (col < n) {
+          float* zr = Z + col * S + wc * C::TS;
 #pragma unroll
-      for (int j4 = 0; j4 < C::TS / 4; ++j4) {
-        if (direct)
-          *(float4*)(zr + 4 * j4) =
-              make_float4(acc[i][4 * j4], acc[i][4 * j4 + 1], acc[i][4 * j4 + 2], acc[i][4 * j4 + 3]);
-        else
-          red_add_v4(zr + 4 * j4, acc[i][4 * j4], acc[i][4 * j4 + 1], acc[i][4 * j4 + 2], acc[i][4 * j4 + 3]);
+          for (int j4 = 0; j4 < C::TS / 4; ++j4) {
+            if (owned)
+              *(float4*)(zr + 4 * j4) =
+                  make_float4(acc[i][4 * j4], acc[i][4 * j4 + 1], acc[i][4 * j4 + 2], acc[i][4 * j4 + 3]);
+            else
+              red_add_v4(zr + 4 * j4, acc[i][4 * j4], acc[i][4 * j4 + 1], acc[i][4 * j4 + 2],
+                         acc[i][4 * j4 + 3]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < C::TS; ++j) acc[i][j] = 0.f;
       }
     }
   }
 }
 
 // P <- P T (T upper-triangular S x S, fp64 given, applied in fp32) and
-// G += P^T P in fp64 (upper triangle, atomics). One block per 64-row tile,
-// grid-strided. Either step can be disabled.
+// G += P^T P in fp64 (upper triangle, atomics). Grid-strided over 64-row
+// tiles; the Gram products are spread over 4x4 register blocks x row groups
+// so that every thread of the block accumulates. Either step can be disabled.
 template <int S>
 __global__ void __launch_bounds__(kThreads)
     finalize_panel(float* __restrict__ P, int64_t rows, const double* __restrict__ T, double* __restrict__ G) {
@@ -268,6 +296,7 @@ __global__ void __launch_bounds__(kThreads)
   constexpr int NB = S / 4;                  // 4-wide blocks per side
   constexpr int NBLK = NB * (NB + 1) / 2;    // upper-triangular 4x4 blocks
   constexpr int BPT = (NBLK + kThreads - 1) / kThreads;
+  constexpr int GROUPS = (NBLK >= kThreads) ? 1 : kThreads / NBLK;  // row groups
   extern __shared__ float fsm[];
   float* sT = fsm;              // S x S
   float* sIn = sT + S * S;      // TR x S
@@ -276,13 +305,15 @@ __global__ void __launch_bounds__(kThreads)
   if (T != nullptr)
     for (int i = tid; i < S * S; i += kThreads) sT[i] = (float)T[i];
 
+  const int grp = tid / (GROUPS > 1 ? NBLK : kThreads);
+  const int bidx = tid - grp * (GROUPS > 1 ? NBLK : kThreads);
   int bi[BPT], bj[BPT];
 #pragma unroll
   for (int q = 0; q < BPT; ++q) {
-    int b = tid + q * kThreads;
+    int b = bidx + q * kThreads;
     bi[q] = -1;
     bj[q] = -1;
-    if (b < NBLK) {
+    if (b < NBLK && grp < GROUPS) {
       int i = 0;
       while (b >= NB - i) {
         b -= NB - i;
@@ -326,7 +357,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
       for (int q = 0; q < BPT; ++q) {
         if (bi[q] < 0) continue;
-        for (int r = 0; r < nr; ++r) {
+        for (int r = grp; r < nr; r += GROUPS) {
           const float4 x = *(const float4*)(src + r * S + 4 * bi[q]);
           const float4 y = *(const float4*)(src + r * S + 4 * bj[q]);
           const double xs[4] = {x.x, x.y, x.z, x.w};
@@ -340,6 +371,20 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   if (G != nullptr) {
+    if (GROUPS > 1) {
+      // fold the row groups in shared memory: one atomic per entry per block
+      double* red = (double*)(sOut + TR * S);  // GROUPS x NBLK x 16
+      __syncthreads();
+      if (bi[0] >= 0)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) red[(grp * NBLK + bidx) * 16 + e] = g[0][e];
+      __syncthreads();
+      if (grp == 0 && bi[0] >= 0)
+        for (int q = 1; q < GROUPS; ++q)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) g[0][e] += red[(q * NBLK + bidx) * 16 + e];
+      if (grp != 0) return;
+    }
 #pragma unroll
     for (int q = 0; q < BPT; ++q) {
       if (bi[q] < 0) continue;
@@ -362,12 +407,10 @@ int launch_forward(const float* A, int64_t m, int64_t n, int64_t lda, const floa
   CNMF_TRY(make_tma_2d(&tX, X, 4, n, S, S, S, 32, false));
   const int nkt = (int)ceil_div(n, 32);
   const int64_t mb = ceil_div(m, C::BM);
-  int nsplit = 1;
-  if (mb < 2 * kNumSMs) nsplit = (int)std::min<int64_t>(ceil_div(2 * kNumSMs, mb), std::max(1, nkt / 8));
-  const int per = (int)ceil_div(nkt, nsplit);
-  nsplit = (int)ceil_div(nkt, per);
-  const int direct = nsplit == 1;
-  if (!direct) CNMF_CUDA(cudaMemsetAsync(Y, 0, (size_t)m * S * 4, st));
+  // whole row blocks per CTA when there are many (no atomics, no memset)
+  const int whole = mb >= 16 * kNumSMs;
+  const int64_t grid = std::min<int64_t>(kNumSMs, whole ? mb : mb * nkt);
+  if (!whole) CNMF_CUDA(cudaMemsetAsync(Y, 0, (size_t)m * S * 4, st));
   constexpr size_t smem = fwd_smem<S>();
   static bool attr = false;
   if (!attr) {
@@ -380,7 +423,7 @@ int launch_forward(const float* A, int64_t m, int64_t n, int64_t lda, const floa
     CNMF_CUDA(cudaEventCreate(&e1));
     CNMF_CUDA(cudaEventRecord(e0, st));
   }
-  fwd_ffma<S><<<dim3((unsigned)mb, (unsigned)nsplit), kThreads, smem, st>>>(tA, tX, Y, m, per, nkt, direct);
+  fwd_ffma<S><<<(unsigned)grid, kThreads, smem, st>>>(tA, tX, Y, m, nkt, mb, whole);
   CNMF_LAUNCH_CHECK();
   if (e0) {
     CNMF_CUDA(cudaEventRecord(e1, st));
@@ -397,12 +440,9 @@ int launch_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const fl
   CNMF_TRY(make_tma_2d(&tW, W, 4, m, S, S, S, C::BR, false));
   const int nrt = (int)ceil_div(m, C::BR);
   const int64_t nb = ceil_div(n, C::BN);
-  int rsplit = 1;
-  if (nb < 4 * kNumSMs) rsplit = (int)std::min<int64_t>(ceil_div(2 * kNumSMs, nb), std::max(1, nrt / 16));
-  const int per = (int)ceil_div(nrt, rsplit);
-  rsplit = (int)ceil_div(nrt, per);
-  const int direct = rsplit == 1;
-  if (!direct) CNMF_CUDA(cudaMemsetAsync(Z, 0, (size_t)n * S * 4, st));
+  const int whole = nb >= 16 * kNumSMs;
+  const int64_t grid = std::min<int64_t>(kNumSMs, whole ? nb : nb * nrt);
+  if (!whole) CNMF_CUDA(cudaMemsetAsync(Z, 0, (size_t)n * S * 4, st));
   constexpr size_t smem = trn_smem<S>();
   static bool attr = false;
   if (!attr) {
@@ -415,7 +455,7 @@ int launch_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const fl
     CNMF_CUDA(cudaEventCreate(&e1));
     CNMF_CUDA(cudaEventRecord(e0, st));
   }
-  trn_ffma<S><<<dim3((unsigned)nb, (unsigned)rsplit), kThreads, smem, st>>>(tA, tW, Z, n, per, nrt, direct);
+  trn_ffma<S><<<(unsigned)grid, kThreads, smem, st>>>(tA, tW, Z, n, nrt, nb, whole);
   CNMF_LAUNCH_CHECK();
   if (e0) {
     CNMF_CUDA(cudaEventRecord(e1, st));
@@ -426,15 +466,17 @@ int launch_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const fl
 
 template <int S>
 int launch_finalize(float* P, int64_t rows, const double* T, double* G, cudaStream_t st) {
-  constexpr size_t smem = (size_t)(S * S + 2 * 64 * S) * 4;
+  constexpr int NB = S / 4, NBLK = NB * (NB + 1) / 2;
+  constexpr int GROUPS = (NBLK >= kThreads) ? 1 : kThreads / NBLK;
+  constexpr size_t smem = (size_t)(S * S + 2 * 64 * S) * 4 + (GROUPS > 1 ? (size_t)GROUPS * NBLK * 16 * 8 : 0);
   static bool attr = false;
   if (!attr) {
     CNMF_CUDA(cudaFuncSetAttribute(finalize_panel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  if (G != nullptr) CNMF_CUDA(cudaMemsetAsync(G, 0, (size_t)S * S * 8, st));
+  // G must be zero on entry (the Cholesky kernel re-zeroes it after use)
   const int64_t tiles = ceil_div(rows, 64);
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * kNumSMs));
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tiles, 4), kNumSMs));
   finalize_panel<S><<<grid, kThreads, smem, st>>>(P, rows, T, G);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;

@@ -20,6 +20,7 @@
 // for exactness).
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -46,6 +47,60 @@ struct SegState {
   int64_t offset;        // output offset (after k2)
   uint32_t chain[4];     // chain-start bits for [seg_start, seg_start + 128)
 };
+
+// The streams of one fill: a single stream (gaussian_matrix) or fixed-size row
+// chunks, chunk c drawn from child_seed(seed, f"chunk{c}") (compress.py:115).
+// Every segment derives its stream from this by arithmetic — no host-built
+// descriptor tables are copied to the device.
+struct Layout {
+  uint64_t key;         // single-stream key, or the parent seed of the chunks
+  int64_t rows, cols;
+  int64_t chunk_rows;   // rows per chunk (== rows for a single stream)
+  int64_t nchunks;
+  int32_t chunked;
+  int32_t nseg_full, nseg_last;
+  int32_t seglen_full, seglen_last;
+  int64_t total_segs;
+};
+
+__device__ uint64_t dev_splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+// child_seed(seed, "chunk" + str(c)) (rng.py:23-35, 56-58)
+__device__ uint64_t dev_chunk_key(uint64_t seed, int64_t c) {
+  uint64_t h = 0xCBF29CE484222325ULL;
+  const char pre[5] = {'c', 'h', 'u', 'n', 'k'};
+  for (int i = 0; i < 5; ++i) h = (h ^ (uint64_t)(unsigned char)pre[i]) * 0x100000001B3ULL;
+  char dig[20];
+  int nd = 0;
+  do {
+    dig[nd++] = (char)('0' + (int)(c % 10));
+    c /= 10;
+  } while (c > 0);
+  while (nd > 0) h = (h ^ (uint64_t)(unsigned char)dig[--nd]) * 0x100000001B3ULL;
+  return dev_splitmix64(seed ^ h);
+}
+
+__device__ StreamDesc stream_of(const Layout& L, int64_t c) {
+  StreamDesc sd;
+  const bool last = c == L.nchunks - 1;
+  sd.key = L.chunked ? dev_chunk_key(L.key, c) : L.key;
+  sd.row0 = c * L.chunk_rows;
+  sd.count = (last ? L.rows - sd.row0 : L.chunk_rows) * L.cols;
+  sd.seg0 = c * L.nseg_full;
+  sd.nseg = last ? L.nseg_last : L.nseg_full;
+  sd.seglen = last ? L.seglen_last : L.seglen_full;
+  return sd;
+}
+
+__device__ __forceinline__ int64_t chunk_of_seg(const Layout& L, int64_t g) {
+  const int64_t c = g / L.nseg_full;
+  return c < L.nchunks - 1 ? c : L.nchunks - 1;
+}
 
 // ---- correctly rounded log(w), w in (0, 1], in double-double arithmetic ----
 struct DD {
@@ -263,11 +318,10 @@ __device__ int64_t walk(uint64_t key, int64_t head, int64_t stop, int64_t seg_st
   return k;
 }
 
-__global__ void k1_speculate(const StreamDesc* streams, int nstreams, const int32_t* seg_stream, SegState* segs,
-                             int64_t total_segs) {
+__global__ void k1_speculate(const Layout L, SegState* segs) {
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (g >= total_segs) return;
-  const StreamDesc sd = streams[seg_stream[g]];
+  if (g >= L.total_segs) return;
+  const StreamDesc sd = stream_of(L, chunk_of_seg(L, g));
   const int64_t w = g - sd.seg0;
   const int64_t s0 = w * sd.seglen, s1 = s0 + sd.seglen;
   uint32_t chain[4] = {0, 0, 0, 0};
@@ -282,8 +336,8 @@ __global__ void k1_speculate(const StreamDesc* streams, int nstreams, const int3
 }
 
 // One CTA per stream: re-anchor each segment at its true entry, scan counts.
-__global__ void k2_anchor_scan(const StreamDesc* streams, SegState* segs, int* flags) {
-  const StreamDesc sd = streams[blockIdx.x];
+__global__ void k2_anchor_scan(const Layout L, SegState* segs, int* flags) {
+  const StreamDesc sd = stream_of(L, blockIdx.x);
   __shared__ int64_t s_cnt[1024];
   __shared__ int s_bad;
   if (threadIdx.x == 0) s_bad = 0;
@@ -331,55 +385,95 @@ __global__ void k2_anchor_scan(const StreamDesc* streams, SegState* segs, int* f
     s_cnt[w] = cnt;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int w = 0; w < sd.nseg; ++w) {
+  // block-wide exclusive scan of the corrected counts (blockDim = 256, 4 each)
+  __shared__ int64_t s_part[256];
+  const int t = threadIdx.x;
+  int64_t loc = 0;
+  for (int q = 0; q < 4; ++q) {
+    const int w = 4 * t + q;
+    if (w < sd.nseg) loc += s_cnt[w];
+  }
+  s_part[t] = loc;
+  __syncthreads();
+  for (int off = 1; off < 256; off <<= 1) {
+    const int64_t v = (t >= off) ? s_part[t - off] : 0;
+    __syncthreads();
+    s_part[t] += v;
+    __syncthreads();
+  }
+  int64_t acc = s_part[t] - loc;
+  for (int q = 0; q < 4; ++q) {
+    const int w = 4 * t + q;
+    if (w < sd.nseg) {
       segs[sd.seg0 + w].offset = acc;
       acc += s_cnt[w];
     }
-    if (acc < sd.count) s_bad = 1;
-    flags[blockIdx.x] = s_bad;
   }
+  if (t == 255) {
+    if (s_part[255] < sd.count) s_bad = 1;
+  }
+  __syncthreads();
+  if (t == 0) flags[blockIdx.x] = s_bad;
 }
 
 template <typename T>
-__global__ void k3_emit(const StreamDesc* streams, const int32_t* seg_stream, const SegState* segs,
-                        int64_t total_segs, const int* flags, T* out, int64_t ld, int64_t cols, TailRec* tails,
+__global__ void k3_emit(const Layout L, const SegState* segs, const int* flags, T* out, int64_t ld, TailRec* tails,
                         unsigned int* ntails, unsigned int tail_cap) {
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  if (g >= total_segs) return;
-  const int sid = seg_stream[g];
-  if (flags[sid]) return;
-  const StreamDesc sd = streams[sid];
+  if (g >= L.total_segs) return;
+  const int64_t c = chunk_of_seg(L, g);
+  if (flags[c]) return;
+  const StreamDesc sd = stream_of(L, c);
   const int64_t w = g - sd.seg0;
   const SegState st = segs[g];
   if (st.offset >= sd.count) return;
   const int64_t s1 = (w + 1) * sd.seglen;
   int64_t ex;
-  walk<true, T>(sd.key, st.entry, s1, -1, nullptr, out, ld, cols, sd.row0, st.offset, sd.count, &ex, tails, ntails,
-                tail_cap);
+  walk<true, T>(sd.key, st.entry, s1, -1, nullptr, out, ld, L.cols, sd.row0, st.offset, sd.count, &ex, tails,
+                ntails, tail_cap);
 }
 
 // Fallback: one warp decodes a whole stream sequentially.
 template <typename T>
-__global__ void k_serial(const StreamDesc* streams, const int* flags, T* out, int64_t ld, int64_t cols,
-                         TailRec* tails, unsigned int* ntails, unsigned int tail_cap) {
-  const StreamDesc sd = streams[blockIdx.x];
+__global__ void k_serial(const Layout L, const int* flags, T* out, int64_t ld, TailRec* tails,
+                         unsigned int* ntails, unsigned int tail_cap) {
   if (!flags[blockIdx.x]) return;
-  // walk in windows until `count` variates are produced
+  const StreamDesc sd = stream_of(L, blockIdx.x);
   int64_t head = 0, k = 0;
   while (k < sd.count) {
     int64_t ex;
-    k += walk<true, T>(sd.key, head, head + 64 * kWin, -1, nullptr, out, ld, cols, sd.row0, k, sd.count, &ex, tails,
-                       ntails, tail_cap);
+    k += walk<true, T>(sd.key, head, head + 64 * kWin, -1, nullptr, out, ld, L.cols, sd.row0, k, sd.count, &ex,
+                       tails, ntails, tail_cap);
     head = ex;
   }
 }
 
+// Tail records to the host (mapped pinned slot): plain stores, one block.
+struct TailSlot {
+  TailRec* recs;      // host pointers
+  double* vals;
+  int64_t* offs;
+  unsigned int* count;
+  TailRec* d_recs;    // device views of the same pinned memory
+  double* d_vals;
+  int64_t* d_offs;
+  unsigned int* d_count;
+  unsigned int cap;
+};
+
+__global__ void export_tail(const TailRec* tails, const unsigned int* ntails, TailRec* dst, unsigned int* dst_count,
+                            unsigned int cap) {
+  const unsigned int n = min(*ntails, cap);
+  for (unsigned int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = tails[i];
+  if (threadIdx.x == 0) *dst_count = *ntails;
+}
+
 template <typename T>
-__global__ void scatter_tail(T* out, const int64_t* offsets, const double* vals, int count) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < count) out[offsets[i]] = (T)vals[i];
+__global__ void scatter_tail(T* out, const int64_t* offsets, const double* vals, const unsigned int* count,
+                             unsigned int cap) {
+  const unsigned int n = min(*count, cap);
+  for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[offsets[i]] = (T)vals[i];
 }
 
 template <typename T>
@@ -407,102 +501,130 @@ __global__ void uniform_kernel(uint64_t key, int64_t rows, int64_t cols, double 
 
 }  // namespace
 
-// Launch the three-phase decode for a list of streams sharing one output.
+// Host part of the tail fix-up: runs on a CUDA callback thread when the
+// stream reaches it (no host synchronisation in the caller).
+static void CUDART_CB tail_fixup(void* p) {
+  TailSlot* s = (TailSlot*)p;
+  const unsigned int n = std::min(*s->count, s->cap);
+  for (unsigned int i = 0; i < n; ++i) {
+    const TailRec& r = s->recs[i];
+    const double u1 = (double)(r.u1 >> 11) * (1.0 / 9007199254740992.0);
+    const double xx = -cnmf_zig::kTailInvR * std::log1p(-u1);
+    s->offs[i] = r.offset;
+    s->vals[i] = r.negative ? -(cnmf_zig::kTailR + xx) : cnmf_zig::kTailR + xx;
+  }
+}
+
+// ring of mapped pinned slots (reused round-robin; a slot is rewritten only
+// eight fills later, long after its stream work retired)
+static TailSlot* tail_slot(unsigned int cap) {
+  static std::mutex mu;
+  static TailSlot ring[8];
+  static unsigned int next = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  TailSlot& s = ring[next++ % 8];
+  if (s.cap < cap) {
+    if (s.recs) cudaFreeHost(s.recs);
+    const size_t bytes = (size_t)cap * (sizeof(TailRec) + 16) + 64;
+    char* h = nullptr;
+    if (cudaHostAlloc((void**)&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    char* d = nullptr;
+    if (cudaHostGetDevicePointer((void**)&d, h, 0) != cudaSuccess) return nullptr;
+    s.recs = (TailRec*)h;
+    s.vals = (double*)(h + (size_t)cap * sizeof(TailRec));
+    s.offs = (int64_t*)(h + (size_t)cap * (sizeof(TailRec) + 8));
+    s.count = (unsigned int*)(h + (size_t)cap * (sizeof(TailRec) + 16));
+    s.d_recs = (TailRec*)d;
+    s.d_vals = (double*)(d + (size_t)cap * sizeof(TailRec));
+    s.d_offs = (int64_t*)(d + (size_t)cap * (sizeof(TailRec) + 8));
+    s.d_count = (unsigned int*)(d + (size_t)cap * (sizeof(TailRec) + 16));
+    s.cap = cap;
+  }
+  return &s;
+}
+
+static Layout make_layout(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_rows) {
+  Layout L{};
+  L.rows = rows;
+  L.cols = cols;
+  L.chunked = chunk_rows > 0;
+  L.chunk_rows = L.chunked ? std::min(chunk_rows, rows) : rows;
+  L.nchunks = ceil_div(rows, L.chunk_rows);
+  L.key = seed;
+  auto seg = [](int64_t count, int32_t* seglen, int32_t* nseg) {
+    const int64_t need = (int64_t)(count * 1.02) + 4 * kWin;
+    int64_t len = 4 * kWin;
+    while (ceil_div(need, len) > 1024) len *= 2;
+    *seglen = (int32_t)len;
+    *nseg = (int32_t)ceil_div(need, len);
+  };
+  seg(L.chunk_rows * cols, &L.seglen_full, &L.nseg_full);
+  seg((rows - (L.nchunks - 1) * L.chunk_rows) * cols, &L.seglen_last, &L.nseg_last);
+  L.total_segs = (L.nchunks - 1) * (int64_t)L.nseg_full + L.nseg_last;
+  return L;
+}
+
+size_t gaussian_workspace(int64_t rows, int64_t cols, int64_t chunk_rows) {
+  const Layout L = make_layout(0, rows, cols, chunk_rows);
+  const int64_t variates = rows * cols;
+  const size_t cap = (size_t)std::min<int64_t>(variates / 256 + 1024, 1 << 26);
+  return (size_t)L.total_segs * sizeof(SegState) + (size_t)L.nchunks * 4 + 64 + cap * sizeof(TailRec) + 512;
+}
+
 template <typename T>
-static int gaussian_streams(std::vector<StreamDesc>& sd, T* out, int64_t ld, int64_t cols, cudaStream_t stream) {
-  int64_t total = 0;
-  std::vector<int32_t> seg_stream;
-  for (size_t i = 0; i < sd.size(); ++i) {
-    const int64_t need = (int64_t)(sd[i].count * 1.02) + 4 * kWin;
-    int64_t seglen = 16 * kWin;
-    while (ceil_div(need, seglen) > 1024) seglen *= 2;
-    sd[i].seglen = (int32_t)seglen;
-    sd[i].nseg = (int32_t)ceil_div(need, seglen);
-    sd[i].seg0 = total;
-    total += sd[i].nseg;
-    for (int w = 0; w < sd[i].nseg; ++w) seg_stream.push_back((int32_t)i);
-  }
-  const size_t bytes_sd = sd.size() * sizeof(StreamDesc);
-  const size_t bytes_map = seg_stream.size() * sizeof(int32_t);
-  const size_t bytes_seg = (size_t)total * sizeof(SegState);
-  const size_t bytes_flags = sd.size() * sizeof(int);
-  int64_t variates = 0;
-  for (auto& x : sd) variates += x.count;
-  const unsigned int tail_cap = (unsigned int)std::min<int64_t>(variates / 256 + 1024, 1 << 26);
-  const size_t bytes_tail = (size_t)tail_cap * sizeof(TailRec) + 64;
-  char* buf = nullptr;
-  CNMF_CUDA(cudaMallocAsync((void**)&buf, bytes_sd + bytes_map + bytes_seg + bytes_flags + bytes_tail + 256, stream));
-  StreamDesc* d_sd = (StreamDesc*)buf;
-  int32_t* d_map = (int32_t*)(buf + bytes_sd);
-  SegState* d_seg = (SegState*)(((uintptr_t)(buf + bytes_sd + bytes_map) + 15) & ~(uintptr_t)15);
-  int* d_flags = (int*)((char*)d_seg + bytes_seg);
-  unsigned int* d_ntail = (unsigned int*)(((uintptr_t)(d_flags + sd.size()) + 63) & ~(uintptr_t)63);
-  TailRec* d_tail = (TailRec*)(d_ntail + 16);
+static int gaussian_streams(const Layout& L, T* out, int64_t ld, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  const unsigned int cap = (unsigned int)std::min<int64_t>(L.rows * L.cols / 256 + 1024, 1 << 26);
+  if (ws_bytes < gaussian_workspace(L.rows, L.cols, L.chunked ? L.chunk_rows : 0))
+    return fail(CNMF_ERR_ARGUMENT, "gaussian_fill: workspace too small");
+  char* p = (char*)(((uintptr_t)ws + 15) & ~(uintptr_t)15);
+  SegState* d_seg = (SegState*)p;
+  p += (size_t)L.total_segs * sizeof(SegState);
+  int* d_flags = (int*)p;
+  p += ((size_t)L.nchunks * 4 + 63) & ~(size_t)63;
+  unsigned int* d_ntail = (unsigned int*)p;
+  TailRec* d_tail = (TailRec*)(p + 64);
+  TailSlot* slot = tail_slot(cap);
+  if (slot == nullptr) return fail(CNMF_ERR_CUDA, "pinned tail buffer allocation failed");
   CNMF_CUDA(cudaMemsetAsync(d_ntail, 0, 4, stream));
-  CNMF_CUDA(cudaMemcpyAsync(d_sd, sd.data(), bytes_sd, cudaMemcpyHostToDevice, stream));
-  CNMF_CUDA(cudaMemcpyAsync(d_map, seg_stream.data(), bytes_map, cudaMemcpyHostToDevice, stream));
   const int wpb = 4;  // warps per block
-  const unsigned grid = (unsigned)ceil_div(total, wpb);
-  k1_speculate<<<grid, 32 * wpb, 0, stream>>>(d_sd, (int)sd.size(), d_map, d_seg, total);
+  const unsigned grid = (unsigned)ceil_div(L.total_segs, wpb);
+  k1_speculate<<<grid, 32 * wpb, 0, stream>>>(L, d_seg);
   CNMF_LAUNCH_CHECK();
-  k2_anchor_scan<<<(unsigned)sd.size(), 256, 0, stream>>>(d_sd, d_seg, d_flags);
+  k2_anchor_scan<<<(unsigned)L.nchunks, 256, 0, stream>>>(L, d_seg, d_flags);
   CNMF_LAUNCH_CHECK();
-  k3_emit<T><<<grid, 32 * wpb, 0, stream>>>(d_sd, d_map, d_seg, total, d_flags, out, ld, cols, d_tail, d_ntail,
-                                            tail_cap);
+  k3_emit<T><<<grid, 32 * wpb, 0, stream>>>(L, d_seg, d_flags, out, ld, d_tail, d_ntail, cap);
   CNMF_LAUNCH_CHECK();
-  k_serial<T><<<(unsigned)sd.size(), 32, 0, stream>>>(d_sd, d_flags, out, ld, cols, d_tail, d_ntail, tail_cap);
+  k_serial<T><<<(unsigned)L.nchunks, 32, 0, stream>>>(L, d_flags, out, ld, d_tail, d_ntail, cap);
   CNMF_LAUNCH_CHECK();
-  // finish the tail variates with the C library's log1p (see TailRec)
-  unsigned int ntail = 0;
-  CNMF_CUDA(cudaMemcpyAsync(&ntail, d_ntail, 4, cudaMemcpyDeviceToHost, stream));
-  CNMF_CUDA(cudaStreamSynchronize(stream));
-  if (ntail > tail_cap) {
-    cudaFreeAsync(buf, stream);
-    return fail(CNMF_ERR_CUDA, "tail record buffer overflow");
-  }
-  if (ntail > 0) {
-    std::vector<TailRec> rec(ntail);
-    CNMF_CUDA(cudaMemcpyAsync(rec.data(), d_tail, ntail * sizeof(TailRec), cudaMemcpyDeviceToHost, stream));
-    CNMF_CUDA(cudaStreamSynchronize(stream));
-    std::vector<int64_t> off(ntail);
-    std::vector<double> val(ntail);
-    for (unsigned int i = 0; i < ntail; ++i) {
-      const double u1 = (double)(rec[i].u1 >> 11) * (1.0 / 9007199254740992.0);
-      const double xx = -cnmf_zig::kTailInvR * std::log1p(-u1);
-      off[i] = rec[i].offset;
-      val[i] = rec[i].negative ? -(cnmf_zig::kTailR + xx) : cnmf_zig::kTailR + xx;
-    }
-    int64_t* d_off = (int64_t*)d_tail;  // reuse the record buffer
-    double* d_val = (double*)(d_off + ntail);
-    CNMF_CUDA(cudaMemcpyAsync(d_off, off.data(), ntail * 8, cudaMemcpyHostToDevice, stream));
-    CNMF_CUDA(cudaMemcpyAsync(d_val, val.data(), ntail * 8, cudaMemcpyHostToDevice, stream));
-    scatter_tail<T><<<(ntail + 255) / 256, 256, 0, stream>>>(out, d_off, d_val, (int)ntail);
-    CNMF_LAUNCH_CHECK();
-    CNMF_CUDA(cudaStreamSynchronize(stream));
-  }
-  CNMF_CUDA(cudaFreeAsync(buf, stream));
+  // tail variates: finish with the C library's log1p on a callback thread
+  export_tail<<<1, 256, 0, stream>>>(d_tail, d_ntail, slot->d_recs, slot->d_count, cap);
+  CNMF_LAUNCH_CHECK();
+  CNMF_CUDA(cudaLaunchHostFunc(stream, tail_fixup, slot));
+  scatter_tail<T><<<8, 256, 0, stream>>>(out, slot->d_offs, slot->d_vals, slot->d_count, cap);
+  CNMF_LAUNCH_CHECK();
   return CNMF_OK;
+}
+
+int gaussian_fill_ws(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_rows, int dtype, void* out, int64_t ld,
+                     void* ws, size_t ws_bytes, cudaStream_t stream) {
+  if (rows < 1 || cols < 1) return fail(CNMF_ERR_ARGUMENT, "gaussian_fill needs positive dims");
+  if (ld < cols) return fail(CNMF_ERR_ARGUMENT, "gaussian_fill: ld < cols");
+  const Layout L = make_layout(seed, rows, cols, chunk_rows);
+  if (dtype == CNMF_F64) return gaussian_streams(L, (double*)out, ld, ws, ws_bytes, stream);
+  if (dtype == CNMF_F32) return gaussian_streams(L, (float*)out, ld, ws, ws_bytes, stream);
+  return fail(CNMF_ERR_ARGUMENT, "unknown dtype");
 }
 
 int gaussian_fill(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_rows, int dtype, void* out, int64_t ld,
                   cudaStream_t stream) {
   if (rows < 1 || cols < 1) return fail(CNMF_ERR_ARGUMENT, "gaussian_fill needs positive dims");
-  if (ld < cols) return fail(CNMF_ERR_ARGUMENT, "gaussian_fill: ld < cols");
-  std::vector<StreamDesc> sd;
-  if (chunk_rows <= 0) {
-    sd.push_back(StreamDesc{seed, rows * cols, 0, 0, 0, 0});
-  } else {
-    // compress.py:115-122: chunk c is drawn from Rng(seed).child(f"chunk{c}")
-    int64_t c = 0;
-    for (int64_t r0 = 0; r0 < rows; r0 += chunk_rows, ++c) {
-      const int64_t rr = std::min(chunk_rows, rows - r0);
-      const std::string tag = "chunk" + std::to_string(c);
-      sd.push_back(StreamDesc{child_seed(seed, tag.c_str()), rr * cols, r0, 0, 0, 0});
-    }
-  }
-  if (dtype == CNMF_F64) return gaussian_streams(sd, (double*)out, ld, cols, stream);
-  if (dtype == CNMF_F32) return gaussian_streams(sd, (float*)out, ld, cols, stream);
-  return fail(CNMF_ERR_ARGUMENT, "unknown dtype");
+  const size_t bytes = gaussian_workspace(rows, cols, chunk_rows);
+  keep_pool();
+  void* ws = nullptr;
+  CNMF_CUDA(cudaMallocAsync(&ws, bytes, stream));
+  const int rc = gaussian_fill_ws(seed, rows, cols, chunk_rows, dtype, out, ld, ws, bytes, stream);
+  cudaFreeAsync(ws, stream);
+  return rc;
 }
 
 int uniform_fill(uint64_t seed, int64_t rows, int64_t cols, double low, double high, int dtype, int transpose,

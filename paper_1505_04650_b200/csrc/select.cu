@@ -398,6 +398,7 @@ int select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const doub
   size_t bytes = (size_t)n * ld * 8 /*R*/ + (size_t)n * 8 * 3 /*sq, denom, score*/ + (size_t)n * 2 /*flags*/ +
                  (size_t)64 * 64 * 8 + (size_t)n * 64 * 8 * 2 /*target, H*/ + 4096 * 16 + 64 * 8 + 1024;
   char* buf = nullptr;
+  keep_pool();
   CNMF_CUDA(cudaMallocAsync((void**)&buf, bytes, st));
   char* p = buf;
   auto take = [&](size_t b) {

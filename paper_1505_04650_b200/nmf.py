@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .compress import CompressionConfig, _compress, adjust_config
+from .compress import CompressionConfig, _check, _compress, adjust_config
 from .device import DeviceMatrix, as_device64, out, stream, zeros
 from .errors import ArgumentError, DivergenceError, UndefinedMetricError
 from .rng import Rng, child_seed
@@ -77,16 +77,23 @@ def _rel_error(A, X, Yt):
     return float(np.sqrt(max(num, 0.0) / den))
 
 
-def compressed_problem(A, cfg):
-    """Bases and core for the compressed ADMM (nmf.py:120-135, 327-332)."""
-    left, _ = _compress(A, replace(cfg, seed=child_seed(cfg.seed, "left-basis")), 0)
-    right, _ = _compress(A, replace(cfg, seed=child_seed(cfg.seed, "right-basis")), 1)
+def compressed_problem(A, cfg, check=True):
+    """Bases and core for the compressed ADMM (nmf.py:120-135, 327-332),
+    enqueued back to back; one status check at the end."""
+    left, _ = _compress(A, replace(cfg, seed=child_seed(cfg.seed, "left-basis")), 0, check=False)
+    right, _ = _compress(A, replace(cfg, seed=child_seed(cfg.seed, "right-basis")), 1, check=False)
     s = cfg.basis_cols
     S = left.panel.shape[1]
     z = zeros((A.n, S))
     _lib.call("cnmf_pass_transpose", A.ptr, A.m, A.n, A.lda, left.panel.data_ptr(), s, z.data_ptr(), stream())
     core = zeros((S, S), dtype=torch.float64)
     _lib.call("cnmf_panel_cross", z.data_ptr(), right.panel.data_ptr(), A.n, S, core.data_ptr(), stream())
+    if check:
+        _check(left)
+        _check(right)
+    if A.on_host:
+        left.Q = left.panel[:, :s].double().cpu().numpy()
+        right.Q = right.panel[:, :s].double().cpu().numpy()
     return left, right, core[:s, :s].contiguous()
 
 

@@ -249,7 +249,8 @@ def test_admm_stopping_rule_and_oracle_error():
 
 
 def test_admm_config1_shape_parity():
-    a = O.dense_lowrank(2000, 1000, 20, 0.01, seed=0)
+    # configs[1] is an fp32 workload: both sides see the same fp32 matrix
+    a = O.dense_lowrank(2000, 1000, 20, 0.01, seed=0).astype(np.float32)
     cfg = C.CompressionConfig(r=20, r_ov=10, w=4, seed=5)
     fp = C.nmf_admm(a, 20, cfg=cfg, max_iter=500, tol=1e-4)
     ref = O.admm(a, 20, cfg=O.Config(20, 10, 4, 5), max_iter=500, tol=1e-4)
