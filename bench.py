@@ -269,7 +269,7 @@ def run_ours(args):
     pass_flops = 2.0 * M * N * 32  # padded panel width 32 for s = 30
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": None,
-                "kernel": "fwd_ffma<32>/trn_ffma<32> streaming passes (CUDA events on the launch stream)",
+                "kernel": "pass_tc<32> tcgen05 3xTF32 streaming passes (CUDA events on the launch stream)",
                 "launches": pl.value, "avg_launch_ms": pass_avg_ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                 "fp32_tflops": pass_flops / (pass_avg_ms * 1e-3) / 1e12, "fp32_peak_tflops_at_clock": fp32_peak,

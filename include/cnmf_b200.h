@@ -54,6 +54,9 @@ int cnmf_panel_ld(int s);
  * device milliseconds, launch count and algorithmic bytes since enabled. */
 int64_t cnmf_launch_count(void);
 void cnmf_set_pass_profiling(int on);
+/* streaming-pass implementation: 1 = tcgen05 3xTF32 (default; panel widths
+ * 32 and 64), 0 = FFMA (all widths; also selected by env CNMF_PASS=ffma) */
+void cnmf_set_pass_impl(int impl);
 int cnmf_pass_stats(double* total_ms, int64_t* launches, double* bytes);
 
 /* ---- RNG (rng.py) --------------------------------------------------------

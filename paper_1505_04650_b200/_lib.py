@@ -29,6 +29,7 @@ SIGNATURES = {
     "cnmf_panel_ld": (c_int, [c_int]),
     "cnmf_launch_count": (c_i64, []),
     "cnmf_set_pass_profiling": (None, [c_int]),
+    "cnmf_set_pass_impl": (None, [c_int]),
     "cnmf_pass_stats": (c_int, [ctypes.POINTER(c_dbl), c_i64p, ctypes.POINTER(c_dbl)]),
     "cnmf_child_seed": (c_u64, [c_u64, ctypes.c_char_p]),
     "cnmf_gaussian_fill": (c_int, [c_u64, c_i64, c_i64, c_i64, c_int, vp, c_i64, vp]),

@@ -31,6 +31,7 @@ int admm_run(const double*, const float*, int64_t, const float*, int64_t, int, i
              double*, double*, double*, double, double, double, int, double, double*, double*, int*, void*, size_t,
              int, int, cudaStream_t);
 int64_t launch_count();
+void set_pass_impl(int);
 void set_pass_profiling(int);
 int pass_stats(double*, int64_t*, double*);
 }  // namespace cnmf
@@ -57,6 +58,8 @@ int cnmf_panel_ld(int s) { return panel_ld(s); }
 int64_t cnmf_launch_count(void) { return launch_count(); }
 
 void cnmf_set_pass_profiling(int on) { set_pass_profiling(on); }
+
+void cnmf_set_pass_impl(int impl) { set_pass_impl(impl); }
 
 int cnmf_pass_stats(double* total_ms, int64_t* launches, double* bytes) {
   return pass_stats(total_ms, launches, bytes);

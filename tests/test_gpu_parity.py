@@ -86,6 +86,33 @@ def test_passes_match_fp64(m, n, s):
     assert np.all(Y.cpu().numpy()[:, s:] == 0) and np.all(Z.cpu().numpy()[:, s:] == 0)
 
 
+@pytest.mark.parametrize("m,n,s", [(1000, 700, 30), (300, 1029, 60), (129, 33, 20), (4096, 2048, 64)])
+def test_tensor_core_passes_match_ffma_and_fp64(m, n, s):
+    """tcgen05 3xTF32 passes agree with fp64 to fp32-level accuracy."""
+    g = np.random.default_rng(7 * m + n)
+    a = g.standard_normal((m, n))
+    A = DeviceMatrix(a)
+    S = C.compress.panel_ld(s)
+    x = np.zeros((n, S), np.float32)
+    x[:, :s] = g.standard_normal((n, s))
+    w = np.zeros((m, S), np.float32)
+    w[:, :s] = g.standard_normal((m, s))
+    X, Wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    a32 = a.astype(np.float32).astype(np.float64)
+    lib = _lib.load()
+    out = {}
+    for impl in (1, 0):
+        lib.cnmf_set_pass_impl(impl)
+        Y, Z = zeros((m, S)), zeros((n, S))
+        _lib.call("cnmf_pass_forward", A.ptr, m, n, A.lda, X.data_ptr(), s, Y.data_ptr(), stream())
+        _lib.call("cnmf_pass_transpose", A.ptr, m, n, A.lda, Wd.data_ptr(), s, Z.data_ptr(), stream())
+        out[impl] = (Y.cpu().numpy()[:, :s].astype(np.float64), Z.cpu().numpy()[:, :s].astype(np.float64))
+    lib.cnmf_set_pass_impl(1)
+    for impl in (1, 0):
+        assert relf(out[impl][0], a32 @ x[:, :s]) < 3e-6, impl
+        assert relf(out[impl][1], a32.T @ w[:, :s]) < 3e-6, impl
+
+
 # --------------------------------------------------------- compression ----
 
 @pytest.mark.parametrize("w", [0, 2, 4])
