@@ -493,9 +493,8 @@ int panel_ld(int s) {
   return -1;
 }
 
-int pass_forward_tc(const float*, int64_t, int64_t, int64_t, const float*, int, float*, float*, cudaStream_t);
-int pass_transpose_tc(const float*, int64_t, int64_t, int64_t, const float*, int, float*, float*, cudaStream_t);
-size_t tc_split_bytes(int64_t rows, int S);
+int pass_forward_tc(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
+int pass_transpose_tc(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
 
 // Pass implementation: tcgen05 3xTF32 (default for panel widths 32/64) or the
 // FFMA kernels (CNMF_PASS=ffma, and widths 128).
@@ -511,14 +510,7 @@ static bool use_tc(int S) {
 
 int pass_forward(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y,
                  cudaStream_t st) {
-  if (use_tc(S)) {
-    keep_pool();
-    float* split = nullptr;
-    CNMF_CUDA(cudaMallocAsync((void**)&split, tc_split_bytes(n, S), st));
-    const int rc = pass_forward_tc(A, m, n, lda, X, S, Y, split, st);
-    cudaFreeAsync(split, st);
-    return rc;
-  }
+  if (use_tc(S)) return pass_forward_tc(A, m, n, lda, X, S, Y, st);
   switch (S) {
     case 32: return launch_forward<32>(A, m, n, lda, X, Y, st);
     case 64: return launch_forward<64>(A, m, n, lda, X, Y, st);
@@ -529,14 +521,7 @@ int pass_forward(const float* A, int64_t m, int64_t n, int64_t lda, const float*
 
 int pass_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const float* W, int S, float* Z,
                    cudaStream_t st) {
-  if (use_tc(S)) {
-    keep_pool();
-    float* split = nullptr;
-    CNMF_CUDA(cudaMallocAsync((void**)&split, tc_split_bytes(m, S), st));
-    const int rc = pass_transpose_tc(A, m, n, lda, W, S, Z, split, st);
-    cudaFreeAsync(split, st);
-    return rc;
-  }
+  if (use_tc(S)) return pass_transpose_tc(A, m, n, lda, W, S, Z, st);
   switch (S) {
     case 32: return launch_transpose<32>(A, m, n, lda, W, Z, st);
     case 64: return launch_transpose<64>(A, m, n, lda, W, Z, st);

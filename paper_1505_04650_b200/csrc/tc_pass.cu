@@ -7,19 +7,27 @@
 // Forward pass  Y = A X   (M = rows of A, K = columns of A, N = s)
 // Transpose     Z = A^T W (M = columns of A, K = rows of A, N = s)
 //
-// Warp roles (224 threads): warp 0 issues TMA (A tile, 128B swizzle, plus the
-// [X_hi | X_lo] panel tile), warp 1 owns TMEM and issues the MMAs (one
-// elected thread), warps 2..5 split each landed A tile in shared memory into
-// hi (in place) and lo (second buffer) and, at the end of every output tile,
-// drain the fp32 accumulator from TMEM (tcgen05.ld) and write the rows.
-// The accumulator is [A_hi X_hi | A_hi X_lo + A_lo X_hi] (N = 2s columns,
-// double buffered in TMEM); the epilogue adds the two halves.
-// kind::tf32 only accepts K-major operands on sm_100a (the transpose bit
-// yields zeros; measured), so every operand is presented K-major: the
-// forward A tile comes K-major straight from TMA (SW128) and is split in
-// place; the transpose-pass A tile (row-major, i.e. MN-major for A^T) is
-// transposed by the splitting warps into K-major SW128 hi/lo tiles; the skinny
-// panel is pre-split and stored transposed ([hi; lo] rows, K contiguous).
+// One CTA per SM, warp-specialised (S/16 + 10 warps):
+//   warp 0      TMA producer: per K tile one stage = raw fp32 A tile (16 KB,
+//               K-major SW128 for the forward pass, row-major for the
+//               transpose pass) + the raw fp32 panel rows [32 k][S];
+//   warps 2..9  A splitters: warp w owns TMEM lane quarter w & 3 (= 32 output
+//               rows) and K half (w - 2) / 4; each thread reads its row from
+//               the stage, releases the stage, splits hi/lo and stores both
+//               into a TMEM ring (tcgen05.st); warps 2..5 also drain the
+//               accumulator at the end of every output tile;
+//   warps 10..  panel splitters: raw [32 k][S] -> K-major SW128 [hi; lo] in a
+//               small shared-memory ring (kind::tf32 only accepts K-major
+//               shared-memory operands on sm_100a; measured);
+//   warp 1      MMA issuer (one elected thread), A from TMEM, panel from SMEM:
+//                 D[:, 0:2s]  = A_hi [X_hi | X_lo]      (N = 2s)
+//                 D[:, s:2s] += A_lo X_hi               (N = s)
+//               so D = [A_hi X_hi | A_hi X_lo + A_lo X_hi] and the epilogue
+//               adds the halves; one tcgen05.commit per K tile releases both
+//               the panel slot and the TMEM A slot.
+// The stage ring is released as soon as the splitters hold the data in
+// registers, so nearly all of it is outstanding DRAM traffic (Little's law:
+// the loaded-HBM latency is several microseconds on B200).
 // Work is distributed exactly like the FFMA passes (contiguous unit ranges,
 // flush on tile change, red.global.add when a tile is shared).
 #include <algorithm>
@@ -29,7 +37,6 @@
 namespace cnmf {
 namespace {
 
-constexpr int kTcThreads = 192;       // warps 0..5
 constexpr int BMT = 128;              // output rows per tile (TMEM lanes)
 constexpr int BKT = 32;               // K per stage (one 128B swizzle atom of fp32)
 
@@ -57,33 +64,19 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                : "memory");
 }
 
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accumulate) {
+// 32 lanes x 16 consecutive fp32 columns per warp
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
   asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-// 32 lanes x 32 consecutive fp32 columns per warp (one column per register)
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
       "tcgen05.wait::ld.sync.aligned;"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr)
       : "memory");
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // SM100 shared-memory matrix descriptor, 128B swizzle.
@@ -103,34 +96,128 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int n, bool a_mn_major, bool b
          ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BMT >> 4) << 24);
 }
 
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// Round to the nearest tf32 value (10 explicit mantissa bits, ties away from
+// zero). The tensor core truncates the low 13 bits of an fp32 operand, so
+// both split halves are pre-rounded: hi = rn(v), lo = rn(v - hi) (v - hi is
+// exact in fp32), which keeps the split error unbiased and <= 2^-22 |v| --
+// truncating would bias every product of nonnegative data toward zero.
+__device__ __forceinline__ float tf32_rn(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+// Slot index + phase parity of a ring of N mbarrier-guarded buffers.
+template <int N>
+struct Ring {
+  int i = 0;
+  uint32_t ph = 0;
+  bool wrapped = false;  // every slot has been handed out at least once
+  __device__ __forceinline__ void next() {
+    if (++i == N) {
+      i = 0;
+      ph ^= 1;
+      wrapped = true;
+    }
+  }
+};
+
+#ifdef CNMF_TC_TRACE
+__device__ long long g_tc_trace[64][16];
+__device__ unsigned long long g_tc_span[148][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TC_SPAN(slot)                                                          \
+  do {                                                                         \
+    if (threadIdx.x == 0) g_tc_span[blockIdx.x][slot] = gtimer();              \
+  } while (0)
+#define TC_TRACE(slot)                                                          \
+  do {                                                                          \
+    if (blockIdx.x == 0 && it < 64) g_tc_trace[it][slot] = clock64();           \
+  } while (0)
+#else
+#define TC_TRACE(slot) \
+  do {                 \
+  } while (0)
+#define TC_SPAN(slot) \
+  do {                \
+  } while (0)
+#endif
 
 template <int S, bool TRANS>
 struct TcCfg {
-  static constexpr int ABYTES = BMT * BKT * 4;        // 16 KB
-  static constexpr int BBYTES = BKT * 2 * S * 4;      // [hi; lo] panel tile: 8 or 16 KB
-  // forward: A (split to hi in place) + lo + B; transpose: raw A + hi + lo + B
-  static constexpr int STAGE = (TRANS ? 3 : 2) * ABYTES + BBYTES;
-  static constexpr int ST = (int)((200 * 1024) / STAGE) < 6 ? (int)((200 * 1024) / STAGE) : 6;
+  static constexpr int ABYTES = BMT * BKT * 4;        // 16 KB raw A tile
+  static constexpr int BRAW = BKT * S * 4;            // raw fp32 panel tile [32 k][S]: 4 or 8 KB
+  static constexpr int STAGE = ABYTES + BRAW;         // one TMA stage: A tile + its panel tile
+  static constexpr int BSPL = BKT * 2 * S * 4;        // split K-major SW128 [hi; lo] panel: 8 or 16 KB
+  static constexpr int ST = (S == 32) ? 10 : 7;       // stage ring depth (DRAM bytes in flight per SM)
+  static constexpr int SSP = 3;                       // split panel ring
+  static constexpr int AST = 4;                       // TMEM ring of split A tiles
+  static constexpr int MD = 4;                        // "MMA of K tile j done" ring (>= SSP, AST)
+  static constexpr int KB = 2;                        // K tiles per tensor-core accumulation block
+  static_assert(MD >= SSP && MD >= AST, "one MMA-done ring serves both consumers");
   static constexpr int ACC_COLS = 2 * S;              // per accumulator buffer
-  static constexpr int TMEM_COLS = (4 * S <= 128) ? 128 : 256;
-  static constexpr size_t SMEM = 1024 + (size_t)ST * STAGE + 256;
+  static constexpr int A_COL0 = 2 * ACC_COLS;         // first TMEM column of the A ring
+  static constexpr int TMEM_COLS = (A_COL0 + AST * 2 * BKT <= 256) ? 256 : 512;
+  static constexpr int NSPLIT = 8;                    // A-splitting warps (2 per TMEM lane quarter)
+  static constexpr int NPW = 2;                       // panel-splitting warps
+  static constexpr int PU = S / 32;                   // panel units (32 columns x 16 k) per panel warp
+  static constexpr int NEPI = 4 * (S / 32);            // epilogue warps (lane quarter x 32-column group)
+  static constexpr int THREADS = 32 * (2 + NSPLIT + NPW + NEPI);
+  static constexpr size_t SMEM = (size_t)ST * STAGE + (size_t)SSP * BSPL + 512;
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert(A_COL0 + AST * 2 * BKT <= 512, "TMEM budget");
 };
 
-// TRANS = false: Y = A X (A tile K-major); TRANS = true: Z = A^T W (A tile
-// MN-major). P = output rows of the pass (m or n); NT = K tiles per output tile.
+constexpr int kWarpTma = 0, kWarpMma = 1, kWarpSplit0 = 2, kWarpPanel0 = 10, kWarpEpi0 = 12;
+
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 32 lanes x 16 consecutive 32-bit columns per warp
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+
+// TRANS = false: Y = A X; TRANS = true: Z = A^T W. P = output rows of the
+// pass (m or n); nt = K tiles per output tile.
+//
+// Rings: stage ring in shared memory (one TMA stage = raw fp32 A tile + the
+// matching raw panel tile), released once the A-splitting warps hold their
+// rows in registers and the panel warp has split the panel tile, so nearly
+// the whole ring is outstanding DRAM traffic; split panel ring (K-major SW128
+// [hi; lo]) released by the MMA commit; TMEM ring of split A tiles (hi and lo,
+// 32 columns each, lane = output row) filled with tcgen05.st and consumed by
+// A-from-TMEM MMAs; double-buffered TMEM accumulators.
 template <int S, bool TRANS>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
     pass_tc(const __grid_constant__ TmaDesc tA, const __grid_constant__ TmaDesc tB, float* __restrict__ out,
             int64_t P, int nt, int64_t nblocks, int whole) {
   using C = TcCfg<S, TRANS>;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + C::ST * C::STAGE);
-  uint64_t* conv = full + C::ST;
-  uint64_t* empty = conv + C::ST;
-  uint64_t* tfull = empty + C::ST;   // [2]
-  uint64_t* tempty = tfull + 2;      // [2]
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* sP = smem + C::ST * C::STAGE;                 // [SSP][BSPL]
+  uint64_t* full = (uint64_t*)(sP + C::SSP * C::BSPL);         // [ST] stage landed
+  uint64_t* empty = full + C::ST;                              // [ST] stage consumed by all splitters
+  uint64_t* pfull = empty + C::ST;                             // [SSP] split panel ready
+  uint64_t* mdone = pfull + C::SSP;                            // [MD] MMAs of K tile j retired
+  uint64_t* afull = mdone + C::MD;                             // [AST] split A in TMEM
+  uint64_t* tfull = afull + C::AST;                            // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;                                // [2] accumulator drained
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -139,22 +226,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int64_t u1 = whole ? ((b + 1) * nblocks / G) * nt : (b + 1) * U / G;
   const int64_t ntiles = u1 - u0;
   if (ntiles <= 0) return;
+  TC_SPAN(0);
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tA);
     prefetch_tmap(&tB);
     for (int s = 0; s < C::ST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 4);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], C::NSPLIT + C::NPW);
     }
+    for (int s = 0; s < C::SSP; ++s) {
+      mbar_init(&pfull[s], C::NPW);
+    }
+    for (int s = 0; s < C::AST; ++s) mbar_init(&afull[s], C::NSPLIT);
+    for (int s = 0; s < C::MD; ++s) mbar_init(&mdone[s], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], C::NEPI);
     }
     fence_barrier_init();
   }
-  if (warp == 1) {
+  if (warp == kWarpMma) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "n"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -164,199 +256,264 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  // Every role walks the same unit sequence u0..u1-1 with incremental
+  // (output tile, K tile) and ring (slot, phase) counters: no 64-bit
+  // division and no dynamically indexed arrays in the steady-state loops.
+  const int64_t ob0 = u0 / nt;
+  const int kt0 = (int)(u0 - ob0 * nt);
+
+  if (warp == kWarpTma) {
     // ---------------- TMA producer ----------------
     if (elect_one()) {
+      Ring<C::ST> r;
+      int64_t ob = ob0;
+      int kt = kt0;
       for (int64_t it = 0; it < ntiles; ++it) {
-        const int stage = (int)(it % C::ST);
-        if (it >= C::ST) mbar_wait(&empty[stage], (uint32_t)(((it / C::ST) - 1) & 1));
-        const int64_t u = u0 + it;
-        const int64_t ob = u / nt;          // output tile
-        const int kt = (int)(u - ob * nt);  // K tile
-        unsigned char* sa = smem + stage * C::STAGE;
-        unsigned char* sb = sa + (TRANS ? 3 : 2) * C::ABYTES;
-        mbar_arrive_expect_tx(&full[stage], C::ABYTES + C::BBYTES);
-        if (!TRANS) {
-          // A rows [ob*128, +128), cols [kt*32, +32): K-major SW128
-          tma_load_2d(sa, &tA, &full[stage], kt * BKT, (int)(ob * BMT));
-        } else {
-          // A rows [kt*32, +32) (K), cols [ob*128, +128) (M): row-major, no swizzle
-          tma_load_2d(sa, &tA, &full[stage], (int)(ob * BMT), kt * BKT);
+        if (it >= C::ST) mbar_wait(&empty[r.i], r.ph ^ 1);
+        TC_TRACE(0);
+        unsigned char* dst = smem + r.i * C::STAGE;
+        mbar_arrive_expect_tx(&full[r.i], C::STAGE);
+        if (!TRANS)  // A rows [ob*128, +128), cols [kt*32, +32): K-major SW128
+          tma_load_2d(dst, &tA, &full[r.i], kt * BKT, (int)(ob * BMT));
+        else         // A rows [kt*32, +32) (K), cols [ob*128, +128) (M): row-major
+          tma_load_2d(dst, &tA, &full[r.i], (int)(ob * BMT), kt * BKT);
+        // panel rows [kt*32, +32) (K), all S columns: row-major [32][S]
+        tma_load_2d(dst + C::ABYTES, &tB, &full[r.i], 0, kt * BKT);
+        r.next();
+        if (++kt == nt) {
+          kt = 0;
+          ++ob;
         }
-        // transposed panel: rows [0, 2S) = [hi; lo] output columns, K cols [kt*32, +32)
-        tma_load_2d(sb, &tB, &full[stage], kt * BKT, 0);
       }
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc_cat = idesc_tf32(2 * S, false, false);
-    constexpr uint32_t idesc_hi = idesc_tf32(S, false, false);
-    int buf = 0;
-    uint32_t tphase[2] = {0, 0};
-    bool first = true;
+  } else if (warp >= kWarpEpi0) {
+    // ---------------- epilogue (warps 12.., one output row x 32 columns each) ----------------
+    // The tensor core accumulates at most KB K tiles into a TMEM buffer; the
+    // partial sums then move to fp32 registers (round-to-nearest adds), so
+    // the error no longer grows with the tensor-core accumulation chain.
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int cg = 32 * ((warp - kWarpEpi0) >> 2);  // first output column of this warp
+    const int row_in_tile = 32 * q + lane;
+    Ring<2> racc;
+    float acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+    int64_t ob = ob0;
+    int kt = kt0;
     for (int64_t it = 0; it < ntiles; ++it) {
-      const int stage = (int)(it % C::ST);
-      const int64_t u = u0 + it;
-      const bool tile_start = first || (u % nt == 0);
-      const bool tile_end = (it == ntiles - 1) || ((u + 1) % nt == 0);
-      // reuse of an accumulator buffer waits until the epilogue drained it
-      if (tile_start && tphase[buf] > 0) mbar_wait(&tempty[buf], (tphase[buf] - 1) & 1);
-      mbar_wait(&full[stage], (uint32_t)((it / C::ST) & 1));
-      mbar_wait(&conv[stage], (uint32_t)((it / C::ST) & 1));
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t base = smem_u32(smem + stage * C::STAGE);
-        const uint32_t shi = TRANS ? base + C::ABYTES : base;        // K-major SW128 hi tile
-        const uint32_t slo = shi + C::ABYTES;                          // K-major SW128 lo tile
-        const uint32_t sb = base + (TRANS ? 3 : 2) * C::ABYTES;       // K-major SW128 [hi; lo]
-        const uint32_t dcat = tmem + buf * C::ACC_COLS;
-        const uint32_t dlo = dcat + S;
-#pragma unroll
-        for (int k = 0; k < BKT / 8; ++k) {
-          // K-major: advance 8 tf32 (32 B) within the 128 B swizzled rows
-          const uint64_t ahi = smem_desc(shi + 32 * k, 16, 1024);
-          const uint64_t alo = smem_desc(slo + 32 * k, 16, 1024);
-          const uint64_t bcat = smem_desc(sb + 32 * k, 16, 1024);
-          const uint32_t acc = (tile_start && k == 0) ? 0u : 1u;
-          tc_mma(dcat, ahi, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
-          tc_mma(dlo, alo, bcat, idesc_hi, 1u);     //            + A_lo X_hi
-        }
-        tc_commit(&empty[stage]);
-        if (tile_end) tc_commit(&tfull[buf]);
-      }
-      __syncwarp();
-      first = false;
-      if (tile_end) {
-        tphase[buf] += 1;
-        buf ^= 1;
-      }
-    }
-  } else if (warp >= 2 && warp < 6) {
-    // ---------------- converter + epilogue (128 threads) ----------------
-    const int ct = threadIdx.x - 64;  // 0..127
-    const int q = warp & 3;           // TMEM lane quarter this warp may access
-    int buf = 0;
-    uint32_t tph[2] = {0, 0};
-    for (int64_t it = 0; it < ntiles; ++it) {
-      const int stage = (int)(it % C::ST);
-      const int64_t u = u0 + it;
-      mbar_wait(&full[stage], (uint32_t)((it / C::ST) & 1));
-      if (!TRANS) {
-        // split the landed K-major A tile: hi in place, lo into the second buffer
-        float4* a4 = (float4*)(smem + stage * C::STAGE);
-        float4* l4 = (float4*)(smem + stage * C::STAGE + C::ABYTES);
-#pragma unroll
-        for (int j = 0; j < C::ABYTES / 16 / 128; ++j) {
-          const int idx = ct + 128 * j;
-          const float4 v = a4[idx];
-          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-          a4[idx] = h;
-          l4[idx] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-        }
-      } else {
-        // thread ct owns output row (A column) ct: gather its 32 K values from
-        // the row-major tile, split, and store them as row ct of K-major SW128
-        // hi / lo tiles (16 B chunk c of row r lives at chunk c ^ (r & 7))
-        const float* raw = (const float*)(smem + stage * C::STAGE);
-        unsigned char* hi = smem + stage * C::STAGE + C::ABYTES;
-        unsigned char* lo = hi + C::ABYTES;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          float v[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) v[e] = raw[(4 * c + e) * BMT + ct];
-          const float4 h = make_float4(tf32_hi(v[0]), tf32_hi(v[1]), tf32_hi(v[2]), tf32_hi(v[3]));
-          const int off = ct * 128 + ((c ^ (ct & 7)) << 4);
-          *(float4*)(hi + off) = h;
-          *(float4*)(lo + off) = make_float4(v[0] - h.x, v[1] - h.y, v[2] - h.z, v[3] - h.w);
-        }
-      }
-      fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[stage]);
-      const bool tile_end = (it == ntiles - 1) || ((u + 1) % nt == 0);
-      if (tile_end) {
-        const int64_t ob = u / nt;
-        const bool owned = (ob * nt >= u0) && ((ob + 1) * nt <= u1);
-        mbar_wait(&tfull[buf], tph[buf] & 1);
-        tph[buf] += 1;
+      const bool tile_end = (it == ntiles - 1) || (kt == nt - 1);
+      if (tile_end || ((kt + 1) % C::KB == 0)) {
+        mbar_wait(&tfull[racc.i], racc.ph);
         tc_fence_after();
-        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + buf * C::ACC_COLS;
-        const int64_t row = ob * BMT + 32 * q + lane;
+        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + racc.i * C::ACC_COLS + cg;
 #pragma unroll
-        for (int c0 = 0; c0 < S; c0 += 32) {
-          float vh[32], vl[32];
-          tmem_ld32(taddr + c0, vh);
-          tmem_ld32(taddr + S + c0, vl);
-          if (row < P) {
-            float* dst = out + row * S + c0;
+        for (int c0 = 0; c0 < 32; c0 += 16) {
+          float vh[16], vl[16];
+          tmem_ld16(taddr + c0, vh);
+          tmem_ld16(taddr + S + c0, vl);
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float x0 = vh[j] + vl[j], x1 = vh[j + 1] + vl[j + 1];
-              const float x2 = vh[j + 2] + vl[j + 2], x3 = vh[j + 3] + vl[j + 3];
-              if (owned)
-                *(float4*)(dst + j) = make_float4(x0, x1, x2, x3);
-              else
-                red_add_v4(dst + j, x0, x1, x2, x3);
-            }
-          }
+          for (int j = 0; j < 16; ++j) acc[c0 + j] += vh[j] + vl[j];
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
-        buf ^= 1;
+        if (lane == 0) mbar_arrive(&tempty[racc.i]);
+        racc.next();
       }
+      if (tile_end) {
+        const int64_t t0 = ob * nt;  // first unit of this output tile
+        const bool owned = (t0 >= u0) && (t0 + nt <= u1);
+        const int64_t row = ob * BMT + row_in_tile;
+        if (row < P) {
+          float* dst = out + row * S + cg;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            if (owned)
+              *(float4*)(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            else
+              red_add_v4(dst + j, acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+      }
+      if (++kt == nt) {
+        kt = 0;
+        ++ob;
+      }
+    }
+  } else if (warp >= kWarpPanel0) {
+    // ---------------- panel splitters: raw [32 k][S] -> K-major SW128 [hi; lo] ----------------
+    // panel warp p covers units p * PU .. p * PU + PU - 1; unit u = columns
+    // [32 (u >> 1), +32) x k half u & 1
+    const int pw = warp - kWarpPanel0;
+    Ring<C::ST> r;
+    Ring<C::SSP> rp;
+    Ring<C::MD> rd;  // tracks K tile it - SSP (the previous user of slot rp.i)
+    for (int64_t it = 0; it < ntiles; ++it) {
+      mbar_wait(&full[r.i], r.ph);
+      if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(7);
+      const float* raw = (const float*)(smem + r.i * C::STAGE + C::ABYTES);
+      float h[C::PU][16], l[C::PU][16];
+#pragma unroll
+      for (int t = 0; t < C::PU; ++t) {
+        const int u = pw * C::PU + t;
+        const int n = 32 * (u >> 1) + lane;  // lanes read consecutive columns
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float v = raw[(16 * (u & 1) + k) * S + n];
+          h[t][k] = tf32_rn(v);
+          l[t][k] = tf32_rn(v - h[t][k]);
+        }
+      }
+      __syncwarp();
+      if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(10);
+      if (lane == 0) mbar_arrive(&empty[r.i]);
+      if (it >= C::SSP) {
+        mbar_wait(&mdone[rd.i], rd.ph);
+        rd.next();
+      }
+      if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(11);
+      unsigned char* dst = sP + rp.i * C::BSPL;
+#pragma unroll
+      for (int t = 0; t < C::PU; ++t) {
+        const int u = pw * C::PU + t;
+        const int n = 32 * (u >> 1) + lane;  // output column = operand row
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c = 4 * (u & 1) + cc;
+          const uint32_t off = (uint32_t)n * 128 + ((c ^ (n & 7)) << 4);
+          *(float4*)(dst + off) = make_float4(h[t][4 * cc], h[t][4 * cc + 1], h[t][4 * cc + 2], h[t][4 * cc + 3]);
+          *(float4*)(dst + S * 128 + off) =
+              make_float4(l[t][4 * cc], l[t][4 * cc + 1], l[t][4 * cc + 2], l[t][4 * cc + 3]);
+        }
+      }
+      if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(12);
+      fence_proxy_async();  // generic-proxy stores -> tensor-core (async proxy) reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull[rp.i]);
+      if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(9);
+      r.next();
+      rp.next();
+    }
+  } else if (warp == kWarpMma) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc_cat = idesc_tf32(2 * S, false, false);
+    constexpr uint32_t idesc_hi = idesc_tf32(S, false, false);
+    Ring<C::SSP> rp;
+    Ring<C::AST> ra;
+    Ring<C::MD> rd;
+    Ring<2> racc;  // accumulator buffer + its reuse phase
+    int kt = kt0;
+    bool block_start = true;
+    for (int64_t it = 0; it < ntiles; ++it) {
+      const bool tile_end = (it == ntiles - 1) || (kt == nt - 1);
+      const bool block_end = tile_end || ((kt + 1) % C::KB == 0);
+      // reuse of an accumulator buffer waits until the epilogue drained it
+      if (block_start && racc.wrapped) mbar_wait(&tempty[racc.i], racc.ph ^ 1);
+      mbar_wait(&pfull[rp.i], rp.ph);
+      mbar_wait(&afull[ra.i], ra.ph);
+      tc_fence_after();
+      if (lane == 0) TC_TRACE(4);
+      if (elect_one()) {
+        const uint32_t sb = smem_u32(sP + rp.i * C::BSPL);        // K-major SW128 [hi; lo]
+        const uint32_t ahi = tmem + C::A_COL0 + ra.i * 2 * BKT;   // split A in TMEM
+        const uint32_t alo = ahi + BKT;
+        const uint32_t dcat = tmem + racc.i * C::ACC_COLS;
+        const uint32_t dlo = dcat + S;
+#pragma unroll
+        for (int k = 0; k < BKT / 8; ++k) {
+          const uint64_t bcat = smem_desc(sb + 32 * k, 16, 1024);  // 8 tf32 = 32 B per K step
+          const uint32_t acc = (block_start && k == 0) ? 0u : 1u;
+          tc_mma_ts(dcat, ahi + 8 * k, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
+          tc_mma_ts(dlo, alo + 8 * k, bcat, idesc_hi, 1u);     //            + A_lo X_hi
+        }
+        tc_commit(&mdone[rd.i]);  // one commit releases the split panel and the TMEM A slot
+        if (block_end) tc_commit(&tfull[racc.i]);
+        TC_TRACE(5);
+      }
+      __syncwarp();
+      rp.next();
+      ra.next();
+      rd.next();
+      block_start = block_end;
+      if (block_end) racc.next();
+      if (++kt == nt) kt = 0;
+    }
+  } else {
+    // ---------------- A splitters (warps 2..9) ----------------
+    // warp w serves TMEM lane quarter w & 3 and K half (w - 2) / 4 of every tile
+    const int q = warp & 3;
+    const int half = (warp - kWarpSplit0) >> 2;
+    const int row_in_tile = 32 * q + lane;
+    Ring<C::ST> r;
+    Ring<C::AST> ra;
+    Ring<C::MD> rd;  // tracks K tile it - AST (the previous user of TMEM slot ra.i)
+    for (int64_t it = 0; it < ntiles; ++it) {
+      mbar_wait(&full[r.i], r.ph);
+      if (threadIdx.x == 64) TC_TRACE(1);
+      float hi[16], lo[16];
+      if (!TRANS) {
+        // row r of the K-major SW128 tile: 16 B chunk c at chunk c ^ (r & 7)
+        const unsigned char* rowp = smem + r.i * C::STAGE + row_in_tile * 128;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c = 4 * half + cc;
+          const float4 v = *(const float4*)(rowp + ((c ^ (row_in_tile & 7)) << 4));
+          hi[4 * cc + 0] = v.x;
+          hi[4 * cc + 1] = v.y;
+          hi[4 * cc + 2] = v.z;
+          hi[4 * cc + 3] = v.w;
+        }
+      } else {
+        // A column = output row: gather 16 K values from the row-major tile
+        const float* raw = (const float*)(smem + r.i * C::STAGE) + row_in_tile;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) hi[k] = raw[(16 * half + k) * BMT];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[r.i]);  // raw tile is in registers: recycle the stage
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float v = hi[k];
+        hi[k] = tf32_rn(v);
+        lo[k] = tf32_rn(v - hi[k]);
+      }
+      if (it >= C::AST) {
+        mbar_wait(&mdone[rd.i], rd.ph);
+        rd.next();
+      }
+      tc_fence_after();
+      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + C::A_COL0 + ra.i * 2 * BKT + 16 * half;
+      tmem_st16(ta, hi);
+      tmem_st16(ta + BKT, lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&afull[ra.i]);
+      if (threadIdx.x == 64) TC_TRACE(3);
+      r.next();
+      ra.next();
     }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1)
+  TC_SPAN(1);
+  if (warp == kWarpMma)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
 }
 
-// Split an fp32 panel P (rows x S) into the transposed [hi; lo] operand
-// PT (2S x ldt): PT[c][r] = hi(P[r][c]), PT[S + c][r] = lo(P[r][c]).
-// 32 x 32 tiles through shared memory keep both sides coalesced.
-__global__ void split_panel_t(const float* __restrict__ src, int64_t rows, int S, float* __restrict__ dst,
-                              int64_t ldt) {
-  __shared__ float tile[32][33];
-  const int64_t r0 = (int64_t)blockIdx.x * 32;
-  const int c0 = blockIdx.y * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-  for (int i = ty; i < 32; i += 8) {
-    const int64_t r = r0 + i;
-    tile[i][tx] = (r < rows && c0 + tx < S) ? src[r * S + c0 + tx] : 0.f;
-  }
-  __syncthreads();
-  for (int i = ty; i < 32; i += 8) {
-    const int c = c0 + i;
-    const int64_t r = r0 + tx;
-    if (c < S && r < rows) {
-      const float x = tile[tx][i];
-      const float h = tf32_hi(x);
-      dst[(int64_t)c * ldt + r] = h;
-      dst[(int64_t)(S + c) * ldt + r] = x - h;
-    }
-  }
-}
-
 template <int S, bool TRANS>
-int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bpanel, float* out, float* split_buf,
-              cudaStream_t st) {
+int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bpanel, float* out, cudaStream_t st) {
   using C = TcCfg<S, TRANS>;
   // skinny operand rows = K extent: n (forward, X) or m (transpose, W)
   const int64_t brows = TRANS ? m : n;
-  const int64_t ldt = (brows + 31) / 32 * 32;
-  split_panel_t<<<dim3((unsigned)ceil_div(brows, 32), (unsigned)(S / 32)), 256, 0, st>>>(Bpanel, brows, S, split_buf,
-                                                                                       ldt);
-  CNMF_LAUNCH_CHECK();
   TmaDesc tA, tB;
   if (!TRANS)
     CNMF_TRY(make_tma_2d(&tA, A, 4, m, n, lda, BKT, BMT, true));
   else
     CNMF_TRY(make_tma_2d(&tA, A, 4, m, n, lda, BMT, BKT, false));
-  CNMF_TRY(make_tma_2d(&tB, split_buf, 4, 2 * S, brows, ldt, BKT, 2 * S, true));
+  CNMF_TRY(make_tma_2d(&tB, Bpanel, 4, brows, S, S, S, BKT, false));
   const int64_t P = TRANS ? n : m;   // output rows
   const int nt = (int)ceil_div(brows, BKT);
   const int64_t nblocks = ceil_div(P, BMT);
@@ -374,7 +531,7 @@ int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bp
     CNMF_CUDA(cudaEventCreate(&e1));
     CNMF_CUDA(cudaEventRecord(e0, st));
   }
-  pass_tc<S, TRANS><<<(unsigned)grid, kTcThreads, C::SMEM, st>>>(tA, tB, out, P, nt, nblocks, whole);
+  pass_tc<S, TRANS><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(tA, tB, out, P, nt, nblocks, whole);
   CNMF_LAUNCH_CHECK();
   if (e0) {
     CNMF_CUDA(cudaEventRecord(e1, st));
@@ -385,22 +542,19 @@ int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bp
 
 }  // namespace
 
-size_t tc_split_bytes(int64_t rows, int S) { return (size_t)((rows + 31) / 32 * 32) * 2 * S * 4 + 256; }
-
-int pass_forward_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y, float* split,
-                    cudaStream_t st) {
+int pass_forward_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y, cudaStream_t st) {
   switch (S) {
-    case 32: return launch_tc<32, false>(A, m, n, lda, X, Y, split, st);
-    case 64: return launch_tc<64, false>(A, m, n, lda, X, Y, split, st);
+    case 32: return launch_tc<32, false>(A, m, n, lda, X, Y, st);
+    case 64: return launch_tc<64, false>(A, m, n, lda, X, Y, st);
   }
   return fail(CNMF_ERR_ARGUMENT, "tensor-core pass supports panel widths 32 and 64");
 }
 
 int pass_transpose_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* W, int S, float* Z,
-                      float* split, cudaStream_t st) {
+                      cudaStream_t st) {
   switch (S) {
-    case 32: return launch_tc<32, true>(A, m, n, lda, W, Z, split, st);
-    case 64: return launch_tc<64, true>(A, m, n, lda, W, Z, split, st);
+    case 32: return launch_tc<32, true>(A, m, n, lda, W, Z, st);
+    case 64: return launch_tc<64, true>(A, m, n, lda, W, Z, st);
   }
   return fail(CNMF_ERR_ARGUMENT, "tensor-core pass supports panel widths 32 and 64");
 }
