@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include "chol.cuh"
 #include "common.cuh"
 
 namespace cnmf {
@@ -24,119 +25,24 @@ int panel_ld(int s);
 int pass_forward(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
 int pass_transpose(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
 int panel_finalize(float*, int64_t, int, const double*, double*, cudaStream_t);
+int panel_finalize_chol(float*, int64_t, int, const double*, double*, int, double*, double*, int*, int, unsigned*,
+                        cudaStream_t);
 int gaussian_fill_ws(uint64_t, int64_t, int64_t, int64_t, int, void*, int64_t, void*, size_t, cudaStream_t);
 size_t gaussian_workspace(int64_t, int64_t, int64_t);
 
 namespace {
 
-// G (upper triangle valid, S x S) = R^T R; T = R^{-1} written S x S (zero
-// outside the leading s x s block). Symmetric Gaussian elimination of G held
-// in place, LU-style: after step k the upper triangle holds D L^T and the
-// strict lower triangle the accumulated row operations E = L^{-1}; scaling
-// row k by d_k^{-1/2} at the end yields R (upper) and R^{-T} (lower) at once,
-// so the factor and its inverse cost s parallel rank-1 steps (two barriers
-// each) instead of two serial triangular sweeps.
-// info[0] |= 1 when a shift was needed, info[1] = min(pass id) whose Gram
-// matrix was not finite or not factorable. One block.
-// the Gram buffer is consumed here and handed back zeroed for the next sweep
-__device__ __forceinline__ void G_rw_zero(const double* G, int idx) { const_cast<double*>(G)[idx] = 0.0; }
-
-__global__ void __launch_bounds__(512) chol_inv_kernel(const double* G, int s, int S,
-                                                       double* __restrict__ T, double* __restrict__ Rout,
-                                                       int* __restrict__ info, int pass_id) {
+__global__ void __launch_bounds__(512) chol_inv_kernel(const double* G, int s, int S, double* __restrict__ T,
+                                                       double* __restrict__ Rout, int* __restrict__ info,
+                                                       int pass_id) {
   extern __shared__ double a[];  // s x s (+ f[s], rowk[s])
-  double* f = a + s * s;
-  double* rowk = f + s;
-  __shared__ double s_maxd;
-  __shared__ int s_fail, s_nonfinite;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  if (tid == 0) {
-    s_maxd = 0.0;
-    s_fail = 0;
-    s_nonfinite = 0;
-  }
-  __syncthreads();
-  for (int idx = tid; idx < s * s; idx += nt) {
-    const int i = idx / s, j = idx - i * s;
-    const double v = (i <= j) ? G[i * S + j] : G[j * S + i];
-    if (!isfinite(v)) s_nonfinite = 1;
-    if (i == j) atomicMax((unsigned long long*)&s_maxd, __double_as_longlong(fmax(v, 0.0)));
-  }
-  __syncthreads();
-  if (s_nonfinite || !(s_maxd > 0.0)) {
-    if (tid == 0) atomicMin(&info[1], pass_id);
-    __syncthreads();
-    for (int idx = tid; idx < S * S; idx += nt) {
-      T[idx] = 0.0;
-      G_rw_zero(G, idx);
-    }
-    return;
-  }
-  const double thr = 1e-15 * s_maxd;
-  for (int attempt = 0; attempt < 2; ++attempt) {
-    const double shift = attempt ? 1e-12 * s_maxd : 0.0;
-    for (int idx = tid; idx < s * s; idx += nt) {
-      const int i = idx / s, j = idx - i * s;
-      a[idx] = ((i <= j) ? G[i * S + j] : G[j * S + i]) + (i == j ? shift : 0.0);
-    }
-    if (tid == 0 && attempt) info[0] |= 1;
-    __syncthreads();
-    for (int k = 0; k < s; ++k) {
-      const double d = a[k * s + k];
-      if (!(d > thr)) break;  // uniform: every thread reads the same value
-      for (int i = tid; i < s; i += nt) {
-        rowk[i] = a[k * s + i];
-        f[i] = (i > k) ? a[i * s + k] / d : 0.0;
-      }
-      __syncthreads();
-      const int rows = s - k - 1;
-      for (int idx = tid; idx < rows * s; idx += nt) {
-        const int i = k + 1 + idx / s, j = idx % s;
-        a[i * s + j] = (j == k) ? -f[i] : a[i * s + j] - f[i] * rowk[j];
-      }
-      __syncthreads();
-    }
-    // a pivot below the threshold aborted the sweep (checked uniformly)
-    bool ok = true;
-    for (int k = 0; k < s; ++k)
-      if (!(a[k * s + k] > thr)) ok = false;
-    if (ok) {
-      s_fail = 0;
-      break;
-    }
-    s_fail = 1;
-    __syncthreads();
-  }
-  if (s_fail) {
-    if (tid == 0) atomicMin(&info[1], pass_id);
-    for (int idx = tid; idx < S * S; idx += nt) {
-      T[idx] = 0.0;
-      G_rw_zero(G, idx);
-    }
-    return;
-  }
-  __syncthreads();
-  for (int idx = tid; idx < S * S; idx += nt) G_rw_zero(G, idx);
-  for (int idx = tid; idx < S * S; idx += nt) {
-    const int i = idx / S, j = idx - i * S;
-    double t = 0.0, r = 0.0;
-    if (i < s && j < s) {
-      // T[i][j] = R^{-T}[j][i]: row j of E scaled by d_j^{-1/2}
-      if (i <= j) {
-        const double dj = sqrt(a[j * s + j]);
-        t = (i == j) ? 1.0 / dj : a[j * s + i] / dj;
-        const double di = sqrt(a[i * s + i]);
-        r = (i == j) ? di : a[i * s + j] / di;
-      }
-    }
-    T[idx] = t;
-    if (Rout != nullptr) Rout[idx] = r;
-  }
+  chol_small(G, s, S, T, Rout, info, pass_id, a);
 }
 
 __global__ void init_info(int* info) {
   info[0] = 0;
   info[1] = 1 << 30;
+  info[4] = 0;  // last-block counter of the fused finalize + factor kernel
 }
 
 }  // namespace
@@ -166,6 +72,7 @@ struct Scratch {
   double* G;
   double* T;
   int* info;
+  unsigned* counter;
 };
 
 static Scratch carve_small(void* base, int S) {
@@ -174,6 +81,7 @@ static Scratch carve_small(void* base, int S) {
   sc.G = (double*)p;
   sc.T = (double*)(p + (size_t)S * S * 8);
   sc.info = (int*)(p + 2 * (size_t)S * S * 8);
+  sc.counter = (unsigned*)(sc.info + 4);
   return sc;
 }
 
@@ -181,8 +89,8 @@ static Scratch carve_small(void* base, int S) {
 // re-factor, apply again (CholeskyQR2 on an already well-conditioned panel).
 static int finish_basis(float* P, int64_t rows, int s, int S, Scratch sc, double* Rfinal, int first_pass_id,
                         cudaStream_t st) {
-  CNMF_TRY(panel_finalize(P, rows, S, sc.T, sc.G, st));
-  CNMF_TRY(chol_inv(sc.G, s, S, sc.T, Rfinal, sc.info, first_pass_id, st));
+  CNMF_TRY(panel_finalize_chol(P, rows, S, nullptr, sc.G, s, sc.T, Rfinal, sc.info, first_pass_id, sc.counter,
+                               st));
   CNMF_TRY(panel_finalize(P, rows, S, sc.T, nullptr, st));
   return CNMF_OK;
 }
@@ -248,13 +156,15 @@ int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s
     cur = Pn;
   }
   int64_t cur_rows = side == 0 ? m : n;
-  bool pending = false;  // sc.T holds a deferred transform for `cur`
+  // One explicit CholeskyQR sweep per pass output: Gram + factor in one
+  // launch, then R^{-1} applied in place. The pass inputs need not be
+  // orthonormal to working precision -- any upper-triangular transform keeps
+  // the leading column spans, and the next output is orthonormalised again --
+  // so the second (polishing) sweep runs only once, on the final basis.
   auto orth_sweep = [&]() -> int {
-    CNMF_TRY(panel_finalize(cur, cur_rows, S, pending ? sc.T : nullptr, sc.G, st));
-    CNMF_TRY(chol_inv(sc.G, s, S, sc.T, nullptr, sc.info, pass_id, st));
-    CNMF_TRY(panel_finalize(cur, cur_rows, S, sc.T, sc.G, st));
-    CNMF_TRY(chol_inv(sc.G, s, S, sc.T, nullptr, sc.info, pass_id, st));
-    pending = true;
+    CNMF_TRY(panel_finalize_chol(cur, cur_rows, S, nullptr, sc.G, s, sc.T, nullptr, sc.info, pass_id, sc.counter,
+                                 st));
+    CNMF_TRY(panel_finalize(cur, cur_rows, S, sc.T, nullptr, st));
     return CNMF_OK;
   };
   CNMF_TRY(orth_sweep());
@@ -266,7 +176,6 @@ int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s
       CNMF_TRY(pass_transpose(A, m, n, lda, cur, S, nxt, st));
     else
       CNMF_TRY(pass_forward(A, m, n, lda, cur, S, nxt, st));
-    // the input's deferred (near-identity) transform commutes with the pass
     cur = nxt;
     cur_rows = to_n ? n : m;
     CNMF_TRY(orth_sweep());
@@ -284,10 +193,8 @@ int orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws
   init_info<<<1, 1, 0, st>>>(sc.info);
   CNMF_LAUNCH_CHECK();
   CNMF_CUDA(cudaMemsetAsync(sc.G, 0, (size_t)S * S * 8, st));
-  CNMF_TRY(panel_finalize(P, rows, S, nullptr, sc.G, st));
-  CNMF_TRY(chol_inv(sc.G, s, S, sc.T, nullptr, sc.info, 0, st));
-  CNMF_TRY(panel_finalize(P, rows, S, sc.T, sc.G, st));
-  CNMF_TRY(chol_inv(sc.G, s, S, sc.T, nullptr, sc.info, 0, st));
+  CNMF_TRY(panel_finalize_chol(P, rows, S, nullptr, sc.G, s, sc.T, nullptr, sc.info, 0, sc.counter, st));
+  CNMF_TRY(panel_finalize(P, rows, S, sc.T, nullptr, st));
   CNMF_TRY(finish_basis(P, rows, s, S, sc, R, 0, st));
   return check_info(sc.info, "orthonormalize", st);
 }

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <string>
 
+#include "chol.cuh"
 #include "common.cuh"
 
 namespace cnmf {
@@ -291,9 +292,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 // G += P^T P in fp64 (upper triangle, atomics). Grid-strided over 64-row
 // tiles; the Gram products are spread over 4x4 register blocks x row groups
 // so that every thread of the block accumulates. Either step can be disabled.
+// With `counter` set, the last block to finish factors the completed Gram
+// matrix (chol_block: Tout = R^{-1}, G handed back zeroed), which saves a
+// launch and a dependent gap per CholeskyQR sweep.
 template <int S>
-__global__ void __launch_bounds__(kThreads)
-    finalize_panel(float* __restrict__ P, int64_t rows, const double* __restrict__ T, double* __restrict__ G) {
+__global__ void __launch_bounds__(kThreads, 2)
+    finalize_panel(float* __restrict__ P, int64_t rows, const double* T, double* __restrict__ G, int s,
+                   double* Tout, double* __restrict__ Rout, int* __restrict__ info, int pass_id,
+                   unsigned* __restrict__ counter) {
   constexpr int TR = 64;
   constexpr int NB = S / 4;                  // 4-wide blocks per side
   constexpr int NBLK = NB * (NB + 1) / 2;    // upper-triangular 4x4 blocks
@@ -385,20 +391,32 @@ __global__ void __launch_bounds__(kThreads)
         for (int q = 1; q < GROUPS; ++q)
 #pragma unroll
           for (int e = 0; e < 16; ++e) g[0][e] += red[(q * NBLK + bidx) * 16 + e];
-      if (grp != 0) return;
     }
+    if (grp == 0) {
 #pragma unroll
-    for (int q = 0; q < BPT; ++q) {
-      if (bi[q] < 0) continue;
+      for (int q = 0; q < BPT; ++q) {
+        if (bi[q] < 0) continue;
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int ia = 4 * bi[q] + a, jb = 4 * bj[q] + b;
-          if (ia <= jb) atomicAdd(G + ia * S + jb, g[q][a * 4 + b]);
-        }
+          for (int b = 0; b < 4; ++b) {
+            const int ia = 4 * bi[q] + a, jb = 4 * bj[q] + b;
+            if (ia <= jb) atomicAdd(G + ia * S + jb, g[q][a * 4 + b]);
+          }
+      }
     }
   }
+  if (counter == nullptr) return;
+  // last block: factor the finished Gram matrix
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  chol_small(G, s, S, Tout, Rout, info, pass_id, reinterpret_cast<double*>(fsm));
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 template <int S>
@@ -467,19 +485,28 @@ int launch_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const fl
 }
 
 template <int S>
-int launch_finalize(float* P, int64_t rows, const double* T, double* G, cudaStream_t st) {
+int launch_finalize(float* P, int64_t rows, const double* T, double* G, int s, double* Tout, double* Rout, int* info,
+                    int pass_id, unsigned* counter, cudaStream_t st) {
   constexpr int NB = S / 4, NBLK = NB * (NB + 1) / 2;
   constexpr int GROUPS = (NBLK >= kThreads) ? 1 : kThreads / NBLK;
-  constexpr size_t smem = (size_t)(S * S + 2 * 64 * S) * 4 + (GROUPS > 1 ? (size_t)GROUPS * NBLK * 16 * 8 : 0);
+  constexpr size_t fin = (size_t)(S * S + 2 * 64 * S) * 4 + (GROUPS > 1 ? (size_t)GROUPS * NBLK * 16 * 8 : 0);
+  constexpr size_t chol = ((size_t)S * S + 2 * (size_t)S) * 8;
+  constexpr size_t smem = fin > chol ? fin : chol;
   static bool attr = false;
   if (!attr) {
     CNMF_CUDA(cudaFuncSetAttribute(finalize_panel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  // G must be zero on entry (the Cholesky kernel re-zeroes it after use)
+  // G must be zero on entry (the Cholesky step re-zeroes it after use).
+  // One wave: a second partial wave would double the (latency-bound) time.
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, finalize_panel<S>, kThreads, smem));
+    per_sm = std::max(per_sm, 1);
+  }
   const int64_t tiles = ceil_div(rows, 64);
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(tiles, 4), kNumSMs));
-  finalize_panel<S><<<grid, kThreads, smem, st>>>(P, rows, T, G);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)per_sm * kNumSMs));
+  finalize_panel<S><<<grid, kThreads, smem, st>>>(P, rows, T, G, s, Tout, Rout, info, pass_id, counter);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }
@@ -532,9 +559,22 @@ int pass_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const floa
 
 int panel_finalize(float* P, int64_t rows, int S, const double* T, double* G, cudaStream_t st) {
   switch (S) {
-    case 32: return launch_finalize<32>(P, rows, T, G, st);
-    case 64: return launch_finalize<64>(P, rows, T, G, st);
-    case 128: return launch_finalize<128>(P, rows, T, G, st);
+    case 32: return launch_finalize<32>(P, rows, T, G, 0, nullptr, nullptr, nullptr, 0, nullptr, st);
+    case 64: return launch_finalize<64>(P, rows, T, G, 0, nullptr, nullptr, nullptr, 0, nullptr, st);
+    case 128: return launch_finalize<128>(P, rows, T, G, 0, nullptr, nullptr, nullptr, 0, nullptr, st);
+  }
+  return fail(CNMF_ERR_ARGUMENT, "panel width must be 32, 64 or 128");
+}
+
+// P <- P Tin (optional), G = P^T P, then Tout = R^{-1} of G = R^T R in the
+// same launch (last-block Cholesky). `counter` must be zero on entry and is
+// left zero.
+int panel_finalize_chol(float* P, int64_t rows, int S, const double* Tin, double* G, int s, double* Tout,
+                        double* Rout, int* info, int pass_id, unsigned* counter, cudaStream_t st) {
+  switch (S) {
+    case 32: return launch_finalize<32>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st);
+    case 64: return launch_finalize<64>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st);
+    case 128: return launch_finalize<128>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st);
   }
   return fail(CNMF_ERR_ARGUMENT, "panel width must be 32, 64 or 128");
 }
