@@ -109,6 +109,17 @@ int cnmf_compress_check(const void* ws, int64_t m, int64_t n, int s, void* strea
 /* orthonormalise a panel in place (compress.py:136 canonical_qr, Q factor);
  * R (s x s, fp64, device, may be NULL) receives the triangular factor. */
 int cnmf_orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, void* stream);
+/* CholeskyQR pieces for panels whose rows are spread over several GPUs
+ * (the Gram matrix is all-reduced between them):
+ * cnmf_cholesky_inverse  G (S x S fp64, device, upper triangle used) = R^T R;
+ *                        Rinv = R^{-1} and R (S x S, device; R may be NULL),
+ *                        zero outside the leading s x s block. G is consumed
+ *                        (returned zeroed). Synchronises `stream`; a Gram
+ *                        matrix that is not finite or not factorable after a
+ *                        1e-12 diagonal shift returns CNMF_ERR_NUMERIC.
+ * cnmf_panel_apply       P <- P T in place (T upper triangular S x S fp64). */
+int cnmf_cholesky_inverse(double* G, int s, int S, double* Rinv, double* R, void* stream);
+int cnmf_panel_apply(float* P, int64_t rows, int S, const double* T, void* stream);
 
 /* ---- separable NMF (snmf.py) ---------------------------------------------
  * The reduced matrix (Q^T A, s x n) is kept transposed: W (n x ld, fp64,

@@ -402,6 +402,15 @@ def admm(a, r, compressed=True, cfg=None, pu=1.0, pv=1.0, step=1.0, max_iter=500
     else:
         left = right = None
         core = a
+    u, v, it, trace, scores = admm_compressed(core, left, right, m, n, r, cfg, pu, pv, step, max_iter, tol,
+                                              on_iteration)
+    return AdmmOut(u, v, it, trace, scores, rel_error(a, u, v), left, right)
+
+
+def admm_compressed(core, left, right, m, n, r, cfg, pu=1.0, pv=1.0, step=1.0, max_iter=500, tol=1e-4,
+                    on_iteration=None):
+    """The ADMM loop of nmf.py:334-377 given the compressed problem (core =
+    L^T A R^T, left L m x s, right R s x n; None for the uncompressed case)."""
     u = uniform_matrix(cfg.seed, "init-left", (m, r))
     v = uniform_matrix(cfg.seed, "init-right", (r, n))
     du = np.zeros((m, r))
@@ -432,7 +441,7 @@ def admm(a, r, compressed=True, cfg=None, pu=1.0, pv=1.0, step=1.0, max_iter=500
             break
         if k >= 50 and score > 10.0 * scores[k - 50]:
             raise OracleError("DivergenceError", "diverging", trace=scores)
-    return AdmmOut(u, v, it, trace, scores, rel_error(a, u, v), left, right)
+    return u, v, it, trace, scores
 
 
 # ----------------------------------------------------------------------------

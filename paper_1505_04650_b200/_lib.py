@@ -42,6 +42,8 @@ SIGNATURES = {
                                                vp]),
     "cnmf_compress_check": (c_int, [vp, c_i64, c_i64, c_int, vp]),
     "cnmf_orthonormalize": (c_int, [vp, c_i64, c_int, vp, vp, c_size, vp]),
+    "cnmf_cholesky_inverse": (c_int, [vp, c_int, c_int, vp, vp, vp]),
+    "cnmf_panel_apply": (c_int, [vp, c_i64, c_int, vp, vp]),
     "cnmf_spa_workspace": (c_size, [c_i64, c_int]),
     "cnmf_panel_to_f64": (c_int, [vp, c_i64, c_int, vp, c_i64, vp]),
     "cnmf_select_spa": (c_int, [vp, c_i64, c_int, c_i64, c_int, c_i64p, c_intp, vp, c_size, vp]),

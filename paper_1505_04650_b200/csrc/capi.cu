@@ -10,6 +10,8 @@ int uniform_fill(uint64_t, int64_t, int64_t, double, double, int, int, void*, cu
 int pass_forward(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
 int pass_transpose(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
 int panel_cross(const float*, const float*, int64_t, int, double*, cudaStream_t);
+int cholesky_inverse(double*, int, int, double*, double*, cudaStream_t);
+int panel_finalize(float*, int64_t, int, const double*, double*, cudaStream_t);
 size_t compress_workspace(int64_t, int64_t, int);
 int structured_compress(const float*, int64_t, int64_t, int64_t, int, int, uint64_t, int, float*, void*, size_t,
                         cudaStream_t, bool);
@@ -112,6 +114,16 @@ int cnmf_compress_check(const void* ws, int64_t m, int64_t n, int s, void* strea
 int cnmf_orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, void* stream) {
   if (rows < s) return fail(CNMF_ERR_ARGUMENT, "panel must be at least as tall as it is wide");
   return orthonormalize(P, rows, s, R, ws, ws_bytes, STREAM(stream));
+}
+
+int cnmf_cholesky_inverse(double* G, int s, int S, double* Rinv, double* R, void* stream) {
+  if (s < 1 || S < s || panel_ld(s) != S) return fail(CNMF_ERR_ARGUMENT, "cholesky_inverse: bad widths");
+  return cholesky_inverse(G, s, S, Rinv, R, STREAM(stream));
+}
+
+int cnmf_panel_apply(float* P, int64_t rows, int S, const double* T, void* stream) {
+  if (rows < 1 || T == nullptr) return fail(CNMF_ERR_ARGUMENT, "panel_apply: empty panel or no transform");
+  return panel_finalize(P, rows, S, T, nullptr, STREAM(stream));
 }
 
 size_t cnmf_spa_workspace(int64_t n, int s) { return spa_workspace(n, s); }

@@ -48,14 +48,15 @@ __global__ void init_info(int* info) {
 }  // namespace
 
 int chol_inv(const double* G, int s, int S, double* T, double* R, int* info, int pass_id, cudaStream_t st) {
-  const size_t smem = ((size_t)s * s + 2 * (size_t)s) * 8;
+  // s <= 32: 256-thread register-tile factorisation (chol_tile32), else the block version
+  const size_t smem = std::max(((size_t)s * s + 2 * (size_t)s) * 8, (size_t)(32 * 33 + 128) * 8);
   static bool attr = false;
   if (!attr) {
     CNMF_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (128 * 128 + 256) * 8));
     attr = true;
   }
-  chol_inv_kernel<<<1, 512, smem, st>>>(G, s, S, T, R, info, pass_id);
+  chol_inv_kernel<<<1, s <= 32 ? 256 : 512, smem, st>>>(G, s, S, T, R, info, pass_id);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }
@@ -183,6 +184,18 @@ int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s
   CNMF_TRY(finish_basis(cur, cur_rows, s, S, sc, nullptr, pass_id, st));
   if (!check) return CNMF_OK;
   return check_info(sc.info, side == 0 ? "column basis" : "row basis", st);
+}
+
+int cholesky_inverse(double* G, int s, int S, double* Rinv, double* R, cudaStream_t st) {
+  keep_pool();
+  int* info = nullptr;
+  CNMF_CUDA(cudaMallocAsync((void**)&info, 64, st));
+  init_info<<<1, 1, 0, st>>>(info);
+  CNMF_LAUNCH_CHECK();
+  const int rc = chol_inv(G, s, S, Rinv, R, info, 0, st);
+  const int rc2 = rc == CNMF_OK ? check_info(info, "cholesky_inverse", st) : rc;
+  cudaFreeAsync(info, st);
+  return rc2;
 }
 
 int orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, cudaStream_t st) {

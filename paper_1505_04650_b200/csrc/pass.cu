@@ -490,7 +490,7 @@ int launch_finalize(float* P, int64_t rows, const double* T, double* G, int s, d
   constexpr int NB = S / 4, NBLK = NB * (NB + 1) / 2;
   constexpr int GROUPS = (NBLK >= kThreads) ? 1 : kThreads / NBLK;
   constexpr size_t fin = (size_t)(S * S + 2 * 64 * S) * 4 + (GROUPS > 1 ? (size_t)GROUPS * NBLK * 16 * 8 : 0);
-  constexpr size_t chol = ((size_t)S * S + 2 * (size_t)S) * 8;
+  constexpr size_t chol = ((size_t)S * S + 2 * (size_t)S + 32 * 33 + 128) * 8;
   constexpr size_t smem = fin > chol ? fin : chol;
   static bool attr = false;
   if (!attr) {

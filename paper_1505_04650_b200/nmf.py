@@ -107,8 +107,29 @@ def nmf_admm(a, r, compressed=True, cfg=None, penalty_u=1.0, penalty_v=1.0, step
     if not compressed:
         raise ArgumentError("the device path implements the compressed ADMM (compressed=True)")
     cfg = _resolve_config(r, cfg, m, n)
-    s = cfg.basis_cols
     left, right, core = compressed_problem(A, cfg)
+
+    def snapshot(k, u, du, vt, dvt, xc, yc):
+        st = AdmmState(xc=out(xc.clone(), A.on_host), yc=out(yc.clone(), A.on_host), u=out(u.clone(), A.on_host),
+                       v=out(vt.t().contiguous(), A.on_host), dual_u=out(du.clone(), A.on_host),
+                       dual_v=out(dvt.t().contiguous(), A.on_host), penalty_u=penalty_u, penalty_v=penalty_v,
+                       step_scale=step_scale)
+        on_iteration(k, st)
+
+    u, vt, iters, trace = run_admm(core, left.panel, m, right.panel, n, cfg, r, penalty_u, penalty_v, step_scale,
+                                   max_iter, tol, snapshot if on_iteration is not None else None)
+    rel = _rel_error(A, u, vt)
+    return FactorPair(X=out(u, A.on_host), Y=out(vt.t().contiguous(), A.on_host), iterations=iters,
+                      objective_trace=trace, rel_error=rel)
+
+
+def run_admm(core, left_panel, m, right_panel, n, cfg, r, penalty_u=1.0, penalty_v=1.0, step_scale=1.0,
+             max_iter=500, tol=1e-4, on_iteration=None):
+    """The ADMM loop of nmf.py:334-377 on the device for a compressed problem
+    (core = L^T A R^T, s x s fp64; left panel m x S, right panel R^T n x S):
+    seeded U[0,1] starts (nmf.py:337-339), then cnmf_admm_run. Returns
+    (U m x r, V^T n x r, iterations, objective trace)."""
+    s = cfg.basis_cols
     rng = Rng(cfg.seed)
     u = rng.child("init-left").uniform((m, r))
     vt = rng.child("init-right").uniform((r, n), transpose=True)  # V^T, n x r
@@ -123,37 +144,29 @@ def nmf_admm(a, r, compressed=True, cfg=None, penalty_u=1.0, penalty_v=1.0, step
     ws = torch.empty(nbytes, dtype=torch.uint8, device=u.device)
     it = ctypes.c_int(0)
     done = ctypes.c_int(0)
-    args = lambda resume, limit: (core.data_ptr(), left.panel.data_ptr(), m, right.panel.data_ptr(), n, s, r,
+    args = lambda resume, limit: (core.data_ptr(), left_panel.data_ptr(), m, right_panel.data_ptr(), n, s, r,
                                   u.data_ptr(), du.data_ptr(), vt.data_ptr(), dvt.data_ptr(), xc.data_ptr(),
                                   yc.data_ptr(), float(penalty_u), float(penalty_v), float(step_scale),
                                   int(max_iter), float(tol), trace.data_ptr(), scores.data_ptr(), ctypes.byref(it),
                                   ctypes.byref(done), resume, limit, ws.data_ptr(), nbytes, stream())
 
-    def diverged(status):
-        k = it.value
-        return dict(trace=scores[:k].tolist())
+    def diverged():
+        return dict(trace=scores[:it.value].tolist())
 
     if on_iteration is None:
         status = lib.cnmf_admm_run(*args(0, 0))
-        _lib.check(status, **diverged(status))
+        _lib.check(status, **diverged())
     else:
         resume = 0
         seen = 0
         while True:
             status = lib.cnmf_admm_run(*args(resume, 1))
-            _lib.check(status, **diverged(status))
+            _lib.check(status, **diverged())
             resume = 1
             if it.value > seen:
                 seen = it.value
-                Lh, Rh = left.Q, right.Q
-                st = AdmmState(xc=out(xc.clone(), A.on_host), yc=out(yc.clone(), A.on_host),
-                               u=out(u.clone(), A.on_host), v=out(vt.t().contiguous(), A.on_host),
-                               dual_u=out(du.clone(), A.on_host), dual_v=out(dvt.t().contiguous(), A.on_host),
-                               penalty_u=penalty_u, penalty_v=penalty_v, step_scale=step_scale)
-                on_iteration(seen - 1, st)
+                on_iteration(seen - 1, u, du, vt, dvt, xc, yc)
             if done.value:
                 break
     iters = it.value
-    rel = _rel_error(A, u, vt)
-    return FactorPair(X=out(u, A.on_host), Y=out(vt.t().contiguous(), A.on_host), iterations=iters,
-                      objective_trace=trace[:iters].tolist(), rel_error=rel)
+    return u, vt, iters, trace[:iters].tolist()
