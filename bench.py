@@ -16,8 +16,11 @@ ADMM iterations and the final relative error (one more pass).
 
 `--impl reference` times the CPU oracle port of the reference (numpy, all
 host threads) on the same workload and reports the e2e-style number.
-Multi-GPU (torchrun, N>1): every rank runs an independent replica (weak
-scaling); the time is the max over ranks.
+Multi-GPU (torchrun, N>1): A is sharded by columns (weak scaling: every
+rank holds an m x 5000 shard of an m x 5000N matrix); the passes all-reduce
+their m x S products over NCCL, CholeskyQR of row-sharded panels all-reduces
+the S x S Gram matrix, the ADMM runs replicated on the compressed problem
+(paper_1505_04650_b200/distributed.py); the time is the max over ranks.
 """
 
 import argparse
@@ -59,7 +62,7 @@ def dist_env():
 def config_block(extra=None):
     c = {"workload": WORKLOAD, "m": M, "n": N, "r": R, "oversample": R_OV, "q": W, "admm_iters": MAX_ITER,
          "passes_compress": PASSES_COMPRESS, "l2": "inputs larger than L2 (A = 200 MB fp32 > 126 MB)",
-         "parallelism": "replicas"}
+         "parallelism": "A column-sharded across GPUs, m x 5000 per GPU (weak scaling)"}
     if extra:
         c.update(extra)
     return c
@@ -175,14 +178,21 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _lib.load()
 
-    # synthetic configs[1] data, generated on the device
-    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    x = torch.rand(M, R, device="cuda", generator=g)
+    from paper_1505_04650_b200 import distributed as D
+
+    # synthetic configs[1] data, generated on the device: X shared by all
+    # ranks, this rank's column block Y_i and noise (global A = X [Y_0 .. Y_k])
+    gx = torch.Generator(device="cuda").manual_seed(1234)
+    g = torch.Generator(device="cuda").manual_seed(4321 + rank)
+    x = torch.rand(M, R, device="cuda", generator=gx)
     y = torch.rand(R, N, device="cuda", generator=g)
     a = torch.addmm(0.01 * torch.randn(M, N, device="cuda", generator=g), x, y).clamp_(min=0.0)
     del x, y
     A = DeviceMatrix(a)
-    cfg = C.adjust_config(C.CompressionConfig(r=R, r_ov=R_OV, w=W, seed=SEED), M, N)
+    n_glob, c0 = N * ws, N * rank
+    cfg = C.adjust_config(C.CompressionConfig(r=R, r_ov=R_OV, w=W, seed=SEED), M, n_glob)
+    comm, ops = D.Comm(), (D.DeviceOps() if ws > 1 else None)
+    counts = [N] * ws
     s = cfg.basis_cols
     st = torch.cuda.current_stream()
     sp = stream()
@@ -190,15 +200,15 @@ def run_ours(args):
     # buffers for the ADMM phase
     rng = Rng(cfg.seed)
     u0 = rng.child("init-left").uniform((M, R))
-    vt0 = rng.child("init-right").uniform((R, N), transpose=True)
+    vt0 = rng.child("init-right").uniform((R, n_glob), transpose=True)
     u, vt = u0.clone(), vt0.clone()
     du = zeros((M, R), torch.float64)
-    dvt = zeros((N, R), torch.float64)
+    dvt = zeros((n_glob, R), torch.float64)
     xc = zeros((s, R), torch.float64)
     yc = zeros((R, s), torch.float64)
     trace = zeros((MAX_ITER,), torch.float64)
     scores = zeros((MAX_ITER,), torch.float64)
-    nbytes = lib.cnmf_admm_workspace(M, N, s, R)
+    nbytes = lib.cnmf_admm_workspace(M, n_glob, s, R)
     wsb = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     it = ctypes.c_int(0)
     done = ctypes.c_int(0)
@@ -206,17 +216,24 @@ def run_ours(args):
 
     def step(ev):
         ev[0].record(st)
-        left, right, core = compressed_problem(A, cfg)
+        if ws == 1:
+            left, right, core = compressed_problem(A, cfg)
+            lp, rp = left.panel, right.panel
+        else:
+            lp, right_local, core = D.compressed_problem(ops, comm, A, M, n_glob, c0, cfg)
+            rp = comm.allgather_rows(right_local, counts)
         ev[1].record(st)
         u.copy_(u0)
         vt.copy_(vt0)
-        _lib.call("cnmf_admm_run", core.data_ptr(), left.panel.data_ptr(), M, right.panel.data_ptr(), N, s, R,
+        _lib.call("cnmf_admm_run", core.data_ptr(), lp.data_ptr(), M, rp.data_ptr(), n_glob, s, R,
                   u.data_ptr(), du.data_ptr(), vt.data_ptr(), dvt.data_ptr(), xc.data_ptr(), yc.data_ptr(), 1.0, 1.0,
                   1.0, MAX_ITER, TOL, trace.data_ptr(), scores.data_ptr(), ctypes.byref(it), ctypes.byref(done), 0,
                   0, wsb.data_ptr(), nbytes, sp)
         ev[2].record(st)
-        _lib.call("cnmf_residual_norms", A.ptr, M, N, A.lda, u.data_ptr(), None, vt.data_ptr(), R,
+        vloc = vt if ws == 1 else vt[c0: c0 + N].contiguous()
+        _lib.call("cnmf_residual_norms", A.ptr, M, N, A.lda, u.data_ptr(), None, vloc.data_ptr(), R,
                   res.data_ptr(), sp)
+        comm.allreduce(res)
         ev[3].record(st)
         return it.value
 
@@ -276,23 +293,34 @@ def run_ours(args):
                 "fp32_frac": pass_flops / (pass_avg_ms * 1e-3) / 1e12 / fp32_peak}
 
     # ---- end to end through the public API with host buffers ----
-    e2e = None
-    if rank == 0:
-        a_host = a.cpu().pin_memory()
-        cfg_pub = C.CompressionConfig(r=R, r_ov=R_OV, w=W, seed=SEED)
-        C.nmf_admm(a_host, R, cfg=cfg_pub, max_iter=MAX_ITER, tol=TOL)  # warm
+    a_host = a.cpu().pin_memory()
+    cfg_pub = C.CompressionConfig(r=R, r_ov=R_OV, w=W, seed=SEED)
+
+    def public_call():
+        if ws == 1:
+            fp = C.nmf_admm(a_host, R, cfg=cfg_pub, max_iter=MAX_ITER, tol=TOL)  # numpy out
+            return fp.X.nbytes + fp.Y.nbytes + 8 * len(fp.objective_trace), fp.rel_error, fp.iterations
+        uu, vv, it_, tr_, rel_ = D.nmf_admm(DeviceMatrix(a_host), M, n_glob, c0, R, cfg_pub, comm, ops,
+                                            max_iter=MAX_ITER, tol=TOL)
+        uh, vh = uu.cpu(), vv.cpu()
+        return uh.numel() * 8 + vh.numel() * 8 + 8 * len(tr_), rel_, it_
+
+    public_call()  # warm
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(max(1, min(args.steps, 3))):
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        d2h, rel_e2e, it_e2e = public_call()
         torch.cuda.synchronize()
-        ts = []
-        for _ in range(max(1, min(args.steps, 3))):
-            t0 = time.perf_counter()
-            fp = C.nmf_admm(a_host, R, cfg=cfg_pub, max_iter=MAX_ITER, tol=TOL)
-            torch.cuda.synchronize()
-            ts.append(time.perf_counter() - t0)
-        te = sum(ts) / len(ts)
-        d2h = fp.X.nbytes + fp.Y.nbytes + 8 * len(fp.objective_trace)
-        e2e = {"value": PASSES_CALL * a_bytes / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": a_bytes,
-               "d2h_bytes_per_step": int(d2h), "ms": te * 1e3, "rel_error": fp.rel_error,
-               "iterations": fp.iterations}
+        ts.append(time.perf_counter() - t0)
+    te_t = torch.tensor([sum(ts) / len(ts)], device="cuda", dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
+    te = te_t.item()
+    e2e = {"value": ws * PASSES_CALL * a_bytes / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": a_bytes,
+           "d2h_bytes_per_step": int(d2h), "ms": te * 1e3, "rel_error": rel_e2e, "iterations": it_e2e}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -309,7 +337,8 @@ def run_ours(args):
                 "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f32", "precision": "f32 passes over A; f64 Gram, Cholesky and ADMM state", "data": "synthetic",
-                "config": config_block({"compress_ms": comp_ms, "admm_ms": admm_ms, "resid_ms": resid_ms,
+                "config": config_block({"n_global": n_glob, "compress_ms": comp_ms, "admm_ms": admm_ms,
+                                        "resid_ms": resid_ms,
                                         "hbm_frac_compress": value / ws / hbm_peak}),
                 "nmf_iters_per_s": iters_per_s, "admm_iterations": iters[0],
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
