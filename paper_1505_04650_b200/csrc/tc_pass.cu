@@ -204,10 +204,19 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
 // [hi; lo]) released by the MMA commit; TMEM ring of split A tiles (hi and lo,
 // 32 columns each, lane = output row) filled with tcgen05.st and consumed by
 // A-from-TMEM MMAs; double-buffered TMEM accumulators.
+// Split-K launches reduce shared output tiles with red.global.add, so the
+// output must start at zero: every CTA zeroes its slice of rows at start-up
+// and counts itself in `arrived`; an epilogue polls the count before its
+// first reduction (long satisfied by then). The last CTA to finish resets
+// the pair for the next launch that draws this slot.
+struct ZSync {
+  unsigned arrived, finished;
+};
+
 template <int S, bool TRANS>
 __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
     pass_tc(const __grid_constant__ TmaDesc tA, const __grid_constant__ TmaDesc tB, float* __restrict__ out,
-            int64_t P, int nt, int64_t nblocks, int whole) {
+            int64_t P, int nt, int64_t nblocks, int whole, ZSync* __restrict__ zs) {
   using C = TcCfg<S, TRANS>;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* sP = smem + C::ST * C::STAGE;                 // [SSP][BSPL]
@@ -251,9 +260,21 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
                  "n"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // programmatic dependent launch: everything above overlapped the tail of
+  // the previous kernel in the stream; its outputs are visible from here on
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (zs != nullptr) {
+    const int64_t z0 = b * P / G, z1 = (b + 1) * P / G;
+    float4* o4 = reinterpret_cast<float4*>(out + z0 * S);
+    for (int64_t i = threadIdx.x; i < (z1 - z0) * S / 4; i += blockDim.x) o4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (zs != nullptr && threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&zs->arrived, 1u);
+  }
   const uint32_t tmem = *tmem_slot;
 
   // Every role walks the same unit sequence u0..u1-1 with incremental
@@ -323,6 +344,15 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
         const int64_t t0 = ob * nt;  // first unit of this output tile
         const bool owned = (t0 >= u0) && (t0 + nt <= u1);
         const int64_t row = ob * BMT + row_in_tile;
+        if (!owned && zs != nullptr) {  // every CTA's zeroing must have landed
+          if (lane == 0) {
+            unsigned v;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&zs->arrived) : "memory");
+            } while (v < gridDim.x);
+          }
+          __syncwarp();
+        }
         if (row < P) {
           float* dst = out + row * S + cg;
 #pragma unroll
@@ -499,6 +529,10 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   TC_SPAN(1);
+  if (zs != nullptr && threadIdx.x == 0 && atomicAdd(&zs->finished, 1u) == gridDim.x - 1) {
+    zs->arrived = 0u;
+    zs->finished = 0u;
+  }
   if (warp == kWarpMma)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
 }
@@ -519,7 +553,16 @@ int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bp
   const int64_t nblocks = ceil_div(P, BMT);
   const int whole = nblocks >= 16 * kNumSMs;
   const int64_t grid = std::min<int64_t>(kNumSMs, whole ? nblocks : nblocks * nt);
-  if (!whole) CNMF_CUDA(cudaMemsetAsync(out, 0, (size_t)P * S * 4, st));
+  ZSync* zs = nullptr;
+  if (!whole) {
+    static ZSync* ring = nullptr;
+    static unsigned next = 0;
+    if (ring == nullptr) {
+      CNMF_CUDA(cudaMalloc(&ring, 64 * sizeof(ZSync)));
+      CNMF_CUDA(cudaMemset(ring, 0, 64 * sizeof(ZSync)));
+    }
+    zs = ring + (next++ % 64);
+  }
   static bool attr = false;
   if (!attr) {
     CNMF_CUDA(cudaFuncSetAttribute(pass_tc<S, TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -531,7 +574,17 @@ int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bp
     CNMF_CUDA(cudaEventCreate(&e1));
     CNMF_CUDA(cudaEventRecord(e0, st));
   }
-  pass_tc<S, TRANS><<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(tA, tB, out, P, nt, nblocks, whole);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)grid);
+  lc.blockDim = dim3(C::THREADS);
+  lc.dynamicSmemBytes = C::SMEM;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  CNMF_CUDA(cudaLaunchKernelEx(&lc, pass_tc<S, TRANS>, tA, tB, out, P, nt, nblocks, whole, zs));
   CNMF_LAUNCH_CHECK();
   if (e0) {
     CNMF_CUDA(cudaEventRecord(e1, st));

@@ -7,9 +7,9 @@
 #include <cstdlib>
 
 int main(int argc, char** argv) {
-  const int64_t M = 20000, N = 10000;
   const int S = argc > 1 ? atoi(argv[1]) : 32;
   const bool trn = argc > 2 && atoi(argv[2]);
+  const int64_t M = argc > 3 ? atoll(argv[3]) : 20000, N = argc > 4 ? atoll(argv[4]) : 10000;
   float *A, *X, *Y;
   cudaMalloc(&A, M * N * 4);
   cudaMemset(A, 0, M * N * 4);
