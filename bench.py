@@ -244,9 +244,10 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
 
+    import paper_1505_04650_b200.nmf as nmf_mod
+
     clocks = Clocks(local)
-    lib.cnmf_set_pass_profiling(1)
-    launches0 = lib.cnmf_launch_count()
+    launches0 = lib.cnmf_launch_count() + nmf_mod.graph_launches
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
@@ -254,8 +255,17 @@ def run_ours(args):
     iters = [step(ev) for ev in evs]
     t_end.record(st)
     torch.cuda.synchronize()
-    launches = lib.cnmf_launch_count() - launches0
+    launches = lib.cnmf_launch_count() + nmf_mod.graph_launches - launches0
     ck = clocks.stop()
+    # the dominant kernel timed live: one more compression, launched eagerly
+    # (graph replays bypass the per-launch events), CUDA events around every
+    # streaming pass on its launch stream
+    lib.cnmf_set_pass_profiling(1)
+    if ws == 1:
+        compressed_problem(A, cfg, graph=False)
+    else:
+        D.compressed_problem(ops, comm, A, M, n_glob, c0, cfg)
+    torch.cuda.synchronize()
     pms, pl, pby = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
     lib.cnmf_pass_stats(ctypes.byref(pms), ctypes.byref(pl), ctypes.byref(pby))
     lib.cnmf_set_pass_profiling(0)

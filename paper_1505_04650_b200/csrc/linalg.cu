@@ -26,7 +26,7 @@ int pass_forward(const float*, int64_t, int64_t, int64_t, const float*, int, flo
 int pass_transpose(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
 int panel_finalize(float*, int64_t, int, const double*, double*, cudaStream_t);
 int panel_finalize_chol(float*, int64_t, int, const double*, double*, int, double*, double*, int*, int, unsigned*,
-                        cudaStream_t);
+                        cudaStream_t, int apply_after = 0);
 int gaussian_fill_ws(uint64_t, int64_t, int64_t, int64_t, int, void*, int64_t, void*, size_t, cudaStream_t);
 size_t gaussian_workspace(int64_t, int64_t, int64_t);
 
@@ -42,7 +42,9 @@ __global__ void __launch_bounds__(512) chol_inv_kernel(const double* G, int s, i
 __global__ void init_info(int* info) {
   info[0] = 0;
   info[1] = 1 << 30;
-  info[4] = 0;  // last-block counter of the fused finalize + factor kernel
+  info[4] = 0;  // counters of the fused finalize + factor (+ apply) kernel
+  info[5] = 0;
+  info[6] = 0;
 }
 
 }  // namespace
@@ -91,8 +93,7 @@ static Scratch carve_small(void* base, int S) {
 static int finish_basis(float* P, int64_t rows, int s, int S, Scratch sc, double* Rfinal, int first_pass_id,
                         cudaStream_t st) {
   CNMF_TRY(panel_finalize_chol(P, rows, S, nullptr, sc.G, s, sc.T, Rfinal, sc.info, first_pass_id, sc.counter,
-                               st));
-  CNMF_TRY(panel_finalize(P, rows, S, sc.T, nullptr, st));
+                               st, 1));
   return CNMF_OK;
 }
 
@@ -164,8 +165,7 @@ int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s
   // so the second (polishing) sweep runs only once, on the final basis.
   auto orth_sweep = [&]() -> int {
     CNMF_TRY(panel_finalize_chol(cur, cur_rows, S, nullptr, sc.G, s, sc.T, nullptr, sc.info, pass_id, sc.counter,
-                                 st));
-    CNMF_TRY(panel_finalize(cur, cur_rows, S, sc.T, nullptr, st));
+                                 st, 1));
     return CNMF_OK;
   };
   CNMF_TRY(orth_sweep());
@@ -206,8 +206,7 @@ int orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws
   init_info<<<1, 1, 0, st>>>(sc.info);
   CNMF_LAUNCH_CHECK();
   CNMF_CUDA(cudaMemsetAsync(sc.G, 0, (size_t)S * S * 8, st));
-  CNMF_TRY(panel_finalize_chol(P, rows, S, nullptr, sc.G, s, sc.T, nullptr, sc.info, 0, sc.counter, st));
-  CNMF_TRY(panel_finalize(P, rows, S, sc.T, nullptr, st));
+  CNMF_TRY(panel_finalize_chol(P, rows, S, nullptr, sc.G, s, sc.T, nullptr, sc.info, 0, sc.counter, st, 1));
   CNMF_TRY(finish_basis(P, rows, s, S, sc, R, 0, st));
   return check_info(sc.info, "orthonormalize", st);
 }

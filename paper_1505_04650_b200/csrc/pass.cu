@@ -299,7 +299,7 @@ template <int S>
 __global__ void __launch_bounds__(kThreads, 2)
     finalize_panel(float* __restrict__ P, int64_t rows, const double* T, double* __restrict__ G, int s,
                    double* Tout, double* __restrict__ Rout, int* __restrict__ info, int pass_id,
-                   unsigned* __restrict__ counter) {
+                   unsigned* __restrict__ counter, int apply_after) {
   constexpr int TR = 64;
   constexpr int NB = S / 4;                  // 4-wide blocks per side
   constexpr int NBLK = NB * (NB + 1) / 2;    // upper-triangular 4x4 blocks
@@ -413,10 +413,61 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  chol_small(G, s, S, Tout, Rout, info, pass_id, reinterpret_cast<double*>(fsm));
-  if (threadIdx.x == 0) *counter = 0u;
+  if (s_last) {
+    __threadfence();
+    chol_small(G, s, S, Tout, Rout, info, pass_id, reinterpret_cast<double*>(fsm));
+    if (!apply_after) {
+      if (threadIdx.x == 0) *counter = 0u;
+      return;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicExch(counter + 1, 1u);  // R^{-1} published
+  } else {
+    if (!apply_after) return;
+    // cooperative launch: every block is resident, so waiting here is safe
+    if (threadIdx.x == 0) {
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter + 1) : "memory");
+      } while (v == 0u);
+    }
+    __syncthreads();
+  }
+  // P <- P R^{-1}: a block that owns a single tile still has it in sIn
+  // (unless it ran the factorisation, which used the shared memory)
+  for (int i = tid; i < S * S; i += kThreads) sT[i] = (float)__ldcg(Tout + i);
+  const bool kept = !s_last && (int64_t)gridDim.x * TR >= rows;
+  for (int64_t t0 = (int64_t)blockIdx.x * TR; t0 < rows; t0 += (int64_t)gridDim.x * TR) {
+    const int nr = (int)min64(TR, rows - t0);
+    if (!kept) {
+      __syncthreads();
+      for (int i = tid; i < TR * S / 4; i += kThreads) {
+        const int r = (i * 4) / S;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < nr) v = *(const float4*)(P + t0 * S + 4 * (int64_t)i);
+        *(float4*)(sIn + 4 * i) = v;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < TR * S; i += kThreads) {
+      const int r = i / S, c = i % S;
+      float acc = 0.f;
+      for (int j = 0; j <= c; ++j) acc = fmaf(sIn[r * S + j], sT[j * S + c], acc);
+      sOut[i] = acc;
+    }
+    __syncthreads();
+    for (int i = tid; i < TR * S / 4; i += kThreads) {
+      const int r = (i * 4) / S;
+      if (r < nr) *(float4*)(P + t0 * S + 4 * (int64_t)i) = *(const float4*)(sOut + 4 * i);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(counter + 2, 1u) == gridDim.x - 1) {
+    counter[0] = 0u;
+    counter[1] = 0u;
+    counter[2] = 0u;
+  }
 }
 
 template <int S>
@@ -486,7 +537,7 @@ int launch_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const fl
 
 template <int S>
 int launch_finalize(float* P, int64_t rows, const double* T, double* G, int s, double* Tout, double* Rout, int* info,
-                    int pass_id, unsigned* counter, cudaStream_t st) {
+                    int pass_id, unsigned* counter, cudaStream_t st, int apply_after = 0) {
   constexpr int NB = S / 4, NBLK = NB * (NB + 1) / 2;
   constexpr int GROUPS = (NBLK >= kThreads) ? 1 : kThreads / NBLK;
   constexpr size_t fin = (size_t)(S * S + 2 * 64 * S) * 4 + (GROUPS > 1 ? (size_t)GROUPS * NBLK * 16 * 8 : 0);
@@ -506,7 +557,22 @@ int launch_finalize(float* P, int64_t rows, const double* T, double* G, int s, d
   }
   const int64_t tiles = ceil_div(rows, 64);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)per_sm * kNumSMs));
-  finalize_panel<S><<<grid, kThreads, smem, st>>>(P, rows, T, G, s, Tout, Rout, info, pass_id, counter);
+  if (apply_after) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CNMF_CUDA(cudaLaunchKernelEx(&lc, finalize_panel<S>, P, rows, T, G, s, Tout, Rout, info, pass_id, counter,
+                                 apply_after));
+  } else {
+    finalize_panel<S><<<grid, kThreads, smem, st>>>(P, rows, T, G, s, Tout, Rout, info, pass_id, counter, 0);
+  }
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }
@@ -567,14 +633,15 @@ int panel_finalize(float* P, int64_t rows, int S, const double* T, double* G, cu
 }
 
 // P <- P Tin (optional), G = P^T P, then Tout = R^{-1} of G = R^T R in the
-// same launch (last-block Cholesky). `counter` must be zero on entry and is
-// left zero.
+// same launch (last-block Cholesky); with `apply_after` the blocks then wait
+// for Tout (cooperative launch) and apply it: one full CholeskyQR sweep per
+// launch. counter[0..2] must be zero on entry and are left zero.
 int panel_finalize_chol(float* P, int64_t rows, int S, const double* Tin, double* G, int s, double* Tout,
-                        double* Rout, int* info, int pass_id, unsigned* counter, cudaStream_t st) {
+                        double* Rout, int* info, int pass_id, unsigned* counter, cudaStream_t st, int apply_after) {
   switch (S) {
-    case 32: return launch_finalize<32>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st);
-    case 64: return launch_finalize<64>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st);
-    case 128: return launch_finalize<128>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st);
+    case 32: return launch_finalize<32>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st, apply_after);
+    case 64: return launch_finalize<64>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st, apply_after);
+    case 128: return launch_finalize<128>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st, apply_after);
   }
   return fail(CNMF_ERR_ARGUMENT, "panel width must be 32, 64 or 128");
 }

@@ -516,7 +516,31 @@ static void CUDART_CB tail_fixup(void* p) {
 }
 
 // ring of mapped pinned slots (reused round-robin; a slot is rewritten only
-// eight fills later, long after its stream work retired)
+// eight fills later, long after its stream work retired). A slot that must
+// grow grows the whole ring, so a fill captured into a CUDA graph right after
+// an eager fill of the same size never allocates (allocation is illegal
+// during capture).
+static bool grow_slot(TailSlot& s, unsigned int cap) {
+  if (s.recs) cudaFreeHost(s.recs);
+  s.recs = nullptr;
+  s.cap = 0;
+  const size_t bytes = (size_t)cap * (sizeof(TailRec) + 16) + 64;
+  char* h = nullptr;
+  if (cudaHostAlloc((void**)&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return false;
+  char* d = nullptr;
+  if (cudaHostGetDevicePointer((void**)&d, h, 0) != cudaSuccess) return false;
+  s.recs = (TailRec*)h;
+  s.vals = (double*)(h + (size_t)cap * sizeof(TailRec));
+  s.offs = (int64_t*)(h + (size_t)cap * (sizeof(TailRec) + 8));
+  s.count = (unsigned int*)(h + (size_t)cap * (sizeof(TailRec) + 16));
+  s.d_recs = (TailRec*)d;
+  s.d_vals = (double*)(d + (size_t)cap * sizeof(TailRec));
+  s.d_offs = (int64_t*)(d + (size_t)cap * (sizeof(TailRec) + 8));
+  s.d_count = (unsigned int*)(d + (size_t)cap * (sizeof(TailRec) + 16));
+  s.cap = cap;
+  return true;
+}
+
 static TailSlot* tail_slot(unsigned int cap) {
   static std::mutex mu;
   static TailSlot ring[8];
@@ -524,21 +548,8 @@ static TailSlot* tail_slot(unsigned int cap) {
   std::lock_guard<std::mutex> lk(mu);
   TailSlot& s = ring[next++ % 8];
   if (s.cap < cap) {
-    if (s.recs) cudaFreeHost(s.recs);
-    const size_t bytes = (size_t)cap * (sizeof(TailRec) + 16) + 64;
-    char* h = nullptr;
-    if (cudaHostAlloc((void**)&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
-    char* d = nullptr;
-    if (cudaHostGetDevicePointer((void**)&d, h, 0) != cudaSuccess) return nullptr;
-    s.recs = (TailRec*)h;
-    s.vals = (double*)(h + (size_t)cap * sizeof(TailRec));
-    s.offs = (int64_t*)(h + (size_t)cap * (sizeof(TailRec) + 8));
-    s.count = (unsigned int*)(h + (size_t)cap * (sizeof(TailRec) + 16));
-    s.d_recs = (TailRec*)d;
-    s.d_vals = (double*)(d + (size_t)cap * sizeof(TailRec));
-    s.d_offs = (int64_t*)(d + (size_t)cap * (sizeof(TailRec) + 8));
-    s.d_count = (unsigned int*)(d + (size_t)cap * (sizeof(TailRec) + 16));
-    s.cap = cap;
+    for (auto& t : ring)
+      if (t.cap < cap && !grow_slot(t, cap)) return nullptr;
   }
   return &s;
 }

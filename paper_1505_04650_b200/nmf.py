@@ -10,6 +10,8 @@ the true relative error from one fused residual pass over A (nmf.py:53-75).
 """
 
 import ctypes
+import os
+from collections import OrderedDict
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -17,7 +19,7 @@ import torch
 
 from . import _lib
 from .compress import CompressionConfig, _check, _compress, adjust_config
-from .device import DeviceMatrix, as_device64, out, stream, zeros
+from .device import MASK64, DeviceMatrix, as_device64, out, stream, zeros
 from .errors import ArgumentError, DivergenceError, UndefinedMetricError
 from .rng import Rng, child_seed
 
@@ -77,9 +79,7 @@ def _rel_error(A, X, Yt):
     return float(np.sqrt(max(num, 0.0) / den))
 
 
-def compressed_problem(A, cfg, check=True):
-    """Bases and core for the compressed ADMM (nmf.py:120-135, 327-332),
-    enqueued back to back; one status check at the end."""
+def _enqueue_problem(A, cfg):
     left, _ = _compress(A, replace(cfg, seed=child_seed(cfg.seed, "left-basis")), 0, check=False)
     right, _ = _compress(A, replace(cfg, seed=child_seed(cfg.seed, "right-basis")), 1, check=False)
     s = cfg.basis_cols
@@ -88,6 +88,55 @@ def compressed_problem(A, cfg, check=True):
     _lib.call("cnmf_pass_transpose", A.ptr, A.m, A.n, A.lda, left.panel.data_ptr(), s, z.data_ptr(), stream())
     core = zeros((S, S), dtype=torch.float64)
     _lib.call("cnmf_panel_cross", z.data_ptr(), right.panel.data_ptr(), A.n, S, core.data_ptr(), stream())
+    return left, right, core, z
+
+
+# CUDA graphs of the whole compressed problem (2 x (2q+1) passes, their
+# CholeskyQR sweeps, the seeded test matrices and the core projection: ~60
+# launches) for device-resident A, keyed by everything the launches bake in:
+# A's address and shape, the basis width, q and the seed. A replay reuses the graph's own
+# output buffers, so the returned bases are valid until the next call with
+# the same key. CNMF_GRAPHS=0 runs the launches eagerly.
+_GRAPHS = OrderedDict()
+_GRAPHS_MAX = 4
+graph_launches = 0  # library kernels launched through graph replays (cnmf_launch_count sees captures only)
+
+
+def _graphs_enabled():
+    return os.environ.get("CNMF_GRAPHS", "1") != "0"
+
+
+def compressed_problem(A, cfg, check=True, graph=None):
+    """Bases and core for the compressed ADMM (nmf.py:120-135, 327-332),
+    enqueued back to back (replayed as one CUDA graph unless graph=False or
+    CNMF_GRAPHS=0); one status check at the end."""
+    # host inputs land in a fresh device buffer per call: a graph keyed on its
+    # address would be re-captured every time, so they run eagerly
+    use_graph = (_graphs_enabled() and not A.on_host) if graph is None else graph
+    if use_graph and not torch.cuda.is_current_stream_capturing():
+        key = (A.ptr, A.m, A.n, A.lda, cfg.basis_cols, cfg.w, cfg.seed & MASK64, torch.cuda.current_device())
+        ent = _GRAPHS.get(key)
+        if ent is None:
+            _enqueue_problem(A, cfg)  # initialises the library's one-time launch state
+            torch.cuda.current_stream().synchronize()
+            lib = _lib.load()
+            g = torch.cuda.CUDAGraph()
+            n0 = lib.cnmf_launch_count()
+            with torch.cuda.graph(g):
+                left, right, core, z = _enqueue_problem(A, cfg)
+            ent = (g, left, right, core, z, lib.cnmf_launch_count() - n0)
+            _GRAPHS[key] = ent
+            while len(_GRAPHS) > _GRAPHS_MAX:
+                _GRAPHS.popitem(last=False)
+        else:
+            _GRAPHS.move_to_end(key)
+        g, left, right, core, _, nk = ent
+        g.replay()
+        global graph_launches
+        graph_launches += nk
+    else:
+        left, right, core, _ = _enqueue_problem(A, cfg)
+    s = cfg.basis_cols
     if check:
         _check(left)
         _check(right)
