@@ -91,9 +91,9 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes,
 }
 
 // kind::tf32 instruction descriptor: D fp32, A/B tf32, M = 128, N given.
-__host__ __device__ constexpr uint32_t idesc_tf32(int n, bool a_mn_major, bool b_mn_major) {
+__host__ __device__ constexpr uint32_t idesc_tf32(int n, bool a_mn_major, bool b_mn_major, int m = BMT) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
-         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BMT >> 4) << 24);
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 // Round to the nearest tf32 value (10 explicit mantissa bits, ties away from
@@ -134,7 +134,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #define TC_TRACE(slot)                                                          \
   do {                                                                          \
-    if (blockIdx.x == 0 && it < 64) g_tc_trace[it][slot] = clock64();           \
+    if (blockIdx.x == CNMF_TC_TRACE_CTA && it < 64) g_tc_trace[it][slot] = clock64();           \
   } while (0)
 #else
 #define TC_TRACE(slot) \
@@ -145,16 +145,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
-template <int S, bool TRANS>
+template <int S, bool TRANS, bool PAIR = false>
 struct TcCfg {
   static constexpr int ABYTES = BMT * BKT * 4;        // 16 KB raw A tile
   static constexpr int BRAW = BKT * S * 4;            // raw fp32 panel tile [32 k][S]: 4 or 8 KB
   static constexpr int STAGE = ABYTES + BRAW;         // one TMA stage: A tile + its panel tile
-  static constexpr int BSPL = BKT * 2 * S * 4;        // split K-major SW128 [hi; lo] panel: 8 or 16 KB
-  static constexpr int ST = (S == 32) ? 10 : 7;       // stage ring depth (DRAM bytes in flight per SM)
-  static constexpr int SSP = 3;                       // split panel ring
-  static constexpr int AST = 4;                       // TMEM ring of split A tiles
-  static constexpr int MD = 4;                        // "MMA of K tile j done" ring (>= SSP, AST)
+  // split K-major SW128 panel slot: [hi; lo] (2S rows), or for a CTA pair this
+  // CTA's halves of the two MMAs' B operands: [hi or lo (S rows); hi half (S/2 rows)]
+  static constexpr int BSPL = PAIR ? BKT * (S + S / 2) * 4 : BKT * 2 * S * 4;
+  // ring depths: a CTA pair's cross-CTA arrivals add ~1 us of latency to the
+  // panel and TMEM rings, so those are deeper there
+  static constexpr int ST = (S == 32) ? (PAIR ? 9 : 10) : 7;  // stage ring (DRAM bytes in flight per SM)
+  static constexpr int SSP = PAIR ? (S == 32 ? 6 : 4) : 3;    // split panel ring
+  static constexpr int AST = PAIR && S == 32 ? 6 : 4;         // TMEM ring of split A tiles
+  static constexpr int MD = SSP > AST ? SSP : AST;    // "MMA of K tile j done" ring (>= SSP, AST)
   static constexpr int KB = 2;                        // K tiles per tensor-core accumulation block
   static_assert(MD >= SSP && MD >= AST, "one MMA-done ring serves both consumers");
   static constexpr int ACC_COLS = 2 * S;              // per accumulator buffer
@@ -182,6 +186,51 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint
       "}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_ts2(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// commit to the same barrier (shared-memory offset) in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+
+// arrive on the barrier at the same offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+
+// wait with cluster-scope acquire (arrivals come from both CTAs of a pair)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // 32 lanes x 16 consecutive 32-bit columns per warp
@@ -213,11 +262,20 @@ struct ZSync {
   unsigned arrived, finished;
 };
 
-template <int S, bool TRANS>
-__global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
+//
+// PAIR: a cluster of two CTAs on one TPC shares every MMA (cta_group::2,
+// M = 256): each CTA splits its own 128 rows of A into its own TMEM and
+// provides half of each B operand ([X_hi | X_lo]: CTA 0 the hi columns, CTA 1
+// the lo columns; X_hi for the correction MMA: one half each), CTA 0 issues
+// the MMAs and commits to both CTAs' barriers. Half the MMA instructions and
+// half the panel splitting per SM.
+template <int S, bool TRANS, bool PAIR>
+__global__ void __launch_bounds__(TcCfg<S, TRANS, PAIR>::THREADS, 1)
     pass_tc(const __grid_constant__ TmaDesc tA, const __grid_constant__ TmaDesc tB, float* __restrict__ out,
             int64_t P, int nt, int64_t nblocks, int whole, ZSync* __restrict__ zs) {
-  using C = TcCfg<S, TRANS>;
+  using C = TcCfg<S, TRANS, PAIR>;
+  constexpr int CW = PAIR ? 2 : 1;          // CTAs per work item
+  constexpr int TILE_ROWS = CW * BMT;       // output rows per work item
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* sP = smem + C::ST * C::STAGE;                 // [SSP][BSPL]
   uint64_t* full = (uint64_t*)(sP + C::SSP * C::BSPL);         // [ST] stage landed
@@ -230,11 +288,12 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t U = nblocks * nt, G = gridDim.x, b = blockIdx.x;
+  const uint32_t rank = PAIR ? (blockIdx.x & 1) : 0;  // cluster dims (2, 1, 1)
+  const int64_t U = nblocks * nt, G = gridDim.x / CW, b = blockIdx.x / CW;
   const int64_t u0 = whole ? (b * nblocks / G) * nt : b * U / G;
   const int64_t u1 = whole ? ((b + 1) * nblocks / G) * nt : (b + 1) * U / G;
   const int64_t ntiles = u1 - u0;
-  if (ntiles <= 0) return;
+  if (!PAIR && ntiles <= 0) return;  // (pairs always have work: grid <= units)
   TC_SPAN(0);
 
   if (threadIdx.x == 0) {
@@ -245,31 +304,40 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
       mbar_init(&empty[s], C::NSPLIT + C::NPW);
     }
     for (int s = 0; s < C::SSP; ++s) {
-      mbar_init(&pfull[s], C::NPW);
+      mbar_init(&pfull[s], CW * C::NPW);
     }
-    for (int s = 0; s < C::AST; ++s) mbar_init(&afull[s], C::NSPLIT);
+    for (int s = 0; s < C::AST; ++s) mbar_init(&afull[s], CW * C::NSPLIT);
     for (int s = 0; s < C::MD; ++s) mbar_init(&mdone[s], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], C::NEPI);
+      mbar_init(&tempty[i], CW * C::NEPI);
     }
     fence_barrier_init();
   }
   if (warp == kWarpMma) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(C::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   // programmatic dependent launch: everything above overlapped the tail of
   // the previous kernel in the stream; its outputs are visible from here on
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (zs != nullptr) {
-    const int64_t z0 = b * P / G, z1 = (b + 1) * P / G;
+    const int64_t z0 = blockIdx.x * P / gridDim.x, z1 = (blockIdx.x + 1) * P / gridDim.x;
     float4* o4 = reinterpret_cast<float4*>(out + z0 * S);
     for (int64_t i = threadIdx.x; i < (z1 - z0) * S / 4; i += blockDim.x) o4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();  // both CTAs' barriers initialised before any remote arrival
+  else
+    __syncthreads();
   tc_fence_after();
   if (zs != nullptr && threadIdx.x == 0) {
     __threadfence();
@@ -294,10 +362,11 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
         TC_TRACE(0);
         unsigned char* dst = smem + r.i * C::STAGE;
         mbar_arrive_expect_tx(&full[r.i], C::STAGE);
-        if (!TRANS)  // A rows [ob*128, +128), cols [kt*32, +32): K-major SW128
-          tma_load_2d(dst, &tA, &full[r.i], kt * BKT, (int)(ob * BMT));
-        else         // A rows [kt*32, +32) (K), cols [ob*128, +128) (M): row-major
-          tma_load_2d(dst, &tA, &full[r.i], (int)(ob * BMT), kt * BKT);
+        const int row0 = (int)(ob * TILE_ROWS + rank * BMT);  // this CTA's 128 output rows
+        if (!TRANS)  // A rows [row0, +128), cols [kt*32, +32): K-major SW128
+          tma_load_2d(dst, &tA, &full[r.i], kt * BKT, row0);
+        else         // A rows [kt*32, +32) (K), cols [row0, +128) (M): row-major
+          tma_load_2d(dst, &tA, &full[r.i], row0, kt * BKT);
         // panel rows [kt*32, +32) (K), all S columns: row-major [32][S]
         tma_load_2d(dst + C::ABYTES, &tB, &full[r.i], 0, kt * BKT);
         r.next();
@@ -337,13 +406,18 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[racc.i]);
+        if (lane == 0) {
+          if (PAIR && rank != 0)
+            mbar_arrive_remote(&tempty[racc.i], 0);
+          else
+            mbar_arrive(&tempty[racc.i]);
+        }
         racc.next();
       }
       if (tile_end) {
         const int64_t t0 = ob * nt;  // first unit of this output tile
         const bool owned = (t0 >= u0) && (t0 + nt <= u1);
-        const int64_t row = ob * BMT + row_in_tile;
+        const int64_t row = ob * TILE_ROWS + rank * BMT + row_in_tile;
         if (!owned && zs != nullptr) {  // every CTA's zeroing must have landed
           if (lane == 0) {
             unsigned v;
@@ -412,23 +486,41 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
         for (int cc = 0; cc < 4; ++cc) {
           const int c = 4 * (u & 1) + cc;
           const uint32_t off = (uint32_t)n * 128 + ((c ^ (n & 7)) << 4);
-          *(float4*)(dst + off) = make_float4(h[t][4 * cc], h[t][4 * cc + 1], h[t][4 * cc + 2], h[t][4 * cc + 3]);
-          *(float4*)(dst + S * 128 + off) =
-              make_float4(l[t][4 * cc], l[t][4 * cc + 1], l[t][4 * cc + 2], l[t][4 * cc + 3]);
+          const float4 hv = make_float4(h[t][4 * cc], h[t][4 * cc + 1], h[t][4 * cc + 2], h[t][4 * cc + 3]);
+          const float4 lv = make_float4(l[t][4 * cc], l[t][4 * cc + 1], l[t][4 * cc + 2], l[t][4 * cc + 3]);
+          if constexpr (PAIR) {
+            // B of the [hi | lo] MMA: CTA 0 holds the hi rows, CTA 1 the lo rows;
+            // B of the correction MMA (X_hi): rows [rank S/2, +S/2) of X_hi
+            *(float4*)(dst + off) = rank == 0 ? hv : lv;
+            const int n2 = n - (int)rank * (S / 2);
+            if (n2 >= 0 && n2 < S / 2) {
+              const uint32_t off2 = (uint32_t)n2 * 128 + ((c ^ (n2 & 7)) << 4);
+              *(float4*)(dst + S * 128 + off2) = hv;
+            }
+          } else {
+            *(float4*)(dst + off) = hv;
+            *(float4*)(dst + S * 128 + off) = lv;
+          }
         }
       }
       if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(12);
       fence_proxy_async();  // generic-proxy stores -> tensor-core (async proxy) reads
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pfull[rp.i]);
+      if (lane == 0) {
+        if (PAIR && rank != 0)
+          mbar_arrive_remote(&pfull[rp.i], 0);
+        else
+          mbar_arrive(&pfull[rp.i]);
+      }
       if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(9);
       r.next();
       rp.next();
     }
   } else if (warp == kWarpMma) {
-    // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc_cat = idesc_tf32(2 * S, false, false);
-    constexpr uint32_t idesc_hi = idesc_tf32(S, false, false);
+    // ---------------- MMA issuer (CTA 0 of a pair) ----------------
+    if (PAIR && rank != 0) goto done;
+    constexpr uint32_t idesc_cat = idesc_tf32(2 * S, false, false, CW * BMT);
+    constexpr uint32_t idesc_hi = idesc_tf32(S, false, false, CW * BMT);
     Ring<C::SSP> rp;
     Ring<C::AST> ra;
     Ring<C::MD> rd;
@@ -439,9 +531,15 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
       const bool tile_end = (it == ntiles - 1) || (kt == nt - 1);
       const bool block_end = tile_end || ((kt + 1) % C::KB == 0);
       // reuse of an accumulator buffer waits until the epilogue drained it
-      if (block_start && racc.wrapped) mbar_wait(&tempty[racc.i], racc.ph ^ 1);
-      mbar_wait(&pfull[rp.i], rp.ph);
-      mbar_wait(&afull[ra.i], ra.ph);
+      if constexpr (PAIR) {
+        if (block_start && racc.wrapped) mbar_wait_cluster(&tempty[racc.i], racc.ph ^ 1);
+        mbar_wait_cluster(&pfull[rp.i], rp.ph);
+        mbar_wait_cluster(&afull[ra.i], ra.ph);
+      } else {
+        if (block_start && racc.wrapped) mbar_wait(&tempty[racc.i], racc.ph ^ 1);
+        mbar_wait(&pfull[rp.i], rp.ph);
+        mbar_wait(&afull[ra.i], ra.ph);
+      }
       tc_fence_after();
       if (lane == 0) TC_TRACE(4);
       if (elect_one()) {
@@ -454,11 +552,22 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
         for (int k = 0; k < BKT / 8; ++k) {
           const uint64_t bcat = smem_desc(sb + 32 * k, 16, 1024);  // 8 tf32 = 32 B per K step
           const uint32_t acc = (block_start && k == 0) ? 0u : 1u;
-          tc_mma_ts(dcat, ahi + 8 * k, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
-          tc_mma_ts(dlo, alo + 8 * k, bcat, idesc_hi, 1u);     //            + A_lo X_hi
+          if constexpr (PAIR) {
+            const uint64_t bhi = smem_desc(sb + S * 128 + 32 * k, 16, 1024);
+            tc_mma_ts2(dcat, ahi + 8 * k, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
+            tc_mma_ts2(dlo, alo + 8 * k, bhi, idesc_hi, 1u);      //            + A_lo X_hi
+          } else {
+            tc_mma_ts(dcat, ahi + 8 * k, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
+            tc_mma_ts(dlo, alo + 8 * k, bcat, idesc_hi, 1u);     //            + A_lo X_hi
+          }
         }
-        tc_commit(&mdone[rd.i]);  // one commit releases the split panel and the TMEM A slot
-        if (block_end) tc_commit(&tfull[racc.i]);
+        if constexpr (PAIR) {
+          tc_commit_pair(&mdone[rd.i]);  // releases the panel slot and the TMEM A slot in both CTAs
+          if (block_end) tc_commit_pair(&tfull[racc.i]);
+        } else {
+          tc_commit(&mdone[rd.i]);  // one commit releases the split panel and the TMEM A slot
+          if (block_end) tc_commit(&tfull[racc.i]);
+        }
         TC_TRACE(5);
       }
       __syncwarp();
@@ -519,14 +628,23 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&afull[ra.i]);
+      if (lane == 0) {
+        if (PAIR && rank != 0)
+          mbar_arrive_remote(&afull[ra.i], 0);
+        else
+          mbar_arrive(&afull[ra.i]);
+      }
       if (threadIdx.x == 64) TC_TRACE(3);
       r.next();
       ra.next();
     }
   }
+done:
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();  // the peer's TMEM and barriers stay alive until CTA 0's MMAs retired
+  else
+    __syncthreads();
   tc_fence_after();
   TC_SPAN(1);
   if (zs != nullptr && threadIdx.x == 0 && atomicAdd(&zs->finished, 1u) == gridDim.x - 1) {
@@ -534,12 +652,25 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS>::THREADS, 1)
     zs->finished = 0u;
   }
   if (warp == kWarpMma)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  {
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  }
 }
 
-template <int S, bool TRANS>
-int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bpanel, float* out, cudaStream_t st) {
-  using C = TcCfg<S, TRANS>;
+// CTA-pair (cta_group::2) kernels are opt-in (CNMF_TC_PAIR=1): correct (same
+// parity tests), but measured slower on B200 -- every cross-CTA arrival with
+// cluster-scope release costs ~1500 cycles on the peer's critical path, and
+// the peer's panel splitting does not shrink -- 400 us vs 170 us for a
+// 20000 x 10000 forward pass (tools/tc_trace.cu with CNMF_TC_TRACE_CTA=1).
+static int g_pair_mode = -1;
+
+template <int S, bool TRANS, bool PAIR>
+int launch_tc_t(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bpanel, float* out, cudaStream_t st) {
+  using C = TcCfg<S, TRANS, PAIR>;
+  constexpr int CW = PAIR ? 2 : 1;
   // skinny operand rows = K extent: n (forward, X) or m (transpose, W)
   const int64_t brows = TRANS ? m : n;
   TmaDesc tA, tB;
@@ -550,9 +681,10 @@ int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bp
   CNMF_TRY(make_tma_2d(&tB, Bpanel, 4, brows, S, S, S, BKT, false));
   const int64_t P = TRANS ? n : m;   // output rows
   const int nt = (int)ceil_div(brows, BKT);
-  const int64_t nblocks = ceil_div(P, BMT);
-  const int whole = nblocks >= 16 * kNumSMs;
-  const int64_t grid = std::min<int64_t>(kNumSMs, whole ? nblocks : nblocks * nt);
+  const int64_t nblocks = ceil_div(P, CW * BMT);  // work items of CW x 128 output rows
+  const int64_t slots = kNumSMs / CW;             // CTAs (pairs) per wave
+  const int whole = nblocks >= 16 * slots;
+  const int64_t grid = CW * std::min<int64_t>(slots, whole ? nblocks : nblocks * nt);
   ZSync* zs = nullptr;
   if (!whole) {
     static ZSync* ring = nullptr;
@@ -565,7 +697,9 @@ int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bp
   }
   static bool attr = false;
   if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(pass_tc<S, TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    CNMF_CUDA(cudaFuncSetAttribute(pass_tc<S, TRANS, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)C::SMEM));
+    if (PAIR) CNMF_CUDA(cudaFuncSetAttribute(pass_tc<S, TRANS, PAIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     attr = true;
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -579,18 +713,32 @@ int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bp
   lc.blockDim = dim3(C::THREADS);
   lc.dynamicSmemBytes = C::SMEM;
   lc.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = CW;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   lc.attrs = at;
-  lc.numAttrs = 1;
-  CNMF_CUDA(cudaLaunchKernelEx(&lc, pass_tc<S, TRANS>, tA, tB, out, P, nt, nblocks, whole, zs));
+  lc.numAttrs = PAIR ? 2 : 1;
+  CNMF_CUDA(cudaLaunchKernelEx(&lc, pass_tc<S, TRANS, PAIR>, tA, tB, out, P, nt, nblocks, whole, zs));
   CNMF_LAUNCH_CHECK();
   if (e0) {
     CNMF_CUDA(cudaEventRecord(e1, st));
     pass_record(e0, e1, 4.0 * ((double)m * n + (double)n * S + (double)m * S));
   }
   return CNMF_OK;
+}
+
+template <int S, bool TRANS>
+int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bpanel, float* out, cudaStream_t st) {
+  if (g_pair_mode < 0) {
+    const char* e = getenv("CNMF_TC_PAIR");
+    g_pair_mode = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (g_pair_mode) return launch_tc_t<S, TRANS, true>(A, m, n, lda, Bpanel, out, st);
+  return launch_tc_t<S, TRANS, false>(A, m, n, lda, Bpanel, out, st);
 }
 
 }  // namespace

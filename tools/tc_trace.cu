@@ -1,6 +1,9 @@
 // Per-iteration timeline of pass_tc (block 0): which role gates the pipeline?
 // Build: see tools/tc_trace.sh
 #define CNMF_TC_TRACE 1
+#ifndef CNMF_TC_TRACE_CTA
+#define CNMF_TC_TRACE_CTA 0
+#endif
 #include "../paper_1505_04650_b200/csrc/tc_pass.cu"
 
 #include <algorithm>
