@@ -241,6 +241,30 @@ def test_snmf_near_separable_config0_shape():
     assert abs(res.rel_error_full - ref.rel_error_full) <= 1e-3 * ref.rel_error_full
 
 
+def test_snmf_tall_skinny_config2_shape():
+    # configs[2]: tall-and-skinny near-separable, fp32, n = 200, r = 20,
+    # alpha = 0.5, noise 0.005, q = 2 (m reduced from 2,000,000 to keep the
+    # oracle's CPU run short; the device path is size-independent here)
+    a, truth = O.near_separable(60_000, 200, 20, 0.5, 0.005, seed=21)
+    a32 = a.astype(np.float32)
+    res = C.snmf(a32, 20, selector="spa", cfg=C.CompressionConfig(r=20, r_ov=10, w=2, seed=4))
+    ref = O.snmf(a32.astype(np.float64), 20, selector="spa", cfg=O.Config(20, 10, 2, 4))
+    assert np.array_equal(res.K, ref.K)
+    assert sorted(res.K.tolist()) == truth.tolist()
+    assert abs(res.rel_error_full - ref.rel_error_full) <= 1e-3 * ref.rel_error_full
+
+
+def test_xray_config3_shape_small():
+    # configs[3] (general shape, XRAY) at reduced size: m = 1200, n = 1500,
+    # r = 40 (s = 50: the 64-wide panel path)
+    a, truth = O.near_separable(1200, 1500, 40, 1.0, 0.01, seed=31)
+    a32 = a.astype(np.float32)
+    res = C.snmf(a32, 40, selector="xray", cfg=C.CompressionConfig(r=40, r_ov=10, w=4, seed=6))
+    ref = O.snmf(a32.astype(np.float64), 40, selector="xray", cfg=O.Config(40, 10, 4, 6))
+    assert np.array_equal(np.sort(res.K), np.sort(ref.K))
+    assert sorted(res.K.tolist()) == truth.tolist()
+
+
 # ---------------------------------------------------------------- ADMM ----
 
 def test_admm_matches_oracle_on_same_bases(golden):
