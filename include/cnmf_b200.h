@@ -119,6 +119,16 @@ int cnmf_orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size
  *                        1e-12 diagonal shift returns CNMF_ERR_NUMERIC.
  * cnmf_panel_apply       P <- P T in place (T upper triangular S x S fp64). */
 int cnmf_cholesky_inverse(double* G, int s, int S, double* Rinv, double* R, void* stream);
+/* Asynchronous variants for a whole sharded range finder with one status
+ * check: `ws` is a small workspace of cnmf_small_workspace(s) bytes (Gram
+ * scratch, counters, failure word). cnmf_status_reset clears it, the async
+ * calls record failures in it, cnmf_status_check synchronises and reports
+ * CNMF_ERR_NUMERIC if any recorded failure. */
+size_t cnmf_small_workspace(int s);
+int cnmf_status_reset(void* ws, int s, void* stream);
+int cnmf_status_check(const void* ws, int s, void* stream);
+int cnmf_orthonormalize_async(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, void* stream);
+int cnmf_cholesky_inverse_async(double* G, int s, int S, double* Rinv, double* R, void* ws, void* stream);
 int cnmf_panel_apply(float* P, int64_t rows, int S, const double* T, void* stream);
 
 /* ---- separable NMF (snmf.py) ---------------------------------------------

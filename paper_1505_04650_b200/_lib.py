@@ -43,6 +43,11 @@ SIGNATURES = {
     "cnmf_compress_check": (c_int, [vp, c_i64, c_i64, c_int, vp]),
     "cnmf_orthonormalize": (c_int, [vp, c_i64, c_int, vp, vp, c_size, vp]),
     "cnmf_cholesky_inverse": (c_int, [vp, c_int, c_int, vp, vp, vp]),
+    "cnmf_small_workspace": (c_size, [c_int]),
+    "cnmf_status_reset": (c_int, [vp, c_int, vp]),
+    "cnmf_status_check": (c_int, [vp, c_int, vp]),
+    "cnmf_orthonormalize_async": (c_int, [vp, c_i64, c_int, vp, vp, c_size, vp]),
+    "cnmf_cholesky_inverse_async": (c_int, [vp, c_int, c_int, vp, vp, vp, vp]),
     "cnmf_panel_apply": (c_int, [vp, c_i64, c_int, vp, vp]),
     "cnmf_spa_workspace": (c_size, [c_i64, c_int]),
     "cnmf_panel_to_f64": (c_int, [vp, c_i64, c_int, vp, c_i64, vp]),

@@ -11,6 +11,11 @@ int pass_forward(const float*, int64_t, int64_t, int64_t, const float*, int, flo
 int pass_transpose(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
 int panel_cross(const float*, const float*, int64_t, int, double*, cudaStream_t);
 int cholesky_inverse(double*, int, int, double*, double*, cudaStream_t);
+int status_reset(void*, int, cudaStream_t);
+size_t small_workspace(int);
+int status_check(const void*, int, const char*, cudaStream_t);
+int orthonormalize_async(float*, int64_t, int, double*, void*, size_t, cudaStream_t);
+int cholesky_inverse_async(double*, int, int, double*, double*, void*, cudaStream_t);
 int panel_finalize(float*, int64_t, int, const double*, double*, cudaStream_t);
 size_t compress_workspace(int64_t, int64_t, int);
 int structured_compress(const float*, int64_t, int64_t, int64_t, int, int, uint64_t, int, float*, void*, size_t,
@@ -114,6 +119,22 @@ int cnmf_compress_check(const void* ws, int64_t m, int64_t n, int s, void* strea
 int cnmf_orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, void* stream) {
   if (rows < s) return fail(CNMF_ERR_ARGUMENT, "panel must be at least as tall as it is wide");
   return orthonormalize(P, rows, s, R, ws, ws_bytes, STREAM(stream));
+}
+
+size_t cnmf_small_workspace(int s) { return small_workspace(s); }
+
+int cnmf_status_reset(void* ws, int s, void* stream) { return status_reset(ws, s, STREAM(stream)); }
+
+int cnmf_status_check(const void* ws, int s, void* stream) { return status_check(ws, s, "device", STREAM(stream)); }
+
+int cnmf_orthonormalize_async(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, void* stream) {
+  if (rows < s) return fail(CNMF_ERR_ARGUMENT, "panel must be at least as tall as it is wide");
+  return orthonormalize_async(P, rows, s, R, ws, ws_bytes, STREAM(stream));
+}
+
+int cnmf_cholesky_inverse_async(double* G, int s, int S, double* Rinv, double* R, void* ws, void* stream) {
+  if (s < 1 || S < s) return fail(CNMF_ERR_ARGUMENT, "cholesky_inverse: bad widths");
+  return cholesky_inverse_async(G, s, S, Rinv, R, ws, STREAM(stream));
 }
 
 int cnmf_cholesky_inverse(double* G, int s, int S, double* Rinv, double* R, void* stream) {

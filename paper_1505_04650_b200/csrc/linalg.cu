@@ -64,6 +64,10 @@ int chol_inv(const double* G, int s, int S, double* T, double* R, int* info, int
 }
 
 static size_t small_bytes(int S) { return 2 * (size_t)S * S * 8 + 256; }
+size_t small_workspace(int s) {
+  const int S = panel_ld(s);
+  return S < 0 ? 0 : small_bytes(S);
+}
 
 size_t compress_workspace(int64_t m, int64_t n, int s) {
   const int S = panel_ld(s);
@@ -198,17 +202,52 @@ int cholesky_inverse(double* G, int s, int S, double* Rinv, double* R, cudaStrea
   return rc2;
 }
 
+int status_reset(void* ws, int s, cudaStream_t st);
+int status_check(const void* ws, int s, const char* what, cudaStream_t st);
+int orthonormalize_async(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, cudaStream_t st);
+
 int orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, cudaStream_t st) {
+  CNMF_TRY(status_reset(ws, s, st));
+  CNMF_TRY(orthonormalize_async(P, rows, s, R, ws, ws_bytes, st));
+  return status_check(ws, s, "orthonormalize", st);
+}
+
+// ---- asynchronous pieces for panels spread over several GPUs -------------
+// The small workspace (small_bytes(S)) carries the Gram matrix, the
+// transform, the last-block counters and the failure word; status_reset
+// clears it once, the async calls only ever record failures in it, and
+// status_check reads it (one synchronisation for a whole range finder).
+
+int status_reset(void* ws, int s, cudaStream_t st) {
   const int S = panel_ld(s);
   if (S < 0) return fail(CNMF_ERR_ARGUMENT, "width must be <= 128");
-  if (ws_bytes < 2 * (size_t)S * S * 8 + 256) return fail(CNMF_ERR_ARGUMENT, "workspace too small");
   Scratch sc = carve_small(ws, S);
   init_info<<<1, 1, 0, st>>>(sc.info);
   CNMF_LAUNCH_CHECK();
   CNMF_CUDA(cudaMemsetAsync(sc.G, 0, (size_t)S * S * 8, st));
+  return CNMF_OK;
+}
+
+int status_check(const void* ws, int s, const char* what, cudaStream_t st) {
+  const int S = panel_ld(s);
+  if (S < 0) return fail(CNMF_ERR_ARGUMENT, "width must be <= 128");
+  return check_info(carve_small(const_cast<void*>(ws), S).info, what, st);
+}
+
+int orthonormalize_async(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int S = panel_ld(s);
+  if (S < 0) return fail(CNMF_ERR_ARGUMENT, "width must be <= 128");
+  if (ws_bytes < small_bytes(S)) return fail(CNMF_ERR_ARGUMENT, "workspace too small");
+  Scratch sc = carve_small(ws, S);
   CNMF_TRY(panel_finalize_chol(P, rows, S, nullptr, sc.G, s, sc.T, nullptr, sc.info, 0, sc.counter, st, 1));
   CNMF_TRY(finish_basis(P, rows, s, S, sc, R, 0, st));
-  return check_info(sc.info, "orthonormalize", st);
+  return CNMF_OK;
+}
+
+// Rinv = R^{-1} of G = R^T R (G consumed), failures recorded in ws
+int cholesky_inverse_async(double* G, int s, int S, double* Rinv, double* R, void* ws, cudaStream_t st) {
+  if (panel_ld(s) != S) return fail(CNMF_ERR_ARGUMENT, "cholesky_inverse: bad widths");
+  return chol_inv(G, s, S, Rinv, R, carve_small(ws, S).info, 0, st);
 }
 
 }  // namespace cnmf

@@ -80,6 +80,19 @@ class DeviceOps:
         require_cuda()
         self._lib = _lib
         self.lib = _lib.load()
+        self._status = None
+
+    def begin(self, s):
+        """Start a range finder: one small device workspace collects the
+        numeric status of every asynchronous step (checked once in end())."""
+        nb = int(self.lib.cnmf_small_workspace(s))
+        self._status = (torch.empty(nb, dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device())),
+                        s, nb)
+        self._lib.call("cnmf_status_reset", self._status[0].data_ptr(), s, self._st())
+
+    def end(self):
+        ws, s, _ = self._status
+        self._lib.call("cnmf_status_check", ws.data_ptr(), s, self._st())
 
     def _st(self):
         from .device import stream
@@ -121,9 +134,8 @@ class DeviceOps:
         return Z
 
     def orthonormalize(self, P, s):
-        nb = 2 * P.shape[1] ** 2 * 8 + 256
-        ws = torch.empty(nb, dtype=torch.uint8, device=P.device)
-        self._lib.call("cnmf_orthonormalize", P.data_ptr(), P.shape[0], s, None, ws.data_ptr(), nb, self._st())
+        ws, _, nb = self._status
+        self._lib.call("cnmf_orthonormalize_async", P.data_ptr(), P.shape[0], s, None, ws.data_ptr(), nb, self._st())
         return P
 
     def cross(self, P1, P2, S):
@@ -133,7 +145,8 @@ class DeviceOps:
 
     def cholesky_inverse(self, G, s, S):
         T = self.zeros((S, S), torch.float64)
-        self._lib.call("cnmf_cholesky_inverse", G.data_ptr(), s, S, T.data_ptr(), None, self._st())
+        self._lib.call("cnmf_cholesky_inverse_async", G.data_ptr(), s, S, T.data_ptr(), None,
+                       self._status[0].data_ptr(), self._st())
         return T
 
     def apply(self, P, T, S):
@@ -168,6 +181,7 @@ def range_finder(ops, comm, A, m, n, c0, cfg, side):
     s = cfg.basis_cols
     S = ops.panel_ld(s)
     oseed = child_seed(cfg.seed, "omega")
+    ops.begin(s)
     if side == 0:
         Y = comm.allreduce(ops.forward(A, ops.omega_rows(oseed, c0, A.n, s, S), S))
         ops.orthonormalize(Y, s)
@@ -175,12 +189,14 @@ def range_finder(ops, comm, A, m, n, c0, cfg, side):
             Z = orthonormalize_sharded(ops, comm, ops.transpose(A, Y, S), s, S)
             Y = comm.allreduce(ops.forward(A, Z, S))
             ops.orthonormalize(Y, s)
+        ops.end()
         return Y
     P = orthonormalize_sharded(ops, comm, ops.transpose(A, ops.omega_rows(oseed, 0, m, s, S), S), s, S)
     for _ in range(cfg.w):
         Y = comm.allreduce(ops.forward(A, P, S))
         ops.orthonormalize(Y, s)
         P = orthonormalize_sharded(ops, comm, ops.transpose(A, Y, S), s, S)
+    ops.end()
     return P
 
 

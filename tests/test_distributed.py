@@ -37,6 +37,12 @@ class NumpyOps:
     def panel_ld(self, s):
         return 32 if s <= 32 else 64 if s <= 64 else 128
 
+    def begin(self, s):
+        pass
+
+    def end(self):
+        pass
+
     def zeros(self, shape, dtype=torch.float64):
         return torch.zeros(shape, dtype=torch.float64)
 
