@@ -295,7 +295,12 @@ def run_ours(args):
     fp32_peak = 148 * 128 * 2 * sm_clock / 1e12  # FFMA peak at the observed SM clock
     pass_flops = 2.0 * M * N * 32  # padded panel width 32 for s = 30
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None,
+                "frac": achieved / hbm_peak,
+                # dram__bytes_read.sum + dram__bytes_write.sum of one configs[1] forward pass_tc launch
+                # (ncu --set full, profiles/r01_pass_tc_cfg1_ncu_full.txt): 205.37 MB + 6.19 MB against
+                # 202 MB algorithmic (A plus the two panels)
+                "traffic": 211.56e6 if (M, N) == (10000, 5000) else None, "traffic_unit": "bytes per launch",
+                "algorithmic_bytes_per_launch": pass_bytes,
                 "kernel": "pass_tc<32> tcgen05 3xTF32 streaming passes (CUDA events on the launch stream)",
                 "launches": pl.value, "avg_launch_ms": pass_avg_ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
