@@ -546,8 +546,10 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
     __syncthreads();
     sstamp(5);
   }
-  // fold the row groups through shared memory (the W scratch), then one
-  // atomic per accumulator entry per CTA
+  // fold the row groups through shared memory, then one atomic per
+  // accumulator entry per CTA; the fold is laid out entry-major so that the
+  // lanes of a warp (consecutive blocks) touch consecutive words -- the
+  // block-major layout put all 32 lanes on one bank (32-way conflicts)
   double* fold = sm.fold;  // GROUPS x NBLK x 16 <= kThreads x 16 doubles
   for (int half = 0; half < (mode == 1 ? 2 : 1); ++half) {
     if (GROUPS > 1) {
@@ -556,7 +558,7 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
-          for (int y = 0; y < 4; ++y) fold[(grp * NBLK + myb) * 16 + x * 4 + y] = half ? ad[x][y] : au[x][y];
+          for (int y = 0; y < 4; ++y) fold[(x * 4 + y) * (GROUPS * NBLK) + grp * NBLK + myb] = half ? ad[x][y] : au[x][y];
       __syncthreads();
     }
     if (own && grp == 0) {
@@ -568,7 +570,7 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
           double v = half ? ad[x][y] : au[x][y];
           if (GROUPS > 1) {
             v = 0.0;
-            for (int g = 0; g < GROUPS; ++g) v += fold[(g * NBLK + myb) * 16 + x * 4 + y];
+            for (int g = 0; g < GROUPS; ++g) v += fold[(x * 4 + y) * (GROUPS * NBLK) + g * NBLK + myb];
           }
           const int j = 4 * bj + x, b = 4 * bb + y;
           if (j < s && b < r) atomicAdd(&accp[j * kMax + b], v);
