@@ -296,7 +296,9 @@ struct Smem {
   double* M;   // RP x RP
   double* T;   // RP x RP  Gauss-Jordan ping-pong buffer
   double* fold;  // 256 x 16: row-group folding of the split accumulators
-  double* Pt;  // rows x SP   (resident slice or one tile)
+  double* Pt;  // rows x (SP + 2) (resident slice or one tile; the padding
+               // shifts consecutive rows by 16 B so paired row reads do not
+               // share banks)
   double* Ut;  // rows x RP
   double* Dt;  // rows x RP
   __device__ Smem(double* base, int rows) {
@@ -309,12 +311,12 @@ struct Smem {
     T = M + RP * LR;
     fold = T + RP * LR;
     Pt = fold + kThreads * 16;
-    Ut = Pt + (size_t)rows * SP;
+    Ut = Pt + (size_t)rows * (SP + 2);
     Dt = Ut + (size_t)rows * RP;
   }
   static size_t bytes(int rows) {
     return ((size_t)2 * SP * LS + 2 * SP * LR + RP * LS + 2 * RP * LR + kThreads * 16 +
-            (size_t)rows * (SP + 2 * RP)) * 8;
+            (size_t)rows * (SP + 2 + 2 * RP)) * 8;
   }
 };
 
@@ -455,7 +457,7 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
     if (!RES || load) {
       for (int i = tid; i < nr * SP; i += kThreads) {
         const int rr = i / SP, c = i % SP;
-        sm.Pt[i] = (c < s) ? (double)a.P[(t0 + rr) * a.S + c] : 0.0;
+        sm.Pt[rr * (SP + 2) + c] = (c < s) ? (double)a.P[(t0 + rr) * a.S + c] : 0.0;
       }
       for (int i = tid; i < nr * RP; i += kThreads) {
         const int rr = i / RP, c = i % RP;
@@ -486,7 +488,7 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
         for (int j = 0; j < SP; ++j) {
           double pv[BR], xv[BJ];
 #pragma unroll
-          for (int x = 0; x < BR; ++x) pv[x] = sm.Pt[rows[x] * SP + j];
+          for (int x = 0; x < BR; ++x) pv[x] = sm.Pt[rows[x] * (SP + 2) + j];
 #pragma unroll
           for (int y = 0; y < BJ; ++y) xv[y] = sm.X[j * LR + tb + 16 * y];
 #pragma unroll
@@ -528,7 +530,7 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
         double pv[4], uv[4], dv[4];
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
-          pv[x] = sm.Pt[rr * SP + 4 * bj + x];
+          pv[x] = sm.Pt[rr * (SP + 2) + 4 * bj + x];
           uv[x] = sm.Ut[rr * RP + 4 * bb + x];
           dv[x] = sm.Dt[rr * RP + 4 * bb + x];
         }
