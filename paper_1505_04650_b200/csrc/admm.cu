@@ -383,15 +383,20 @@ __device__ void core_step(const Smem<SP, RP>& sm, const Acc* a, int s, int r, do
   double* W = sm.W;
   const double* C = sm.C;
   double* M = sm.M;
-  // Xc = rhs (yc yc^T + pu I)^{-1},  rhs = C yc^T + pu L^T U - L^T dU
-  bgemm<RP, RP, SP>([&](int i, int k) { return yc[i * LS + k]; }, [&](int k, int j) { return yc[j * LS + k]; },
-                    [&](int i, int j, double v) { M[i * LR + j] = v + (i == j ? pu : 0.0); });
+  // Xc = rhs (yc yc^T + pu I)^{-1},  rhs = C yc^T + pu L^T U - L^T dU:
+  // one product [yc; C] yc^T gives the ridge matrix and the right-hand side
+  bgemm<RP + SP, RP, SP>(
+      [&](int i, int k) { return i < RP ? yc[i * LS + k] : C[(i - RP) * LS + k]; },
+      [&](int k, int j) { return yc[j * LS + k]; },
+      [&](int i, int j, double v) {
+        if (i < RP) {
+          M[i * LR + j] = v + (i == j ? pu : 0.0);
+        } else {
+          const int q = i - RP;
+          W[q * LS + j] = v + pu * ld(&a->LtU[q * kMax + j]) - ld(&a->LtDU[q * kMax + j]);
+        }
+      });
   __syncthreads();
-  auto rhs1 = [&](int i, int j, double v) {
-    W[i * LS + j] = v + pu * ld(&a->LtU[i * kMax + j]) - ld(&a->LtDU[i * kMax + j]);
-  };
-  bgemm<SP, RP, SP>([&](int i, int k) { return C[i * LS + k]; }, [&](int k, int j) { return yc[j * LS + k]; },
-                    rhs1);
   if constexpr (RP <= 32)
     gj_inverse_reg<RP>(M, sm.T, r);  // its first barrier also orders the products above
   else
@@ -400,15 +405,20 @@ __device__ void core_step(const Smem<SP, RP>& sm, const Acc* a, int s, int r, do
   bgemm<SP, RP, RP>([&](int i, int k) { return W[i * LS + k]; }, [&](int k, int j) { return M[k * LR + j]; },
                     [&](int i, int j, double v) { xc[i * LR + j] = (i < s && j < r) ? v : 0.0; });
   __syncthreads();
-  // Yc = (xc^T xc + pv I)^{-1} (xc^T C + pv V R^T - dV R^T)
-  bgemm<RP, RP, SP>([&](int i, int k) { return xc[k * LR + i]; }, [&](int k, int j) { return xc[k * LR + j]; },
-                    [&](int i, int j, double v) { M[i * LR + j] = v + (i == j ? pv : 0.0); });
+  // Yc = (xc^T xc + pv I)^{-1} (xc^T C + pv V R^T - dV R^T): one product
+  // xc^T [xc | C]
+  bgemm<RP, RP + SP, SP>(
+      [&](int i, int k) { return xc[k * LR + i]; },
+      [&](int k, int j) { return j < RP ? xc[k * LR + j] : C[k * LS + (j - RP)]; },
+      [&](int i, int j, double v) {
+        if (j < RP) {
+          M[i * LR + j] = v + (i == j ? pv : 0.0);
+        } else {
+          const int q = j - RP;
+          W[i * LS + q] = v + pv * ld(&a->RtV[q * kMax + i]) - ld(&a->RtDV[q * kMax + i]);
+        }
+      });
   __syncthreads();
-  auto rhs2 = [&](int i, int j, double v) {
-    W[i * LS + j] = v + pv * ld(&a->RtV[j * kMax + i]) - ld(&a->RtDV[j * kMax + i]);
-  };
-  bgemm<RP, SP, SP>([&](int i, int k) { return xc[k * LR + i]; }, [&](int k, int j) { return C[k * LS + j]; },
-                    rhs2);
   if constexpr (RP <= 32)
     gj_inverse_reg<RP>(M, sm.T, r);
   else
