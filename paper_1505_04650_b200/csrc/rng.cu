@@ -129,6 +129,37 @@ __device__ DD dd_div(DD a, DD b) {
 }
 // log(w) = e ln2 + 2 atanh((m-1)/(m+1)), m in [sqrt(1/2), sqrt(2)), series to
 // ~2^-110; rounded once at the end.
+// 1/(2k+1) as double-double pairs (exact rational rounded twice), so the
+// series below needs no double-double division per term: the tail path was
+// the slowest warp of every fill (tools/rng_probe.cu: 44 us vs 7 us median)
+__device__ const double kInvOdd[25][2] = {
+    {0x1.0000000000000p+0, 0x0.0p+0},  // 1/1
+    {0x1.5555555555555p-2, 0x1.5555555555555p-56},  // 1/3
+    {0x1.999999999999ap-3, -0x1.999999999999ap-57},  // 1/5
+    {0x1.2492492492492p-3, 0x1.2492492492492p-57},  // 1/7
+    {0x1.c71c71c71c71cp-4, 0x1.c71c71c71c71cp-58},  // 1/9
+    {0x1.745d1745d1746p-4, -0x1.745d1745d1746p-59},  // 1/11
+    {0x1.3b13b13b13b14p-4, -0x1.3b13b13b13b14p-58},  // 1/13
+    {0x1.1111111111111p-4, 0x1.1111111111111p-60},  // 1/15
+    {0x1.e1e1e1e1e1e1ep-5, 0x1.e1e1e1e1e1e1ep-61},  // 1/17
+    {0x1.af286bca1af28p-5, 0x1.af286bca1af28p-59},  // 1/19
+    {0x1.8618618618618p-5, 0x1.8618618618618p-59},  // 1/21
+    {0x1.642c8590b2164p-5, 0x1.642c8590b2164p-60},  // 1/23
+    {0x1.47ae147ae147bp-5, -0x1.eb851eb851eb8p-61},  // 1/25
+    {0x1.2f684bda12f68p-5, 0x1.2f684bda12f68p-59},  // 1/27
+    {0x1.1a7b9611a7b96p-5, 0x1.1a7b9611a7b96p-61},  // 1/29
+    {0x1.0842108421084p-5, 0x1.0842108421084p-60},  // 1/31
+    {0x1.f07c1f07c1f08p-6, -0x1.f07c1f07c1f08p-61},  // 1/33
+    {0x1.d41d41d41d41dp-6, 0x1.0750750750750p-60},  // 1/35
+    {0x1.bacf914c1bad0p-6, -0x1.bacf914c1bad0p-60},  // 1/37
+    {0x1.a41a41a41a41ap-6, 0x1.0690690690690p-60},  // 1/39
+    {0x1.8f9c18f9c18fap-6, -0x1.f3831f3831f38p-61},  // 1/41
+    {0x1.7d05f417d05f4p-6, 0x1.7d05f417d05f4p-62},  // 1/43
+    {0x1.6c16c16c16c17p-6, -0x1.f49f49f49f49fp-61},  // 1/45
+    {0x1.5c9882b931057p-6, 0x1.310572620ae4cp-61},  // 1/47
+    {0x1.4e5e0a72f0539p-6, 0x1.e0a72f0539783p-60},  // 1/49
+};
+
 __device__ double cr_log(double w) {
   int e;
   double m = frexp(w, &e);
@@ -138,8 +169,8 @@ __device__ double cr_log(double w) {
   }
   const DD s = dd_div(DD{m - 1.0, 0.0}, two_sum(m, 1.0));
   const DD z = dd_mul(s, s);
-  DD p = dd_div(DD{1.0, 0.0}, DD{49.0, 0.0});
-  for (int k = 23; k >= 0; --k) p = dd_add(dd_mul(p, z), dd_div(DD{1.0, 0.0}, DD{2.0 * k + 1, 0.0}));
+  DD p = DD{kInvOdd[24][0], kInvOdd[24][1]};
+  for (int k = 23; k >= 0; --k) p = dd_add(dd_mul(p, z), DD{kInvOdd[k][0], kInvOdd[k][1]});
   const DD lm = dd_mul(DD{2.0 * s.hi, 2.0 * s.lo}, p);
   const DD r = dd_add(dd_mul(DD{(double)e, 0.0}, DD{0x1.62e42fefa39efp-1, 0x1.abc9e3b39803fp-56}), lm);
   return r.hi + r.lo;
@@ -209,6 +240,20 @@ __device__ double slow_normal(uint64_t key, int64_t pos, uint64_t r0, int64_t* n
   }
 }
 
+// Per-block shared-memory copies of the ziggurat tables used on the fast
+// path: every lane indexes them with its own random layer, which __constant__
+// memory serialises (one access per distinct address per warp).
+__shared__ uint64_t s_zki[256];
+__shared__ double s_zwi[256];
+
+__device__ __forceinline__ void load_zig_tables() {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    s_zki[i] = cnmf_zig::kKi[i];
+    s_zwi[i] = cnmf_zig::kWi[i];
+  }
+  __syncthreads();
+}
+
 template <typename T>
 __device__ __forceinline__ void store_variate(T* out, int64_t ld, int64_t cols, int64_t row0, int64_t k,
                                               int64_t count, double x) {
@@ -241,9 +286,9 @@ __device__ int64_t walk(uint64_t key, int64_t head, int64_t stop, int64_t seg_st
       const int idx = (int)(r & 0xff);
       r >>= 8;
       const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-      double x = __dmul_rn((double)rabs, cnmf_zig::kWi[idx]);
+      double x = __dmul_rn((double)rabs, s_zwi[idx]);
       xs[j] = (r & 1) ? -x : x;
-      if (!(rabs < cnmf_zig::kKi[idx])) slow |= 1u << j;
+      if (!(rabs < s_zki[idx])) slow |= 1u << j;
     }
     uint32_t m[4];
 #pragma unroll
@@ -252,14 +297,14 @@ __device__ int64_t walk(uint64_t key, int64_t head, int64_t stop, int64_t seg_st
 
     int p = (int)(head - base);
     while (p < kWin && base + p < stop) {
-      // first slow position >= p
+      // first slow position >= p (static indices only: a dynamically
+      // indexed m[] would live in local memory)
       int f = kWin;
-      for (int q = p >> 5; q < 4; ++q) {
-        uint32_t w = m[q] & (q == (p >> 5) ? (0xffffffffu << (p & 31)) : 0xffffffffu);
-        if (w) {
-          f = q * 32 + __ffs(w) - 1;
-          break;
-        }
+      const int pq = p >> 5;
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        const uint32_t w = q < pq ? 0u : m[q] & (q == pq ? (0xffffffffu << (p & 31)) : 0xffffffffu);
+        if (w) f = q * 32 + __ffs(w) - 1;
       }
       // fast run [p, f) — but never start a variate at or beyond `stop`
       int fe = f;
@@ -296,7 +341,10 @@ __device__ int64_t walk(uint64_t key, int64_t head, int64_t stop, int64_t seg_st
       uint64_t tu1 = 0;
       int tneg = -1;
       const double x = slow_normal(key, base + f, rf, &nxt, &tu1, &tneg);
-      if (chain != nullptr && base == seg_start) chain[f >> 5] |= 1u << (f & 31);
+      if (chain != nullptr && base == seg_start) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) chain[q] |= ((f >> 5) == q) ? (1u << (f & 31)) : 0u;
+      }
       if (WRITE && lane == 0) {
         store_variate(out, ld, cols, row0, k0 + k, count, x);
         const int64_t kk = k0 + k;
@@ -318,7 +366,20 @@ __device__ int64_t walk(uint64_t key, int64_t head, int64_t stop, int64_t seg_st
   return k;
 }
 
+#ifdef CNMF_RNG_PROBE
+__device__ unsigned long long g_rng_probe[4096][2];
+__device__ __forceinline__ unsigned long long probe_time() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 __global__ void k1_speculate(const Layout L, SegState* segs) {
+#ifdef CNMF_RNG_PROBE
+  const unsigned long long pt0 = probe_time();
+#endif
+  load_zig_tables();
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (g >= L.total_segs) return;
   const StreamDesc sd = stream_of(L, chunk_of_seg(L, g));
@@ -327,6 +388,12 @@ __global__ void k1_speculate(const Layout L, SegState* segs) {
   uint32_t chain[4] = {0, 0, 0, 0};
   int64_t ex;
   const int64_t n = walk<false, float>(sd.key, s0, s1, s0, chain, nullptr, 0, 1, 0, 0, 0, &ex);
+#ifdef CNMF_RNG_PROBE
+  if ((threadIdx.x & 31) == 0 && g < 4096) {
+    g_rng_probe[g][0] = pt0;
+    g_rng_probe[g][1] = probe_time();
+  }
+#endif
   if ((threadIdx.x & 31) == 0) {
     segs[g].exit = ex;
     segs[g].count = n;
@@ -337,6 +404,7 @@ __global__ void k1_speculate(const Layout L, SegState* segs) {
 
 // One CTA per stream: re-anchor each segment at its true entry, scan counts.
 __global__ void k2_anchor_scan(const Layout L, SegState* segs, int* flags) {
+  load_zig_tables();
   const StreamDesc sd = stream_of(L, blockIdx.x);
   __shared__ int64_t s_cnt[1024];
   __shared__ int s_bad;
@@ -362,7 +430,7 @@ __global__ void k2_anchor_scan(const Layout L, SegState* segs, int* flags) {
       const int idx = (int)(r & 0xff);
       const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
       int64_t nxt = p + 1;
-      if (!(rabs < cnmf_zig::kKi[idx])) (void)slow_normal(sd.key, p, r, &nxt);
+      if (!(rabs < s_zki[idx])) (void)slow_normal(sd.key, p, r, &nxt);
       d += 1;
       p = nxt;
     }
@@ -419,6 +487,7 @@ __global__ void k2_anchor_scan(const Layout L, SegState* segs, int* flags) {
 template <typename T>
 __global__ void k3_emit(const Layout L, const SegState* segs, const int* flags, T* out, int64_t ld, TailRec* tails,
                         unsigned int* ntails, unsigned int tail_cap) {
+  load_zig_tables();
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (g >= L.total_segs) return;
   const int64_t c = chunk_of_seg(L, g);
@@ -437,6 +506,7 @@ __global__ void k3_emit(const Layout L, const SegState* segs, const int* flags, 
 template <typename T>
 __global__ void k_serial(const Layout L, const int* flags, T* out, int64_t ld, TailRec* tails,
                          unsigned int* ntails, unsigned int tail_cap) {
+  load_zig_tables();
   if (!flags[blockIdx.x]) return;
   const StreamDesc sd = stream_of(L, blockIdx.x);
   int64_t head = 0, k = 0;
@@ -564,7 +634,7 @@ static Layout make_layout(uint64_t seed, int64_t rows, int64_t cols, int64_t chu
   L.key = seed;
   auto seg = [](int64_t count, int32_t* seglen, int32_t* nseg) {
     const int64_t need = (int64_t)(count * 1.02) + 4 * kWin;
-    int64_t len = 4 * kWin;
+    int64_t len = kWin;  // one window per segment: 4x the warps of 4-window segments (latency-bound walk)
     while (ceil_div(need, len) > 1024) len *= 2;
     *seglen = (int32_t)len;
     *nseg = (int32_t)ceil_div(need, len);
