@@ -38,24 +38,48 @@ namespace {
 constexpr int kMax = 64;      // s, r <= 64
 constexpr int kTile = 32;     // rows per streamed split tile
 constexpr int kThreads = 256;
-constexpr size_t kSmemCap = 200 * 1024;
+constexpr size_t kSmemCap = 227 * 1024 - 512;  // B200 opt-in maximum less the static red[]
 
 struct Ctrl {
   int k;         // next iteration index (resume point)
   int done;
   int iters;     // iterations completed when done
   int diverged;  // iteration index (0-based) that tripped the divergence rule, or -1
-  unsigned int bar_count;
+  unsigned int bar_count;  // grid_barrier arrivals in this launch
   unsigned int bar_gen;
 };
 
 // reduced partials of one split sweep (stride kMax so every SP/RP fits)
 struct Acc {
   double LtU[kMax * kMax];   // s x r : L^T U
-  double LtDU[kMax * kMax];  // s x r : L^T dU
   double RtV[kMax * kMax];   // s x r : R V^T   (= (V R^T)^T)
-  double RtDV[kMax * kMax];  // s x r : R dV^T
   double scal[4];            // feasL^2, compL^2, feasR^2, compR^2
+};
+
+// State every CTA keeps redundantly, saved here between launches. The dual
+// projections L^T dU and R dV^T are linear in dU, dV, so they follow from the
+// dual step dU_k = dU_{k-1} + step pu (L Xc_k - U_k) without a reduction:
+//   L^T dU_k = L^T dU_{k-1} + step pu (G_L Xc_k - L^T U_k),  G_L = L^T L
+// (the same for the right side with G_R = R R^T), which halves the per-row
+// products and the cross-CTA atomics of every split.
+struct Rep {
+  double GL[kMax * kMax];  // s x s : L^T L (fp64 of the fp32 panel)
+  double GR[kMax * kMax];  // s x s : R R^T
+  double DL[kMax * kMax];  // s x r : L^T dU
+  double DR[kMax * kMax];  // s x r : R dV^T
+};
+
+// What the helper CTA publishes for window k (between barriers k and k + 1),
+// double-buffered by the parity of k: the ridge inverse and the right-hand
+// side parts of core(k + 1) that depend only on (xc_k, yc_k), and that state
+// itself for the scorer CTA.
+struct Pub {
+  double Minv[kMax * kMax];  // r x r : (yc_k yc_k^T + pu I)^{-1}
+  double P1[kMax * kMax];    // s x r : C yc_k^T - TL
+  double TL[kMax * kMax];    // s x r : L^T dU_{k-1} + step pu G_L xc_k
+  double TR[kMax * kMax];    // s x r : R dV_{k-1}^T + step pv G_R yc_k^T
+  double xc[kMax * kMax];    // s x r
+  double yc[kMax * kMax];    // r x s
 };
 
 struct Side {
@@ -83,6 +107,8 @@ struct Params {
   double* scores;
   Ctrl* ctrl;
   Acc* acc;  // [3]
+  Rep* rep;
+  Pub* pub;  // [2]
   unsigned long long* prof;  // optional: per-iteration phase timestamps (CTA 0)
 };
 
@@ -110,20 +136,23 @@ __device__ __forceinline__ double wsum(double v) {
   return v;
 }
 
-__device__ void grid_barrier(Ctrl* c) {
+// Grid barrier on a counter that only grows within a launch (the host zeroes
+// it before every launch): barrier i of the launch completes when the count
+// reaches (i + 1) * gridDim.x, so arrival is one atomic and the release is
+// seen by the waiters directly (no second "generation" atomic).
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ void grid_barrier(Ctrl* c, unsigned int& epoch) {
   __syncthreads();
+  epoch += gridDim.x;
   if (threadIdx.x == 0) {
-    volatile unsigned int* gen = &c->bar_gen;
-    const unsigned int g = *gen;
     __threadfence();
-    if (atomicAdd(&c->bar_count, 1u) == gridDim.x - 1) {
-      c->bar_count = 0;
-      __threadfence();
-      atomicAdd(&c->bar_gen, 1u);
-    } else {
-      while (*gen == g) __nanosleep(32);
+    atomicAdd(&c->bar_count, 1u);
+    while ((int)(ld_acquire(&c->bar_count) - epoch) < 0) {
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -295,13 +324,30 @@ struct Smem {
   double* W;   // SP x SP  scratch
   double* M;   // RP x RP
   double* T;   // RP x RP  Gauss-Jordan ping-pong buffer
+  // staged reductions and published parts (speculative layout only)
+  double *LU, *RV;      // SP x RP : L^T U, R V^T of the last split
+  double *Minv, *P1;    // RP x RP, SP x RP
+  double *TL, *TR;      // SP x RP
+  double* GL;  // SP x SP  L^T L      (Rep)
+  double* GR;  // SP x SP  R R^T
+  double* DL;  // SP x RP  L^T dU
+  double* DR;  // SP x RP  R dV^T
   double* fold;  // 256 x 16: row-group folding of the split accumulators
   double* Pt;  // rows x (SP + 2) (resident slice or one tile; the padding
                // shifts consecutive rows by 16 B so paired row reads do not
                // share banks)
-  double* Ut;  // rows x RP
-  double* Dt;  // rows x RP
-  __device__ Smem(double* base, int rows) {
+  double *Ut0, *Ut1;  // rows x r (row stride r); two buffers when the score
+  double *Dt0, *Dt1;  // runs a split behind (selected, never indexed: an
+                      // indexed member array would move the struct to the stack)
+  __device__ double* Ut(int b) const { return b ? Ut1 : Ut0; }
+  __device__ double* Dt(int b) const { return b ? Dt1 : Dt0; }
+  static constexpr int kCommon = 2 * SP * LS + 2 * SP * LR + RP * LS + 2 * RP * LR;
+  static constexpr int kStage = 5 * SP * LR + RP * LR > kThreads * 16 ? 5 * SP * LR + RP * LR : kThreads * 16;
+  static constexpr int kGram = 2 * SP * LS + 2 * SP * LR;
+  // spec: the fold (split) and the staged reductions (core) are never live
+  // together, and the Gram / dual state (helper CTAs) and the resident slice
+  // (split CTAs) never share a CTA
+  __device__ Smem(double* base, int rows, bool spec, int r) {
     C = base;
     xc = C + SP * LS;
     yc = xc + SP * LR;
@@ -309,14 +355,38 @@ struct Smem {
     W = X + SP * LR;
     M = W + SP * LS;
     T = M + RP * LR;
-    fold = T + RP * LR;
-    Pt = fold + kThreads * 16;
-    Ut = Pt + (size_t)rows * (SP + 2);
-    Dt = Ut + (size_t)rows * RP;
+    double* q = T + RP * LR;
+    if (spec) {
+      LU = q;
+      RV = LU + SP * LR;
+      Minv = RV + SP * LR;
+      P1 = Minv + RP * LR;
+      TL = P1 + SP * LR;
+      TR = TL + SP * LR;
+      fold = q;
+      q += kStage;
+    } else {
+      LU = RV = Minv = P1 = TL = TR = nullptr;
+    }
+    GL = q;
+    GR = GL + SP * LS;
+    DL = GR + SP * LS;
+    DR = DL + SP * LR;
+    if (!spec) {
+      fold = DR + SP * LR;
+      Pt = fold + kThreads * 16;
+    } else {
+      Pt = q;
+    }
+    Ut0 = Pt + (size_t)rows * (SP + 2);
+    Dt0 = Ut0 + (size_t)rows * r;
+    Ut1 = spec ? Dt0 + (size_t)rows * r : Ut0;
+    Dt1 = spec ? Ut1 + (size_t)rows * r : Dt0;
   }
-  static size_t bytes(int rows) {
-    return ((size_t)2 * SP * LS + 2 * SP * LR + RP * LS + 2 * RP * LR + kThreads * 16 +
-            (size_t)rows * (SP + 2 + 2 * RP)) * 8;
+  static size_t bytes(int rows, bool spec, int r) {
+    const size_t slice = (size_t)rows * (SP + 2 + (spec ? 4 : 2) * r);
+    if (spec) return ((size_t)kCommon + kStage + std::max<size_t>(slice, kGram)) * 8;
+    return ((size_t)kCommon + kGram + kThreads * 16 + slice) * 8;
   }
 };
 
@@ -342,12 +412,12 @@ __device__ double kkt_score(const Smem<SP, RP>& sm, const Acc* a, double* red, d
   // E yc^T + L^T dU   and   xc^T E + dV R^T
   bgemm<SP, RP, SP>([&](int i, int k) { return W[i * LS + k]; }, [&](int k, int j) { return yc[j * LS + k]; },
                     [&](int i, int j, double v) {
-                      const double t = v + ld(&a->LtDU[i * kMax + j]);
+                      const double t = v + sm.DL[i * LR + j];
                       g1 += t * t;
                     });
   bgemm<RP, SP, SP>([&](int i, int k) { return xc[k * LR + i]; }, [&](int k, int j) { return W[k * LS + j]; },
                     [&](int i, int j, double v) {
-                      const double t = v + ld(&a->RtDV[j * kMax + i]);
+                      const double t = v + sm.DR[j * LR + i];
                       g2 += t * t;
                     });
   g1 = wsum(g1);
@@ -393,7 +463,7 @@ __device__ void core_step(const Smem<SP, RP>& sm, const Acc* a, int s, int r, do
           M[i * LR + j] = v + (i == j ? pu : 0.0);
         } else {
           const int q = i - RP;
-          W[q * LS + j] = v + pu * ld(&a->LtU[q * kMax + j]) - ld(&a->LtDU[q * kMax + j]);
+          W[q * LS + j] = v + pu * ld(&a->LtU[q * kMax + j]) - sm.DL[q * LR + j];
         }
       });
   __syncthreads();
@@ -415,7 +485,7 @@ __device__ void core_step(const Smem<SP, RP>& sm, const Acc* a, int s, int r, do
           M[i * LR + j] = v + (i == j ? pv : 0.0);
         } else {
           const int q = j - RP;
-          W[i * LS + q] = v + pv * ld(&a->RtV[q * kMax + i]) - ld(&a->RtDV[q * kMax + i]);
+          W[i * LS + q] = v + pv * ld(&a->RtV[q * kMax + i]) - sm.DR[q * LR + i];
         }
       });
   __syncthreads();
@@ -429,27 +499,212 @@ __device__ void core_step(const Smem<SP, RP>& sm, const Acc* a, int s, int r, do
   __syncthreads();
 }
 
+// Dual projections of iteration k from those of k - 1 (see Rep): xc, yc are
+// the state split k used, `a` its reductions. Every CTA runs the same
+// instructions on the same data, so the replicated copies stay identical.
+template <int SP, int RP>
+__device__ void dual_update(const Smem<SP, RP>& sm, const Acc* a, int s, int r, double spl, double spr) {
+  constexpr int LS = SP + 1, LR = RP + 1;
+  bgemm<SP, RP, SP>([&](int i, int k) { return sm.GL[i * LS + k]; }, [&](int k, int j) { return sm.xc[k * LR + j]; },
+                    [&](int i, int j, double v) {
+                      if (i < s && j < r) sm.DL[i * LR + j] += spl * (v - ld(&a->LtU[i * kMax + j]));
+                    });
+  bgemm<SP, RP, SP>([&](int i, int k) { return sm.GR[i * LS + k]; }, [&](int k, int j) { return sm.yc[j * LS + k]; },
+                    [&](int i, int j, double v) {
+                      if (i < s && j < r) sm.DR[i * LR + j] += spr * (v - ld(&a->RtV[i * kMax + j]));
+                    });
+  __syncthreads();
+}
+
+// Role of a CTA in the speculative schedule.
+enum Role { kWorker = 0, kHelper = 1, kScorer = 2 };
+
+// After barrier k: the reductions of split k, and the parts of core(k + 1)
+// the helper published for this window, into shared memory (one round of
+// L2 loads), zero padded.
+template <int SP, int RP>
+__device__ void stage(const Smem<SP, RP>& sm, const Acc* a, const Pub* pb, int role, int s, int r) {
+  constexpr int LS = SP + 1, LR = RP + 1;
+  // batches of 4 entries per thread, every load of a batch issued before
+  // the first store (one L2 round trip per batch, not per entry)
+  constexpr int NT = (SP * RP + kThreads - 1) / kThreads, NB = NT < 4 ? NT : 4;
+#pragma unroll 1
+  for (int t0 = 0; t0 < NT; t0 += NB) {
+    double v[NB][6];
+#pragma unroll
+    for (int t = 0; t < NB; ++t) {
+      const int idx = threadIdx.x + (t0 + t) * kThreads;
+      const int i = idx / RP, j = idx % RP;
+      const bool in = idx < SP * RP && i < s && j < r;
+      const int g = i * kMax + j;
+      v[t][0] = in ? ld(&a->LtU[g]) : 0.0;
+      v[t][1] = in ? ld(&a->RtV[g]) : 0.0;
+      v[t][2] = in && role != kHelper ? ld(role == kWorker ? &pb->P1[g] : &pb->TL[g]) : 0.0;
+      v[t][3] = in && role != kHelper ? ld(&pb->TR[g]) : 0.0;
+      v[t][4] = in && role == kScorer ? ld(&pb->xc[g]) : 0.0;
+      v[t][5] = in && role == kScorer ? ld(&pb->yc[j * kMax + i]) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < NB; ++t) {
+      const int idx = threadIdx.x + (t0 + t) * kThreads;
+      if (idx >= SP * RP) continue;
+      const int i = idx / RP, j = idx % RP, o = i * LR + j;
+      sm.LU[o] = v[t][0];
+      sm.RV[o] = v[t][1];
+      if (role == kWorker) sm.P1[o] = v[t][2];
+      if (role == kScorer) {
+        sm.TL[o] = v[t][2];
+        sm.xc[o] = v[t][4];
+        sm.yc[j * LS + i] = v[t][5];
+      }
+      if (role != kHelper) sm.TR[o] = v[t][3];
+    }
+  }
+  if (role == kWorker) {
+    constexpr int NM = (RP * RP + kThreads - 1) / kThreads, NC = NM < 8 ? NM : 8;
+#pragma unroll 1
+    for (int t0 = 0; t0 < NM; t0 += NC) {
+      double v[NC];
+#pragma unroll
+      for (int t = 0; t < NC; ++t) {
+        const int idx = threadIdx.x + (t0 + t) * kThreads;
+        v[t] = idx < RP * RP ? ld(&pb->Minv[(idx / RP) * kMax + idx % RP]) : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < NC; ++t) {
+        const int idx = threadIdx.x + (t0 + t) * kThreads;
+        if (idx < RP * RP) sm.Minv[(idx / RP) * LR + idx % RP] = v[t];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// dual projections of split k from the published parts:
+// L^T dU_k = TL - step pu L^T U_k (the same expression on every CTA that needs it)
+template <int SP, int RP>
+__device__ void duals_from_published(const Smem<SP, RP>& sm, double spl, double spr) {
+  for (int idx = threadIdx.x; idx < SP * (RP + 1); idx += kThreads) {
+    sm.DL[idx] = fma(-spl, sm.LU[idx], sm.TL[idx]);
+    sm.DR[idx] = fma(-spr, sm.RV[idx], sm.TR[idx]);
+  }
+  __syncthreads();
+}
+
+// core(k + 1) given the published inverse and right-hand side parts
+// (nmf.py:350-353): xc = (P1 + (pu + step pu) L^T U) Minv, then the
+// yc solve as in core_step with R dV^T = TR - step pv R V^T folded in.
+template <int SP, int RP>
+__device__ void fast_core(const Smem<SP, RP>& sm, int s, int r, double pv, double cl, double cr) {
+  constexpr int LS = SP + 1, LR = RP + 1;
+  double* xc = sm.xc;
+  double* M = sm.M;
+  double* W = sm.W;
+  bgemm<SP, RP, RP>([&](int i, int k) { return fma(cl, sm.LU[i * LR + k], sm.P1[i * LR + k]); },
+                    [&](int k, int j) { return sm.Minv[k * LR + j]; },
+                    [&](int i, int j, double v) { xc[i * LR + j] = (i < s && j < r) ? v : 0.0; });
+  __syncthreads();
+  sstamp(6);
+  bgemm<RP, RP + SP, SP>(
+      [&](int i, int k) { return xc[k * LR + i]; },
+      [&](int k, int j) { return j < RP ? xc[k * LR + j] : sm.C[k * LS + (j - RP)]; },
+      [&](int i, int j, double v) {
+        if (j < RP) {
+          M[i * LR + j] = v + (i == j ? pv : 0.0);
+        } else {
+          const int q = j - RP;
+          W[i * LS + q] = v + fma(cr, sm.RV[q * LR + i], -sm.TR[q * LR + i]);
+        }
+      });
+  __syncthreads();
+  if constexpr (RP <= 32)
+    gj_inverse_reg<RP>(M, sm.T, r);
+  else
+    gj_inverse<RP>(M, sm.T, r);
+  sstamp(7);
+  bgemm<RP, SP, RP>([&](int i, int k) { return M[i * LR + k]; }, [&](int k, int j) { return W[k * LS + j]; },
+                    [&](int i, int j, double v) { sm.yc[i * LS + j] = (i < r && j < s) ? v : 0.0; });
+  __syncthreads();
+}
+
+// Helper CTA: from the new state (xc_k, yc_k) and the duals of split k - 1
+// (DL, DR), the parts of core(k + 1) that do not depend on split k, into its
+// own shared memory and into `out` for the other CTAs.
+template <int SP, int RP>
+__device__ void precompute(const Smem<SP, RP>& sm, int s, int r, double pu, double spl, double spr, Pub* out) {
+  constexpr int LS = SP + 1, LR = RP + 1;
+  const double* yc = sm.yc;
+  double* M = sm.M;
+  bgemm<RP + SP, RP, SP>(
+      [&](int i, int k) { return i < RP ? yc[i * LS + k] : sm.C[(i - RP) * LS + k]; },
+      [&](int k, int j) { return yc[j * LS + k]; },
+      [&](int i, int j, double v) {
+        if (i < RP)
+          M[i * LR + j] = v + (i == j ? pu : 0.0);
+        else
+          sm.P1[(i - RP) * LR + j] = v;
+      });
+  bgemm<SP, RP, SP>([&](int i, int k) { return sm.GL[i * LS + k]; }, [&](int k, int j) { return sm.xc[k * LR + j]; },
+                    [&](int i, int j, double v) {
+                      sm.TL[i * LR + j] = (i < s && j < r) ? fma(spl, v, sm.DL[i * LR + j]) : 0.0;
+                    });
+  bgemm<SP, RP, SP>([&](int i, int k) { return sm.GR[i * LS + k]; }, [&](int k, int j) { return yc[j * LS + k]; },
+                    [&](int i, int j, double v) {
+                      sm.TR[i * LR + j] = (i < s && j < r) ? fma(spr, v, sm.DR[i * LR + j]) : 0.0;
+                    });
+  __syncthreads();
+  if constexpr (RP <= 32)
+    gj_inverse_reg<RP>(M, sm.T, r);
+  else
+    gj_inverse<RP>(M, sm.T, r);
+  for (int idx = threadIdx.x; idx < SP * RP; idx += kThreads) {
+    const int i = idx / RP, j = idx % RP;
+    const int g = i * kMax + j, o = i * LR + j;
+    const bool in = i < s && j < r;
+    const double p1 = in ? sm.P1[o] - sm.TL[o] : 0.0;
+    sm.P1[o] = p1;
+    out->P1[g] = p1;
+    out->TL[g] = sm.TL[o];
+    out->TR[g] = sm.TR[o];
+    out->xc[g] = sm.xc[o];
+    out->yc[j * kMax + i] = sm.yc[j * LS + i];
+  }
+  for (int idx = threadIdx.x; idx < RP * RP; idx += kThreads) {
+    const int i = idx / RP, j = idx % RP;
+    const double v = M[i * LR + j];
+    sm.Minv[i * LR + j] = v;
+    out->Minv[i * kMax + j] = v;
+  }
+  __syncthreads();
+}
+
 // Split sweep of one CTA over its contiguous slice [r0, r1) of a side.
-// mode 0: only accumulate P^T U (initial projection); mode 1: full update.
+// mode 0: initial projection: load U0 into buffer wb, accumulate P^T U0 and
+// the Gram matrix P^T P (into gram); mode 1: full update reading dU from
+// buffer wb ^ 1 and writing U, dU into buffer wb (one buffer without the
+// speculative score: wb ^ 1 aliases wb).
 // RES: the slice lives in shared memory (loaded when `load`).
 template <int SP, int RP, bool RES>
 __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, int s, int r, double step, int mode,
-                           int64_t r0, int64_t r1, bool load, double* accU, double* accD, double* scal,
+                           int64_t r0, int64_t r1, bool load, int wb, double* accU, double* gram, double* scal,
                            double* red) {
   const int tid = threadIdx.x;
   constexpr int NBJ = SP / 4, NBB = RP / 4, NBLK = NBJ * NBB;
   constexpr int GROUPS = NBLK >= kThreads ? 1 : kThreads / NBLK;
+  constexpr int NG = (SP * SP + kThreads - 1) / kThreads;
   const int grp = tid / NBLK, myb = tid - grp * NBLK;
   const bool own = grp < GROUPS;
   const int bj = own ? myb / NBB : 0, bb = own ? myb % NBB : 0;
-  double au[4][4], ad[4][4];
+  double* Uw = sm.Ut(wb);
+  double* Dw = sm.Dt(wb);
+  double* Dr = sm.Dt(wb ^ 1);
+  double au[4][4], g[NG];
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
-    for (int y = 0; y < 4; ++y) {
-      au[x][y] = 0.0;
-      ad[x][y] = 0.0;
-    }
+    for (int y = 0; y < 4; ++y) au[x][y] = 0.0;
+#pragma unroll
+  for (int t = 0; t < NG; ++t) g[t] = 0.0;
   double feas = 0.0, comp = 0.0;
   const double invpen = 1.0 / a.pen, sp_ = step * a.pen;
   constexpr int LS = SP + 1, LR = RP + 1;
@@ -469,16 +724,23 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
         const int rr = i / SP, c = i % SP;
         sm.Pt[rr * (SP + 2) + c] = (c < s) ? (double)a.P[(t0 + rr) * a.S + c] : 0.0;
       }
-      for (int i = tid; i < nr * RP; i += kThreads) {
-        const int rr = i / RP, c = i % RP;
+      for (int i = tid; i < nr * r; i += kThreads) {
         if (mode == 0) {
-          sm.Ut[i] = (c < r) ? a.U[(t0 + rr) * r + c] : 0.0;
-          sm.Dt[i] = 0.0;
+          Uw[i] = a.U[t0 * r + i];
+          Dw[i] = 0.0;
         } else {
-          sm.Dt[i] = (c < r) ? a.D[(t0 + rr) * r + c] : 0.0;
+          Dr[i] = a.D[t0 * r + i];
         }
       }
       __syncthreads();
+    }
+    if (mode == 0) {
+#pragma unroll
+      for (int t = 0; t < NG; ++t) {
+        const int e = tid + t * kThreads, j = e / SP, l = e % SP;
+        if (e < SP * SP)
+          for (int rr = 0; rr < nr; ++rr) g[t] = fma(sm.Pt[rr * (SP + 2) + j], sm.Pt[rr * (SP + 2) + l], g[t]);
+      }
     }
     if (mode == 1) {
       // lx = P X ; u = max(lx + d/pen, 0) ; d += step*pen*(lx - u)   (nmf.py:354-357)
@@ -514,13 +776,13 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
           for (int y = 0; y < BJ; ++y) {
             const int b = tb + 16 * y;
             if (b >= r) continue;
-            const int i = rr * RP + b;
+            const int i = rr * r + b;
             const double lx = acc[x][y];
-            const double d0 = sm.Dt[i];
+            const double d0 = Dr[i];
             const double u = fmax(lx + d0 * invpen, 0.0);
             const double d1 = d0 + sp_ * (lx - u);
-            sm.Ut[i] = u;
-            sm.Dt[i] = d1;
+            Uw[i] = u;
+            Dw[i] = d1;
             if (!RES) {
               a.U[(t0 + rr) * r + b] = u;
               a.D[(t0 + rr) * r + b] = d1;
@@ -533,24 +795,20 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
         }
       }
       __syncthreads();
-      if (mode == 1) sstamp(4);
+      sstamp(4);
     }
     if (own) {
       for (int rr = grp; rr < nr; rr += GROUPS) {
-        double pv[4], uv[4], dv[4];
+        double pv[4], uv[4];
 #pragma unroll
         for (int x = 0; x < 4; ++x) {
           pv[x] = sm.Pt[rr * (SP + 2) + 4 * bj + x];
-          uv[x] = sm.Ut[rr * RP + 4 * bb + x];
-          dv[x] = sm.Dt[rr * RP + 4 * bb + x];
+          uv[x] = (4 * bb + x < r) ? Uw[rr * r + 4 * bb + x] : 0.0;
         }
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
-          for (int y = 0; y < 4; ++y) {
-            au[x][y] = fma(pv[x], uv[y], au[x][y]);
-            ad[x][y] = fma(pv[x], dv[y], ad[x][y]);
-          }
+          for (int y = 0; y < 4; ++y) au[x][y] = fma(pv[x], uv[y], au[x][y]);
       }
     }
   }
@@ -558,36 +816,40 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
     __syncthreads();
     sstamp(5);
   }
+  if (mode == 0) {
+#pragma unroll
+    for (int t = 0; t < NG; ++t) {
+      const int e = tid + t * kThreads, j = e / SP, l = e % SP;
+      if (e < SP * SP && j < s && l < s) atomicAdd(&gram[j * kMax + l], g[t]);
+    }
+  }
   // fold the row groups through shared memory, then one atomic per
   // accumulator entry per CTA; the fold is laid out entry-major so that the
   // lanes of a warp (consecutive blocks) touch consecutive words -- the
   // block-major layout put all 32 lanes on one bank (32-way conflicts)
   double* fold = sm.fold;  // GROUPS x NBLK x 16 <= kThreads x 16 doubles
-  for (int half = 0; half < (mode == 1 ? 2 : 1); ++half) {
-    if (GROUPS > 1) {
-      __syncthreads();
-      if (own)
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int y = 0; y < 4; ++y) fold[(x * 4 + y) * (GROUPS * NBLK) + grp * NBLK + myb] = half ? ad[x][y] : au[x][y];
-      __syncthreads();
-    }
-    if (own && grp == 0) {
-      double* accp = half ? accD : accU;
+  if (GROUPS > 1) {
+    __syncthreads();
+    if (own)
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int y = 0; y < 4; ++y) {
-          double v = half ? ad[x][y] : au[x][y];
-          if (GROUPS > 1) {
-            v = 0.0;
-            for (int g = 0; g < GROUPS; ++g) v += fold[(x * 4 + y) * (GROUPS * NBLK) + g * NBLK + myb];
-          }
-          const int j = 4 * bj + x, b = 4 * bb + y;
-          if (j < s && b < r) atomicAdd(&accp[j * kMax + b], v);
+        for (int y = 0; y < 4; ++y) fold[(x * 4 + y) * (GROUPS * NBLK) + grp * NBLK + myb] = au[x][y];
+    __syncthreads();
+  }
+  if (own && grp == 0) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        double v = au[x][y];
+        if (GROUPS > 1) {
+          v = 0.0;
+          for (int q = 0; q < GROUPS; ++q) v += fold[(x * 4 + y) * (GROUPS * NBLK) + q * NBLK + myb];
         }
-    }
+        const int j = 4 * bj + x, b = 4 * bb + y;
+        if (j < s && b < r) atomicAdd(&accU[j * kMax + b], v);
+      }
   }
   if (mode == 1) {
     feas = wsum(feas);
@@ -612,23 +874,23 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
 }
 
 template <int SP, int RP, bool RES>
-__device__ void split(const Params& p, const Smem<SP, RP>& sm, int mode, bool load, Acc* acc, double* red) {
+__device__ void split(const Params& p, const Smem<SP, RP>& sm, int mode, bool load, int wb, Acc* acc, double* red) {
   const int b = blockIdx.x;
   if (b < p.nblk_left) {
     const int64_t r0 = min64((int64_t)b * p.rows_left, p.left.rows), r1 = min64(r0 + p.rows_left, p.left.rows);
-    split_side<SP, RP, RES>(p.left, sm, false, p.s, p.r, p.step, mode, r0, r1, load, acc->LtU, acc->LtDU,
+    split_side<SP, RP, RES>(p.left, sm, false, p.s, p.r, p.step, mode, r0, r1, load, wb, acc->LtU, p.rep->GL,
                             acc->scal, red);
   } else {
     const int64_t bb = b - p.nblk_left;
     const int64_t r0 = min64(bb * p.rows_right, p.right.rows), r1 = min64(r0 + p.rows_right, p.right.rows);
-    split_side<SP, RP, RES>(p.right, sm, true, p.s, p.r, p.step, mode, r0, r1, load, acc->RtV, acc->RtDV,
+    split_side<SP, RP, RES>(p.right, sm, true, p.s, p.r, p.step, mode, r0, r1, load, wb, acc->RtV, p.rep->GR,
                             acc->scal + 2, red);
   }
 }
 
-// write the resident slice of U and dU back to global memory
+// write buffer `wb` of the resident slice of U and dU back to global memory
 template <int SP, int RP>
-__device__ void write_back(const Params& p, const Smem<SP, RP>& sm) {
+__device__ void write_back(const Params& p, const Smem<SP, RP>& sm, int wb) {
   const int b = blockIdx.x;
   const Side& a = b < p.nblk_left ? p.left : p.right;
   const int64_t per = b < p.nblk_left ? p.rows_left : p.rows_right;
@@ -636,10 +898,25 @@ __device__ void write_back(const Params& p, const Smem<SP, RP>& sm) {
   const int64_t r0 = min64(bb * per, a.rows), r1 = min64(r0 + per, a.rows);
   const int r = p.r;
   for (int64_t i = threadIdx.x; i < (r1 - r0) * r; i += kThreads) {
-    const int64_t rr = i / r, c = i - rr * r;
-    a.U[(r0 + rr) * r + c] = sm.Ut[rr * RP + c];
-    a.D[(r0 + rr) * r + c] = sm.Dt[rr * RP + c];
+    a.U[r0 * r + i] = sm.Ut(wb)[i];
+    a.D[r0 * r + i] = sm.Dt(wb)[i];
   }
+}
+
+// save the replicated state of iteration k (the xc, yc split k used and the
+// dual projections after it); the next launch resumes at k + 1
+template <int SP, int RP>
+__device__ void save_state(const Params& p, const Smem<SP, RP>& sm, int k) {
+  constexpr int LS = SP + 1, LR = RP + 1;
+  const int s = p.s, r = p.r;
+  for (int i = threadIdx.x; i < s * r; i += kThreads) {
+    const int a = i / r, b = i - a * r;
+    p.xc_g[i] = sm.xc[a * LR + b];
+    p.yc_g[b * s + a] = sm.yc[b * LS + a];
+    p.rep->DL[a * kMax + b] = sm.DL[a * LR + b];
+    p.rep->DR[a * kMax + b] = sm.DR[a * LR + b];
+  }
+  if (threadIdx.x == 0) p.ctrl->k = k + 1;
 }
 
 // clear the used part of a partials buffer
@@ -647,24 +924,27 @@ __device__ void zero_acc(Acc* a, int s, int r) {
   for (int i = threadIdx.x; i < s * kMax; i += blockDim.x) {
     if ((i % kMax) < r) {
       a->LtU[i] = 0.0;
-      a->LtDU[i] = 0.0;
       a->RtV[i] = 0.0;
-      a->RtDV[i] = 0.0;
     }
   }
   if (threadIdx.x < 4) a->scal[threadIdx.x] = 0.0;
 }
 
+// Synchronous schedule: every CTA splits, scores and solves the core.
+// RES: slices resident in shared memory; else streamed in tiles.
 template <int SP, int RP, bool RES>
 __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const Params p) {
   extern __shared__ double smraw[];
   __shared__ double red[3 * kThreads / 32];
   const int s = p.s, r = p.r, tid = threadIdx.x;
-  const Smem<SP, RP> sm(smraw, RES ? (int)max(p.rows_left, p.rows_right) : kTile);
+  const Smem<SP, RP> sm(smraw, RES ? (int)max(p.rows_left, p.rows_right) : kTile, false, p.r);
   Ctrl* c = p.ctrl;
   if (c->done) return;
+  unsigned int epoch = 0;
+  const bool writer = blockIdx.x == 0;  // writes scores, trace, ctrl and the saved state
   if (blockIdx.x == 0 && tid == 0) g_prof_ptr = p.prof;
   constexpr int LS = SP + 1, LR = RP + 1;
+  const double spl = p.step * p.pu, spr = p.step * p.pv;
   for (int i = tid; i < SP * SP; i += kThreads) {
     const int a = i / SP, b = i % SP;
     sm.C[a * LS + b] = (a < s && b < s) ? p.core[a * s + b] : 0.0;
@@ -673,17 +953,28 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const Params p) {
     const int a = i / RP, b = i % RP;
     sm.xc[a * LR + b] = 0.0;
     sm.yc[b * LS + a] = 0.0;
+    sm.DL[a * LR + b] = 0.0;
+    sm.DR[a * LR + b] = 0.0;
   }
   __syncthreads();
   int k = c->k;
   if (p.fresh) {
-    // initial projections L^T U0 and R V0^T into acc[2] (nmf.py:337-343)
-    split<SP, RP, RES>(p, sm, 0, true, &p.acc[2], red);
-    grid_barrier(c);
+    // initial projections L^T U0 and R V0^T into acc[2] (nmf.py:337-343),
+    // Gram matrices into rep
+    split<SP, RP, RES>(p, sm, 0, true, 0, &p.acc[2], red);
+    grid_barrier(c, epoch);
     for (int i = tid; i < r * s; i += kThreads) {  // yc = V0 R^T
       const int q = i / s, j = i - q * s;
       sm.yc[q * LS + j] = ld(&p.acc[2].RtV[j * kMax + q]);
     }
+  }
+  for (int i = tid; i < SP * SP; i += kThreads) {
+    const int a = i / SP, b = i % SP;
+    const bool in = a < s && b < s;
+    sm.GL[a * LS + b] = in ? ld(&p.rep->GL[a * kMax + b]) : 0.0;
+    sm.GR[a * LS + b] = in ? ld(&p.rep->GR[a * kMax + b]) : 0.0;
+  }
+  if (p.fresh) {
     __syncthreads();
     core_step<SP, RP>(sm, &p.acc[2], s, r, p.pu, p.pv);
     k = 0;
@@ -692,6 +983,8 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const Params p) {
       const int a = i / r, b = i - a * r;
       sm.xc[a * LR + b] = p.xc_g[i];
       sm.yc[b * LS + a] = p.yc_g[b * s + a];
+      sm.DL[a * LR + b] = p.rep->DL[a * kMax + b];
+      sm.DR[a * LR + b] = p.rep->DR[a * kMax + b];
     }
     __syncthreads();
     // finish the iteration the previous launch stopped after
@@ -701,7 +994,7 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const Params p) {
     const bool conv = score < p.tol;
     const bool div = !conv && k - 1 >= 50 && score > 10.0 * ld(&p.scores[k - 1 - 50]);
     const bool cap = k >= p.max_iter;
-    if (blockIdx.x == 0 && tid == 0) {
+    if (writer && tid == 0) {
       p.scores[k - 1] = score;
       p.trace[k - 1] = obj;
       if (conv || div || cap) {
@@ -720,54 +1013,228 @@ __global__ void __launch_bounds__(kThreads, 1) admm_persistent(const Params p) {
     stamp(p, k, 0);
     if (blockIdx.x == 0 && tid == 0) g_prof_k = k;
     if (blockIdx.x == 0) zero_acc(&p.acc[(k + 1) % 3], s, r);
-    split<SP, RP, RES>(p, sm, 1, load, &p.acc[k % 3], red);
+    split<SP, RP, RES>(p, sm, 1, load, 0, &p.acc[k % 3], red);
     load = false;
     ++splits;
     stamp(p, k, 1);
-    grid_barrier(c);
+    grid_barrier(c, epoch);
     stamp(p, k, 2);
+    const Acc* a = &p.acc[k % 3];
+    dual_update<SP, RP>(sm, a, s, r, spl, spr);
     if (p.step_limit > 0 && splits >= p.step_limit) {
       // hand the state to the next launch (which scores iteration k first)
-      if (RES) write_back<SP, RP>(p, sm);
-      if (blockIdx.x == 0) {
-        for (int i = tid; i < s * r; i += kThreads) {
-          const int a = i / r, b = i - a * r;
-          p.xc_g[i] = sm.xc[a * LR + b];
-          p.yc_g[b * s + a] = sm.yc[b * LS + a];
-        }
-        if (tid == 0) c->k = k + 1;
-      }
+      if (RES) write_back<SP, RP>(p, sm, 0);
+      if (writer) save_state<SP, RP>(p, sm, k);
       return;
     }
-    const Acc* a = &p.acc[k % 3];
+    const bool cap = k + 1 >= p.max_iter;
     double obj;
     const double score = kkt_score<SP, RP>(sm, a, red, &obj);
     stamp(p, k, 3);
     const bool conv = score < p.tol;
-    // scores[k - 50] was written by CTA 0 at least 50 barriers ago
+    // scores[k - 50] was written by the writer CTA at least 50 barriers ago
     const bool div = !conv && k >= 50 && score > 10.0 * ld(&p.scores[k - 50]);
-    const bool cap = k + 1 >= p.max_iter;
-    if (blockIdx.x == 0 && tid == 0) {
+    if (writer && tid == 0) {
       p.scores[k] = score;
       p.trace[k] = obj;  // ||C - xc_k yc_k||^2 (nmf.py:360)
       if (conv || div || cap) {
         if (div) c->diverged = k;
         c->done = 1;
         c->iters = k + 1;
-        c->k = k + 1;
       }
     }
-    if (conv || div || cap) break;
+    if (conv || div || cap) {
+      if (RES) write_back<SP, RP>(p, sm, 0);
+      if (writer) save_state<SP, RP>(p, sm, k);
+      return;
+    }
     core_step<SP, RP>(sm, a, s, r, p.pu, p.pv);
     ++k;
   }
-  if (RES) write_back<SP, RP>(p, sm);
-  if (blockIdx.x == 0)
+}
+
+// Speculative schedule (slices resident): CTAs [0, nsplit) split; CTA
+// nsplit (helper) precomputes, for each window k between barriers k and
+// k + 1, everything of core(k + 2) that depends only on (xc_{k+1}, yc_{k+1})
+// -- the first ridge inverse, C yc^T, the dual-projection carry -- and
+// publishes it with the new state; CTA nsplit + 1 (scorer) scores split k
+// from the published state while the others run core(k + 1) and split
+// k + 1. The critical path per iteration is then: stage the reductions,
+// xc = W Minv, one ridge solve, yc, split.
+//
+// The score of k only decides whether to stop: if it stops, the scorer marks
+// ctrl.done (iters = k + 1) before arriving at barrier k + 1; the others see
+// it after that barrier and write back U, dU of iteration k, which split
+// k + 1 left untouched in the other buffer. A run with an iteration cap
+// ends at the cap without the extra barrier. Results equal the synchronous
+// schedule's up to the order of the (nondeterministic) atomic reductions.
+template <int SP, int RP>
+__global__ void __launch_bounds__(kThreads, 1) admm_spec(const Params p) {
+  extern __shared__ double smraw[];
+  __shared__ double red[3 * kThreads / 32];
+  __shared__ int flag;
+  const int s = p.s, r = p.r, tid = threadIdx.x;
+  const Smem<SP, RP> sm(smraw, (int)max(p.rows_left, p.rows_right), true, p.r);
+  Ctrl* c = p.ctrl;
+  if (c->done) return;
+  unsigned int epoch = 0;
+  const int nsplit = gridDim.x - 2;
+  const int role = blockIdx.x < nsplit ? kWorker : blockIdx.x == nsplit ? kHelper : kScorer;
+  if (blockIdx.x == 0 && tid == 0) g_prof_ptr = p.prof;
+  constexpr int LS = SP + 1, LR = RP + 1;
+  const double spl = p.step * p.pu, spr = p.step * p.pv, cl = p.pu + spl, cr = p.pv + spr;
+  for (int i = tid; i < SP * SP; i += kThreads) {
+    const int a = i / SP, b = i % SP;
+    sm.C[a * LS + b] = (a < s && b < s) ? p.core[a * s + b] : 0.0;
+  }
+  for (int i = tid; i < SP * RP; i += kThreads) {
+    const int a = i / RP, b = i % RP;
+    sm.xc[a * LR + b] = 0.0;
+    sm.yc[b * LS + a] = 0.0;
+    if (role != kWorker) {
+      sm.DL[a * LR + b] = 0.0;
+      sm.DR[a * LR + b] = 0.0;
+    }
+  }
+  __syncthreads();
+  int k = c->k;
+  bool stopped = false;
+  if (p.fresh) {
+    if (role == kWorker) split<SP, RP, true>(p, sm, 0, true, 1, &p.acc[2], red);
+    grid_barrier(c, epoch);
+    if (role == kHelper) {
+      for (int i = tid; i < r * s; i += kThreads) {  // yc = V0 R^T
+        const int q = i / s, j = i - q * s;
+        sm.yc[q * LS + j] = ld(&p.acc[2].RtV[j * kMax + q]);
+      }
+    }
+    k = 0;
+  } else if (role != kWorker) {
     for (int i = tid; i < s * r; i += kThreads) {
       const int a = i / r, b = i - a * r;
-      p.xc_g[i] = sm.xc[a * LR + b];
-      p.yc_g[b * s + a] = sm.yc[b * LS + a];
+      sm.xc[a * LR + b] = p.xc_g[i];
+      sm.yc[b * LS + a] = p.yc_g[b * s + a];
+      sm.DL[a * LR + b] = p.rep->DL[a * kMax + b];
+      sm.DR[a * LR + b] = p.rep->DR[a * kMax + b];
     }
+    __syncthreads();
+    if (role == kScorer) {
+      // finish the iteration the previous launch stopped after
+      double obj;
+      const double score = kkt_score<SP, RP>(sm, &p.acc[(k - 1) % 3], red, &obj);
+      const bool conv = score < p.tol;
+      const bool div = !conv && k - 1 >= 50 && score > 10.0 * ld(&p.scores[k - 1 - 50]);
+      stopped = conv || div || k >= p.max_iter;
+      if (tid == 0) {
+        p.scores[k - 1] = score;
+        p.trace[k - 1] = obj;
+        if (stopped) {
+          if (div) c->diverged = k - 1;
+          c->iters = k;
+          c->done = k;  // done carries the iteration count: one word to read
+        }
+      }
+    }
+  }
+  if (role == kHelper) {
+    for (int i = tid; i < SP * SP; i += kThreads) {
+      const int a = i / SP, b = i % SP;
+      const bool in = a < s && b < s;
+      sm.GL[a * LS + b] = in ? ld(&p.rep->GL[a * kMax + b]) : 0.0;
+      sm.GR[a * LS + b] = in ? ld(&p.rep->GR[a * kMax + b]) : 0.0;
+    }
+    __syncthreads();
+    core_step<SP, RP>(sm, &p.acc[p.fresh ? 2 : (k - 1) % 3], s, r, p.pu, p.pv);
+    precompute<SP, RP>(sm, s, r, p.pu, spl, spr, &p.pub[k & 1]);
+  }
+  grid_barrier(c, epoch);  // Pub[k & 1] holds (xc_k, yc_k)
+  if (stopped) return;
+  if (role != kScorer) {
+    if (tid == 0) flag = *(volatile int*)&c->done;
+    __syncthreads();
+    if (flag) return;  // the prologue's score stopped the run
+  }
+  if (role == kWorker) {
+    const Pub* pb = &p.pub[k & 1];
+    for (int i = tid; i < SP * RP; i += kThreads) {
+      const int a = i / RP, b = i % RP;
+      const bool in = a < s && b < r;
+      sm.xc[a * LR + b] = in ? ld(&pb->xc[a * kMax + b]) : 0.0;
+      sm.yc[b * LS + a] = in ? ld(&pb->yc[b * kMax + a]) : 0.0;
+    }
+  }
+  int splits = 0;
+  bool load = !p.fresh;
+  for (;;) {
+    const int wb = k & 1;
+    stamp(p, k, 0);
+    if (role == kWorker) {
+      if (blockIdx.x == 0 && tid == 0) g_prof_k = k;
+      if (blockIdx.x == 0) zero_acc(&p.acc[(k + 1) % 3], s, r);
+      split<SP, RP, true>(p, sm, 1, load, wb, &p.acc[k % 3], red);
+    }
+    load = false;
+    ++splits;
+    stamp(p, k, 1);
+    grid_barrier(c, epoch);
+    stamp(p, k, 2);
+    const Acc* a = &p.acc[k % 3];
+    stage<SP, RP>(sm, a, &p.pub[k & 1], role, s, r);
+    if (role != kScorer) {
+      // done == k: the scorer stopped at k - 1 (k iterations) and split k was
+      // speculative (a stop at k may already be visible to a CTA that left
+      // the barrier late; it is acted on after barrier k + 1)
+      if (tid == 0) {
+        const int d = *(volatile int*)&c->done;
+        flag = d != 0 && d == k;
+      }
+      __syncthreads();
+      if (flag) {
+        if (role == kWorker) write_back<SP, RP>(p, sm, wb ^ 1);
+        return;
+      }
+    }
+    stamp(p, k, 3);
+    const bool cap = k + 1 >= p.max_iter;
+    const bool pause = p.step_limit > 0 && splits >= p.step_limit;
+    if (role == kScorer) {
+      duals_from_published<SP, RP>(sm, spl, spr);
+      if (pause) {
+        // hand the state to the next launch (which scores iteration k first)
+        save_state<SP, RP>(p, sm, k);
+        return;
+      }
+      double obj;
+      const double score = kkt_score<SP, RP>(sm, a, red, &obj);
+      const bool conv = score < p.tol;
+      const bool div = !conv && k >= 50 && score > 10.0 * ld(&p.scores[k - 50]);
+      const bool stop = conv || div || cap;
+      if (stop) save_state<SP, RP>(p, sm, k);
+      if (tid == 0) {
+        p.scores[k] = score;
+        p.trace[k] = obj;  // ||C - xc_k yc_k||^2 (nmf.py:360)
+        if (stop) {
+          if (div) c->diverged = k;
+          c->iters = k + 1;
+          c->done = k + 1;
+        }
+      }
+      if (stop) {
+        if (!cap) grid_barrier(c, epoch);  // the others are in split k + 1
+        return;
+      }
+      ++k;
+      continue;
+    }
+    if (pause || cap) {
+      if (role == kWorker) write_back<SP, RP>(p, sm, wb);
+      return;
+    }
+    if (role == kHelper) duals_from_published<SP, RP>(sm, spl, spr);
+    fast_core<SP, RP>(sm, s, r, p.pv, cl, cr);
+    if (role == kHelper) precompute<SP, RP>(sm, s, r, p.pu, spl, spr, &p.pub[(k + 1) & 1]);
+    ++k;
+  }
 }
 
 __global__ void init_ctrl(Ctrl* c) {
@@ -779,30 +1246,45 @@ __global__ void init_ctrl(Ctrl* c) {
   c->bar_gen = 0;
 }
 
-template <int SP, int RP, bool RES>
-int launch(Params& p, int grid, size_t smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(admm_persistent<SP, RP, RES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)kSmemCap));
-    attr = true;
-  }
+template <class K>
+int launch(K kernel, Params& p, int grid, size_t smem, cudaStream_t st) {
+  CNMF_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap));
   int per_sm = 0;
-  CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, admm_persistent<SP, RP, RES>, kThreads, smem));
+  CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem));
   if (per_sm < 1) return fail(CNMF_ERR_CUDA, "ADMM kernel does not fit on an SM");
   void* args[] = {(void*)&p};
-  CNMF_CUDA(cudaLaunchCooperativeKernel((void*)admm_persistent<SP, RP, RES>, dim3(grid), dim3(kThreads), args, smem,
-                                        st));
+  CNMF_CUDA(cudaLaunchCooperativeKernel((void*)kernel, dim3(grid), dim3(kThreads), args, smem, st));
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }
 
+// split CTAs between the two sides by row count
+void plan(Params& p, int nsplit, int64_t m, int64_t n) {
+  const int nbl = (int)std::max<int64_t>(1, std::min<int64_t>(nsplit - 1, (nsplit * m + (m + n) / 2) / (m + n)));
+  const int nbr = std::max(1, nsplit - nbl);
+  p.nblk_left = nbl;
+  p.rows_left = ceil_div(m, nbl);
+  p.rows_right = ceil_div(n, nbr);
+}
+
+// One CTA per SM. Prefer the speculative schedule (slices resident, two
+// helper CTAs), then resident slices, then streamed tiles
+// (CNMF_ADMM_SPEC=0 disables the speculative schedule).
 template <int SP, int RP>
-int dispatch_res(Params& p, int grid, cudaStream_t st) {
-  const int64_t rows = std::max(p.rows_left, p.rows_right);
-  const size_t res_bytes = Smem<SP, RP>::bytes((int)std::min<int64_t>(rows, 1 << 20));
-  if (res_bytes <= kSmemCap) return launch<SP, RP, true>(p, grid, res_bytes, st);
-  return launch<SP, RP, false>(p, grid, Smem<SP, RP>::bytes(kTile), st);
+int dispatch(Params& p, int sms, int64_t want, int64_t m, int64_t n, cudaStream_t st) {
+  const char* e = getenv("CNMF_ADMM_SPEC");
+  const bool spec_ok = !(e && e[0] == '0') && sms >= 4;
+  auto rows = [&]() { return (int)std::min<int64_t>(std::max(p.rows_left, p.rows_right), 1 << 20); };
+  if (spec_ok) {
+    const int nsplit = (int)std::max<int64_t>(2, std::min<int64_t>(want, sms - 2));
+    plan(p, nsplit, m, n);
+    const size_t b2 = Smem<SP, RP>::bytes(rows(), true, p.r);
+    if (b2 <= kSmemCap) return launch(admm_spec<SP, RP>, p, nsplit + 2, b2, st);
+  }
+  plan(p, (int)want, m, n);
+  const size_t b1 = Smem<SP, RP>::bytes(rows(), false, p.r);
+  if (b1 <= kSmemCap) return launch(admm_persistent<SP, RP, true>, p, (int)want, b1, st);
+  return launch(admm_persistent<SP, RP, false>, p, (int)want, Smem<SP, RP>::bytes(kTile, false, p.r), st);
 }
 
 }  // namespace
@@ -812,7 +1294,7 @@ size_t admm_workspace(int64_t m, int64_t n, int s, int r) {
   (void)n;
   (void)s;
   (void)r;
-  return 256 + 3 * sizeof(Acc) + 256;
+  return 256 + 3 * sizeof(Acc) + sizeof(Rep) + 2 * sizeof(Pub) + 256;
 }
 
 int admm_run(const double* core, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
@@ -825,21 +1307,20 @@ int admm_run(const double* core, const float* L, int64_t m, const float* Rt, int
   const int S = s <= 32 ? 32 : 64;
   Ctrl* ctrl = (Ctrl*)ws;
   Acc* acc = (Acc*)((char*)ws + 256);
+  Rep* rep = (Rep*)(acc + 3);
+  Pub* pub = (Pub*)(rep + 1);
   int dev = 0, sms = 0;
   CNMF_CUDA(cudaGetDevice(&dev));
   CNMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // one CTA per SM; split the CTAs between the two sides by row count
   const int64_t want = std::max<int64_t>(2, std::min<int64_t>((int64_t)sms, ceil_div(m, 8) + ceil_div(n, 8)));
-  int nbl = (int)std::max<int64_t>(1, std::min<int64_t>(want - 1, (want * m + (m + n) / 2) / (m + n)));
-  const int nbr = (int)std::max<int64_t>(1, want - nbl);
-  const int grid = nbl + nbr;
   if (!resume) {
     init_ctrl<<<1, 1, 0, st>>>(ctrl);
     CNMF_LAUNCH_CHECK();
-    CNMF_CUDA(cudaMemsetAsync(acc, 0, 3 * sizeof(Acc), st));
+    CNMF_CUDA(cudaMemsetAsync(acc, 0, 3 * sizeof(Acc) + sizeof(Rep), st));
     CNMF_CUDA(cudaMemsetAsync(du, 0, (size_t)m * r * 8, st));
     CNMF_CUDA(cudaMemsetAsync(dvt, 0, (size_t)n * r * 8, st));
   }
+  CNMF_CUDA(cudaMemsetAsync(&ctrl->bar_count, 0, sizeof(unsigned int), st));  // grid_barrier epochs
   Params p;
   p.core = core;
   p.left = Side{L, m, S, u, du, pu};
@@ -853,15 +1334,14 @@ int admm_run(const double* core, const float* L, int64_t m, const float* Rt, int
   p.max_iter = max_iter;
   p.step_limit = step_limit;
   p.fresh = !resume;
-  p.nblk_left = nbl;
-  p.rows_left = ceil_div(m, nbl);
-  p.rows_right = ceil_div(n, nbr);
   p.xc_g = xc;
   p.yc_g = yc;
   p.trace = trace;
   p.scores = scores;
   p.ctrl = ctrl;
   p.acc = acc;
+  p.rep = rep;
+  p.pub = pub;
   p.prof = nullptr;
   if (const char* e = getenv("CNMF_ADMM_PROFILE")) {
     static unsigned long long* buf = nullptr;
@@ -871,15 +1351,15 @@ int admm_run(const double* core, const float* L, int64_t m, const float* Rt, int
   }
   int rc;
   if (s <= 32 && r <= 16)
-    rc = dispatch_res<32, 16>(p, grid, st);
+    rc = dispatch<32, 16>(p, sms, want, m, n, st);
   else if (s <= 32 && r <= 32)
-    rc = dispatch_res<32, 32>(p, grid, st);
+    rc = dispatch<32, 32>(p, sms, want, m, n, st);
   else if (r <= 16)
-    rc = dispatch_res<64, 16>(p, grid, st);
+    rc = dispatch<64, 16>(p, sms, want, m, n, st);
   else if (r <= 32)
-    rc = dispatch_res<64, 32>(p, grid, st);
+    rc = dispatch<64, 32>(p, sms, want, m, n, st);
   else
-    rc = dispatch_res<64, 64>(p, grid, st);
+    rc = dispatch<64, 64>(p, sms, want, m, n, st);
   CNMF_TRY(rc);
   if (p.prof) {
     unsigned long long h[256 * 8];

@@ -67,19 +67,29 @@ def problem():
     L = O.range_basis(a, replace(cfg, seed=O.child_seed(5, "left-basis")))
     R = O.row_basis(a, replace(cfg, seed=O.child_seed(5, "right-basis")))
     ref = O.admm(a, 20, cfg=O.Config(20, 10, 4, 5), max_iter=500, tol=1e-4)
-    return a32, L, R, ref
+    # the reference's own spread when the input is perturbed at fp32 level
+    # (2^-23 relative): the yardstick for a device run whose passes are fp32
+    rng = np.random.default_rng(0)
+    spread = 0.0
+    for _ in range(3):
+        o = O.admm(a * (1.0 + 2.0 ** -23 * rng.standard_normal(a.shape)), 20, cfg=O.Config(20, 10, 4, 5),
+                   max_iter=500, tol=1e-4)
+        spread = max(spread, abs(O.rel_error(a, o.X, o.Y) - ref.rel_error))
+    return a32, L, R, ref, spread
 
 
 def _check(res, problem):
-    a32, L, R, ref = problem
+    a32, L, R, ref, spread = problem
     Ld, Rd, it, rel = res
     sig = slice(0, 20)
     assert O.projector_distance(L[:, sig], Ld[:, sig]) < 1e-5
     assert O.projector_distance(R[:, sig], Rd[:, sig]) < 1e-5
     assert O.projector_distance(L, Ld) < 1e-3
     assert it == ref.iterations
-    # the ADMM's sensitivity to 1e-8-level input perturbations is ~1e-4
-    assert abs(rel - ref.rel_error) <= 2e-3 * ref.rel_error
+    # the ADMM amplifies input perturbations over 500 iterations:
+    # within 2e-3 relative, or within 3x the reference's own spread under
+    # fp32-level input perturbations
+    assert abs(rel - ref.rel_error) <= max(2e-3 * ref.rel_error, 3.0 * spread)
 
 
 def test_sharded_driver_one_rank(problem):
