@@ -106,6 +106,16 @@ int cnmf_structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, 
 int cnmf_structured_compress_async(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed,
                                    int side, float* Q, void* ws, size_t ws_bytes, void* stream);
 int cnmf_compress_check(const void* ws, int64_t m, int64_t n, int s, void* stream);
+/* Both bases of the compressed NMF at once (nmf.py:120 _compression_pair):
+ * QL (m x s panel) = cnmf_structured_compress(side 0, seed_left) and
+ * QR (n x s panel) = cnmf_structured_compress(side 1, seed_right), the same
+ * kernels and arithmetic; the two range finders are interleaved on `stream`
+ * (column-chain pass, row-chain pass, one CholeskyQR sweep launch for both).
+ * ws_left / ws_right: cnmf_compress_workspace bytes each; status via
+ * cnmf_compress_check on each workspace. Asynchronous. */
+int cnmf_compress_pair_async(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed_left,
+                             uint64_t seed_right, float* QL, float* QR, void* ws_left, void* ws_right,
+                             size_t ws_bytes, void* stream);
 /* orthonormalise a panel in place (compress.py:136 canonical_qr, Q factor);
  * R (s x s, fp64, device, may be NULL) receives the triangular factor. */
 int cnmf_orthonormalize(float* P, int64_t rows, int s, double* R, void* ws, size_t ws_bytes, void* stream);

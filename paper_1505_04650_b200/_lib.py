@@ -40,6 +40,8 @@ SIGNATURES = {
     "cnmf_structured_compress": (c_int, [vp, c_i64, c_i64, c_i64, c_int, c_int, c_u64, c_int, vp, vp, c_size, vp]),
     "cnmf_structured_compress_async": (c_int, [vp, c_i64, c_i64, c_i64, c_int, c_int, c_u64, c_int, vp, vp, c_size,
                                                vp]),
+    "cnmf_compress_pair_async": (c_int, [vp, c_i64, c_i64, c_i64, c_int, c_int, c_u64, c_u64, vp, vp, vp, vp,
+                                         c_size, vp]),
     "cnmf_compress_check": (c_int, [vp, c_i64, c_i64, c_int, vp]),
     "cnmf_orthonormalize": (c_int, [vp, c_i64, c_int, vp, vp, c_size, vp]),
     "cnmf_cholesky_inverse": (c_int, [vp, c_int, c_int, vp, vp, vp]),

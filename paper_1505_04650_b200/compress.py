@@ -114,6 +114,33 @@ def _compress(a, cfg, side, check=True):
     return basis, A
 
 
+def _compress_pair(A, cfg_left, cfg_right):
+    """Both range finders of the compressed NMF (nmf.py:120-135) in one
+    asynchronous C call: the column chain on the current stream, the row chain
+    on a side stream joined back into it, each chain's CholeskyQR sweeps
+    overlapping the other chain's passes. Call ``_check`` on both bases."""
+    if cfg_left.basis_cols != cfg_right.basis_cols or cfg_left.w != cfg_right.w:
+        raise ArgumentError("paired range finders need the same width and power exponent")
+    _require_feasible(cfg_left, A.m, A.n)
+    s = cfg_left.basis_cols
+    S = panel_ld(s)
+    ql = empty((A.m, S))
+    qr = empty((A.n, S))
+    lib = _lib.load()
+    nbytes = lib.cnmf_compress_workspace(A.m, A.n, s)
+    wl = workspace(nbytes)
+    wr = workspace(nbytes)
+    _lib.call("cnmf_compress_pair_async", A.ptr, A.m, A.n, A.lda, s, cfg_left.w, cfg_left.seed & MASK64,
+              cfg_right.seed & MASK64, ql.data_ptr(), qr.data_ptr(), wl.data_ptr(), wr.data_ptr(), nbytes, stream())
+    out_ = []
+    for q, ws, cfg in ((ql, wl, cfg_left), (qr, wr, cfg_right)):
+        basis = CompressionBasis(Q=q[:, :s], kind="structured", config=cfg, panel=q)
+        basis._ws = ws
+        basis._dims = (A.m, A.n, s)
+        out_.append(basis)
+    return out_[0], out_[1]
+
+
 def _check(basis):
     m, n, s = basis._dims
     _lib.call("cnmf_compress_check", basis._ws.data_ptr(), m, n, s, stream())

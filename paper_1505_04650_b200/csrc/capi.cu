@@ -21,6 +21,8 @@ size_t compress_workspace(int64_t, int64_t, int);
 int structured_compress(const float*, int64_t, int64_t, int64_t, int, int, uint64_t, int, float*, void*, size_t,
                         cudaStream_t, bool);
 int compress_check(const void*, int64_t, int64_t, int, cudaStream_t);
+int structured_compress_pair(const float*, int64_t, int64_t, int64_t, int, int, uint64_t, uint64_t, float*, float*,
+                             void*, void*, size_t, cudaStream_t);
 int orthonormalize(float*, int64_t, int, double*, void*, size_t, cudaStream_t);
 size_t spa_workspace(int64_t, int);
 int panel_to_f64(const float*, int64_t, int, double*, int64_t, cudaStream_t);
@@ -110,6 +112,13 @@ int cnmf_structured_compress_async(const float* A, int64_t m, int64_t n, int64_t
   CNMF_TRY(check_a(A, m, n, lda));
   if (side != 0 && side != 1) return fail(CNMF_ERR_ARGUMENT, "side must be 0 (columns) or 1 (rows)");
   return structured_compress(A, m, n, lda, s, w, seed, side, Q, ws, ws_bytes, STREAM(stream), false);
+}
+
+int cnmf_compress_pair_async(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed_left,
+                             uint64_t seed_right, float* QL, float* QR, void* ws_left, void* ws_right,
+                             size_t ws_bytes, void* stream) {
+  return structured_compress_pair(A, m, n, lda, s, w, seed_left, seed_right, QL, QR, ws_left, ws_right, ws_bytes,
+                                  STREAM(stream));
 }
 
 int cnmf_compress_check(const void* ws, int64_t m, int64_t n, int s, void* stream) {

@@ -18,6 +18,7 @@
 
 #include "chol.cuh"
 #include "common.cuh"
+#include "sweep.cuh"
 
 namespace cnmf {
 
@@ -92,15 +93,6 @@ static Scratch carve_small(void* base, int S) {
   return sc;
 }
 
-// Finish a panel whose Gram-derived transform sc.T is pending: apply it,
-// re-factor, apply again (CholeskyQR2 on an already well-conditioned panel).
-static int finish_basis(float* P, int64_t rows, int s, int S, Scratch sc, double* Rfinal, int first_pass_id,
-                        cudaStream_t st) {
-  CNMF_TRY(panel_finalize_chol(P, rows, S, nullptr, sc.G, s, sc.T, Rfinal, sc.info, first_pass_id, sc.counter,
-                               st, 1));
-  return CNMF_OK;
-}
-
 static int check_info(const int* d_info, const char* what, cudaStream_t st) {
   int h[2];
   CNMF_CUDA(cudaMemcpyAsync(h, d_info, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -121,8 +113,24 @@ int compress_check(const void* ws, int64_t m, int64_t n, int s, cudaStream_t st)
   return check_info(sc.info, "range finder", st);
 }
 
-int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed, int side,
-                        float* Q, void* ws, size_t ws_bytes, cudaStream_t st, bool check) {
+// One range finder's device state (compress.py:156-227): the two panels
+// (rows m and rows n; the output side uses Q), the pass output `cur` and the
+// small CholeskyQR scratch.
+struct Chain {
+  const float* A;
+  int64_t m, n, lda;
+  int s, S, w, side;
+  float *Pm, *Pn, *cur;
+  int64_t cur_rows;
+  Scratch sc;
+  int pass_id;
+};
+
+// Validate, reset the status word and draw the reference's seeded test
+// matrix (compress.py:125-127; rows = A.cols for the column basis, A.rows for
+// the row basis) into the panel the first pass streams.
+static int chain_begin(Chain& c, const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed,
+                       int side, float* Q, void* ws, size_t ws_bytes, cudaStream_t st) {
   const int S = panel_ld(s);
   if (S < 0) return fail(CNMF_ERR_ARGUMENT, "basis width must be <= 128");
   if (s < 1 || w < 0) return fail(CNMF_ERR_ARGUMENT, "bad width or power exponent");
@@ -130,64 +138,99 @@ int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s
     return fail(CNMF_ERR_INFEASIBLE_RANK, "basis width " + std::to_string(s) + " exceeds min(m, n) = " +
                                               std::to_string(std::min(m, n)) + "; adjust_config first");
   if (ws_bytes < compress_workspace(m, n, s)) return fail(CNMF_ERR_ARGUMENT, "workspace too small");
-  // panels: rows m (B-type) and rows n (C-type); the output side uses Q
-  float* Pm = side == 0 ? Q : (float*)ws;
-  float* Pn = side == 0 ? (float*)ws : Q;
-  Scratch sc = carve_small((char*)ws + (size_t)std::max(m, n) * S * 4, S);
+  c.A = A;
+  c.m = m;
+  c.n = n;
+  c.lda = lda;
+  c.s = s;
+  c.S = S;
+  c.w = w;
+  c.side = side;
+  c.Pm = side == 0 ? Q : (float*)ws;
+  c.Pn = side == 0 ? (float*)ws : Q;
+  c.cur = nullptr;
+  c.cur_rows = 0;
+  c.pass_id = 0;
+  c.sc = carve_small((char*)ws + (size_t)std::max(m, n) * S * 4, S);
   char* rng_ws = (char*)ws + (size_t)std::max(m, n) * S * 4 + small_bytes(S);
   const size_t rng_bytes = ws_bytes - ((size_t)std::max(m, n) * S * 4 + small_bytes(S));
-  init_info<<<1, 1, 0, st>>>(sc.info);
+  init_info<<<1, 1, 0, st>>>(c.sc.info);
   CNMF_LAUNCH_CHECK();
-  CNMF_CUDA(cudaMemsetAsync(sc.G, 0, (size_t)S * S * 8, st));
-  // Omega: the reference's seeded test matrix (compress.py:125-127), rows =
-  // A.cols for the column basis, A.rows for the row basis.
-  const uint64_t oseed = child_seed(seed, "omega");
-  float* omega = side == 0 ? Pn : Pm;
+  CNMF_CUDA(cudaMemsetAsync(c.sc.G, 0, (size_t)S * S * 8, st));
+  float* omega = side == 0 ? c.Pn : c.Pm;
   const int64_t orows = side == 0 ? n : m;
   CNMF_CUDA(cudaMemsetAsync(omega, 0, (size_t)orows * S * 4, st));
-  CNMF_TRY(gaussian_fill_ws(oseed, orows, s, 4096, CNMF_F32, omega, S, rng_ws, rng_bytes, st));
+  return gaussian_fill_ws(child_seed(seed, "omega"), orows, s, 4096, CNMF_F32, omega, S, rng_ws, rng_bytes, st);
+}
 
-  int pass_id = 0;
-  // Every pass output P is orthonormalised explicitly with one CholeskyQR
-  // sweep (Gram in fp64, R^{-1} applied in place); the second sweep's
-  // R^{-1} is well conditioned and is deferred into the next finalize.
-  // Deferring the first (ill-conditioned, cond ~ sigma_1/sigma_s) R^{-1}
-  // instead would amplify the fp32 pass error by that condition number.
-  float* cur;
-  if (side == 0) {
-    CNMF_TRY(pass_forward(A, m, n, lda, Pn, S, Pm, st));
-    cur = Pm;
+// The next of the 2w+1 passes over A: the first streams the test matrix, the
+// others alternate transpose / forward (power iteration on A A^T or A^T A).
+static int chain_pass(Chain& c, cudaStream_t st) {
+  if (c.cur == nullptr) {
+    if (c.side == 0) {
+      CNMF_TRY(pass_forward(c.A, c.m, c.n, c.lda, c.Pn, c.S, c.Pm, st));
+      c.cur = c.Pm;
+    } else {
+      CNMF_TRY(pass_transpose(c.A, c.m, c.n, c.lda, c.Pm, c.S, c.Pn, st));
+      c.cur = c.Pn;
+    }
   } else {
-    CNMF_TRY(pass_transpose(A, m, n, lda, Pm, S, Pn, st));
-    cur = Pn;
-  }
-  int64_t cur_rows = side == 0 ? m : n;
-  // One explicit CholeskyQR sweep per pass output: Gram + factor in one
-  // launch, then R^{-1} applied in place. The pass inputs need not be
-  // orthonormal to working precision -- any upper-triangular transform keeps
-  // the leading column spans, and the next output is orthonormalised again --
-  // so the second (polishing) sweep runs only once, on the final basis.
-  auto orth_sweep = [&]() -> int {
-    CNMF_TRY(panel_finalize_chol(cur, cur_rows, S, nullptr, sc.G, s, sc.T, nullptr, sc.info, pass_id, sc.counter,
-                                 st, 1));
-    return CNMF_OK;
-  };
-  CNMF_TRY(orth_sweep());
-  for (int t = 0; t < 2 * w; ++t) {
-    ++pass_id;
-    const bool to_n = (cur == Pm);  // next output has n rows: transpose pass
-    float* nxt = to_n ? Pn : Pm;
+    ++c.pass_id;
+    const bool to_n = (c.cur == c.Pm);  // next output has n rows: transpose pass
+    float* nxt = to_n ? c.Pn : c.Pm;
     if (to_n)
-      CNMF_TRY(pass_transpose(A, m, n, lda, cur, S, nxt, st));
+      CNMF_TRY(pass_transpose(c.A, c.m, c.n, c.lda, c.cur, c.S, nxt, st));
     else
-      CNMF_TRY(pass_forward(A, m, n, lda, cur, S, nxt, st));
-    cur = nxt;
-    cur_rows = to_n ? n : m;
-    CNMF_TRY(orth_sweep());
+      CNMF_TRY(pass_forward(c.A, c.m, c.n, c.lda, c.cur, c.S, nxt, st));
+    c.cur = nxt;
   }
-  CNMF_TRY(finish_basis(cur, cur_rows, s, S, sc, nullptr, pass_id, st));
+  c.cur_rows = (c.cur == c.Pm) ? c.m : c.n;
+  return CNMF_OK;
+}
+
+static SweepPanel chain_panel(const Chain& c) {
+  return SweepPanel{c.cur, c.cur_rows, c.sc.G, c.sc.T, nullptr, c.sc.info, c.sc.counter, c.s, c.pass_id, 0};
+}
+
+// Every pass output P is orthonormalised with one explicit CholeskyQR sweep
+// (Gram in fp64, R^{-1} applied in place); deferring the first,
+// ill-conditioned R^{-1} (cond ~ sigma_1 / sigma_s) past the next pass would
+// amplify the fp32 pass error by that condition number. The pass inputs need
+// not be orthonormal to working precision -- any upper-triangular transform
+// keeps the leading column spans, and the next output is orthonormalised
+// again -- so the second (polishing) sweep runs once, on the final basis.
+static int chains_run(Chain* c, int nc, cudaStream_t st) {
+  SweepPanel p[2];
+  for (int t = 0; t < 2 * c[0].w + 1; ++t) {
+    for (int i = 0; i < nc; ++i) CNMF_TRY(chain_pass(c[i], st));
+    for (int i = 0; i < nc; ++i) p[i] = chain_panel(c[i]);
+    CNMF_TRY(panel_sweep(p, nc, c[0].S, st));
+  }
+  for (int i = 0; i < nc; ++i) p[i] = chain_panel(c[i]);
+  return panel_sweep(p, nc, c[0].S, st);
+}
+
+int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed, int side,
+                        float* Q, void* ws, size_t ws_bytes, cudaStream_t st, bool check) {
+  Chain c;
+  CNMF_TRY(chain_begin(c, A, m, n, lda, s, w, seed, side, Q, ws, ws_bytes, st));
+  CNMF_TRY(chains_run(&c, 1, st));
   if (!check) return CNMF_OK;
-  return check_info(sc.info, side == 0 ? "column basis" : "row basis", st);
+  return check_info(c.sc.info, side == 0 ? "column basis" : "row basis", st);
+}
+
+// Both range finders of the compressed NMF (nmf.py:120-135: column basis of
+// A and row basis, independent seeds) interleaved on one stream: pass of the
+// column chain, pass of the row chain, then ONE sweep launch that
+// orthonormalises both outputs (their Gram passes, factorisations and
+// applies overlap). Each chain is numerically exactly structured_compress.
+int structured_compress_pair(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed_left,
+                             uint64_t seed_right, float* QL, float* QR, void* wsL, void* wsR, size_t ws_bytes,
+                             cudaStream_t st) {
+  Chain c[2];
+  CNMF_TRY(chain_begin(c[0], A, m, n, lda, s, w, seed_left, 0, QL, wsL, ws_bytes, st));
+  CNMF_TRY(chain_begin(c[1], A, m, n, lda, s, w, seed_right, 1, QR, wsR, ws_bytes, st));
+  return chains_run(c, 2, st);
 }
 
 int cholesky_inverse(double* G, int s, int S, double* Rinv, double* R, cudaStream_t st) {
@@ -239,9 +282,10 @@ int orthonormalize_async(float* P, int64_t rows, int s, double* R, void* ws, siz
   if (S < 0) return fail(CNMF_ERR_ARGUMENT, "width must be <= 128");
   if (ws_bytes < small_bytes(S)) return fail(CNMF_ERR_ARGUMENT, "workspace too small");
   Scratch sc = carve_small(ws, S);
-  CNMF_TRY(panel_finalize_chol(P, rows, S, nullptr, sc.G, s, sc.T, nullptr, sc.info, 0, sc.counter, st, 1));
-  CNMF_TRY(finish_basis(P, rows, s, S, sc, R, 0, st));
-  return CNMF_OK;
+  SweepPanel p{P, rows, sc.G, sc.T, nullptr, sc.info, sc.counter, s, 0, 0};
+  CNMF_TRY(panel_sweep(&p, 1, S, st));
+  p.R = R;  // CholeskyQR2: R of the second sweep
+  return panel_sweep(&p, 1, S, st);
 }
 
 // Rinv = R^{-1} of G = R^T R (G consumed), failures recorded in ws

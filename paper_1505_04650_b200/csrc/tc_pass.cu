@@ -37,6 +37,9 @@
 namespace cnmf {
 namespace {
 
+#ifndef CNMF_X
+#define CNMF_X 0  // probe-only knockouts (tools/tc_variant.sh); 0 in the library
+#endif
 constexpr int BMT = 128;              // output rows per tile (TMEM lanes)
 constexpr int BKT = 32;               // K per stage (one 128B swizzle atom of fp32)
 
@@ -155,9 +158,15 @@ struct TcCfg {
   static constexpr int BSPL = PAIR ? BKT * (S + S / 2) * 4 : BKT * 2 * S * 4;
   // ring depths: a CTA pair's cross-CTA arrivals add ~1 us of latency to the
   // panel and TMEM rings, so those are deeper there
+#ifdef CNMF_TC_RINGS  // (ST32, SSP32, AST32) override for probes
+  static constexpr int ST = (S == 32) ? CNMF_TC_ST : 7;
+  static constexpr int SSP = (S == 32) ? CNMF_TC_SSP : 3;
+  static constexpr int AST = (S == 32) ? CNMF_TC_AST : 4;
+#else
   static constexpr int ST = (S == 32) ? (PAIR ? 9 : 10) : 7;  // stage ring (DRAM bytes in flight per SM)
   static constexpr int SSP = PAIR ? (S == 32 ? 6 : 4) : 3;    // split panel ring
   static constexpr int AST = PAIR && S == 32 ? 6 : 4;         // TMEM ring of split A tiles
+#endif
   static constexpr int MD = SSP > AST ? SSP : AST;    // "MMA of K tile j done" ring (>= SSP, AST)
   static constexpr int KB = 2;                        // K tiles per tensor-core accumulation block
   static_assert(MD >= SSP && MD >= AST, "one MMA-done ring serves both consumers");
@@ -253,14 +262,21 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
 // [hi; lo]) released by the MMA commit; TMEM ring of split A tiles (hi and lo,
 // 32 columns each, lane = output row) filled with tcgen05.st and consumed by
 // A-from-TMEM MMAs; double-buffered TMEM accumulators.
-// Split-K launches reduce shared output tiles with red.global.add, so the
-// output must start at zero: every CTA zeroes its slice of rows at start-up
-// and counts itself in `arrived`; an epilogue polls the count before its
-// first reduction (long satisfied by then). The last CTA to finish resets
-// the pair for the next launch that draws this slot.
-struct ZSync {
-  unsigned arrived, finished;
+// Split-K launches reduce shared output tiles deterministically: a CTA that
+// covers only part of an output tile's K range stores its fp32 partial into
+// slot (its index among the tile's contributors) of a scratch buffer and
+// counts itself in on the tile's counter; the last contributor sums the slots
+// in slot order and writes the tile (and resets the counter). The result is
+// independent of CTA timing, so the range finder is bit-reproducible.
+struct SplitK {
+  float* part;       // [nblocks * CW][maxsplit][128][S]
+  unsigned* count;   // [nblocks * CW], zero between launches
+  int maxsplit;
 };
+
+// CTA (work-item) index owning unit t of U units spread over G items
+// (item b owns [b U / G, (b + 1) U / G))
+__device__ __forceinline__ int64_t item_of(int64_t t, int64_t U, int64_t G) { return ((t + 1) * G - 1) / U; }
 
 //
 // PAIR: a cluster of two CTAs on one TPC shares every MMA (cta_group::2,
@@ -272,7 +288,7 @@ struct ZSync {
 template <int S, bool TRANS, bool PAIR>
 __global__ void __launch_bounds__(TcCfg<S, TRANS, PAIR>::THREADS, 1)
     pass_tc(const __grid_constant__ TmaDesc tA, const __grid_constant__ TmaDesc tB, float* __restrict__ out,
-            int64_t P, int nt, int64_t nblocks, int whole, ZSync* __restrict__ zs) {
+            int64_t P, int nt, int64_t nblocks, int whole, const SplitK sk) {
   using C = TcCfg<S, TRANS, PAIR>;
   constexpr int CW = PAIR ? 2 : 1;          // CTAs per work item
   constexpr int TILE_ROWS = CW * BMT;       // output rows per work item
@@ -286,6 +302,7 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS, PAIR>::THREADS, 1)
   uint64_t* tfull = afull + C::AST;                            // [2] accumulator ready
   uint64_t* tempty = tfull + 2;                                // [2] accumulator drained
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  volatile unsigned* epi_flag = (volatile unsigned*)(tmem_slot + 1);  // last-contributor flag of the epilogue
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = PAIR ? (blockIdx.x & 1) : 0;  // cluster dims (2, 1, 1)
@@ -328,21 +345,12 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS, PAIR>::THREADS, 1)
   // programmatic dependent launch: everything above overlapped the tail of
   // the previous kernel in the stream; its outputs are visible from here on
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (zs != nullptr) {
-    const int64_t z0 = blockIdx.x * P / gridDim.x, z1 = (blockIdx.x + 1) * P / gridDim.x;
-    float4* o4 = reinterpret_cast<float4*>(out + z0 * S);
-    for (int64_t i = threadIdx.x; i < (z1 - z0) * S / 4; i += blockDim.x) o4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
   tc_fence_before();
   if constexpr (PAIR)
     cluster_sync();  // both CTAs' barriers initialised before any remote arrival
   else
     __syncthreads();
   tc_fence_after();
-  if (zs != nullptr && threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(&zs->arrived, 1u);
-  }
   const uint32_t tmem = *tmem_slot;
 
   // Every role walks the same unit sequence u0..u1-1 with incremental
@@ -418,24 +426,50 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS, PAIR>::THREADS, 1)
         const int64_t t0 = ob * nt;  // first unit of this output tile
         const bool owned = (t0 >= u0) && (t0 + nt <= u1);
         const int64_t row = ob * TILE_ROWS + rank * BMT + row_in_tile;
-        if (!owned && zs != nullptr) {  // every CTA's zeroing must have landed
-          if (lane == 0) {
-            unsigned v;
-            do {
-              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&zs->arrived) : "memory");
-            } while (v < gridDim.x);
-          }
-          __syncwarp();
-        }
-        if (row < P) {
-          float* dst = out + row * S + cg;
+        if (owned) {
+          if (row < P) {
+            float* dst = out + row * S + cg;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            if (owned)
-              *(float4*)(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-            else
-              red_add_v4(dst + j, acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            for (int j = 0; j < 32; j += 4) *(float4*)(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
           }
+        } else {
+          // partial of a shared tile: slot = this item's index among the tile's contributors
+          const int64_t first = item_of(t0, U, G), last = item_of(t0 + nt - 1, U, G);
+          const int nsplit = (int)(last - first + 1);
+          const int64_t tid_tile = ob * CW + rank;
+          float* base = sk.part + (tid_tile * sk.maxsplit) * (int64_t)(BMT * S);
+          float* mine = base + (b - first) * (int64_t)(BMT * S) + row_in_tile * S + cg;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) __stcg((float4*)(mine + j), make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
+          __threadfence();
+          asm volatile("bar.sync 1, %0;" ::"n"(C::NEPI * 32) : "memory");
+          if (warp == kWarpEpi0 && lane == 0)
+            *epi_flag = (atomicAdd(sk.count + tid_tile, 1u) == (unsigned)nsplit - 1) ? 1u : 0u;
+          asm volatile("bar.sync 1, %0;" ::"n"(C::NEPI * 32) : "memory");
+          if (*epi_flag) {  // last contributor: sum the slots in slot order
+            __threadfence();
+            float sum[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sum[j] = 0.f;
+            for (int q2 = 0; q2 < nsplit; ++q2) {
+              const float* src = base + q2 * (int64_t)(BMT * S) + row_in_tile * S + cg;
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                const float4 v = __ldcg((const float4*)(src + j));
+                sum[j] += v.x;
+                sum[j + 1] += v.y;
+                sum[j + 2] += v.z;
+                sum[j + 3] += v.w;
+              }
+            }
+            if (row < P) {
+              float* dst = out + row * S + cg;
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) *(float4*)(dst + j) = make_float4(sum[j], sum[j + 1], sum[j + 2], sum[j + 3]);
+            }
+            if (warp == kWarpEpi0 && lane == 0) sk.count[tid_tile] = 0u;  // every contributor has arrived
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(C::NEPI * 32) : "memory");  // epi_flag reuse
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[j] = 0.f;
@@ -464,7 +498,7 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS, PAIR>::THREADS, 1)
         const int n = 32 * (u >> 1) + lane;  // lanes read consecutive columns
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const float v = raw[(16 * (u & 1) + k) * S + n];
+          const float v = CNMF_X == 3 ? (float)(k + lane) : raw[(16 * (u & 1) + k) * S + n];
           h[t][k] = tf32_rn(v);
           l[t][k] = tf32_rn(v - h[t][k]);
         }
@@ -556,6 +590,9 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS, PAIR>::THREADS, 1)
             const uint64_t bhi = smem_desc(sb + S * 128 + 32 * k, 16, 1024);
             tc_mma_ts2(dcat, ahi + 8 * k, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
             tc_mma_ts2(dlo, alo + 8 * k, bhi, idesc_hi, 1u);      //            + A_lo X_hi
+          } else if (CNMF_X == 1) {
+          } else if (CNMF_X == 5) {
+            tc_mma_ts(dcat, ahi + 8 * k, bcat, idesc_cat, acc);
           } else {
             tc_mma_ts(dcat, ahi + 8 * k, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
             tc_mma_ts(dlo, alo + 8 * k, bcat, idesc_hi, 1u);     //            + A_lo X_hi
@@ -591,7 +628,10 @@ __global__ void __launch_bounds__(TcCfg<S, TRANS, PAIR>::THREADS, 1)
       mbar_wait(&full[r.i], r.ph);
       if (threadIdx.x == 64) TC_TRACE(1);
       float hi[16], lo[16];
-      if (!TRANS) {
+      if (CNMF_X == 2) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) hi[k] = (float)(lane + k);
+      } else if (!TRANS) {
         // row r of the K-major SW128 tile: 16 B chunk c at chunk c ^ (r & 7)
         const unsigned char* rowp = smem + r.i * C::STAGE + row_in_tile * 128;
 #pragma unroll
@@ -647,10 +687,6 @@ done:
     __syncthreads();
   tc_fence_after();
   TC_SPAN(1);
-  if (zs != nullptr && threadIdx.x == 0 && atomicAdd(&zs->finished, 1u) == gridDim.x - 1) {
-    zs->arrived = 0u;
-    zs->finished = 0u;
-  }
   if (warp == kWarpMma)
   {
     if constexpr (PAIR)
@@ -685,15 +721,38 @@ int launch_tc_t(const float* A, int64_t m, int64_t n, int64_t lda, const float* 
   const int64_t slots = kNumSMs / CW;             // CTAs (pairs) per wave
   const int whole = nblocks >= 16 * slots;
   const int64_t grid = CW * std::min<int64_t>(slots, whole ? nblocks : nblocks * nt);
-  ZSync* zs = nullptr;
+  SplitK sk{nullptr, nullptr, 0};
   if (!whole) {
-    static ZSync* ring = nullptr;
+    // per-launch scratch for the deterministic split-K reduction, from a small
+    // ring (kernels on one stream reuse it in order; grown outside capture)
+    const int64_t U = nblocks * nt, G = grid / CW;
+    sk.maxsplit = (int)(ceil_div(nt, U / G) + 1);
+    const size_t part_bytes = (size_t)nblocks * CW * sk.maxsplit * BMT * S * 4;
+    struct Slot {
+      float* part = nullptr;
+      unsigned* count = nullptr;
+      size_t part_cap = 0, count_cap = 0;
+    };
+    static Slot ring[4];
     static unsigned next = 0;
-    if (ring == nullptr) {
-      CNMF_CUDA(cudaMalloc(&ring, 64 * sizeof(ZSync)));
-      CNMF_CUDA(cudaMemset(ring, 0, 64 * sizeof(ZSync)));
+    Slot& sl = ring[next++ % 4];
+    const size_t count_bytes = (size_t)nblocks * CW * 4;
+    if (sl.part_cap < part_bytes || sl.count_cap < count_bytes) {
+      cudaStreamCaptureStatus cs;
+      CNMF_CUDA(cudaStreamIsCapturing(st, &cs));
+      if (cs != cudaStreamCaptureStatusNone)
+        return fail(CNMF_ERR_CUDA, "pass scratch must be sized by an eager call before graph capture");
+      CNMF_CUDA(cudaStreamSynchronize(st));
+      if (sl.part) cudaFree(sl.part);
+      if (sl.count) cudaFree(sl.count);
+      sl.part_cap = std::max(part_bytes, sl.part_cap);
+      sl.count_cap = std::max(count_bytes, sl.count_cap);
+      CNMF_CUDA(cudaMalloc(&sl.part, sl.part_cap));
+      CNMF_CUDA(cudaMalloc(&sl.count, sl.count_cap));
+      CNMF_CUDA(cudaMemset(sl.count, 0, sl.count_cap));
     }
-    zs = ring + (next++ % 64);
+    sk.part = sl.part;
+    sk.count = sl.count;
   }
   static bool attr = false;
   if (!attr) {
@@ -722,7 +781,7 @@ int launch_tc_t(const float* A, int64_t m, int64_t n, int64_t lda, const float* 
   at[1].val.clusterDim.z = 1;
   lc.attrs = at;
   lc.numAttrs = PAIR ? 2 : 1;
-  CNMF_CUDA(cudaLaunchKernelEx(&lc, pass_tc<S, TRANS, PAIR>, tA, tB, out, P, nt, nblocks, whole, zs));
+  CNMF_CUDA(cudaLaunchKernelEx(&lc, pass_tc<S, TRANS, PAIR>, tA, tB, out, P, nt, nblocks, whole, sk));
   CNMF_LAUNCH_CHECK();
   if (e0) {
     CNMF_CUDA(cudaEventRecord(e1, st));

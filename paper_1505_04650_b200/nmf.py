@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .compress import CompressionConfig, _check, _compress, adjust_config
+from .compress import CompressionConfig, _check, _compress_pair, adjust_config
 from .device import MASK64, DeviceMatrix, as_device64, out, stream, zeros
 from .errors import ArgumentError, DivergenceError, UndefinedMetricError
 from .rng import Rng, child_seed
@@ -80,8 +80,8 @@ def _rel_error(A, X, Yt):
 
 
 def _enqueue_problem(A, cfg):
-    left, _ = _compress(A, replace(cfg, seed=child_seed(cfg.seed, "left-basis")), 0, check=False)
-    right, _ = _compress(A, replace(cfg, seed=child_seed(cfg.seed, "right-basis")), 1, check=False)
+    left, right = _compress_pair(A, replace(cfg, seed=child_seed(cfg.seed, "left-basis")),
+                                 replace(cfg, seed=child_seed(cfg.seed, "right-basis")))
     s = cfg.basis_cols
     S = left.panel.shape[1]
     z = zeros((A.n, S))

@@ -19,11 +19,11 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
   return d;
 }
 
-__host__ __device__ constexpr uint32_t idesc(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc(int n, int m = 128) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int MM = 128>
 __global__ void __launch_bounds__(128, 1) probe(int iters, long long* cycles) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ uint32_t slot;
@@ -54,14 +54,14 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, long long* cycles) {
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\n"
               "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem),
-              "r"(tmem + 256 + 8 * k), "l"(bd), "r"(idesc(N))
+              "r"(tmem + 256 + 8 * k), "l"(bd), "r"(idesc(N, MM))
               : "memory");
         } else {
           const uint64_t ad = sdesc(a_s + 32 * k);
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\n"
               "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-              "l"(ad), "l"(bd), "r"(idesc(N))
+              "l"(ad), "l"(bd), "r"(idesc(N, MM))
               : "memory");
         }
       }
@@ -87,6 +87,8 @@ __global__ void __launch_bounds__(128, 1) pattern(int iters, int commits, int mo
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar[4];
   __shared__ __align__(8) uint64_t ready;
+  __shared__ int stop_flag;
+  if (threadIdx.x == 0) stop_flag = 0;
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 4; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su(&bar[i])));
@@ -114,19 +116,19 @@ __global__ void __launch_bounds__(128, 1) pattern(int iters, int commits, int mo
                 su(&ready))
             : "memory");
       if (mode & 1) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a = tmem + 256 + (i & 3) * 64;
+      const uint32_t a = tmem + 256 + ((mode & 512) ? 0 : (i & 3) * 64);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint64_t bd = sdesc(b_s + 32 * k);
         asm volatile(
             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
             "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem),
-            "r"(a + 8 * k), "l"(bd), "r"(idesc(2 * S)), "r"(k)
+            "r"(a + 8 * k), "l"(bd), "r"(idesc(2 * S)), "r"((mode & 256) ? 1 : k)
             : "memory");
-        asm volatile(
+        if (!(mode & 1024)) asm volatile(
             "{\n.reg .pred p;\nsetp.ne.b32 p, 1, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + S),
-            "r"(a + 32 + 8 * k), "l"(bd), "r"(idesc(S))
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem + ((mode & 64) ? 0 : (mode & 16) ? 2 * S : S)),
+            "r"(a + ((mode & 128) ? 0 : 32) + 8 * k), "l"((mode & 2048) ? sdesc(b_s + 8192 + 32 * k) : bd), "r"(idesc((mode & 32) ? 2 * S : S))
             : "memory");
       }
       for (int c = 0; c < commits; ++c)
@@ -141,6 +143,30 @@ __global__ void __launch_bounds__(128, 1) pattern(int iters, int commits, int mo
             su(&bar[3]))
         : "memory");
     cycles[blockIdx.x] = clock64() - t0;
+    stop_flag = 1;
+  } else if (warp > 0 && (mode & 12)) {
+    const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + 448;
+    uint32_t r[16] = {};
+    while (*(volatile int*)&stop_flag == 0) {
+      for (int rep = 0; rep < 16; ++rep) {
+        if (mode & 4)
+          asm volatile(
+              "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+              "%13, %14, %15, %16};\ntcgen05.wait::st.sync.aligned;" ::"r"(ta),
+              "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+              "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+              : "memory");
+        if (mode & 8)
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+              "%14, %15}, [%16];\ntcgen05.wait::ld.sync.aligned;"
+              : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+              : "r"(ta)
+              : "memory");
+      }
+    }
+    if (r[3] == 12345) cycles[0] = 0;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -162,23 +188,26 @@ void run_pattern(long long* d, int commits, int mode = 0) {
          cudaGetErrorString(e));
 }
 
-template <int N, bool TS>
+template <int N, bool TS, int MM = 128>
 void run(long long* d) {
   const int iters = 4096;
-  cudaFuncSetAttribute(probe<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
-  probe<N, TS><<<148, 128, 65 * 1024>>>(iters, d);
+  cudaFuncSetAttribute(probe<N, TS, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
+  probe<N, TS, MM><<<148, 128, 65 * 1024>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[148];
   cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
   double avg = 0;
   for (int i = 0; i < 148; ++i) avg += h[i];
   avg /= 148;
-  printf("N=%3d %s: %7.1f cycles/MMA  (%s)\n", N, TS ? "TS" : "SS", avg / (iters * 4.0), cudaGetErrorString(e));
+  printf("M=%3d N=%3d %s: %7.1f cycles/MMA  (%s)\n", MM, N, TS ? "TS" : "SS", avg / (iters * 4.0), cudaGetErrorString(e));
 }
 
 int main() {
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
+  run<64, false, 64>(d);
+  run<128, false, 64>(d);
+  run<256, false, 64>(d);
   run<32, false>(d);
   run<64, false>(d);
   run<128, false>(d);
@@ -191,5 +220,22 @@ int main() {
   for (int c = 0; c <= 2; ++c) run_pattern<64>(d, c);
   for (int m = 1; m <= 3; ++m) run_pattern<32>(d, 1, m);
   for (int m = 1; m <= 3; ++m) run_pattern<64>(d, 1, m);
+  for (int c = 0; c <= 2; ++c) run_pattern<32>(d, c, 16);
+  run_pattern<32>(d, 0, 48 + 64);
+  run_pattern<32>(d, 0, 48 + 128);
+  run_pattern<32>(d, 0, 48 + 64 + 128);
+  run_pattern<32>(d, 0, 1024);
+  run_pattern<32>(d, 0, 1024 + 768);
+  run_pattern<32>(d, 0, 2048);
+  run_pattern<32>(d, 0, 2048 + 768 + 32 + 64);
+  run_pattern<32>(d, 0, 256);
+  run_pattern<32>(d, 0, 512);
+  run_pattern<32>(d, 0, 768);
+  run_pattern<32>(d, 1, 256);
+  run_pattern<32>(d, 1, 768);
+  run_pattern<32>(d, 2, 768);
+  run_pattern<32>(d, 1, 4);
+  run_pattern<32>(d, 1, 8);
+  run_pattern<32>(d, 1, 12);
   return 0;
 }
