@@ -20,10 +20,10 @@
 // for exactness).
 #include <algorithm>
 #include <cmath>
-#include <mutex>
 #include <vector>
 
 #include "common.cuh"
+#include "glibc_log1p.cuh"
 #include "ziggurat_tables.h"
 
 namespace cnmf {
@@ -102,98 +102,14 @@ __device__ __forceinline__ int64_t chunk_of_seg(const Layout& L, int64_t g) {
   return c < L.nchunks - 1 ? c : L.nchunks - 1;
 }
 
-// ---- correctly rounded log(w), w in (0, 1], in double-double arithmetic ----
-struct DD {
-  double hi, lo;
-};
-__device__ __forceinline__ DD two_sum(double a, double b) {
-  const double s = a + b, bb = s - a;
-  return {s, (a - (s - bb)) + (b - bb)};
-}
-__device__ __forceinline__ DD dd_add(DD a, DD b) {
-  DD s = two_sum(a.hi, b.hi);
-  return two_sum(s.hi, s.lo + a.lo + b.lo);
-}
-__device__ __forceinline__ DD dd_mul(DD a, DD b) {
-  const double p = a.hi * b.hi;
-  const double e = fma(a.hi, b.hi, -p) + (a.hi * b.lo + a.lo * b.hi);
-  return two_sum(p, e);
-}
-__device__ DD dd_div(DD a, DD b) {
-  const double q1 = a.hi / b.hi;
-  DD r = dd_add(a, dd_mul(DD{-q1, 0.0}, b));
-  const double q2 = r.hi / b.hi;
-  r = dd_add(r, dd_mul(DD{-q2, 0.0}, b));
-  const double q3 = r.hi / b.hi;
-  return dd_add(two_sum(q1, q2), DD{q3, 0.0});
-}
-// log(w) = e ln2 + 2 atanh((m-1)/(m+1)), m in [sqrt(1/2), sqrt(2)), series to
-// ~2^-110; rounded once at the end.
-// 1/(2k+1) as double-double pairs (exact rational rounded twice), so the
-// series below needs no double-double division per term: the tail path was
-// the slowest warp of every fill (tools/rng_probe.cu: 44 us vs 7 us median)
-__device__ const double kInvOdd[25][2] = {
-    {0x1.0000000000000p+0, 0x0.0p+0},  // 1/1
-    {0x1.5555555555555p-2, 0x1.5555555555555p-56},  // 1/3
-    {0x1.999999999999ap-3, -0x1.999999999999ap-57},  // 1/5
-    {0x1.2492492492492p-3, 0x1.2492492492492p-57},  // 1/7
-    {0x1.c71c71c71c71cp-4, 0x1.c71c71c71c71cp-58},  // 1/9
-    {0x1.745d1745d1746p-4, -0x1.745d1745d1746p-59},  // 1/11
-    {0x1.3b13b13b13b14p-4, -0x1.3b13b13b13b14p-58},  // 1/13
-    {0x1.1111111111111p-4, 0x1.1111111111111p-60},  // 1/15
-    {0x1.e1e1e1e1e1e1ep-5, 0x1.e1e1e1e1e1e1ep-61},  // 1/17
-    {0x1.af286bca1af28p-5, 0x1.af286bca1af28p-59},  // 1/19
-    {0x1.8618618618618p-5, 0x1.8618618618618p-59},  // 1/21
-    {0x1.642c8590b2164p-5, 0x1.642c8590b2164p-60},  // 1/23
-    {0x1.47ae147ae147bp-5, -0x1.eb851eb851eb8p-61},  // 1/25
-    {0x1.2f684bda12f68p-5, 0x1.2f684bda12f68p-59},  // 1/27
-    {0x1.1a7b9611a7b96p-5, 0x1.1a7b9611a7b96p-61},  // 1/29
-    {0x1.0842108421084p-5, 0x1.0842108421084p-60},  // 1/31
-    {0x1.f07c1f07c1f08p-6, -0x1.f07c1f07c1f08p-61},  // 1/33
-    {0x1.d41d41d41d41dp-6, 0x1.0750750750750p-60},  // 1/35
-    {0x1.bacf914c1bad0p-6, -0x1.bacf914c1bad0p-60},  // 1/37
-    {0x1.a41a41a41a41ap-6, 0x1.0690690690690p-60},  // 1/39
-    {0x1.8f9c18f9c18fap-6, -0x1.f3831f3831f38p-61},  // 1/41
-    {0x1.7d05f417d05f4p-6, 0x1.7d05f417d05f4p-62},  // 1/43
-    {0x1.6c16c16c16c17p-6, -0x1.f49f49f49f49fp-61},  // 1/45
-    {0x1.5c9882b931057p-6, 0x1.310572620ae4cp-61},  // 1/47
-    {0x1.4e5e0a72f0539p-6, 0x1.e0a72f0539783p-60},  // 1/49
-};
-
-__device__ double cr_log(double w) {
-  int e;
-  double m = frexp(w, &e);
-  if (m < 0.7071067811865476) {
-    m *= 2.0;
-    e -= 1;
-  }
-  const DD s = dd_div(DD{m - 1.0, 0.0}, two_sum(m, 1.0));
-  const DD z = dd_mul(s, s);
-  DD p = DD{kInvOdd[24][0], kInvOdd[24][1]};
-  for (int k = 23; k >= 0; --k) p = dd_add(dd_mul(p, z), DD{kInvOdd[k][0], kInvOdd[k][1]});
-  const DD lm = dd_mul(DD{2.0 * s.hi, 2.0 * s.lo}, p);
-  const DD r = dd_add(dd_mul(DD{(double)e, 0.0}, DD{0x1.62e42fefa39efp-1, 0x1.abc9e3b39803fp-56}), lm);
-  return r.hi + r.lo;
-}
-
-// A tail variate (|x| > r) is finished on the host with the C library's
-// log1p, the very call numpy makes: that libm is not correctly rounded (it
-// differs from the exact log in ~7% of arguments), so bit-exactness with the
-// reference needs the same function. The device decides acceptance with a
-// correctly rounded log (a flip needs the two to straddle a rounding
-// boundary of the acceptance test, ~1e-16 per draw).
-struct TailRec {
-  int64_t offset;  // element offset into the output
-  uint64_t u1;     // accepted first uniform (raw)
-  int32_t negative;
-  int32_t pad;
-};
-
+// A tail variate (|x| > r): numpy draws xx = -log1p(-u1) / r and
+// yy = -log1p(-u2) with the C library's log1p (random_standard_normal), which
+// is not correctly rounded; glibc_log1p.cuh restates that exact function, so
+// the acceptance test and the variate are bit-identical on the device.
 // Slow path of numpy's random_standard_normal starting at raw position `pos`
 // whose first draw `r0` failed the fast acceptance. Returns the variate and
 // sets *next to the position after the last consumed draw.
-__device__ double slow_normal(uint64_t key, int64_t pos, uint64_t r0, int64_t* next, uint64_t* tail_u1 = nullptr,
-                              int* tail_neg = nullptr) {
+__device__ double slow_normal(uint64_t key, int64_t pos, uint64_t r0, int64_t* next) {
   uint64_t r = r0;
   int64_t p = pos + 1;
   for (;;) {
@@ -209,21 +125,15 @@ __device__ double slow_normal(uint64_t key, int64_t pos, uint64_t r0, int64_t* n
     }
     if (idx == 0) {
       for (;;) {
-        const uint64_t r1 = philox_raw(key, (uint64_t)p);
-        const double u1 = raw_to_unit(r1);
+        const double u1 = raw_to_unit(philox_raw(key, (uint64_t)p));
         const double u2 = raw_to_unit(philox_raw(key, (uint64_t)(p + 1)));
         p += 2;
-        // 1 - u is exact for u = k 2^-53, so log1p(-u) = log(1 - u)
-        const double xx = __dmul_rn(-cnmf_zig::kTailInvR, cr_log(1.0 - u1));
-        const double yy = -cr_log(1.0 - u2);
+        const double xx = __dmul_rn(-cnmf_zig::kTailInvR, glibc_log1p(-u1));
+        const double yy = -glibc_log1p(-u2);
         if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
           *next = p;
-          const int neg = (int)((rabs >> 8) & 1);
-          if (tail_u1) {
-            *tail_u1 = r1;
-            *tail_neg = neg;
-          }
-          return neg ? -(cnmf_zig::kTailR + xx) : cnmf_zig::kTailR + xx;
+          const double v = __dadd_rn(cnmf_zig::kTailR, xx);
+          return ((rabs >> 8) & 1) ? -v : v;
         }
       }
     }
@@ -270,8 +180,7 @@ __device__ __forceinline__ void store_variate(T* out, int64_t ld, int64_t cols, 
 // the start bits of the first window [seg_start, seg_start+128) are recorded.
 template <bool WRITE, typename T>
 __device__ int64_t walk(uint64_t key, int64_t head, int64_t stop, int64_t seg_start, uint32_t* chain, T* out,
-                        int64_t ld, int64_t cols, int64_t row0, int64_t k0, int64_t count, int64_t* exit_pos,
-                        TailRec* tails = nullptr, unsigned int* ntails = nullptr, unsigned int tail_cap = 0) {
+                        int64_t ld, int64_t cols, int64_t row0, int64_t k0, int64_t count, int64_t* exit_pos) {
   const int lane = threadIdx.x & 31;
   int64_t k = 0;
   int64_t base = (head / kWin) * kWin;
@@ -338,24 +247,12 @@ __device__ int64_t walk(uint64_t key, int64_t head, int64_t stop, int64_t seg_st
       const int jj = f & 3;
       const uint64_t rf = jj == 0 ? r0 : jj == 1 ? r1 : jj == 2 ? r2 : r3;
       int64_t nxt;
-      uint64_t tu1 = 0;
-      int tneg = -1;
-      const double x = slow_normal(key, base + f, rf, &nxt, &tu1, &tneg);
+      const double x = slow_normal(key, base + f, rf, &nxt);
       if (chain != nullptr && base == seg_start) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) chain[q] |= ((f >> 5) == q) ? (1u << (f & 31)) : 0u;
       }
-      if (WRITE && lane == 0) {
-        store_variate(out, ld, cols, row0, k0 + k, count, x);
-        const int64_t kk = k0 + k;
-        if (tneg >= 0 && tails != nullptr && kk < count) {
-          const unsigned int slot = atomicAdd(ntails, 1u);
-          if (slot < tail_cap) {
-            const int64_t row = row0 + kk / cols, col = kk - (kk / cols) * cols;
-            tails[slot] = TailRec{row * ld + col, tu1, tneg, 0};
-          }
-        }
-      }
+      if (WRITE && lane == 0) store_variate(out, ld, cols, row0, k0 + k, count, x);
       k += 1;
       p = (int)(nxt - base);
     }
@@ -485,8 +382,7 @@ __global__ void k2_anchor_scan(const Layout L, SegState* segs, int* flags) {
 }
 
 template <typename T>
-__global__ void k3_emit(const Layout L, const SegState* segs, const int* flags, T* out, int64_t ld, TailRec* tails,
-                        unsigned int* ntails, unsigned int tail_cap) {
+__global__ void k3_emit(const Layout L, const SegState* segs, const int* flags, T* out, int64_t ld) {
   load_zig_tables();
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (g >= L.total_segs) return;
@@ -498,52 +394,21 @@ __global__ void k3_emit(const Layout L, const SegState* segs, const int* flags, 
   if (st.offset >= sd.count) return;
   const int64_t s1 = (w + 1) * sd.seglen;
   int64_t ex;
-  walk<true, T>(sd.key, st.entry, s1, -1, nullptr, out, ld, L.cols, sd.row0, st.offset, sd.count, &ex, tails,
-                ntails, tail_cap);
+  walk<true, T>(sd.key, st.entry, s1, -1, nullptr, out, ld, L.cols, sd.row0, st.offset, sd.count, &ex);
 }
 
 // Fallback: one warp decodes a whole stream sequentially.
 template <typename T>
-__global__ void k_serial(const Layout L, const int* flags, T* out, int64_t ld, TailRec* tails,
-                         unsigned int* ntails, unsigned int tail_cap) {
+__global__ void k_serial(const Layout L, const int* flags, T* out, int64_t ld) {
   load_zig_tables();
   if (!flags[blockIdx.x]) return;
   const StreamDesc sd = stream_of(L, blockIdx.x);
   int64_t head = 0, k = 0;
   while (k < sd.count) {
     int64_t ex;
-    k += walk<true, T>(sd.key, head, head + 64 * kWin, -1, nullptr, out, ld, L.cols, sd.row0, k, sd.count, &ex,
-                       tails, ntails, tail_cap);
+    k += walk<true, T>(sd.key, head, head + 64 * kWin, -1, nullptr, out, ld, L.cols, sd.row0, k, sd.count, &ex);
     head = ex;
   }
-}
-
-// Tail records to the host (mapped pinned slot): plain stores, one block.
-struct TailSlot {
-  TailRec* recs;      // host pointers
-  double* vals;
-  int64_t* offs;
-  unsigned int* count;
-  TailRec* d_recs;    // device views of the same pinned memory
-  double* d_vals;
-  int64_t* d_offs;
-  unsigned int* d_count;
-  unsigned int cap;
-};
-
-__global__ void export_tail(const TailRec* tails, const unsigned int* ntails, TailRec* dst, unsigned int* dst_count,
-                            unsigned int cap) {
-  const unsigned int n = min(*ntails, cap);
-  for (unsigned int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = tails[i];
-  if (threadIdx.x == 0) *dst_count = *ntails;
-}
-
-template <typename T>
-__global__ void scatter_tail(T* out, const int64_t* offsets, const double* vals, const unsigned int* count,
-                             unsigned int cap) {
-  const unsigned int n = min(*count, cap);
-  for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    out[offsets[i]] = (T)vals[i];
 }
 
 template <typename T>
@@ -571,59 +436,6 @@ __global__ void uniform_kernel(uint64_t key, int64_t rows, int64_t cols, double 
 
 }  // namespace
 
-// Host part of the tail fix-up: runs on a CUDA callback thread when the
-// stream reaches it (no host synchronisation in the caller).
-static void CUDART_CB tail_fixup(void* p) {
-  TailSlot* s = (TailSlot*)p;
-  const unsigned int n = std::min(*s->count, s->cap);
-  for (unsigned int i = 0; i < n; ++i) {
-    const TailRec& r = s->recs[i];
-    const double u1 = (double)(r.u1 >> 11) * (1.0 / 9007199254740992.0);
-    const double xx = -cnmf_zig::kTailInvR * std::log1p(-u1);
-    s->offs[i] = r.offset;
-    s->vals[i] = r.negative ? -(cnmf_zig::kTailR + xx) : cnmf_zig::kTailR + xx;
-  }
-}
-
-// ring of mapped pinned slots (reused round-robin; a slot is rewritten only
-// eight fills later, long after its stream work retired). A slot that must
-// grow grows the whole ring, so a fill captured into a CUDA graph right after
-// an eager fill of the same size never allocates (allocation is illegal
-// during capture).
-static bool grow_slot(TailSlot& s, unsigned int cap) {
-  if (s.recs) cudaFreeHost(s.recs);
-  s.recs = nullptr;
-  s.cap = 0;
-  const size_t bytes = (size_t)cap * (sizeof(TailRec) + 16) + 64;
-  char* h = nullptr;
-  if (cudaHostAlloc((void**)&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return false;
-  char* d = nullptr;
-  if (cudaHostGetDevicePointer((void**)&d, h, 0) != cudaSuccess) return false;
-  s.recs = (TailRec*)h;
-  s.vals = (double*)(h + (size_t)cap * sizeof(TailRec));
-  s.offs = (int64_t*)(h + (size_t)cap * (sizeof(TailRec) + 8));
-  s.count = (unsigned int*)(h + (size_t)cap * (sizeof(TailRec) + 16));
-  s.d_recs = (TailRec*)d;
-  s.d_vals = (double*)(d + (size_t)cap * sizeof(TailRec));
-  s.d_offs = (int64_t*)(d + (size_t)cap * (sizeof(TailRec) + 8));
-  s.d_count = (unsigned int*)(d + (size_t)cap * (sizeof(TailRec) + 16));
-  s.cap = cap;
-  return true;
-}
-
-static TailSlot* tail_slot(unsigned int cap) {
-  static std::mutex mu;
-  static TailSlot ring[8];
-  static unsigned int next = 0;
-  std::lock_guard<std::mutex> lk(mu);
-  TailSlot& s = ring[next++ % 8];
-  if (s.cap < cap) {
-    for (auto& t : ring)
-      if (t.cap < cap && !grow_slot(t, cap)) return nullptr;
-  }
-  return &s;
-}
-
 static Layout make_layout(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_rows) {
   Layout L{};
   L.rows = rows;
@@ -647,41 +459,26 @@ static Layout make_layout(uint64_t seed, int64_t rows, int64_t cols, int64_t chu
 
 size_t gaussian_workspace(int64_t rows, int64_t cols, int64_t chunk_rows) {
   const Layout L = make_layout(0, rows, cols, chunk_rows);
-  const int64_t variates = rows * cols;
-  const size_t cap = (size_t)std::min<int64_t>(variates / 256 + 1024, 1 << 26);
-  return (size_t)L.total_segs * sizeof(SegState) + (size_t)L.nchunks * 4 + 64 + cap * sizeof(TailRec) + 512;
+  return (size_t)L.total_segs * sizeof(SegState) + (size_t)L.nchunks * 4 + 64 + 512;
 }
 
 template <typename T>
 static int gaussian_streams(const Layout& L, T* out, int64_t ld, void* ws, size_t ws_bytes, cudaStream_t stream) {
-  const unsigned int cap = (unsigned int)std::min<int64_t>(L.rows * L.cols / 256 + 1024, 1 << 26);
   if (ws_bytes < gaussian_workspace(L.rows, L.cols, L.chunked ? L.chunk_rows : 0))
     return fail(CNMF_ERR_ARGUMENT, "gaussian_fill: workspace too small");
   char* p = (char*)(((uintptr_t)ws + 15) & ~(uintptr_t)15);
   SegState* d_seg = (SegState*)p;
   p += (size_t)L.total_segs * sizeof(SegState);
   int* d_flags = (int*)p;
-  p += ((size_t)L.nchunks * 4 + 63) & ~(size_t)63;
-  unsigned int* d_ntail = (unsigned int*)p;
-  TailRec* d_tail = (TailRec*)(p + 64);
-  TailSlot* slot = tail_slot(cap);
-  if (slot == nullptr) return fail(CNMF_ERR_CUDA, "pinned tail buffer allocation failed");
-  CNMF_CUDA(cudaMemsetAsync(d_ntail, 0, 4, stream));
   const int wpb = 4;  // warps per block
   const unsigned grid = (unsigned)ceil_div(L.total_segs, wpb);
   k1_speculate<<<grid, 32 * wpb, 0, stream>>>(L, d_seg);
   CNMF_LAUNCH_CHECK();
   k2_anchor_scan<<<(unsigned)L.nchunks, 256, 0, stream>>>(L, d_seg, d_flags);
   CNMF_LAUNCH_CHECK();
-  k3_emit<T><<<grid, 32 * wpb, 0, stream>>>(L, d_seg, d_flags, out, ld, d_tail, d_ntail, cap);
+  k3_emit<T><<<grid, 32 * wpb, 0, stream>>>(L, d_seg, d_flags, out, ld);
   CNMF_LAUNCH_CHECK();
-  k_serial<T><<<(unsigned)L.nchunks, 32, 0, stream>>>(L, d_flags, out, ld, d_tail, d_ntail, cap);
-  CNMF_LAUNCH_CHECK();
-  // tail variates: finish with the C library's log1p on a callback thread
-  export_tail<<<1, 256, 0, stream>>>(d_tail, d_ntail, slot->d_recs, slot->d_count, cap);
-  CNMF_LAUNCH_CHECK();
-  CNMF_CUDA(cudaLaunchHostFunc(stream, tail_fixup, slot));
-  scatter_tail<T><<<8, 256, 0, stream>>>(out, slot->d_offs, slot->d_vals, slot->d_count, cap);
+  k_serial<T><<<(unsigned)L.nchunks, 32, 0, stream>>>(L, d_flags, out, ld);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }

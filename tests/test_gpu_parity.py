@@ -54,6 +54,15 @@ def test_unchunked_stream_bitexact_large():
     assert np.array_equal(got, want)
 
 
+def test_ziggurat_tail_bitexact():
+    # tail variates (|x| > r) take numpy's log1p path (glibc's FMA build,
+    # restated on the device): bit-exact over thousands of tail draws
+    got = C.Rng(2024).standard_normal((1, 8_000_000)).cpu().numpy().ravel()
+    want = O.generator(2024).standard_normal(8_000_000)
+    assert np.count_nonzero(np.abs(want) > 3.6541528853610088) > 1000
+    assert np.array_equal(got, want)
+
+
 def test_uniform_bitexact(golden):
     got = C.Rng(5).child("init-left").uniform((30, 4)).cpu().numpy()
     assert np.array_equal(got, golden["uniform_init_left_seed5"])
