@@ -1,14 +1,14 @@
 // extern "C" entry points (include/cnmf_b200.h). Thin: argument checks and
 // dispatch into the cnmf:: implementations; no torch types cross this line.
 #include "common.cuh"
+#include "pass.cuh"
 
 namespace cnmf {
 const char* last_error();
 int panel_ld(int s);
 int gaussian_fill(uint64_t, int64_t, int64_t, int64_t, int, void*, int64_t, cudaStream_t);
 int uniform_fill(uint64_t, int64_t, int64_t, double, double, int, int, void*, cudaStream_t);
-int pass_forward(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
-int pass_transpose(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
+
 int panel_cross(const float*, const float*, int64_t, int, double*, cudaStream_t);
 int cholesky_inverse(double*, int, int, double*, double*, cudaStream_t);
 int status_reset(void*, int, cudaStream_t);

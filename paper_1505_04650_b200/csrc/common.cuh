@@ -48,6 +48,8 @@ __host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? 
 
 constexpr int kNumSMs = 148;
 
+
+
 // ---------------------------------------------------------------------------
 // Philox4x64-10 (the reference's bit generator, rng.py:49-51), counter-based.
 // Raw draw i of a stream keyed by `key` is word (i & 3) of the block with

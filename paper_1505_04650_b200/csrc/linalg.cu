@@ -15,16 +15,17 @@
 // nothing in exact arithmetic); numerically this is the stable variant.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "chol.cuh"
 #include "common.cuh"
+#include "pass.cuh"
 #include "sweep.cuh"
 
 namespace cnmf {
 
 int panel_ld(int s);
-int pass_forward(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
-int pass_transpose(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
+
 int panel_finalize(float*, int64_t, int, const double*, double*, cudaStream_t);
 int panel_finalize_chol(float*, int64_t, int, const double*, double*, int, double*, double*, int*, int, unsigned*,
                         cudaStream_t, int apply_after = 0);
@@ -130,7 +131,7 @@ struct Chain {
 // matrix (compress.py:125-127; rows = A.cols for the column basis, A.rows for
 // the row basis) into the panel the first pass streams.
 static int chain_begin(Chain& c, const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed,
-                       int side, float* Q, void* ws, size_t ws_bytes, cudaStream_t st) {
+                       int side, float* Q, void* ws, size_t ws_bytes, cudaStream_t st, cudaStream_t omega_st) {
   const int S = panel_ld(s);
   if (S < 0) return fail(CNMF_ERR_ARGUMENT, "basis width must be <= 128");
   if (s < 1 || w < 0) return fail(CNMF_ERR_ARGUMENT, "bad width or power exponent");
@@ -152,15 +153,17 @@ static int chain_begin(Chain& c, const float* A, int64_t m, int64_t n, int64_t l
   c.cur_rows = 0;
   c.pass_id = 0;
   c.sc = carve_small((char*)ws + (size_t)std::max(m, n) * S * 4, S);
-  char* rng_ws = (char*)ws + (size_t)std::max(m, n) * S * 4 + small_bytes(S);
-  const size_t rng_bytes = ws_bytes - ((size_t)std::max(m, n) * S * 4 + small_bytes(S));
+  const size_t used = (size_t)std::max(m, n) * S * 4 + small_bytes(S);
+  char* rng_ws = (char*)ws + used;
+  const size_t rng_bytes = ws_bytes - used;
   init_info<<<1, 1, 0, st>>>(c.sc.info);
   CNMF_LAUNCH_CHECK();
   CNMF_CUDA(cudaMemsetAsync(c.sc.G, 0, (size_t)S * S * 8, st));
   float* omega = side == 0 ? c.Pn : c.Pm;
   const int64_t orows = side == 0 ? n : m;
-  CNMF_CUDA(cudaMemsetAsync(omega, 0, (size_t)orows * S * 4, st));
-  return gaussian_fill_ws(child_seed(seed, "omega"), orows, s, 4096, CNMF_F32, omega, S, rng_ws, rng_bytes, st);
+  CNMF_CUDA(cudaMemsetAsync(omega, 0, (size_t)orows * S * 4, omega_st));
+  return gaussian_fill_ws(child_seed(seed, "omega"), orows, s, 4096, CNMF_F32, omega, S, rng_ws, rng_bytes,
+                          omega_st);
 }
 
 // The next of the 2w+1 passes over A: the first streams the test matrix, the
@@ -201,7 +204,8 @@ static SweepPanel chain_panel(const Chain& c) {
 // again -- so the second (polishing) sweep runs once, on the final basis.
 static int chains_run(Chain* c, int nc, cudaStream_t st) {
   SweepPanel p[2];
-  for (int t = 0; t < 2 * c[0].w + 1; ++t) {
+  const int passes = 2 * c[0].w + 1;
+  for (int t = 0; t < passes; ++t) {
     for (int i = 0; i < nc; ++i) CNMF_TRY(chain_pass(c[i], st));
     for (int i = 0; i < nc; ++i) p[i] = chain_panel(c[i]);
     CNMF_TRY(panel_sweep(p, nc, c[0].S, st));
@@ -213,7 +217,7 @@ static int chains_run(Chain* c, int nc, cudaStream_t st) {
 int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed, int side,
                         float* Q, void* ws, size_t ws_bytes, cudaStream_t st, bool check) {
   Chain c;
-  CNMF_TRY(chain_begin(c, A, m, n, lda, s, w, seed, side, Q, ws, ws_bytes, st));
+  CNMF_TRY(chain_begin(c, A, m, n, lda, s, w, seed, side, Q, ws, ws_bytes, st, st));
   CNMF_TRY(chains_run(&c, 1, st));
   if (!check) return CNMF_OK;
   return check_info(c.sc.info, side == 0 ? "column basis" : "row basis", st);
@@ -224,12 +228,42 @@ int structured_compress(const float* A, int64_t m, int64_t n, int64_t lda, int s
 // column chain, pass of the row chain, then ONE sweep launch that
 // orthonormalises both outputs (their Gram passes, factorisations and
 // applies overlap). Each chain is numerically exactly structured_compress.
+static int side_stream(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join) {
+  static cudaStream_t streams[64] = {};
+  static cudaEvent_t forks[64] = {}, joins[64] = {};
+  int dev = 0;
+  CNMF_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(CNMF_ERR_CUDA, "device index out of range");
+  if (streams[dev] == nullptr) {
+    CNMF_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+    CNMF_CUDA(cudaEventCreateWithFlags(&forks[dev], cudaEventDisableTiming));
+    CNMF_CUDA(cudaEventCreateWithFlags(&joins[dev], cudaEventDisableTiming));
+  }
+  *side = streams[dev];
+  *fork = forks[dev];
+  *join = joins[dev];
+  return CNMF_OK;
+}
+
 int structured_compress_pair(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed_left,
                              uint64_t seed_right, float* QL, float* QR, void* wsL, void* wsR, size_t ws_bytes,
                              cudaStream_t st) {
+  // the two seeded test matrices (small latency-bound grids) are drawn
+  // concurrently: the row chain's on a side stream forked from and joined
+  // back into `st` (two parallel branches inside a graph capture)
+  cudaStream_t side;
+  cudaEvent_t fork, join;
+  CNMF_TRY(side_stream(&side, &fork, &join));
+  CNMF_CUDA(cudaEventRecord(fork, st));
+  CNMF_CUDA(cudaStreamWaitEvent(side, fork, 0));
   Chain c[2];
-  CNMF_TRY(chain_begin(c[0], A, m, n, lda, s, w, seed_left, 0, QL, wsL, ws_bytes, st));
-  CNMF_TRY(chain_begin(c[1], A, m, n, lda, s, w, seed_right, 1, QR, wsR, ws_bytes, st));
+  int rc = chain_begin(c[0], A, m, n, lda, s, w, seed_left, 0, QL, wsL, ws_bytes, st, st);
+  const int rc2 = chain_begin(c[1], A, m, n, lda, s, w, seed_right, 1, QR, wsR, ws_bytes, st, side);
+  // always join (a capture must not be left forked)
+  CNMF_CUDA(cudaEventRecord(join, side));
+  CNMF_CUDA(cudaStreamWaitEvent(st, join, 0));
+  CNMF_TRY(rc);
+  CNMF_TRY(rc2);
   return chains_run(c, 2, st);
 }
 

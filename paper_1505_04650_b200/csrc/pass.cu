@@ -19,6 +19,7 @@
 
 #include "chol.cuh"
 #include "common.cuh"
+#include "pass.cuh"
 
 namespace cnmf {
 namespace {
@@ -586,8 +587,7 @@ int panel_ld(int s) {
   return -1;
 }
 
-int pass_forward_tc(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
-int pass_transpose_tc(const float*, int64_t, int64_t, int64_t, const float*, int, float*, cudaStream_t);
+
 
 // Pass implementation: tcgen05 3xTF32 (default for panel widths 32/64) or the
 // FFMA kernels (CNMF_PASS=ffma, and widths 128).

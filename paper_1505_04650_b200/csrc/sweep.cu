@@ -7,8 +7,8 @@
 // One sweep: every block accumulates the fp64 Gram matrix of its 64-row
 // tiles (fp32 products are exact in fp64) and stores the partial; partials
 // are summed in a fixed order (groups of 16 blocks, then the group sums, each
-// by the group's last-arriving block), so G -- and the whole range finder --
-// is bit-reproducible; the block completing the last group factors
+// by the group's last-arriving block), so G is bit-reproducible for a given
+// panel; the block completing the last group factors
 // G = R^T R (chol.cuh) into T = R^{-1}; the panel's blocks wait for T
 // (cooperative launch: all blocks are resident) and apply it to the tiles
 // they still hold in shared memory.

@@ -1,45 +1,43 @@
 // Streaming passes over A on the 5th-generation tensor cores (tcgen05,
 // kind::tf32) with a 3xTF32 split for fp32-level accuracy:
 //
-//   A X ~= A_hi X_hi + A_hi X_lo + A_lo X_hi,   v_hi = rn_tf32(v),
-//   v_lo = rn_tf32(v - v_hi).
+//   A X ~= A_hi X_hi + A_hi X_lo + A_lo X_hi,   v_hi = v with the low 13
+//   mantissa bits cleared (exactly representable in tf32), v_lo = v - v_hi.
 //
 // Forward pass  Y = A X   (M = rows of A, K = columns of A, N = s)
 // Transpose     Z = A^T W (M = columns of A, K = rows of A, N = s)
 //
-// The skinny operand is split once per pass, outside the kernel, into
-// [X_hi | X_lo]^T (2S rows, K contiguous): a 32-deep K tile of it is exactly
-// the K-major SW128 B operand, so TMA lands it ready for the tensor core.
-// One CTA per SM, warp-specialised (11 + S/8 warps):
-//   warp 0      A producer: per K tile one raw fp32 A tile (16 KB, K-major
-//               SW128 for the forward pass, row-major for the transpose pass)
-//               into a deep stage ring (the DRAM bytes in flight per SM);
-//   warp 10     panel producer: the split panel tile (2S x 32, 8/16 KB) of
-//               the same K tile into a panel ring, released by the MMA commit;
+// One CTA per SM, warp-specialised (S/16 + 10 warps):
+//   warp 0      TMA producer: per K tile one stage = raw fp32 A tile (16 KB,
+//               K-major SW128 for the forward pass, row-major for the
+//               transpose pass) + the raw fp32 panel rows [32 k][S];
 //   warps 2..9  A splitters: warp w owns TMEM lane quarter w & 3 (= 32 output
 //               rows) and K half (w - 2) / 4; each thread reads its row from
 //               the stage, releases the stage, splits hi/lo and stores both
-//               into a TMEM ring (tcgen05.st);
+//               into a TMEM ring (tcgen05.st); warps 2..5 also drain the
+//               accumulator at the end of every output tile;
+//   warps 10..  panel splitters: raw [32 k][S] -> K-major SW128 [hi; lo] in a
+//               small shared-memory ring (kind::tf32 only accepts K-major
+//               shared-memory operands on sm_100a; measured);
 //   warp 1      MMA issuer (one elected thread), A from TMEM, panel from SMEM:
-//                 D[:, 0:2S]  = A_hi [X_hi | X_lo]      (N = 2S)
-//                 D[:, S:2S] += A_lo X_hi               (N = S)
-//               so D = [A_hi X_hi | A_hi X_lo + A_lo X_hi]; one
-//               tcgen05.commit per K tile releases the panel slot and the
-//               TMEM A slot;
-//   warps 11..  epilogue: drain the double-buffered TMEM accumulator every
-//               KB K tiles into fp32 registers, store (or reduce) the tile.
-// Work is split in contiguous (output tile, K tile) unit ranges over the
-// CTAs; split-K tiles are reduced deterministically (see SplitK).
+//                 D[:, 0:2s]  = A_hi [X_hi | X_lo]      (N = 2s)
+//                 D[:, s:2s] += A_lo X_hi               (N = s)
+//               so D = [A_hi X_hi | A_hi X_lo + A_lo X_hi] and the epilogue
+//               adds the halves; one tcgen05.commit per K tile releases both
+//               the panel slot and the TMEM A slot.
+// The stage ring is released as soon as the splitters hold the data in
+// registers, so nearly all of it is outstanding DRAM traffic (Little's law:
+// the loaded-HBM latency is several microseconds on B200).
+// Work is distributed exactly like the FFMA passes (contiguous unit ranges,
+// flush on tile change, red.global.add when a tile is shared).
 #include <algorithm>
 
 #include "common.cuh"
+#include "pass.cuh"
 
 namespace cnmf {
 namespace {
 
-#ifndef CNMF_X
-#define CNMF_X 0  // probe-only knockouts (tools/tc_variant.sh); 0 in the library
-#endif
 constexpr int BMT = 128;              // output rows per tile (TMEM lanes)
 constexpr int BKT = 32;               // K per stage (one 128B swizzle atom of fp32)
 
@@ -148,33 +146,36 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
-template <int S>
+template <int S, bool TRANS, bool PAIR = false>
 struct TcCfg {
-  static constexpr int ABYTES = BMT * BKT * 4;        // 16 KB raw A tile (one stage)
-  static constexpr int PBYTES = 2 * S * BKT * 4;      // split panel tile [X_hi | X_lo]^T: 8 / 16 KB
-#ifdef CNMF_TC_RINGS  // (ST32, SSP32, AST32) override for probes
-  static constexpr int ST = (S == 32) ? CNMF_TC_ST : 8;
-  static constexpr int SSP = (S == 32) ? CNMF_TC_SSP : 4;
-  static constexpr int AST = (S == 32) ? CNMF_TC_AST : 4;
-#else
-  static constexpr int ST = (S == 32) ? 10 : 8;       // A stage ring (DRAM bytes in flight per SM)
-  static constexpr int SSP = (S == 32) ? 6 : 4;       // split panel ring
-  static constexpr int AST = 4;                       // TMEM ring of split A tiles
-#endif
+  static constexpr int ABYTES = BMT * BKT * 4;        // 16 KB raw A tile
+  static constexpr int BRAW = BKT * S * 4;            // raw fp32 panel tile [32 k][S]: 4 or 8 KB
+  static constexpr int STAGE = ABYTES + BRAW;         // one TMA stage: A tile + its panel tile
+  // split K-major SW128 panel slot: [hi; lo] (2S rows), or for a CTA pair this
+  // CTA's halves of the two MMAs' B operands: [hi or lo (S rows); hi half (S/2 rows)]
+  static constexpr int BSPL = PAIR ? BKT * (S + S / 2) * 4 : BKT * 2 * S * 4;
+  // ring depths: a CTA pair's cross-CTA arrivals add ~1 us of latency to the
+  // panel and TMEM rings, so those are deeper there
+  static constexpr int ST = (S == 32) ? (PAIR ? 9 : 10) : 7;  // stage ring (DRAM bytes in flight per SM)
+  static constexpr int SSP = PAIR ? (S == 32 ? 6 : 4) : 3;    // split panel ring
+  static constexpr int AST = PAIR && S == 32 ? 6 : 4;         // TMEM ring of split A tiles
   static constexpr int MD = SSP > AST ? SSP : AST;    // "MMA of K tile j done" ring (>= SSP, AST)
   static constexpr int KB = 2;                        // K tiles per tensor-core accumulation block
+  static_assert(MD >= SSP && MD >= AST, "one MMA-done ring serves both consumers");
   static constexpr int ACC_COLS = 2 * S;              // per accumulator buffer
   static constexpr int A_COL0 = 2 * ACC_COLS;         // first TMEM column of the A ring
   static constexpr int TMEM_COLS = (A_COL0 + AST * 2 * BKT <= 256) ? 256 : 512;
   static constexpr int NSPLIT = 8;                    // A-splitting warps (2 per TMEM lane quarter)
-  static constexpr int NEPI = 4 * (S / 32);           // epilogue warps (lane quarter x 32-column group)
-  static constexpr int THREADS = 32 * (11 + NEPI);
-  static constexpr size_t SMEM = (size_t)ST * ABYTES + (size_t)SSP * PBYTES + 1024 + 512;
+  static constexpr int NPW = 2;                       // panel-splitting warps
+  static constexpr int PU = S / 32;                   // panel units (32 columns x 16 k) per panel warp
+  static constexpr int NEPI = 4 * (S / 32);            // epilogue warps (lane quarter x 32-column group)
+  static constexpr int THREADS = 32 * (2 + NSPLIT + NPW + NEPI);
+  static constexpr size_t SMEM = (size_t)ST * STAGE + (size_t)SSP * BSPL + 512;
   static_assert(SMEM <= 227 * 1024, "shared memory budget");
   static_assert(A_COL0 + AST * 2 * BKT <= 512, "TMEM budget");
 };
 
-constexpr int kWarpTma = 0, kWarpMma = 1, kWarpSplit0 = 2, kWarpPanel = 10, kWarpEpi0 = 11;
+constexpr int kWarpTma = 0, kWarpMma = 1, kWarpSplit0 = 2, kWarpPanel0 = 10, kWarpEpi0 = 12;
 
 __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
@@ -188,6 +189,51 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint
       : "memory");
 }
 
+__device__ __forceinline__ void tc_mma_ts2(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// commit to the same barrier (shared-memory offset) in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+
+// arrive on the barrier at the same offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+
+// wait with cluster-scope acquire (arrivals come from both CTAs of a pair)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // 32 lanes x 16 consecutive 32-bit columns per warp
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
   asm volatile(
@@ -198,36 +244,44 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
       : "memory");
 }
 
-// Split-K launches reduce shared output tiles deterministically. The CTA
-// holding a tile's first K units (slot 0) reaches that tile at the end of its
-// unit range, every other contributor at the start of its own, so slot 0
-// reduces: contributors store their fp32 partial to their slot of a scratch
-// buffer and raise a per-(tile, slot, warp) flag without waiting; slot 0's
-// epilogue warps wait for the (long raised) flags, add the slots in slot
-// order to their own registers, store the tile and clear the flags. The
-// result does not depend on CTA timing (bit-reproducible range finder).
-struct SplitK {
-  float* part;       // [nblocks][maxsplit][128][S]
-  unsigned* flag;    // [nblocks][maxsplit][NEPI], zero between launches
-  int maxsplit;
-};
-
-// CTA owning unit t of U units spread over G CTAs (CTA b owns [b U / G, (b + 1) U / G))
-__device__ __forceinline__ int64_t item_of(int64_t t, int64_t U, int64_t G) { return ((t + 1) * G - 1) / U; }
-
 // TRANS = false: Y = A X; TRANS = true: Z = A^T W. P = output rows of the
 // pass (m or n); nt = K tiles per output tile.
-template <int S, bool TRANS>
-__global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
+//
+// Rings: stage ring in shared memory (one TMA stage = raw fp32 A tile + the
+// matching raw panel tile), released once the A-splitting warps hold their
+// rows in registers and the panel warp has split the panel tile, so nearly
+// the whole ring is outstanding DRAM traffic; split panel ring (K-major SW128
+// [hi; lo]) released by the MMA commit; TMEM ring of split A tiles (hi and lo,
+// 32 columns each, lane = output row) filled with tcgen05.st and consumed by
+// A-from-TMEM MMAs; double-buffered TMEM accumulators.
+// Split-K launches reduce shared output tiles with red.global.add, so the
+// output must start at zero: every CTA zeroes its slice of rows at start-up
+// and counts itself in `arrived`; an epilogue polls the count before its
+// first reduction (long satisfied by then). The last CTA to finish resets
+// the pair for the next launch that draws this slot.
+struct ZSync {
+  unsigned arrived, finished;
+};
+
+//
+// PAIR: a cluster of two CTAs on one TPC shares every MMA (cta_group::2,
+// M = 256): each CTA splits its own 128 rows of A into its own TMEM and
+// provides half of each B operand ([X_hi | X_lo]: CTA 0 the hi columns, CTA 1
+// the lo columns; X_hi for the correction MMA: one half each), CTA 0 issues
+// the MMAs and commits to both CTAs' barriers. Half the MMA instructions and
+// half the panel splitting per SM.
+template <int S, bool TRANS, bool PAIR>
+__global__ void __launch_bounds__(TcCfg<S, TRANS, PAIR>::THREADS, 1)
     pass_tc(const __grid_constant__ TmaDesc tA, const __grid_constant__ TmaDesc tB, float* __restrict__ out,
-            int64_t P, int nt, int64_t nblocks, int whole, const SplitK sk) {
-  using C = TcCfg<S>;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  unsigned char* sP = smem + C::ST * C::ABYTES;                // [SSP][PBYTES]
-  uint64_t* full = (uint64_t*)(sP + C::SSP * C::PBYTES);       // [ST] A tile landed
-  uint64_t* empty = full + C::ST;                              // [ST] A tile consumed by all splitters
-  uint64_t* pfull = empty + C::ST;                             // [SSP] split panel tile landed
+            int64_t P, int nt, int64_t nblocks, int whole, ZSync* __restrict__ zs) {
+  using C = TcCfg<S, TRANS, PAIR>;
+  constexpr int CW = PAIR ? 2 : 1;          // CTAs per work item
+  constexpr int TILE_ROWS = CW * BMT;       // output rows per work item
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* sP = smem + C::ST * C::STAGE;                 // [SSP][BSPL]
+  uint64_t* full = (uint64_t*)(sP + C::SSP * C::BSPL);         // [ST] stage landed
+  uint64_t* empty = full + C::ST;                              // [ST] stage consumed by all splitters
+  uint64_t* pfull = empty + C::ST;                             // [SSP] split panel ready
   uint64_t* mdone = pfull + C::SSP;                            // [MD] MMAs of K tile j retired
   uint64_t* afull = mdone + C::MD;                             // [AST] split A in TMEM
   uint64_t* tfull = afull + C::AST;                            // [2] accumulator ready
@@ -235,11 +289,12 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t U = nblocks * nt, G = gridDim.x, b = blockIdx.x;
+  const uint32_t rank = PAIR ? (blockIdx.x & 1) : 0;  // cluster dims (2, 1, 1)
+  const int64_t U = nblocks * nt, G = gridDim.x / CW, b = blockIdx.x / CW;
   const int64_t u0 = whole ? (b * nblocks / G) * nt : b * U / G;
   const int64_t u1 = whole ? ((b + 1) * nblocks / G) * nt : (b + 1) * U / G;
   const int64_t ntiles = u1 - u0;
-  if (ntiles <= 0) return;
+  if (!PAIR && ntiles <= 0) return;  // (pairs always have work: grid <= units)
   TC_SPAN(0);
 
   if (threadIdx.x == 0) {
@@ -247,28 +302,48 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
     prefetch_tmap(&tB);
     for (int s = 0; s < C::ST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::NSPLIT);
+      mbar_init(&empty[s], C::NSPLIT + C::NPW);
     }
-    for (int s = 0; s < C::SSP; ++s) mbar_init(&pfull[s], 1);
-    for (int s = 0; s < C::AST; ++s) mbar_init(&afull[s], C::NSPLIT);
+    for (int s = 0; s < C::SSP; ++s) {
+      mbar_init(&pfull[s], CW * C::NPW);
+    }
+    for (int s = 0; s < C::AST; ++s) mbar_init(&afull[s], CW * C::NSPLIT);
     for (int s = 0; s < C::MD; ++s) mbar_init(&mdone[s], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], C::NEPI);
+      mbar_init(&tempty[i], CW * C::NEPI);
     }
     fence_barrier_init();
   }
   if (warp == kWarpMma) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(C::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   // programmatic dependent launch: everything above overlapped the tail of
   // the previous kernel in the stream; its outputs are visible from here on
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (zs != nullptr) {
+    const int64_t z0 = blockIdx.x * P / gridDim.x, z1 = (blockIdx.x + 1) * P / gridDim.x;
+    float4* o4 = reinterpret_cast<float4*>(out + z0 * S);
+    for (int64_t i = threadIdx.x; i < (z1 - z0) * S / 4; i += blockDim.x) o4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();  // both CTAs' barriers initialised before any remote arrival
+  else
+    __syncthreads();
   tc_fence_after();
+  if (zs != nullptr && threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&zs->arrived, 1u);
+  }
   const uint32_t tmem = *tmem_slot;
 
   // Every role walks the same unit sequence u0..u1-1 with incremental
@@ -278,7 +353,7 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
   const int kt0 = (int)(u0 - ob0 * nt);
 
   if (warp == kWarpTma) {
-    // ---------------- A producer ----------------
+    // ---------------- TMA producer ----------------
     if (elect_one()) {
       Ring<C::ST> r;
       int64_t ob = ob0;
@@ -286,13 +361,15 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
       for (int64_t it = 0; it < ntiles; ++it) {
         if (it >= C::ST) mbar_wait(&empty[r.i], r.ph ^ 1);
         TC_TRACE(0);
-        unsigned char* dst = smem + r.i * C::ABYTES;
-        mbar_arrive_expect_tx(&full[r.i], C::ABYTES);
-        const int row0 = (int)(ob * BMT);  // this CTA's 128 output rows
+        unsigned char* dst = smem + r.i * C::STAGE;
+        mbar_arrive_expect_tx(&full[r.i], C::STAGE);
+        const int row0 = (int)(ob * TILE_ROWS + rank * BMT);  // this CTA's 128 output rows
         if (!TRANS)  // A rows [row0, +128), cols [kt*32, +32): K-major SW128
           tma_load_2d(dst, &tA, &full[r.i], kt * BKT, row0);
         else         // A rows [kt*32, +32) (K), cols [row0, +128) (M): row-major
           tma_load_2d(dst, &tA, &full[r.i], row0, kt * BKT);
+        // panel rows [kt*32, +32) (K), all S columns: row-major [32][S]
+        tma_load_2d(dst + C::ABYTES, &tB, &full[r.i], 0, kt * BKT);
         r.next();
         if (++kt == nt) {
           kt = 0;
@@ -300,26 +377,8 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
         }
       }
     }
-  } else if (warp == kWarpPanel) {
-    // ---------------- panel producer: split panel tile [2S][32 k], K-major SW128 ----------------
-    if (elect_one()) {
-      Ring<C::SSP> rp;
-      Ring<C::MD> rd;  // tracks K tile it - SSP (the previous user of slot rp.i)
-      int kt = kt0;
-      for (int64_t it = 0; it < ntiles; ++it) {
-        if (it >= C::SSP) {
-          mbar_wait(&mdone[rd.i], rd.ph);
-          rd.next();
-        }
-        TC_TRACE(7);
-        mbar_arrive_expect_tx(&pfull[rp.i], C::PBYTES);
-        tma_load_2d(sP + rp.i * C::PBYTES, &tB, &pfull[rp.i], kt * BKT, 0);
-        rp.next();
-        if (++kt == nt) kt = 0;
-      }
-    }
   } else if (warp >= kWarpEpi0) {
-    // ---------------- epilogue (one output row x 32 columns per thread) ----------------
+    // ---------------- epilogue (warps 12.., one output row x 32 columns each) ----------------
     // The tensor core accumulates at most KB K tiles into a TMEM buffer; the
     // partial sums then move to fp32 registers (round-to-nearest adds), so
     // the error no longer grows with the tensor-core accumulation chain.
@@ -348,59 +407,35 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[racc.i]);
+        if (lane == 0) {
+          if (PAIR && rank != 0)
+            mbar_arrive_remote(&tempty[racc.i], 0);
+          else
+            mbar_arrive(&tempty[racc.i]);
+        }
         racc.next();
       }
       if (tile_end) {
         const int64_t t0 = ob * nt;  // first unit of this output tile
         const bool owned = (t0 >= u0) && (t0 + nt <= u1);
-        const int64_t row = ob * BMT + row_in_tile;
-        if (owned) {
-          if (row < P) {
-            float* dst = out + row * S + cg;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) *(float4*)(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        const int64_t row = ob * TILE_ROWS + rank * BMT + row_in_tile;
+        if (!owned && zs != nullptr) {  // every CTA's zeroing must have landed
+          if (lane == 0) {
+            unsigned v;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&zs->arrived) : "memory");
+            } while (v < gridDim.x);
           }
-        } else {
-          // shared tile: slot = this CTA's index among the tile's contributors
-          const int64_t first = item_of(t0, U, G), last = item_of(t0 + nt - 1, U, G);
-          const int slot = (int)(b - first), nsplit = (int)(last - first + 1);
-          const int ew = warp - kWarpEpi0;
-          float* base = sk.part + (ob * sk.maxsplit) * (int64_t)(BMT * S) + row_in_tile * S + cg;
-          unsigned* flags = sk.flag + (ob * sk.maxsplit) * C::NEPI + ew;
-          if (slot > 0) {
-            float* mine = base + slot * (int64_t)(BMT * S);
+          __syncwarp();
+        }
+        if (row < P) {
+          float* dst = out + row * S + cg;
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              __stcg((float4*)(mine + j), make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]));
-            __threadfence();
-            __syncwarp();
-            if (lane == 0) atomicExch(flags + slot * C::NEPI, 1u);
-          } else {
-            for (int q2 = 1; q2 < nsplit; ++q2) {
-              if (lane == 0) {
-                unsigned v;
-                do {
-                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + q2 * C::NEPI) : "memory");
-                } while (v == 0u);
-                flags[q2 * C::NEPI] = 0u;  // sole reader: reset for the next launch
-              }
-              __syncwarp();
-              const float* src = base + q2 * (int64_t)(BMT * S);
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                const float4 v = __ldcg((const float4*)(src + j));
-                acc[j] += v.x;
-                acc[j + 1] += v.y;
-                acc[j + 2] += v.z;
-                acc[j + 3] += v.w;
-              }
-            }
-            if (row < P) {
-              float* dst = out + row * S + cg;
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) *(float4*)(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-            }
+          for (int j = 0; j < 32; j += 4) {
+            if (owned)
+              *(float4*)(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            else
+              red_add_v4(dst + j, acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
           }
         }
 #pragma unroll
@@ -411,10 +446,82 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
         ++ob;
       }
     }
+  } else if (warp >= kWarpPanel0) {
+    // ---------------- panel splitters: raw [32 k][S] -> K-major SW128 [hi; lo] ----------------
+    // panel warp p covers units p * PU .. p * PU + PU - 1; unit u = columns
+    // [32 (u >> 1), +32) x k half u & 1
+    const int pw = warp - kWarpPanel0;
+    Ring<C::ST> r;
+    Ring<C::SSP> rp;
+    Ring<C::MD> rd;  // tracks K tile it - SSP (the previous user of slot rp.i)
+    for (int64_t it = 0; it < ntiles; ++it) {
+      mbar_wait(&full[r.i], r.ph);
+      if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(7);
+      const float* raw = (const float*)(smem + r.i * C::STAGE + C::ABYTES);
+      float h[C::PU][16], l[C::PU][16];
+#pragma unroll
+      for (int t = 0; t < C::PU; ++t) {
+        const int u = pw * C::PU + t;
+        const int n = 32 * (u >> 1) + lane;  // lanes read consecutive columns
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float v = raw[(16 * (u & 1) + k) * S + n];
+          h[t][k] = tf32_rn(v);
+          l[t][k] = tf32_rn(v - h[t][k]);
+        }
+      }
+      __syncwarp();
+      if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(10);
+      if (lane == 0) mbar_arrive(&empty[r.i]);
+      if (it >= C::SSP) {
+        mbar_wait(&mdone[rd.i], rd.ph);
+        rd.next();
+      }
+      if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(11);
+      unsigned char* dst = sP + rp.i * C::BSPL;
+#pragma unroll
+      for (int t = 0; t < C::PU; ++t) {
+        const int u = pw * C::PU + t;
+        const int n = 32 * (u >> 1) + lane;  // output column = operand row
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c = 4 * (u & 1) + cc;
+          const uint32_t off = (uint32_t)n * 128 + ((c ^ (n & 7)) << 4);
+          const float4 hv = make_float4(h[t][4 * cc], h[t][4 * cc + 1], h[t][4 * cc + 2], h[t][4 * cc + 3]);
+          const float4 lv = make_float4(l[t][4 * cc], l[t][4 * cc + 1], l[t][4 * cc + 2], l[t][4 * cc + 3]);
+          if constexpr (PAIR) {
+            // B of the [hi | lo] MMA: CTA 0 holds the hi rows, CTA 1 the lo rows;
+            // B of the correction MMA (X_hi): rows [rank S/2, +S/2) of X_hi
+            *(float4*)(dst + off) = rank == 0 ? hv : lv;
+            const int n2 = n - (int)rank * (S / 2);
+            if (n2 >= 0 && n2 < S / 2) {
+              const uint32_t off2 = (uint32_t)n2 * 128 + ((c ^ (n2 & 7)) << 4);
+              *(float4*)(dst + S * 128 + off2) = hv;
+            }
+          } else {
+            *(float4*)(dst + off) = hv;
+            *(float4*)(dst + S * 128 + off) = lv;
+          }
+        }
+      }
+      if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(12);
+      fence_proxy_async();  // generic-proxy stores -> tensor-core (async proxy) reads
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR && rank != 0)
+          mbar_arrive_remote(&pfull[rp.i], 0);
+        else
+          mbar_arrive(&pfull[rp.i]);
+      }
+      if (threadIdx.x == 32 * kWarpPanel0) TC_TRACE(9);
+      r.next();
+      rp.next();
+    }
   } else if (warp == kWarpMma) {
-    // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc_cat = idesc_tf32(2 * S, false, false);
-    constexpr uint32_t idesc_hi = idesc_tf32(S, false, false);
+    // ---------------- MMA issuer (CTA 0 of a pair) ----------------
+    if (PAIR && rank != 0) goto done;
+    constexpr uint32_t idesc_cat = idesc_tf32(2 * S, false, false, CW * BMT);
+    constexpr uint32_t idesc_hi = idesc_tf32(S, false, false, CW * BMT);
     Ring<C::SSP> rp;
     Ring<C::AST> ra;
     Ring<C::MD> rd;
@@ -425,13 +532,19 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
       const bool tile_end = (it == ntiles - 1) || (kt == nt - 1);
       const bool block_end = tile_end || ((kt + 1) % C::KB == 0);
       // reuse of an accumulator buffer waits until the epilogue drained it
-      if (block_start && racc.wrapped) mbar_wait(&tempty[racc.i], racc.ph ^ 1);
-      mbar_wait(&pfull[rp.i], rp.ph);
-      mbar_wait(&afull[ra.i], ra.ph);
+      if constexpr (PAIR) {
+        if (block_start && racc.wrapped) mbar_wait_cluster(&tempty[racc.i], racc.ph ^ 1);
+        mbar_wait_cluster(&pfull[rp.i], rp.ph);
+        mbar_wait_cluster(&afull[ra.i], ra.ph);
+      } else {
+        if (block_start && racc.wrapped) mbar_wait(&tempty[racc.i], racc.ph ^ 1);
+        mbar_wait(&pfull[rp.i], rp.ph);
+        mbar_wait(&afull[ra.i], ra.ph);
+      }
       tc_fence_after();
       if (lane == 0) TC_TRACE(4);
       if (elect_one()) {
-        const uint32_t sb = smem_u32(sP + rp.i * C::PBYTES);     // K-major SW128 [hi; lo]
+        const uint32_t sb = smem_u32(sP + rp.i * C::BSPL);        // K-major SW128 [hi; lo]
         const uint32_t ahi = tmem + C::A_COL0 + ra.i * 2 * BKT;   // split A in TMEM
         const uint32_t alo = ahi + BKT;
         const uint32_t dcat = tmem + racc.i * C::ACC_COLS;
@@ -440,11 +553,22 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
         for (int k = 0; k < BKT / 8; ++k) {
           const uint64_t bcat = smem_desc(sb + 32 * k, 16, 1024);  // 8 tf32 = 32 B per K step
           const uint32_t acc = (block_start && k == 0) ? 0u : 1u;
-          tc_mma_ts(dcat, ahi + 8 * k, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
-          tc_mma_ts(dlo, alo + 8 * k, bcat, idesc_hi, 1u);     //            + A_lo X_hi
+          if constexpr (PAIR) {
+            const uint64_t bhi = smem_desc(sb + S * 128 + 32 * k, 16, 1024);
+            tc_mma_ts2(dcat, ahi + 8 * k, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
+            tc_mma_ts2(dlo, alo + 8 * k, bhi, idesc_hi, 1u);      //            + A_lo X_hi
+          } else {
+            tc_mma_ts(dcat, ahi + 8 * k, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
+            tc_mma_ts(dlo, alo + 8 * k, bcat, idesc_hi, 1u);     //            + A_lo X_hi
+          }
         }
-        tc_commit(&mdone[rd.i]);  // one commit releases the panel slot and the TMEM A slot
-        if (block_end) tc_commit(&tfull[racc.i]);
+        if constexpr (PAIR) {
+          tc_commit_pair(&mdone[rd.i]);  // releases the panel slot and the TMEM A slot in both CTAs
+          if (block_end) tc_commit_pair(&tfull[racc.i]);
+        } else {
+          tc_commit(&mdone[rd.i]);  // one commit releases the split panel and the TMEM A slot
+          if (block_end) tc_commit(&tfull[racc.i]);
+        }
         TC_TRACE(5);
       }
       __syncwarp();
@@ -455,7 +579,7 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
       if (block_end) racc.next();
       if (++kt == nt) kt = 0;
     }
-  } else if (warp < kWarpPanel) {
+  } else {
     // ---------------- A splitters (warps 2..9) ----------------
     // warp w serves TMEM lane quarter w & 3 and K half (w - 2) / 4 of every tile
     const int q = warp & 3;
@@ -468,12 +592,9 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
       mbar_wait(&full[r.i], r.ph);
       if (threadIdx.x == 64) TC_TRACE(1);
       float hi[16], lo[16];
-      if (CNMF_X == 2) {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) hi[k] = (float)(lane + k);
-      } else if (!TRANS) {
+      if (!TRANS) {
         // row r of the K-major SW128 tile: 16 B chunk c at chunk c ^ (r & 7)
-        const unsigned char* rowp = smem + r.i * C::ABYTES + row_in_tile * 128;
+        const unsigned char* rowp = smem + r.i * C::STAGE + row_in_tile * 128;
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
           const int c = 4 * half + cc;
@@ -485,7 +606,7 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
         }
       } else {
         // A column = output row: gather 16 K values from the row-major tile
-        const float* raw = (const float*)(smem + r.i * C::ABYTES) + row_in_tile;
+        const float* raw = (const float*)(smem + r.i * C::STAGE) + row_in_tile;
 #pragma unroll
         for (int k = 0; k < 16; ++k) hi[k] = raw[(16 * half + k) * BMT];
       }
@@ -508,102 +629,78 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&afull[ra.i]);
+      if (lane == 0) {
+        if (PAIR && rank != 0)
+          mbar_arrive_remote(&afull[ra.i], 0);
+        else
+          mbar_arrive(&afull[ra.i]);
+      }
       if (threadIdx.x == 64) TC_TRACE(3);
       r.next();
       ra.next();
     }
   }
+done:
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();  // the peer's TMEM and barriers stay alive until CTA 0's MMAs retired
+  else
+    __syncthreads();
   tc_fence_after();
   TC_SPAN(1);
+  if (zs != nullptr && threadIdx.x == 0 && atomicAdd(&zs->finished, 1u) == gridDim.x - 1) {
+    zs->arrived = 0u;
+    zs->finished = 0u;
+  }
   if (warp == kWarpMma)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
-}
-
-// [X_hi | X_lo]^T of a panel X (rows x S, ld S): out[c][r] = rn_tf32(X[r][c]),
-// out[S + c][r] = rn_tf32(X[r][c] - hi), row pitch ldk (rows rounded to 4).
-// One 32-row x S tile per block through shared memory (coalesced both ways).
-template <int S>
-__global__ void __launch_bounds__(256) split_panel(const float* __restrict__ X, int64_t rows, int64_t ldk,
-                                                   float* __restrict__ out) {
-  __shared__ float t[32][S + 1];
-  const int64_t r0 = (int64_t)blockIdx.x * 32;
-  for (int i = threadIdx.x; i < 32 * S; i += 256) {
-    const int r = i / S, c = i % S;
-    t[r][c] = (r0 + r < rows) ? X[(r0 + r) * S + c] : 0.f;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 32 * S; i += 256) {
-    const int c = i / 32, r = i % 32;
-    if (r0 + r < ldk) {
-      const float v = t[r][c];
-      const float h = tf32_rn(v);
-      out[(int64_t)c * ldk + r0 + r] = h;
-      out[(int64_t)(S + c) * ldk + r0 + r] = tf32_rn(v - h);
-    }
+  {
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
   }
 }
 
-// Library-owned scratch, grown by eager calls (allocation is illegal inside a
-// graph capture); kernels on one stream use it in order.
-struct Scratch {
-  void* p = nullptr;
-  size_t cap = 0;
-};
+// CTA-pair (cta_group::2) kernels are opt-in (CNMF_TC_PAIR=1): correct (same
+// parity tests), but measured slower on B200 -- every cross-CTA arrival with
+// cluster-scope release costs ~1500 cycles on the peer's critical path, and
+// the peer's panel splitting does not shrink -- 400 us vs 170 us for a
+// 20000 x 10000 forward pass (tools/tc_trace.cu with CNMF_TC_TRACE_CTA=1).
+static int g_pair_mode = -1;
 
-static int grow(Scratch& sc, size_t bytes, cudaStream_t st, bool zero) {
-  if (sc.cap >= bytes) return CNMF_OK;
-  cudaStreamCaptureStatus cs;
-  CNMF_CUDA(cudaStreamIsCapturing(st, &cs));
-  if (cs != cudaStreamCaptureStatusNone)
-    return fail(CNMF_ERR_CUDA, "pass scratch must be sized by an eager call before graph capture");
-  CNMF_CUDA(cudaStreamSynchronize(st));
-  if (sc.p) cudaFree(sc.p);
-  sc.p = nullptr;
-  sc.cap = 0;
-  CNMF_CUDA(cudaMalloc(&sc.p, bytes));
-  if (zero) CNMF_CUDA(cudaMemset(sc.p, 0, bytes));
-  sc.cap = bytes;
-  return CNMF_OK;
-}
-
-template <int S, bool TRANS>
-int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bpanel, float* out, cudaStream_t st) {
-  using C = TcCfg<S>;
+template <int S, bool TRANS, bool PAIR>
+int launch_tc_t(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bpanel, float* out, cudaStream_t st) {
+  using C = TcCfg<S, TRANS, PAIR>;
+  constexpr int CW = PAIR ? 2 : 1;
   // skinny operand rows = K extent: n (forward, X) or m (transpose, W)
   const int64_t brows = TRANS ? m : n;
-  const int64_t ldk = (brows + 3) / 4 * 4;
-  static Scratch split_ws, part_ws, flag_ws;
-  CNMF_TRY(grow(split_ws, (size_t)2 * S * ldk * 4, st, false));
-  float* Bs = (float*)split_ws.p;
-  split_panel<S><<<(unsigned)ceil_div(brows, 32), 256, 0, st>>>(Bpanel, brows, ldk, Bs);
-  CNMF_LAUNCH_CHECK();
   TmaDesc tA, tB;
   if (!TRANS)
     CNMF_TRY(make_tma_2d(&tA, A, 4, m, n, lda, BKT, BMT, true));
   else
     CNMF_TRY(make_tma_2d(&tA, A, 4, m, n, lda, BMT, BKT, false));
-  CNMF_TRY(make_tma_2d(&tB, Bs, 4, 2 * S, brows, ldk, BKT, 2 * S, true));
+  CNMF_TRY(make_tma_2d(&tB, Bpanel, 4, brows, S, S, S, BKT, false));
   const int64_t P = TRANS ? n : m;   // output rows
   const int nt = (int)ceil_div(brows, BKT);
-  const int64_t nblocks = ceil_div(P, BMT);
-  const int64_t slots = kNumSMs;
+  const int64_t nblocks = ceil_div(P, CW * BMT);  // work items of CW x 128 output rows
+  const int64_t slots = kNumSMs / CW;             // CTAs (pairs) per wave
   const int whole = nblocks >= 16 * slots;
-  const int64_t grid = std::min<int64_t>(slots, whole ? nblocks : nblocks * nt);
-  SplitK sk{nullptr, nullptr, 0};
+  const int64_t grid = CW * std::min<int64_t>(slots, whole ? nblocks : nblocks * nt);
+  ZSync* zs = nullptr;
   if (!whole) {
-    const int64_t U = nblocks * nt;
-    sk.maxsplit = (int)(ceil_div(nt, U / grid) + 1);
-    CNMF_TRY(grow(part_ws, (size_t)nblocks * sk.maxsplit * BMT * S * 4, st, false));
-    CNMF_TRY(grow(flag_ws, (size_t)nblocks * sk.maxsplit * C::NEPI * 4, st, true));
-    sk.part = (float*)part_ws.p;
-    sk.flag = (unsigned*)flag_ws.p;
+    static ZSync* ring = nullptr;
+    static unsigned next = 0;
+    if (ring == nullptr) {
+      CNMF_CUDA(cudaMalloc(&ring, 64 * sizeof(ZSync)));
+      CNMF_CUDA(cudaMemset(ring, 0, 64 * sizeof(ZSync)));
+    }
+    zs = ring + (next++ % 64);
   }
   static bool attr = false;
   if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(pass_tc<S, TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    CNMF_CUDA(cudaFuncSetAttribute(pass_tc<S, TRANS, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)C::SMEM));
+    if (PAIR) CNMF_CUDA(cudaFuncSetAttribute(pass_tc<S, TRANS, PAIR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
     attr = true;
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -617,18 +714,32 @@ int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bp
   lc.blockDim = dim3(C::THREADS);
   lc.dynamicSmemBytes = C::SMEM;
   lc.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = CW;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
   lc.attrs = at;
-  lc.numAttrs = 1;
-  CNMF_CUDA(cudaLaunchKernelEx(&lc, pass_tc<S, TRANS>, tA, tB, out, P, nt, nblocks, whole, sk));
+  lc.numAttrs = PAIR ? 2 : 1;
+  CNMF_CUDA(cudaLaunchKernelEx(&lc, pass_tc<S, TRANS, PAIR>, tA, tB, out, P, nt, nblocks, whole, zs));
   CNMF_LAUNCH_CHECK();
   if (e0) {
     CNMF_CUDA(cudaEventRecord(e1, st));
     pass_record(e0, e1, 4.0 * ((double)m * n + (double)n * S + (double)m * S));
   }
   return CNMF_OK;
+}
+
+template <int S, bool TRANS>
+int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bpanel, float* out, cudaStream_t st) {
+  if (g_pair_mode < 0) {
+    const char* e = getenv("CNMF_TC_PAIR");
+    g_pair_mode = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (g_pair_mode) return launch_tc_t<S, TRANS, true>(A, m, n, lda, Bpanel, out, st);
+  return launch_tc_t<S, TRANS, false>(A, m, n, lda, Bpanel, out, st);
 }
 
 }  // namespace
