@@ -23,7 +23,21 @@
 namespace cnmf {
 namespace {
 
+#ifndef SWEEP_X
+#define SWEEP_X 0  // probe-only variants (tools/sweep_probe.cu); 0 in the library
+#endif
 constexpr int kSweepThreads = 256;
+#ifdef SWEEP_TRACE
+__device__ unsigned long long g_sw_t[512][12];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SWT(k) do { if (threadIdx.x == 0) g_sw_t[blockIdx.x][k] = gtime(); } while (0)
+#else
+#define SWT(k) do {} while (0)
+#endif
 constexpr int kTR = 64;  // panel rows per tile
 
 constexpr int kGroup = 16;  // blocks per first-level Gram reduction group
@@ -60,6 +74,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(const __grid_co
   const int b = (int)blockIdx.x - (which ? set.p[0].blocks : 0), nb = pp.blocks;
   float* __restrict__ P = pp.P;
   const int64_t rows = pp.rows;
+  SWT(0);
 
   // ---- Gram: thread (grp, bidx) accumulates 4x4 block(s) over row group grp
   const int grp = tid / (GROUPS > 1 ? NBLK : kSweepThreads);
@@ -95,9 +110,10 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(const __grid_co
       *(float4*)(sIn + 4 * i) = v;
     }
     __syncthreads();
+    SWT(8);
 #pragma unroll
     for (int q = 0; q < BPT; ++q) {
-      if (bi[q] < 0) continue;
+      if (bi[q] < 0 || SWEEP_X == 3) continue;
       for (int r = grp; r < nr; r += GROUPS) {
         const float4 x = *(const float4*)(sIn + r * S + 4 * bi[q]);
         const float4 y = *(const float4*)(sIn + r * S + 4 * bj[q]);
@@ -110,18 +126,26 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(const __grid_co
       }
     }
   }
+  SWT(9);
   if (GROUPS > 1) {
     // fold the row groups in shared memory: one partial per block
-    double* red = (double*)(sOut + kTR * S);  // GROUPS x NBLK x 16
+    // entry-major [16][GROUPS][NBLK]: a warp's 32 threads touch consecutive
+    // doubles (a block-major layout put all 32 on one bank: 32-way conflicts)
+    double* red = (double*)(sOut + kTR * S);
     __syncthreads();
     if (bi[0] >= 0)
 #pragma unroll
-      for (int e = 0; e < 16; ++e) red[(grp * NBLK + bidx) * 16 + e] = g[0][e];
+      for (int e = 0; e < 16; ++e) red[(e * GROUPS + grp) * NBLK + bidx] = g[0][e];
     __syncthreads();
     if (grp == 0 && bi[0] >= 0)
       for (int q = 1; q < GROUPS; ++q)
 #pragma unroll
-        for (int e = 0; e < 16; ++e) g[0][e] += red[(q * NBLK + bidx) * 16 + e];
+        for (int e = 0; e < 16; ++e) g[0][e] += red[(e * GROUPS + q) * NBLK + bidx];
+  }
+  SWT(1);
+  if (SWEEP_X == 5) {  // probe: Gram only
+    if (tid == 0 && g[0][0] == 12345.0) pp.G[0] = 1.0;
+    return;
   }
   // ---- deterministic reduction of the block partials (fixed order, no
   // floating-point atomics): groups of kGroup blocks, then the group sums;
@@ -143,14 +167,21 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(const __grid_co
   __shared__ int s_role;  // 0: done, 1: group reducer, 2: group reducer that also factors
   __threadfence();
   __syncthreads();
+  SWT(2);
   const int grp_id = b / kGroup, g0 = grp_id * kGroup, g1 = min(nb, g0 + kGroup);
   if (tid == 0) s_role = atomicAdd(set.gcount + which * 64 + grp_id, 1u) == (unsigned)(g1 - g0) - 1 ? 1 : 0;
   __syncthreads();
   if (s_role) {
     __threadfence();
+    // the group's partials are loaded together (independent L2 reads), then
+    // added in block order: a load-add loop would serialise 16 L2 round trips
     for (int e = tid; e < NE; e += kSweepThreads) {
-      double acc = 0.0;
-      for (int j = g0; j < g1; ++j) acc += __ldcg(set.part + (size_t)(b0 + j) * NE + e);
+      double v[kGroup];
+#pragma unroll
+      for (int j = 0; j < kGroup; ++j) v[j] = (g0 + j < g1) ? __ldcg(set.part + (size_t)(b0 + g0 + j) * NE + e) : 0.0;
+      double acc = v[0];
+#pragma unroll
+      for (int j = 1; j < kGroup; ++j) acc += v[j];
       __stcg(gsum + (size_t)grp_id * NE + e, acc);
     }
     __threadfence();
@@ -161,12 +192,19 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(const __grid_co
     }
     __syncthreads();
   }
+  SWT(3);
   const bool s_last = s_role == 2;
   if (s_last) {
     __threadfence();
     for (int e = tid; e < NE; e += kSweepThreads) {
       double acc = 0.0;
-      for (int j = 0; j < ngroups; ++j) acc += __ldcg(gsum + (size_t)j * NE + e);
+      for (int j0 = 0; j0 < ngroups; j0 += 8) {  // 8 independent loads, then in-order adds
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = (j0 + j < ngroups) ? __ldcg(gsum + (size_t)(j0 + j) * NE + e) : 0.0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc += v[j];
+      }
       int k = e >> 4, i = 0;  // 4x4 block k -> (bi, bj)
       while (k >= NB - i) {
         k -= NB - i;
@@ -177,9 +215,15 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(const __grid_co
     }
     __threadfence();
     __syncthreads();
+    SWT(4);
+#if SWEEP_X == 1  // probe: no factorisation (T = I)
+    for (int i = tid; i < S * S; i += kSweepThreads) pp.T[i] = (i / S == i % S) ? 1.0 : 0.0;
+#else
     chol_small(pp.G, pp.s, S, pp.T, pp.R, pp.info, pp.pass_id, reinterpret_cast<double*>(fsm));
+#endif
     __threadfence();
     __syncthreads();
+    SWT(5);
     if (tid == 0) atomicExch(pp.counter + 1, 1u);  // R^{-1} published
   } else {
     if (tid == 0) {
@@ -191,6 +235,8 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(const __grid_co
     __syncthreads();
   }
 
+  SWT(6);
+  if (SWEEP_X == 2) return;  // probe: no apply (counters left dirty; timing only)
   // ---- P <- P R^{-1}: a block that owned a single tile still holds it in sIn
   for (int i = tid; i < S * S; i += kSweepThreads) sT[i] = (float)__ldcg(pp.T + i);
   const bool kept = !s_last && (int64_t)nb * kTR >= rows;
@@ -206,11 +252,44 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(const __grid_co
       }
     }
     __syncthreads();
-    for (int i = tid; i < kTR * S; i += kSweepThreads) {
-      const int r = i / S, c = i % S;
-      float acc = 0.f;
-      for (int j = 0; j <= c; ++j) acc = fmaf(sIn[r * S + j], sT[j * S + c], acc);
-      sOut[i] = acc;
+    if constexpr (S <= 64) {
+      // thread = one row x CPT consecutive columns: the row in registers, T
+      // rows read as float4 (T is upper triangular, so the j > c terms add
+      // exact zeros: the same sums, in the same order, as a j <= c loop)
+      constexpr int CPT = kTR * S / kSweepThreads, TPR = S / CPT;
+      const int r = tid / TPR, c0 = (tid % TPR) * CPT;
+      float rowv[S], acc[CPT];
+#pragma unroll
+      for (int k = 0; k < S / 4; ++k) {
+        const float4 v = *(const float4*)(sIn + r * S + 4 * k);
+        rowv[4 * k] = v.x;
+        rowv[4 * k + 1] = v.y;
+        rowv[4 * k + 2] = v.z;
+        rowv[4 * k + 3] = v.w;
+      }
+#pragma unroll
+      for (int cc = 0; cc < CPT; ++cc) acc[cc] = 0.f;
+#pragma unroll
+      for (int j = 0; j < S; ++j) {
+#pragma unroll
+        for (int cc = 0; cc < CPT; cc += 4) {
+          const float4 t4 = *(const float4*)(sT + j * S + c0 + cc);
+          acc[cc] = fmaf(rowv[j], t4.x, acc[cc]);
+          acc[cc + 1] = fmaf(rowv[j], t4.y, acc[cc + 1]);
+          acc[cc + 2] = fmaf(rowv[j], t4.z, acc[cc + 2]);
+          acc[cc + 3] = fmaf(rowv[j], t4.w, acc[cc + 3]);
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < CPT; cc += 4)
+        *(float4*)(sOut + r * S + c0 + cc) = make_float4(acc[cc], acc[cc + 1], acc[cc + 2], acc[cc + 3]);
+    } else {
+      for (int i = tid; i < kTR * S; i += kSweepThreads) {
+        const int r = i / S, c = i % S;
+        float acc = 0.f;
+        for (int j = 0; j <= c; ++j) acc = fmaf(sIn[r * S + j], sT[j * S + c], acc);
+        sOut[i] = acc;
+      }
     }
     __syncthreads();
     for (int i = tid; i < kTR * S / 4; i += kSweepThreads) {
@@ -219,6 +298,7 @@ __global__ void __launch_bounds__(kSweepThreads, 2) sweep_kernel(const __grid_co
     }
   }
   __syncthreads();
+  SWT(7);
   if (tid == 0 && atomicAdd(pp.counter + 2, 1u) == (unsigned)nb - 1) {
     pp.counter[0] = 0u;
     pp.counter[1] = 0u;

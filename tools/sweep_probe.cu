@@ -1,65 +1,60 @@
-// Composition of one CholeskyQR sweep on a configs[1]-sized panel:
-// Gram only / Gram + last-block factor / full cooperative sweep (Gram,
-// factor, apply), CUDA-event timed back to back.
-// Build: nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a tools/sweep_probe.cu
-//        paper_1505_04650_b200/csrc/build/{pass,tc_pass,common}.o -o tools/sweep_probe.bin -lcuda
+// Time one dual CholeskyQR sweep (configs[1] panels: 10000 and 5000 rows,
+// s = 30) back to back; build variants with -DSWEEP_X=1 (no factorisation:
+// the last block publishes T = I) to see the factorisation's share.
+// Build: tools/sweep_probe.sh
+#include "../paper_1505_04650_b200/csrc/sweep.cu"
+
 #include <cstdio>
 #include <cstdlib>
-#include <cstdint>
-#include <cuda_runtime.h>
+#include <vector>
 
-namespace cnmf {
-int panel_finalize_chol(float*, int64_t, int, const double*, double*, int, double*, double*, int*, int, unsigned*,
-                        cudaStream_t, int apply_after);
-}
-
-int main(int argc, char** argv) {
-  const int64_t rows = argc > 1 ? atoll(argv[1]) : 10000;
-  const int s = 30, S = 32, reps = 50;
-  float* P;
-  double *G, *T;
-  int* info;
-  unsigned* counter;
-  cudaMalloc(&P, rows * S * 4);
-  cudaMalloc(&G, S * S * 8);
-  cudaMalloc(&T, S * S * 8);
-  cudaMalloc(&info, 64);
-  cudaMalloc(&counter, 64);
-  cudaMemset(G, 0, S * S * 8);
-  cudaMemset(info, 0, 64);
-  cudaMemset(counter, 0, 64);
-  float* h = (float*)malloc(rows * S * 4);
+int main() {
+  const int s = 30, S = 32, reps = 40;
+  const int64_t rows[2] = {10000, 5000};
+  cnmf::SweepPanel p[2];
+  std::vector<float> h(10000 * S);
   srand(3);
-  for (int64_t i = 0; i < rows * S; ++i) h[i] = (i % S) < s ? rand() / (float)RAND_MAX - 0.5f : 0.f;
+  for (size_t i = 0; i < h.size(); ++i) h[i] = (i % S) < (size_t)s ? rand() / (float)RAND_MAX - 0.5f : 0.f;
+  for (int k = 0; k < 2; ++k) {
+    float* P;
+    double *G, *T;
+    int* info;
+    unsigned* counter;
+    cudaMalloc(&P, rows[k] * S * 4);
+    cudaMalloc(&G, S * S * 8);
+    cudaMalloc(&T, S * S * 8);
+    cudaMalloc(&info, 64);
+    cudaMalloc(&counter, 64);
+    cudaMemset(G, 0, S * S * 8);
+    cudaMemset(info, 0, 64);
+    cudaMemset(counter, 0, 64);
+    cudaMemcpy(P, h.data(), rows[k] * S * 4, cudaMemcpyHostToDevice);
+    p[k] = cnmf::SweepPanel{P, rows[k], G, T, nullptr, info, counter, s, 0, 0};
+  }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const char* names[3] = {"gram only", "gram+factor", "gram+factor+apply (coop)"};
-  for (int mode = 0; mode < 3; ++mode) {
-    float tot = 0;
-    for (int r = 0; r < reps; ++r) {
-      cudaMemcpy(P, h, rows * S * 4, cudaMemcpyHostToDevice);
-      cudaMemset(G, 0, S * S * 8);
-      cudaEventRecord(e0);
-      cnmf::panel_finalize_chol(P, rows, S, nullptr, G, s, T, nullptr, info, 0, mode ? counter : nullptr, 0,
-                                mode == 2 ? 1 : 0);
-      cudaEventRecord(e1);
-      cudaEventSynchronize(e1);
-      float ms;
-      cudaEventElapsedTime(&ms, e0, e1);
-      if (r >= 5) tot += ms;
-    }
-    printf("rows %lld %-28s %7.1f us (%s)\n", (long long)rows, names[mode], tot / (reps - 5) * 1e3,
-           cudaGetErrorString(cudaGetLastError()));
+  for (int np = 1; np <= 2; ++np) {
+    for (int r = 0; r < 3; ++r) cnmf::panel_sweep(p, np, S, 0);
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) cnmf::panel_sweep(p, np, S, 0);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("%d panel(s): %.1f us per sweep (%s)\n", np, ms / reps * 1e3, cudaGetErrorString(cudaGetLastError()));
+#ifdef SWEEP_TRACE
+    unsigned long long t[512][12];
+    cudaMemcpyFromSymbol(t, cnmf::g_sw_t, sizeof t);
+    unsigned long long t0 = ~0ull;
+    const int nbk = np == 2 ? 236 : 157;
+    for (int b = 0; b < nbk; ++b) t0 = t[b][0] < t0 ? t[b][0] : t0;
+    auto mx = [&](int k) { unsigned long long m = 0; for (int b = 0; b < nbk; ++b) if (t[b][k] > m && t[b][k] < t0 + 1000000) m = t[b][k]; return (m - t0) * 1e-3; };
+    auto mn = [&](int k) { unsigned long long m = ~0ull; for (int b = 0; b < nbk; ++b) if (t[b][k] >= t0 && t[b][k] < m) m = t[b][k]; return (m - t0) * 1e-3; };
+    printf("  tile loaded max %.2f | gram computed max %.2f\n", mx(8), mx(9));
+    printf("  start spread %.2f | gram done max %.2f | partial stored max %.2f | reducers done max %.2f | final reduce %.2f..%.2f | factor done %.2f | T seen min %.2f max %.2f | apply done max %.2f us\n",
+           mx(0), mx(1), mx(2), mx(3), mn(4), mx(4), mx(5), mn(6), mx(6), mx(7));
+#endif
   }
-  // back-to-back sweeps (what the range finder does between passes)
-  cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r)
-    cnmf::panel_finalize_chol(P, rows, S, nullptr, G, s, T, nullptr, info, 0, counter, 0, 1);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  float ms;
-  cudaEventElapsedTime(&ms, e0, e1);
-  printf("rows %lld back-to-back full sweeps: %7.1f us each\n", (long long)rows, ms / reps * 1e3);
   return 0;
 }
