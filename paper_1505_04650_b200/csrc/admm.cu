@@ -1297,6 +1297,11 @@ size_t admm_workspace(int64_t m, int64_t n, int s, int r) {
   return 256 + 3 * sizeof(Acc) + sizeof(Rep) + 2 * sizeof(Pub) + 256;
 }
 
+int admm_stream_run(const double* core, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
+                    double* du, double* vt, double* dvt, double* xc, double* yc, double pu, double pv, double step,
+                    int max_iter, double tol, double* trace, double* scores, int* iterations, void* ws, int resume,
+                    int step_limit, cudaStream_t st);
+
 int admm_run(const double* core, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
              double* du, double* vt, double* dvt, double* xc, double* yc, double pu, double pv, double step,
              int max_iter, double tol, double* trace, double* scores, int* iterations, void* ws, size_t ws_bytes,
@@ -1349,6 +1354,14 @@ int admm_run(const double* core, const float* L, int64_t m, const float* Rt, int
     p.prof = buf;
     (void)e;
   }
+  // the persistent kernel keeps its s x s / s x r state per CTA in shared
+  // memory; where that cannot fit (s > 32 with r > 32) the three-launch
+  // streaming iteration runs instead (csrc/admm_stream.cu; CNMF_ADMM_STREAM=1
+  // forces it)
+  const char* fe = getenv("CNMF_ADMM_STREAM");
+  if ((fe && fe[0] == '1') || (s > 32 && r > 32))
+    return admm_stream_run(core, L, m, Rt, n, s, r, u, du, vt, dvt, xc, yc, pu, pv, step, max_iter, tol, trace,
+                           scores, iterations, ws, resume, step_limit, st);
   int rc;
   if (s <= 32 && r <= 16)
     rc = dispatch<32, 16>(p, sms, want, m, n, st);

@@ -7,6 +7,8 @@ bases; relative error of the final NMF fit within 1e-3 (relative) of the
 oracle; fp32 pass products within 2e-5 relative Frobenius error of fp64.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -371,6 +373,43 @@ def test_compression_repeatable():
     q1 = C.structured_compress(a, cfg).Q
     q2 = C.structured_compress(a, cfg).Q
     assert O.projector_distance(q1[:, :20], q2[:, :20]) < 1e-6
+
+
+def test_admm_stream_matches_persistent():
+    # the three-launch streaming iteration (csrc/admm_stream.cu, forced with
+    # CNMF_ADMM_STREAM=1) against the persistent kernel on the same
+    # compressed problem: same iterates up to fp64 summation order
+    from paper_1505_04650_b200.nmf import compressed_problem, run_admm
+
+    a = O.dense_lowrank(2000, 1001, 20, 0.01, seed=0).astype(np.float32)
+    A = DeviceMatrix(torch.from_numpy(a).cuda())
+    cfg = C.adjust_config(C.CompressionConfig(r=20, r_ov=10, w=4, seed=5), 2000, 1001)
+    left, right, core = compressed_problem(A, cfg)
+    outs = []
+    for force in ("0", "1"):
+        os.environ["CNMF_ADMM_STREAM"] = force
+        try:
+            u, vt, it, tr = run_admm(core, left.panel, 2000, right.panel, 1001, cfg, 20, max_iter=100, tol=0.0)
+        finally:
+            os.environ.pop("CNMF_ADMM_STREAM", None)
+        torch.cuda.synchronize()
+        outs.append((u.cpu().numpy(), vt.cpu().numpy(), it, np.array(tr)))
+    (u0, v0, i0, t0), (u1, v1, i1, t1) = outs
+    assert i0 == i1 == 100
+    assert np.abs(u0 - u1).max() <= 1e-6 * np.abs(u0).max()
+    assert np.abs(v0 - v1).max() <= 1e-6 * np.abs(v0).max()
+    assert np.allclose(t0, t1, rtol=1e-8)
+
+
+def test_admm_rank_above_32_matches_oracle():
+    # r > 32 with s > 32 (the shape class of configs[4], r = 50) runs on the
+    # streaming iteration; parity with the oracle at a size it finishes fast
+    a = O.dense_lowrank(900, 700, 40, 0.01, seed=4).astype(np.float32)
+    cfg = C.CompressionConfig(r=40, r_ov=10, w=2, seed=3)
+    fp = C.nmf_admm(a, 40, cfg=cfg, max_iter=60, tol=1e-4)
+    ref = O.admm(a, 40, cfg=O.Config(40, 10, 2, 3), max_iter=60, tol=1e-4)
+    assert fp.iterations == ref.iterations
+    assert abs(fp.rel_error - ref.rel_error) <= 1e-3 * ref.rel_error
 
 
 def test_relative_error_matches(golden):
