@@ -56,9 +56,9 @@ __global__ void __launch_bounds__(kT) row_sweep(SSide L, SSide R, int nbl, const
                                                  double* __restrict__ part, const SCtrl* ctrl) {
   if (update && ctrl->done) return;
   extern __shared__ __align__(16) unsigned char sm[];
-  double* Z = (double*)sm;                  // s x (r + 1)
-  double* Xt = Z + SP * (kMaxD + 1);        // kTR x r
-  double* Dt = Xt + kTR * kMaxD;            // kTR x r
+  double* Z = (double*)sm;                  // SP x kMaxD (rows c, cols k; zero padded)
+  double* Xt = Z + SP * kMaxD;              // kTR x kMaxD
+  double* Dt = Xt + kTR * kMaxD;            // kTR x kMaxD
   float* Pt = (float*)(Dt + kTR * kMaxD);   // kTR x SP
   __shared__ double red[4][kT / 32];
   const bool left = (int)blockIdx.x < nbl;
@@ -66,15 +66,22 @@ __global__ void __launch_bounds__(kT) row_sweep(SSide L, SSide R, int nbl, const
   const int b = left ? (int)blockIdx.x : (int)blockIdx.x - nbl;
   const int nb = left ? nbl : (int)gridDim.x - nbl;
   const int64_t r0 = sd.rows * b / nb, r1 = sd.rows * (b + 1) / nb;
-  const int tid = threadIdx.x, rp = r + 1, sr = s * r;
+  const int tid = threadIdx.x, sr = s * r;
   const double* Zs = left ? Zl : Zr;
-  if (update)
-    for (int i = tid; i < s * r; i += kT) Z[(i / r) * rp + i % r] = Zs[i];
-  constexpr int QE = (kMaxD * kMaxD + kT - 1) / kT;  // accumulator entries per thread
-  double au[QE], ad[QE];
+  for (int i = tid; i < SP * kMaxD; i += kT) {
+    const int c = i / kMaxD, k = i % kMaxD;
+    Z[i] = (update && c < s && k < r) ? Zs[c * r + k] : 0.0;
+  }
+  for (int i = tid; i < 2 * kTR * kMaxD; i += kT) Xt[i] = 0.0;  // padding columns stay zero
+  // lane j of a half-warp owns the columns k = j + 16 q (q < 4): consecutive
+  // lanes touch consecutive doubles in Z, Xt, Dt and in x, dx (no bank
+  // conflicts; a 4-consecutive-column split put 4 lanes on each bank)
+  const int j16 = tid & 15, cg = tid >> 4;  // reduction tile: rows 4 cg .. 4 cg + 3 of P^T
+  const bool red_on = 4 * cg < s;
+  double au[16], ad[16];
 #pragma unroll
-  for (int q = 0; q < QE; ++q) au[q] = ad[q] = 0.0;
-  double k0 = 0.0, k1 = 0.0, k2 = 0.0, k3 = 0.0;
+  for (int q = 0; q < 16; ++q) au[q] = ad[q] = 0.0;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   for (int64_t t0 = r0; t0 < r1; t0 += kTR) {
     const int nr = (int)min64(kTR, r1 - t0);
     __syncthreads();
@@ -83,60 +90,81 @@ __global__ void __launch_bounds__(kT) row_sweep(SSide L, SSide R, int nbl, const
       Pt[i] = (row < nr && c < s) ? sd.P[(t0 + row) * sd.ldp + c] : 0.f;
     }
     __syncthreads();
-    for (int i = tid; i < kTR * r; i += kT) {
-      const int row = i / r, k = i % r;
-      double xn = 0.0, dxn = 0.0;
-      if (row < nr) {
-        const int64_t gi = (t0 + row) * r + k;
-        const double xo = sd.x[gi], dxo = sd.dx[gi];
-        if (update) {
-          double lx = 0.0;
-          for (int c = 0; c < s; ++c) lx = fma((double)Pt[row * SP + c], Z[c * rp + k], lx);
-          xn = fmax(lx + dxo / sd.pen, 0.0);
-          dxn = dxo + step * sd.pen * (lx - xn);
-          sd.x[gi] = xn;
-          sd.dx[gi] = dxn;
-          const double dl = lx - xn, dp = dxn * xn, dpos = fmax(dxn, 0.0), xneg = fmax(-xn, 0.0);
-          k0 += dl * dl;
-          k1 += dp * dp;
-          k2 += dpos * dpos;
-          k3 += xneg * xneg;
-        } else {
-          xn = xo;
-          dxn = dxo;
+    // ---- update: thread = (row, lane j), columns j + 16 q ----
+#pragma unroll 1
+    for (int row = tid >> 4; row < kTR; row += kT / 16) {
+      double lx[4] = {0.0, 0.0, 0.0, 0.0};
+      if (update && row < nr) {
+#pragma unroll 4
+        for (int c = 0; c < s; ++c) {
+          const double p = (double)Pt[row * SP + c];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) lx[q] = fma(p, Z[c * kMaxD + j16 + 16 * q], lx[q]);
         }
       }
-      Xt[row * kMaxD + k] = xn;
-      Dt[row * kMaxD + k] = dxn;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = j16 + 16 * q;
+        double xn = 0.0, dxn = 0.0;
+        if (row < nr && k < r) {
+          const int64_t gi = (t0 + row) * r + k;
+          const double xo = sd.x[gi], dxo = sd.dx[gi];
+          if (update) {
+            xn = fmax(lx[q] + dxo / sd.pen, 0.0);
+            dxn = dxo + step * sd.pen * (lx[q] - xn);
+            sd.x[gi] = xn;
+            sd.dx[gi] = dxn;
+            const double dl = lx[q] - xn, dp = dxn * xn, dpos = fmax(dxn, 0.0), xneg = fmax(-xn, 0.0);
+            s0 += dl * dl;
+            s1 += dp * dp;
+            s2 += dpos * dpos;
+            s3 += xneg * xneg;
+          } else {
+            xn = xo;
+            dxn = dxo;
+          }
+        }
+        Xt[row * kMaxD + k] = xn;
+        Dt[row * kMaxD + k] = dxn;
+      }
     }
     __syncthreads();
+    // ---- partials P^T x, P^T dx: 4 rows of P^T x 4 strided columns ----
+    if (red_on) {
+      for (int row = 0; row < nr; ++row) {
+        const float4 p4 = *(const float4*)(Pt + row * SP + 4 * cg);
+        const double pc[4] = {p4.x, p4.y, p4.z, p4.w};
+        double xv[4], dv[4];
 #pragma unroll
-    for (int q = 0; q < QE; ++q) {
-      const int e = tid + q * kT;
-      if (e < sr) {
-        const int c = e / r, k = e % r;
-        double su = au[q], sdv = ad[q];
-        for (int row = 0; row < nr; ++row) {
-          const double pv = (double)Pt[row * SP + c];
-          su = fma(pv, Xt[row * kMaxD + k], su);
-          sdv = fma(pv, Dt[row * kMaxD + k], sdv);
+        for (int q = 0; q < 4; ++q) {
+          xv[q] = Xt[row * kMaxD + j16 + 16 * q];
+          dv[q] = Dt[row * kMaxD + j16 + 16 * q];
         }
-        au[q] = su;
-        ad[q] = sdv;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            au[a * 4 + q] = fma(pc[a], xv[q], au[a * 4 + q]);
+            ad[a * 4 + q] = fma(pc[a], dv[q], ad[a * 4 + q]);
+          }
       }
     }
   }
   double* out = part + (size_t)blockIdx.x * sums_len(s, r);
+  if (red_on) {
 #pragma unroll
-  for (int q = 0; q < QE; ++q) {
-    const int e = tid + q * kT;
-    if (e < sr) {
-      out[e] = au[q];
-      out[sr + e] = ad[q];
-    }
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = 4 * cg + a, k = j16 + 16 * q;
+        if (c < s && k < r) {
+          out[c * r + k] = au[a * 4 + q];
+          out[sr + c * r + k] = ad[a * 4 + q];
+        }
+      }
   }
   // KKT sums: warp shuffles, then the warps in order
-  double v[4] = {k0, k1, k2, k3};
+  double v[4] = {s0, s1, s2, s3};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
 #pragma unroll
@@ -210,18 +238,28 @@ __global__ void __launch_bounds__(kT) core_step(const double* __restrict__ core,
   double* A = (double*)sm;      // 64 x 65 scratch (s x s or s x r)
   double* B = A + kMaxD * LD;   // 64 x 65
   double* M = B + kMaxD * LD;   // r x r
-  double* piv = M + kMaxD * LD;
+  double* piv = M + kMaxD * LD; // 2 x 64
+  // the small operands staged in shared memory (every loop below reads them
+  // many times): core (s x s), xc (s x r), yc (r x s)
+  double* coreS = piv + 2 * kMaxD;
+  double* xcS = coreS + s * s;
+  double* ycS = xcS + s * r;
   __shared__ double red[6][kT / 32];
   __shared__ int s_stop;
   const int tid = threadIdx.x, sr = s * r, len = sums_len(s, r);
   const double* sl = sums;        // left: L^T U | L^T dU | sums
   const double* srt = sums + len; // right: R V^T | R dV^T (as s x r) | sums
   if (tid == 0) s_stop = 0;
+  for (int i = tid; i < s * s; i += kT) coreS[i] = core[i];
+  for (int i = tid; i < s * r; i += kT) xcS[i] = xc[i];
+  for (int i = tid; i < r * s; i += kT) ycS[i] = yc[i];
+  __syncthreads();
   if (first) {
     // yc = V R^T (nmf.py:338): the reduced right sums of the initial state
     for (int i = tid; i < r * s; i += kT) {
       const int a = i / s, c = i % s;
       yc[i] = srt[c * r + a];
+      ycS[i] = srt[c * r + a];
     }
     __syncthreads();
   } else if (k > 0) {
@@ -229,8 +267,9 @@ __global__ void __launch_bounds__(kT) core_step(const double* __restrict__ core,
     // A = E = xc yc - core (s x s)
     for (int i = tid; i < s * s; i += kT) {
       const int a = i / s, c = i % s;
-      double e = -core[i];
-      for (int j = 0; j < r; ++j) e = fma(xc[a * r + j], yc[j * s + c], e);
+      double e = -coreS[i];
+      #pragma unroll 4
+      for (int j = 0; j < r; ++j) e = fma(xcS[a * r + j], ycS[j * s + c], e);
       A[a * LD + c] = e;
     }
     __syncthreads();
@@ -239,13 +278,15 @@ __global__ void __launch_bounds__(kT) core_step(const double* __restrict__ core,
     for (int i = tid; i < s * r; i += kT) {  // (E yc^T + L^T dU)[a][j]
       const int a = i / r, j = i % r;
       double v = sl[sr + a * r + j];
-      for (int c = 0; c < s; ++c) v = fma(A[a * LD + c], yc[j * s + c], v);
+      #pragma unroll 4
+      for (int c = 0; c < s; ++c) v = fma(A[a * LD + c], ycS[j * s + c], v);
       t1 += v * v;
     }
     for (int i = tid; i < r * s; i += kT) {  // (xc^T E + dV R^T)[j][c]
       const int j = i / s, c = i % s;
       double v = srt[sr + c * r + j];
-      for (int a = 0; a < s; ++a) v = fma(xc[a * r + j], A[a * LD + c], v);
+      #pragma unroll 4
+      for (int a = 0; a < s; ++a) v = fma(xcS[a * r + j], A[a * LD + c], v);
       t2 += v * v;
     }
     double vals[3] = {t1, t2, obj};
@@ -289,21 +330,25 @@ __global__ void __launch_bounds__(kT) core_step(const double* __restrict__ core,
   for (int i = tid; i < r * r; i += kT) {
     const int a = i / r, c = i % r;
     double v = (a == c) ? pu : 0.0;
-    for (int j = 0; j < s; ++j) v = fma(yc[a * s + j], yc[c * s + j], v);
+    #pragma unroll 4
+    for (int j = 0; j < s; ++j) v = fma(ycS[a * s + j], ycS[c * s + j], v);
     M[a * LD + c] = v;
   }
   for (int i = tid; i < s * r; i += kT) {  // rhs (s x r) in A
     const int a = i / r, c = i % r;
     double v = pu * sl[a * r + c] - sl[sr + a * r + c];
-    for (int j = 0; j < s; ++j) v = fma(core[a * s + j], yc[c * s + j], v);
+    #pragma unroll 4
+    for (int j = 0; j < s; ++j) v = fma(coreS[a * s + j], ycS[c * s + j], v);
     A[a * LD + c] = v;
   }
   spd_inverse(M, piv, r);
   for (int i = tid; i < s * r; i += kT) {
     const int a = i / r, c = i % r;
     double v = 0.0;
+    #pragma unroll 4
     for (int j = 0; j < r; ++j) v = fma(A[a * LD + j], M[j * LD + c], v);
     xc[i] = v;
+    xcS[i] = v;
     Zl[i] = v;
   }
   __syncthreads();
@@ -311,19 +356,22 @@ __global__ void __launch_bounds__(kT) core_step(const double* __restrict__ core,
   for (int i = tid; i < r * r; i += kT) {
     const int a = i / r, c = i % r;
     double v = (a == c) ? pv : 0.0;
-    for (int j = 0; j < s; ++j) v = fma(xc[j * r + a], xc[j * r + c], v);
+    #pragma unroll 4
+    for (int j = 0; j < s; ++j) v = fma(xcS[j * r + a], xcS[j * r + c], v);
     M[a * LD + c] = v;
   }
   for (int i = tid; i < r * s; i += kT) {  // rhs2 (r x s) in B
     const int a = i / s, c = i % s;
     double v = pv * srt[c * r + a] - srt[sr + c * r + a];
-    for (int j = 0; j < s; ++j) v = fma(xc[j * r + a], core[j * s + c], v);
+    #pragma unroll 4
+    for (int j = 0; j < s; ++j) v = fma(xcS[j * r + a], coreS[j * s + c], v);
     B[a * LD + c] = v;
   }
   spd_inverse(M, piv, r);
   for (int i = tid; i < r * s; i += kT) {
     const int a = i / s, c = i % s;
     double v = 0.0;
+    #pragma unroll 4
     for (int j = 0; j < r; ++j) v = fma(M[a * LD + j], B[j * LD + c], v);
     yc[i] = v;
     Zr[c * r + a] = v;  // Z for the right rows: yc^T (s x r)
@@ -369,14 +417,15 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   double* sums = part + (size_t)total * len;
   double* Zl = sums + 2 * len;
   double* Zr = Zl + kMaxD * kMaxD;
-  const size_t sweep_smem = ((size_t)S * (kMaxD + 1) + 2 * kTR * kMaxD) * 8 + (size_t)kTR * S * 4;
-  const size_t core_smem = (3 * (size_t)kMaxD * (kMaxD + 1) + 2 * kMaxD) * 8;
+  const size_t sweep_smem = ((size_t)S * kMaxD + 2 * kTR * kMaxD) * 8 + (size_t)kTR * S * 4;
+  const size_t core_smem = (3 * (size_t)kMaxD * (kMaxD + 1) + 2 * kMaxD + (size_t)s * s + 2 * (size_t)s * r) * 8;
   static bool attr = false;
   if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(row_sweep<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem));
+    CNMF_CUDA(cudaFuncSetAttribute(row_sweep<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(((size_t)32 * kMaxD + 2 * kTR * kMaxD) * 8 + (size_t)kTR * 32 * 4)));
     CNMF_CUDA(cudaFuncSetAttribute(row_sweep<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(((size_t)64 * (kMaxD + 1) + 2 * kTR * kMaxD) * 8 + (size_t)kTR * 64 * 4)));
-    CNMF_CUDA(cudaFuncSetAttribute(core_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)core_smem));
+                                   (int)(((size_t)64 * kMaxD + 2 * kTR * kMaxD) * 8 + (size_t)kTR * 64 * 4)));
+    CNMF_CUDA(cudaFuncSetAttribute(core_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)((3 * kMaxD * (kMaxD + 1) + 2 * kMaxD + 3 * kMaxD * kMaxD) * 8)));
     attr = true;
   }
   const SSide sl{L, m, S, u, du, pu}, sr{Rt, n, S, vt, dvt, pv};
