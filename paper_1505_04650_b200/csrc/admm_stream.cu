@@ -198,6 +198,21 @@ __global__ void __launch_bounds__(kT) reduce_parts(const double* __restrict__ pa
   sums[side * len + e] = acc;
 }
 
+// sum_j a[j * sa] * b[j * sb] with four interleaved partial sums (the
+// single-block core step is bound by the fp64 FMA latency of one long chain)
+__device__ __forceinline__ double dot4(const double* a, int sa, const double* b, int sb, int len) {
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+  int j = 0;
+  for (; j + 4 <= len; j += 4) {
+    v0 = fma(a[j * sa], b[j * sb], v0);
+    v1 = fma(a[(j + 1) * sa], b[(j + 1) * sb], v1);
+    v2 = fma(a[(j + 2) * sa], b[(j + 2) * sb], v2);
+    v3 = fma(a[(j + 3) * sa], b[(j + 3) * sb], v3);
+  }
+  for (; j < len; ++j) v0 = fma(a[j * sa], b[j * sb], v0);
+  return (v0 + v1) + (v2 + v3);
+}
+
 // In-place inverse of an SPD r x r matrix (ld kMaxD + 1) by Gauss-Jordan
 // without pivoting (the ridge term keeps the pivots >= the penalty).
 __device__ void spd_inverse(double* M, double* piv, int r) {
@@ -268,8 +283,7 @@ __global__ void __launch_bounds__(kT) core_step(const double* __restrict__ core,
     for (int i = tid; i < s * s; i += kT) {
       const int a = i / s, c = i % s;
       double e = -coreS[i];
-      #pragma unroll 4
-      for (int j = 0; j < r; ++j) e = fma(xcS[a * r + j], ycS[j * s + c], e);
+      e += dot4(xcS + a * r, 1, ycS + c, s, r);
       A[a * LD + c] = e;
     }
     __syncthreads();
@@ -278,15 +292,13 @@ __global__ void __launch_bounds__(kT) core_step(const double* __restrict__ core,
     for (int i = tid; i < s * r; i += kT) {  // (E yc^T + L^T dU)[a][j]
       const int a = i / r, j = i % r;
       double v = sl[sr + a * r + j];
-      #pragma unroll 4
-      for (int c = 0; c < s; ++c) v = fma(A[a * LD + c], ycS[j * s + c], v);
+      v += dot4(A + a * LD, 1, ycS + j * s, 1, s);
       t1 += v * v;
     }
     for (int i = tid; i < r * s; i += kT) {  // (xc^T E + dV R^T)[j][c]
       const int j = i / s, c = i % s;
       double v = srt[sr + c * r + j];
-      #pragma unroll 4
-      for (int a = 0; a < s; ++a) v = fma(xcS[a * r + j], A[a * LD + c], v);
+      v += dot4(xcS + j, r, A + c, LD, s);
       t2 += v * v;
     }
     double vals[3] = {t1, t2, obj};
@@ -330,23 +342,20 @@ __global__ void __launch_bounds__(kT) core_step(const double* __restrict__ core,
   for (int i = tid; i < r * r; i += kT) {
     const int a = i / r, c = i % r;
     double v = (a == c) ? pu : 0.0;
-    #pragma unroll 4
-    for (int j = 0; j < s; ++j) v = fma(ycS[a * s + j], ycS[c * s + j], v);
+    v += dot4(ycS + a * s, 1, ycS + c * s, 1, s);
     M[a * LD + c] = v;
   }
   for (int i = tid; i < s * r; i += kT) {  // rhs (s x r) in A
     const int a = i / r, c = i % r;
     double v = pu * sl[a * r + c] - sl[sr + a * r + c];
-    #pragma unroll 4
-    for (int j = 0; j < s; ++j) v = fma(coreS[a * s + j], ycS[c * s + j], v);
+    v += dot4(coreS + a * s, 1, ycS + c * s, 1, s);
     A[a * LD + c] = v;
   }
   spd_inverse(M, piv, r);
   for (int i = tid; i < s * r; i += kT) {
     const int a = i / r, c = i % r;
     double v = 0.0;
-    #pragma unroll 4
-    for (int j = 0; j < r; ++j) v = fma(A[a * LD + j], M[j * LD + c], v);
+    v += dot4(A + a * LD, 1, M + c, LD, r);
     xc[i] = v;
     xcS[i] = v;
     Zl[i] = v;
@@ -356,23 +365,20 @@ __global__ void __launch_bounds__(kT) core_step(const double* __restrict__ core,
   for (int i = tid; i < r * r; i += kT) {
     const int a = i / r, c = i % r;
     double v = (a == c) ? pv : 0.0;
-    #pragma unroll 4
-    for (int j = 0; j < s; ++j) v = fma(xcS[j * r + a], xcS[j * r + c], v);
+    v += dot4(xcS + a, r, xcS + c, r, s);
     M[a * LD + c] = v;
   }
   for (int i = tid; i < r * s; i += kT) {  // rhs2 (r x s) in B
     const int a = i / s, c = i % s;
     double v = pv * srt[c * r + a] - srt[sr + c * r + a];
-    #pragma unroll 4
-    for (int j = 0; j < s; ++j) v = fma(xcS[j * r + a], coreS[j * s + c], v);
+    v += dot4(xcS + a, r, coreS + c, s, s);
     B[a * LD + c] = v;
   }
   spd_inverse(M, piv, r);
   for (int i = tid; i < r * s; i += kT) {
     const int a = i / s, c = i % s;
     double v = 0.0;
-    #pragma unroll 4
-    for (int j = 0; j < r; ++j) v = fma(M[a * LD + j], B[j * LD + c], v);
+    v += dot4(M + a * LD, 1, B + c, LD, r);
     yc[i] = v;
     Zr[c * r + a] = v;  // Z for the right rows: yc^T (s x r)
   }
