@@ -3,16 +3,16 @@
 // Reference: compress.py:156-199 structured_compress, compress.py:202-227
 // structured_compress_rows, compress.py:136-145 canonical_qr, tsqr.py:65-135.
 //
-// Every pass output is re-orthonormalised on the device by CholeskyQR: the
-// finalize kernel computes the fp64 Gram matrix of the skinny panel while it
-// streams it, one CTA factors G = R^T R (with a shift when G is numerically
-// singular) and inverts R, and the next finalize applies R^{-1} in place. The
-// first sweep runs explicitly (its R^{-1} carries cond(P) ~ sigma_1/sigma_s);
-// the second sweep's near-identity R^{-1} is deferred into the next pass's
-// finalize, because A (P T) = (A P) T. All transforms are upper triangular, so
-// the leading column spans — and therefore the sign-canonical Q of the
-// reference — are those of the reference (its reorthogonalize flag changes
-// nothing in exact arithmetic); numerically this is the stable variant.
+// Every pass output is re-orthonormalised on the device by one CholeskyQR
+// sweep (csrc/sweep.cu: fp64 Gram matrix, fixed-order reduction, one block
+// factors G = R^T R -- with a shift when G is numerically singular -- into
+// R^{-1}, and the grid applies it in place); the final basis gets a second,
+// polishing sweep. The two range finders of the compressed NMF are
+// interleaved so that one sweep launch serves both. All transforms are upper
+// triangular, so the leading column spans -- and therefore the
+// sign-canonical Q of the reference -- are those of the reference (its
+// reorthogonalize flag changes nothing in exact arithmetic); numerically this
+// is the stable variant.
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -27,8 +27,6 @@ namespace cnmf {
 int panel_ld(int s);
 
 int panel_finalize(float*, int64_t, int, const double*, double*, cudaStream_t);
-int panel_finalize_chol(float*, int64_t, int, const double*, double*, int, double*, double*, int*, int, unsigned*,
-                        cudaStream_t, int apply_after = 0);
 int gaussian_fill_ws(uint64_t, int64_t, int64_t, int64_t, int, void*, int64_t, void*, size_t, cudaStream_t);
 size_t gaussian_workspace(int64_t, int64_t, int64_t);
 

@@ -17,7 +17,6 @@
 #include <cstdlib>
 #include <string>
 
-#include "chol.cuh"
 #include "common.cuh"
 #include "pass.cuh"
 
@@ -289,55 +288,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// P <- P T (T upper-triangular S x S, fp64 given, applied in fp32) and
-// G += P^T P in fp64 (upper triangle, atomics). Grid-strided over 64-row
-// tiles; the Gram products are spread over 4x4 register blocks x row groups
-// so that every thread of the block accumulates. Either step can be disabled.
-// With `counter` set, the last block to finish factors the completed Gram
-// matrix (chol_block: Tout = R^{-1}, G handed back zeroed), which saves a
-// launch and a dependent gap per CholeskyQR sweep.
+// P <- P T (T upper-triangular S x S, fp64 given, applied in fp32), grid-
+// strided over 64-row tiles (cnmf_panel_apply; the CholeskyQR sweeps of the
+// range finders apply their transform inside csrc/sweep.cu).
 template <int S>
-__global__ void __launch_bounds__(kThreads, 2)
-    finalize_panel(float* __restrict__ P, int64_t rows, const double* T, double* __restrict__ G, int s,
-                   double* Tout, double* __restrict__ Rout, int* __restrict__ info, int pass_id,
-                   unsigned* __restrict__ counter, int apply_after) {
+__global__ void __launch_bounds__(kThreads) apply_panel(float* __restrict__ P, int64_t rows, const double* T) {
   constexpr int TR = 64;
-  constexpr int NB = S / 4;                  // 4-wide blocks per side
-  constexpr int NBLK = NB * (NB + 1) / 2;    // upper-triangular 4x4 blocks
-  constexpr int BPT = (NBLK + kThreads - 1) / kThreads;
-  constexpr int GROUPS = (NBLK >= kThreads) ? 1 : kThreads / NBLK;  // row groups
   extern __shared__ float fsm[];
   float* sT = fsm;              // S x S
   float* sIn = sT + S * S;      // TR x S
   float* sOut = sIn + TR * S;   // TR x S
   const int tid = threadIdx.x;
-  if (T != nullptr)
-    for (int i = tid; i < S * S; i += kThreads) sT[i] = (float)T[i];
-
-  const int grp = tid / (GROUPS > 1 ? NBLK : kThreads);
-  const int bidx = tid - grp * (GROUPS > 1 ? NBLK : kThreads);
-  int bi[BPT], bj[BPT];
-#pragma unroll
-  for (int q = 0; q < BPT; ++q) {
-    int b = bidx + q * kThreads;
-    bi[q] = -1;
-    bj[q] = -1;
-    if (b < NBLK && grp < GROUPS) {
-      int i = 0;
-      while (b >= NB - i) {
-        b -= NB - i;
-        ++i;
-      }
-      bi[q] = i;
-      bj[q] = i + b;
-    }
-  }
-  double g[BPT][16];
-#pragma unroll
-  for (int q = 0; q < BPT; ++q)
-#pragma unroll
-    for (int e = 0; e < 16; ++e) g[q][e] = 0.0;
-
+  for (int i = tid; i < S * S; i += kThreads) sT[i] = (float)T[i];
   for (int64_t t0 = (int64_t)blockIdx.x * TR; t0 < rows; t0 += (int64_t)gridDim.x * TR) {
     __syncthreads();
     const int nr = (int)min64(TR, rows - t0);
@@ -346,109 +308,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (r < nr) v = *(const float4*)(P + t0 * S + 4 * (int64_t)i);
       *(float4*)(sIn + 4 * i) = v;
-    }
-    __syncthreads();
-    if (T != nullptr) {
-      for (int i = tid; i < TR * S; i += kThreads) {
-        const int r = i / S, c = i % S;
-        float acc = 0.f;
-        for (int j = 0; j <= c; ++j) acc = fmaf(sIn[r * S + j], sT[j * S + c], acc);
-        sOut[i] = acc;
-      }
-      __syncthreads();
-      for (int i = tid; i < TR * S / 4; i += kThreads) {
-        const int r = (i * 4) / S;
-        if (r < nr) *(float4*)(P + t0 * S + 4 * (int64_t)i) = *(const float4*)(sOut + 4 * i);
-      }
-    }
-    if (G != nullptr) {
-      const float* src = (T != nullptr) ? sOut : sIn;
-#pragma unroll
-      for (int q = 0; q < BPT; ++q) {
-        if (bi[q] < 0) continue;
-        for (int r = grp; r < nr; r += GROUPS) {
-          const float4 x = *(const float4*)(src + r * S + 4 * bi[q]);
-          const float4 y = *(const float4*)(src + r * S + 4 * bj[q]);
-          const double xs[4] = {x.x, x.y, x.z, x.w};
-          const double ys[4] = {y.x, y.y, y.z, y.w};
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) g[q][a * 4 + b] = fma(xs[a], ys[b], g[q][a * 4 + b]);
-        }
-      }
-    }
-  }
-  if (G != nullptr) {
-    if (GROUPS > 1) {
-      // fold the row groups in shared memory: one atomic per entry per block
-      double* red = (double*)(sOut + TR * S);  // GROUPS x NBLK x 16
-      __syncthreads();
-      if (bi[0] >= 0)
-#pragma unroll
-        for (int e = 0; e < 16; ++e) red[(grp * NBLK + bidx) * 16 + e] = g[0][e];
-      __syncthreads();
-      if (grp == 0 && bi[0] >= 0)
-        for (int q = 1; q < GROUPS; ++q)
-#pragma unroll
-          for (int e = 0; e < 16; ++e) g[0][e] += red[(q * NBLK + bidx) * 16 + e];
-    }
-    if (grp == 0) {
-#pragma unroll
-      for (int q = 0; q < BPT; ++q) {
-        if (bi[q] < 0) continue;
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int ia = 4 * bi[q] + a, jb = 4 * bj[q] + b;
-            if (ia <= jb) atomicAdd(G + ia * S + jb, g[q][a * 4 + b]);
-          }
-      }
-    }
-  }
-  if (counter == nullptr) return;
-  // last block: factor the finished Gram matrix
-  __shared__ bool s_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    chol_small(G, s, S, Tout, Rout, info, pass_id, reinterpret_cast<double*>(fsm));
-    if (!apply_after) {
-      if (threadIdx.x == 0) *counter = 0u;
-      return;
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) atomicExch(counter + 1, 1u);  // R^{-1} published
-  } else {
-    if (!apply_after) return;
-    // cooperative launch: every block is resident, so waiting here is safe
-    if (threadIdx.x == 0) {
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter + 1) : "memory");
-      } while (v == 0u);
-    }
-    __syncthreads();
-  }
-  // P <- P R^{-1}: a block that owns a single tile still has it in sIn
-  // (unless it ran the factorisation, which used the shared memory)
-  for (int i = tid; i < S * S; i += kThreads) sT[i] = (float)__ldcg(Tout + i);
-  const bool kept = !s_last && (int64_t)gridDim.x * TR >= rows;
-  for (int64_t t0 = (int64_t)blockIdx.x * TR; t0 < rows; t0 += (int64_t)gridDim.x * TR) {
-    const int nr = (int)min64(TR, rows - t0);
-    if (!kept) {
-      __syncthreads();
-      for (int i = tid; i < TR * S / 4; i += kThreads) {
-        const int r = (i * 4) / S;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r < nr) v = *(const float4*)(P + t0 * S + 4 * (int64_t)i);
-        *(float4*)(sIn + 4 * i) = v;
-      }
     }
     __syncthreads();
     for (int i = tid; i < TR * S; i += kThreads) {
@@ -462,12 +321,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int r = (i * 4) / S;
       if (r < nr) *(float4*)(P + t0 * S + 4 * (int64_t)i) = *(const float4*)(sOut + 4 * i);
     }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && atomicAdd(counter + 2, 1u) == gridDim.x - 1) {
-    counter[0] = 0u;
-    counter[1] = 0u;
-    counter[2] = 0u;
   }
 }
 
@@ -537,43 +390,15 @@ int launch_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const fl
 }
 
 template <int S>
-int launch_finalize(float* P, int64_t rows, const double* T, double* G, int s, double* Tout, double* Rout, int* info,
-                    int pass_id, unsigned* counter, cudaStream_t st, int apply_after = 0) {
-  constexpr int NB = S / 4, NBLK = NB * (NB + 1) / 2;
-  constexpr int GROUPS = (NBLK >= kThreads) ? 1 : kThreads / NBLK;
-  constexpr size_t fin = (size_t)(S * S + 2 * 64 * S) * 4 + (GROUPS > 1 ? (size_t)GROUPS * NBLK * 16 * 8 : 0);
-  constexpr size_t chol = ((size_t)S * S + 2 * (size_t)S + 32 * 33 + 128) * 8;
-  constexpr size_t smem = fin > chol ? fin : chol;
+int launch_apply(float* P, int64_t rows, const double* T, cudaStream_t st) {
+  constexpr size_t smem = (size_t)(S * S + 2 * 64 * S) * 4;
   static bool attr = false;
   if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(finalize_panel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CNMF_CUDA(cudaFuncSetAttribute(apply_panel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  // G must be zero on entry (the Cholesky step re-zeroes it after use).
-  // One wave: a second partial wave would double the (latency-bound) time.
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, finalize_panel<S>, kThreads, smem));
-    per_sm = std::max(per_sm, 1);
-  }
-  const int64_t tiles = ceil_div(rows, 64);
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)per_sm * kNumSMs));
-  if (apply_after) {
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(kThreads);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    CNMF_CUDA(cudaLaunchKernelEx(&lc, finalize_panel<S>, P, rows, T, G, s, Tout, Rout, info, pass_id, counter,
-                                 apply_after));
-  } else {
-    finalize_panel<S><<<grid, kThreads, smem, st>>>(P, rows, T, G, s, Tout, Rout, info, pass_id, counter, 0);
-  }
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 64), 2 * kNumSMs));
+  apply_panel<S><<<grid, kThreads, smem, st>>>(P, rows, T);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }
@@ -624,24 +449,11 @@ int pass_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const floa
 }
 
 int panel_finalize(float* P, int64_t rows, int S, const double* T, double* G, cudaStream_t st) {
+  if (G != nullptr) return fail(CNMF_ERR_ARGUMENT, "panel_finalize: Gram accumulation moved to panel_sweep");
   switch (S) {
-    case 32: return launch_finalize<32>(P, rows, T, G, 0, nullptr, nullptr, nullptr, 0, nullptr, st);
-    case 64: return launch_finalize<64>(P, rows, T, G, 0, nullptr, nullptr, nullptr, 0, nullptr, st);
-    case 128: return launch_finalize<128>(P, rows, T, G, 0, nullptr, nullptr, nullptr, 0, nullptr, st);
-  }
-  return fail(CNMF_ERR_ARGUMENT, "panel width must be 32, 64 or 128");
-}
-
-// P <- P Tin (optional), G = P^T P, then Tout = R^{-1} of G = R^T R in the
-// same launch (last-block Cholesky); with `apply_after` the blocks then wait
-// for Tout (cooperative launch) and apply it: one full CholeskyQR sweep per
-// launch. counter[0..2] must be zero on entry and are left zero.
-int panel_finalize_chol(float* P, int64_t rows, int S, const double* Tin, double* G, int s, double* Tout,
-                        double* Rout, int* info, int pass_id, unsigned* counter, cudaStream_t st, int apply_after) {
-  switch (S) {
-    case 32: return launch_finalize<32>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st, apply_after);
-    case 64: return launch_finalize<64>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st, apply_after);
-    case 128: return launch_finalize<128>(P, rows, Tin, G, s, Tout, Rout, info, pass_id, counter, st, apply_after);
+    case 32: return launch_apply<32>(P, rows, T, st);
+    case 64: return launch_apply<64>(P, rows, T, st);
+    case 128: return launch_apply<128>(P, rows, T, st);
   }
   return fail(CNMF_ERR_ARGUMENT, "panel width must be 32, 64 or 128");
 }
