@@ -86,6 +86,10 @@ int cnmf_pass_forward(const float* A, int64_t m, int64_t n, int64_t lda, const f
                       void* stream);
 int cnmf_pass_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const float* W, int s, float* Z,
                         void* stream);
+/* Both at once: Y = A X and Z = A^T W in one launch (the two range finders'
+ * passes of a power step; one pipeline ramp-up and tail instead of two). */
+int cnmf_pass_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W,
+                   float* Z, int s, void* stream);
 
 /* ---- structured compression (compress.py:156 structured_compress,
  *      compress.py:202 structured_compress_rows, nmf.py:120 _compression_pair)

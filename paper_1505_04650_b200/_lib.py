@@ -36,6 +36,7 @@ SIGNATURES = {
     "cnmf_uniform_fill": (c_int, [c_u64, c_i64, c_i64, c_dbl, c_dbl, c_int, c_int, vp, vp]),
     "cnmf_pass_forward": (c_int, [vp, c_i64, c_i64, c_i64, vp, c_int, vp, vp]),
     "cnmf_pass_transpose": (c_int, [vp, c_i64, c_i64, c_i64, vp, c_int, vp, vp]),
+    "cnmf_pass_pair": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, vp, vp, c_int, vp]),
     "cnmf_compress_workspace": (c_size, [c_i64, c_i64, c_int]),
     "cnmf_structured_compress": (c_int, [vp, c_i64, c_i64, c_i64, c_int, c_int, c_u64, c_int, vp, vp, c_size, vp]),
     "cnmf_structured_compress_async": (c_int, [vp, c_i64, c_i64, c_i64, c_int, c_int, c_u64, c_int, vp, vp, c_size,

@@ -114,6 +114,13 @@ int cnmf_structured_compress_async(const float* A, int64_t m, int64_t n, int64_t
   return structured_compress(A, m, n, lda, s, w, seed, side, Q, ws, ws_bytes, STREAM(stream), false);
 }
 
+int cnmf_pass_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W,
+                   float* Z, int s, void* stream) {
+  const int S = panel_ld(s);
+  if (S < 0) return fail(CNMF_ERR_ARGUMENT, "panel width must be <= 128");
+  return pass_pair(A, m, n, lda, X, Y, W, Z, S, STREAM(stream));
+}
+
 int cnmf_compress_pair_async(const float* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed_left,
                              uint64_t seed_right, float* QL, float* QR, void* ws_left, void* ws_right,
                              size_t ws_bytes, void* stream) {

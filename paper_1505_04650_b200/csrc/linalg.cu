@@ -166,26 +166,41 @@ static int chain_begin(Chain& c, const float* A, int64_t m, int64_t n, int64_t l
 
 // The next of the 2w+1 passes over A: the first streams the test matrix, the
 // others alternate transpose / forward (power iteration on A A^T or A^T A).
-static int chain_pass(Chain& c, cudaStream_t st) {
-  if (c.cur == nullptr) {
-    if (c.side == 0) {
-      CNMF_TRY(pass_forward(c.A, c.m, c.n, c.lda, c.Pn, c.S, c.Pm, st));
-      c.cur = c.Pm;
-    } else {
-      CNMF_TRY(pass_transpose(c.A, c.m, c.n, c.lda, c.Pm, c.S, c.Pn, st));
-      c.cur = c.Pn;
-    }
-  } else {
-    ++c.pass_id;
-    const bool to_n = (c.cur == c.Pm);  // next output has n rows: transpose pass
-    float* nxt = to_n ? c.Pn : c.Pm;
-    if (to_n)
-      CNMF_TRY(pass_transpose(c.A, c.m, c.n, c.lda, c.cur, c.S, nxt, st));
-    else
-      CNMF_TRY(pass_forward(c.A, c.m, c.n, c.lda, c.cur, c.S, nxt, st));
-    c.cur = nxt;
-  }
+struct PassPlan {
+  bool trans;
+  const float* in;
+  float* out;
+};
+
+static PassPlan chain_plan(const Chain& c) {
+  if (c.cur == nullptr) return c.side == 0 ? PassPlan{false, c.Pn, c.Pm} : PassPlan{true, c.Pm, c.Pn};
+  const bool to_n = (c.cur == c.Pm);  // next output has n rows: transpose pass
+  return to_n ? PassPlan{true, c.cur, c.Pn} : PassPlan{false, c.cur, c.Pm};
+}
+
+static void chain_advance(Chain& c, const PassPlan& p) {
+  if (c.cur != nullptr) ++c.pass_id;
+  c.cur = p.out;
   c.cur_rows = (c.cur == c.Pm) ? c.m : c.n;
+}
+
+static int run_plan(const Chain& c, const PassPlan& p, cudaStream_t st) {
+  return p.trans ? pass_transpose(c.A, c.m, c.n, c.lda, p.in, c.S, p.out, st)
+                 : pass_forward(c.A, c.m, c.n, c.lda, p.in, c.S, p.out, st);
+}
+
+// the passes of one power step: with both range finders there is always one
+// forward and one transpose pass, run as ONE paired launch
+static int chains_pass(Chain* c, int nc, cudaStream_t st) {
+  PassPlan p[2];
+  for (int i = 0; i < nc; ++i) p[i] = chain_plan(c[i]);
+  if (nc == 2 && p[0].trans != p[1].trans) {
+    const int f = p[0].trans ? 1 : 0, t = 1 - f;
+    CNMF_TRY(pass_pair(c[0].A, c[0].m, c[0].n, c[0].lda, p[f].in, p[f].out, p[t].in, p[t].out, c[0].S, st));
+  } else {
+    for (int i = 0; i < nc; ++i) CNMF_TRY(run_plan(c[i], p[i], st));
+  }
+  for (int i = 0; i < nc; ++i) chain_advance(c[i], p[i]);
   return CNMF_OK;
 }
 
@@ -204,7 +219,7 @@ static int chains_run(Chain* c, int nc, cudaStream_t st) {
   SweepPanel p[2];
   const int passes = 2 * c[0].w + 1;
   for (int t = 0; t < passes; ++t) {
-    for (int i = 0; i < nc; ++i) CNMF_TRY(chain_pass(c[i], st));
+    CNMF_TRY(chains_pass(c, nc, st));
     for (int i = 0; i < nc; ++i) p[i] = chain_panel(c[i]);
     CNMF_TRY(panel_sweep(p, nc, c[0].S, st));
   }

@@ -437,6 +437,20 @@ int pass_forward(const float* A, int64_t m, int64_t n, int64_t lda, const float*
   return fail(CNMF_ERR_ARGUMENT, "panel width must be 32, 64 or 128");
 }
 
+// the paired launch on the tensor-core path; two launches otherwise (or with
+// CNMF_PAIR_PASS=0)
+int pass_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W, float* Z,
+              int S, cudaStream_t st) {
+  static int paired = -1;
+  if (paired < 0) {
+    const char* e = getenv("CNMF_PAIR_PASS");
+    paired = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (paired && use_tc(S)) return pass_pair_tc(A, m, n, lda, X, Y, W, Z, S, st);
+  CNMF_TRY(pass_forward(A, m, n, lda, X, S, Y, st));
+  return pass_transpose(A, m, n, lda, W, S, Z, st);
+}
+
 int pass_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const float* W, int S, float* Z,
                    cudaStream_t st) {
   if (use_tc(S)) return pass_transpose_tc(A, m, n, lda, W, S, Z, st);

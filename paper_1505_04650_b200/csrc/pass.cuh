@@ -14,5 +14,10 @@ int pass_forward_tc(const float* A, int64_t m, int64_t n, int64_t lda, const flo
                     cudaStream_t st);
 int pass_transpose_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* W, int S, float* Z,
                       cudaStream_t st);
+// Y = A X and Z = A^T W in one launch (one A-read pipeline ramp per pair)
+int pass_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W, float* Z,
+              int S, cudaStream_t st);
+int pass_pair_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W, float* Z,
+                 int S, cudaStream_t st);
 
 }  // namespace cnmf

@@ -742,12 +742,415 @@ int launch_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* Bp
   return launch_tc_t<S, TRANS, false>(A, m, n, lda, Bpanel, out, st);
 }
 
+// ---------------------------------------------------------------------------
+// Paired pass: Y = A X (unit range 0) and Z = A^T W (unit range 1) in ONE
+// launch. The two range finders of the compressed NMF need exactly one
+// forward and one transpose pass per power step; a single launch pays the
+// pipeline ramp-up and tail once per step instead of twice. Every role walks
+// the concatenated unit sequence; the direction (A tile layout, panel,
+// output) is a per-tile runtime switch, the pipeline is the same as pass_tc.
+// ---------------------------------------------------------------------------
+struct PassSide {
+  float* out;
+  int64_t P;        // output rows
+  int64_t nblocks;  // 128-row output tiles
+  int nt;           // K tiles per output tile
+};
+
+// the (pass, output tile, K tile) walk of one CTA's unit range
+struct Walk {
+  int p;
+  int64_t ob;
+  int kt;
+  __device__ __forceinline__ void start(int64_t u0, int64_t U0, const PassSide& s0, const PassSide& s1) {
+    if (u0 < U0) {
+      p = 0;
+      ob = u0 / s0.nt;
+      kt = (int)(u0 - ob * s0.nt);
+    } else {
+      p = 1;
+      ob = (u0 - U0) / s1.nt;
+      kt = (int)(u0 - U0 - ob * s1.nt);
+    }
+  }
+  __device__ __forceinline__ void next(const PassSide& s0, const PassSide& s1) {
+    if (++kt == (p ? s1.nt : s0.nt)) {
+      kt = 0;
+      if (++ob == s0.nblocks && p == 0) {
+        p = 1;
+        ob = 0;
+      }
+    }
+  }
+};
+
+template <int S>
+__global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
+    pass_tc_pair(const __grid_constant__ TmaDesc tAf, const __grid_constant__ TmaDesc tX,
+                 const __grid_constant__ TmaDesc tAt, const __grid_constant__ TmaDesc tW, const PassSide s0,
+                 const PassSide s1, ZSync* __restrict__ zs) {
+  using C = TcCfg<S, false, false>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* sP = smem + C::ST * C::STAGE;                 // [SSP][BSPL]
+  uint64_t* full = (uint64_t*)(sP + C::SSP * C::BSPL);         // [ST] stage landed
+  uint64_t* empty = full + C::ST;                              // [ST] stage consumed by all splitters
+  uint64_t* pfull = empty + C::ST;                             // [SSP] split panel ready
+  uint64_t* mdone = pfull + C::SSP;                            // [MD] MMAs of K tile j retired
+  uint64_t* afull = mdone + C::MD;                             // [AST] split A in TMEM
+  uint64_t* tfull = afull + C::AST;                            // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;                                // [2] accumulator drained
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t U0 = s0.nblocks * s0.nt, U = U0 + s1.nblocks * s1.nt, G = gridDim.x, b = blockIdx.x;
+  const int64_t u0 = b * U / G, u1 = (b + 1) * U / G;
+  const int64_t ntiles = u1 - u0;
+  if (ntiles <= 0) return;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tAf);
+    prefetch_tmap(&tX);
+    prefetch_tmap(&tAt);
+    prefetch_tmap(&tW);
+    for (int s = 0; s < C::ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NSPLIT + C::NPW);
+    }
+    for (int s = 0; s < C::SSP; ++s) mbar_init(&pfull[s], C::NPW);
+    for (int s = 0; s < C::AST; ++s) mbar_init(&afull[s], C::NSPLIT);
+    for (int s = 0; s < C::MD; ++s) mbar_init(&mdone[s], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], C::NEPI);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kWarpMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // split-K outputs start at zero: every CTA zeroes a row slice of both
+  for (int q = 0; q < 2; ++q) {
+    const PassSide& sd = q ? s1 : s0;
+    const int64_t z0 = blockIdx.x * sd.P / gridDim.x, z1 = (blockIdx.x + 1) * sd.P / gridDim.x;
+    float4* o4 = reinterpret_cast<float4*>(sd.out + z0 * S);
+    for (int64_t i = threadIdx.x; i < (z1 - z0) * S / 4; i += blockDim.x) o4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&zs->arrived, 1u);
+  }
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kWarpTma) {
+    // ---------------- TMA producer ----------------
+    if (elect_one()) {
+      Ring<C::ST> r;
+      Walk w;
+      w.start(u0, U0, s0, s1);
+      for (int64_t it = 0; it < ntiles; ++it) {
+        if (it >= C::ST) mbar_wait(&empty[r.i], r.ph ^ 1);
+        unsigned char* dst = smem + r.i * C::STAGE;
+        mbar_arrive_expect_tx(&full[r.i], C::STAGE);
+        const int row0 = (int)(w.ob * BMT);
+        if (w.p == 0) {  // A rows [row0, +128), cols [kt*32, +32): K-major SW128; X rows [kt*32, +32)
+          tma_load_2d(dst, &tAf, &full[r.i], w.kt * BKT, row0);
+          tma_load_2d(dst + C::ABYTES, &tX, &full[r.i], 0, w.kt * BKT);
+        } else {  // A rows [kt*32, +32) (K), cols [row0, +128) (M): row-major; W rows [kt*32, +32)
+          tma_load_2d(dst, &tAt, &full[r.i], row0, w.kt * BKT);
+          tma_load_2d(dst + C::ABYTES, &tW, &full[r.i], 0, w.kt * BKT);
+        }
+        r.next();
+        w.next(s0, s1);
+      }
+    }
+  } else if (warp >= kWarpEpi0) {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;
+    const int cg = 32 * ((warp - kWarpEpi0) >> 2);
+    const int row_in_tile = 32 * q + lane;
+    Ring<2> racc;
+    float acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+    Walk w;
+    w.start(u0, U0, s0, s1);
+    for (int64_t it = 0; it < ntiles; ++it) {
+      const int nt = w.p ? s1.nt : s0.nt;
+      const bool tile_end = (it == ntiles - 1) || (w.kt == nt - 1);
+      if (tile_end || ((w.kt + 1) % C::KB == 0)) {
+        mbar_wait(&tfull[racc.i], racc.ph);
+        tc_fence_after();
+        const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + racc.i * C::ACC_COLS + cg;
+#pragma unroll
+        for (int c0 = 0; c0 < 32; c0 += 16) {
+          float vh[16], vl[16];
+          tmem_ld16(taddr + c0, vh);
+          tmem_ld16(taddr + S + c0, vl);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[c0 + j] += vh[j] + vl[j];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[racc.i]);
+        racc.next();
+      }
+      if (tile_end) {
+        const PassSide& sd = w.p ? s1 : s0;
+        const int64_t t0 = (w.p ? U0 : 0) + w.ob * nt;  // first unit of this output tile
+        const bool owned = (t0 >= u0) && (t0 + nt <= u1);
+        const int64_t row = w.ob * BMT + row_in_tile;
+        if (!owned) {  // every CTA's zeroing must have landed
+          if (lane == 0) {
+            unsigned v;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&zs->arrived) : "memory");
+            } while (v < gridDim.x);
+          }
+          __syncwarp();
+        }
+        if (row < sd.P) {
+          float* dst = sd.out + row * S + cg;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            if (owned)
+              *(float4*)(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            else
+              red_add_v4(dst + j, acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+      }
+      w.next(s0, s1);
+    }
+  } else if (warp >= kWarpPanel0) {
+    // ---------------- panel splitters (direction-independent) ----------------
+    const int pw = warp - kWarpPanel0;
+    Ring<C::ST> r;
+    Ring<C::SSP> rp;
+    Ring<C::MD> rd;
+    for (int64_t it = 0; it < ntiles; ++it) {
+      mbar_wait(&full[r.i], r.ph);
+      const float* raw = (const float*)(smem + r.i * C::STAGE + C::ABYTES);
+      float h[C::PU][16], l[C::PU][16];
+#pragma unroll
+      for (int t = 0; t < C::PU; ++t) {
+        const int u = pw * C::PU + t;
+        const int n = 32 * (u >> 1) + lane;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float v = raw[(16 * (u & 1) + k) * S + n];
+          h[t][k] = tf32_rn(v);
+          l[t][k] = tf32_rn(v - h[t][k]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[r.i]);
+      if (it >= C::SSP) {
+        mbar_wait(&mdone[rd.i], rd.ph);
+        rd.next();
+      }
+      unsigned char* dst = sP + rp.i * C::BSPL;
+#pragma unroll
+      for (int t = 0; t < C::PU; ++t) {
+        const int u = pw * C::PU + t;
+        const int n = 32 * (u >> 1) + lane;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c = 4 * (u & 1) + cc;
+          const uint32_t off = (uint32_t)n * 128 + ((c ^ (n & 7)) << 4);
+          *(float4*)(dst + off) = make_float4(h[t][4 * cc], h[t][4 * cc + 1], h[t][4 * cc + 2], h[t][4 * cc + 3]);
+          *(float4*)(dst + S * 128 + off) =
+              make_float4(l[t][4 * cc], l[t][4 * cc + 1], l[t][4 * cc + 2], l[t][4 * cc + 3]);
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull[rp.i]);
+      r.next();
+      rp.next();
+    }
+  } else if (warp == kWarpMma) {
+    // ---------------- MMA issuer (direction-independent) ----------------
+    constexpr uint32_t idesc_cat = idesc_tf32(2 * S, false, false);
+    constexpr uint32_t idesc_hi = idesc_tf32(S, false, false);
+    Ring<C::SSP> rp;
+    Ring<C::AST> ra;
+    Ring<C::MD> rd;
+    Ring<2> racc;
+    Walk w;
+    w.start(u0, U0, s0, s1);
+    bool block_start = true;
+    for (int64_t it = 0; it < ntiles; ++it) {
+      const int nt = w.p ? s1.nt : s0.nt;
+      const bool tile_end = (it == ntiles - 1) || (w.kt == nt - 1);
+      const bool block_end = tile_end || ((w.kt + 1) % C::KB == 0);
+      if (block_start && racc.wrapped) mbar_wait(&tempty[racc.i], racc.ph ^ 1);
+      mbar_wait(&pfull[rp.i], rp.ph);
+      mbar_wait(&afull[ra.i], ra.ph);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sb = smem_u32(sP + rp.i * C::BSPL);
+        const uint32_t ahi = tmem + C::A_COL0 + ra.i * 2 * BKT;
+        const uint32_t alo = ahi + BKT;
+        const uint32_t dcat = tmem + racc.i * C::ACC_COLS;
+        const uint32_t dlo = dcat + S;
+#pragma unroll
+        for (int k = 0; k < BKT / 8; ++k) {
+          const uint64_t bcat = smem_desc(sb + 32 * k, 16, 1024);
+          const uint32_t acc = (block_start && k == 0) ? 0u : 1u;
+          tc_mma_ts(dcat, ahi + 8 * k, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
+          tc_mma_ts(dlo, alo + 8 * k, bcat, idesc_hi, 1u);     //            + A_lo X_hi
+        }
+        tc_commit(&mdone[rd.i]);
+        if (block_end) tc_commit(&tfull[racc.i]);
+      }
+      __syncwarp();
+      rp.next();
+      ra.next();
+      rd.next();
+      block_start = block_end;
+      if (block_end) racc.next();
+      w.next(s0, s1);
+    }
+  } else {
+    // ---------------- A splitters (warps 2..9): per-tile direction ----------------
+    const int q = warp & 3;
+    const int half = (warp - kWarpSplit0) >> 2;
+    const int row_in_tile = 32 * q + lane;
+    Ring<C::ST> r;
+    Ring<C::AST> ra;
+    Ring<C::MD> rd;
+    Walk w;
+    w.start(u0, U0, s0, s1);
+    for (int64_t it = 0; it < ntiles; ++it) {
+      mbar_wait(&full[r.i], r.ph);
+      float hi[16], lo[16];
+      if (w.p == 0) {
+        const unsigned char* rowp = smem + r.i * C::STAGE + row_in_tile * 128;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c = 4 * half + cc;
+          const float4 v = *(const float4*)(rowp + ((c ^ (row_in_tile & 7)) << 4));
+          hi[4 * cc + 0] = v.x;
+          hi[4 * cc + 1] = v.y;
+          hi[4 * cc + 2] = v.z;
+          hi[4 * cc + 3] = v.w;
+        }
+      } else {
+        const float* raw = (const float*)(smem + r.i * C::STAGE) + row_in_tile;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) hi[k] = raw[(16 * half + k) * BMT];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[r.i]);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float v = hi[k];
+        hi[k] = tf32_rn(v);
+        lo[k] = tf32_rn(v - hi[k]);
+      }
+      if (it >= C::AST) {
+        mbar_wait(&mdone[rd.i], rd.ph);
+        rd.next();
+      }
+      tc_fence_after();
+      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + C::A_COL0 + ra.i * 2 * BKT + 16 * half;
+      tmem_st16(ta, hi);
+      tmem_st16(ta + BKT, lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&afull[ra.i]);
+      r.next();
+      ra.next();
+      w.next(s0, s1);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0 && atomicAdd(&zs->finished, 1u) == gridDim.x - 1) {
+    zs->arrived = 0u;
+    zs->finished = 0u;
+  }
+  if (warp == kWarpMma)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+}
+
+template <int S>
+int launch_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W, float* Z,
+                cudaStream_t st) {
+  using C = TcCfg<S, false, false>;
+  TmaDesc tAf, tX, tAt, tW;
+  CNMF_TRY(make_tma_2d(&tAf, A, 4, m, n, lda, BKT, BMT, true));
+  CNMF_TRY(make_tma_2d(&tAt, A, 4, m, n, lda, BMT, BKT, false));
+  CNMF_TRY(make_tma_2d(&tX, X, 4, n, S, S, S, BKT, false));
+  CNMF_TRY(make_tma_2d(&tW, W, 4, m, S, S, S, BKT, false));
+  const PassSide s0{Y, m, ceil_div(m, BMT), (int)ceil_div(n, BKT)};
+  const PassSide s1{Z, n, ceil_div(n, BMT), (int)ceil_div(m, BKT)};
+  const int64_t U = s0.nblocks * s0.nt + s1.nblocks * s1.nt;
+  const int64_t grid = std::min<int64_t>(kNumSMs, U);
+  static ZSync* ring = nullptr;
+  static unsigned next = 0;
+  if (ring == nullptr) {
+    CNMF_CUDA(cudaMalloc(&ring, 64 * sizeof(ZSync)));
+    CNMF_CUDA(cudaMemset(ring, 0, 64 * sizeof(ZSync)));
+  }
+  ZSync* zs = ring + (next++ % 64);
+  static bool attr = false;
+  if (!attr) {
+    CNMF_CUDA(cudaFuncSetAttribute(pass_tc_pair<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (pass_profiling()) {
+    CNMF_CUDA(cudaEventCreate(&e0));
+    CNMF_CUDA(cudaEventCreate(&e1));
+    CNMF_CUDA(cudaEventRecord(e0, st));
+  }
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)grid);
+  lc.blockDim = dim3(C::THREADS);
+  lc.dynamicSmemBytes = C::SMEM;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  CNMF_CUDA(cudaLaunchKernelEx(&lc, pass_tc_pair<S>, tAf, tX, tAt, tW, s0, s1, zs));
+  CNMF_LAUNCH_CHECK();
+  if (e0) {
+    CNMF_CUDA(cudaEventRecord(e1, st));
+    // bytes of two passes: A twice plus the four panels
+    pass_record(e0, e1, 2.0 * 4.0 * ((double)m * n + (double)n * S + (double)m * S));
+  }
+  return CNMF_OK;
+}
+
 }  // namespace
 
 int pass_forward_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y, cudaStream_t st) {
   switch (S) {
     case 32: return launch_tc<32, false>(A, m, n, lda, X, Y, st);
     case 64: return launch_tc<64, false>(A, m, n, lda, X, Y, st);
+  }
+  return fail(CNMF_ERR_ARGUMENT, "tensor-core pass supports panel widths 32 and 64");
+}
+
+// Y = A X and Z = A^T W in one launch (tensor-core path, panel widths 32/64)
+int pass_pair_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W, float* Z,
+                 int S, cudaStream_t st) {
+  switch (S) {
+    case 32: return launch_pair<32>(A, m, n, lda, X, Y, W, Z, st);
+    case 64: return launch_pair<64>(A, m, n, lda, X, Y, W, Z, st);
   }
   return fail(CNMF_ERR_ARGUMENT, "tensor-core pass supports panel widths 32 and 64");
 }

@@ -365,6 +365,30 @@ def test_passes_split_k_repeated(m, n):
         assert ((z.double() - zref).abs().max() / zref.abs().max()).item() < 1e-5
 
 
+@pytest.mark.parametrize("m,n,s", [(10000, 5000, 30), (4000, 3000, 30), (3000, 4000, 30), (300, 200, 30),
+                                   (2500, 1300, 60)])
+def test_paired_pass_matches_separate(m, n, s):
+    # one launch computing Y = A X and Z = A^T W (both range finders' passes)
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n)
+    a = torch.rand(m, n, device="cuda", generator=g)
+    A = DeviceMatrix(a)
+    S = 32 if s <= 32 else 64
+    x = zeros((n, S))
+    w = zeros((m, S))
+    x[:, :s] = torch.randn(n, s, device="cuda", generator=g)
+    w[:, :s] = torch.randn(m, s, device="cuda", generator=g)
+    lib = _lib.load()
+    yref = a.double() @ x.double()
+    zref = a.double().t() @ w.double()
+    for _ in range(6):
+        y, z = zeros((m, S)), zeros((n, S))
+        _lib.call("cnmf_pass_pair", A.ptr, m, n, A.lda, x.data_ptr(), y.data_ptr(), w.data_ptr(), z.data_ptr(), s,
+                  stream())
+        torch.cuda.synchronize()
+        assert ((y.double() - yref).abs().max() / yref.abs().max()).item() < 1e-5
+        assert ((z.double() - zref).abs().max() / zref.abs().max()).item() < 1e-5
+
+
 def test_compression_repeatable():
     # split-K passes reduce with fp32 atomics (order varies run to run); the
     # signal subspace is stable far below the 1e-4 tolerance
