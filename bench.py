@@ -303,12 +303,13 @@ def run_ours(args):
     pass_flops = 2.0 * M * N * 32  # padded panel width 32 for s = 30
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak,
-                # dram__bytes_read.sum + dram__bytes_write.sum of one configs[1] forward pass_tc launch
-                # (ncu --set full, profiles/r01_pass_tc_cfg1_ncu_full.txt): 205.37 MB + 6.19 MB against
-                # 202 MB algorithmic (A plus the two panels)
-                "traffic": 211.56e6 if (M, N) == (10000, 5000) else None, "traffic_unit": "bytes per launch",
+                # dram__bytes_read.sum + dram__bytes_write.sum of one configs[1] pass_tc_pair launch (ncu --set
+                # full, profiles/r01_pass_tc_pair_cfg1_ncu_full.txt): 332.88 MB + 6.72 MB against 403.8 MB
+                # algorithmic -- the second direction's A tiles partly come from L2
+                "traffic": 339.6e6 if (M, N) == (10000, 5000) else None, "traffic_unit": "bytes per paired launch",
                 "algorithmic_bytes_per_launch": pass_bytes,
-                "kernel": "pass_tc<32> tcgen05 3xTF32 streaming passes (CUDA events on the launch stream)",
+                "kernel": "pass_tc_pair<32> (both range finders' passes of a power step in one launch) + pass_tc<32> "
+                          "(core projection), tcgen05 3xTF32, CUDA events on the launch stream",
                 "launches": pl.value, "avg_launch_ms": pass_avg_ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
                 "fp32_tflops": pass_flops / (pass_avg_ms * 1e-3) / 1e12, "fp32_peak_tflops_at_clock": fp32_peak,
