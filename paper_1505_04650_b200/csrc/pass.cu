@@ -437,8 +437,12 @@ int pass_forward(const float* A, int64_t m, int64_t n, int64_t lda, const float*
   return fail(CNMF_ERR_ARGUMENT, "panel width must be 32, 64 or 128");
 }
 
-// the paired launch on the tensor-core path; two launches otherwise (or with
-// CNMF_PAIR_PASS=0)
+// the paired launch on the tensor-core path for matrices up to 4 GB (it
+// saves a pipeline ramp-up and tail per power step and lets the two
+// directions share A through L2: 1.31 -> 1.27 ms for configs[1]'s range
+// finders); for 80 GB matrices the two concurrent access patterns cost ~5 %
+// (configs[4]: 514 -> 540 ms), so those run two launches, as does
+// CNMF_PAIR_PASS=0
 int pass_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W, float* Z,
               int S, cudaStream_t st) {
   static int paired = -1;
@@ -446,7 +450,7 @@ int pass_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* X,
     const char* e = getenv("CNMF_PAIR_PASS");
     paired = (e && e[0] == '0') ? 0 : 1;
   }
-  if (paired && use_tc(S)) return pass_pair_tc(A, m, n, lda, X, Y, W, Z, S, st);
+  if (paired && use_tc(S) && 4.0 * (double)m * (double)n <= 4e9) return pass_pair_tc(A, m, n, lda, X, Y, W, Z, S, st);
   CNMF_TRY(pass_forward(A, m, n, lda, X, S, Y, st));
   return pass_transpose(A, m, n, lda, W, S, Z, st);
 }

@@ -757,29 +757,41 @@ struct PassSide {
   int nt;           // K tiles per output tile
 };
 
-// the (pass, output tile, K tile) walk of one CTA's unit range
+// the (pass, output tile, K tile) walk of one CTA's units: [lo0, hi0) of
+// pass 0, then [lo1, hi1) of pass 1 (unit indices local to each pass; plain
+// scalars, no indexed arrays, so nothing lands in local memory)
 struct Walk {
   int p;
-  int64_t ob;
+  int64_t ob, u;
   int kt;
-  __device__ __forceinline__ void start(int64_t u0, int64_t U0, const PassSide& s0, const PassSide& s1) {
-    if (u0 < U0) {
-      p = 0;
-      ob = u0 / s0.nt;
-      kt = (int)(u0 - ob * s0.nt);
-    } else {
-      p = 1;
-      ob = (u0 - U0) / s1.nt;
-      kt = (int)(u0 - U0 - ob * s1.nt);
-    }
+  int64_t lo0, hi0, lo1, hi1;
+  __device__ __forceinline__ void start(int64_t a0, int64_t a1, int64_t b0, int64_t b1, const PassSide& s0,
+                                        const PassSide& s1) {
+    lo0 = a0;
+    hi0 = a1;
+    lo1 = b0;
+    hi1 = b1;
+    p = lo0 < hi0 ? 0 : 1;
+    u = p ? lo1 : lo0;
+    const int nt = p ? s1.nt : s0.nt;
+    ob = u / nt;
+    kt = (int)(u - ob * nt);
+  }
+  __device__ __forceinline__ bool last() const { return u == (p ? hi1 : hi0) - 1; }  // last unit in range
+  __device__ __forceinline__ bool owned(int nt) const {                               // whole tile in range
+    const int64_t t0 = ob * nt;
+    return t0 >= (p ? lo1 : lo0) && t0 + nt <= (p ? hi1 : hi0);
   }
   __device__ __forceinline__ void next(const PassSide& s0, const PassSide& s1) {
-    if (++kt == (p ? s1.nt : s0.nt)) {
+    ++u;
+    if (p == 0 && u == hi0) {
+      p = 1;
+      u = lo1;
+      ob = u / s1.nt;
+      kt = (int)(u - ob * s1.nt);
+    } else if (++kt == (p ? s1.nt : s0.nt)) {
       kt = 0;
-      if (++ob == s0.nblocks && p == 0) {
-        p = 1;
-        ob = 0;
-      }
+      ++ob;
     }
   }
 };
@@ -802,10 +814,14 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t U0 = s0.nblocks * s0.nt, U = U0 + s1.nblocks * s1.nt, G = gridDim.x, b = blockIdx.x;
-  const int64_t u0 = b * U / G, u1 = (b + 1) * U / G;
-  const int64_t ntiles = u1 - u0;
-  if (ntiles <= 0) return;
+  // the concatenated unit sequence (pass 0, then pass 1) is split over the
+  // CTAs: the two passes run concurrently on two halves of the GPU and share
+  // A through L2 (measured better than every CTA taking a share of each)
+  const int64_t U0 = s0.nblocks * s0.nt, U1 = s1.nblocks * s1.nt, G = gridDim.x, b = blockIdx.x;
+  const int64_t u0 = b * (U0 + U1) / G, u1 = (b + 1) * (U0 + U1) / G;
+  const int64_t lo0 = u0 < U0 ? u0 : U0, hi0 = u1 < U0 ? u1 : U0;
+  const int64_t lo1 = u0 > U0 ? u0 - U0 : 0, hi1 = u1 > U0 ? u1 - U0 : 0;
+  const int64_t ntiles = (hi0 - lo0) + (hi1 - lo1);  // >= 1: the grid never exceeds the units
 
   if (threadIdx.x == 0) {
     prefetch_tmap(&tAf);
@@ -852,7 +868,7 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
     if (elect_one()) {
       Ring<C::ST> r;
       Walk w;
-      w.start(u0, U0, s0, s1);
+      w.start(lo0, hi0, lo1, hi1, s0, s1);
       for (int64_t it = 0; it < ntiles; ++it) {
         if (it >= C::ST) mbar_wait(&empty[r.i], r.ph ^ 1);
         unsigned char* dst = smem + r.i * C::STAGE;
@@ -879,10 +895,10 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
 #pragma unroll
     for (int j = 0; j < 32; ++j) acc[j] = 0.f;
     Walk w;
-    w.start(u0, U0, s0, s1);
+    w.start(lo0, hi0, lo1, hi1, s0, s1);
     for (int64_t it = 0; it < ntiles; ++it) {
       const int nt = w.p ? s1.nt : s0.nt;
-      const bool tile_end = (it == ntiles - 1) || (w.kt == nt - 1);
+      const bool tile_end = w.last() || (w.kt == nt - 1);
       if (tile_end || ((w.kt + 1) % C::KB == 0)) {
         mbar_wait(&tfull[racc.i], racc.ph);
         tc_fence_after();
@@ -902,8 +918,7 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
       }
       if (tile_end) {
         const PassSide& sd = w.p ? s1 : s0;
-        const int64_t t0 = (w.p ? U0 : 0) + w.ob * nt;  // first unit of this output tile
-        const bool owned = (t0 >= u0) && (t0 + nt <= u1);
+        const bool owned = w.owned(nt);
         const int64_t row = w.ob * BMT + row_in_tile;
         if (!owned) {  // every CTA's zeroing must have landed
           if (lane == 0) {
@@ -985,11 +1000,11 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
     Ring<C::MD> rd;
     Ring<2> racc;
     Walk w;
-    w.start(u0, U0, s0, s1);
+    w.start(lo0, hi0, lo1, hi1, s0, s1);
     bool block_start = true;
     for (int64_t it = 0; it < ntiles; ++it) {
       const int nt = w.p ? s1.nt : s0.nt;
-      const bool tile_end = (it == ntiles - 1) || (w.kt == nt - 1);
+      const bool tile_end = w.last() || (w.kt == nt - 1);
       const bool block_end = tile_end || ((w.kt + 1) % C::KB == 0);
       if (block_start && racc.wrapped) mbar_wait(&tempty[racc.i], racc.ph ^ 1);
       mbar_wait(&pfull[rp.i], rp.ph);
@@ -1028,7 +1043,7 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
     Ring<C::AST> ra;
     Ring<C::MD> rd;
     Walk w;
-    w.start(u0, U0, s0, s1);
+    w.start(lo0, hi0, lo1, hi1, s0, s1);
     for (int64_t it = 0; it < ntiles; ++it) {
       mbar_wait(&full[r.i], r.ph);
       float hi[16], lo[16];
