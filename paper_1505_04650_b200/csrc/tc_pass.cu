@@ -244,6 +244,13 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
       : "memory");
 }
 
+// 32 lanes x 8 consecutive 32-bit columns per warp
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+
 // TRANS = false: Y = A X; TRANS = true: Z = A^T W. P = output rows of the
 // pass (m or n); nt = K tiles per output tile.
 //
@@ -796,12 +803,21 @@ struct Walk {
   }
 };
 
-template <int S>
-__global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
+// NS A-splitting warps (8: two per TMEM lane quarter, 16 K values each; 16:
+// four per quarter, 8 K values each)
+template <int NS>
+struct PairWarps {
+  static constexpr int kSplit0 = 2, kPanel0 = 2 + NS, kEpi0 = 4 + NS, KP = 128 / NS;
+};
+
+template <int S, int NS>
+__global__ void __launch_bounds__(32 * (4 + NS + 4 * (S / 32)), 1)
     pass_tc_pair(const __grid_constant__ TmaDesc tAf, const __grid_constant__ TmaDesc tX,
                  const __grid_constant__ TmaDesc tAt, const __grid_constant__ TmaDesc tW, const PassSide s0,
                  const PassSide s1, ZSync* __restrict__ zs) {
   using C = TcCfg<S, false, false>;
+  using PW = PairWarps<NS>;
+  constexpr int kWarpSplit0 = PW::kSplit0, kWarpPanel0 = PW::kPanel0, kWarpEpi0 = PW::kEpi0, KP = PW::KP;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* sP = smem + C::ST * C::STAGE;                 // [SSP][BSPL]
   uint64_t* full = (uint64_t*)(sP + C::SSP * C::BSPL);         // [ST] stage landed
@@ -830,10 +846,10 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
     prefetch_tmap(&tW);
     for (int s = 0; s < C::ST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], C::NSPLIT + C::NPW);
+      mbar_init(&empty[s], NS + C::NPW);
     }
     for (int s = 0; s < C::SSP; ++s) mbar_init(&pfull[s], C::NPW);
-    for (int s = 0; s < C::AST; ++s) mbar_init(&afull[s], C::NSPLIT);
+    for (int s = 0; s < C::AST; ++s) mbar_init(&afull[s], NS);
     for (int s = 0; s < C::MD; ++s) mbar_init(&mdone[s], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -1035,9 +1051,10 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
       w.next(s0, s1);
     }
   } else {
-    // ---------------- A splitters (warps 2..9): per-tile direction ----------------
+    // ---------------- A splitters: per-tile direction ----------------
+    // warp w serves TMEM lane quarter w & 3 and K part (w - 2) / 4 (KP values)
     const int q = warp & 3;
-    const int half = (warp - kWarpSplit0) >> 2;
+    const int part = (warp - kWarpSplit0) >> 2;
     const int row_in_tile = 32 * q + lane;
     Ring<C::ST> r;
     Ring<C::AST> ra;
@@ -1046,12 +1063,12 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
     w.start(lo0, hi0, lo1, hi1, s0, s1);
     for (int64_t it = 0; it < ntiles; ++it) {
       mbar_wait(&full[r.i], r.ph);
-      float hi[16], lo[16];
+      float hi[KP], lo[KP];
       if (w.p == 0) {
         const unsigned char* rowp = smem + r.i * C::STAGE + row_in_tile * 128;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const int c = 4 * half + cc;
+        for (int cc = 0; cc < KP / 4; ++cc) {
+          const int c = (KP / 4) * part + cc;
           const float4 v = *(const float4*)(rowp + ((c ^ (row_in_tile & 7)) << 4));
           hi[4 * cc + 0] = v.x;
           hi[4 * cc + 1] = v.y;
@@ -1061,12 +1078,12 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
       } else {
         const float* raw = (const float*)(smem + r.i * C::STAGE) + row_in_tile;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) hi[k] = raw[(16 * half + k) * BMT];
+        for (int k = 0; k < KP; ++k) hi[k] = raw[(KP * part + k) * BMT];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[r.i]);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < KP; ++k) {
         const float v = hi[k];
         hi[k] = tf32_rn(v);
         lo[k] = tf32_rn(v - hi[k]);
@@ -1076,9 +1093,14 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
         rd.next();
       }
       tc_fence_after();
-      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + C::A_COL0 + ra.i * 2 * BKT + 16 * half;
-      tmem_st16(ta, hi);
-      tmem_st16(ta + BKT, lo);
+      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + C::A_COL0 + ra.i * 2 * BKT + KP * part;
+      if constexpr (KP == 16) {
+        tmem_st16(ta, *reinterpret_cast<const float(*)[16]>(hi));
+        tmem_st16(ta + BKT, *reinterpret_cast<const float(*)[16]>(lo));
+      } else {
+        tmem_st8(ta, hi);
+        tmem_st8(ta + BKT, lo);
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
@@ -1098,6 +1120,10 @@ __global__ void __launch_bounds__(TcCfg<S, false, false>::THREADS, 1)
   if (warp == kWarpMma)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
 }
+
+#ifndef CNMF_PAIR_NSPLIT
+#define CNMF_PAIR_NSPLIT 8
+#endif
 
 template <int S>
 int launch_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W, float* Z,
@@ -1121,7 +1147,7 @@ int launch_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* 
   ZSync* zs = ring + (next++ % 64);
   static bool attr = false;
   if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(pass_tc_pair<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    CNMF_CUDA(cudaFuncSetAttribute(pass_tc_pair<S, CNMF_PAIR_NSPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1132,7 +1158,7 @@ int launch_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* 
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3((unsigned)grid);
-  lc.blockDim = dim3(C::THREADS);
+  lc.blockDim = dim3(32 * (4 + CNMF_PAIR_NSPLIT + 4 * (S / 32)));
   lc.dynamicSmemBytes = C::SMEM;
   lc.stream = st;
   cudaLaunchAttribute at[1];
@@ -1140,7 +1166,7 @@ int launch_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  CNMF_CUDA(cudaLaunchKernelEx(&lc, pass_tc_pair<S>, tAf, tX, tAt, tW, s0, s1, zs));
+  CNMF_CUDA(cudaLaunchKernelEx(&lc, pass_tc_pair<S, CNMF_PAIR_NSPLIT>, tAf, tX, tAt, tW, s0, s1, zs));
   CNMF_LAUNCH_CHECK();
   if (e0) {
     CNMF_CUDA(cudaEventRecord(e1, st));
