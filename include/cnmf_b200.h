@@ -182,7 +182,7 @@ int cnmf_nnls_gram(const double* gram, const double* target, int64_t k, int q, d
 int cnmf_gram_f64(const double* X, int64_t p, int a, const double* Y, int b, double* out, void* stream);
 
 /* ---- projections (nmf.py:138 _projected_data, nmf.py:329-332) ------------
- * out (S x S, fp64, device) = P1^T P2 for row-aligned panels (S = 32, 64). */
+ * out (S x S, fp64, device) = P1^T P2 for row-aligned panels (S = 32, 64, 128). */
 int cnmf_panel_cross(const float* P1, const float* P2, int64_t rows, int S, double* out, void* stream);
 
 /* ---- relative error (nmf.py:53 relative_error) ---------------------------

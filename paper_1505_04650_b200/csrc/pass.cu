@@ -486,7 +486,7 @@ template <int S>
 __global__ void __launch_bounds__(256)
     panel_cross_kernel(const float* __restrict__ P1, const float* __restrict__ P2, int64_t rows,
                        double* __restrict__ out) {
-  constexpr int TR = 64, NB = S / 4, NBLK = NB * NB, BPT = (NBLK + 255) / 256;
+  constexpr int TR = S > 64 ? 32 : 64, NB = S / 4, NBLK = NB * NB, BPT = (NBLK + 255) / 256;
   __shared__ __align__(16) float s1[TR * S];
   __shared__ __align__(16) float s2[TR * S];
   const int tid = threadIdx.x;
@@ -553,8 +553,9 @@ int panel_cross(const float* P1, const float* P2, int64_t rows, int S, double* o
   switch (S) {
     case 32: return launch_cross<32>(P1, P2, rows, out, st);
     case 64: return launch_cross<64>(P1, P2, rows, out, st);
+    case 128: return launch_cross<128>(P1, P2, rows, out, st);
   }
-  return fail(CNMF_ERR_ARGUMENT, "panel_cross supports widths 32 and 64");
+  return fail(CNMF_ERR_ARGUMENT, "panel_cross supports widths 32, 64 and 128");
 }
 
 }  // namespace cnmf

@@ -163,10 +163,19 @@ def snmf(a, r, selector="spa", reduction="compressed", cfg=None, nnls_tol=1e-10,
         cfg = adjust_config(cfg, m, n)
         basis, _ = _compress(A, cfg, 0)
         q = basis.panel
+    elif reduction == "qr" and n > m:
+        # full QR reduction of a fat matrix (snmf.py:140-151): Q is square
+        # (m x m) and orthogonal, so Q^T A is a rotation of A. SPA's norms and
+        # projections, XRAY's mass functional (Q Q^T 1 = 1) and the NNLS
+        # objectives do not depend on which orthogonal Q it is, so Q = I gives
+        # the reference's selections and errors without factorising anything
+        if m > 128:
+            raise ArgumentError("qr reduction of a fat matrix on the device needs m <= 128")
+        S = panel_ld(m)
+        q = zeros((m, S))
+        q[:, :m] = torch.eye(m, dtype=q.dtype, device=q.device)
     elif reduction == "qr":
-        # full QR reduction: orthonormalise A itself (tall inputs, n <= 128)
-        if n > m:
-            raise ArgumentError("qr reduction on the device needs a tall matrix (n <= m)")
+        # full QR reduction of a tall matrix: orthonormalise A itself (n <= 128)
         S = panel_ld(n)
         q = zeros((m, S))
         q[:, :n] = A.t[:, :n]
@@ -174,7 +183,7 @@ def snmf(a, r, selector="spa", reduction="compressed", cfg=None, nnls_tol=1e-10,
         _lib.call("cnmf_orthonormalize", q.data_ptr(), m, n, None, ws.data_ptr(), ws.numel(), stream())
     else:
         raise ArgumentError(f"unknown reduction {reduction!r}")
-    s = int(min(q.shape[1], n if reduction == "qr" else cfg.basis_cols))
+    s = int(min(q.shape[1], min(m, n) if reduction == "qr" else cfg.basis_cols))
     S = q.shape[1]
     # reduced matrix (Q^T A), kept transposed: one transpose pass over A
     z = zeros((n, S))

@@ -244,6 +244,32 @@ def test_snmf_pipeline_vs_oracle(golden, sel):
     assert res.rel_error_full < 1e-5 and res.rel_error_reduced < 1e-5
 
 
+@pytest.mark.parametrize("sel", ["spa", "xray"])
+def test_snmf_qr_reduction_fat_and_tall(sel):
+    # the reference's own cases (tests/test_snmf.py: 50 x 200 and 40 x 300 fat
+    # matrices, exact rank 5; qr and compressed reductions must agree) plus a
+    # tall one, each against the oracle with the reference's canonical QR basis
+    for m, n, seed in ((50, 200, 0), (50, 200, 3), (40, 300, 14), (3000, 120, 12)):
+        a, truth = O.near_separable(m, n, 5 if m < 3000 else 4, 1.0, 0.0, seed=seed)
+        r = len(truth)
+        res = C.snmf(a, r, selector=sel, reduction="qr")
+        ref = O.snmf(a, r, selector=sel, basis=O.qr_pos(a)[0])
+        assert sorted(res.K.tolist()) == truth.tolist()
+        assert np.array_equal(res.K, ref.K)
+        assert res.rel_error_full <= 1e-6 and res.Y.min() >= 0
+        assert np.abs(res.Y - ref.Y).max() < 1e-4
+        cmp = C.snmf(a, r, selector=sel, reduction="compressed", cfg=C.CompressionConfig(r=r, r_ov=10, w=0, seed=seed))
+        assert set(cmp.K.tolist()) == set(res.K.tolist())
+
+
+def test_snmf_qr_reduction_limits():
+    a, _ = O.near_separable(200, 400, 5, 1.0, 0.0, seed=1)
+    with pytest.raises(C.ArgumentError):
+        C.snmf(a, 5, reduction="qr")  # fat with m > 128
+    with pytest.raises(C.ArgumentError):
+        C.snmf(a.T.copy(), 5, reduction="qr")  # tall with n > 128
+
+
 def test_snmf_near_separable_config0_shape():
     a, truth = O.near_separable(500, 2000, 10, 1.0, 0.01, seed=11)
     res = C.snmf(a, 10, selector="spa", cfg=C.CompressionConfig(r=10, r_ov=10, w=4, seed=2))
