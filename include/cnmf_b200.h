@@ -213,6 +213,20 @@ int cnmf_admm_run(const double* core, const float* L, int64_t m, const float* Rt
                   double step, int max_iter, double tol, double* trace, double* scores, int* iterations, int* done,
                   int resume, int step_limit, void* ws, size_t ws_bytes, void* stream);
 
+/* ---- uncompressed ADMM (nmf_admm(compressed=False), nmf.py:306-377 with
+ * identity bases: a_comp = A) ------------------------------------------------
+ * A (m x n fp32, device); u (m x r), vt (n x r) hold the seeded starts on
+ * entry (resume = 0) and U, V^T on return; du, dvt, xc (m x r) and yct
+ * (n x r, yc^T) are fp64 device buffers the call owns. trace / scores get one
+ * entry per iteration (nmf.py:362, 366). Protocol of cnmf_admm_run
+ * (resume, step_limit, *done). r <= 32. DivergenceError ->
+ * CNMF_ERR_DIVERGENCE with *iterations = the diverging iteration + 1. */
+size_t cnmf_admm_full_workspace(int64_t m, int64_t n, int r);
+int cnmf_admm_full_run(const float* A, int64_t m, int64_t n, int64_t lda, int r, double* u, double* du, double* vt,
+                       double* dvt, double* xc, double* yct, double pu, double pv, double step, int max_iter,
+                       double tol, double* trace, double* scores, int* iterations, int* done, int resume,
+                       int step_limit, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

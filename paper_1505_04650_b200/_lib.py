@@ -37,6 +37,9 @@ SIGNATURES = {
     "cnmf_pass_forward": (c_int, [vp, c_i64, c_i64, c_i64, vp, c_int, vp, vp]),
     "cnmf_pass_transpose": (c_int, [vp, c_i64, c_i64, c_i64, vp, c_int, vp, vp]),
     "cnmf_pass_pair": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, vp, vp, c_int, vp]),
+    "cnmf_admm_full_workspace": (c_size, [c_i64, c_i64, c_int]),
+    "cnmf_admm_full_run": (c_int, [vp, c_i64, c_i64, c_i64, c_int, vp, vp, vp, vp, vp, vp, c_dbl, c_dbl, c_dbl, c_int,
+                                   c_dbl, vp, vp, c_intp, c_intp, c_int, c_int, vp, c_size, vp]),
     "cnmf_compress_workspace": (c_size, [c_i64, c_i64, c_int]),
     "cnmf_structured_compress": (c_int, [vp, c_i64, c_i64, c_i64, c_int, c_int, c_u64, c_int, vp, vp, c_size, vp]),
     "cnmf_structured_compress_async": (c_int, [vp, c_i64, c_i64, c_i64, c_int, c_int, c_u64, c_int, vp, vp, c_size,

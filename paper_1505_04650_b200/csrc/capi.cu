@@ -10,6 +10,11 @@ int gaussian_fill(uint64_t, int64_t, int64_t, int64_t, int, void*, int64_t, cuda
 int uniform_fill(uint64_t, int64_t, int64_t, double, double, int, int, void*, cudaStream_t);
 
 int panel_cross(const float*, const float*, int64_t, int, double*, cudaStream_t);
+size_t admm_full_workspace(int64_t m, int64_t n, int r);
+int admm_full_run(const float* A, int64_t m, int64_t n, int64_t lda, int r, double* u, double* du, double* vt,
+                  double* dvt, double* xc, double* yct, double pu, double pv, double step, int max_iter, double tol,
+                  double* trace, double* scores, int* iterations, int* done, int resume, int step_limit, void* ws,
+                  size_t ws_bytes, cudaStream_t st);
 int cholesky_inverse(double*, int, int, double*, double*, cudaStream_t);
 int status_reset(void*, int, cudaStream_t);
 size_t small_workspace(int);
@@ -212,6 +217,23 @@ int cnmf_residual_norms(const float* A, int64_t m, int64_t n, int64_t lda, const
 }
 
 size_t cnmf_admm_workspace(int64_t m, int64_t n, int s, int r) { return admm_workspace(m, n, s, r); }
+
+size_t cnmf_admm_full_workspace(int64_t m, int64_t n, int r) { return admm_full_workspace(m, n, r); }
+
+int cnmf_admm_full_run(const float* A, int64_t m, int64_t n, int64_t lda, int r, double* u, double* du, double* vt,
+                       double* dvt, double* xc, double* yct, double pu, double pv, double step, int max_iter,
+                       double tol, double* trace, double* scores, int* iterations, int* done, int resume,
+                       int step_limit, void* ws, size_t ws_bytes, void* stream) {
+  CNMF_TRY(check_a(A, m, n, lda));
+  if (max_iter < 0) return fail(CNMF_ERR_ARGUMENT, "max_iter must be >= 0");
+  if (max_iter == 0) {
+    if (iterations) *iterations = 0;
+    if (done) *done = 1;
+    return CNMF_OK;
+  }
+  return admm_full_run(A, m, n, lda, r, u, du, vt, dvt, xc, yct, pu, pv, step, max_iter, tol, trace, scores,
+                       iterations, done, resume, step_limit, ws, ws_bytes, STREAM(stream));
+}
 
 int cnmf_admm_run(const double* core, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
                   double* du, double* vt, double* dvt, double* xc, double* yc, double pu, double pv, double step,

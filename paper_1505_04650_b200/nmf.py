@@ -154,7 +154,7 @@ def nmf_admm(a, r, compressed=True, cfg=None, penalty_u=1.0, penalty_v=1.0, step
     A = DeviceMatrix(a)
     m, n = A.m, A.n
     if not compressed:
-        raise ArgumentError("the device path implements the compressed ADMM (compressed=True)")
+        return _nmf_admm_full(A, r, cfg, penalty_u, penalty_v, step_scale, max_iter, tol, on_iteration)
     cfg = _resolve_config(r, cfg, m, n)
     left, right, core = compressed_problem(A, cfg)
 
@@ -170,6 +170,62 @@ def nmf_admm(a, r, compressed=True, cfg=None, penalty_u=1.0, penalty_v=1.0, step
     rel = _rel_error(A, u, vt)
     return FactorPair(X=out(u, A.on_host), Y=out(vt.t().contiguous(), A.on_host), iterations=iters,
                       objective_trace=trace, rel_error=rel)
+
+
+def _nmf_admm_full(A, r, cfg, penalty_u, penalty_v, step_scale, max_iter, tol, on_iteration):
+    """nmf_admm(compressed=False): the same loop with identity bases and
+    a_comp = A (nmf.py:326-335), csrc/admm_full.cu."""
+    m, n = A.m, A.n
+    if cfg is None:
+        cfg = CompressionConfig(r=r, r_ov=10, w=4, seed=0)
+    if cfg.r != r:
+        raise ArgumentError(f"cfg.r = {cfg.r} disagrees with rank argument {r}")
+    if not 1 <= r <= min(m, n):  # nmf.py:113-115
+        raise ArgumentError(f"rank {r} out of range for {m}x{n}")
+    rng = Rng(cfg.seed)
+    u = rng.child("init-left").uniform((m, r))
+    vt = rng.child("init-right").uniform((r, n), transpose=True)  # V^T, n x r
+    du = zeros((m, r), dtype=torch.float64)
+    dvt = zeros((n, r), dtype=torch.float64)
+    xc = zeros((m, r), dtype=torch.float64)
+    yct = zeros((n, r), dtype=torch.float64)
+    trace = zeros((max(max_iter, 1),), dtype=torch.float64)
+    scores = zeros((max(max_iter, 1),), dtype=torch.float64)
+    lib = _lib.load()
+    nbytes = lib.cnmf_admm_full_workspace(m, n, r)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=u.device)
+    it = ctypes.c_int(0)
+    done = ctypes.c_int(0)
+    args = lambda resume, limit: (A.ptr, m, n, A.lda, r, u.data_ptr(), du.data_ptr(), vt.data_ptr(), dvt.data_ptr(),
+                                  xc.data_ptr(), yct.data_ptr(), float(penalty_u), float(penalty_v), float(step_scale),
+                                  int(max_iter), float(tol), trace.data_ptr(), scores.data_ptr(), ctypes.byref(it),
+                                  ctypes.byref(done), resume, limit, ws.data_ptr(), nbytes, stream())
+
+    def diverged():
+        return dict(trace=scores[:it.value].tolist())
+
+    if on_iteration is None:
+        _lib.check(lib.cnmf_admm_full_run(*args(0, 0)), **diverged())
+    else:
+        resume = 0
+        seen = 0
+        while True:
+            _lib.check(lib.cnmf_admm_full_run(*args(resume, 1)), **diverged())
+            resume = 1
+            if it.value > seen:
+                seen = it.value
+                host = A.on_host
+                on_iteration(seen - 1, AdmmState(
+                    xc=out(xc.clone(), host), yc=out(yct.t().contiguous(), host), u=out(u.clone(), host),
+                    v=out(vt.t().contiguous(), host), dual_u=out(du.clone(), host),
+                    dual_v=out(dvt.t().contiguous(), host), penalty_u=penalty_u, penalty_v=penalty_v,
+                    step_scale=step_scale))
+            if done.value:
+                break
+    iters = it.value
+    rel = _rel_error(A, u, vt)
+    return FactorPair(X=out(u, A.on_host), Y=out(vt.t().contiguous(), A.on_host), iterations=iters,
+                      objective_trace=trace[:iters].tolist(), rel_error=rel)
 
 
 def run_admm(core, left_panel, m, right_panel, n, cfg, r, penalty_u=1.0, penalty_v=1.0, step_scale=1.0,

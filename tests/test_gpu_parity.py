@@ -472,3 +472,53 @@ def test_relative_error_matches(golden):
 def test_admm_validates():
     with pytest.raises(C.ArgumentError):
         C.nmf_admm(np.random.default_rng(0).uniform(size=(40, 30)), 2, penalty_u=0.0)
+
+
+# ---------------------------------------------------------------------------
+# nmf_admm(compressed=False): the uncompressed loop (csrc/admm_full.cu)
+
+def _full_case(m=300, n=200, r=5, seed=3):
+    a = O.dense_lowrank(m, n, r, 0.01, seed=seed).astype(np.float32)
+    return a, C.CompressionConfig(r=r, r_ov=10, w=4, seed=7), O.Config(r, 10, 4, 7)
+
+
+def test_admm_uncompressed_matches_oracle():
+    a, cfg, ocfg = _full_case()
+    res = C.nmf_admm(a, 5, compressed=False, cfg=cfg, max_iter=60)
+    ref = O.admm(a.astype(np.float64), 5, compressed=False, cfg=ocfg, max_iter=60)
+    assert res.iterations == ref.iterations == 60
+    assert abs(res.rel_error - ref.rel_error) <= 1e-3 * ref.rel_error
+    # the objective ||A - xc yc||^2 per iteration (nmf.py:362), evaluated as
+    # ||A||^2 - 2 <yc^T, A^T xc> + <Gx, Gy> from the iteration's own fp32
+    # products: absolute error ~1e-7 of ||A||^2 (3xTF32 and fp32 panels)
+    na2 = float(np.sum(a.astype(np.float64) ** 2))
+    assert np.abs(np.array(res.objective_trace) - np.array(ref.trace)).max() <= 1e-6 * na2
+    # early iterates agree to the fp32 products' precision
+    short = C.nmf_admm(a, 5, compressed=False, cfg=cfg, max_iter=5)
+    sref = O.admm(a.astype(np.float64), 5, compressed=False, cfg=ocfg, max_iter=5)
+    assert np.abs(short.X - sref.X).max() <= 1e-4 * max(1.0, np.abs(sref.X).max())
+    assert np.abs(short.Y - sref.Y).max() <= 1e-4 * max(1.0, np.abs(sref.Y).max())
+    assert short.X.min() >= 0 and short.Y.min() >= 0
+
+
+def test_admm_uncompressed_tol_stop_and_callback():
+    a, cfg, ocfg = _full_case(seed=5)
+    probe = O.admm(a.astype(np.float64), 5, compressed=False, cfg=ocfg, max_iter=30, tol=0.0)
+    tol = probe.scores[12] * (1 + 1e-3)  # first reached at iteration <= 12
+    ref = O.admm(a.astype(np.float64), 5, compressed=False, cfg=ocfg, max_iter=30, tol=tol)
+    seen = []
+    res = C.nmf_admm(a, 5, compressed=False, cfg=cfg, max_iter=30, tol=tol,
+                     on_iteration=lambda k, st: seen.append((k, np.array(st.u))))
+    assert res.iterations == ref.iterations < 30
+    assert [k for k, _ in seen] == list(range(res.iterations))
+    plain = C.nmf_admm(a, 5, compressed=False, cfg=cfg, max_iter=30, tol=tol)
+    assert plain.iterations == res.iterations
+    assert np.abs(seen[-1][1] - res.X).max() == 0.0
+
+
+def test_admm_uncompressed_limits():
+    a, cfg, _ = _full_case(m=100, n=80, r=5)
+    with pytest.raises(C.ArgumentError):
+        C.nmf_admm(a, 40, compressed=False, cfg=C.CompressionConfig(r=40, r_ov=10, w=4, seed=1))
+    res = C.nmf_admm(a, 5, compressed=False, cfg=cfg, max_iter=0)
+    assert res.iterations == 0
