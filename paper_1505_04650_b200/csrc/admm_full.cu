@@ -35,6 +35,7 @@ namespace {
 
 constexpr int kR = 32;        // lanes = columns of the iterates (r <= 32)
 constexpr int kThreads = 256;  // 8 warps, one row per warp at a time
+constexpr int kB = 4;          // rows whose loads a warp keeps in flight together
 
 struct FullCtrl {
   unsigned ticket[3];  // last-block detection of full_kkt / full_left / full_right
@@ -91,6 +92,18 @@ __device__ __forceinline__ void gram_acc(double (&g)[kR], double x, int r) {
   }
 }
 
+// the block's warps add their Gram rows into blk (r x r, stride kR) in turn:
+// plain shared-memory adds, no atomics
+__device__ __forceinline__ void block_gram(double* blk, const double (&g)[kR], int r, int lane, int warp) {
+  for (int w = 0; w < kThreads / 32; ++w) {
+    if (warp == w && lane < r)
+#pragma unroll
+      for (int l = 0; l < kR; ++l)
+        if (l < r) blk[lane * kR + l] += g[l];
+    __syncthreads();
+  }
+}
+
 // (G + ridge I)^-1 of an SPD r x r matrix by Gauss-Jordan in shared memory
 // (one block; the ridge keeps every pivot >= ridge > 0)
 __device__ void ridge_inverse(const double* G, double ridge, int r, double* H, double* w) {
@@ -103,10 +116,10 @@ __device__ void ridge_inverse(const double* G, double ridge, int r, double* H, d
   }
   __syncthreads();
   for (int k = 0; k < r; ++k) {
-    const double piv = w[k * W + k];
+    const double inv = 1.0 / w[k * W + k];
     __syncthreads();
     // scale row k, then eliminate column k from the other rows
-    for (int j = tid; j < W; j += blockDim.x) w[k * W + j] /= piv;
+    for (int j = tid; j < W; j += blockDim.x) w[k * W + j] *= inv;
     __syncthreads();
     for (int idx = tid; idx < r * W; idx += blockDim.x) {
       const int i = idx / W, j = idx - i * W;
@@ -160,11 +173,21 @@ __global__ void __launch_bounds__(kThreads) full_kkt(FullArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r = a.r;
   double g2 = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < a.m; i += (int64_t)gridDim.x * 8) {
-    const double x = lane < r ? a.xc[i * r + lane] : 0.0;
-    const double t = row_times(x, Gy, r, lane);
-    if (lane < r) {
-      const double g = t - (double)a.Y[i * a.S + lane] + a.du[i * r + lane];
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  for (int64_t i0 = (int64_t)blockIdx.x * 8 + warp; i0 < a.m; i0 += kB * stride) {
+    double x4[kB], y4[kB], d4[kB];  // loads of kB rows in flight together
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const int64_t i = i0 + q * stride;
+      const bool ok = lane < r && i < a.m;
+      x4[q] = ok ? a.xc[i * r + lane] : 0.0;
+      y4[q] = ok ? (double)a.Y[i * a.S + lane] : 0.0;
+      d4[q] = ok ? a.du[i * r + lane] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const double t = row_times(x4[q], Gy, r, lane);
+      const double g = t - y4[q] + d4[q];  // zero for padding lanes and rows past m
       g2 = fma(g, g, g2);
     }
   }
@@ -211,26 +234,40 @@ __global__ void __launch_bounds__(kThreads) full_left(FullArgs a) {
 #pragma unroll
   for (int l = 0; l < kR; ++l) g[l] = 0.0;
   double feas = 0.0, comp = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < a.m; i += (int64_t)gridDim.x * 8) {
-    const bool on = lane < r;
-    const double rhs = on ? (double)a.Y[i * a.S + lane] + a.pu * a.u[i * r + lane] - a.du[i * r + lane] : 0.0;
-    const double x = row_times(rhs, Hy, r, lane);
-    gram_acc(g, on ? x : 0.0, r);
-    a.Pxc[i * a.S + lane] = on ? (float)x : 0.f;
-    if (on) {
-      const double du0 = a.du[i * r + lane];
-      const double un = fmax(x + du0 / a.pu, 0.0);
-      const double dun = du0 + a.step * a.pu * (x - un);
-      a.xc[i * r + lane] = x;
-      a.u[i * r + lane] = un;
-      a.du[i * r + lane] = dun;
-      feas = fma(x - un, x - un, feas);
-      const double p = fmax(dun, 0.0);
-      comp += (dun * un) * (dun * un) + p * p;  // neg(u) = 0: u is a projection
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  const bool on = lane < r;
+  for (int64_t i0 = (int64_t)blockIdx.x * 8 + warp; i0 < a.m; i0 += kB * stride) {
+    double y4[kB], u4[kB], d4[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const int64_t i = i0 + q * stride;
+      const bool ok = on && i < a.m;
+      y4[q] = ok ? (double)a.Y[i * a.S + lane] : 0.0;
+      u4[q] = ok ? a.u[i * r + lane] : 0.0;
+      d4[q] = ok ? a.du[i * r + lane] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const int64_t i = i0 + q * stride;
+      if (i >= a.m) break;  // warp-uniform
+      const double rhs = y4[q] + a.pu * u4[q] - d4[q];
+      const double x = row_times(rhs, Hy, r, lane);
+      gram_acc(g, on ? x : 0.0, r);
+      a.Pxc[i * a.S + lane] = on ? (float)x : 0.f;
+      if (on) {
+        const double du0 = d4[q];
+        const double un = fmax(x + du0 / a.pu, 0.0);
+        const double dun = du0 + a.step * a.pu * (x - un);
+        a.xc[i * r + lane] = x;
+        a.u[i * r + lane] = un;
+        a.du[i * r + lane] = dun;
+        feas = fma(x - un, x - un, feas);
+        const double p = fmax(dun, 0.0);
+        comp += (dun * un) * (dun * un) + p * p;  // neg(u) = 0: u is a projection
+      }
     }
   }
-  if (lane < r)
-    for (int l = 0; l < r; ++l) atomicAdd(&blk[lane * kR + l], g[l]);
+  block_gram(blk, g, r, lane, warp);
   feas = warp_sum(feas);
   comp = warp_sum(comp);
   if (lane == 0) {
@@ -281,36 +318,50 @@ __global__ void __launch_bounds__(kThreads) full_right(FullArgs a, int init) {
 #pragma unroll
   for (int l = 0; l < kR; ++l) g[l] = 0.0;
   double yz = 0.0, grad = 0.0, feas = 0.0, comp = 0.0;
-  for (int64_t j = (int64_t)blockIdx.x * 8 + warp; j < a.n; j += (int64_t)gridDim.x * 8) {
-    double y;
-    if (init) {  // the start: yc = v (identity right basis, nmf.py:342)
-      y = on ? a.vt[j * r + lane] : 0.0;
-      if (on) a.yct[j * r + lane] = y;
-    } else {
-      const double z = on ? (double)a.Z[j * a.S + lane] : 0.0;
-      const double rhs = on ? z + a.pv * a.vt[j * r + lane] - a.dvt[j * r + lane] : 0.0;
-      y = row_times(rhs, Hx, r, lane);
-      const double t = row_times(on ? y : 0.0, Gx, r, lane);  // (yc^T Gx)_j
-      if (on) {
-        const double dv0 = a.dvt[j * r + lane];
-        const double vn = fmax(y + dv0 / a.pv, 0.0);
-        const double dvn = dv0 + a.step * a.pv * (y - vn);
-        a.yct[j * r + lane] = y;
-        a.vt[j * r + lane] = vn;
-        a.dvt[j * r + lane] = dvn;
-        yz = fma(y, z, yz);
-        const double gr = t - z + dvn;
-        grad = fma(gr, gr, grad);
-        feas = fma(y - vn, y - vn, feas);
-        const double p = fmax(dvn, 0.0);
-        comp += (dvn * vn) * (dvn * vn) + p * p;
-      }
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  for (int64_t j0 = (int64_t)blockIdx.x * 8 + warp; j0 < a.n; j0 += kB * stride) {
+    double z4[kB], v4[kB], d4[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const int64_t j = j0 + q * stride;
+      const bool ok = on && j < a.n;
+      z4[q] = ok && !init ? (double)a.Z[j * a.S + lane] : 0.0;
+      v4[q] = ok ? a.vt[j * r + lane] : 0.0;
+      d4[q] = ok && !init ? a.dvt[j * r + lane] : 0.0;
     }
-    gram_acc(g, on ? y : 0.0, r);
-    a.Pyc[j * a.S + lane] = on ? (float)y : 0.f;
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const int64_t j = j0 + q * stride;
+      if (j >= a.n) break;  // warp-uniform
+      double y;
+      if (init) {  // the start: yc = v (identity right basis, nmf.py:342)
+        y = v4[q];
+        if (on) a.yct[j * r + lane] = y;
+      } else {
+        const double z = z4[q];
+        const double rhs = z + a.pv * v4[q] - d4[q];
+        y = row_times(rhs, Hx, r, lane);
+        const double t = row_times(y, Gx, r, lane);  // (yc^T Gx)_j
+        if (on) {
+          const double dv0 = d4[q];
+          const double vn = fmax(y + dv0 / a.pv, 0.0);
+          const double dvn = dv0 + a.step * a.pv * (y - vn);
+          a.yct[j * r + lane] = y;
+          a.vt[j * r + lane] = vn;
+          a.dvt[j * r + lane] = dvn;
+          yz = fma(y, z, yz);
+          const double gr = t - z + dvn;
+          grad = fma(gr, gr, grad);
+          feas = fma(y - vn, y - vn, feas);
+          const double p = fmax(dvn, 0.0);
+          comp += (dvn * vn) * (dvn * vn) + p * p;
+        }
+      }
+      gram_acc(g, on ? y : 0.0, r);
+      a.Pyc[j * a.S + lane] = on ? (float)y : 0.f;
+    }
   }
-  if (on)
-    for (int l = 0; l < r; ++l) atomicAdd(&blk[lane * kR + l], g[l]);
+  block_gram(blk, g, r, lane, warp);
   const double sums[4] = {warp_sum(yz), warp_sum(grad), warp_sum(feas), warp_sum(comp)};
   if (lane == 0)
     for (int q = 0; q < 4; ++q) atomicAdd(&blk[kR * kR + q], sums[q]);
@@ -418,8 +469,11 @@ int admm_full_run(const float* A, int64_t m, int64_t n, int64_t lda, int r, doub
   a.yct = yct;
   a.trace = trace;
   a.scores = scores;
-  const unsigned gl = (unsigned)std::max<int64_t>(1, std::min<int64_t>(2 * kNumSMs, ceil_div(m, 8)));
-  const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(2 * kNumSMs, ceil_div(n, 8)));
+  // one block per SM (210 registers per thread: one resident block), each
+  // warp >= 4 rows (one batch of kB loads); every block adds one r x r Gram
+  // partial to the same r^2 global words
+  const unsigned gl = (unsigned)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, ceil_div(m, 32)));
+  const unsigned gr = (unsigned)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, ceil_div(n, 32)));
   if (!resume) {
     full_init_ctrl<<<1, 1, 0, st>>>(a.ctrl);
     CNMF_LAUNCH_CHECK();
@@ -433,33 +487,75 @@ int admm_full_run(const float* A, int64_t m, int64_t n, int64_t lda, int r, doub
     CNMF_LAUNCH_CHECK();
   }
   FullCtrl hc;
-  CNMF_CUDA(cudaMemcpyAsync(&hc, a.ctrl, sizeof(FullCtrl), cudaMemcpyDeviceToHost, st));
-  CNMF_CUDA(cudaStreamSynchronize(st));
-  int k = hc.k;
-  int steps = 0;
-  while (!hc.done) {
-    // Y = A yc^T; the previous iteration's score; then iteration k (unless stopped)
-    CNMF_TRY(pass_forward(A, m, n, lda, a.Pyc, S, a.Y, st));
-    if (k > 0) {
-      full_kkt<<<gl, kThreads, 0, st>>>(a);
+  auto sync_ctrl = [&]() -> int {
+    CNMF_CUDA(cudaMemcpyAsync(&hc, a.ctrl, sizeof(FullCtrl), cudaMemcpyDeviceToHost, st));
+    CNMF_CUDA(cudaStreamSynchronize(st));
+    return CNMF_OK;
+  };
+  // one iteration on stream s: Y = A yc^T, the previous iteration's score,
+  // then the updates (which return at once after a stop)
+  auto iteration = [&](cudaStream_t s, bool score) -> int {
+    CNMF_TRY(pass_forward(A, m, n, lda, a.Pyc, S, a.Y, s));
+    if (score) {
+      full_kkt<<<gl, kThreads, 0, s>>>(a);
       CNMF_LAUNCH_CHECK();
     }
-    if (k >= max_iter) {  // only the last score was still owed
-      CNMF_CUDA(cudaMemcpyAsync(&hc, a.ctrl, sizeof(FullCtrl), cudaMemcpyDeviceToHost, st));
-      CNMF_CUDA(cudaStreamSynchronize(st));
+    full_left<<<gl, kThreads, 0, s>>>(a);
+    CNMF_LAUNCH_CHECK();
+    CNMF_TRY(pass_transpose(A, m, n, lda, a.Pxc, S, a.Z, s));
+    full_right<<<gr, kThreads, 0, s>>>(a, 0);
+    CNMF_LAUNCH_CHECK();
+    return CNMF_OK;
+  };
+  CNMF_TRY(sync_ctrl());
+  int k = hc.k;
+  int steps = 0;
+  // a run to completion replays 8 iterations per CUDA graph launch (the
+  // kernels read the iteration index from the control block), checking the
+  // stop flag between launches
+  constexpr int kChunk = 8;
+  if (step_limit == 0 && !hc.done && k == 0 && max_iter > 2 * kChunk) {  // the first iteration has no score
+    CNMF_TRY(iteration(st, false));
+    ++k;
+  }
+  if (step_limit == 0 && !hc.done && k > 0 && max_iter - k >= 2 * kChunk) {
+    cudaStream_t cs;
+    CNMF_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CNMF_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    int rc = CNMF_OK;
+    for (int g = 0; g < kChunk && rc == CNMF_OK; ++g) rc = iteration(cs, true);
+    const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+    if (rc == CNMF_OK && ce == cudaSuccess) {
+      CNMF_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      while (!hc.done && max_iter - k >= kChunk) {
+        CNMF_CUDA(cudaGraphLaunch(exec, st));
+        k += kChunk;
+        CNMF_TRY(sync_ctrl());
+      }
+      cudaGraphExecDestroy(exec);
+    }
+    if (graph) cudaGraphDestroy(graph);
+    cudaStreamDestroy(cs);
+    CNMF_TRY(rc);
+    if (ce != cudaSuccess) return fail(CNMF_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    if (!hc.done) k = hc.k;
+  }
+  while (!hc.done) {
+    if (k >= max_iter) {  // only the last score is still owed
+      CNMF_TRY(pass_forward(A, m, n, lda, a.Pyc, S, a.Y, st));
+      full_kkt<<<gl, kThreads, 0, st>>>(a);
+      CNMF_LAUNCH_CHECK();
+      CNMF_TRY(sync_ctrl());
       break;
     }
-    full_left<<<gl, kThreads, 0, st>>>(a);
-    CNMF_LAUNCH_CHECK();
-    CNMF_TRY(pass_transpose(A, m, n, lda, a.Pxc, S, a.Z, st));
-    full_right<<<gr, kThreads, 0, st>>>(a, 0);
-    CNMF_LAUNCH_CHECK();
+    CNMF_TRY(iteration(st, k > 0));
     ++k;
     ++steps;
     const bool pause = step_limit > 0 && steps >= step_limit;
     if (pause || (k & 7) == 0) {
-      CNMF_CUDA(cudaMemcpyAsync(&hc, a.ctrl, sizeof(FullCtrl), cudaMemcpyDeviceToHost, st));
-      CNMF_CUDA(cudaStreamSynchronize(st));
+      CNMF_TRY(sync_ctrl());
       k = hc.done ? k : hc.k;
       if (pause) break;
     }
