@@ -1,26 +1,39 @@
-"""Benchmark: compressed NMF on BASELINE.json configs[1] (dense NMF, fp32,
-m=10000, n=5000, r=20, two-sided compression with oversampling 10 and q=4,
-then compressed ADMM for 500 iterations).
+"""Benchmark: the compressed-NMF hot path on BASELINE.json's configurations.
 
-One "step" = the whole compressed-NMF job on device-resident A: both range
-finders (2 x 9 streaming passes), the core L^T A R^T (one more pass), the
-ADMM iterations and the final relative error (one more pass).
+Default workload (N = 1 headline): configs[4], the largest configuration that
+fits one B200 -- dense classical NMF, fp32, m = 200,000, n = 100,000, r = 50
+(A = 80 GB), two-sided compression with oversampling 10 and q = 4, then 200
+compressed-ADMM iterations. `--config K` selects another BASELINE.json
+configuration (0..3); those runs are the per-config throughput table in
+DESIGN.md, not the driver's headline.
 
-  value  = compression GB/s of A per pass: 19 passes x |A| / device time of
-           the compression phase (BASELINE.json metric, first half);
-  nmf_iters_per_s = ADMM iterations / device time of the ADMM phase (second
-           half of the metric);
-  e2e    = the same per-pass GB/s through the public API with host buffers:
-           nmf_admm(pinned host A) -> host factors; 20 passes x |A| / wall
-           time of the call (H2D of A, D2H of X, Y inside the timed region).
+One "step" = the whole job on device-resident A:
+  NMF  (configs 1, 4): both range finders (2 x (2q+1) passes), the core
+       L^T A R^T (one more pass), the ADMM iterations, the final relative error
+       (one more pass);
+  SNMF (configs 0, 2, 3): the range finder (2q+1 passes), Q^T A (one pass),
+       SPA / XRAY selection, the NNLS right factor and both relative errors
+       (one more pass).
 
-`--impl reference` times the CPU oracle port of the reference (numpy, all
-host threads) on the same workload and reports the e2e-style number.
-Multi-GPU (torchrun, N>1): A is sharded by columns (weak scaling: every
-rank holds an m x 5000 shard of an m x 5000N matrix); the passes all-reduce
-their m x S products over NCCL, CholeskyQR of row-sharded panels all-reduces
-the S x S Gram matrix, the ADMM runs replicated on the compressed problem
-(paper_1505_04650_b200/distributed.py); the time is the max over ranks.
+  value  = compression GB/s of A per pass: compression passes x |A| / device
+           time of the compression phase (BASELINE.json metric, first half);
+  nmf_iters_per_s = ADMM iterations / device time of the ADMM phase;
+  e2e    = the whole job through the public API (nmf_admm / snmf) on a pinned
+           HOST matrix, in the same unit: all passes of the job x |A| / wall
+           time of the call, the H2D copy of A and the D2H of the factors
+           inside the timed region.
+|A| counts 4 bytes per element (A is fp32 in HBM).
+
+`--impl reference` times the reference's CPU path (the numpy oracle port,
+all host threads) on a bounded row sample of the same configuration: value =
+its compression phase, e2e = its whole job, both in the same unit.
+
+Multi-GPU (torchrun, N > 1): strong scaling -- one A of the configuration,
+column-sharded (rank i owns a contiguous column block); Sum A_i Omega_i and
+Sum A_i (A_i^T Q) are NCCL all-reduces of m x S panels, Q^T A_i stays local,
+the ADMM updates U replicated and V^T by column shard (s x r all-reduces),
+SPA / XRAY picks are all-reduces of (score, index) pairs
+(paper_1505_04650_b200/distributed.py); every time is the max over ranks.
 """
 
 import argparse
@@ -33,11 +46,31 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-M, N, R, R_OV, W, MAX_ITER, TOL, SEED = 10000, 5000, 20, 10, 4, 500, 1e-4, 5
-PASSES_COMPRESS = 2 * (2 * W + 1) + 1   # two range finders + the core projection
-PASSES_CALL = PASSES_COMPRESS + 1       # + relative-error pass
-WORKLOAD = ("configs[1]: dense NMF fp32 m=10000 n=5000 r=20, X,Y~U[0,1], A=max(XY+N(0,0.01^2),0); "
-            "two-sided compression r_ov=10 q=4; compressed ADMM 500 iterations")
+METRIC = "compression GB/s of A per pass (% HBM roofline); compressed-NMF iters/sec"
+R_OV = 10
+SEED = 5
+
+# BASELINE.json configs: kind, shape, rank, power passes, generator
+CONFIGS = {
+    0: dict(kind="snmf", m=500, n=2000, r=10, q=4, sel="spa", alpha=1.0, sigma=0.01,
+            text="configs[0]: near-separable SNMF m=500 n=2000 r=10, W~|N(0,1)|, H=[I|Dirichlet(1)] permuted, "
+                 "noise N(0,0.01^2) clipped; compression r_ov=10 q=4; compressed SPA"),
+    1: dict(kind="nmf", m=10000, n=5000, r=20, q=4, iters=500, sparse=0.0, sigma=0.01,
+            text="configs[1]: dense NMF fp32 m=10000 n=5000 r=20, X,Y~U[0,1], A=max(XY+N(0,0.01^2),0); "
+                 "two-sided compression r_ov=10 q=4; compressed ADMM 500 iterations"),
+    2: dict(kind="snmf", m=2_000_000, n=200, r=20, q=2, sel="spa", alpha=0.5, sigma=0.005,
+            text="configs[2]: tall near-separable SNMF fp32 m=2000000 n=200 r=20, H=[I|Dirichlet(0.5)] permuted, "
+                 "noise N(0,0.005^2) clipped; compression r_ov=10 q=2; compressed SPA"),
+    3: dict(kind="snmf", m=100_000, n=200_000, r=50, q=4, sel="xray", alpha=1.0, sigma=0.01,
+            text="configs[3]: general-shape near-separable SNMF fp32 m=100000 n=200000 r=50, H=[I|Dirichlet(1)] "
+                 "permuted, noise N(0,0.01^2) clipped; compression r_ov=10 q=4; compressed XRAY"),
+    4: dict(kind="nmf", m=200_000, n=100_000, r=50, q=4, iters=200, sparse=0.7, sigma=0.01,
+            text="configs[4]: classical NMF fp32 m=200000 n=100000 r=50, X~U[0,1], Y 70% zeros else U[0,1], "
+                 "A=max(XY+N(0,0.01^2),0); two-sided compression r_ov=10 q=4; compressed ADMM 200 iterations"),
+}
+# the reference arm's bounded sample: rows (and columns) of the same generator
+SAMPLE = {0: (500, 2000), 1: (10000, 5000), 2: (200_000, 200), 3: (2000, 20_000), 4: (2000, 100_000)}
+TOL = 1e-4
 
 
 def parse():
@@ -46,7 +79,9 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
 
 
@@ -57,69 +92,172 @@ def dist_env():
     return ws, rank, local
 
 
-def config_block(extra=None):
-    c = {"workload": WORKLOAD, "m": M, "n": N, "r": R, "oversample": R_OV, "q": W, "admm_iters": MAX_ITER,
-         "passes_compress": PASSES_COMPRESS, "l2": "inputs larger than L2 (A = 200 MB fp32 > 126 MB)",
-         "parallelism": "A column-sharded across GPUs, m x 5000 per GPU (weak scaling)"}
+def passes(c):
+    """Streaming passes over A: compression phase, whole job."""
+    if c["kind"] == "nmf":
+        comp = 2 * (2 * c["q"] + 1) + 1  # two range finders + the core projection
+        return comp, comp + 1            # + the relative-error pass
+    comp = 2 * c["q"] + 1                # one range finder
+    return comp, comp + 2                # + Q^T A + the full-space error pass
+
+
+def config_block(cid, ws, extra=None):
+    c = CONFIGS[cid]
+    out = {"workload": c["text"], "config_index": cid, "m": c["m"], "n": c["n"], "r": c["r"], "oversample": R_OV,
+           "q": c["q"], "passes_compress": passes(c)[0], "passes_job": passes(c)[1],
+           "l2": ("inputs larger than L2 (A = %.1f GB fp32 > 126 MB)" % (4e-9 * c["m"] * c["n"])
+                  if 4 * c["m"] * c["n"] > 126e6 else "A fits in L2: consecutive passes hit L2"),
+           "parallelism": f"A column-sharded over {ws} GPU(s) (strong scaling)" if ws > 1 else "single GPU"}
+    if c["kind"] == "nmf":
+        out["admm_iters"] = c["iters"]
+    else:
+        out["selector"] = c["sel"]
     if extra:
-        c.update(extra)
-    return c
-
-
-# --------------------------------------------------------------- oracle ----
-
-def oracle_job(a):
-    """The reference's CPU path (oracle port) for the same job."""
-    from oracle import cnmf_oracle as O
-
-    out = O.admm(a, R, compressed=True, cfg=O.Config(R, R_OV, W, SEED), max_iter=MAX_ITER, tol=TOL)
+        out.update(extra)
     return out
 
 
-def synth_host(seed=0):
+# ------------------------------------------------------------- synthetic data ----
+
+def numpy_sample(cid, rows, cols, seed=0):
+    """A seeded row/column sample of configuration cid's generator (fp64)."""
     import numpy as np
 
+    c = CONFIGS[cid]
     g = np.random.default_rng(seed)
-    x = g.uniform(size=(M, R)).astype(np.float32)
-    y = g.uniform(size=(R, N)).astype(np.float32)
-    a = x @ y + 0.01 * g.standard_normal((M, N), dtype=np.float32)
+    r = c["r"]
+    if c["kind"] == "nmf":
+        x = g.uniform(size=(rows, r))
+        y = g.uniform(size=(r, cols))
+        if c["sparse"]:
+            y *= g.uniform(size=(r, cols)) >= c["sparse"]
+        a = x @ y
+    else:
+        w = np.abs(g.standard_normal((rows, r)))
+        h = np.zeros((r, cols))
+        h[:, :r] = np.eye(r)
+        h[:, r:] = g.dirichlet(np.full(r, c["alpha"]), size=cols - r).T
+        a = w @ h[:, g.permutation(cols)]
+    a += c["sigma"] * g.standard_normal(a.shape)
     return np.maximum(a, 0.0, out=a)
+
+
+def device_data(cid, c0, ncols, rank):
+    """This rank's column block [c0, c0 + ncols) of configuration cid, generated
+    on the device (the factors are drawn for the whole matrix from a shared
+    seed, so the blocks of all ranks form one A; the noise is per rank)."""
+    import torch
+
+    c = CONFIGS[cid]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device=dev).manual_seed(1000 + cid)
+    m, n, r = c["m"], c["n"], c["r"]
+    if c["kind"] == "nmf":
+        x = torch.rand(m, r, device=dev, generator=g)
+        y = torch.rand(r, n, device=dev, generator=g)
+        if c["sparse"]:
+            y.mul_((torch.rand(r, n, device=dev, generator=g) >= c["sparse"]).float())
+        a = x @ y[:, c0:c0 + ncols].contiguous()
+        truth = None
+    else:
+        w = torch.randn(m, r, device=dev, generator=g).abs_()
+        conc = torch.full((r,), float(c["alpha"]), device=dev)
+        torch.manual_seed(2000 + cid)
+        d = torch.distributions.Dirichlet(conc).sample((n - r,)).t()
+        h = torch.cat([torch.eye(r, device=dev), d], 1)
+        perm = torch.randperm(n, device=dev, generator=g)
+        h = h[:, perm]
+        truth = sorted(torch.argsort(perm)[:r].tolist())
+        a = w @ h[:, c0:c0 + ncols].contiguous()
+        del w, h, d
+    gn = torch.Generator(device=dev).manual_seed(3000 + 17 * rank + cid)
+    rows = max(1, (1 << 29) // max(1, ncols))  # ~2 GB noise chunks
+    for i in range(0, m, rows):
+        blk = a[i:i + rows]
+        blk.add_(torch.randn(blk.shape, device=dev, generator=gn), alpha=c["sigma"]).clamp_(min=0.0)
+    return a, truth
+
+
+# ------------------------------------------------------------------ oracle ----
+
+def oracle_job(cid, a, timings):
+    """The reference's CPU path (oracle port) for the whole job on `a`; fills
+    timings['compress_s'] with the compression phase."""
+    from oracle import cnmf_oracle as O
+
+    c = CONFIGS[cid]
+    cfg = O.adjust(O.Config(c["r"], R_OV, c["q"], SEED), *a.shape)
+    if c["kind"] == "nmf":
+        t0 = time.perf_counter()
+        left, right = O.compressed_bases(a, cfg)
+        core = (left.T @ a) @ right.T
+        timings["compress_s"] = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        u, v, it, _, _ = O.admm_compressed(core, left, right, a.shape[0], a.shape[1], c["r"], cfg,
+                                           max_iter=c["iters"], tol=TOL)
+        timings["admm_s"] = time.perf_counter() - t1
+        timings["iters"] = it
+        O.rel_error(a, u, v)
+        return
+    t0 = time.perf_counter()
+    q = O.range_basis(a, cfg)
+    timings["compress_s"] = time.perf_counter() - t0
+    O.snmf(a, c["r"], selector=c["sel"], cfg=cfg, basis=q)
+
+
+def cpu_sample(cid):
+    import numpy as np
+
+    rows, cols = SAMPLE[cid]
+    return numpy_sample(cid, rows, cols).astype(np.float64)
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    import numpy as np
-
-    a = synth_host().astype(np.float64)
-    for _ in range(max(args.warmup, 1) if args.warmup else 0):
-        oracle_job(a)
-    ts = []
+    c = CONFIGS[args.config]
+    a = cpu_sample(args.config)
+    rows, cols = a.shape
+    pc, pj = passes(c)
+    abytes = 4.0 * rows * cols
+    for _ in range(args.warmup):
+        oracle_job(args.config, a, {})
+    ts, tc, ti = [], [], []
     for _ in range(args.steps):
+        tm = {}
         t0 = time.perf_counter()
-        oracle_job(a)
+        oracle_job(args.config, a, tm)
         ts.append(time.perf_counter() - t0)
-    t = sum(ts) / len(ts)
-    gbs = PASSES_CALL * M * N * 4 / t / 1e9
+        tc.append(tm["compress_s"])
+        if "admm_s" in tm:
+            ti.append(tm["iters"] / tm["admm_s"])
+    t, tcomp = sum(ts) / len(ts), sum(tc) / len(tc)
+    value = pc * abytes / tcomp / 1e9
+    e2e = pj * abytes / t / 1e9
     cores = os.cpu_count()
-    line = {"metric": "compression GB/s of A per pass (% HBM roofline); compressed-NMF iters/sec",
-            "value": gbs, "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": config_block({"reference_impl": "oracle port (numpy) of the reference cnmf package"}),
-            "nmf_iters_per_s": MAX_ITER / t,
-            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
-                             "sample": f"full configs[1] job, {args.steps} steps"},
-            "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    sample = (f"rows {rows} x cols {cols} of the configs[{args.config}] generator (full size "
+              f"{c['m']} x {c['n']}), fp64 numpy, whole job per step")
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": config_block(args.config, ws, {"reference_impl": "oracle port (numpy) of the reference cnmf "
+                                                                       "package, all host threads",
+                                                     "sample_rows": rows, "sample_cols": cols}),
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample,
+                             "whole_job_gbs": e2e},
+            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if ti:
+        line["nmf_iters_per_s"] = sum(ti) / len(ti)
     print(json.dumps(line), flush=True)
 
 
-# ----------------------------------------------------------------- ours ----
+# -------------------------------------------------------------------- ours ----
 
 class Clocks:
     """SM clock and throttle reasons sampled every 5 ms during the timed
-    region (NVML in a background thread; nvidia-smi as the fallback)."""
+    region (NVML in a background thread)."""
 
     def __init__(self, index):
         import threading
@@ -166,83 +304,90 @@ class Clocks:
                 "samples": len(self.sm), "source": "NVML every 5 ms during the timed steps"}
 
 
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    return 6650.0, "fallback 6650 GB/s (B200_PROFILING.md)"
+
+
 def run_ours(args):
     import ctypes
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_1505_04650_b200 as C
     from paper_1505_04650_b200 import _lib
-    from paper_1505_04650_b200.device import DeviceMatrix, stream, zeros
+    from paper_1505_04650_b200 import distributed as D
+    from paper_1505_04650_b200.compress import _compress
+    from paper_1505_04650_b200.device import DeviceMatrix
     from paper_1505_04650_b200.nmf import compressed_problem
-    from paper_1505_04650_b200.rng import Rng
+    import paper_1505_04650_b200.nmf as nmf_mod
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _lib.load()
-
-    from paper_1505_04650_b200 import distributed as D
-
-    # synthetic configs[1] data, generated on the device: X shared by all
-    # ranks, this rank's column block Y_i and noise (global A = X [Y_0 .. Y_k])
-    gx = torch.Generator(device="cuda").manual_seed(1234)
-    g = torch.Generator(device="cuda").manual_seed(4321 + rank)
-    x = torch.rand(M, R, device="cuda", generator=gx)
-    y = torch.rand(R, N, device="cuda", generator=g)
-    a = torch.addmm(0.01 * torch.randn(M, N, device="cuda", generator=g), x, y).clamp_(min=0.0)
-    del x, y
+    cid = args.config
+    c = CONFIGS[cid]
+    m, n, r = c["m"], c["n"], c["r"]
+    c0, ncols = D.column_shard(n, ws, rank)
+    a, truth = device_data(cid, c0, ncols, rank)
+    torch.cuda.synchronize()
     A = DeviceMatrix(a)
-    n_glob, c0 = N * ws, N * rank
-    cfg = C.adjust_config(C.CompressionConfig(r=R, r_ov=R_OV, w=W, seed=SEED), M, n_glob)
+    cfg = C.adjust_config(C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED), m, n)
     comm, ops = D.Comm(), (D.DeviceOps() if ws > 1 else None)
-    counts = [N] * ws
-    s = cfg.basis_cols
     st = torch.cuda.current_stream()
-    sp = stream()
+    pc, pj = passes(c)
+    abytes = 4.0 * m * n  # the whole matrix (all shards)
+    info = {}
 
-    # buffers for the ADMM phase
-    rng = Rng(cfg.seed)
-    u0 = rng.child("init-left").uniform((M, R))
-    vt0 = rng.child("init-right").uniform((R, n_glob), transpose=True)
-    u, vt = u0.clone(), vt0.clone()
-    du = zeros((M, R), torch.float64)
-    dvt = zeros((n_glob, R), torch.float64)
-    xc = zeros((s, R), torch.float64)
-    yc = zeros((R, s), torch.float64)
-    trace = zeros((MAX_ITER,), torch.float64)
-    scores = zeros((MAX_ITER,), torch.float64)
-    nbytes = lib.cnmf_admm_workspace(M, n_glob, s, R)
-    wsb = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-    it = ctypes.c_int(0)
-    done = ctypes.c_int(0)
-    res = zeros((2,), torch.float64)
+    if c["kind"] == "nmf":
+        def compress():
+            if ws == 1:
+                return compressed_problem(A, cfg)
+            return D.compressed_problem(ops, comm, A, m, n, c0, cfg)
 
-    def step(ev):
-        ev[0].record(st)
-        if ws == 1:
-            left, right, core = compressed_problem(A, cfg)
-            lp, rp = left.panel, right.panel
-        else:
-            lp, right_local, core = D.compressed_problem(ops, comm, A, M, n_glob, c0, cfg)
-            rp = comm.allgather_rows(right_local, counts)
-        ev[1].record(st)
-        u.copy_(u0)
-        vt.copy_(vt0)
-        _lib.call("cnmf_admm_run", core.data_ptr(), lp.data_ptr(), M, rp.data_ptr(), n_glob, s, R,
-                  u.data_ptr(), du.data_ptr(), vt.data_ptr(), dvt.data_ptr(), xc.data_ptr(), yc.data_ptr(), 1.0, 1.0,
-                  1.0, MAX_ITER, TOL, trace.data_ptr(), scores.data_ptr(), ctypes.byref(it), ctypes.byref(done), 0,
-                  0, wsb.data_ptr(), nbytes, sp)
-        ev[2].record(st)
-        vloc = vt if ws == 1 else vt[c0: c0 + N].contiguous()
-        _lib.call("cnmf_residual_norms", A.ptr, M, N, A.lda, u.data_ptr(), None, vloc.data_ptr(), R,
-                  res.data_ptr(), sp)
-        comm.allreduce(res)
-        ev[3].record(st)
-        return it.value
+        def step(ev):
+            ev[0].record(st)
+            prob = compress()
+            ev[1].record(st)
+            if ws == 1:
+                left, right, core = prob
+                u, vt, it, _ = nmf_mod.run_admm(core, left.panel, m, right.panel, n, cfg, r, max_iter=c["iters"],
+                                                tol=TOL)
+                ev[2].record(st)
+                nmf_mod._rel_error(A, u, vt)
+            else:
+                left, right_local, core = prob
+                u, vt, it, _ = D.admm(ops, comm, core, left, m, right_local, n, c0, cfg, r, max_iter=c["iters"],
+                                      tol=TOL)
+                ev[2].record(st)
+                D.rel_error(ops, comm, A, u, vt)
+            ev[3].record(st)
+            return it
+    else:
+        def compress():
+            if ws == 1:
+                return _compress(A, cfg, 0, check=False)
+            return D.range_finder(ops, comm, A, m, n, c0, cfg, 0)
+
+        def step(ev):
+            ev[0].record(st)
+            compress()
+            ev[1].record(st)
+            if ws == 1:
+                res = C.snmf(A, r, selector=c["sel"], cfg=C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED))
+            else:
+                res = D.snmf(ops, comm, A, m, n, c0, r, selector=c["sel"],
+                             cfg=C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED))
+            ev[2].record(st)
+            ev[3].record(st)
+            info["picks"] = [int(k) for k in res.K]
+            return 0
 
     for _ in range(args.warmup):
         step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
@@ -250,8 +395,6 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-
-    import paper_1505_04650_b200.nmf as nmf_mod
 
     clocks = Clocks(local)
     launches0 = lib.cnmf_launch_count() + nmf_mod.graph_launches
@@ -264,14 +407,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     launches = lib.cnmf_launch_count() + nmf_mod.graph_launches - launches0
     ck = clocks.stop()
+    if ws > 1:
+        dist.barrier()
+
     # the dominant kernel timed live: one more compression, launched eagerly
     # (graph replays bypass the per-launch events), CUDA events around every
     # streaming pass on its launch stream
     lib.cnmf_set_pass_profiling(1)
-    if ws == 1:
+    if c["kind"] == "nmf" and ws == 1:
         compressed_problem(A, cfg, graph=False)
     else:
-        D.compressed_problem(ops, comm, A, M, n_glob, c0, cfg)
+        compress()
     torch.cuda.synchronize()
     pms, pl, pby = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
     lib.cnmf_pass_stats(ctypes.byref(pms), ctypes.byref(pl), ctypes.byref(pby))
@@ -280,95 +426,142 @@ def run_ours(args):
     total_ms = t_start.elapsed_time(t_end)
     comp_ms = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     admm_ms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
-    resid_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
-    t_local = torch.tensor([total_ms, comp_ms, admm_ms], device="cuda", dtype=torch.float64)
+    tail_ms = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
+    t_local = torch.tensor([total_ms, comp_ms, admm_ms, tail_ms], device="cuda", dtype=torch.float64)
     if ws > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
-    total_ms, comp_ms, admm_ms = t_local.tolist()
+    total_ms, comp_ms, admm_ms, tail_ms = t_local.tolist()
     ms_per_step = total_ms / args.steps
-    a_bytes = M * N * 4
-    value = ws * PASSES_COMPRESS * a_bytes / (comp_ms * 1e-3) / 1e9
-    iters_per_s = ws * (sum(iters) / len(iters)) / (admm_ms * 1e-3)
+    value = pc * abytes / (comp_ms * 1e-3) / 1e9
 
-    peaks = {}
-    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(pk_path):
-        peaks = json.load(open(pk_path))
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_peak, peak_src = peaks()
     pass_avg_ms = pms.value / max(pl.value, 1)
     pass_bytes = pby.value / max(pl.value, 1)
     achieved = pass_bytes / (pass_avg_ms * 1e-3) / 1e9
-    sm_clock = (ck.get("sm_mhz") or 1965.0) * 1e6
-    fp32_peak = 148 * 128 * 2 * sm_clock / 1e12  # FFMA peak at the observed SM clock
-    pass_flops = 2.0 * M * N * 32  # padded panel width 32 for s = 30
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak,
-                # dram__bytes_read.sum + dram__bytes_write.sum of one configs[1] pass_tc_pair launch (ncu --set
-                # full, profiles/r01_pass_tc_pair_cfg1_ncu_full.txt): 332.88 MB + 6.72 MB against 403.8 MB
-                # algorithmic -- the second direction's A tiles partly come from L2
-                "traffic": 339.6e6 if (M, N) == (10000, 5000) else None, "traffic_unit": "bytes per paired launch",
+    S = 32 if cfg.basis_cols <= 32 else 64
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": TRAFFIC.get(cid), "traffic_unit": "dram bytes read+written per launch (ncu --set full)",
                 "algorithmic_bytes_per_launch": pass_bytes,
-                "kernel": "pass_tc_pair<32> (both range finders' passes of a power step in one launch) + pass_tc<32> "
-                          "(core projection), tcgen05 3xTF32, CUDA events on the launch stream",
-                "launches": pl.value, "avg_launch_ms": pass_avg_ms,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650",
-                "fp32_tflops": pass_flops / (pass_avg_ms * 1e-3) / 1e12, "fp32_peak_tflops_at_clock": fp32_peak,
-                "fp32_frac": pass_flops / (pass_avg_ms * 1e-3) / 1e12 / fp32_peak}
+                "kernel": f"stream_pass<{S}> (tcgen05 3xTF32, TMA-fed; one or two sides per launch), CUDA events "
+                          "on the launch stream around every pass of one compression",
+                "launches": pl.value, "avg_launch_ms": pass_avg_ms, "peak_source": peak_src,
+                "share_of_step": pms.value / ms_per_step if ms_per_step else None}
+
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+            "precision": "f32 A, 3xTF32 tensor-core passes (fp32-level); fp64 Gram, Cholesky, ADMM, NNLS state",
+            "data": "synthetic (seeded, generated on the device with the configuration's distributions)",
+            "config": config_block(cid, ws, {"n_global": n, "compress_ms": comp_ms, "rest_ms": admm_ms,
+                                             "tail_ms": tail_ms, "hbm_frac_compress": value / ws / hbm_peak}),
+            "roofline": roofline, "clocks": ck, "gpu_launches": int(launches)}
+    if c["kind"] == "nmf":
+        it_avg = sum(iters) / len(iters)
+        line["nmf_iters_per_s"] = it_avg / (admm_ms * 1e-3)
+        line["admm_iterations"] = it_avg
+        line["roofline_admm"] = admm_roofline(m, n, cfg.basis_cols, r, admm_ms / max(it_avg, 1))
+    else:
+        line["picks_true"] = len(set(info.get("picks", [])) & set(truth or [])) if truth else None
 
     # ---- end to end through the public API with host buffers ----
-    a_host = a.cpu().pin_memory()
-    cfg_pub = C.CompressionConfig(r=R, r_ov=R_OV, w=W, seed=SEED)
+    host = None
+    if not args.no_e2e:
+        # pinned host copy of this rank's block (chunked D2H; allocation untimed)
+        host = torch.empty((m, ncols), dtype=torch.float32, pin_memory=True)
+        step_rows = max(1, (1 << 28) // ncols)
+        for i in range(0, m, step_rows):
+            host[i:i + step_rows].copy_(a[i:i + step_rows])
+        torch.cuda.synchronize()
+    # the device copy the benchmark used is released: the public call allocates its own
+    del A, a
+    nmf_mod._GRAPHS.clear()
+    torch.cuda.empty_cache()
+    line["e2e"] = e2e_run(args, cid, host, c0, ncols, comm, ops, pj, abytes) if host is not None else None
+    del host
 
-    def public_call():
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        sa = cpu_sample(cid)
+        tm = {}
+        t0 = time.perf_counter()
+        oracle_job(cid, sa, tm)
+        tj = time.perf_counter() - t0
+        sb = 4.0 * sa.shape[0] * sa.shape[1]
+        cpu = {"value": pc * sb / tm["compress_s"] / 1e9, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"rows {sa.shape[0]} x cols {sa.shape[1]} of the configs[{cid}] generator, fp64 numpy "
+                         "oracle port, one whole job (value = its compression phase)",
+               "whole_job_gbs": pj * sb / tj / 1e9, "seconds": tj}
+    line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+# dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+# kernel at the configuration's size (ncu --set full; profiles/)
+TRAFFIC = {}
+
+
+def admm_roofline(m, n, s, r, ms_per_iter):
+    """The ADMM iteration against the fp64 pipe: per iteration the row updates
+    form P z (2 (m+n) s r flops) and the reduced sums P^T x, P^T dx
+    (4 (m+n) s r), and stream U, dU, V^T, dV^T (read + write, fp64) plus the
+    fp32 bases."""
+    flops = 6.0 * (m + n) * s * r
+    bytes_ = 32.0 * (m + n) * r + 4.0 * (m + n) * (32 if s <= 32 else 64)
+    fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12  # 64 fp64 FMA / SM / cycle at 1965 MHz (nominal)
+    t = ms_per_iter * 1e-3
+    return {"bound": "fp64", "achieved": flops / t / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
+            "frac": flops / t / 1e12 / fp64_peak, "bytes_per_iter": bytes_, "hbm_gbs": bytes_ / t / 1e9,
+            "ms_per_iter": ms_per_iter, "peak_source": "nominal fp64 rate (no measured fp64 peak in MEASURED_PEAKS)"}
+
+
+def e2e_run(args, cid, host, c0, ncols, comm, ops, pj, abytes):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1505_04650_b200 as C
+    from paper_1505_04650_b200 import distributed as D
+    from paper_1505_04650_b200.device import DeviceMatrix
+
+    ws, rank, _ = dist_env()
+    c = CONFIGS[cid]
+    m, n, r = c["m"], c["n"], c["r"]
+    pub = C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED)
+
+    def call():
+        if c["kind"] == "nmf":
+            if ws == 1:
+                fp = C.nmf_admm(host, r, cfg=pub, max_iter=c["iters"], tol=TOL)
+                return fp.X.nbytes + fp.Y.nbytes + 8 * len(fp.objective_trace), fp.rel_error
+            u, vt, it, tr, rel = D.nmf_admm(DeviceMatrix(host), m, n, c0, r, pub, comm, ops, max_iter=c["iters"],
+                                            tol=TOL)
+            uh, vh = u.cpu(), vt.cpu()
+            return uh.numel() * 8 + vh.numel() * 8 + 8 * len(tr), rel
         if ws == 1:
-            fp = C.nmf_admm(a_host, R, cfg=cfg_pub, max_iter=MAX_ITER, tol=TOL)  # numpy out
-            return fp.X.nbytes + fp.Y.nbytes + 8 * len(fp.objective_trace), fp.rel_error, fp.iterations
-        uu, vv, it_, tr_, rel_ = D.nmf_admm(DeviceMatrix(a_host), M, n_glob, c0, R, cfg_pub, comm, ops,
-                                            max_iter=MAX_ITER, tol=TOL)
-        uh, vh = uu.cpu(), vv.cpu()
-        return uh.numel() * 8 + vh.numel() * 8 + 8 * len(tr_), rel_, it_
+            res = C.snmf(host, r, selector=c["sel"], cfg=pub)
+        else:
+            res = D.snmf(ops, comm, DeviceMatrix(host), m, n, c0, r, selector=c["sel"], cfg=pub, host_out=True)
+        return res.Y.nbytes + res.K.nbytes, res.rel_error_full
 
-    public_call()  # warm
+    call()  # warm
     torch.cuda.synchronize()
     ts = []
     for _ in range(max(1, min(args.steps, 3))):
         if ws > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        d2h, rel_e2e, it_e2e = public_call()
+        d2h, rel = call()
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
     te_t = torch.tensor([sum(ts) / len(ts)], device="cuda", dtype=torch.float64)
     if ws > 1:
         dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
     te = te_t.item()
-    e2e = {"value": ws * PASSES_CALL * a_bytes / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": a_bytes,
-           "d2h_bytes_per_step": int(d2h), "ms": te * 1e3, "rel_error": rel_e2e, "iterations": it_e2e}
-
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        a64 = a.cpu().double().numpy()
-        t0 = time.perf_counter()
-        oracle_job(a64)
-        tc = time.perf_counter() - t0
-        cpu = {"value": PASSES_CALL * a_bytes / tc / 1e9, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": "one full configs[1] job (compression + 500 ADMM iterations + error) on the oracle port",
-               "seconds": tc}
-
-    if rank == 0:
-        line = {"metric": "compression GB/s of A per pass (% HBM roofline); compressed-NMF iters/sec",
-                "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f32", "precision": "f32 passes over A; f64 Gram, Cholesky and ADMM state", "data": "synthetic",
-                "config": config_block({"n_global": n_glob, "compress_ms": comp_ms, "admm_ms": admm_ms,
-                                        "resid_ms": resid_ms,
-                                        "hbm_frac_compress": value / ws / hbm_peak}),
-                "nmf_iters_per_s": iters_per_s, "admm_iterations": iters[0],
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
-                "gpu_launches": int(launches)}
-        print(json.dumps(line), flush=True)
-    if ws > 1:
-        dist.destroy_process_group()
+    return {"value": pj * abytes / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(4 * m * ncols),
+            "d2h_bytes_per_step": int(d2h), "ms": te * 1e3, "rel_error": rel, "steps": len(ts),
+            "what": "public nmf_admm / snmf on a pinned host matrix; all passes of the job x |A| / wall time"}
 
 
 def main():

@@ -11,7 +11,7 @@ import os
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcnmf_b200.so")
+LIB_PATH = os.environ.get("CNMF_LIB_PATH") or os.path.join(_HERE, "libcnmf_b200.so")  # override: A/B tools only
 
 c_i64 = ctypes.c_int64
 c_int = ctypes.c_int

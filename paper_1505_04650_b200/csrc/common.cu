@@ -3,6 +3,7 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -81,6 +82,79 @@ void keep_pool() {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   done[dev] = true;
+}
+
+namespace {
+std::mutex g_dev_mu;
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  return dev;
+}
+}  // namespace
+
+int device_sms() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = kNumSMs;
+  cache[dev] = sms;
+  return sms;
+}
+
+int ensure_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(dev, fn);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return CNMF_OK;
+  CNMF_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done[key] = bytes;
+  return CNMF_OK;
+}
+
+int device_scratch(const char* tag, size_t bytes, void** out, cudaStream_t st) {
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  static std::map<std::pair<int, std::string>, Buf> bufs;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  Buf& b = bufs[std::make_pair(dev, std::string(tag))];
+  if (b.cap < bytes) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CNMF_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(CNMF_ERR_CUDA, std::string("library scratch '") + tag +
+                                     "' must be allocated by an eager call before graph capture");
+    CNMF_CUDA(cudaDeviceSynchronize());  // the old buffer may still be in use
+    if (b.p) CNMF_CUDA(cudaFree(b.p));
+    b.p = nullptr;
+    b.cap = 0;
+    CNMF_CUDA(cudaMalloc(&b.p, bytes));
+    CNMF_CUDA(cudaMemset(b.p, 0, bytes));
+    b.cap = bytes;
+  }
+  *out = b.p;
+  return CNMF_OK;
+}
+
+unsigned device_ticket(const char* tag) {
+  static std::map<std::pair<int, std::string>, std::atomic<unsigned>> counters;
+  const int dev = current_device();
+  std::atomic<unsigned>* c;
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    c = &counters[std::make_pair(dev, std::string(tag))];
+  }
+  return c->fetch_add(1u);
 }
 
 uint64_t fnv1a64(const char* s) {

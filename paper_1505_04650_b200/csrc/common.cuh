@@ -46,7 +46,21 @@ void pass_record(cudaEvent_t start, cudaEvent_t stop, double bytes);
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
 
-constexpr int kNumSMs = 148;
+constexpr int kNumSMs = 148;  // B200; launch sites size grids with device_sms()
+
+// ---------------------------------------------------------------------------
+// per-device library state (thread-safe; every entry is keyed by the current
+// device, so a process driving several GPUs gets one of each per GPU)
+// ---------------------------------------------------------------------------
+// SM count of the current device (cudaDevAttrMultiProcessorCount, cached)
+int device_sms();
+// cudaFuncAttributeMaxDynamicSharedMemorySize = bytes, once per (device, fn)
+int ensure_smem_attr(const void* fn, int bytes);
+// a library-owned device buffer, one per (device, tag), zero-filled when it
+// is (re)allocated; grows on demand, which is refused during graph capture
+int device_scratch(const char* tag, size_t bytes, void** out, cudaStream_t st);
+// next value of a per-(device, tag) counter (lock-free)
+unsigned device_ticket(const char* tag);
 
 
 

@@ -65,6 +65,13 @@ class DeviceMatrix:
         if (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and lda == n
                 and t.data_ptr() % 16 == 0):
             self.t = t
+        elif lda == n:
+            # one device allocation, one copy (a pinned host matrix is copied
+            # asynchronously on the current stream)
+            src = t if t.dtype == torch.float32 else t.to(torch.float32)
+            buf = torch.empty((m, n), dtype=torch.float32, device=dev)
+            buf.copy_(src, non_blocking=src.is_pinned() if not src.is_cuda else True)
+            self.t = buf
         else:
             buf = torch.zeros((m, lda), dtype=torch.float32, device=dev)
             buf[:, :n].copy_(t.to(dev, non_blocking=True))
