@@ -75,6 +75,19 @@ int cnmf_gaussian_fill(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_
                        int64_t ld, void* stream);
 int cnmf_uniform_fill(uint64_t seed, int64_t rows, int64_t cols, double low, double high, int dtype,
                       int transpose, void* out, void* stream);
+/* Stream continuation (rng.py:38-70: successive draws on one Rng continue
+ * numpy's Philox stream). Raw 64-bit draw `start` is the first one used.
+ * cnmf_uniform_fill_at   Rng.uniform from raw position `start` (one raw draw
+ *                        per variate: the next position is start + rows*cols).
+ * cnmf_normal_fill_at    Rng.standard_normal: `count` variates from raw
+ *                        position `start` into out (device, contiguous);
+ *                        *d_end (device int64) receives the raw position after
+ *                        the last variate (the ziggurat consumes a variable
+ *                        number of draws). */
+int cnmf_uniform_fill_at(uint64_t seed, int64_t start, int64_t rows, int64_t cols, double low, double high, int dtype,
+                         int transpose, void* out, void* stream);
+int cnmf_normal_fill_at(uint64_t seed, int64_t start, int64_t count, int dtype, void* out, int64_t* d_end,
+                        void* stream);
 
 /* ---- streaming passes over A (store.py:578 matmul_blocked,
  *      store.py:600 matmul_transposed_blocked) --------------------------------

@@ -34,6 +34,8 @@ SIGNATURES = {
     "cnmf_child_seed": (c_u64, [c_u64, ctypes.c_char_p]),
     "cnmf_gaussian_fill": (c_int, [c_u64, c_i64, c_i64, c_i64, c_int, vp, c_i64, vp]),
     "cnmf_uniform_fill": (c_int, [c_u64, c_i64, c_i64, c_dbl, c_dbl, c_int, c_int, vp, vp]),
+    "cnmf_uniform_fill_at": (c_int, [c_u64, c_i64, c_i64, c_i64, c_dbl, c_dbl, c_int, c_int, vp, vp]),
+    "cnmf_normal_fill_at": (c_int, [c_u64, c_i64, c_i64, c_int, vp, vp, vp]),
     "cnmf_pass_forward": (c_int, [vp, c_i64, c_i64, c_i64, vp, c_int, vp, vp]),
     "cnmf_pass_transpose": (c_int, [vp, c_i64, c_i64, c_i64, vp, c_int, vp, vp]),
     "cnmf_pass_pair": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, vp, vp, c_int, vp]),

@@ -25,7 +25,6 @@ namespace cnmf {
 namespace {
 
 constexpr int kT = 256;   // threads per block
-constexpr int kTR = 32;   // rows per tile
 constexpr int kMaxD = 64; // s, r <= 64
 
 struct SCtrl {
@@ -48,18 +47,25 @@ struct SSide {
 __host__ __device__ inline int sums_len(int s, int r) { return 2 * s * r + 4; }
 
 // ---------------------------------------------------------------------------
-// row sweep: blocks [0, nbl) take left rows, [nbl, grid) right rows
+// row sweep: blocks [0, nbl) take left rows, [nbl, grid) right rows.
+// Register-tiled: per 64-row tile, thread (row group, column group) forms a
+// 4 x 4 block of P z (one float4 of P^T and two double2 of Z per 16 DFMA),
+// updates its 16 (x, dx) pairs, and then thread (c group, column group)
+// accumulates a 4 x 4 block of P^T x and P^T dx over the tile's rows (the
+// block partials). The fp64 FMA pipe is the bound, not shared memory.
 // ---------------------------------------------------------------------------
+constexpr int kRT = 64;  // rows per tile
+
 template <int SP>
-__global__ void __launch_bounds__(kT) row_sweep(SSide L, SSide R, int nbl, const double* __restrict__ Zl,
-                                                 const double* __restrict__ Zr, int s, int r, double step, int update,
-                                                 double* __restrict__ part, const SCtrl* ctrl) {
+__global__ void __launch_bounds__(kT, 2) row_sweep(SSide L, SSide R, int nbl, const double* __restrict__ Zl,
+                                                    const double* __restrict__ Zr, int s, int r, double step,
+                                                    int update, double* __restrict__ part, const SCtrl* ctrl) {
   if (update && ctrl->done) return;
   extern __shared__ __align__(16) unsigned char sm[];
-  double* Z = (double*)sm;                  // SP x kMaxD (rows c, cols k; zero padded)
-  double* Xt = Z + SP * kMaxD;              // kTR x kMaxD
-  double* Dt = Xt + kTR * kMaxD;            // kTR x kMaxD
-  float* Pt = (float*)(Dt + kTR * kMaxD);   // kTR x SP
+  double* Z = (double*)sm;                 // [SP][kMaxD] (rows c, cols k; zero padded)
+  double* Xs = Z + SP * kMaxD;             // [kRT][kMaxD] updated x of the tile
+  double* Ds = Xs + kRT * kMaxD;           // [kRT][kMaxD] updated dx of the tile
+  float* PtT = (float*)(Ds + kRT * kMaxD); // [SP][kRT] the tile's panel rows, transposed
   __shared__ double red[4][kT / 32];
   const bool left = (int)blockIdx.x < nbl;
   const SSide sd = left ? L : R;
@@ -72,73 +78,117 @@ __global__ void __launch_bounds__(kT) row_sweep(SSide L, SSide R, int nbl, const
     const int c = i / kMaxD, k = i % kMaxD;
     Z[i] = (update && c < s && k < r) ? Zs[c * r + k] : 0.0;
   }
-  for (int i = tid; i < 2 * kTR * kMaxD; i += kT) Xt[i] = 0.0;  // padding columns stay zero
-  // lane j of a half-warp owns the columns k = j + 16 q (q < 4): consecutive
-  // lanes touch consecutive doubles in Z, Xt, Dt and in x, dx (no bank
-  // conflicts; a 4-consecutive-column split put 4 lanes on each bank)
-  const int j16 = tid & 15, cg = tid >> 4;  // reduction tile: rows 4 cg .. 4 cg + 3 of P^T
-  const bool red_on = 4 * cg < s;
+  const int g4 = tid >> 4;   // row group (update) / c group (reduction): 4 consecutive
+  const int k4 = tid & 15;   // columns k = k4 + 16 q (consecutive lanes, consecutive doubles)
+  const bool kon = k4 < r;
+  const bool con = 4 * g4 < s;
   double au[16], ad[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) au[q] = ad[q] = 0.0;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  for (int64_t t0 = r0; t0 < r1; t0 += kTR) {
-    const int nr = (int)min64(kTR, r1 - t0);
-    __syncthreads();
-    for (int i = tid; i < kTR * SP; i += kT) {
-      const int row = i / SP, c = i % SP;
-      Pt[i] = (row < nr && c < s) ? sd.P[(t0 + row) * sd.ldp + c] : 0.f;
+  // P rows of the next tile, prefetched into registers during the previous
+  // tile's reduction (float4 i of the tile: row i / (SP / 4))
+  constexpr int PF = kRT * (SP / 4) / kT;
+  float4 pf[PF];
+  auto load_p = [&](int64_t t0n) {
+    const int nrn = (int)min64(kRT, r1 - t0n);
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+      const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
+      pf[j] = (t0n < r1 && row < nrn) ? *(const float4*)(sd.P + (t0n + row) * sd.ldp + c4)
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+  };
+  load_p(r0);
+  for (int64_t t0 = r0; t0 < r1; t0 += kRT) {
+    const int nr = (int)min64(kRT, r1 - t0);
+    __syncthreads();  // previous tile's reduction done with PtT, Xs, Ds
+#pragma unroll
+    for (int j = 0; j < PF; ++j) {
+      const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
+      PtT[(c4 + 0) * kRT + row] = c4 + 0 < s ? pf[j].x : 0.f;
+      PtT[(c4 + 1) * kRT + row] = c4 + 1 < s ? pf[j].y : 0.f;
+      PtT[(c4 + 2) * kRT + row] = c4 + 2 < s ? pf[j].z : 0.f;
+      PtT[(c4 + 3) * kRT + row] = c4 + 3 < s ? pf[j].w : 0.f;
+    }
+    // the tile's old x, dx land in Xs, Ds asynchronously while P z is formed
+    for (int i = tid; i < nr * r; i += kT) {
+      const int row = i / r, k = i - row * r;
+      const double* gx = sd.x + (t0 + row) * r + k;
+      const double* gd = sd.dx + (t0 + row) * r + k;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(Xs + row * kMaxD + k)), "l"(gx)
+                   : "memory");
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(Ds + row * kMaxD + k)), "l"(gd)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     __syncthreads();
-    // ---- update: thread = (row, lane j), columns j + 16 q ----
-#pragma unroll 1
-    for (int row = tid >> 4; row < kTR; row += kT / 16) {
-      double lx[4] = {0.0, 0.0, 0.0, 0.0};
-      if (update && row < nr) {
-#pragma unroll 4
+    // ---- update: rows 4 g4 .. 4 g4 + 3, columns k4 + 16 q ----
+    {
+      double lx[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) lx[a][q] = 0.0;
+      if (update && kon) {
+#pragma unroll 2
         for (int c = 0; c < s; ++c) {
-          const double p = (double)Pt[row * SP + c];
+          const float4 p4 = *(const float4*)(PtT + c * kRT + 4 * g4);
+          const double pv[4] = {p4.x, p4.y, p4.z, p4.w};
+          double zv[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) lx[q] = fma(p, Z[c * kMaxD + j16 + 16 * q], lx[q]);
+          for (int q = 0; q < 4; ++q) zv[q] = Z[c * kMaxD + k4 + 16 * q];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) lx[a][q] = fma(pv[a], zv[q], lx[a][q]);
         }
       }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int k = j16 + 16 * q;
-        double xn = 0.0, dxn = 0.0;
-        if (row < nr && k < r) {
-          const int64_t gi = (t0 + row) * r + k;
-          const double xo = sd.x[gi], dxo = sd.dx[gi];
-          if (update) {
-            xn = fmax(lx[q] + dxo / sd.pen, 0.0);
-            dxn = dxo + step * sd.pen * (lx[q] - xn);
-            sd.x[gi] = xn;
-            sd.dx[gi] = dxn;
-            const double dl = lx[q] - xn, dp = dxn * xn, dpos = fmax(dxn, 0.0), xneg = fmax(-xn, 0.0);
-            s0 += dl * dl;
-            s1 += dp * dp;
-            s2 += dpos * dpos;
-            s3 += xneg * xneg;
-          } else {
-            xn = xo;
-            dxn = dxo;
+      for (int a = 0; a < 4; ++a) {
+        const int row = 4 * g4 + a;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = k4 + 16 * q;
+          double xn = 0.0, dxn = 0.0;
+          if (row < nr && k < r) {
+            const int64_t gi = (t0 + row) * r + k;
+            const double xo = Xs[row * kMaxD + k], dxo = Ds[row * kMaxD + k];
+            if (update) {
+              xn = fmax(lx[a][q] + dxo / sd.pen, 0.0);
+              dxn = dxo + step * sd.pen * (lx[a][q] - xn);
+              sd.x[gi] = xn;
+              sd.dx[gi] = dxn;
+              const double dl = lx[a][q] - xn, dp = dxn * xn, dpos = fmax(dxn, 0.0), xneg = fmax(-xn, 0.0);
+              s0 += dl * dl;
+              s1 += dp * dp;
+              s2 += dpos * dpos;
+              s3 += xneg * xneg;
+            } else {
+              xn = xo;
+              dxn = dxo;
+            }
           }
+          Xs[row * kMaxD + k] = xn;
+          Ds[row * kMaxD + k] = dxn;
         }
-        Xt[row * kMaxD + k] = xn;
-        Dt[row * kMaxD + k] = dxn;
       }
     }
+    load_p(t0 + kRT);  // next tile's P rows: in flight during the reduction
     __syncthreads();
-    // ---- partials P^T x, P^T dx: 4 rows of P^T x 4 strided columns ----
-    if (red_on) {
+    // ---- partials P^T x, P^T dx: c = 4 g4 .. 4 g4 + 3, k = k4 + 16 q ----
+    if (con && kon) {
+#pragma unroll 2
       for (int row = 0; row < nr; ++row) {
-        const float4 p4 = *(const float4*)(Pt + row * SP + 4 * cg);
-        const double pc[4] = {p4.x, p4.y, p4.z, p4.w};
+        const double pc[4] = {PtT[(4 * g4 + 0) * kRT + row], PtT[(4 * g4 + 1) * kRT + row],
+                              PtT[(4 * g4 + 2) * kRT + row], PtT[(4 * g4 + 3) * kRT + row]};
         double xv[4], dv[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          xv[q] = Xt[row * kMaxD + j16 + 16 * q];
-          dv[q] = Dt[row * kMaxD + j16 + 16 * q];
+          xv[q] = Xs[row * kMaxD + k4 + 16 * q];
+          dv[q] = Ds[row * kMaxD + k4 + 16 * q];
         }
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -151,12 +201,12 @@ __global__ void __launch_bounds__(kT) row_sweep(SSide L, SSide R, int nbl, const
     }
   }
   double* out = part + (size_t)blockIdx.x * sums_len(s, r);
-  if (red_on) {
+  if (con && kon) {
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int c = 4 * cg + a, k = j16 + 16 * q;
+        const int c = 4 * g4 + a, k = k4 + 16 * q;
         if (c < s && k < r) {
           out[c * r + k] = au[a * 4 + q];
           out[sr + c * r + k] = ad[a * 4 + q];
@@ -179,6 +229,11 @@ __global__ void __launch_bounds__(kT) row_sweep(SSide L, SSide R, int nbl, const
   }
 }
 
+template <int SP>
+constexpr size_t sweep_smem() {
+  return ((size_t)SP * kMaxD + 2 * kRT * kMaxD) * 8 + (size_t)SP * kRT * 4;
+}
+
 // fixed-order sums of the block partials of each side: sums[side][e]
 __global__ void __launch_bounds__(kT) reduce_parts(const double* __restrict__ part, int nbl, int nbr, int len,
                                                     double* __restrict__ sums, const SCtrl* ctrl, int update) {
@@ -198,123 +253,147 @@ __global__ void __launch_bounds__(kT) reduce_parts(const double* __restrict__ pa
   sums[side * len + e] = acc;
 }
 
-// sum_j a[j * sa] * b[j * sb] with four interleaved partial sums (the
-// single-block core step is bound by the fp64 FMA latency of one long chain)
-__device__ __forceinline__ double dot4(const double* a, int sa, const double* b, int sb, int len) {
-  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-  int j = 0;
-  for (; j + 4 <= len; j += 4) {
-    v0 = fma(a[j * sa], b[j * sb], v0);
-    v1 = fma(a[(j + 1) * sa], b[(j + 1) * sb], v1);
-    v2 = fma(a[(j + 2) * sa], b[(j + 2) * sb], v2);
-    v3 = fma(a[(j + 3) * sa], b[(j + 3) * sb], v3);
+// ---------------------------------------------------------------------------
+// core step: one block of kCT threads; every small product is a register-
+// tiled shared-memory GEMM (2 x 4 outputs per thread, operands broadcast
+// within a warp), the two r x r ridge systems are inverted by Gauss-Jordan
+// ---------------------------------------------------------------------------
+constexpr int kCT = 512;
+
+// C(m, n) = sum_k A[m * am + k * ak] * B[k * bk + n] for m < M, n < N <= 64,
+// M <= 64; out(m, n, value) consumes every result. Thread t owns rows
+// m = t / 16 + 32 p (p < 2) and columns n = t % 16 + 16 q (q < 4): a warp
+// reads 2 distinct A values (broadcast) and 16 consecutive B values per k
+// (conflict-free), with 8 independent FMA chains per thread.
+template <class F>
+__device__ __forceinline__ void small_gemm(int M, int N, int K, const double* A, int am, int ak, const double* B,
+                                           int bk, F out) {
+  static_assert(kCT == 512, "thread mapping covers 64 x 64");
+  const int tm = threadIdx.x >> 4, tn = threadIdx.x & 15;
+  if (tm >= M || tn >= N) return;
+  const int m1 = tm + 32 < M ? tm + 32 : tm;  // clamped reads; results masked below
+  int nn[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) nn[q] = tn + 16 * q < N ? tn + 16 * q : tn;
+  double c[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+#pragma unroll 4
+  for (int k = 0; k < K; ++k) {
+    const double a0 = A[tm * am + k * ak], a1 = A[m1 * am + k * ak];
+    double bv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) bv[q] = B[k * bk + nn[q]];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      c[0][q] = fma(a0, bv[q], c[0][q]);
+      c[1][q] = fma(a1, bv[q], c[1][q]);
+    }
   }
-  for (; j < len; ++j) v0 = fma(a[j * sa], b[j * sb], v0);
-  return (v0 + v1) + (v2 + v3);
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (tm + 32 * p < M && tn + 16 * q < N) out(tm + 32 * p, tn + 16 * q, c[p][q]);
 }
 
-// In-place inverse of an SPD r x r matrix (ld kMaxD + 1) by Gauss-Jordan
-// without pivoting (the ridge term keeps the pivots >= the penalty).
+// In-place inverse of an SPD r x r matrix (ld r) by Gauss-Jordan without
+// pivoting (the ridge term keeps the pivots >= the penalty).
 __device__ void spd_inverse(double* M, double* piv, int r) {
   const int tid = threadIdx.x;
-  constexpr int LD = kMaxD + 1;
   double* colk = piv + kMaxD;
   for (int k = 0; k < r; ++k) {
     __syncthreads();
-    const double inv = 1.0 / M[k * LD + k];
-    for (int j = tid; j < r; j += kT) {
-      piv[j] = M[k * LD + j] * inv;  // scaled pivot row
-      colk[j] = M[j * LD + k];       // column k before this step overwrites it
+    const double inv = 1.0 / M[k * r + k];
+    for (int j = tid; j < r; j += kCT) {
+      piv[j] = M[k * r + j] * inv;  // scaled pivot row
+      colk[j] = M[j * r + k];       // column k before this step overwrites it
     }
     __syncthreads();
-    for (int i = tid; i < r * r; i += kT) {
+    for (int i = tid; i < r * r; i += kCT) {
       const int a = i / r, c = i % r;
       if (a == k) {
-        M[a * LD + c] = (c == k) ? inv : piv[c];
+        M[i] = (c == k) ? inv : piv[c];
       } else {
         const double f = colk[a];
-        M[a * LD + c] = (c == k) ? -f * inv : fma(-f, piv[c], M[a * LD + c]);
+        M[i] = (c == k) ? -f * inv : fma(-f, piv[c], M[i]);
       }
     }
   }
   __syncthreads();
 }
 
+__device__ __forceinline__ double block_sum(double v, double* red, int slot) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[slot * (kCT / 32) + (threadIdx.x >> 5)] = v;
+  return v;
+}
+
 // KKT of the iteration just swept (k > 0), the stopping / divergence rule,
 // then the two ridge solves of iteration k (nmf.py:341-350).
-__global__ void __launch_bounds__(kT) core_step(const double* __restrict__ core, const double* __restrict__ sums,
-                                                 double* __restrict__ xc, double* __restrict__ yc, double* Zl,
-                                                 double* Zr, int s, int r, double pu, double pv, double tol,
-                                                 double* trace, double* scores, SCtrl* ctrl, int k, int max_iter,
-                                                 int first, int solve) {
+__global__ void __launch_bounds__(kCT) core_step(const double* __restrict__ core, const double* __restrict__ sums,
+                                                  double* __restrict__ xc, double* __restrict__ yc, double* Zl,
+                                                  double* Zr, int s, int r, double pu, double pv, double tol,
+                                                  double* trace, double* scores, SCtrl* ctrl, int k, int max_iter,
+                                                  int first, int solve) {
   if (ctrl->done) return;
   extern __shared__ __align__(16) unsigned char sm[];
-  constexpr int LD = kMaxD + 1;
-  double* A = (double*)sm;      // 64 x 65 scratch (s x s or s x r)
-  double* B = A + kMaxD * LD;   // 64 x 65
-  double* M = B + kMaxD * LD;   // r x r
-  double* piv = M + kMaxD * LD; // 2 x 64
-  // the small operands staged in shared memory (every loop below reads them
-  // many times): core (s x s), xc (s x r), yc (r x s)
-  double* coreS = piv + 2 * kMaxD;
-  double* xcS = coreS + s * s;
-  double* ycS = xcS + s * r;
-  __shared__ double red[6][kT / 32];
+  double* E = (double*)sm;         // s x s: E = xc yc - core, later the rhs (s x r)
+  double* B = E + s * s;           // rhs2 (r x s)
+  double* M = B + r * s;           // r x r
+  double* piv = M + r * r;         // 2 x 64
+  double* coreS = piv + 2 * kMaxD; // s x s
+  double* xcS = coreS + s * s;     // s x r
+  double* ycS = xcS + s * r;       // r x s
+  double* ycT = ycS + r * s;       // s x r (yc transposed: conflict-free B operand)
+  __shared__ double red[3 * (kCT / 32)];
   __shared__ int s_stop;
   const int tid = threadIdx.x, sr = s * r, len = sums_len(s, r);
-  const double* sl = sums;        // left: L^T U | L^T dU | sums
-  const double* srt = sums + len; // right: R V^T | R dV^T (as s x r) | sums
+  const double* sl = sums;         // left: L^T U | L^T dU | sums
+  const double* srt = sums + len;  // right: R V^T | R dV^T (as s x r) | sums
   if (tid == 0) s_stop = 0;
-  for (int i = tid; i < s * s; i += kT) coreS[i] = core[i];
-  for (int i = tid; i < s * r; i += kT) xcS[i] = xc[i];
-  for (int i = tid; i < r * s; i += kT) ycS[i] = yc[i];
+  for (int i = tid; i < s * s; i += kCT) coreS[i] = core[i];
+  for (int i = tid; i < s * r; i += kCT) xcS[i] = xc[i];
+  for (int i = tid; i < r * s; i += kCT) {
+    ycS[i] = yc[i];
+    ycT[(i % s) * r + i / s] = yc[i];
+  }
   __syncthreads();
   if (first) {
     // yc = V R^T (nmf.py:338): the reduced right sums of the initial state
-    for (int i = tid; i < r * s; i += kT) {
+    for (int i = tid; i < r * s; i += kCT) {
       const int a = i / s, c = i % s;
       yc[i] = srt[c * r + a];
       ycS[i] = srt[c * r + a];
+      ycT[c * r + a] = srt[c * r + a];
     }
     __syncthreads();
   } else if (k > 0) {
     // ---- KKT score of iteration k - 1 (nmf.py:281-303) ----
-    // A = E = xc yc - core (s x s)
-    for (int i = tid; i < s * s; i += kT) {
-      const int a = i / s, c = i % s;
-      double e = -coreS[i];
-      e += dot4(xcS + a * r, 1, ycS + c, s, r);
-      A[a * LD + c] = e;
-    }
+    double obj = 0.0, t1 = 0.0, t2 = 0.0;
+    small_gemm(s, s, r, xcS, r, 1, ycS, s, [&](int a, int c, double v) {
+      const double e = v - coreS[a * s + c];
+      E[a * s + c] = e;
+      obj += e * e;
+    });
     __syncthreads();
-    double t1 = 0.0, t2 = 0.0, obj = 0.0;
-    for (int i = tid; i < s * s; i += kT) obj += A[(i / s) * LD + i % s] * A[(i / s) * LD + i % s];
-    for (int i = tid; i < s * r; i += kT) {  // (E yc^T + L^T dU)[a][j]
-      const int a = i / r, j = i % r;
-      double v = sl[sr + a * r + j];
-      v += dot4(A + a * LD, 1, ycS + j * s, 1, s);
-      t1 += v * v;
-    }
-    for (int i = tid; i < r * s; i += kT) {  // (xc^T E + dV R^T)[j][c]
-      const int j = i / s, c = i % s;
-      double v = srt[sr + c * r + j];
-      v += dot4(xcS + j, r, A + c, LD, s);
-      t2 += v * v;
-    }
-    double vals[3] = {t1, t2, obj};
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) vals[q] += __shfl_xor_sync(0xffffffffu, vals[q], o);
-      if ((tid & 31) == 0) red[q][tid >> 5] = vals[q];
-    }
+    small_gemm(s, r, s, E, s, 1, ycT, r, [&](int a, int j, double v) {  // (E yc^T + L^T dU)[a][j]
+      const double w = v + sl[sr + a * r + j];
+      t1 += w * w;
+    });
+    small_gemm(r, s, s, xcS, 1, r, E, s, [&](int j, int c, double v) {  // (xc^T E + dV R^T)[j][c]
+      const double w = v + srt[sr + c * r + j];
+      t2 += w * w;
+    });
+    block_sum(t1, red, 0);
+    block_sum(t2, red, 1);
+    block_sum(obj, red, 2);
     __syncthreads();
     if (tid == 0) {
       double a1 = 0, a2 = 0, ob = 0;
-      for (int w = 0; w < kT / 32; ++w) {
-        a1 += red[0][w];
-        a2 += red[1][w];
-        ob += red[2][w];
+      for (int w = 0; w < kCT / 32; ++w) {
+        a1 += red[w];
+        a2 += red[(kCT / 32) + w];
+        ob += red[2 * (kCT / 32) + w];
       }
       const double sc = fmax(fmax(fmax(sqrt(a1), sqrt(a2)), fmax(sqrt(sl[2 * sr]), sqrt(srt[2 * sr]))),
                              fmax(sqrt(sl[2 * sr + 1] + sl[2 * sr + 2] + sl[2 * sr + 3]),
@@ -339,49 +418,27 @@ __global__ void __launch_bounds__(kT) core_step(const double* __restrict__ core,
   }
   if (!solve || k >= max_iter) return;
   // ---- xc = (core yc^T + pu L^T U - L^T dU) (yc yc^T + pu I)^-1 ----
-  for (int i = tid; i < r * r; i += kT) {
-    const int a = i / r, c = i % r;
-    double v = (a == c) ? pu : 0.0;
-    v += dot4(ycS + a * s, 1, ycS + c * s, 1, s);
-    M[a * LD + c] = v;
-  }
-  for (int i = tid; i < s * r; i += kT) {  // rhs (s x r) in A
-    const int a = i / r, c = i % r;
-    double v = pu * sl[a * r + c] - sl[sr + a * r + c];
-    v += dot4(coreS + a * s, 1, ycS + c * s, 1, s);
-    A[a * LD + c] = v;
-  }
+  small_gemm(r, r, s, ycS, s, 1, ycT, r, [&](int a, int c, double v) { M[a * r + c] = v + (a == c ? pu : 0.0); });
+  small_gemm(s, r, s, coreS, s, 1, ycT, r, [&](int a, int c, double v) {  // rhs (s x r) in E
+    E[a * r + c] = v + (pu * sl[a * r + c] - sl[sr + a * r + c]);
+  });
   spd_inverse(M, piv, r);
-  for (int i = tid; i < s * r; i += kT) {
-    const int a = i / r, c = i % r;
-    double v = 0.0;
-    v += dot4(A + a * LD, 1, M + c, LD, r);
-    xc[i] = v;
-    xcS[i] = v;
-    Zl[i] = v;
-  }
+  small_gemm(s, r, r, E, r, 1, M, r, [&](int a, int c, double v) {
+    xc[a * r + c] = v;
+    xcS[a * r + c] = v;
+    Zl[a * r + c] = v;
+  });
   __syncthreads();
   // ---- yc = (xc^T xc + pv I)^-1 (xc^T core + pv V R^T - dV R^T) ----
-  for (int i = tid; i < r * r; i += kT) {
-    const int a = i / r, c = i % r;
-    double v = (a == c) ? pv : 0.0;
-    v += dot4(xcS + a, r, xcS + c, r, s);
-    M[a * LD + c] = v;
-  }
-  for (int i = tid; i < r * s; i += kT) {  // rhs2 (r x s) in B
-    const int a = i / s, c = i % s;
-    double v = pv * srt[c * r + a] - srt[sr + c * r + a];
-    v += dot4(xcS + a, r, coreS + c, s, s);
-    B[a * LD + c] = v;
-  }
+  small_gemm(r, r, s, xcS, 1, r, xcS, r, [&](int a, int c, double v) { M[a * r + c] = v + (a == c ? pv : 0.0); });
+  small_gemm(r, s, s, xcS, 1, r, coreS, s, [&](int a, int c, double v) {  // rhs2 (r x s) in B
+    B[a * s + c] = v + (pv * srt[c * r + a] - srt[sr + c * r + a]);
+  });
   spd_inverse(M, piv, r);
-  for (int i = tid; i < r * s; i += kT) {
-    const int a = i / s, c = i % s;
-    double v = 0.0;
-    v += dot4(M + a * LD, 1, B + c, LD, r);
-    yc[i] = v;
+  small_gemm(r, s, r, M, r, 1, B, s, [&](int a, int c, double v) {
+    yc[a * s + c] = v;
     Zr[c * r + a] = v;  // Z for the right rows: yc^T (s x r)
-  }
+  });
 }
 
 __global__ void init_sctrl(SCtrl* c) {
@@ -408,38 +465,24 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   const int nbr = total - nbl;
   const int len = sums_len(s, r);
   // library scratch: block partials, reduced sums, Z operands
-  static double* scratch = nullptr;
-  static size_t cap = 0;
   const size_t need = ((size_t)total * len + 2 * (size_t)len + 2 * kMaxD * kMaxD) * 8;
-  if (cap < need) {
-    CNMF_CUDA(cudaStreamSynchronize(st));
-    if (scratch) cudaFree(scratch);
-    scratch = nullptr;
-    cap = 0;
-    CNMF_CUDA(cudaMalloc(&scratch, need));
-    cap = need;
-  }
+  void* scr = nullptr;
+  CNMF_TRY(device_scratch("admm-stream", need, &scr, st));
+  double* scratch = (double*)scr;
   double* part = scratch;
   double* sums = part + (size_t)total * len;
   double* Zl = sums + 2 * len;
   double* Zr = Zl + kMaxD * kMaxD;
-  const size_t sweep_smem = ((size_t)S * kMaxD + 2 * kTR * kMaxD) * 8 + (size_t)kTR * S * 4;
-  const size_t core_smem = (3 * (size_t)kMaxD * (kMaxD + 1) + 2 * kMaxD + (size_t)s * s + 2 * (size_t)s * r) * 8;
-  static bool attr = false;
-  if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(row_sweep<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(((size_t)32 * kMaxD + 2 * kTR * kMaxD) * 8 + (size_t)kTR * 32 * 4)));
-    CNMF_CUDA(cudaFuncSetAttribute(row_sweep<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(((size_t)64 * kMaxD + 2 * kTR * kMaxD) * 8 + (size_t)kTR * 64 * 4)));
-    CNMF_CUDA(cudaFuncSetAttribute(core_step, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)((3 * kMaxD * (kMaxD + 1) + 2 * kMaxD + 3 * kMaxD * kMaxD) * 8)));
-    attr = true;
-  }
+  const size_t core_smem = (2 * (size_t)s * s + 4 * (size_t)s * r + (size_t)r * r + 2 * kMaxD) * 8;
+  CNMF_TRY(ensure_smem_attr((const void*)row_sweep<32>, (int)sweep_smem<32>()));
+  CNMF_TRY(ensure_smem_attr((const void*)row_sweep<64>, (int)sweep_smem<64>()));
+  CNMF_TRY(ensure_smem_attr((const void*)core_step, (int)((7 * kMaxD * kMaxD + 2 * kMaxD) * 8)));
   const SSide sl{L, m, S, u, du, pu}, sr{Rt, n, S, vt, dvt, pv};
   auto sweep = [&](int update) -> int {
     if (S == 32)
-      row_sweep<32><<<total, kT, sweep_smem, st>>>(sl, sr, nbl, Zl, Zr, s, r, step, update, part, ctrl);
+      row_sweep<32><<<total, kT, sweep_smem<32>(), st>>>(sl, sr, nbl, Zl, Zr, s, r, step, update, part, ctrl);
     else
-      row_sweep<64><<<total, kT, sweep_smem, st>>>(sl, sr, nbl, Zl, Zr, s, r, step, update, part, ctrl);
+      row_sweep<64><<<total, kT, sweep_smem<64>(), st>>>(sl, sr, nbl, Zl, Zr, s, r, step, update, part, ctrl);
     CNMF_LAUNCH_CHECK();
     reduce_parts<<<dim3((unsigned)ceil_div(len, kT), 2), kT, 0, st>>>(part, nbl, nbr, len, sums, ctrl, update);
     CNMF_LAUNCH_CHECK();
@@ -464,13 +507,13 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   }
   const int k1 = step_limit > 0 ? std::min(max_iter, k0 + step_limit) : max_iter;
   for (int k = k0; k < k1; ++k) {
-    core_step<<<1, kT, core_smem, st>>>(core, sums, xc, yc, Zl, Zr, s, r, pu, pv, tol, trace, scores, ctrl, k,
+    core_step<<<1, kCT, core_smem, st>>>(core, sums, xc, yc, Zl, Zr, s, r, pu, pv, tol, trace, scores, ctrl, k,
                                         max_iter, k == 0 && !resume, 1);
     CNMF_LAUNCH_CHECK();
     CNMF_TRY(sweep(1));
   }
   // score of the last swept iteration (and the stop decision)
-  core_step<<<1, kT, core_smem, st>>>(core, sums, xc, yc, Zl, Zr, s, r, pu, pv, tol, trace, scores, ctrl, k1,
+  core_step<<<1, kCT, core_smem, st>>>(core, sums, xc, yc, Zl, Zr, s, r, pu, pv, tol, trace, scores, ctrl, k1,
                                       max_iter, 0, 0);
   CNMF_LAUNCH_CHECK();
   SCtrl h;

@@ -8,6 +8,8 @@ const char* last_error();
 int panel_ld(int s);
 int gaussian_fill(uint64_t, int64_t, int64_t, int64_t, int, void*, int64_t, cudaStream_t);
 int uniform_fill(uint64_t, int64_t, int64_t, double, double, int, int, void*, cudaStream_t);
+int uniform_fill_at(uint64_t, int64_t, int64_t, int64_t, double, double, int, int, void*, cudaStream_t);
+int normal_fill_at(uint64_t, int64_t, int64_t, int, void*, int64_t*, cudaStream_t);
 
 int panel_cross(const float*, const float*, int64_t, int, double*, cudaStream_t);
 size_t admm_full_workspace(int64_t m, int64_t n, int r);
@@ -89,6 +91,16 @@ int cnmf_gaussian_fill(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_
 int cnmf_uniform_fill(uint64_t seed, int64_t rows, int64_t cols, double low, double high, int dtype, int transpose,
                       void* out, void* stream) {
   return uniform_fill(seed, rows, cols, low, high, dtype, transpose, out, STREAM(stream));
+}
+
+int cnmf_uniform_fill_at(uint64_t seed, int64_t start, int64_t rows, int64_t cols, double low, double high, int dtype,
+                         int transpose, void* out, void* stream) {
+  return uniform_fill_at(seed, start, rows, cols, low, high, dtype, transpose, out, STREAM(stream));
+}
+
+int cnmf_normal_fill_at(uint64_t seed, int64_t start, int64_t count, int dtype, void* out, int64_t* d_end,
+                        void* stream) {
+  return normal_fill_at(seed, start, count, dtype, out, d_end, STREAM(stream));
 }
 
 int cnmf_pass_forward(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int s, float* Y,

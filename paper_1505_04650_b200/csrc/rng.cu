@@ -33,6 +33,7 @@ constexpr int kWin = 128;  // raw positions per warp step (32 lanes x 4 words)
 
 struct StreamDesc {
   uint64_t key;
+  int64_t base;     // raw position of the stream's first variate
   int64_t count;    // variates in this stream
   int64_t row0;     // first output row
   int64_t seg0;     // first segment index (global)
@@ -61,6 +62,7 @@ struct Layout {
   int32_t nseg_full, nseg_last;
   int32_t seglen_full, seglen_last;
   int64_t total_segs;
+  int64_t start;        // single stream: raw position of its first variate (stream continuation)
 };
 
 __device__ uint64_t dev_splitmix64(uint64_t x) {
@@ -89,6 +91,7 @@ __device__ StreamDesc stream_of(const Layout& L, int64_t c) {
   StreamDesc sd;
   const bool last = c == L.nchunks - 1;
   sd.key = L.chunked ? dev_chunk_key(L.key, c) : L.key;
+  sd.base = L.chunked ? 0 : L.start;
   sd.row0 = c * L.chunk_rows;
   sd.count = (last ? L.rows - sd.row0 : L.chunk_rows) * L.cols;
   sd.seg0 = c * L.nseg_full;
@@ -178,9 +181,12 @@ __device__ __forceinline__ void store_variate(T* out, int64_t ld, int64_t cols, 
 // When WRITE, variates are stored from output index `k0`. Returns the number
 // of variates started; *exit_pos receives the final head. When chain != null
 // the start bits of the first window [seg_start, seg_start+128) are recorded.
+// When end != null, the raw position after the stream's last variate (output
+// index count - 1) is stored there (Rng stream continuation).
 template <bool WRITE, typename T>
 __device__ int64_t walk(uint64_t key, int64_t head, int64_t stop, int64_t seg_start, uint32_t* chain, T* out,
-                        int64_t ld, int64_t cols, int64_t row0, int64_t k0, int64_t count, int64_t* exit_pos) {
+                        int64_t ld, int64_t cols, int64_t row0, int64_t k0, int64_t count, int64_t* exit_pos,
+                        int64_t* end = nullptr) {
   const int lane = threadIdx.x & 31;
   int64_t k = 0;
   int64_t base = (head / kWin) * kWin;
@@ -233,7 +239,10 @@ __device__ int64_t walk(uint64_t key, int64_t head, int64_t stop, int64_t seg_st
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int pos = 4 * lane + j;
-          if (pos >= p && pos < fe) store_variate(out, ld, cols, row0, k0 + k + (pos - p), count, xs[j]);
+          if (pos >= p && pos < fe) {
+            store_variate(out, ld, cols, row0, k0 + k + (pos - p), count, xs[j]);
+            if (end != nullptr && k0 + k + (pos - p) == count - 1) *end = base + pos + 1;
+          }
         }
       }
       k += fe - p;
@@ -252,7 +261,10 @@ __device__ int64_t walk(uint64_t key, int64_t head, int64_t stop, int64_t seg_st
 #pragma unroll
         for (int q = 0; q < 4; ++q) chain[q] |= ((f >> 5) == q) ? (1u << (f & 31)) : 0u;
       }
-      if (WRITE && lane == 0) store_variate(out, ld, cols, row0, k0 + k, count, x);
+      if (WRITE && lane == 0) {
+        store_variate(out, ld, cols, row0, k0 + k, count, x);
+        if (end != nullptr && k0 + k == count - 1) *end = nxt;
+      }
       k += 1;
       p = (int)(nxt - base);
     }
@@ -281,7 +293,7 @@ __global__ void k1_speculate(const Layout L, SegState* segs) {
   if (g >= L.total_segs) return;
   const StreamDesc sd = stream_of(L, chunk_of_seg(L, g));
   const int64_t w = g - sd.seg0;
-  const int64_t s0 = w * sd.seglen, s1 = s0 + sd.seglen;
+  const int64_t s0 = sd.base + w * sd.seglen, s1 = s0 + sd.seglen;
   uint32_t chain[4] = {0, 0, 0, 0};
   int64_t ex;
   const int64_t n = walk<false, float>(sd.key, s0, s1, s0, chain, nullptr, 0, 1, 0, 0, 0, &ex);
@@ -309,8 +321,8 @@ __global__ void k2_anchor_scan(const Layout L, SegState* segs, int* flags) {
   __syncthreads();
   for (int w = threadIdx.x; w < sd.nseg; w += blockDim.x) {
     SegState& st = segs[sd.seg0 + w];
-    const int64_t s0 = (int64_t)w * sd.seglen;
-    const int64_t entry = (w == 0) ? 0 : segs[sd.seg0 + w - 1].exit;
+    const int64_t s0 = sd.base + (int64_t)w * sd.seglen;
+    const int64_t entry = (w == 0) ? sd.base : segs[sd.seg0 + w - 1].exit;
     int64_t d = 0;
     int64_t p = entry;
     bool merged = false;
@@ -382,7 +394,7 @@ __global__ void k2_anchor_scan(const Layout L, SegState* segs, int* flags) {
 }
 
 template <typename T>
-__global__ void k3_emit(const Layout L, const SegState* segs, const int* flags, T* out, int64_t ld) {
+__global__ void k3_emit(const Layout L, const SegState* segs, const int* flags, T* out, int64_t ld, int64_t* end) {
   load_zig_tables();
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (g >= L.total_segs) return;
@@ -392,37 +404,42 @@ __global__ void k3_emit(const Layout L, const SegState* segs, const int* flags, 
   const int64_t w = g - sd.seg0;
   const SegState st = segs[g];
   if (st.offset >= sd.count) return;
-  const int64_t s1 = (w + 1) * sd.seglen;
+  const int64_t s1 = sd.base + (w + 1) * sd.seglen;
   int64_t ex;
-  walk<true, T>(sd.key, st.entry, s1, -1, nullptr, out, ld, L.cols, sd.row0, st.offset, sd.count, &ex);
+  walk<true, T>(sd.key, st.entry, s1, -1, nullptr, out, ld, L.cols, sd.row0, st.offset, sd.count, &ex,
+                end);
 }
 
 // Fallback: one warp decodes a whole stream sequentially.
 template <typename T>
-__global__ void k_serial(const Layout L, const int* flags, T* out, int64_t ld) {
+__global__ void k_serial(const Layout L, const int* flags, T* out, int64_t ld, int64_t* end) {
   load_zig_tables();
   if (!flags[blockIdx.x]) return;
   const StreamDesc sd = stream_of(L, blockIdx.x);
-  int64_t head = 0, k = 0;
+  int64_t head = sd.base, k = 0;
   while (k < sd.count) {
     int64_t ex;
-    k += walk<true, T>(sd.key, head, head + 64 * kWin, -1, nullptr, out, ld, L.cols, sd.row0, k, sd.count, &ex);
+    k += walk<true, T>(sd.key, head, head + 64 * kWin, -1, nullptr, out, ld, L.cols, sd.row0, k, sd.count, &ex,
+                       end);
     head = ex;
   }
 }
 
 template <typename T>
-__global__ void uniform_kernel(uint64_t key, int64_t rows, int64_t cols, double low, double high, int transpose,
-                               T* out) {
+__global__ void uniform_kernel(uint64_t key, int64_t start, int64_t rows, int64_t cols, double low, double high,
+                               int transpose, T* out) {
+  // raw draw start + i feeds variate i; thread b covers Philox block
+  // start / 4 + b (words before `start` in the first block are skipped)
   const int64_t total = rows * cols;
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // Philox block
-  if (b * 4 >= total) return;
-  const U64x4 blk = philox4x64((uint64_t)b + 1, 0, key, 0);
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t b0 = start / 4;
+  if ((b0 + b) * 4 >= start + total) return;
+  const U64x4 blk = philox4x64((uint64_t)(b0 + b) + 1, 0, key, 0);
   const double span = __dadd_rn(high, -low);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int64_t i = b * 4 + j;
-    if (i < total) {
+    const int64_t i = (b0 + b) * 4 + j - start;
+    if (i >= 0 && i < total) {
       const double v = __dadd_rn(low, __dmul_rn(span, raw_to_unit(blk.v[j])));
       if (transpose) {
         const int64_t r = i / cols, c = i - (i / cols) * cols;
@@ -436,8 +453,9 @@ __global__ void uniform_kernel(uint64_t key, int64_t rows, int64_t cols, double 
 
 }  // namespace
 
-static Layout make_layout(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_rows) {
+static Layout make_layout(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_rows, int64_t start = 0) {
   Layout L{};
+  L.start = chunk_rows > 0 ? 0 : start;
   L.rows = rows;
   L.cols = cols;
   L.chunked = chunk_rows > 0;
@@ -463,7 +481,8 @@ size_t gaussian_workspace(int64_t rows, int64_t cols, int64_t chunk_rows) {
 }
 
 template <typename T>
-static int gaussian_streams(const Layout& L, T* out, int64_t ld, void* ws, size_t ws_bytes, cudaStream_t stream) {
+static int gaussian_streams(const Layout& L, T* out, int64_t ld, void* ws, size_t ws_bytes, cudaStream_t stream,
+                            int64_t* end = nullptr) {
   if (ws_bytes < gaussian_workspace(L.rows, L.cols, L.chunked ? L.chunk_rows : 0))
     return fail(CNMF_ERR_ARGUMENT, "gaussian_fill: workspace too small");
   char* p = (char*)(((uintptr_t)ws + 15) & ~(uintptr_t)15);
@@ -476,9 +495,9 @@ static int gaussian_streams(const Layout& L, T* out, int64_t ld, void* ws, size_
   CNMF_LAUNCH_CHECK();
   k2_anchor_scan<<<(unsigned)L.nchunks, 256, 0, stream>>>(L, d_seg, d_flags);
   CNMF_LAUNCH_CHECK();
-  k3_emit<T><<<grid, 32 * wpb, 0, stream>>>(L, d_seg, d_flags, out, ld);
+  k3_emit<T><<<grid, 32 * wpb, 0, stream>>>(L, d_seg, d_flags, out, ld, end);
   CNMF_LAUNCH_CHECK();
-  k_serial<T><<<(unsigned)L.nchunks, 32, 0, stream>>>(L, d_flags, out, ld);
+  k_serial<T><<<(unsigned)L.nchunks, 32, 0, stream>>>(L, d_flags, out, ld, end);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }
@@ -505,19 +524,47 @@ int gaussian_fill(uint64_t seed, int64_t rows, int64_t cols, int64_t chunk_rows,
   return rc;
 }
 
-int uniform_fill(uint64_t seed, int64_t rows, int64_t cols, double low, double high, int dtype, int transpose,
-                 void* out, cudaStream_t stream) {
+int uniform_fill_at(uint64_t seed, int64_t start, int64_t rows, int64_t cols, double low, double high, int dtype,
+                    int transpose, void* out, cudaStream_t stream) {
   if (rows < 1 || cols < 1) return fail(CNMF_ERR_ARGUMENT, "uniform_fill needs positive dims");
-  const int64_t blocks = ceil_div(rows * cols, 4);
+  if (start < 0) return fail(CNMF_ERR_ARGUMENT, "uniform_fill: negative stream position");
+  const int64_t blocks = ceil_div(start % 4 + rows * cols, 4);
   const unsigned grid = (unsigned)ceil_div(blocks, 256);
   if (dtype == CNMF_F64)
-    uniform_kernel<double><<<grid, 256, 0, stream>>>(seed, rows, cols, low, high, transpose, (double*)out);
+    uniform_kernel<double><<<grid, 256, 0, stream>>>(seed, start, rows, cols, low, high, transpose, (double*)out);
   else if (dtype == CNMF_F32)
-    uniform_kernel<float><<<grid, 256, 0, stream>>>(seed, rows, cols, low, high, transpose, (float*)out);
+    uniform_kernel<float><<<grid, 256, 0, stream>>>(seed, start, rows, cols, low, high, transpose, (float*)out);
   else
     return fail(CNMF_ERR_ARGUMENT, "unknown dtype");
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
+}
+
+int uniform_fill(uint64_t seed, int64_t rows, int64_t cols, double low, double high, int dtype, int transpose,
+                 void* out, cudaStream_t stream) {
+  return uniform_fill_at(seed, 0, rows, cols, low, high, dtype, transpose, out, stream);
+}
+
+// One stream of `count` standard normals starting at raw position `start`;
+// *d_end (device int64) receives the raw position after the last variate.
+int normal_fill_at(uint64_t seed, int64_t start, int64_t count, int dtype, void* out, int64_t* d_end,
+                   cudaStream_t stream) {
+  if (count < 1) return fail(CNMF_ERR_ARGUMENT, "normal_fill needs a positive count");
+  if (start < 0) return fail(CNMF_ERR_ARGUMENT, "normal_fill: negative stream position");
+  const Layout L = make_layout(seed, 1, count, 0, start);
+  const size_t bytes = gaussian_workspace(1, count, 0);
+  keep_pool();
+  void* ws = nullptr;
+  CNMF_CUDA(cudaMallocAsync(&ws, bytes, stream));
+  int rc;
+  if (dtype == CNMF_F64)
+    rc = gaussian_streams(L, (double*)out, count, ws, bytes, stream, d_end);
+  else if (dtype == CNMF_F32)
+    rc = gaussian_streams(L, (float*)out, count, ws, bytes, stream, d_end);
+  else
+    rc = fail(CNMF_ERR_ARGUMENT, "unknown dtype");
+  cudaFreeAsync(ws, stream);
+  return rc;
 }
 
 }  // namespace cnmf

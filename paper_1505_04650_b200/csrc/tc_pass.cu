@@ -31,7 +31,7 @@
 //               so D = [A_hi X_hi | A_hi X_lo + A_lo X_hi]; one
 //               tcgen05.commit per K tile releases the TMEM A slot and the
 //               panel slot together.
-//   warps 10..  epilogue: the tensor core accumulates at most KB = 2 K tiles
+//   warps 10..  epilogue: the tensor core accumulates at most KB = 4 K tiles
 //               into a double-buffered TMEM accumulator, the partial sums
 //               move to fp32 registers (round-to-nearest adds), so the error
 //               does not grow with the tensor-core accumulation chain.
@@ -58,7 +58,13 @@ constexpr int BMT = 128;  // output rows per tile (TMEM lanes)
 constexpr int BKT = 32;   // K per stage (one 128B swizzle atom of fp32)
 constexpr int NSPL = 8;   // splitter warps (2 per TMEM lane quarter; 8 panel K chunks)
 #ifndef CNMF_PASS_KB
-#define CNMF_PASS_KB 2
+#define CNMF_PASS_KB 4
+#endif
+#ifndef CNMF_PASS_NACC
+#define CNMF_PASS_NACC 2
+#endif
+#ifndef CNMF_PASS_AST64
+#define CNMF_PASS_AST64 4
 #endif
 
 // mbarrier wait with a suspend-time hint: a waiting warp sleeps in the
@@ -101,19 +107,17 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                : "memory");
 }
 
-// 32 lanes x 16 consecutive fp32 columns per warp
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
+// 32 lanes x 8 consecutive fp32 columns per warp
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15}, [%16];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
       "tcgen05.wait::ld.sync.aligned;"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
       : "r"(taddr)
       : "memory");
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 // 32 lanes x 16 consecutive 32-bit columns per warp
@@ -184,11 +188,12 @@ struct TcCfg {
   static constexpr int BRAW = BKT * S * 4;      // raw fp32 panel tile [32 k][S]: 4 or 8 KB
   static constexpr int STAGE = ABYTES + BRAW;   // one TMA stage: A tile + its panel tile
   static constexpr int BSPL = BKT * 2 * S * 4;  // split K-major SW128 panel slot [hi; lo]
-  static constexpr int AST = 4;                 // TMEM A ring = split panel ring = MMA-done ring
+  static constexpr int NACC = CNMF_PASS_NACC;   // TMEM accumulator buffers
+  static constexpr int AST = S == 64 ? CNMF_PASS_AST64 : 4;  // TMEM A ring = split panel ring = MMA-done ring
   static constexpr int ST = (227 * 1024 - 1024 - AST * BSPL) / STAGE;  // stage ring (DRAM bytes in flight)
   static constexpr int KB = CNMF_PASS_KB;       // K tiles per tensor-core accumulation block
   static constexpr int ACC_COLS = 2 * S;        // per accumulator buffer
-  static constexpr int A_COL0 = 2 * ACC_COLS;   // first TMEM column of the A ring
+  static constexpr int A_COL0 = NACC * ACC_COLS;  // first TMEM column of the A ring
   static constexpr int TMEM_COLS = (A_COL0 + AST * 2 * BKT <= 256) ? 256 : 512;
   static constexpr int NEPI = 4 * (S / 32);     // epilogue warps (lane quarter x 32-column group)
   static constexpr int THREADS = 32 * (2 + NSPL + NEPI);
@@ -291,8 +296,8 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
   uint64_t* afull = empty + C::ST;                      // [AST] split A in TMEM + split panel in SMEM
   uint64_t* mdone = afull + C::AST;                     // [AST] MMAs of the slot's K tile retired
   uint64_t* tfull = mdone + C::AST;                     // [2] accumulator ready
-  uint64_t* tempty = tfull + 2;                         // [2] accumulator drained
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* tempty = tfull + C::NACC;                   // [NACC] accumulator drained
+  uint32_t* tmem_slot = (uint32_t*)(tempty + C::NACC);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // this CTA's share of the concatenated unit sequence (side 0, then side 1)
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
       mbar_init(&afull[s], NSPL);
       mbar_init(&mdone[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::NACC; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], C::NEPI);
     }
@@ -388,7 +393,7 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
     const int q = warp & 3;                         // TMEM lane quarter this warp may access
     const int cg = 32 * ((warp - kWarpEpi0) >> 2);  // first output column of this warp
     const int row_in_tile = 32 * q + lane;
-    Ring<2> racc;
+    Ring<C::NACC> racc;
     float acc[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) acc[j] = 0.f;
@@ -405,12 +410,12 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
       tc_fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + racc.i * C::ACC_COLS + cg;
 #pragma unroll
-      for (int c0 = 0; c0 < 32; c0 += 16) {
-        float vh[16], vl[16];
-        tmem_ld16(taddr + c0, vh);
-        tmem_ld16(taddr + S + c0, vl);
+      for (int c0 = 0; c0 < 32; c0 += 8) {  // 8 columns at a time: few live temporaries (96-register cap at S = 64)
+        float vh[8], vl[8];
+        tmem_ld8(taddr + c0, vh);
+        tmem_ld8(taddr + S + c0, vl);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[c0 + j] += vh[j] + vl[j];
+        for (int j = 0; j < 8; ++j) acc[c0 + j] += vh[j] + vl[j];
       }
       tc_fence_before();
       __syncwarp();
@@ -450,7 +455,7 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
     constexpr uint32_t idesc_cat = idesc_tf32(2 * S);
     constexpr uint32_t idesc_hi = idesc_tf32(S);
     Ring<C::AST> ra;
-    Ring<2> racc;
+    Ring<C::NACC> racc;
     Walk w;
     w.start(lo0, hi0, lo1, hi1, s0, s1);
     bool block_start = true;
@@ -472,8 +477,10 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
         for (int k = 0; k < BKT / 8; ++k) {
           const uint64_t bcat = smem_desc(sb + 32 * k, 16, 1024);  // 8 tf32 = 32 B per K step
           const uint32_t acc = (block_start && k == 0) ? 0u : 1u;
+#ifndef CNMF_VARIANT_NOMMA
           tc_mma_ts(dcat, ahi + 8 * k, bcat, idesc_cat, acc);  // [A_hi X_hi | A_hi X_lo]
           tc_mma_ts(dlo, alo + 8 * k, bcat, idesc_hi, 1u);     //            + A_lo X_hi
+#endif
         }
         tc_commit(&mdone[ra.i]);  // releases the TMEM A slot and the split panel slot
         if (block_end) tc_commit(&tfull[racc.i]);
@@ -536,6 +543,7 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[r.i]);
+#ifndef CNMF_VARIANT_NOSPLIT
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const float v = hi[k];
@@ -550,6 +558,14 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
           ph[t][j] = tf32_rn(v);
           pl[t][j] = tf32_rn(v - ph[t][j]);
         }
+#else
+#pragma unroll
+      for (int k = 0; k < 16; ++k) lo[k] = hi[k];
+#pragma unroll
+      for (int t = 0; t < PT; ++t)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) pl[t][j] = ph[t][j];
+#endif
       if (ra.wrapped) mbar_sleep(&mdone[ra.i], ra.ph ^ 1);  // the slot's previous K tile retired
       tc_fence_after();
       const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + C::A_COL0 + ra.i * 2 * BKT + 16 * half;

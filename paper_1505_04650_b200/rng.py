@@ -36,13 +36,21 @@ def child_seed(seed, tag):
 
 
 class Rng:
-    """Seeded device stream (rng.py:38-70). Each call starts the stream from
-    its beginning, like a freshly constructed reference ``Rng`` would."""
+    """Seeded device stream (rng.py:38-70). Successive draws continue the
+    stream like the reference's numpy Generator: the instance tracks the raw
+    64-bit draw position (uniform: one raw draw per variate; standard_normal:
+    the ziggurat's variable count, reported back by the device sampler).
+
+    ``integers`` and ``permutation`` (rng.py:66-70) draw through numpy's
+    bounded-integer samplers (32-bit buffered draws, rejection loops); they are
+    not on the compression / NMF / SNMF path and have no device sampler here:
+    they raise ``ArgumentError`` (INTEGRATION.md, "Rng")."""
 
     algorithm = ALGORITHM
 
     def __init__(self, seed):
         self.seed = int(seed) & MASK64
+        self._pos = 0  # raw 64-bit draws consumed so far
 
     def __repr__(self):
         return f"Rng(seed={self.seed}, algorithm={self.algorithm!r})"
@@ -54,16 +62,28 @@ class Rng:
         rows, cols = _shape2(shape)
         require_cuda()
         t = empty((rows, cols), dtype=dtype)
-        _lib.call("cnmf_gaussian_fill", self.seed, rows, cols, 0, _code(dtype), t.data_ptr(), cols, stream())
+        end = torch.zeros(1, dtype=torch.int64, device=t.device)
+        _lib.call("cnmf_normal_fill_at", self.seed, self._pos, rows * cols, _code(dtype), t.data_ptr(),
+                  end.data_ptr(), stream())
+        self._pos = int(end.item())
         return t.reshape(shape)
 
     def uniform(self, shape, low=0.0, high=1.0, dtype=torch.float64, transpose=False):
         rows, cols = _shape2(shape)
         require_cuda()
         t = empty((cols, rows) if transpose else (rows, cols), dtype=dtype)
-        _lib.call("cnmf_uniform_fill", self.seed, rows, cols, float(low), float(high), _code(dtype),
+        _lib.call("cnmf_uniform_fill_at", self.seed, self._pos, rows, cols, float(low), float(high), _code(dtype),
                   int(bool(transpose)), t.data_ptr(), stream())
+        self._pos += rows * cols
         return t if transpose else t.reshape(shape)
+
+    def integers(self, low, high, size=None):
+        raise ArgumentError("Rng.integers has no device sampler (not on the compressed-NMF path); "
+                            "draw indices with numpy from Rng.child(tag).seed")
+
+    def permutation(self, n):
+        raise ArgumentError("Rng.permutation has no device sampler (not on the compressed-NMF path); "
+                            "draw permutations with numpy from Rng.child(tag).seed")
 
 
 def _shape2(shape):

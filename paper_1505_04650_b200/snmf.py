@@ -96,6 +96,9 @@ def select_columns_xray(r_mat, r, mass=None, nnls_tol=1e-10):
 
 
 def _right_factor(red, picks, nnls_tol):
+    """NNLS coefficients of every reduced column over the picked ones; a
+    tripped exchange cap raises ConvergenceError (its ``best`` is the capped
+    iterate, and ``picks`` the selection it was computed for)."""
     k = len(picks)
     d_picks = torch.as_tensor(np.asarray(picks, dtype=np.int64), device=red.W.device)
     Ht = zeros((red.n, k), dtype=torch.float64)
@@ -103,7 +106,9 @@ def _right_factor(red, picks, nnls_tol):
     _lib.call("cnmf_right_factor", red.W.data_ptr(), red.n, red.s, red.ld, d_picks.data_ptr(), k, float(nnls_tol),
               Ht.data_ptr(), ctypes.byref(capped), stream())
     if capped.value:
-        raise ConvergenceError(f"active-set exchange cap {3 * k} exceeded", best=Ht.t().cpu().numpy())
+        err = ConvergenceError(f"active-set exchange cap {3 * k} exceeded", best=Ht.t().cpu().numpy())
+        err.picks = np.asarray(picks, dtype=np.int64)
+        raise err
     return Ht, d_picks
 
 

@@ -66,6 +66,26 @@ def test_ziggurat_tail_bitexact():
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("seed", [3, 2**64 - 5])
+def test_rng_successive_draws_continue_the_stream(seed):
+    # rng.py:38-70: successive draws on one Rng continue numpy's Philox
+    # stream (uniform = one raw draw per variate, normals = the ziggurat's
+    # variable count), including starts in the middle of a 4-word block
+    r = C.Rng(seed)
+    g = O.generator(seed)
+    for kind, shape in (("u", (3, 5)), ("n", (1, 1001)), ("u", (7,)), ("n", (40, 25)), ("n", (3,)),
+                        ("u", (2, 9)), ("n", (1, 200_001)), ("u", (1, 6))):
+        if kind == "u":
+            got = r.uniform(shape).cpu().numpy()
+            want = g.uniform(0.0, 1.0, size=shape)
+        else:
+            got = r.standard_normal(shape).cpu().numpy()
+            want = g.standard_normal(shape)
+        assert np.array_equal(got, want), (kind, shape)
+    with pytest.raises(C.ArgumentError):
+        r.permutation(5)
+
+
 def test_uniform_bitexact(golden):
     got = C.Rng(5).child("init-left").uniform((30, 4)).cpu().numpy()
     assert np.array_equal(got, golden["uniform_init_left_seed5"])
