@@ -240,6 +240,64 @@ int cnmf_admm_full_run(const float* A, int64_t m, int64_t n, int64_t lda, int r,
                        double tol, double* trace, double* scores, int* iterations, int* done, int resume,
                        int step_limit, void* ws, size_t ws_bytes, void* stream);
 
+
+/* ---- column-sharded multi-GPU pieces (paper_1505_04650_b200/distributed.py)
+ * The host drives these one phase at a time and all-reduces between them
+ * (NCCL through torch.distributed); every buffer is device memory.
+ *
+ * Compressed ADMM with U / dU row-sharded (the rows of L this rank owns) and
+ * V^T / dV^T column-sharded (the rows of R^T of this rank's columns),
+ * nmf.py:334-377: per iteration
+ *   cnmf_admm_shard_core   the replicated core step (KKT score of the previous
+ *                          iteration from the all-reduced sums, the stop and
+ *                          divergence rules, the two ridge solves);
+ *   cnmf_admm_shard_sweep  this rank's rows: x = max(P z + dx / p, 0), the dual
+ *                          update, and the partial sums L_i^T U_i, L_i^T dU_i,
+ *                          R_i V_i^T, R_i dV_i^T and the four KKT sums per side,
+ *                          written at byte offset cnmf_admm_shard_sums_offset()
+ *                          of ws (2 x (2 s r + 4) doubles) -- the block the host
+ *                          all-reduces (SUM) before the next core step.
+ * ws: cnmf_admm_shard_workspace(s, r) bytes; cnmf_admm_shard_begin resets it;
+ * cnmf_admm_shard_status copies (next iteration, done, iterations, diverged
+ * iteration or -1) to the host int[4] (synchronises).
+ *
+ * Column selection on a column shard W_i (n_i x ld, fp64, the local rows of
+ * (Q^T A)^T), snmf.py:39-126:
+ *   cnmf_shard_argmax      (value, index) of the best unpicked entry of v
+ *                          (ties -> lowest index), into device scalars; the
+ *                          host all-gathers the pairs of all ranks;
+ *   cnmf_spa_shard_step    project every local column off v (NULL: none) and
+ *                          store the residual squared norms (picked -> 0);
+ *   cnmf_xray_shard_scores score_c = (r_j . W_c) / denom_c for the broadcast
+ *                          residual column r_j;
+ *   cnmf_col_mass          denom_c = mass . W_c;
+ *   cnmf_right_factor_given / cnmf_refit_given  NNLS coefficients of every
+ *                          local column over k picked columns given
+ *                          explicitly (P: k x ld fp64, replicated), and the
+ *                          residual R / squared norms sq / (res, ref) totals.
+ */
+size_t cnmf_admm_shard_workspace(int s, int r);
+size_t cnmf_admm_shard_sums_offset(void);
+int cnmf_admm_shard_begin(void* ws, int s, int r, void* stream);
+int cnmf_admm_shard_sweep(void* ws, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
+                          double* du, double* vt, double* dvt, double pu, double pv, double step, int update,
+                          void* stream);
+int cnmf_admm_shard_core(void* ws, const double* core, double* xc, double* yc, int s, int r, double pu, double pv,
+                         double tol, double* trace, double* scores, int k, int max_iter, int first, int solve,
+                         void* stream);
+int cnmf_admm_shard_status(const void* ws, int* state, void* stream);
+int cnmf_shard_argmax(const double* v, int64_t n, const uint8_t* picked, const uint8_t* valid, double* out_v,
+                      int64_t* out_i, void* stream);
+int cnmf_spa_shard_step(double* W, int64_t n, int s, int64_t ld, const double* v, const uint8_t* picked, double* sq,
+                        void* stream);
+int cnmf_xray_shard_scores(const double* W, int64_t n, int s, int64_t ld, const double* rj, const double* denom,
+                           double* score, void* stream);
+int cnmf_col_mass(const double* W, int64_t n, int s, int64_t ld, const double* mass, double* denom, void* stream);
+int cnmf_right_factor_given(const double* W, int64_t n, int s, int64_t ld, const double* P, int k, double tol,
+                            double* Ht, int64_t* n_capped, void* stream);
+int cnmf_refit_given(const double* W, int64_t n, int s, int64_t ld, const double* P, int k, const double* Ht,
+                     double* R, double* sq, double* tot, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,20 @@ SIGNATURES = {
     "cnmf_panel_cross": (c_int, [vp, vp, c_i64, c_int, vp, vp]),
     "cnmf_residual_norms": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, vp, c_int, vp, vp]),
     "cnmf_admm_workspace": (c_size, [c_i64, c_i64, c_int, c_int]),
+    "cnmf_admm_shard_workspace": (c_size, [c_int, c_int]),
+    "cnmf_admm_shard_sums_offset": (c_size, []),
+    "cnmf_admm_shard_begin": (c_int, [vp, c_int, c_int, vp]),
+    "cnmf_admm_shard_sweep": (c_int, [vp, vp, c_i64, vp, c_i64, c_int, c_int, vp, vp, vp, vp, c_dbl, c_dbl, c_dbl,
+                                      c_int, vp]),
+    "cnmf_admm_shard_core": (c_int, [vp, vp, vp, vp, c_int, c_int, c_dbl, c_dbl, c_dbl, vp, vp, c_int, c_int, c_int,
+                                     c_int, vp]),
+    "cnmf_admm_shard_status": (c_int, [vp, c_intp, vp]),
+    "cnmf_shard_argmax": (c_int, [vp, c_i64, vp, vp, vp, vp, vp]),
+    "cnmf_spa_shard_step": (c_int, [vp, c_i64, c_int, c_i64, vp, vp, vp, vp]),
+    "cnmf_xray_shard_scores": (c_int, [vp, c_i64, c_int, c_i64, vp, vp, vp, vp]),
+    "cnmf_col_mass": (c_int, [vp, c_i64, c_int, c_i64, vp, vp, vp]),
+    "cnmf_right_factor_given": (c_int, [vp, c_i64, c_int, c_i64, vp, c_int, c_dbl, vp, c_i64p, vp]),
+    "cnmf_refit_given": (c_int, [vp, c_i64, c_int, c_i64, vp, c_int, vp, vp, vp, vp, vp]),
     "cnmf_admm_run": (c_int, [vp, vp, c_i64, vp, c_i64, c_int, c_int, vp, vp, vp, vp, vp, vp, c_dbl, c_dbl,
                               c_dbl, c_int, c_dbl, vp, vp, c_intp, c_intp, c_int, c_int, vp, c_size, vp]),
 }

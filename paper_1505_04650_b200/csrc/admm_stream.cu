@@ -528,4 +528,82 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   return CNMF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Column-sharded ADMM (paper_1505_04650_b200/distributed.py): the same
+// kernels driven one phase at a time by the host, so that the reduced sums of
+// every rank's row blocks can be all-reduced (NCCL) between the sweep and the
+// replicated core step. Workspace (doubles): [ctrl 8 | Zl 64 x 64 | Zr 64 x 64 |
+// sums 2 x sums_len(s, r)]; the sums are [left: L^T U | L^T dU | 4 KKT sums,
+// right: R V^T | R dV^T | 4 KKT sums] (s x r blocks, row-major).
+// ---------------------------------------------------------------------------
+size_t admm_shard_workspace(int s, int r) { return (8 + 2 * (size_t)kMaxD * kMaxD + 2 * (size_t)sums_len(s, r)) * 8; }
+size_t admm_shard_sums_offset() { return (8 + 2 * (size_t)kMaxD * kMaxD) * 8; }
+
+struct ShardWs {
+  SCtrl* ctrl;
+  double* Zl;
+  double* Zr;
+  double* sums;
+};
+
+static ShardWs shard_ws(void* ws) {
+  double* p = (double*)ws;
+  return ShardWs{(SCtrl*)p, p + 8, p + 8 + kMaxD * kMaxD, p + 8 + 2 * kMaxD * kMaxD};
+}
+
+int admm_shard_begin(void* ws, int s, int r, cudaStream_t st) {
+  if (s < 1 || r < 1 || s > kMaxD || r > kMaxD) return fail(CNMF_ERR_ARGUMENT, "sharded ADMM: 1 <= r, s <= 64");
+  init_sctrl<<<1, 1, 0, st>>>(shard_ws(ws).ctrl);
+  CNMF_LAUNCH_CHECK();
+  return CNMF_OK;
+}
+
+int admm_shard_sweep(void* ws, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
+                     double* du, double* vt, double* dvt, double pu, double pv, double step, int update,
+                     cudaStream_t st) {
+  if (s < 1 || r < 1 || s > kMaxD || r > kMaxD) return fail(CNMF_ERR_ARGUMENT, "sharded ADMM: 1 <= r, s <= 64");
+  const ShardWs w = shard_ws(ws);
+  const int S = s <= 32 ? 32 : 64;
+  const int total = 2 * device_sms();
+  const int64_t rows = std::max<int64_t>(m + n, 1);
+  const int nbl = (int)std::max<int64_t>(1, std::min<int64_t>(total - 1, (total * m + rows / 2) / rows));
+  const int nbr = total - nbl;
+  const int len = sums_len(s, r);
+  void* part = nullptr;
+  CNMF_TRY(device_scratch("admm-shard-part", (size_t)total * len * 8, &part, st));
+  CNMF_TRY(ensure_smem_attr((const void*)row_sweep<32>, (int)sweep_smem<32>()));
+  CNMF_TRY(ensure_smem_attr((const void*)row_sweep<64>, (int)sweep_smem<64>()));
+  const SSide sl{L, m, S, u, du, pu}, sr{Rt, n, S, vt, dvt, pv};
+  if (S == 32)
+    row_sweep<32><<<total, kT, sweep_smem<32>(), st>>>(sl, sr, nbl, w.Zl, w.Zr, s, r, step, update, (double*)part,
+                                                        w.ctrl);
+  else
+    row_sweep<64><<<total, kT, sweep_smem<64>(), st>>>(sl, sr, nbl, w.Zl, w.Zr, s, r, step, update, (double*)part,
+                                                        w.ctrl);
+  CNMF_LAUNCH_CHECK();
+  reduce_parts<<<dim3((unsigned)ceil_div(len, kT), 2), kT, 0, st>>>((double*)part, nbl, nbr, len, w.sums, w.ctrl,
+                                                                    update);
+  CNMF_LAUNCH_CHECK();
+  return CNMF_OK;
+}
+
+int admm_shard_core(void* ws, const double* core, double* xc, double* yc, int s, int r, double pu, double pv,
+                    double tol, double* trace, double* scores, int k, int max_iter, int first, int solve,
+                    cudaStream_t st) {
+  const ShardWs w = shard_ws(ws);
+  const size_t core_smem = (2 * (size_t)s * s + 4 * (size_t)s * r + (size_t)r * r + 2 * kMaxD) * 8;
+  CNMF_TRY(ensure_smem_attr((const void*)core_step, (int)((7 * kMaxD * kMaxD + 2 * kMaxD) * 8)));
+  core_step<<<1, kCT, core_smem, st>>>(core, w.sums, xc, yc, w.Zl, w.Zr, s, r, pu, pv, tol, trace, scores, w.ctrl, k,
+                                      max_iter, first, solve);
+  CNMF_LAUNCH_CHECK();
+  return CNMF_OK;
+}
+
+// state[0..3] = (next iteration, done, iterations, diverged iteration or -1)
+int admm_shard_status(const void* ws, int* state, cudaStream_t st) {
+  CNMF_CUDA(cudaMemcpyAsync(state, ws, sizeof(SCtrl), cudaMemcpyDeviceToHost, st));
+  CNMF_CUDA(cudaStreamSynchronize(st));
+  return CNMF_OK;
+}
+
 }  // namespace cnmf

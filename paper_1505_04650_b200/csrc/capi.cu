@@ -47,6 +47,22 @@ int admm_run(const double*, const float*, int64_t, const float*, int64_t, int, i
              double*, double*, double*, double, double, double, int, double, double*, double*, int*, void*, size_t,
              int, int, cudaStream_t);
 int64_t launch_count();
+size_t admm_shard_workspace(int, int);
+size_t admm_shard_sums_offset();
+int admm_shard_begin(void*, int, int, cudaStream_t);
+int admm_shard_sweep(void*, const float*, int64_t, const float*, int64_t, int, int, double*, double*, double*,
+                     double*, double, double, double, int, cudaStream_t);
+int admm_shard_core(void*, const double*, double*, double*, int, int, double, double, double, double*, double*, int,
+                    int, int, int, cudaStream_t);
+int admm_shard_status(const void*, int*, cudaStream_t);
+int shard_argmax(const double*, int64_t, const uint8_t*, const uint8_t*, double*, int64_t*, cudaStream_t);
+int spa_shard_step(double*, int64_t, int, int64_t, const double*, const uint8_t*, double*, cudaStream_t);
+int xray_shard_scores(const double*, int64_t, int, int64_t, const double*, const double*, double*, cudaStream_t);
+int col_mass_denoms(const double*, int64_t, int, int64_t, const double*, double*, cudaStream_t);
+int right_factor_given(const double*, int64_t, int, int64_t, const double*, int, double, double*, int64_t*,
+                       cudaStream_t);
+int refit_given(const double*, int64_t, int, int64_t, const double*, int, const double*, double*, double*, double*,
+                cudaStream_t);
 void set_pass_impl(int);
 void set_pass_profiling(int);
 int pass_stats(double*, int64_t*, double*);
@@ -265,4 +281,46 @@ int cnmf_admm_run(const double* core, const float* L, int64_t m, const float* Rt
   return rc;
 }
 
+
+/* ---- column-shard primitives (multi-GPU; distributed.py) ---------------- */
+size_t cnmf_admm_shard_workspace(int s, int r) { return admm_shard_workspace(s, r); }
+size_t cnmf_admm_shard_sums_offset(void) { return admm_shard_sums_offset(); }
+int cnmf_admm_shard_begin(void* ws, int s, int r, void* stream) { return admm_shard_begin(ws, s, r, STREAM(stream)); }
+int cnmf_admm_shard_sweep(void* ws, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
+                          double* du, double* vt, double* dvt, double pu, double pv, double step, int update,
+                          void* stream) {
+  return admm_shard_sweep(ws, L, m, Rt, n, s, r, u, du, vt, dvt, pu, pv, step, update, STREAM(stream));
+}
+int cnmf_admm_shard_core(void* ws, const double* core, double* xc, double* yc, int s, int r, double pu, double pv,
+                         double tol, double* trace, double* scores, int k, int max_iter, int first, int solve,
+                         void* stream) {
+  return admm_shard_core(ws, core, xc, yc, s, r, pu, pv, tol, trace, scores, k, max_iter, first, solve,
+                         STREAM(stream));
+}
+int cnmf_admm_shard_status(const void* ws, int* state, void* stream) {
+  return admm_shard_status(ws, state, STREAM(stream));
+}
+int cnmf_shard_argmax(const double* v, int64_t n, const uint8_t* picked, const uint8_t* valid, double* out_v,
+                      int64_t* out_i, void* stream) {
+  return shard_argmax(v, n, picked, valid, out_v, out_i, STREAM(stream));
+}
+int cnmf_spa_shard_step(double* W, int64_t n, int s, int64_t ld, const double* v, const uint8_t* picked, double* sq,
+                        void* stream) {
+  return spa_shard_step(W, n, s, ld, v, picked, sq, STREAM(stream));
+}
+int cnmf_xray_shard_scores(const double* W, int64_t n, int s, int64_t ld, const double* rj, const double* denom,
+                           double* score, void* stream) {
+  return xray_shard_scores(W, n, s, ld, rj, denom, score, STREAM(stream));
+}
+int cnmf_col_mass(const double* W, int64_t n, int s, int64_t ld, const double* mass, double* denom, void* stream) {
+  return col_mass_denoms(W, n, s, ld, mass, denom, STREAM(stream));
+}
+int cnmf_right_factor_given(const double* W, int64_t n, int s, int64_t ld, const double* P, int k, double tol,
+                            double* Ht, int64_t* n_capped, void* stream) {
+  return right_factor_given(W, n, s, ld, P, k, tol, Ht, n_capped, STREAM(stream));
+}
+int cnmf_refit_given(const double* W, int64_t n, int s, int64_t ld, const double* P, int k, const double* Ht,
+                     double* R, double* sq, double* tot, void* stream) {
+  return refit_given(W, n, s, ld, P, k, Ht, R, sq, tot, STREAM(stream));
+}
 }  // extern "C"

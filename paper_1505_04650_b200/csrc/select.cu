@@ -149,12 +149,12 @@ __global__ void f32_to_f64_panel(const float* __restrict__ src, int64_t rows, in
 
 // gram[a][b] = W_{p_a} . W_{p_b};  target[c][k] = W_c . W_{p_k}
 __global__ void __launch_bounds__(kSelThreads)
-    gather_gram(const double* __restrict__ W, int64_t n, int s, int64_t ld, const int64_t* __restrict__ picks, int k,
-                double* __restrict__ gram, double* __restrict__ target) {
-  extern __shared__ double sc[];  // k x s picked columns
+    gather_gram(const double* __restrict__ W, int64_t n, int s, int64_t ld, const double* __restrict__ Wp,
+                const int64_t* __restrict__ picks, int k, double* __restrict__ gram, double* __restrict__ target) {
+  extern __shared__ double sc[];  // k x s picked columns: rows picks[a] of Wp (Wp = W, or a gathered copy)
   for (int i = threadIdx.x; i < k * s; i += blockDim.x) {
     const int a = i / s, j = i % s;
-    sc[i] = W[picks[a] * ld + j];
+    sc[i] = Wp[(picks ? picks[a] : a) * ld + j];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -188,13 +188,13 @@ __global__ void __launch_bounds__(kSelThreads)
 // res_c = W_c - sum_a H[c][a] W_{p_a}; out: residual squared norms (and the
 // residual itself when R != null); picked columns report 0.
 __global__ void __launch_bounds__(kSelThreads)
-    refit_residual(const double* __restrict__ W, int64_t n, int s, int64_t ld, const int64_t* __restrict__ picks,
-                   int k, const double* __restrict__ H, double* __restrict__ R, double* __restrict__ sq_out,
-                   double* __restrict__ tot) {
+    refit_residual(const double* __restrict__ W, int64_t n, int s, int64_t ld, const double* __restrict__ Wp,
+                   const int64_t* __restrict__ picks, int k, const double* __restrict__ H, double* __restrict__ R,
+                   double* __restrict__ sq_out, double* __restrict__ tot) {
   extern __shared__ double sc[];
   for (int i = threadIdx.x; i < k * s; i += blockDim.x) {
     const int a = i / s, j = i % s;
-    sc[i] = W[picks[a] * ld + j];
+    sc[i] = Wp[(picks ? picks[a] : a) * ld + j];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(kSelThreads)
     xray_scores(const double* __restrict__ W, const double* __restrict__ R, int64_t n, int s, int64_t ld,
                 const int64_t* __restrict__ jsel, const double* __restrict__ denom, double* __restrict__ score) {
   __shared__ double rj[kMaxS];
-  const int64_t j = *jsel;
+  const int64_t j = jsel ? *jsel : 0;  // jsel = null: R is the residual column itself
   for (int i = threadIdx.x; i < s; i += blockDim.x) rj[i] = R[j * ld + i];
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -348,6 +348,128 @@ int select_spa(double* W, int64_t n, int s, int64_t ld, int r, int64_t* picks_ho
   return CNMF_OK;
 }
 
+namespace {
+
+// SPA on a column shard: project every column off v (v != null), store the
+// residual squared norms (picked columns report 0)
+__global__ void __launch_bounds__(kSelThreads)
+    spa_project_norms(double* __restrict__ W, int64_t n, int s, int64_t ld, const double* __restrict__ v,
+                      const uint8_t* __restrict__ picked, double* __restrict__ sq) {
+  __shared__ double sv[kMaxS];
+  for (int i = threadIdx.x; i < s; i += blockDim.x) sv[i] = v ? v[i] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t c = (int64_t)blockIdx.x * kSelWarps + warp; c < n; c += (int64_t)gridDim.x * kSelWarps) {
+    double* col = W + c * ld;
+    double x[kMaxS / 32];
+#pragma unroll
+    for (int q = 0; q < kMaxS / 32; ++q) {
+      const int i = lane + 32 * q;
+      x[q] = (i < s) ? col[i] : 0.0;
+    }
+    if (v != nullptr) {
+      double d = 0.0;
+#pragma unroll
+      for (int q = 0; q < kMaxS / 32; ++q) {
+        const int i = lane + 32 * q;
+        if (i < s) d += sv[i] * x[q];
+      }
+      d = wsum(d);
+#pragma unroll
+      for (int q = 0; q < kMaxS / 32; ++q) {
+        const int i = lane + 32 * q;
+        if (i < s) {
+          x[q] -= sv[i] * d;
+          col[i] = x[q];
+        }
+      }
+    }
+    double q2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kMaxS / 32; ++q) q2 += x[q] * x[q];
+    q2 = wsum(q2);
+    if (lane == 0) sq[c] = picked[c] ? 0.0 : q2;
+  }
+}
+
+// final stage of the two-stage argmax: (value, index) of the best block
+__global__ void argmax_final(const double* __restrict__ blk_v, const int64_t* __restrict__ blk_i, int nb,
+                             double* __restrict__ out_v, int64_t* __restrict__ out_i) {
+  if (threadIdx.x != 0) return;
+  double bv = -DBL_MAX;
+  int64_t bi = INT64_MAX;
+  for (int b = 0; b < nb; ++b) better(bv, bi, blk_v[b], blk_i[b]);
+  *out_v = bv;
+  *out_i = bi;
+}
+
+}  // namespace
+
+// ---- column-shard primitives (multi-GPU SPA / XRAY, distributed.py) ------
+// argmax over v[0..n) of the unpicked (and valid) entries; ties -> lowest
+// index (numpy.argmax); picked entries count as 0 (valid == null, residual
+// norms) or -inf (valid != null, scores). out_v / out_i: device scalars.
+int shard_argmax(const double* v, int64_t n, const uint8_t* picked, const uint8_t* valid, double* out_v,
+                 int64_t* out_i, cudaStream_t st) {
+  const unsigned agrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kSelThreads), 4 * kNumSMs));
+  void* scr = nullptr;
+  CNMF_TRY(device_scratch("shard-argmax", (size_t)agrid * 16, &scr, st));
+  double* bv = (double*)scr;
+  int64_t* bi = (int64_t*)(bv + agrid);
+  argmax_unpicked<<<agrid, kSelThreads, 0, st>>>(v, n, picked, valid, bv, bi);
+  CNMF_LAUNCH_CHECK();
+  argmax_final<<<1, 32, 0, st>>>(bv, bi, (int)agrid, out_v, out_i);
+  CNMF_LAUNCH_CHECK();
+  return CNMF_OK;
+}
+
+int spa_shard_step(double* W, int64_t n, int s, int64_t ld, const double* v, const uint8_t* picked, double* sq,
+                   cudaStream_t st) {
+  if (s > kMaxS) return fail(CNMF_ERR_ARGUMENT, "SPA supports s <= 128");
+  spa_project_norms<<<sel_grid(n), kSelThreads, 0, st>>>(W, n, s, ld, v, picked, sq);
+  CNMF_LAUNCH_CHECK();
+  return CNMF_OK;
+}
+
+// XRAY on a column shard: scores of every local column against the
+// residual column rj (an s-vector), denominators, NNLS right factor and
+// residual refit against k picked columns given explicitly (P: k x ld fp64).
+int xray_shard_scores(const double* W, int64_t n, int s, int64_t ld, const double* rj, const double* denom,
+                      double* score, cudaStream_t st) {
+  xray_scores<<<sel_grid(n), kSelThreads, 0, st>>>(W, rj, n, s, ld, nullptr, denom, score);
+  CNMF_LAUNCH_CHECK();
+  return CNMF_OK;
+}
+
+int col_mass_denoms(const double* W, int64_t n, int s, int64_t ld, const double* mass, double* denom, cudaStream_t st) {
+  col_mass<<<sel_grid(n), kSelThreads, 0, st>>>(W, n, s, ld, mass, denom);
+  CNMF_LAUNCH_CHECK();
+  return CNMF_OK;
+}
+
+int right_factor_given(const double* W, int64_t n, int s, int64_t ld, const double* P, int k, double tol, double* Ht,
+                       int64_t* n_capped, cudaStream_t st) {
+  if (k < 1 || k > 64 || s > kMaxS) return fail(CNMF_ERR_ARGUMENT, "right factor: 1 <= k <= 64, s <= 128");
+  void* scr = nullptr;
+  CNMF_TRY(device_scratch("right-factor-given", ((size_t)k * k + (size_t)n * k) * 8, &scr, st));
+  double* gram = (double*)scr;
+  double* target = gram + (size_t)k * k;
+  CNMF_TRY(ensure_smem_attr((const void*)gather_gram, 200 * 1024));
+  gather_gram<<<sel_grid(n), kSelThreads, (size_t)k * s * 8, st>>>(W, n, s, ld, P, nullptr, k, gram, target);
+  CNMF_LAUNCH_CHECK();
+  return nnls_gram(gram, target, n, k, tol, 0, Ht, n_capped, st);
+}
+
+int refit_given(const double* W, int64_t n, int s, int64_t ld, const double* P, int k, const double* Ht, double* R,
+                double* sq, double* tot, cudaStream_t st) {
+  CNMF_TRY(ensure_smem_attr((const void*)refit_residual, 200 * 1024));
+  if (tot) CNMF_CUDA(cudaMemsetAsync(tot, 0, 16, st));
+  refit_residual<<<sel_grid(n), kSelThreads, (size_t)std::max(k, 1) * s * 8, st>>>(W, n, s, ld, P, nullptr, k, Ht,
+                                                                                    R, sq, tot);
+  CNMF_LAUNCH_CHECK();
+  return CNMF_OK;
+}
+
 int panel_to_f64(const float* src, int64_t rows, int S, double* dst, int64_t ld, cudaStream_t st) {
   const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(rows * S, 256), 8 * kNumSMs);
   f32_to_f64_panel<<<grid, 256, 0, st>>>(src, rows, S, dst, ld);
@@ -367,7 +489,7 @@ int right_factor(const double* W, int64_t n, int s, int64_t ld, const int64_t* d
     CNMF_CUDA(cudaFuncSetAttribute(gather_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  gather_gram<<<sel_grid(n), kSelThreads, sm, st>>>(W, n, s, ld, d_picks, k, gram, target);
+  gather_gram<<<sel_grid(n), kSelThreads, sm, st>>>(W, n, s, ld, W, d_picks, k, gram, target);
   CNMF_LAUNCH_CHECK();
   return nnls_gram(gram, target, n, k, tol, 0, Ht, n_capped, st);
 }
@@ -381,7 +503,8 @@ int refit_norms(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_
     attr = true;
   }
   if (tot) CNMF_CUDA(cudaMemsetAsync(tot, 0, 16, st));
-  refit_residual<<<sel_grid(n), kSelThreads, (size_t)k * s * 8, st>>>(W, n, s, ld, d_picks, k, Ht, R, sq_out, tot);
+  refit_residual<<<sel_grid(n), kSelThreads, (size_t)k * s * 8, st>>>(W, n, s, ld, W, d_picks, k, Ht, R, sq_out,
+                                                                      tot);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }

@@ -31,7 +31,7 @@
 //               so D = [A_hi X_hi | A_hi X_lo + A_lo X_hi]; one
 //               tcgen05.commit per K tile releases the TMEM A slot and the
 //               panel slot together.
-//   warps 10..  epilogue: the tensor core accumulates at most KB = 4 K tiles
+//   warps 10..  epilogue: the tensor core accumulates at most KB = 2 K tiles
 //               into a double-buffered TMEM accumulator, the partial sums
 //               move to fp32 registers (round-to-nearest adds), so the error
 //               does not grow with the tensor-core accumulation chain.
@@ -58,7 +58,12 @@ constexpr int BMT = 128;  // output rows per tile (TMEM lanes)
 constexpr int BKT = 32;   // K per stage (one 128B swizzle atom of fp32)
 constexpr int NSPL = 8;   // splitter warps (2 per TMEM lane quarter; 8 panel K chunks)
 #ifndef CNMF_PASS_KB
-#define CNMF_PASS_KB 4
+#define CNMF_PASS_KB 2
+#endif
+#ifdef CNMF_PASS_ACC64
+using acc_t = double;
+#else
+using acc_t = float;
 #endif
 #ifndef CNMF_PASS_NACC
 #define CNMF_PASS_NACC 2
@@ -394,9 +399,9 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
     const int cg = 32 * ((warp - kWarpEpi0) >> 2);  // first output column of this warp
     const int row_in_tile = 32 * q + lane;
     Ring<C::NACC> racc;
-    float acc[32];
+    acc_t acc[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+    for (int j = 0; j < 32; ++j) acc[j] = 0.0;
     Walk w;
     w.start(lo0, hi0, lo1, hi1, s0, s1);
     // one iteration per accumulation block (<= KB K tiles of one output tile)
@@ -415,7 +420,7 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
         tmem_ld8(taddr + c0, vh);
         tmem_ld8(taddr + S + c0, vl);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[c0 + j] += vh[j] + vl[j];
+        for (int j = 0; j < 8; ++j) acc[c0 + j] += (acc_t)(vh[j] + vl[j]);
       }
       tc_fence_before();
       __syncwarp();
@@ -438,14 +443,16 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
           float* dst = sd.out + row * S + cg;
           if (owned) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) *(float4*)(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            for (int j = 0; j < 32; j += 4)
+              *(float4*)(dst + j) = make_float4((float)acc[j], (float)acc[j + 1], (float)acc[j + 2], (float)acc[j + 3]);
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) red_add_v4(dst + j, acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            for (int j = 0; j < 32; j += 4)
+              red_add_v4(dst + j, (float)acc[j], (float)acc[j + 1], (float)acc[j + 2], (float)acc[j + 3]);
           }
         }
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+        for (int j = 0; j < 32; ++j) acc[j] = 0.0;
       }
       w.skip(len, s0, s1);
       it += len;

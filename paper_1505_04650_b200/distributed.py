@@ -14,13 +14,19 @@ One process per GPU; rank i owns the column shard A[:, c0 : c0 + n_i]
   row-sharded panel all-reduces the S x S Gram matrix, factors it on every
   rank and applies R^{-1} locally;
 * core L^T A R^T = sum_i (L^T A_i) R_i^T: one S x S all-reduce;
-* the ADMM (nmf.py:334-377) acts on O((m + n) r) compressed state and runs
-  replicated after one all-gather of R^T; the final ||A - X Y||_F is two
-  scalars all-reduced;
-* SNMF: the reduced matrix Q^T A (s x n) is gathered once (s * n values, far
-  smaller than A) and the column selection runs replicated -- one collective
-  instead of an all-reduce of (norm, index) plus a broadcast per pick; the
-  picked columns of A are assembled with one all-reduce for the full error.
+* ADMM (nmf.py:334-377), `admm`: U and dU are row-sharded (rank i updates the
+  rows of its row block of L), V^T and dV^T follow the column shards (the rows
+  of R_i^T); per iteration every rank sweeps its rows and the s x r reduced
+  sums L_i^T U_i, L_i^T dU_i, R_i V_i^T, R_i dV_i^T plus the KKT sums are ONE
+  all-reduce of 2 (2 s r + 4) doubles; the core step (KKT score, stopping
+  rule, the two r x r ridge solves) runs replicated on identical inputs;
+* SNMF (snmf.py:154-232), `snmf`: the reduced matrix stays column-sharded
+  ((Q^T A_i)^T on rank i); every SPA / XRAY pick is an all-gather of the
+  ranks' (score, global index) pairs -- ties to the lowest index, like
+  numpy.argmax -- and the owner of the pick broadcasts the one s-vector
+  everybody needs (the normalised column for SPA; the residual column and
+  the picked column for XRAY); the NNLS right factor is column-local; the
+  full-space error gathers the k picked columns of A once.
 
 Collectives go through `Comm` (torch.distributed: NCCL between GPUs, gloo in
 the CPU tests); local arithmetic through an ops object -- `DeviceOps` (the C
@@ -34,6 +40,7 @@ import torch
 import torch.distributed as dist
 
 from .compress import OMEGA_CHUNK, CompressionConfig, adjust_config
+from .errors import ConvergenceError, RankDeficiencyError, UndefinedMetricError
 from .rng import child_seed
 
 
@@ -57,6 +64,31 @@ class Comm:
         if self.world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
+
+    def allreduce_max(self, t):
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return t
+
+    def best_pair(self, val, idx):
+        """Global (max value, lowest index among the maxima) over the ranks'
+        local (value, global index) pairs -- numpy.argmax's tie rule."""
+        pair = torch.tensor([float(val), float(idx)], dtype=torch.float64, device=self._dev())
+        if self.world == 1:
+            return float(val), int(idx)
+        parts = [torch.empty_like(pair) for _ in range(self.world)]
+        dist.all_gather(parts, pair, group=self.group)
+        best_v, best_i = None, None
+        for p in parts:
+            v, i = float(p[0]), int(p[1])
+            if best_v is None or v > best_v or (v == best_v and i < best_i):
+                best_v, best_i = v, i
+        return best_v, best_i
+
+    def _dev(self):
+        if dist.is_initialized() and dist.get_backend(self.group) == "nccl":
+            return torch.device("cuda", torch.cuda.current_device())
+        return torch.device("cpu")
 
     def allgather_rows(self, t, counts):
         """Concatenate every rank's (counts[k] x ...) block in rank order."""
@@ -153,17 +185,103 @@ class DeviceOps:
         self._lib.call("cnmf_panel_apply", P.data_ptr(), P.shape[0], S, T.data_ptr(), self._st())
         return P
 
-    def admm(self, core, left, m, right, n, cfg, r, **kw):
-        from .nmf import run_admm
-
-        return run_admm(core, left, m, right, n, cfg, r, **kw)
-
     def residual(self, A, X, Yt):
         """(||A - X Y||^2, ||A||^2) over the local shard, fp64 device vector."""
         res = self.zeros((2,), torch.float64)
         self._lib.call("cnmf_residual_norms", A.ptr, A.m, A.n, A.lda, X.data_ptr(), None, Yt.data_ptr(),
                        X.shape[1], res.data_ptr(), self._st())
         return res
+
+    # ---- sharded ADMM (include/cnmf_b200.h, "column-sharded multi-GPU") ----
+    def uniform(self, seed, start, rows, cols, transpose=False):
+        """Rows of the seeded U[0, 1) stream from raw position `start`
+        (rng.py:63; nmf.py:337-339's splits, any row block)."""
+        t = self.zeros((cols, rows) if transpose else (rows, cols), torch.float64)
+        self._lib.call("cnmf_uniform_fill_at", seed, start, rows, cols, 0.0, 1.0, 1, int(bool(transpose)),
+                       t.data_ptr(), self._st())
+        return t
+
+    def admm_shard_begin(self, s, r):
+        nb = int(self.lib.cnmf_admm_shard_workspace(s, r))
+        ws = torch.zeros(nb // 8, dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+        self._lib.call("cnmf_admm_shard_begin", ws.data_ptr(), s, r, self._st())
+        off = int(self.lib.cnmf_admm_shard_sums_offset()) // 8
+        return {"ws": ws, "sums": ws[off: off + 2 * (2 * s * r + 4)]}
+
+    def admm_shard_sweep(self, st, L, Rt, u, du, vt, dvt, s, r, pu, pv, step, update):
+        self._lib.call("cnmf_admm_shard_sweep", st["ws"].data_ptr(), L.data_ptr(), L.shape[0], Rt.data_ptr(),
+                       Rt.shape[0], s, r, u.data_ptr(), du.data_ptr(), vt.data_ptr(), dvt.data_ptr(), float(pu),
+                       float(pv), float(step), int(update), self._st())
+        return st["sums"]
+
+    def admm_shard_core(self, st, core, xc, yc, s, r, pu, pv, tol, trace, scores, k, max_iter, first, solve):
+        self._lib.call("cnmf_admm_shard_core", st["ws"].data_ptr(), core.data_ptr(), xc.data_ptr(), yc.data_ptr(), s,
+                       r, float(pu), float(pv), float(tol), trace.data_ptr(), scores.data_ptr(), int(k),
+                       int(max_iter), int(first), int(solve), self._st())
+
+    def admm_shard_status(self, st):
+        import ctypes
+
+        h = (ctypes.c_int * 4)()
+        self._lib.call("cnmf_admm_shard_status", st["ws"].data_ptr(), h, self._st())
+        return int(h[0]), int(h[1]), int(h[2]), int(h[3])
+
+    # ---- sharded column selection ----
+    def to_f64(self, Z, S):
+        W = self.zeros((Z.shape[0], S), torch.float64)
+        self._lib.call("cnmf_panel_to_f64", Z.data_ptr(), Z.shape[0], S, W.data_ptr(), S, self._st())
+        return W
+
+    def picked_mask(self, n):
+        return torch.zeros(n, dtype=torch.uint8, device=torch.device("cuda", torch.cuda.current_device()))
+
+    def argmax(self, v, picked, valid=None):
+        out = self.zeros((2,), torch.float64)
+        idx = torch.zeros(1, dtype=torch.int64, device=out.device)
+        self._lib.call("cnmf_shard_argmax", v.data_ptr(), v.shape[0], picked.data_ptr(),
+                       valid.data_ptr() if valid is not None else None, out.data_ptr(), idx.data_ptr(), self._st())
+        return float(out[0]), int(idx[0])
+
+    def spa_step(self, W, s, v, picked):
+        sq = self.zeros((W.shape[0],), torch.float64)
+        self._lib.call("cnmf_spa_shard_step", W.data_ptr(), W.shape[0], s, W.shape[1],
+                       v.data_ptr() if v is not None else None, picked.data_ptr(), sq.data_ptr(), self._st())
+        return sq
+
+    def col_mass(self, W, s, mass):
+        d = self.zeros((W.shape[0],), torch.float64)
+        self._lib.call("cnmf_col_mass", W.data_ptr(), W.shape[0], s, W.shape[1], mass.data_ptr(), d.data_ptr(),
+                       self._st())
+        return d
+
+    def xray_scores(self, W, s, rj, denom):
+        sc = self.zeros((W.shape[0],), torch.float64)
+        self._lib.call("cnmf_xray_shard_scores", W.data_ptr(), W.shape[0], s, W.shape[1], rj.data_ptr(),
+                       denom.data_ptr(), sc.data_ptr(), self._st())
+        return sc
+
+    def right_factor_given(self, W, s, P, k, tol):
+        import ctypes
+
+        Ht = self.zeros((W.shape[0], k), torch.float64)
+        capped = ctypes.c_int64(0)
+        self._lib.call("cnmf_right_factor_given", W.data_ptr(), W.shape[0], s, W.shape[1], P.data_ptr(), k,
+                       float(tol), Ht.data_ptr(), ctypes.byref(capped), self._st())
+        return Ht, int(capped.value)
+
+    def refit_given(self, W, s, P, k, Ht, R=None):
+        sq = self.zeros((W.shape[0],), torch.float64)
+        tot = self.zeros((2,), torch.float64)
+        self._lib.call("cnmf_refit_given", W.data_ptr(), W.shape[0], s, W.shape[1], P.data_ptr(), k,
+                       Ht.data_ptr() if Ht is not None else None, R.data_ptr() if R is not None else None,
+                       sq.data_ptr(), tot.data_ptr(), self._st())
+        return sq, tot
+
+    def columns_f64(self, A, idx):
+        """A[:, idx] of the local shard as fp64 (m x len(idx))."""
+        if len(idx) == 0:
+            return self.zeros((A.m, 0), torch.float64)
+        return A.t[:, torch.as_tensor(idx, device=A.t.device)].double()
 
 
 def orthonormalize_sharded(ops, comm, P, s, S):
@@ -211,6 +329,62 @@ def compressed_problem(ops, comm, A, m, n, c0, cfg):
     return left, right, core[:s, :s].contiguous()
 
 
+def admm(ops, comm, core, left, m, right_local, n, c0, cfg, r, penalty_u=1.0, penalty_v=1.0, step_scale=1.0,
+         max_iter=500, tol=1e-4, check_every=25):
+    """Sharded compressed ADMM (nmf.py:334-377). `left` is the replicated
+    left basis (m x S), `right_local` this rank's rows of R^T (n_i x S).
+    Rank i updates U rows [m0, m0 + m_i) (`column_shard(m, ...)`) and its
+    V^T rows; one all-reduce of the reduced sums per iteration. Returns
+    (U m x r assembled on every rank, V^T local rows, iterations, trace)."""
+    s = cfg.basis_cols
+    m0, mi = column_shard(m, comm.world, comm.rank)
+    ni = right_local.shape[0]
+    L_loc = left[m0: m0 + mi].contiguous()
+    # the seeded U[0, 1) starts (nmf.py:337-339): this rank's U rows are
+    # positions [m0 r, (m0 + m_i) r) of the init-left stream; V^T rows of the
+    # local columns are taken from the (small) full n x r draw
+    u = ops.uniform(child_seed(cfg.seed, "init-left"), m0 * r, mi, r)
+    vt = ops.uniform(child_seed(cfg.seed, "init-right"), 0, r, n, transpose=True)[c0: c0 + ni].contiguous()
+    du = ops.zeros((mi, r), torch.float64)
+    dvt = ops.zeros((ni, r), torch.float64)
+    xc = ops.zeros((s, r), torch.float64)
+    yc = ops.zeros((r, s), torch.float64)
+    trace = ops.zeros((max(max_iter, 1),), torch.float64)
+    scores = ops.zeros((max(max_iter, 1),), torch.float64)
+    st = ops.admm_shard_begin(s, r)
+    args = (L_loc, right_local, u, du, vt, dvt, s, r, penalty_u, penalty_v, step_scale)
+    comm.allreduce(ops.admm_shard_sweep(st, *args, update=0))  # L^T U, V R^T of the start
+    for k in range(max_iter):
+        ops.admm_shard_core(st, core, xc, yc, s, r, penalty_u, penalty_v, tol, trace, scores, k, max_iter,
+                            first=(k == 0), solve=1)
+        comm.allreduce(ops.admm_shard_sweep(st, *args, update=1))
+        if check_every and (k + 1) % check_every == 0 and ops.admm_shard_status(st)[1]:
+            break  # every rank takes the same decision (identical all-reduced inputs)
+    ops.admm_shard_core(st, core, xc, yc, s, r, penalty_u, penalty_v, tol, trace, scores, max_iter, max_iter,
+                        first=False, solve=False)
+    _, done, iters, diverged = ops.admm_shard_status(st)
+    if not done:
+        iters = max_iter
+    if diverged >= 0:
+        from .errors import DivergenceError
+
+        raise DivergenceError(f"KKT residual grew 10x over 50 iterations at iteration {diverged}",
+                              trace=scores[: diverged + 1].tolist())
+    counts = [column_shard(m, comm.world, k)[1] for k in range(comm.world)]
+    u_full = comm.allgather_rows(u, counts)
+    return u_full, vt, iters, trace[:iters].tolist()
+
+
+def rel_error(ops, comm, A, u, vt_local):
+    """||A - U V||_F / ||A||_F over the column shards (nmf.py:53-75): two
+    scalars all-reduced."""
+    res = comm.allreduce(ops.residual(A, u, vt_local))
+    num, den = (float(x) for x in res.tolist())
+    if den == 0.0:
+        raise UndefinedMetricError("relative error undefined: ||A||_F is zero")
+    return float(np.sqrt(max(num, 0.0) / den))
+
+
 def nmf_admm(A, m, n, c0, r, cfg=None, comm=None, ops=None, penalty_u=1.0, penalty_v=1.0, step_scale=1.0,
              max_iter=500, tol=1e-4):
     """Column-sharded compressed ADMM NMF (nmf.py:306-377). `A` is this
@@ -222,15 +396,9 @@ def nmf_admm(A, m, n, c0, r, cfg=None, comm=None, ops=None, penalty_u=1.0, penal
         cfg = CompressionConfig(r=r, r_ov=10, w=4, seed=0)
     cfg = adjust_config(cfg, m, n)
     left, right_local, core = compressed_problem(ops, comm, A, m, n, c0, cfg)
-    counts = [column_shard(n, comm.world, k)[1] for k in range(comm.world)]
-    right = comm.allgather_rows(right_local, counts)
-    u, vt, iters, trace = ops.admm(core, left, m, right, n, cfg, r, penalty_u=penalty_u, penalty_v=penalty_v,
-                                   step_scale=step_scale, max_iter=max_iter, tol=tol)
-    vt_local = vt[c0: c0 + A.n].contiguous()
-    res = comm.allreduce(ops.residual(A, u, vt_local))
-    num, den = (float(x) for x in res.tolist())
-    rel = float(np.sqrt(max(num, 0.0) / den)) if den > 0 else float("nan")
-    return u, vt_local, iters, trace, rel
+    u, vt_local, iters, trace = admm(ops, comm, core, left, m, right_local, n, c0, cfg, r, penalty_u, penalty_v,
+                                     step_scale, max_iter, tol)
+    return u, vt_local, iters, trace, rel_error(ops, comm, A, u, vt_local)
 
 
 def reduced_matrix(ops, comm, A, m, n, c0, cfg):
@@ -241,3 +409,145 @@ def reduced_matrix(ops, comm, A, m, n, c0, cfg):
     counts = [column_shard(n, comm.world, k)[1] for k in range(comm.world)]
     W = comm.allgather_rows(ops.transpose(A, Q, S), counts)
     return Q, W
+
+
+# ------------------------------------------------------------ selection ----
+
+def _owner_row(comm, W, gidx, c0, width):
+    """Row `gidx` (global) of the column-sharded W, replicated: the owner
+    contributes it, the others zeros, one all-reduce."""
+    buf = torch.zeros(width, dtype=W.dtype, device=W.device)
+    loc = gidx - c0
+    if 0 <= loc < W.shape[0]:
+        buf.copy_(W[loc, :width])
+    return comm.allreduce(buf)
+
+
+def select_spa(ops, comm, W, s, r, c0, n):
+    """Sharded SPA (snmf.py:39-71) on the local rows of (Q^T A)^T; W is
+    projected in place. Picks in order, global column indices."""
+    if not 1 <= r <= min(s, n):
+        from .errors import ArgumentError
+
+        raise ArgumentError(f"cannot pick {r} columns from a {s}x{n} matrix")
+    picked = ops.picked_mask(W.shape[0])
+    sq = ops.spa_step(W, s, None, picked)
+    smax = comm.allreduce_max(torch.tensor([float(sq.max()) if sq.numel() else 0.0], dtype=torch.float64,
+                                           device=comm._dev()))
+    floor = (np.sqrt(float(smax[0])) * 1e-14) ** 2
+    picks = []
+    for _ in range(r):
+        v, j = ops.argmax(sq, picked) if sq.numel() else (-1.0, 0)
+        v, g = comm.best_pair(v, c0 + j)
+        if not v > floor:
+            raise RankDeficiencyError(f"only {len(picks)} numerically independent columns found", picks=picks)
+        picks.append(g)
+        col = _owner_row(comm, W, g, c0, W.shape[1])
+        if 0 <= g - c0 < W.shape[0]:
+            picked[g - c0] = 1
+        vec = (col / np.sqrt(v)).contiguous()
+        sq = ops.spa_step(W, s, vec, picked)
+    return np.asarray(picks, dtype=np.int64)
+
+
+def select_xray(ops, comm, W, s, r, c0, n, mass, nnls_tol=1e-10):
+    """Sharded XRAY (snmf.py:74-126): per pick, the argmax of the residual
+    norms and of the scores are all-gathers of (value, global index); the
+    owner broadcasts the residual column and the picked column; the NNLS refit
+    of every column is local. Returns (picks, P: the picked columns, k x S)."""
+    if not 1 <= r <= min(s, n):
+        from .errors import ArgumentError
+
+        raise ArgumentError(f"cannot pick {r} columns from a {s}x{n} matrix")
+    S = W.shape[1]
+    dev = comm._dev()
+    picked = ops.picked_mask(W.shape[0])
+    denom = ops.col_mass(W, s, mass)
+    dmax = comm.allreduce_max(torch.tensor([float(denom.abs().max()) if denom.numel() else 0.0],
+                                           dtype=torch.float64, device=dev))
+    scorable = (denom > 1e-14 * max(float(dmax[0]), 1.0)).to(torch.uint8)
+    P = torch.zeros((max(r, 1), S), dtype=torch.float64, device=W.device)
+    R = W.clone()
+    sq, _ = ops.refit_given(W, s, P, 0, None, R)
+    smax = comm.allreduce_max(torch.tensor([float(sq.max()) if sq.numel() else 0.0], dtype=torch.float64,
+                                           device=dev))
+    floor = (np.sqrt(float(smax[0])) * 1e-14) ** 2
+    picks = []
+    for t in range(r):
+        v, j = ops.argmax(sq, picked) if sq.numel() else (-1.0, 0)
+        v, gj = comm.best_pair(v, c0 + j)
+        if not v > floor:
+            raise RankDeficiencyError(f"only {len(picks)} numerically independent columns found", picks=picks)
+        rj = _owner_row(comm, R, gj, c0, S)
+        score = ops.xray_scores(W, s, rj, denom)
+        v, i = ops.argmax(score, picked, scorable) if score.numel() else (-np.inf, 0)
+        v, gi = comm.best_pair(v, c0 + i)
+        if not (np.isfinite(v) and v > -1.7e308):
+            raise RankDeficiencyError("no scorable columns left", picks=picks)
+        picks.append(gi)
+        P[t].copy_(_owner_row(comm, W, gi, c0, S))
+        if 0 <= gi - c0 < W.shape[0]:
+            picked[gi - c0] = 1
+        Ht, _ = ops.right_factor_given(W, s, P, t + 1, nnls_tol)
+        sq, _ = ops.refit_given(W, s, P, t + 1, Ht, R)
+    return np.asarray(picks, dtype=np.int64), P[: len(picks)]
+
+
+def snmf(ops, comm, A, m, n, c0, r, selector="spa", cfg=None, nnls_tol=1e-10, host_out=False):
+    """Column-sharded compressed SNMF (snmf.py:154-232): the replicated basis,
+    the reduced matrix kept column-sharded, sharded SPA / XRAY, the NNLS right
+    factor of the local columns, both relative errors all-reduced. Returns a
+    SnmfResult with the picks, Y (all columns, gathered) and the errors."""
+    from .snmf import SnmfResult
+
+    if selector not in ("spa", "xray"):
+        from .errors import ArgumentError
+
+        raise ArgumentError(f"unknown selector {selector!r}")
+    if cfg is None:
+        cfg = CompressionConfig(r=r, r_ov=10, w=0, seed=0)
+    cfg = adjust_config(cfg, m, n)
+    s = cfg.basis_cols
+    Q = range_finder(ops, comm, A, m, n, c0, cfg, 0)
+    S = Q.shape[1]
+    W = ops.to_f64(ops.transpose(A, Q, S), S)  # local rows of (Q^T A)^T
+    if selector == "spa":
+        picks = select_spa(ops, comm, W.clone(), s, r, c0, n)
+        P = torch.stack([_owner_row(comm, W, int(g), c0, S) for g in picks])
+    else:
+        mass = ops.cross(Q, _ones_panel(ops, Q), S)[:, 0].contiguous()  # Q^T 1 (snmf.py:151, 158)
+        picks, P = select_xray(ops, comm, W, s, r, c0, n, mass, nnls_tol)
+    k = len(picks)
+    Ht, capped = ops.right_factor_given(W, s, P, k, nnls_tol)
+    capped_all = comm.allreduce(torch.tensor([float(capped)], dtype=torch.float64, device=comm._dev()))
+    counts = [column_shard(n, comm.world, q)[1] for q in range(comm.world)]
+    if float(capped_all[0]):
+        err = ConvergenceError(f"active-set exchange cap {3 * k} exceeded",
+                               best=comm.allgather_rows(Ht, counts).t().cpu().numpy())
+        err.picks = picks
+        raise err
+    _, tot = ops.refit_given(W, s, P, k, Ht, None)
+    tot = comm.allreduce(tot)
+    res_red, ref_red = (float(x) for x in tot.tolist())
+    if ref_red == 0.0:
+        raise UndefinedMetricError("reduced matrix has zero norm")
+    # full-space error: the picked columns of A, gathered once (m x k)
+    own = [int(g) - c0 for g in picks if 0 <= int(g) - c0 < A.n]
+    AK = ops.zeros((A.m, k), torch.float64)
+    if own:
+        cols = ops.columns_f64(A, own)
+        pos = [t for t, g in enumerate(picks) if 0 <= int(g) - c0 < A.n]
+        AK[:, pos] = cols
+    AK = comm.allreduce(AK)
+    full = comm.allreduce(ops.residual(A, AK, Ht))
+    res_f, ref_f = (float(x) for x in full.tolist())
+    Y = comm.allgather_rows(Ht, counts).t().contiguous()
+    return SnmfResult(K=np.asarray(picks, dtype=np.int64), Y=Y.cpu().numpy() if host_out else Y,
+                      rel_error_reduced=float(np.sqrt(max(res_red, 0.0) / ref_red)),
+                      rel_error_full=float(np.sqrt(max(res_f, 0.0) / ref_f)) if ref_f else 0.0)
+
+
+def _ones_panel(ops, Q):
+    o = ops.zeros(tuple(Q.shape), Q.dtype)
+    o[:, 0] = 1.0
+    return o

@@ -81,16 +81,126 @@ class NumpyOps:
         P.copy_(P @ T)
         return P
 
-    def admm(self, core, left, m, right, n, cfg, r, penalty_u, penalty_v, step_scale, max_iter, tol):
-        s = cfg.basis_cols
-        u, v, it, trace, _ = O.admm_compressed(core.numpy(), left[:, :s].numpy(), right[:, :s].numpy().T, m, n, r,
-                                               O.Config(cfg.r, cfg.r_ov, cfg.w, cfg.seed), penalty_u, penalty_v,
-                                               step_scale, max_iter, tol)
-        return torch.from_numpy(u), torch.from_numpy(np.ascontiguousarray(v.T)), it, trace
-
     def residual(self, A, X, Yt):
         d = A.a - X.numpy() @ Yt.numpy().T
         return torch.tensor([float((d * d).sum()), float((A.a * A.a).sum())], dtype=torch.float64)
+
+    # ---- sharded ADMM: the phases of nmf.py:334-377 in numpy ----
+    def uniform(self, seed, start, rows, cols, transpose=False):
+        g = O.generator(seed)
+        g.bit_generator.advance(start // 4)
+        g.bit_generator.random_raw(start % 4)
+        x = g.uniform(0.0, 1.0, size=(rows, cols))
+        return torch.from_numpy(np.ascontiguousarray(x.T) if transpose else x)
+
+    def admm_shard_begin(self, s, r):
+        return {"s": s, "r": r, "k": 0, "done": 0, "iters": 0, "div": -1,
+                "sums": torch.zeros(2 * (2 * s * r + 4), dtype=torch.float64), "xc": None, "yc": None}
+
+    def admm_shard_sweep(self, st, L, Rt, u, du, vt, dvt, s, r, pu, pv, step, update):
+        if update and st["done"]:
+            return st["sums"]
+        out = []
+        for P, x, dx, z, pen in ((L, u, du, st["xc"], pu), (Rt, vt, dvt, None if st["yc"] is None else st["yc"].T, pv)):
+            Pn = P[:, :s].numpy()
+            if update:
+                lx = Pn @ z
+                xn = np.maximum(lx + dx.numpy() / pen, 0.0)
+                dxn = dx.numpy() + step * pen * (lx - xn)
+                x.copy_(torch.from_numpy(xn))
+                dx.copy_(torch.from_numpy(dxn))
+                kkt = [float(((lx - xn) ** 2).sum()), float(((dxn * xn) ** 2).sum()),
+                       float((np.maximum(dxn, 0) ** 2).sum()), float((np.maximum(-xn, 0) ** 2).sum())]
+            else:
+                kkt = [0.0] * 4
+            out += [(Pn.T @ x.numpy()).ravel(), (Pn.T @ dx.numpy()).ravel(), np.array(kkt)]
+        st["sums"].copy_(torch.from_numpy(np.concatenate(out)))
+        return st["sums"]
+
+    def admm_shard_core(self, st, core, xc, yc, s, r, pu, pv, tol, trace, scores, k, max_iter, first, solve):
+        if st["done"]:
+            return
+        sr, ln = s * r, 2 * s * r + 4
+        sm = st["sums"].numpy()
+        lu, ldu, lk = sm[:sr].reshape(s, r), sm[sr:2 * sr].reshape(s, r), sm[2 * sr:ln]
+        rv, rdv, rk = sm[ln:ln + sr].reshape(s, r), sm[ln + sr:ln + 2 * sr].reshape(s, r), sm[ln + 2 * sr:]
+        cm = core.numpy()
+        if first:
+            st["yc"] = rv.T.copy()
+        elif k > 0:
+            x_, y_ = st["xc"], st["yc"]
+            e = x_ @ y_ - cm
+            sc = max(np.linalg.norm(e @ y_.T + ldu), np.linalg.norm(x_.T @ e + rdv.T), np.sqrt(lk[0]),
+                     np.sqrt(rk[0]), np.sqrt(lk[1] + lk[2] + lk[3]), np.sqrt(rk[1] + rk[2] + rk[3]))
+            trace[k - 1] = float((e * e).sum())
+            scores[k - 1] = sc
+            st["k"] = k
+            if sc < tol or k >= max_iter:
+                st["done"], st["iters"] = 1, k
+                return
+            if k - 1 >= 50 and sc > 10.0 * float(scores[k - 51]):
+                st["div"], st["done"], st["iters"] = k - 1, 1, k
+                return
+        if not solve or k >= max_iter:
+            return
+        eye = np.eye(r)
+        y_ = st["yc"]
+        x_ = np.linalg.solve(y_ @ y_.T + pu * eye, (cm @ y_.T + pu * lu - ldu).T).T
+        y_ = np.linalg.solve(x_.T @ x_ + pv * eye, x_.T @ cm + pv * rv.T - rdv.T)
+        st["xc"], st["yc"] = x_, y_
+        xc.copy_(torch.from_numpy(x_))
+        yc.copy_(torch.from_numpy(y_))
+
+    def admm_shard_status(self, st):
+        return st["k"], st["done"], st["iters"], st["div"]
+
+    # ---- sharded selection ----
+    def to_f64(self, Z, S):
+        return Z.clone().double()
+
+    def picked_mask(self, n):
+        return torch.zeros(n, dtype=torch.uint8)
+
+    def argmax(self, v, picked, valid=None):
+        x = v.numpy().copy()
+        p = picked.numpy().astype(bool)
+        if valid is None:
+            x[p] = 0.0
+        else:
+            x[p | ~valid.numpy().astype(bool)] = -np.finfo(np.float64).max
+        j = int(np.argmax(x))
+        return float(x[j]), j
+
+    def spa_step(self, W, s, v, picked):
+        w = W[:, :s].numpy()
+        if v is not None:
+            vv = v[:s].numpy()
+            w -= np.outer(w @ vv, vv)
+        sq = (w * w).sum(axis=1)
+        sq[picked.numpy().astype(bool)] = 0.0
+        return torch.from_numpy(sq)
+
+    def col_mass(self, W, s, mass):
+        return torch.from_numpy(W[:, :s].numpy() @ mass[:s].numpy())
+
+    def xray_scores(self, W, s, rj, denom):
+        return torch.from_numpy((W[:, :s].numpy() @ rj[:s].numpy()) / denom.numpy())
+
+    def right_factor_given(self, W, s, P, k, tol):
+        c = P[:k, :s].numpy().T
+        h = O.nnls(c, W[:, :s].numpy().T, tol=tol)
+        return torch.from_numpy(np.ascontiguousarray(h.T)), 0
+
+    def refit_given(self, W, s, P, k, Ht, R=None):
+        w = W[:, :s].numpy()
+        res = w - (Ht.numpy() @ P[:k, :s].numpy() if k else 0.0)
+        if R is not None:
+            R[:, :s] = torch.from_numpy(res)
+        sq = (res * res).sum(axis=1)
+        return torch.from_numpy(sq), torch.tensor([float(sq.sum()), float((w * w).sum())], dtype=torch.float64)
+
+    def columns_f64(self, A, idx):
+        return torch.from_numpy(A.a[:, idx])
 
 
 def _free_port():
@@ -120,6 +230,10 @@ def _jobs(rank, world, a, a_sep):
     cfg = adjust_config(CompressionConfig(r=4, r_ov=6, w=2, seed=11), m, n)
     Q, W = D.reduced_matrix(ops, comm, A, m, n, c0, cfg)
     res["snmf"] = (O.spa(W[:, : cfg.basis_cols].numpy().T, 4), Q[:, : cfg.basis_cols].numpy())
+    for sel in ("spa", "xray"):
+        out = D.snmf(ops, comm, A, m, n, c0, 4, selector=sel, cfg=CompressionConfig(r=4, r_ov=6, w=2, seed=11),
+                     host_out=True)
+        res["dsnmf_" + sel] = (out.K, out.Y, out.rel_error_reduced, out.rel_error_full)
     return res
 
 
@@ -204,3 +318,22 @@ def test_sharded_reduced_matrix_spa_matches_oracle(sharded):
     ref = O.snmf(a, 4, selector="spa", cfg=O.Config(4, 6, 2, 11))
     np.testing.assert_array_equal(np.sort(picks), np.sort(ref.K))
     np.testing.assert_array_equal(picks, ref.K)
+
+
+@pytest.mark.parametrize("sel", ["spa", "xray"])
+def test_sharded_snmf_matches_oracle(sharded, sel):
+    # column-sharded selection: every pick is an all-gather of (score, global
+    # index) pairs, the NNLS right factor is column-local
+    a = _near_separable()
+    K, Y, rr, rf = sharded["dsnmf_" + sel]
+    ref = O.snmf(a, 4, selector=sel, cfg=O.Config(4, 6, 2, 11))
+    np.testing.assert_array_equal(K, ref.K)
+    np.testing.assert_allclose(Y, ref.Y, rtol=1e-7, atol=1e-9)
+    assert abs(rr - ref.rel_error_reduced) <= 1e-9
+    assert abs(rf - ref.rel_error_full) <= 1e-9
+
+
+def test_best_pair_tie_rule():
+    # (value, global index) all-gather reduction: max value, lowest index
+    c = D.Comm()
+    assert c.best_pair(3.0, 7) == (3.0, 7)
