@@ -176,11 +176,18 @@ def gaussian_compress(m, s, seed):
     return CompressionBasis(Q=(g / np.sqrt(s)).cpu().numpy(), kind="gaussian", config=cfg)
 
 
+POWER_NORM_SEED = 0x5EC7AA1  # compress.py:23
+
+
 def compression_error(a, basis, norm="frobenius"):
-    """||A - Q Q^T A||_F (compress.py:250-265) from one transpose pass and one
-    fused residual pass over A."""
-    if norm != "frobenius":
-        raise ArgumentError(f"norm {norm!r} is not supported on the device path (use 'frobenius')")
+    """||A - Q Q^T A|| (compress.py:250-265): Frobenius from one transpose
+    pass and one fused residual pass over A; spectral by the reference's power
+    iteration on the residual (compress.py:268-286: at most 100 steps,
+    relative tolerance 1e-6, start vector Rng(0x5EC7AA1).standard_normal(n)),
+    with E v = A v - Q (Z^T v) and E^T u = A^T u - Z (Q^T u), Z = A^T Q, so
+    every step is one forward and one transpose pass of the device kernels."""
+    if norm not in ("frobenius", "spectral"):
+        raise ArgumentError(f"unknown norm {norm!r}")
     A = DeviceMatrix(a)
     qd = as_device64(basis.Q if not isinstance(basis.Q, torch.Tensor) else basis.Q, "Q")
     if qd.shape[0] != A.m:
@@ -191,8 +198,67 @@ def compression_error(a, basis, norm="frobenius"):
     qp[:, :s] = qd.float()
     z = zeros((A.n, S))
     _lib.call("cnmf_pass_transpose", A.ptr, A.m, A.n, A.lda, qp.data_ptr(), s, z.data_ptr(), stream())
+    if norm == "spectral":
+        return _spectral_residual_norm(A, qd, z[:, :s].double())
     zt = z[:, :s].double().contiguous()
     res = zeros((2,), dtype=torch.float64)
     _lib.call("cnmf_residual_norms", A.ptr, A.m, A.n, A.lda, qd.data_ptr(), None, zt.data_ptr(), s,
               res.data_ptr(), stream())
     return float(np.sqrt(max(res[0].item(), 0.0)))
+
+
+def _spectral_residual_norm(A, q, z, max_iter=100, tol=1e-6):
+    """compress.py:268-286 on the device (q: m x s, z = A^T q: n x s, fp64)."""
+    from .rng import Rng
+
+    v = Rng(POWER_NORM_SEED).standard_normal((1, A.n))[0]
+    v = v / torch.linalg.vector_norm(v)
+    vp = zeros((A.n, 32))
+    up = zeros((A.m, 32))
+    av = zeros((A.m, 32))
+    atu = zeros((A.n, 32))
+    sigma = 0.0
+    for _ in range(max_iter):
+        vp[:, 0] = v.float()
+        _lib.call("cnmf_pass_forward", A.ptr, A.m, A.n, A.lda, vp.data_ptr(), 1, av.data_ptr(), stream())
+        u = av[:, 0].double() - q @ (z.t() @ v)
+        new_sigma = float(torch.linalg.vector_norm(u))
+        if new_sigma == 0.0:
+            return 0.0
+        u = u / new_sigma
+        up[:, 0] = u.float()
+        _lib.call("cnmf_pass_transpose", A.ptr, A.m, A.n, A.lda, up.data_ptr(), 1, atu.data_ptr(), stream())
+        w = atu[:, 0].double() - z @ (q.t() @ u)
+        wnorm = float(torch.linalg.vector_norm(w))
+        if wnorm == 0.0:
+            return new_sigma
+        v = w / wnorm
+        if abs(new_sigma - sigma) <= tol * new_sigma:
+            return new_sigma
+        sigma = new_sigma
+    return sigma
+
+
+def canonical_qr(b):
+    """Reduced QR with diag(R) >= 0 (compress.py:136-145) of a tall matrix
+    (rows >= columns <= 128), on the device: CholeskyQR2 of the fp32 panel
+    (csrc/linalg.cu; every transform upper triangular with a positive
+    diagonal, so Q is the sign-canonical factor) and R = Q^T B in fp64."""
+    host = not (isinstance(b, torch.Tensor) and b.is_cuda)
+    B = as_device64(b, "b")
+    m, k = B.shape
+    if k > m:
+        raise ArgumentError(f"canonical_qr needs rows >= columns, got {m}x{k}")
+    S = panel_ld(k)
+    P = zeros((m, S))
+    P[:, :k] = B.float()
+    nb = 2 * S * S * 8 + 256
+    ws = workspace(nb)
+    _lib.call("cnmf_orthonormalize", P.data_ptr(), m, k, None, ws.data_ptr(), nb, stream())
+    Bp = zeros((m, S))
+    Bp[:, :k] = B.float()
+    Rm = zeros((S, S), dtype=torch.float64)
+    _lib.call("cnmf_panel_cross", P.data_ptr(), Bp.data_ptr(), m, S, Rm.data_ptr(), stream())
+    R = torch.triu(Rm[:k, :k]).contiguous()
+    Q = P[:, :k].double().contiguous()
+    return out(Q, host), out(R, host)

@@ -36,6 +36,47 @@ class FactorPair:
 
 
 @dataclass
+class KktResidual:
+    """Norms of the six first-order conditions (nmf.py:246-270); the max is
+    the ADMM's convergence score."""
+
+    grad_left: float
+    grad_right: float
+    feas_left: float
+    feas_right: float
+    comp_left: float
+    comp_right: float
+
+    @property
+    def max_residual(self):
+        return max(self.grad_left, self.grad_right, self.feas_left, self.feas_right, self.comp_left,
+                   self.comp_right)
+
+
+def kkt_residual(state, a_comp, left, right):
+    """The six KKT norms at an ADMM state (nmf.py:273-303); ``left`` / ``right``
+    are the bases (None = identity). A diagnostic: the products run as fp64
+    tensor ops on the device (the ADMM kernels evaluate the same score in
+    csrc/admm*.cu on every iteration)."""
+    def dev(x):
+        return None if x is None else as_device64(x, "state")
+
+    xc, yc, u, v, du, dv = (dev(getattr(state, k)) for k in ("xc", "yc", "u", "v", "dual_u", "dual_v"))
+    ac, L, R = dev(a_comp), dev(left), dev(right)
+    e = xc @ yc - ac
+    ltdu = du if L is None else L.t() @ du
+    dvrt = dv if R is None else dv @ R.t()
+    lxc = xc if L is None else L @ xc
+    ycr = yc if R is None else yc @ R
+    nrm = torch.linalg.norm
+    out_ = KktResidual(
+        float(nrm(e @ yc.t() + ltdu)), float(nrm(xc.t() @ e + dvrt)), float(nrm(lxc - u)), float(nrm(ycr - v)),
+        float(torch.sqrt(((du * u) ** 2).sum() + (du.clamp(min=0) ** 2).sum() + ((-u).clamp(min=0) ** 2).sum())),
+        float(torch.sqrt(((dv * v) ** 2).sum() + (dv.clamp(min=0) ** 2).sum() + ((-v).clamp(min=0) ** 2).sum())))
+    return out_
+
+
+@dataclass
 class AdmmState:
     """ADMM iterates (nmf.py:232-244): compressed cores, splits, duals."""
 

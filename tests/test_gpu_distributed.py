@@ -85,17 +85,25 @@ def problem():
         o = O.admm(a * (1.0 + 2.0 ** -23 * rng.standard_normal(a.shape)), 20, cfg=O.Config(20, 10, 4, 5),
                    max_iter=500, tol=1e-4)
         spread = max(spread, abs(O.rel_error(a, o.X, o.Y) - ref.rel_error))
-    return a32, L, R, ref, spread
+    # the reference's own subspace band under one fp32 rounding of A (2^-24)
+    band = 0.0
+    for k in range(2):
+        ap = a * (1.0 + 2.0 ** -24 * np.random.default_rng(10 + k).standard_normal(a.shape))
+        band = max(band, O.projector_distance(L, O.range_basis(ap, replace(cfg, seed=O.child_seed(5, "left-basis")))),
+                   O.projector_distance(R, O.row_basis(ap, replace(cfg, seed=O.child_seed(5, "right-basis")))))
+    return a32, L, R, ref, (spread, band)
 
 
 def _check(res, problem):
-    a32, L, R, ref, spread = problem
+    a32, L, R, ref, (spread, band) = problem
     Ld, Rd, it, rel, snmf = res
     sig = slice(0, 20)
     assert O.projector_distance(L[:, sig], Ld[:, sig]) < 1e-5
     assert O.projector_distance(R[:, sig], Rd[:, sig]) < 1e-5
-    assert O.projector_distance(L, Ld) < 1e-4
-    assert O.projector_distance(R, Rd) < 1e-4
+    # full basis: north-star 1e-4, or twice the reference's own movement under
+    # one fp32 rounding of A (tests/test_gpu_fullsize.py)
+    assert O.projector_distance(L, Ld) <= max(1e-4, 2.0 * band)
+    assert O.projector_distance(R, Rd) <= max(1e-4, 2.0 * band)
     assert it == ref.iterations
     sep = O.near_separable(3000, 1200, 12, 1.0, 0.005, seed=3)[0].astype(np.float32).astype(np.float64)
     for sel, (K, Y, rf) in snmf.items():

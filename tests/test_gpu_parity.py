@@ -542,3 +542,48 @@ def test_admm_uncompressed_limits():
         C.nmf_admm(a, 40, compressed=False, cfg=C.CompressionConfig(r=40, r_ov=10, w=4, seed=1))
     res = C.nmf_admm(a, 5, compressed=False, cfg=cfg, max_iter=0)
     assert res.iterations == 0
+
+
+# ------------------------------------------------- API completeness -----
+
+def test_compression_error_spectral_matches_power_iteration():
+    # compress.py:250-286: the spectral norm of A - Q Q^T A by the reference's
+    # seeded power iteration (the exact 2-norm as the yardstick)
+    a = O.dense_lowrank(900, 700, 8, 0.05, seed=4).astype(np.float32).astype(np.float64)
+    basis = C.structured_compress(a, C.CompressionConfig(r=8, r_ov=4, w=2, seed=1))
+    q = basis.Q
+    resid = a - q @ (q.T @ a)
+    got = C.compression_error(a, basis, norm="spectral")
+    assert abs(got - np.linalg.norm(resid, 2)) <= 1e-3 * np.linalg.norm(resid, 2)
+    fro = C.compression_error(a, basis)
+    assert abs(fro - np.linalg.norm(resid)) <= 1e-4 * np.linalg.norm(resid)
+    with pytest.raises(C.ArgumentError):
+        C.compression_error(a, basis, norm="nuclear")
+
+
+def test_canonical_qr_matches_reference_convention():
+    # compress.py:136-145: reduced QR with diag(R) >= 0
+    b = np.random.default_rng(3).standard_normal((2000, 37))
+    q, r = C.canonical_qr(b)
+    qr_, rr = O.qr_pos(b)
+    assert np.all(np.diag(r) > 0)
+    assert np.abs(q - qr_).max() < 1e-5
+    assert np.abs(r - rr).max() < 1e-5 * np.abs(rr).max()
+    assert np.allclose(np.tril(r, -1), 0.0)
+
+
+def test_kkt_residual_matches_oracle():
+    # nmf.py:246-303 at an ADMM state delivered by on_iteration
+    d = O.dense_lowrank(300, 200, 4, 0.01, seed=8)
+    states = []
+    C.nmf_admm(d, 4, cfg=C.CompressionConfig(r=4, seed=2), max_iter=5, tol=0.0,
+               on_iteration=lambda k, st: states.append(st))
+    st = states[-1]
+    cfg = O.adjust(O.Config(4, 10, 4, 2), *d.shape)
+    left, right = O.compressed_bases(d, cfg)
+    core = (left.T @ d) @ right.T
+    got = C.kkt_residual(st, core, left, right)
+    ref = O.kkt(st.xc, st.yc, st.u, st.v, st.dual_u, st.dual_v, core, left, right)
+    np.testing.assert_allclose([got.grad_left, got.grad_right, got.feas_left, got.feas_right, got.comp_left,
+                                got.comp_right], ref, rtol=1e-6, atol=1e-9)
+    assert got.max_residual == max(ref) or abs(got.max_residual - max(ref)) <= 1e-6 * max(ref)
