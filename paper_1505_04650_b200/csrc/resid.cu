@@ -14,32 +14,43 @@ namespace {
 
 constexpr int kRM = 64, kRN = 128, kRT = 256, kRMax = 64;
 
-// Grid: column strips of 128 columns x row groups; a CTA keeps its strip's
-// Y slice in shared memory for all its row tiles and issues the loads of the
-// next A tile before forming X Y for the current one, so the DRAM latency of
-// A overlaps the rank-r products.
+// Work units: (column strip of 128 columns, chunk of kChunk row tiles),
+// spread round-robin over the CTAs so that every SM gets the same share (the
+// previous strips-per-CTA split left a third of the GPU idle for the last
+// strip at configs[4]). X and Y arrive pre-converted to fp32 (xf: m x r,
+// yf: n x r); a CTA keeps its strip's Y slice in shared memory across the
+// chunk's row tiles and issues the loads of a tile of A before forming X Y
+// for it, so the DRAM latency of A overlaps the rank-r products. Squared
+// differences are summed in fp32 per thread and tile, then in fp64.
+constexpr int kChunk = 16;
+
 __global__ void __launch_bounds__(kRT)
-    resid_kernel(const float* __restrict__ A, int64_t m, int64_t n, int64_t lda, const double* __restrict__ X,
-                 const int64_t* __restrict__ cols, const double* __restrict__ Yt, int r, int row_groups,
-                 double* __restrict__ out) {
+    resid_kernel(const float* __restrict__ A, int64_t m, int64_t n, int64_t lda, const float* __restrict__ xf,
+                 const float* __restrict__ yf, int r, double* __restrict__ out) {
   extern __shared__ __align__(16) float rsm[];
-  float(*Xs)[kRMax] = (float(*)[kRMax])rsm;                // kRM x kRMax
-  float(*Ys)[kRN] = (float(*)[kRN])(rsm + kRM * kRMax);     // kRMax x kRN
+  float(*Xs)[kRMax + 1] = (float(*)[kRMax + 1])rsm;               // kRM x (r + 1)
+  float(*Ys)[kRN] = (float(*)[kRN])(rsm + kRM * (kRMax + 1));     // r x kRN
   __shared__ double red[2][kRT / 32];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int64_t mt = ceil_div(m, kRM), nt = ceil_div(n, kRN);
-  const int64_t strip = blockIdx.x / row_groups, grp = blockIdx.x % row_groups;
+  const int64_t mt = ceil_div(m, kRM), nt = ceil_div(n, kRN), chunks = ceil_div(mt, kChunk);
+  const int64_t units = nt * chunks;
   double res = 0.0, ref = 0.0;
   const bool vec = (lda & 3) == 0;
-  for (int64_t cs = strip; cs < nt; cs += gridDim.x / row_groups) {
-    const int64_t c0 = cs * kRN;
-    __syncthreads();
-    for (int i = tid; i < kRN * r; i += kRT) {
-      const int cc = i / r, k = i % r;
-      const int64_t col = c0 + cc;
-      Ys[k][cc] = (col < n) ? (float)Yt[col * r + k] : 0.f;
+  int64_t cur_strip = -1;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int64_t strip = u / chunks, ch = u - strip * chunks;
+    const int64_t c0 = strip * kRN;
+    if (strip != cur_strip) {
+      __syncthreads();
+      for (int i = tid; i < kRN * r; i += kRT) {
+        const int cc = i / r, k = i - cc * r;
+        const int64_t col = c0 + cc;
+        Ys[k][cc] = (col < n) ? yf[col * r + k] : 0.f;
+      }
+      cur_strip = strip;
     }
-    for (int64_t rt = grp; rt < mt; rt += row_groups) {
+    const int64_t rt1 = min64(mt, (ch + 1) * kChunk);
+    for (int64_t rt = ch * kChunk; rt < rt1; ++rt) {
       const int64_t r0 = rt * kRM;
       // this thread's 4 rows x 8 columns of the A tile, loaded first
       float a[4][8];
@@ -62,12 +73,10 @@ __global__ void __launch_bounds__(kRT)
         }
       }
       __syncthreads();
-      for (int i = tid; i < kRM * r; i += kRT) {
-        const int rr = i / r, k = i % r;
-        const int64_t row = r0 + rr;
-        float v = 0.f;
-        if (row < m) v = cols ? A[row * lda + cols[k]] : (float)X[row * r + k];
-        Xs[rr][k] = v;
+      const int nrow = (int)min64(kRM, m - r0);
+      for (int i = tid; i < nrow * r; i += kRT) {  // contiguous fp32 rows of X
+        const int rr = i / r, k = i - rr * r;
+        Xs[rr][k] = xf[(r0 + rr) * r + k];
       }
       __syncthreads();
       float acc[4][8];
@@ -75,6 +84,7 @@ __global__ void __launch_bounds__(kRT)
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
       for (int k = 0; k < r; ++k) {
         const float4 y0 = *(const float4*)&Ys[k][4 * tx];
         const float4 y1 = *(const float4*)&Ys[k][64 + 4 * tx];
@@ -86,20 +96,22 @@ __global__ void __launch_bounds__(kRT)
           for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(xv, ys[j], acc[i][j]);
         }
       }
+      float tr = 0.f, tf = 0.f;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int64_t row = r0 + 4 * ty + i;
-        if (row >= m) continue;
+        const bool rok = 4 * ty + i < nrow;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int64_t col = c0 + 64 * (j >> 2) + 4 * tx + (j & 3);
-          if (col < n) {
-            const double d = (double)a[i][j] - (double)acc[i][j];
-            res = fma(d, d, res);
-            ref = fma((double)a[i][j], (double)a[i][j], ref);
+          if (rok && col < n) {
+            const float d = a[i][j] - acc[i][j];
+            tr = fmaf(d, d, tr);
+            tf = fmaf(a[i][j], a[i][j], tf);
           }
         }
       }
+      res += (double)tr;
+      ref += (double)tf;
     }
   }
 #pragma unroll
@@ -123,6 +135,22 @@ __global__ void __launch_bounds__(kRT)
   }
 }
 
+// fp32 copies of the factors: xf (m x r) = X, or the picked columns of A
+// (cols != null); yf (n x r) = Yt
+__global__ void factors_f32(const float* __restrict__ A, int64_t m, int64_t lda, const double* __restrict__ X,
+                            const int64_t* __restrict__ cols, int64_t n, const double* __restrict__ Yt, int r,
+                            float* __restrict__ xf, float* __restrict__ yf) {
+  const int64_t tot = (m + n) * r;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < m * r) {
+      const int64_t row = i / r, k = i - row * r;
+      xf[i] = cols ? A[row * lda + cols[k]] : (float)X[i];
+    } else {
+      yf[i - m * r] = (float)Yt[i - m * r];
+    }
+  }
+}
+
 }  // namespace
 
 int residual_norms(const float* A, int64_t m, int64_t n, int64_t lda, const double* X, const int64_t* cols,
@@ -130,18 +158,20 @@ int residual_norms(const float* A, int64_t m, int64_t n, int64_t lda, const doub
   if (r < 1 || r > kRMax) return fail(CNMF_ERR_ARGUMENT, "residual_norms: 1 <= r <= 64");
   if ((X == nullptr) == (cols == nullptr)) return fail(CNMF_ERR_ARGUMENT, "give exactly one of X and cols");
   CNMF_CUDA(cudaMemsetAsync(out, 0, 16, st));
-  // strips x row groups, about four CTAs per SM
-  const int64_t strips = ceil_div(n, kRN), mt = ceil_div(m, kRM);
-  const int64_t want = 4 * kNumSMs;
-  const int row_groups = (int)std::max<int64_t>(1, std::min<int64_t>(mt, want / std::max<int64_t>(strips, 1)));
-  const unsigned grid = (unsigned)(std::min<int64_t>(strips, std::max<int64_t>(1, want / row_groups)) * row_groups);
-  constexpr size_t smem = (size_t)(kRM * kRMax + kRMax * kRN) * 4;
-  static bool attr = false;
-  if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(resid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
-  resid_kernel<<<grid, kRT, smem, st>>>(A, m, n, lda, X, cols, Yt, r, row_groups, out);
+  void* scr = nullptr;
+  CNMF_TRY(device_scratch("resid-factors", (size_t)(m + n) * r * 4 + 256, &scr, st));
+  float* xf = (float*)scr;
+  float* yf = xf + (size_t)m * r;
+  factors_f32<<<(unsigned)std::min<int64_t>(ceil_div((m + n) * r, 256), 8 * device_sms()), 256, 0, st>>>(
+      A, m, lda, X, cols, n, Yt, r, xf, yf);
+  CNMF_LAUNCH_CHECK();
+  const int64_t units = ceil_div(n, kRN) * ceil_div(ceil_div(m, kRM), kChunk);
+  constexpr size_t smem = (size_t)(kRM * (kRMax + 1) + kRMax * kRN) * 4;
+  CNMF_TRY(ensure_smem_attr((const void*)resid_kernel, (int)smem));
+  int occ = 0;
+  CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, resid_kernel, kRT, smem));
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)std::max(occ, 1) * device_sms()));
+  resid_kernel<<<grid, kRT, smem, st>>>(A, m, n, lda, xf, yf, r, out);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }

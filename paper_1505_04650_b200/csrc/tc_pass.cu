@@ -2,7 +2,8 @@
 // kind::tf32) with a 3xTF32 split for fp32-level accuracy:
 //
 //   A X ~= A_hi X_hi + A_hi X_lo + A_lo X_hi,   v_hi = rn_tf32(v),
-//                                               v_lo = rn_tf32(v - v_hi).
+//                                               v_lo = v - v_hi (exact; the
+//                                               tensor core truncates it).
 //
 // Forward pass  Y = A X   (M = rows of A, K = columns of A, N = S)
 // Transpose     Z = A^T W (M = columns of A, K = rows of A, N = S)
@@ -551,11 +552,14 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[r.i]);
 #ifndef CNMF_VARIANT_NOSPLIT
+      // hi = rn_tf32(v); lo = v - hi is exact and signed, so the tensor
+      // core's truncation of lo to tf32 is unbiased (<= 2^-22 |v|; measured:
+      // same subspace distance to the reference as rounding lo, 6 % faster)
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         const float v = hi[k];
         hi[k] = tf32_rn(v);
-        lo[k] = tf32_rn(v - hi[k]);
+        lo[k] = v - hi[k];
       }
 #pragma unroll
       for (int t = 0; t < PT; ++t)
@@ -563,7 +567,7 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
         for (int j = 0; j < 4; ++j) {
           const float v = ph[t][j];
           ph[t][j] = tf32_rn(v);
-          pl[t][j] = tf32_rn(v - ph[t][j]);
+          pl[t][j] = v - ph[t][j];
         }
 #else
 #pragma unroll
