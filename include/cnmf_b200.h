@@ -298,6 +298,26 @@ int cnmf_right_factor_given(const double* W, int64_t n, int s, int64_t ld, const
 int cnmf_refit_given(const double* W, int64_t n, int s, int64_t ld, const double* P, int k, const double* Ht,
                      double* R, double* sq, double* tot, void* stream);
 
+
+/* ---- fp64 path for float64 inputs (BASELINE.json configs[0] is an fp64
+ * workload; compress.py:156-227, snmf.py:154-232 with precision="fp64") ----
+ * A: fp64 row-major m x n (lda >= n); panels fp64 with ld = cnmf_panel_ld(s)
+ * (s <= 64). The same algorithm as the fp32 path -- seeded test matrix,
+ * 2w + 1 passes, every pass output re-orthonormalised (CholeskyQR2 in fp64)
+ * -- with DFMA passes (plain tiled kernels, meant for CPU-sized inputs).
+ * cnmf_structured_compress_f64  Q (m x S or n x S for side 1), synchronises
+ *                               (NumericError if a Gram matrix fails).
+ * cnmf_pass_transpose_f64       Z (n x S) = A^T W.
+ * cnmf_residual_norms_f64       out[0] = ||A - X Y||^2, out[1] = ||A||^2
+ *                               (X: m x r fp64, or A[:, cols]; Yt: n x r). */
+size_t cnmf_compress_f64_workspace(int64_t m, int64_t n, int s);
+int cnmf_structured_compress_f64(const double* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed,
+                                 int side, double* Q, void* ws, size_t ws_bytes, void* stream);
+int cnmf_pass_transpose_f64(const double* A, int64_t m, int64_t n, int64_t lda, const double* W, int s, double* Z,
+                            void* stream);
+int cnmf_residual_norms_f64(const double* A, int64_t m, int64_t n, int64_t lda, const double* X, const int64_t* cols,
+                            const double* Yt, int r, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,11 @@ SIGNATURES = {
     "cnmf_panel_cross": (c_int, [vp, vp, c_i64, c_int, vp, vp]),
     "cnmf_residual_norms": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, vp, c_int, vp, vp]),
     "cnmf_admm_workspace": (c_size, [c_i64, c_i64, c_int, c_int]),
+    "cnmf_compress_f64_workspace": (c_size, [c_i64, c_i64, c_int]),
+    "cnmf_structured_compress_f64": (c_int, [vp, c_i64, c_i64, c_i64, c_int, c_int, c_u64, c_int, vp, vp, c_size,
+                                             vp]),
+    "cnmf_pass_transpose_f64": (c_int, [vp, c_i64, c_i64, c_i64, vp, c_int, vp, vp]),
+    "cnmf_residual_norms_f64": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, vp, c_int, vp, vp]),
     "cnmf_admm_shard_workspace": (c_size, [c_int, c_int]),
     "cnmf_admm_shard_sums_offset": (c_size, []),
     "cnmf_admm_shard_begin": (c_int, [vp, c_int, c_int, vp]),

@@ -23,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import MASK64, DeviceMatrix, as_device64, empty, out, panel_ld, stream, workspace, zeros
+from .device import MASK64, DeviceMatrix, DeviceMatrix64, as_device64, empty, out, panel_ld, stream, workspace, zeros
 from .errors import ArgumentError, InfeasibleRankError
 from .rng import child_seed
 
@@ -146,13 +146,47 @@ def _check(basis):
     _lib.call("cnmf_compress_check", basis._ws.data_ptr(), m, n, s, stream())
 
 
-def structured_compress(a, cfg, reorthogonalize=False, scratch_dir=None):
-    """Orthonormal basis for the dominant column space of ``a`` (compress.py:156)."""
+def _compress_f64(a, cfg, side):
+    """The fp64 range finder (csrc/f64_path.cu): A, panels and products in
+    fp64, CholeskyQR2 after every pass."""
+    A = DeviceMatrix64(a)
+    _require_feasible(cfg, A.m, A.n)
+    s = cfg.basis_cols
+    S = panel_ld(s)
+    if S > 64:
+        raise ArgumentError("the fp64 range finder supports basis widths <= 64")
+    rows = A.m if side == 0 else A.n
+    q = zeros((rows, S), dtype=torch.float64)
+    nb = _lib.load().cnmf_compress_f64_workspace(A.m, A.n, s)
+    ws = workspace(nb)
+    _lib.call("cnmf_structured_compress_f64", A.ptr, A.m, A.n, A.lda, s, cfg.w, cfg.seed & MASK64, side,
+              q.data_ptr(), ws.data_ptr(), nb, stream())
+    view = q[:, :s]
+    basis = CompressionBasis(Q=view.cpu().numpy() if A.on_host else view, kind="structured", config=cfg, panel=q)
+    basis.precision = "fp64"
+    return basis, A
+
+
+def _precision(p):
+    if p not in ("fp32", "fp64"):
+        raise ArgumentError(f"precision must be 'fp32' or 'fp64', got {p!r}")
+    return p
+
+
+def structured_compress(a, cfg, reorthogonalize=False, scratch_dir=None, precision="fp32"):
+    """Orthonormal basis for the dominant column space of ``a`` (compress.py:156).
+    ``precision="fp64"`` selects the fp64 range finder (float64 workloads such
+    as BASELINE.json configs[0]); the default streams A in fp32 through the
+    3xTF32 tensor-core passes."""
+    if _precision(precision) == "fp64":
+        return _compress_f64(a, cfg, 0)[0]
     return _compress(a, cfg, 0)[0]
 
 
-def structured_compress_rows(a, cfg, reorthogonalize=False, scratch_dir=None):
+def structured_compress_rows(a, cfg, reorthogonalize=False, scratch_dir=None, precision="fp32"):
     """Orthonormal basis for the dominant row space of ``a`` (compress.py:202)."""
+    if _precision(precision) == "fp64":
+        return _compress_f64(a, cfg, 1)[0]
     return _compress(a, cfg, 1)[0]
 
 

@@ -47,6 +47,12 @@ int admm_run(const double*, const float*, int64_t, const float*, int64_t, int, i
              double*, double*, double*, double, double, double, int, double, double*, double*, int*, void*, size_t,
              int, int, cudaStream_t);
 int64_t launch_count();
+size_t compress_f64_workspace(int64_t, int64_t, int);
+int structured_compress_f64(const double*, int64_t, int64_t, int64_t, int, int, uint64_t, int, double*, void*, size_t,
+                            cudaStream_t);
+int pass_transpose_f64(const double*, int64_t, int64_t, int64_t, const double*, int, double*, cudaStream_t);
+int residual_norms_f64(const double*, int64_t, int64_t, int64_t, const double*, const int64_t*, const double*, int,
+                       double*, cudaStream_t);
 size_t admm_shard_workspace(int, int);
 size_t admm_shard_sums_offset();
 int admm_shard_begin(void*, int, int, cudaStream_t);
@@ -322,5 +328,19 @@ int cnmf_right_factor_given(const double* W, int64_t n, int s, int64_t ld, const
 int cnmf_refit_given(const double* W, int64_t n, int s, int64_t ld, const double* P, int k, const double* Ht,
                      double* R, double* sq, double* tot, void* stream) {
   return refit_given(W, n, s, ld, P, k, Ht, R, sq, tot, STREAM(stream));
+}
+/* ---- fp64 path (float64 inputs; BASELINE.json configs[0]) --------------- */
+size_t cnmf_compress_f64_workspace(int64_t m, int64_t n, int s) { return compress_f64_workspace(m, n, s); }
+int cnmf_structured_compress_f64(const double* A, int64_t m, int64_t n, int64_t lda, int s, int w, uint64_t seed,
+                                 int side, double* Q, void* ws, size_t ws_bytes, void* stream) {
+  return structured_compress_f64(A, m, n, lda, s, w, seed, side, Q, ws, ws_bytes, STREAM(stream));
+}
+int cnmf_pass_transpose_f64(const double* A, int64_t m, int64_t n, int64_t lda, const double* W, int s, double* Z,
+                            void* stream) {
+  return pass_transpose_f64(A, m, n, lda, W, s, Z, STREAM(stream));
+}
+int cnmf_residual_norms_f64(const double* A, int64_t m, int64_t n, int64_t lda, const double* X, const int64_t* cols,
+                            const double* Yt, int r, double* out, void* stream) {
+  return residual_norms_f64(A, m, n, lda, X, cols, Yt, r, out, STREAM(stream));
 }
 }  // extern "C"

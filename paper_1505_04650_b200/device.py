@@ -87,6 +87,37 @@ class DeviceMatrix:
         return (self.m, self.n)
 
 
+class DeviceMatrix64:
+    """A (m x n) as fp64 row-major on the device (the fp64 path: float64
+    inputs with precision="fp64", BASELINE.json configs[0])."""
+
+    def __init__(self, a, name="matrix"):
+        require_cuda()
+        if isinstance(a, DeviceMatrix64):
+            self.__dict__.update(a.__dict__)
+            return
+        self.on_host = not (isinstance(a, torch.Tensor) and a.is_cuda)
+        if hasattr(a, "to_dense") and not isinstance(a, torch.Tensor):
+            a = a.to_dense()
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+        if t.dim() != 2:
+            raise ArgumentError(f"{name} must be 2-D, got shape {tuple(t.shape)}")
+        m, n = t.shape
+        if m == 0 or n == 0:
+            raise ArgumentError(f"{name} must be non-empty, got shape {tuple(t.shape)}")
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.t = t.to(device=dev, dtype=torch.float64).contiguous()
+        self.m, self.n, self.lda = int(m), int(n), int(n)
+
+    @property
+    def ptr(self):
+        return self.t.data_ptr()
+
+    @property
+    def shape(self):
+        return (self.m, self.n)
+
+
 def zeros(shape, dtype=torch.float32):
     return torch.zeros(shape, dtype=dtype, device=torch.device("cuda", torch.cuda.current_device()))
 

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .compress import CompressionConfig, _compress, adjust_config
+from .compress import CompressionConfig, _compress, _compress_f64, _precision, adjust_config
 from .device import DeviceMatrix, as_device64, out, panel_ld, stream, zeros
 from .errors import ArgumentError, ConvergenceError, RankDeficiencyError, UndefinedMetricError
 
@@ -154,8 +154,13 @@ def nnls_solve(c, d, tol=1e-10, max_exchanges=None):
     return res[:, 0] if vector_target else res
 
 
-def snmf(a, r, selector="spa", reduction="compressed", cfg=None, nnls_tol=1e-10, scratch_dir=None):
-    """Separable NMF A ~ A[:, K] Y (snmf.py:170-232)."""
+def snmf(a, r, selector="spa", reduction="compressed", cfg=None, nnls_tol=1e-10, scratch_dir=None,
+         precision="fp32"):
+    """Separable NMF A ~ A[:, K] Y (snmf.py:170-232). ``precision="fp64"``
+    keeps A and the compression in fp64 (csrc/f64_path.cu; compressed
+    reduction only)."""
+    if _precision(precision) == "fp64":
+        return _snmf_f64(a, r, selector, reduction, cfg, nnls_tol)
     A = DeviceMatrix(a)
     m, n = A.m, A.n
     if not 1 <= r <= min(m, n):
@@ -214,6 +219,49 @@ def snmf(a, r, selector="spa", reduction="compressed", cfg=None, nnls_tol=1e-10,
         raise UndefinedMetricError("reduced matrix has zero norm")
     full = zeros((2,), dtype=torch.float64)
     _lib.call("cnmf_residual_norms", A.ptr, m, n, A.lda, None, d_picks.data_ptr(), Ht.data_ptr(), len(picks),
+              full.data_ptr(), stream())
+    res_f, ref_f = full.tolist()
+    Y = out(Ht.t().contiguous(), A.on_host)
+    return SnmfResult(K=picks, Y=Y, rel_error_reduced=float(np.sqrt(max(res_red, 0.0) / ref_red)),
+                      rel_error_full=float(np.sqrt(max(res_f, 0.0) / ref_f)) if ref_f else 0.0)
+
+
+def _snmf_f64(a, r, selector, reduction, cfg, nnls_tol):
+    """snmf() with A, the basis and Q^T A in fp64 (the selection, the NNLS
+    right factor and the error norms are fp64 on every path)."""
+    if reduction != "compressed":
+        raise ArgumentError("precision='fp64' supports the compressed reduction")
+    if selector not in ("spa", "xray"):
+        raise ArgumentError(f"unknown selector {selector!r}")
+    from .device import DeviceMatrix64
+
+    A = DeviceMatrix64(a)
+    m, n = A.m, A.n
+    if not 1 <= r <= min(m, n):
+        raise ArgumentError(f"rank {r} out of range for a {m}x{n} matrix")
+    if cfg is None:
+        cfg = CompressionConfig(r=r, r_ov=10, w=0, seed=0)
+    cfg = adjust_config(cfg, m, n)
+    basis, _ = _compress_f64(A, cfg, 0)
+    q = basis.panel
+    s, S = cfg.basis_cols, q.shape[1]
+    W = zeros((n, S), dtype=torch.float64)
+    _lib.call("cnmf_pass_transpose_f64", A.ptr, m, n, A.lda, q.data_ptr(), s, W.data_ptr(), stream())
+    red = _Reduced(W, s, n, A.on_host)
+    if selector == "spa":
+        picks = _spa(red, r)
+    else:
+        mass = q[:, :s].sum(dim=0)  # Q^T 1 (snmf.py:151, 158)
+        picks = _xray(red, r, mass.cpu().numpy(), nnls_tol)
+    Ht, d_picks = _right_factor(red, picks, nnls_tol)
+    norms = zeros((2,), dtype=torch.float64)
+    _lib.call("cnmf_refit_norms", W.data_ptr(), n, s, S, d_picks.data_ptr(), len(picks), Ht.data_ptr(),
+              norms.data_ptr(), stream())
+    res_red, ref_red = norms.tolist()
+    if ref_red == 0.0:
+        raise UndefinedMetricError("reduced matrix has zero norm")
+    full = zeros((2,), dtype=torch.float64)
+    _lib.call("cnmf_residual_norms_f64", A.ptr, m, n, A.lda, None, d_picks.data_ptr(), Ht.data_ptr(), len(picks),
               full.data_ptr(), stream())
     res_f, ref_f = full.tolist()
     Y = out(Ht.t().contiguous(), A.on_host)

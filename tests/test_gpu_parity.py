@@ -587,3 +587,30 @@ def test_kkt_residual_matches_oracle():
     np.testing.assert_allclose([got.grad_left, got.grad_right, got.feas_left, got.feas_right, got.comp_left,
                                 got.comp_right], ref, rtol=1e-6, atol=1e-9)
     assert got.max_residual == max(ref) or abs(got.max_residual - max(ref)) <= 1e-6 * max(ref)
+
+
+# --------------------------------------------------------- fp64 path -----
+
+def test_fp64_range_finder_matches_reference_golden(golden):
+    # precision="fp64" (configs[0] is an fp64 workload): the reference's own
+    # reorthogonalized basis to fp64 accuracy, columns included
+    a = golden["cmp_a"]
+    cfg = C.CompressionConfig(r=8, r_ov=12, w=2, seed=3)
+    q = C.structured_compress(a, cfg, precision="fp64").Q
+    ref = golden["cmp_q_w2_reorth"]
+    assert O.projector_distance(q, ref) < 1e-9
+    assert np.abs(q - ref).max() < 1e-8
+    qr_ = C.structured_compress_rows(a, cfg, precision="fp64").Q
+    assert O.projector_distance(qr_, golden["cmp_qrows_w2_reorth"]) < 1e-9
+
+
+@pytest.mark.parametrize("sel", ["spa", "xray"])
+def test_fp64_snmf_config0_shape(sel):
+    a, truth = O.near_separable(500, 2000, 10, 1.0, 0.01, seed=11)
+    cfg = C.CompressionConfig(r=10, r_ov=10, w=4, seed=2)
+    res = C.snmf(a, 10, selector=sel, cfg=cfg, precision="fp64")
+    ref = O.snmf(a, 10, selector=sel, cfg=O.Config(10, 10, 4, 2))
+    assert np.array_equal(res.K, ref.K)
+    assert abs(res.rel_error_full - ref.rel_error_full) <= 1e-9 * ref.rel_error_full
+    assert abs(res.rel_error_reduced - ref.rel_error_reduced) <= 1e-8 * max(ref.rel_error_reduced, 1e-12)
+    assert np.abs(res.Y - ref.Y).max() <= 1e-8 * max(1.0, np.abs(ref.Y).max())
