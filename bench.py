@@ -53,7 +53,7 @@ SEED = 5
 
 # BASELINE.json configs: kind, shape, rank, power passes, generator
 CONFIGS = {
-    0: dict(kind="snmf", m=500, n=2000, r=10, q=4, sel="spa", alpha=1.0, sigma=0.01,
+    0: dict(kind="snmf", m=500, n=2000, r=10, q=4, sel="spa", alpha=1.0, sigma=0.01, precision="fp64",
             text="configs[0]: near-separable SNMF m=500 n=2000 r=10, W~|N(0,1)|, H=[I|Dirichlet(1)] permuted, "
                  "noise N(0,0.01^2) clipped; compression r_ov=10 q=4; compressed SPA"),
     1: dict(kind="nmf", m=10000, n=5000, r=20, q=4, iters=500, sparse=0.0, sigma=0.01,
@@ -394,8 +394,15 @@ def run_ours(args):
     m, n, r = c["m"], c["n"], c["r"]
     c0, ncols = D.column_shard(n, ws, rank)
     a, truth = device_data(cid, c0, ncols, rank)
+    prec = c.get("precision", "fp32")
+    if prec == "fp64":
+        if ws > 1:
+            raise SystemExit("the fp64 configuration runs on one GPU")
+        from paper_1505_04650_b200.device import DeviceMatrix64
+
+        a = a.double()
     torch.cuda.synchronize()
-    A = DeviceMatrix(a)
+    A = DeviceMatrix64(a) if prec == "fp64" else DeviceMatrix(a)
     cfg = C.adjust_config(C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED), m, n)
     comm, ops = D.Comm(), (D.DeviceOps() if ws > 1 else None)
     st = torch.cuda.current_stream()
@@ -429,6 +436,10 @@ def run_ours(args):
             return it
     else:
         def compress():
+            if prec == "fp64":
+                from paper_1505_04650_b200.compress import _compress_f64
+
+                return _compress_f64(A, cfg, 0)
             if ws == 1:
                 return _compress(A, cfg, 0, check=False)
             return D.range_finder(ops, comm, A, m, n, c0, cfg, 0)
@@ -438,7 +449,8 @@ def run_ours(args):
             compress()
             ev[1].record(st)
             if ws == 1:
-                res = C.snmf(A, r, selector=c["sel"], cfg=C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED))
+                res = C.snmf(A.t if prec == "fp64" else A, r, selector=c["sel"],
+                             cfg=C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED), precision=prec)
             else:
                 res = D.snmf(ops, comm, A, m, n, c0, r, selector=c["sel"],
                              cfg=C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED))
@@ -495,7 +507,7 @@ def run_ours(args):
     hbm_peak, peak_src = peaks()
     pass_avg_ms = pms.value / max(pl.value, 1)
     pass_bytes = pby.value / max(pl.value, 1)
-    achieved = pass_bytes / (pass_avg_ms * 1e-3) / 1e9
+    achieved = pass_bytes / (pass_avg_ms * 1e-3) / 1e9 if pl.value else 0.0
     S = 32 if cfg.basis_cols <= 32 else 64
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                 "traffic": TRAFFIC.get(cid), "traffic_unit": "dram bytes read+written per launch (ncu --set full)",
@@ -507,8 +519,9 @@ def run_ours(args):
 
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f32",
-            "precision": "f32 A, 3xTF32 tensor-core passes (fp32-level); fp64 Gram, Cholesky, ADMM, NNLS state",
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64" if prec == "fp64" else "f32",
+            "precision": ("f64 A and DFMA passes (csrc/f64_path.cu)" if prec == "fp64" else
+                          "f32 A, 3xTF32 tensor-core passes (fp32-level); fp64 Gram, Cholesky, ADMM, NNLS state"),
             "data": "synthetic (seeded, generated on the device with the configuration's distributions)",
             "config": config_block(cid, ws, {"n_global": n, "compress_ms": comp_ms, "rest_ms": admm_ms,
                                              "tail_ms": tail_ms, "hbm_frac_compress": value / ws / hbm_peak}),
@@ -525,7 +538,7 @@ def run_ours(args):
     host = None
     if not args.no_e2e:
         # pinned host copy of this rank's block (chunked D2H; allocation untimed)
-        host = torch.empty((m, ncols), dtype=torch.float32, pin_memory=True)
+        host = torch.empty((m, ncols), dtype=torch.float64 if prec == "fp64" else torch.float32, pin_memory=True)
         step_rows = max(1, (1 << 28) // ncols)
         for i in range(0, m, step_rows):
             host[i:i + step_rows].copy_(a[i:i + step_rows])
@@ -593,7 +606,7 @@ def e2e_run(args, cid, host, c0, ncols, comm, ops, pj, abytes):
             uh, vh = u.cpu(), vt.cpu()
             return uh.numel() * 8 + vh.numel() * 8 + 8 * len(tr), rel
         if ws == 1:
-            res = C.snmf(host, r, selector=c["sel"], cfg=pub)
+            res = C.snmf(host, r, selector=c["sel"], cfg=pub, precision=c.get("precision", "fp32"))
         else:
             res = D.snmf(ops, comm, DeviceMatrix(host), m, n, c0, r, selector=c["sel"], cfg=pub, host_out=True)
         return res.Y.nbytes + res.K.nbytes, res.rel_error_full
@@ -612,7 +625,7 @@ def e2e_run(args, cid, host, c0, ncols, comm, ops, pj, abytes):
     if ws > 1:
         dist.all_reduce(te_t, op=dist.ReduceOp.MAX)
     te = te_t.item()
-    return {"value": pj * abytes / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(4 * m * ncols),
+    return {"value": pj * abytes / te / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(host.element_size() * m * ncols),
             "d2h_bytes_per_step": int(d2h), "ms": te * 1e3, "rel_error": rel, "steps": len(ts),
             "what": "public nmf_admm / snmf on a pinned host matrix; all passes of the job x |A| / wall time"}
 

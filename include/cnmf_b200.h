@@ -253,11 +253,17 @@ int cnmf_admm_full_run(const float* A, int64_t m, int64_t n, int64_t lda, int r,
  *                          divergence rules, the two ridge solves);
  *   cnmf_admm_shard_sweep  this rank's rows: x = max(P z + dx / p, 0), the dual
  *                          update, and the partial sums L_i^T U_i, L_i^T dU_i,
- *                          R_i V_i^T, R_i dV_i^T and the four KKT sums per side,
- *                          written at byte offset cnmf_admm_shard_sums_offset()
- *                          of ws (2 x (2 s r + 4) doubles) -- the block the host
- *                          all-reduces (SUM) before the next core step.
- * ws: cnmf_admm_shard_workspace(s, r) bytes; cnmf_admm_shard_begin resets it;
+ *                          R_i V_i^T and the four KKT sums per side, written at
+ *                          byte offset cnmf_admm_shard_sums_offset() of ws
+ *                          (2 x (2 s r + 4) doubles; the dual projections are
+ *                          not reduced -- the core step carries L^T dU and
+ *                          R dV^T by the recurrence L^T dU += step pu (G_L xc -
+ *                          L^T U), G_L = L^T L, likewise G_R = R R^T) -- the
+ *                          block the host all-reduces (SUM) before the next
+ *                          core step.
+ * ws: cnmf_admm_shard_workspace(s, r) bytes; cnmf_admm_shard_begin resets it
+ * and takes G_L, G_R (ld x ld fp64, ld = the panel width, summed over all
+ * ranks' rows);
  * cnmf_admm_shard_status copies (next iteration, done, iterations, diverged
  * iteration or -1) to the host int[4] (synchronises).
  *
@@ -278,13 +284,13 @@ int cnmf_admm_full_run(const float* A, int64_t m, int64_t n, int64_t lda, int r,
  */
 size_t cnmf_admm_shard_workspace(int s, int r);
 size_t cnmf_admm_shard_sums_offset(void);
-int cnmf_admm_shard_begin(void* ws, int s, int r, void* stream);
+int cnmf_admm_shard_begin(void* ws, int s, int r, const double* GL, const double* GR, int ld, void* stream);
 int cnmf_admm_shard_sweep(void* ws, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
                           double* du, double* vt, double* dvt, double pu, double pv, double step, int update,
                           void* stream);
 int cnmf_admm_shard_core(void* ws, const double* core, double* xc, double* yc, int s, int r, double pu, double pv,
-                         double tol, double* trace, double* scores, int k, int max_iter, int first, int solve,
-                         void* stream);
+                         double step, double tol, double* trace, double* scores, int k, int max_iter, int first,
+                         int solve, void* stream);
 int cnmf_admm_shard_status(const void* ws, int* state, void* stream);
 int cnmf_shard_argmax(const double* v, int64_t n, const uint8_t* picked, const uint8_t* valid, double* out_v,
                       int64_t* out_i, void* stream);

@@ -75,11 +75,11 @@ SIGNATURES = {
     "cnmf_residual_norms_f64": (c_int, [vp, c_i64, c_i64, c_i64, vp, vp, vp, c_int, vp, vp]),
     "cnmf_admm_shard_workspace": (c_size, [c_int, c_int]),
     "cnmf_admm_shard_sums_offset": (c_size, []),
-    "cnmf_admm_shard_begin": (c_int, [vp, c_int, c_int, vp]),
+    "cnmf_admm_shard_begin": (c_int, [vp, c_int, c_int, vp, vp, c_int, vp]),
     "cnmf_admm_shard_sweep": (c_int, [vp, vp, c_i64, vp, c_i64, c_int, c_int, vp, vp, vp, vp, c_dbl, c_dbl, c_dbl,
                                       c_int, vp]),
-    "cnmf_admm_shard_core": (c_int, [vp, vp, vp, vp, c_int, c_int, c_dbl, c_dbl, c_dbl, vp, vp, c_int, c_int, c_int,
-                                     c_int, vp]),
+    "cnmf_admm_shard_core": (c_int, [vp, vp, vp, vp, c_int, c_int, c_dbl, c_dbl, c_dbl, c_dbl, vp, vp, c_int, c_int,
+                                     c_int, c_int, vp]),
     "cnmf_admm_shard_status": (c_int, [vp, c_intp, vp]),
     "cnmf_shard_argmax": (c_int, [vp, c_i64, vp, vp, vp, vp, vp]),
     "cnmf_spa_shard_step": (c_int, [vp, c_i64, c_int, c_i64, vp, vp, vp, vp]),

@@ -22,6 +22,9 @@
 #include "common.cuh"
 
 namespace cnmf {
+
+int panel_cross(const float* P1, const float* P2, int64_t rows, int S, double* out, cudaStream_t st);
+
 namespace {
 
 constexpr int kT = 256;   // threads per block
@@ -54,7 +57,7 @@ __host__ __device__ inline int sums_len(int s, int r) { return 2 * s * r + 4; }
 // accumulates a 4 x 4 block of P^T x and P^T dx over the tile's rows (the
 // block partials). The fp64 FMA pipe is the bound, not shared memory.
 // ---------------------------------------------------------------------------
-constexpr int kRT = 64;  // rows per tile
+constexpr int kRT = 32;  // rows per tile
 
 template <int SP>
 __global__ void __launch_bounds__(kT, 2) row_sweep(SSide L, SSide R, int nbl, const double* __restrict__ Zl,
@@ -65,7 +68,8 @@ __global__ void __launch_bounds__(kT, 2) row_sweep(SSide L, SSide R, int nbl, co
   double* Z = (double*)sm;                 // [SP][kMaxD] (rows c, cols k; zero padded)
   double* Xs = Z + SP * kMaxD;             // [kRT][kMaxD] updated x of the tile
   double* Ds = Xs + kRT * kMaxD;           // [kRT][kMaxD] updated dx of the tile
-  float* PtT = (float*)(Ds + kRT * kMaxD); // [SP][kRT] the tile's panel rows, transposed
+  double* PtT = Ds + kRT * kMaxD;          // [SP][kRT] the tile's panel rows, transposed (fp64: one
+                                           // conversion per element, not one per use)
   __shared__ double red[4][kT / 32];
   const bool left = (int)blockIdx.x < nbl;
   const SSide sd = left ? L : R;
@@ -82,9 +86,9 @@ __global__ void __launch_bounds__(kT, 2) row_sweep(SSide L, SSide R, int nbl, co
   const int k4 = tid & 15;   // columns k = k4 + 16 q (consecutive lanes, consecutive doubles)
   const bool kon = k4 < r;
   const bool con = 4 * g4 < s;
-  double au[16], ad[16];
+  double au[16];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) au[q] = ad[q] = 0.0;
+  for (int q = 0; q < 16; ++q) au[q] = 0.0;
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   // P rows of the next tile, prefetched into registers during the previous
   // tile's reduction (float4 i of the tile: row i / (SP / 4))
@@ -106,10 +110,10 @@ __global__ void __launch_bounds__(kT, 2) row_sweep(SSide L, SSide R, int nbl, co
 #pragma unroll
     for (int j = 0; j < PF; ++j) {
       const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
-      PtT[(c4 + 0) * kRT + row] = c4 + 0 < s ? pf[j].x : 0.f;
-      PtT[(c4 + 1) * kRT + row] = c4 + 1 < s ? pf[j].y : 0.f;
-      PtT[(c4 + 2) * kRT + row] = c4 + 2 < s ? pf[j].z : 0.f;
-      PtT[(c4 + 3) * kRT + row] = c4 + 3 < s ? pf[j].w : 0.f;
+      PtT[(c4 + 0) * kRT + row] = c4 + 0 < s ? (double)pf[j].x : 0.0;
+      PtT[(c4 + 1) * kRT + row] = c4 + 1 < s ? (double)pf[j].y : 0.0;
+      PtT[(c4 + 2) * kRT + row] = c4 + 2 < s ? (double)pf[j].z : 0.0;
+      PtT[(c4 + 3) * kRT + row] = c4 + 3 < s ? (double)pf[j].w : 0.0;
     }
     // the tile's old x, dx land in Xs, Ds asynchronously while P z is formed
     for (int i = tid; i < nr * r; i += kT) {
@@ -123,23 +127,23 @@ __global__ void __launch_bounds__(kT, 2) row_sweep(SSide L, SSide R, int nbl, co
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
     __syncthreads();
-    // ---- update: rows 4 g4 .. 4 g4 + 3, columns k4 + 16 q ----
+    // ---- update: rows 2 g4, 2 g4 + 1, columns k4 + 16 q ----
     {
-      double lx[4][4];
+      double lx[2][4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int a = 0; a < 2; ++a)
 #pragma unroll
         for (int q = 0; q < 4; ++q) lx[a][q] = 0.0;
       if (update && kon) {
-#pragma unroll 2
+#pragma unroll 4
         for (int c = 0; c < s; ++c) {
-          const float4 p4 = *(const float4*)(PtT + c * kRT + 4 * g4);
-          const double pv[4] = {p4.x, p4.y, p4.z, p4.w};
+          const double2 p2 = *(const double2*)(PtT + c * kRT + 2 * g4);
+          const double pv[2] = {p2.x, p2.y};
           double zv[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) zv[q] = Z[c * kMaxD + k4 + 16 * q];
 #pragma unroll
-          for (int a = 0; a < 4; ++a)
+          for (int a = 0; a < 2; ++a)
 #pragma unroll
             for (int q = 0; q < 4; ++q) lx[a][q] = fma(pv[a], zv[q], lx[a][q]);
         }
@@ -147,8 +151,8 @@ __global__ void __launch_bounds__(kT, 2) row_sweep(SSide L, SSide R, int nbl, co
       asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int row = 4 * g4 + a;
+      for (int a = 0; a < 2; ++a) {
+        const int row = 2 * g4 + a;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int k = k4 + 16 * q;
@@ -183,20 +187,14 @@ __global__ void __launch_bounds__(kT, 2) row_sweep(SSide L, SSide R, int nbl, co
 #pragma unroll 2
       for (int row = 0; row < nr; ++row) {
         const double pc[4] = {PtT[(4 * g4 + 0) * kRT + row], PtT[(4 * g4 + 1) * kRT + row],
-                              PtT[(4 * g4 + 2) * kRT + row], PtT[(4 * g4 + 3) * kRT + row]};
-        double xv[4], dv[4];
+                              PtT[(4 * g4 + 2) * kRT + row], PtT[(4 * g4 + 3) * kRT + row]};  // fp64 already
+        double xv[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          xv[q] = Xs[row * kMaxD + k4 + 16 * q];
-          dv[q] = Ds[row * kMaxD + k4 + 16 * q];
-        }
+        for (int q = 0; q < 4; ++q) xv[q] = Xs[row * kMaxD + k4 + 16 * q];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            au[a * 4 + q] = fma(pc[a], xv[q], au[a * 4 + q]);
-            ad[a * 4 + q] = fma(pc[a], dv[q], ad[a * 4 + q]);
-          }
+          for (int q = 0; q < 4; ++q) au[a * 4 + q] = fma(pc[a], xv[q], au[a * 4 + q]);
       }
     }
   }
@@ -207,10 +205,7 @@ __global__ void __launch_bounds__(kT, 2) row_sweep(SSide L, SSide R, int nbl, co
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int c = 4 * g4 + a, k = k4 + 16 * q;
-        if (c < s && k < r) {
-          out[c * r + k] = au[a * 4 + q];
-          out[sr + c * r + k] = ad[a * 4 + q];
-        }
+        if (c < s && k < r) out[c * r + k] = au[a * 4 + q];
       }
   }
   // KKT sums: warp shuffles, then the warps in order
@@ -231,7 +226,7 @@ __global__ void __launch_bounds__(kT, 2) row_sweep(SSide L, SSide R, int nbl, co
 
 template <int SP>
 constexpr size_t sweep_smem() {
-  return ((size_t)SP * kMaxD + 2 * kRT * kMaxD) * 8 + (size_t)SP * kRT * 4;
+  return ((size_t)SP * kMaxD + 2 * kRT * kMaxD + (size_t)SP * kRT) * 8;
 }
 
 // fixed-order sums of the block partials of each side: sums[side][e]
@@ -242,6 +237,11 @@ __global__ void __launch_bounds__(kT) reduce_parts(const double* __restrict__ pa
   const int side = blockIdx.y;
   if (e >= len) return;
   const int b0 = side ? nbl : 0, nb = side ? nbr : nbl;
+  const int sr = (len - 4) / 2;
+  if (e >= sr && e < 2 * sr) {  // the dual projections come from the core step's recurrence
+    sums[side * len + e] = 0.0;
+    return;
+  }
   double acc = 0.0;
   for (int j0 = 0; j0 < nb; j0 += 8) {
     double v[8];
@@ -330,11 +330,19 @@ __device__ __forceinline__ double block_sum(double v, double* red, int slot) {
 
 // KKT of the iteration just swept (k > 0), the stopping / divergence rule,
 // then the two ridge solves of iteration k (nmf.py:341-350).
+// The dual projections follow from the dual step without a reduction (the
+// persistent kernel's recurrence, csrc/admm.cu):
+//   L^T dU_k = L^T dU_{k-1} + step pu (G_L xc_k - L^T U_k),   G_L = L^T L,
+//   R dV_k^T = R dV_{k-1}^T + step pv (G_R yc_k^T - R V_k^T), G_R = R R^T,
+// so the row sweep reduces L^T U and R V^T only. DL, DR (s x r) carry the
+// projections between launches; `first` zeroes them (dU, dV start at 0).
 __global__ void __launch_bounds__(kCT) core_step(const double* __restrict__ core, const double* __restrict__ sums,
                                                   double* __restrict__ xc, double* __restrict__ yc, double* Zl,
-                                                  double* Zr, int s, int r, double pu, double pv, double tol,
-                                                  double* trace, double* scores, SCtrl* ctrl, int k, int max_iter,
-                                                  int first, int solve) {
+                                                  double* Zr, const double* __restrict__ GL,
+                                                  const double* __restrict__ GR, int ldg, double* __restrict__ DL,
+                                                  double* __restrict__ DR, int s, int r, double pu, double pv,
+                                                  double step, double tol, double* trace, double* scores, SCtrl* ctrl,
+                                                  int k, int max_iter, int first, int solve) {
   if (ctrl->done) return;
   extern __shared__ __align__(16) unsigned char sm[];
   double* E = (double*)sm;         // s x s: E = xc yc - core, later the rhs (s x r)
@@ -366,8 +374,17 @@ __global__ void __launch_bounds__(kCT) core_step(const double* __restrict__ core
       ycS[i] = srt[c * r + a];
       ycT[c * r + a] = srt[c * r + a];
     }
+    for (int i = tid; i < sr; i += kCT) DL[i] = DR[i] = 0.0;
     __syncthreads();
   } else if (k > 0) {
+    // dual projections after the sweep of iteration k - 1 (xc, yc of k - 1)
+    small_gemm(s, r, s, GL, ldg, 1, xcS, r, [&](int a, int j, double v) {
+      DL[a * r + j] += step * pu * (v - sl[a * r + j]);
+    });
+    small_gemm(s, r, s, GR, ldg, 1, ycT, r, [&](int c, int j, double v) {
+      DR[c * r + j] += step * pv * (v - srt[c * r + j]);
+    });
+    __syncthreads();
     // ---- KKT score of iteration k - 1 (nmf.py:281-303) ----
     double obj = 0.0, t1 = 0.0, t2 = 0.0;
     small_gemm(s, s, r, xcS, r, 1, ycS, s, [&](int a, int c, double v) {
@@ -377,11 +394,11 @@ __global__ void __launch_bounds__(kCT) core_step(const double* __restrict__ core
     });
     __syncthreads();
     small_gemm(s, r, s, E, s, 1, ycT, r, [&](int a, int j, double v) {  // (E yc^T + L^T dU)[a][j]
-      const double w = v + sl[sr + a * r + j];
+      const double w = v + DL[a * r + j];
       t1 += w * w;
     });
     small_gemm(r, s, s, xcS, 1, r, E, s, [&](int j, int c, double v) {  // (xc^T E + dV R^T)[j][c]
-      const double w = v + srt[sr + c * r + j];
+      const double w = v + DR[c * r + j];
       t2 += w * w;
     });
     block_sum(t1, red, 0);
@@ -420,7 +437,7 @@ __global__ void __launch_bounds__(kCT) core_step(const double* __restrict__ core
   // ---- xc = (core yc^T + pu L^T U - L^T dU) (yc yc^T + pu I)^-1 ----
   small_gemm(r, r, s, ycS, s, 1, ycT, r, [&](int a, int c, double v) { M[a * r + c] = v + (a == c ? pu : 0.0); });
   small_gemm(s, r, s, coreS, s, 1, ycT, r, [&](int a, int c, double v) {  // rhs (s x r) in E
-    E[a * r + c] = v + (pu * sl[a * r + c] - sl[sr + a * r + c]);
+    E[a * r + c] = v + (pu * sl[a * r + c] - DL[a * r + c]);
   });
   spd_inverse(M, piv, r);
   small_gemm(s, r, r, E, r, 1, M, r, [&](int a, int c, double v) {
@@ -432,7 +449,7 @@ __global__ void __launch_bounds__(kCT) core_step(const double* __restrict__ core
   // ---- yc = (xc^T xc + pv I)^-1 (xc^T core + pv V R^T - dV R^T) ----
   small_gemm(r, r, s, xcS, 1, r, xcS, r, [&](int a, int c, double v) { M[a * r + c] = v + (a == c ? pv : 0.0); });
   small_gemm(r, s, s, xcS, 1, r, coreS, s, [&](int a, int c, double v) {  // rhs2 (r x s) in B
-    B[a * s + c] = v + (pv * srt[c * r + a] - srt[sr + c * r + a]);
+    B[a * s + c] = v + (pv * srt[c * r + a] - DR[c * r + a]);
   });
   spd_inverse(M, piv, r);
   small_gemm(r, s, r, M, r, 1, B, s, [&](int a, int c, double v) {
@@ -465,7 +482,7 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   const int nbr = total - nbl;
   const int len = sums_len(s, r);
   // library scratch: block partials, reduced sums, Z operands
-  const size_t need = ((size_t)total * len + 2 * (size_t)len + 2 * kMaxD * kMaxD) * 8;
+  const size_t need = ((size_t)total * len + 2 * (size_t)len + 6 * kMaxD * kMaxD) * 8;
   void* scr = nullptr;
   CNMF_TRY(device_scratch("admm-stream", need, &scr, st));
   double* scratch = (double*)scr;
@@ -473,6 +490,10 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   double* sums = part + (size_t)total * len;
   double* Zl = sums + 2 * len;
   double* Zr = Zl + kMaxD * kMaxD;
+  double* GL = Zr + kMaxD * kMaxD;  // L^T L and R R^T (S x S), for the dual-projection recurrence
+  double* GR = GL + kMaxD * kMaxD;
+  double* DL = GR + kMaxD * kMaxD;  // L^T dU, R dV^T (s x r)
+  double* DR = DL + kMaxD * kMaxD;
   const size_t core_smem = (2 * (size_t)s * s + 4 * (size_t)s * r + (size_t)r * r + 2 * kMaxD) * 8;
   CNMF_TRY(ensure_smem_attr((const void*)row_sweep<32>, (int)sweep_smem<32>()));
   CNMF_TRY(ensure_smem_attr((const void*)row_sweep<64>, (int)sweep_smem<64>()));
@@ -492,6 +513,8 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   if (!resume) {
     init_sctrl<<<1, 1, 0, st>>>(ctrl);
     CNMF_LAUNCH_CHECK();
+    CNMF_TRY(panel_cross(L, L, m, S, GL, st));
+    CNMF_TRY(panel_cross(Rt, Rt, n, S, GR, st));
     CNMF_CUDA(cudaMemsetAsync(du, 0, (size_t)m * r * 8, st));
     CNMF_CUDA(cudaMemsetAsync(dvt, 0, (size_t)n * r * 8, st));
     CNMF_TRY(sweep(0));  // L^T U and V R^T of the start
@@ -507,13 +530,15 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   }
   const int k1 = step_limit > 0 ? std::min(max_iter, k0 + step_limit) : max_iter;
   for (int k = k0; k < k1; ++k) {
-    core_step<<<1, kCT, core_smem, st>>>(core, sums, xc, yc, Zl, Zr, s, r, pu, pv, tol, trace, scores, ctrl, k,
+    core_step<<<1, kCT, core_smem, st>>>(core, sums, xc, yc, Zl, Zr, GL, GR, S, DL, DR, s, r, pu, pv, step, tol,
+                                        trace, scores, ctrl, k,
                                         max_iter, k == 0 && !resume, 1);
     CNMF_LAUNCH_CHECK();
     CNMF_TRY(sweep(1));
   }
   // score of the last swept iteration (and the stop decision)
-  core_step<<<1, kCT, core_smem, st>>>(core, sums, xc, yc, Zl, Zr, s, r, pu, pv, tol, trace, scores, ctrl, k1,
+  core_step<<<1, kCT, core_smem, st>>>(core, sums, xc, yc, Zl, Zr, GL, GR, S, DL, DR, s, r, pu, pv, step, tol, trace,
+                                      scores, ctrl, k1,
                                       max_iter, 0, 0);
   CNMF_LAUNCH_CHECK();
   SCtrl h;
@@ -536,7 +561,7 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
 // sums 2 x sums_len(s, r)]; the sums are [left: L^T U | L^T dU | 4 KKT sums,
 // right: R V^T | R dV^T | 4 KKT sums] (s x r blocks, row-major).
 // ---------------------------------------------------------------------------
-size_t admm_shard_workspace(int s, int r) { return (8 + 2 * (size_t)kMaxD * kMaxD + 2 * (size_t)sums_len(s, r)) * 8; }
+size_t admm_shard_workspace(int s, int r) { return (8 + 6 * (size_t)kMaxD * kMaxD + 2 * (size_t)sums_len(s, r)) * 8; }
 size_t admm_shard_sums_offset() { return (8 + 2 * (size_t)kMaxD * kMaxD) * 8; }
 
 struct ShardWs {
@@ -544,17 +569,27 @@ struct ShardWs {
   double* Zl;
   double* Zr;
   double* sums;
+  double *GL, *GR, *DL, *DR;
 };
 
-static ShardWs shard_ws(void* ws) {
+static ShardWs shard_ws(void* ws, int s, int r) {
   double* p = (double*)ws;
-  return ShardWs{(SCtrl*)p, p + 8, p + 8 + kMaxD * kMaxD, p + 8 + 2 * kMaxD * kMaxD};
+  double* g = p + 8 + 2 * kMaxD * kMaxD + 2 * (size_t)sums_len(s, r);
+  return ShardWs{(SCtrl*)p, p + 8, p + 8 + kMaxD * kMaxD, p + 8 + 2 * kMaxD * kMaxD,
+                 g, g + kMaxD * kMaxD, g + 2 * kMaxD * kMaxD, g + 3 * kMaxD * kMaxD};
 }
 
-int admm_shard_begin(void* ws, int s, int r, cudaStream_t st) {
-  if (s < 1 || r < 1 || s > kMaxD || r > kMaxD) return fail(CNMF_ERR_ARGUMENT, "sharded ADMM: 1 <= r, s <= 64");
-  init_sctrl<<<1, 1, 0, st>>>(shard_ws(ws).ctrl);
+// GL = L^T L over all rows of L, GR = R R^T over all columns of R (ld x ld
+// fp64, ld = the panel width): the dual-projection recurrence's Gram
+// matrices, all-reduced by the caller for a sharded R
+int admm_shard_begin(void* ws, int s, int r, const double* GL, const double* GR, int ld, cudaStream_t st) {
+  if (s < 1 || r < 1 || s > kMaxD || r > kMaxD || ld < s || ld > kMaxD)
+    return fail(CNMF_ERR_ARGUMENT, "sharded ADMM: 1 <= r, s <= ld <= 64");
+  const ShardWs w = shard_ws(ws, s, r);
+  init_sctrl<<<1, 1, 0, st>>>(w.ctrl);
   CNMF_LAUNCH_CHECK();
+  CNMF_CUDA(cudaMemcpyAsync(w.GL, GL, (size_t)ld * ld * 8, cudaMemcpyDeviceToDevice, st));
+  CNMF_CUDA(cudaMemcpyAsync(w.GR, GR, (size_t)ld * ld * 8, cudaMemcpyDeviceToDevice, st));
   return CNMF_OK;
 }
 
@@ -562,7 +597,7 @@ int admm_shard_sweep(void* ws, const float* L, int64_t m, const float* Rt, int64
                      double* du, double* vt, double* dvt, double pu, double pv, double step, int update,
                      cudaStream_t st) {
   if (s < 1 || r < 1 || s > kMaxD || r > kMaxD) return fail(CNMF_ERR_ARGUMENT, "sharded ADMM: 1 <= r, s <= 64");
-  const ShardWs w = shard_ws(ws);
+  const ShardWs w = shard_ws(ws, s, r);
   const int S = s <= 32 ? 32 : 64;
   const int total = 2 * device_sms();
   const int64_t rows = std::max<int64_t>(m + n, 1);
@@ -588,12 +623,14 @@ int admm_shard_sweep(void* ws, const float* L, int64_t m, const float* Rt, int64
 }
 
 int admm_shard_core(void* ws, const double* core, double* xc, double* yc, int s, int r, double pu, double pv,
-                    double tol, double* trace, double* scores, int k, int max_iter, int first, int solve,
+                    double step, double tol, double* trace, double* scores, int k, int max_iter, int first, int solve,
                     cudaStream_t st) {
-  const ShardWs w = shard_ws(ws);
+  const ShardWs w = shard_ws(ws, s, r);
+  const int S = s <= 32 ? 32 : 64;
   const size_t core_smem = (2 * (size_t)s * s + 4 * (size_t)s * r + (size_t)r * r + 2 * kMaxD) * 8;
   CNMF_TRY(ensure_smem_attr((const void*)core_step, (int)((7 * kMaxD * kMaxD + 2 * kMaxD) * 8)));
-  core_step<<<1, kCT, core_smem, st>>>(core, w.sums, xc, yc, w.Zl, w.Zr, s, r, pu, pv, tol, trace, scores, w.ctrl, k,
+  core_step<<<1, kCT, core_smem, st>>>(core, w.sums, xc, yc, w.Zl, w.Zr, w.GL, w.GR, S, w.DL, w.DR, s, r, pu, pv,
+                                      step, tol, trace, scores, w.ctrl, k,
                                       max_iter, first, solve);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;

@@ -55,11 +55,11 @@ int residual_norms_f64(const double*, int64_t, int64_t, int64_t, const double*, 
                        double*, cudaStream_t);
 size_t admm_shard_workspace(int, int);
 size_t admm_shard_sums_offset();
-int admm_shard_begin(void*, int, int, cudaStream_t);
+int admm_shard_begin(void*, int, int, const double*, const double*, int, cudaStream_t);
 int admm_shard_sweep(void*, const float*, int64_t, const float*, int64_t, int, int, double*, double*, double*,
                      double*, double, double, double, int, cudaStream_t);
-int admm_shard_core(void*, const double*, double*, double*, int, int, double, double, double, double*, double*, int,
-                    int, int, int, cudaStream_t);
+int admm_shard_core(void*, const double*, double*, double*, int, int, double, double, double, double, double*,
+                    double*, int, int, int, int, cudaStream_t);
 int admm_shard_status(const void*, int*, cudaStream_t);
 int shard_argmax(const double*, int64_t, const uint8_t*, const uint8_t*, double*, int64_t*, cudaStream_t);
 int spa_shard_step(double*, int64_t, int, int64_t, const double*, const uint8_t*, double*, cudaStream_t);
@@ -291,16 +291,18 @@ int cnmf_admm_run(const double* core, const float* L, int64_t m, const float* Rt
 /* ---- column-shard primitives (multi-GPU; distributed.py) ---------------- */
 size_t cnmf_admm_shard_workspace(int s, int r) { return admm_shard_workspace(s, r); }
 size_t cnmf_admm_shard_sums_offset(void) { return admm_shard_sums_offset(); }
-int cnmf_admm_shard_begin(void* ws, int s, int r, void* stream) { return admm_shard_begin(ws, s, r, STREAM(stream)); }
+int cnmf_admm_shard_begin(void* ws, int s, int r, const double* GL, const double* GR, int ld, void* stream) {
+  return admm_shard_begin(ws, s, r, GL, GR, ld, STREAM(stream));
+}
 int cnmf_admm_shard_sweep(void* ws, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
                           double* du, double* vt, double* dvt, double pu, double pv, double step, int update,
                           void* stream) {
   return admm_shard_sweep(ws, L, m, Rt, n, s, r, u, du, vt, dvt, pu, pv, step, update, STREAM(stream));
 }
 int cnmf_admm_shard_core(void* ws, const double* core, double* xc, double* yc, int s, int r, double pu, double pv,
-                         double tol, double* trace, double* scores, int k, int max_iter, int first, int solve,
-                         void* stream) {
-  return admm_shard_core(ws, core, xc, yc, s, r, pu, pv, tol, trace, scores, k, max_iter, first, solve,
+                         double step, double tol, double* trace, double* scores, int k, int max_iter, int first,
+                         int solve, void* stream) {
+  return admm_shard_core(ws, core, xc, yc, s, r, pu, pv, step, tol, trace, scores, k, max_iter, first, solve,
                          STREAM(stream));
 }
 int cnmf_admm_shard_status(const void* ws, int* state, void* stream) {

@@ -201,10 +201,11 @@ class DeviceOps:
                        t.data_ptr(), self._st())
         return t
 
-    def admm_shard_begin(self, s, r):
+    def admm_shard_begin(self, s, r, GL, GR):
         nb = int(self.lib.cnmf_admm_shard_workspace(s, r))
         ws = torch.zeros(nb // 8, dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
-        self._lib.call("cnmf_admm_shard_begin", ws.data_ptr(), s, r, self._st())
+        self._lib.call("cnmf_admm_shard_begin", ws.data_ptr(), s, r, GL.data_ptr(), GR.data_ptr(), GL.shape[0],
+                       self._st())
         off = int(self.lib.cnmf_admm_shard_sums_offset()) // 8
         return {"ws": ws, "sums": ws[off: off + 2 * (2 * s * r + 4)]}
 
@@ -214,9 +215,9 @@ class DeviceOps:
                        float(pv), float(step), int(update), self._st())
         return st["sums"]
 
-    def admm_shard_core(self, st, core, xc, yc, s, r, pu, pv, tol, trace, scores, k, max_iter, first, solve):
+    def admm_shard_core(self, st, core, xc, yc, s, r, pu, pv, step, tol, trace, scores, k, max_iter, first, solve):
         self._lib.call("cnmf_admm_shard_core", st["ws"].data_ptr(), core.data_ptr(), xc.data_ptr(), yc.data_ptr(), s,
-                       r, float(pu), float(pv), float(tol), trace.data_ptr(), scores.data_ptr(), int(k),
+                       r, float(pu), float(pv), float(step), float(tol), trace.data_ptr(), scores.data_ptr(), int(k),
                        int(max_iter), int(first), int(solve), self._st())
 
     def admm_shard_status(self, st):
@@ -351,17 +352,22 @@ def admm(ops, comm, core, left, m, right_local, n, c0, cfg, r, penalty_u=1.0, pe
     yc = ops.zeros((r, s), torch.float64)
     trace = ops.zeros((max(max_iter, 1),), torch.float64)
     scores = ops.zeros((max(max_iter, 1),), torch.float64)
-    st = ops.admm_shard_begin(s, r)
+    # Gram matrices of the dual-projection recurrence (csrc/admm_stream.cu):
+    # G_L = L^T L from the replicated left basis, G_R = sum_i R_i R_i^T
+    S = left.shape[1]
+    GL = ops.cross(left, left, S)
+    GR = comm.allreduce(ops.cross(right_local, right_local, S))
+    st = ops.admm_shard_begin(s, r, GL, GR)
     args = (L_loc, right_local, u, du, vt, dvt, s, r, penalty_u, penalty_v, step_scale)
     comm.allreduce(ops.admm_shard_sweep(st, *args, update=0))  # L^T U, V R^T of the start
     for k in range(max_iter):
-        ops.admm_shard_core(st, core, xc, yc, s, r, penalty_u, penalty_v, tol, trace, scores, k, max_iter,
-                            first=(k == 0), solve=1)
+        ops.admm_shard_core(st, core, xc, yc, s, r, penalty_u, penalty_v, step_scale, tol, trace, scores, k,
+                            max_iter, first=(k == 0), solve=1)
         comm.allreduce(ops.admm_shard_sweep(st, *args, update=1))
         if check_every and (k + 1) % check_every == 0 and ops.admm_shard_status(st)[1]:
             break  # every rank takes the same decision (identical all-reduced inputs)
-    ops.admm_shard_core(st, core, xc, yc, s, r, penalty_u, penalty_v, tol, trace, scores, max_iter, max_iter,
-                        first=False, solve=False)
+    ops.admm_shard_core(st, core, xc, yc, s, r, penalty_u, penalty_v, step_scale, tol, trace, scores, max_iter,
+                        max_iter, first=False, solve=False)
     _, done, iters, diverged = ops.admm_shard_status(st)
     if not done:
         iters = max_iter

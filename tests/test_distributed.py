@@ -93,7 +93,7 @@ class NumpyOps:
         x = g.uniform(0.0, 1.0, size=(rows, cols))
         return torch.from_numpy(np.ascontiguousarray(x.T) if transpose else x)
 
-    def admm_shard_begin(self, s, r):
+    def admm_shard_begin(self, s, r, GL, GR):
         return {"s": s, "r": r, "k": 0, "done": 0, "iters": 0, "div": -1,
                 "sums": torch.zeros(2 * (2 * s * r + 4), dtype=torch.float64), "xc": None, "yc": None}
 
@@ -117,7 +117,7 @@ class NumpyOps:
         st["sums"].copy_(torch.from_numpy(np.concatenate(out)))
         return st["sums"]
 
-    def admm_shard_core(self, st, core, xc, yc, s, r, pu, pv, tol, trace, scores, k, max_iter, first, solve):
+    def admm_shard_core(self, st, core, xc, yc, s, r, pu, pv, step, tol, trace, scores, k, max_iter, first, solve):
         if st["done"]:
             return
         sr, ln = s * r, 2 * s * r + 4
