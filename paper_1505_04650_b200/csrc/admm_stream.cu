@@ -296,25 +296,33 @@ __device__ __forceinline__ void small_gemm(int M, int N, int K, const double* A,
 }
 
 // In-place inverse of an SPD r x r matrix (ld r) by Gauss-Jordan without
-// pivoting (the ridge term keeps the pivots >= the penalty).
+// pivoting (the ridge term keeps the pivots >= the penalty). Thread t owns
+// row t / 8 and columns t % 8 + 8 j (no integer division in the r elimination
+// steps; the 1-D version spent ~40 % of the core step's instructions on it).
 __device__ void spd_inverse(double* M, double* piv, int r) {
-  const int tid = threadIdx.x;
+  static_assert(kCT == 512, "64 rows x 8 column lanes");
+  const int tid = threadIdx.x, a = tid >> 3, c8 = tid & 7;
   double* colk = piv + kMaxD;
   for (int k = 0; k < r; ++k) {
     __syncthreads();
     const double inv = 1.0 / M[k * r + k];
-    for (int j = tid; j < r; j += kCT) {
-      piv[j] = M[k * r + j] * inv;  // scaled pivot row
-      colk[j] = M[j * r + k];       // column k before this step overwrites it
+    if (tid < r) {
+      piv[tid] = M[k * r + tid] * inv;  // scaled pivot row
+      colk[tid] = M[tid * r + k];       // column k before this step overwrites it
     }
     __syncthreads();
-    for (int i = tid; i < r * r; i += kCT) {
-      const int a = i / r, c = i % r;
-      if (a == k) {
-        M[i] = (c == k) ? inv : piv[c];
-      } else {
-        const double f = colk[a];
-        M[i] = (c == k) ? -f * inv : fma(-f, piv[c], M[i]);
+    if (a < r) {
+      const double f = colk[a];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int c = c8 + 8 * j;
+        if (c < r) {
+          double* e = M + a * r + c;
+          if (a == k)
+            *e = (c == k) ? inv : piv[c];
+          else
+            *e = (c == k) ? -f * inv : fma(-f, piv[c], *e);
+        }
       }
     }
   }
