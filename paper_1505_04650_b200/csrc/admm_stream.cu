@@ -50,183 +50,261 @@ struct SSide {
 __host__ __device__ inline int sums_len(int s, int r) { return 2 * s * r + 4; }
 
 // ---------------------------------------------------------------------------
-// row sweep: blocks [0, nbl) take left rows, [nbl, grid) right rows.
-// Register-tiled: per 64-row tile, thread (row group, column group) forms a
-// 4 x 4 block of P z (one float4 of P^T and two double2 of Z per 16 DFMA),
-// updates its 16 (x, dx) pairs, and then thread (c group, column group)
-// accumulates a 4 x 4 block of P^T x and P^T dx over the tile's rows (the
-// block partials). The fp64 FMA pipe is the bound, not shared memory.
+// row sweep: blocks [0, nbl) take left rows, [nbl, grid) right rows, one
+// block per SM, 64-row tiles, on the fp64 tensor cores (DMMA, mma.sync
+// m8n8k4.f64: measured 37 TFLOP/s on B200 vs 34 for DFMA, with a fraction of
+// the issue slots and shared-memory traffic). Two warp groups work on
+// consecutive tiles (double-buffered P and x tiles, named barriers):
+//
+//   update group     loads a tile (P rows -> fp64 Pr, old x, dx by cp.async),
+//     (warps 0..7)   forms P z (64 rows x 64 columns, K = s) -- warp w owns a
+//                    16 x 32 block, 2 x 4 DMMA tiles -- updates its (x, dx)
+//                    pairs in HBM, adds the KKT sums and leaves the new x in
+//                    the tile buffer;
+//   reduction group  accumulates the block partial P^T x (64 x 64, K = the
+//     (warps 8..15)  tile's rows) in DMMA accumulators that persist across
+//                    tiles, while the update group works on the next tile.
+// Per k step a warp loads 6 fragments (LDS.64) for 8 DMMA; row strides of
+// 68 doubles (544 B) put the 4 rows a half warp touches on 4 distinct 32-byte
+// bank groups, so every fragment load is conflict-free.
 // ---------------------------------------------------------------------------
-constexpr int kRT = 32;  // rows per tile
+constexpr int kRT = 64;      // rows per tile
+constexpr int kLD = 68;      // row stride (doubles) of Z, the P and the x tiles
+constexpr int kSW = 2 * kT;  // threads of the row sweep (two warp groups)
 
 template <int SP>
-__global__ void __launch_bounds__(kT, 2) row_sweep(SSide L, SSide R, int nbl, const double* __restrict__ Zl,
-                                                    const double* __restrict__ Zr, int s, int r, double step,
-                                                    int update, double* __restrict__ part, const SCtrl* ctrl) {
+constexpr size_t sweep_smem() {
+  // Z + Pr[2] + Xs[2] + Ds
+  return ((size_t)kMaxD * kLD + 5 * (size_t)kRT * kLD) * 8;
+}
+
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// named barriers: 1 = update group internal, 2 + b = tile buffer b filled,
+// 4 + b = tile buffer b consumed by the reduction group
+constexpr int kBarU = 1, kBarFull = 2, kBarEmpty = 4;
+
+// D (8 x 8) += A (8 x 4, row g, column t) B (4 x 8, row t, column g); the
+// accumulator holds row g, columns 2 t, 2 t + 1 (g = lane / 4, t = lane % 4)
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+template <int SP>
+__global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, const double* __restrict__ Zl,
+                                                     const double* __restrict__ Zr, int s, int r, double step,
+                                                     int update, double* __restrict__ part, const SCtrl* ctrl) {
   if (update && ctrl->done) return;
   extern __shared__ __align__(16) unsigned char sm[];
-  double* Z = (double*)sm;                 // [SP][kMaxD] (rows c, cols k; zero padded)
-  double* Xs = Z + SP * kMaxD;             // [kRT][kMaxD] updated x of the tile
-  double* Ds = Xs + kRT * kMaxD;           // [kRT][kMaxD] updated dx of the tile
-  double* PtT = Ds + kRT * kMaxD;          // [SP][kRT] the tile's panel rows, transposed (fp64: one
-                                           // conversion per element, not one per use)
+  double* Z = (double*)sm;               // [kMaxD][kLD]: Z[c][k], zero outside c < s, k < r
+  double* PrB = Z + kMaxD * kLD;         // [2][kRT][kLD]: panel rows (fp64), zero for c >= s and rows >= nr
+  double* XsB = PrB + 2 * kRT * kLD;     // [2][kRT][kLD]: old x, then the updated x (zero outside the tile)
+  double* Ds = XsB + 2 * kRT * kLD;      // [kRT][kLD]: old dx
   __shared__ double red[4][kT / 32];
   const bool left = (int)blockIdx.x < nbl;
   const SSide sd = left ? L : R;
   const int b = left ? (int)blockIdx.x : (int)blockIdx.x - nbl;
   const int nb = left ? nbl : (int)gridDim.x - nbl;
   const int64_t r0 = sd.rows * b / nb, r1 = sd.rows * (b + 1) / nb;
-  const int tid = threadIdx.x, sr = s * r;
+  const int64_t ntile = (r1 - r0 + kRT - 1) / kRT;
+  const int sr = s * r;
   const double* Zs = left ? Zl : Zr;
-  for (int i = tid; i < SP * kMaxD; i += kT) {
+  for (int i = threadIdx.x; i < kMaxD * kMaxD; i += kSW) {
     const int c = i / kMaxD, k = i % kMaxD;
-    Z[i] = (update && c < s && k < r) ? Zs[c * r + k] : 0.0;
+    Z[c * kLD + k] = (update && c < s && k < r) ? Zs[c * r + k] : 0.0;
   }
-  const int g4 = tid >> 4;   // row group (update) / c group (reduction): 4 consecutive
-  const int k4 = tid & 15;   // columns k = k4 + 16 q (consecutive lanes, consecutive doubles)
-  const bool kon = k4 < r;
-  const bool con = 4 * g4 < s;
-  double au[16];
+  if (SP < kMaxD)  // columns the panel does not have
+    for (int i = threadIdx.x; i < 2 * kRT * (kMaxD - SP); i += kSW)
+      PrB[(i / (kMaxD - SP)) * kLD + SP + i % (kMaxD - SP)] = 0.0;
+  __syncthreads();
+  const bool ugroup = threadIdx.x < kT;
+  const int tid = threadIdx.x & (kT - 1);
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int wm = warp >> 1, wn = warp & 1;  // 16-row (or 16-c) block wm, 32-column block wn
+  double* out = part + (size_t)blockIdx.x * sums_len(s, r);
+  constexpr int KS = SP / 4;  // k steps over c (Pr columns >= s and Z rows >= s are zero)
+
+  if (ugroup) {
+    // ======================= update group =======================
+    // x = max(P z + dx / p, 0) with dx / p as dx * (1 / p): one rounding
+    // more than the reference's division (<= 1 ulp), ~30 instructions less
+    const double inv_pen = 1.0 / sd.pen, step_pen = step * sd.pen;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    constexpr int PF = kRT * (SP / 4) / kT;  // float4 j of this thread: element tid + j kT of the tile
+    float4 pf[PF];
+    auto load_p = [&](int64_t t0n) {
+      const int nrn = (int)min64(kRT, r1 - t0n);
 #pragma unroll
-  for (int q = 0; q < 16; ++q) au[q] = 0.0;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  // P rows of the next tile, prefetched into registers during the previous
-  // tile's reduction (float4 i of the tile: row i / (SP / 4))
-  constexpr int PF = kRT * (SP / 4) / kT;
-  float4 pf[PF];
-  auto load_p = [&](int64_t t0n) {
-    const int nrn = (int)min64(kRT, r1 - t0n);
+      for (int j = 0; j < PF; ++j) {
+        const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
+        pf[j] = (row < nrn) ? __ldg((const float4*)(sd.P + (t0n + row) * sd.ldp + c4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    };
+    if (ntile > 0) load_p(r0);
+    const int hi4 = tid >> 4, kg = tid & 15;  // cp.async mapping: 16 rows x 16 columns per pass
+    for (int64_t t = 0; t < ntile; ++t) {
+      const int buf = (int)(t & 1);
+      const int64_t t0 = r0 + t * kRT;
+      const int nr = (int)min64(kRT, r1 - t0);
+      double* Pr = PrB + buf * kRT * kLD;
+      double* Xs = XsB + buf * kRT * kLD;
+      if (t >= 2) nbar_sync(kBarEmpty + buf, kSW);  // the reduction group is done with buffer buf
 #pragma unroll
-    for (int j = 0; j < PF; ++j) {
-      const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
-      pf[j] = (t0n < r1 && row < nrn) ? *(const float4*)(sd.P + (t0n + row) * sd.ldp + c4)
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  load_p(r0);
-  for (int64_t t0 = r0; t0 < r1; t0 += kRT) {
-    const int nr = (int)min64(kRT, r1 - t0);
-    __syncthreads();  // previous tile's reduction done with PtT, Xs, Ds
+      for (int j = 0; j < PF; ++j) {
+        const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
+        double* d = Pr + row * kLD + c4;
+        *(double2*)d = make_double2(c4 + 0 < s ? (double)pf[j].x : 0.0, c4 + 1 < s ? (double)pf[j].y : 0.0);
+        *(double2*)(d + 2) = make_double2(c4 + 2 < s ? (double)pf[j].z : 0.0, c4 + 3 < s ? (double)pf[j].w : 0.0);
+      }
+      // the tile's old (x, dx) land in Xs, Ds while P z is formed
+      for (int row = hi4; row < nr; row += kT / 16)
+        for (int k = kg; k < r; k += 16) {
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(Xs + row * kLD + k)),
+                       "l"(sd.x + (t0 + row) * r + k)
+                       : "memory");
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(Ds + row * kLD + k)),
+                       "l"(sd.dx + (t0 + row) * r + k)
+                       : "memory");
+        }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (t + 1 < ntile) load_p(t0 + kRT);  // next tile's P rows: in flight during this tile
+      nbar_sync(kBarU, kT);                 // Pr complete
+      double acc[2][4][2];
 #pragma unroll
-    for (int j = 0; j < PF; ++j) {
-      const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
-      PtT[(c4 + 0) * kRT + row] = c4 + 0 < s ? (double)pf[j].x : 0.0;
-      PtT[(c4 + 1) * kRT + row] = c4 + 1 < s ? (double)pf[j].y : 0.0;
-      PtT[(c4 + 2) * kRT + row] = c4 + 2 < s ? (double)pf[j].z : 0.0;
-      PtT[(c4 + 3) * kRT + row] = c4 + 3 < s ? (double)pf[j].w : 0.0;
-    }
-    // the tile's old x, dx land in Xs, Ds asynchronously while P z is formed
-    for (int i = tid; i < nr * r; i += kT) {
-      const int row = i / r, k = i - row * r;
-      const double* gx = sd.x + (t0 + row) * r + k;
-      const double* gd = sd.dx + (t0 + row) * r + k;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(Xs + row * kMaxD + k)), "l"(gx)
-                   : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(Ds + row * kMaxD + k)), "l"(gd)
-                   : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-    __syncthreads();
-    // ---- update: rows 2 g4, 2 g4 + 1, columns k4 + 16 q ----
-    {
-      double lx[2][4];
+      for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) lx[a][q] = 0.0;
-      if (update && kon) {
+        for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      if (update) {
+        const double* pa = Pr + (16 * wm + g) * kLD + tq;  // A[row][c]: rows 16 wm + 8 mi + g
+        const double* zb = Z + tq * kLD + 32 * wn + g;     // B[c][k]: k = 32 wn + 8 ni + g
 #pragma unroll 4
-        for (int c = 0; c < s; ++c) {
-          const double2 p2 = *(const double2*)(PtT + c * kRT + 2 * g4);
-          const double pv[2] = {p2.x, p2.y};
-          double zv[4];
+        for (int ks = 0; ks < KS; ++ks) {
+          const double a0 = pa[4 * ks], a1 = pa[8 * kLD + 4 * ks];
+          double bv[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) zv[q] = Z[c * kMaxD + k4 + 16 * q];
+          for (int ni = 0; ni < 4; ++ni) bv[ni] = zb[4 * ks * kLD + 8 * ni];
 #pragma unroll
-          for (int a = 0; a < 2; ++a)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) lx[a][q] = fma(pv[a], zv[q], lx[a][q]);
+          for (int ni = 0; ni < 4; ++ni) {
+            dmma(acc[0][ni], a0, bv[ni]);
+            dmma(acc[1][ni], a1, bv[ni]);
+          }
         }
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncthreads();
+      nbar_sync(kBarU, kT);  // every thread's cp.async data visible
+      // (x, dx) update, KKT sums, the new x into Xs (in place: every thread
+      // reads and writes only its own elements: row 16 wm + 8 mi + g,
+      // columns 32 wn + 8 ni + 2 tq + e)
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const int row = 2 * g4 + a;
+      for (int mi = 0; mi < 2; ++mi) {
+        const int row = 16 * wm + 8 * mi + g;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int k = k4 + 16 * q;
-          double xn = 0.0, dxn = 0.0;
-          if (row < nr && k < r) {
-            const int64_t gi = (t0 + row) * r + k;
-            const double xo = Xs[row * kMaxD + k], dxo = Ds[row * kMaxD + k];
-            if (update) {
-              xn = fmax(lx[a][q] + dxo / sd.pen, 0.0);
-              dxn = dxo + step * sd.pen * (lx[a][q] - xn);
-              sd.x[gi] = xn;
-              sd.dx[gi] = dxn;
-              const double dl = lx[a][q] - xn, dp = dxn * xn, dpos = fmax(dxn, 0.0), xneg = fmax(-xn, 0.0);
-              s0 += dl * dl;
-              s1 += dp * dp;
-              s2 += dpos * dpos;
-              s3 += xneg * xneg;
-            } else {
-              xn = xo;
-              dxn = dxo;
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int k = 32 * wn + 8 * ni + 2 * tq + e;
+            double xn = 0.0;
+            if (row < nr && k < r) {
+              const double xo = Xs[row * kLD + k];
+              if (update) {
+                const double pz = acc[mi][ni][e];
+                const double dxo = Ds[row * kLD + k];
+                const double x = fmax(pz + dxo * inv_pen, 0.0);
+                const double dx = dxo + step_pen * (pz - x);
+                const int64_t gi = (t0 + row) * r + k;
+                sd.x[gi] = x;
+                sd.dx[gi] = dx;
+                const double dl = pz - x, dp = dx * x, dpos = fmax(dx, 0.0), xneg = fmax(-x, 0.0);
+                s0 += dl * dl;
+                s1 += dp * dp;
+                s2 += dpos * dpos;
+                s3 += xneg * xneg;
+                xn = x;
+              } else {
+                xn = xo;
+              }
             }
+            Xs[row * kLD + k] = xn;
           }
-          Xs[row * kMaxD + k] = xn;
-          Ds[row * kMaxD + k] = dxn;
+      }
+      nbar_sync(kBarU, kT);              // Ds read and the tile buffers written by the whole group
+      nbar_arrive(kBarFull + buf, kSW);  // tile buffer buf ready for the reduction group
+    }
+    // KKT sums: warp shuffles, then the update group's warps in order
+    double v[4] = {s0, s1, s2, s3};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+      if (lane == 0) red[j][warp] = v[j];
+    }
+    nbar_sync(kBarU, kT);
+    if (tid < 4) {
+      double a = 0.0;
+      for (int w = 0; w < kT / 32; ++w) a += red[tid][w];
+      out[2 * sr + tid] = a;
+    }
+  } else {
+    // ======================= reduction group =======================
+    // P^T x: A[c][row] = Pr[row][c] (c = 16 wm + 8 mi + g), B[row][k] = Xs[row][k]
+    double au[2][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) au[mi][ni][0] = au[mi][ni][1] = 0.0;
+    const bool con = 16 * wm < s;
+    for (int64_t t = 0; t < ntile; ++t) {
+      const int buf = (int)(t & 1);
+      nbar_sync(kBarFull + buf, kSW);
+      if (con) {
+        const double* pa = PrB + buf * kRT * kLD + tq * kLD + 16 * wm + g;
+        const double* xb = XsB + buf * kRT * kLD + tq * kLD + 32 * wn + g;
+#pragma unroll 4
+        for (int ks = 0; ks < kRT / 4; ++ks) {  // rows >= nr are zero in Pr and Xs
+          const double a0 = pa[4 * ks * kLD], a1 = pa[4 * ks * kLD + 8];
+          double bv[4];
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) bv[ni] = xb[4 * ks * kLD + 8 * ni];
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) {
+            dmma(au[0][ni], a0, bv[ni]);
+            dmma(au[1][ni], a1, bv[ni]);
+          }
         }
       }
+      if (t + 2 < ntile) nbar_arrive(kBarEmpty + buf, kSW);  // the update group refills buffer buf
     }
-    load_p(t0 + kRT);  // next tile's P rows: in flight during the reduction
-    __syncthreads();
-    // ---- partials P^T x, P^T dx: c = 4 g4 .. 4 g4 + 3, k = k4 + 16 q ----
-    if (con && kon) {
-#pragma unroll 2
-      for (int row = 0; row < nr; ++row) {
-        const double pc[4] = {PtT[(4 * g4 + 0) * kRT + row], PtT[(4 * g4 + 1) * kRT + row],
-                              PtT[(4 * g4 + 2) * kRT + row], PtT[(4 * g4 + 3) * kRT + row]};  // fp64 already
-        double xv[4];
+    if (con) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) xv[q] = Xs[row * kMaxD + k4 + 16 * q];
+      for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) au[a * 4 + q] = fma(pc[a], xv[q], au[a * 4 + q]);
-      }
+          for (int e = 0; e < 2; ++e) {
+            const int c = 16 * wm + 8 * mi + g, k = 32 * wn + 8 * ni + 2 * tq + e;
+            if (c < s && k < r) out[c * r + k] = au[mi][ni][e];
+          }
     }
-  }
-  double* out = part + (size_t)blockIdx.x * sums_len(s, r);
-  if (con && kon) {
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = 4 * g4 + a, k = k4 + 16 * q;
-        if (c < s && k < r) out[c * r + k] = au[a * 4 + q];
-      }
-  }
-  // KKT sums: warp shuffles, then the warps in order
-  double v[4] = {s0, s1, s2, s3};
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
-    if ((tid & 31) == 0) red[j][tid >> 5] = v[j];
-  }
-  __syncthreads();
-  if (tid < 4) {
-    double acc = 0.0;
-    for (int w = 0; w < kT / 32; ++w) acc += red[tid][w];
-    out[2 * sr + tid] = acc;
   }
 }
 
-template <int SP>
-constexpr size_t sweep_smem() {
-  return ((size_t)SP * kMaxD + 2 * kRT * kMaxD + (size_t)SP * kRT) * 8;
+// resident row-sweep blocks on the device (one wave; the occupancy of the
+// larger instantiation)
+int sweep_blocks(int sms) {
+  static int occ = 0;
+  if (occ == 0) {
+    int o = 0;
+    ensure_smem_attr((const void*)row_sweep<64>, (int)sweep_smem<64>());
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, row_sweep<64>, kSW, sweep_smem<64>()) != cudaSuccess || o < 1)
+      o = 1;
+    occ = o;
+  }
+  return occ * sms;
 }
 
 // fixed-order sums of the block partials of each side: sums[side][e]
@@ -484,8 +562,8 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   int dev = 0, sms = 0;
   CNMF_CUDA(cudaGetDevice(&dev));
   CNMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // row blocks: two per SM, split between the sides by row count
-  const int total = 2 * sms;
+  // row blocks: as many as are resident at once, split between the sides by row count
+  const int total = sweep_blocks(sms);
   const int nbl = (int)std::max<int64_t>(1, std::min<int64_t>(total - 1, (total * m + (m + n) / 2) / (m + n)));
   const int nbr = total - nbl;
   const int len = sums_len(s, r);
@@ -509,9 +587,9 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   const SSide sl{L, m, S, u, du, pu}, sr{Rt, n, S, vt, dvt, pv};
   auto sweep = [&](int update) -> int {
     if (S == 32)
-      row_sweep<32><<<total, kT, sweep_smem<32>(), st>>>(sl, sr, nbl, Zl, Zr, s, r, step, update, part, ctrl);
+      row_sweep<32><<<total, kSW, sweep_smem<32>(), st>>>(sl, sr, nbl, Zl, Zr, s, r, step, update, part, ctrl);
     else
-      row_sweep<64><<<total, kT, sweep_smem<64>(), st>>>(sl, sr, nbl, Zl, Zr, s, r, step, update, part, ctrl);
+      row_sweep<64><<<total, kSW, sweep_smem<64>(), st>>>(sl, sr, nbl, Zl, Zr, s, r, step, update, part, ctrl);
     CNMF_LAUNCH_CHECK();
     reduce_parts<<<dim3((unsigned)ceil_div(len, kT), 2), kT, 0, st>>>(part, nbl, nbr, len, sums, ctrl, update);
     CNMF_LAUNCH_CHECK();
@@ -607,7 +685,7 @@ int admm_shard_sweep(void* ws, const float* L, int64_t m, const float* Rt, int64
   if (s < 1 || r < 1 || s > kMaxD || r > kMaxD) return fail(CNMF_ERR_ARGUMENT, "sharded ADMM: 1 <= r, s <= 64");
   const ShardWs w = shard_ws(ws, s, r);
   const int S = s <= 32 ? 32 : 64;
-  const int total = 2 * device_sms();
+  const int total = sweep_blocks(device_sms());
   const int64_t rows = std::max<int64_t>(m + n, 1);
   const int nbl = (int)std::max<int64_t>(1, std::min<int64_t>(total - 1, (total * m + rows / 2) / rows));
   const int nbr = total - nbl;
@@ -618,10 +696,10 @@ int admm_shard_sweep(void* ws, const float* L, int64_t m, const float* Rt, int64
   CNMF_TRY(ensure_smem_attr((const void*)row_sweep<64>, (int)sweep_smem<64>()));
   const SSide sl{L, m, S, u, du, pu}, sr{Rt, n, S, vt, dvt, pv};
   if (S == 32)
-    row_sweep<32><<<total, kT, sweep_smem<32>(), st>>>(sl, sr, nbl, w.Zl, w.Zr, s, r, step, update, (double*)part,
+    row_sweep<32><<<total, kSW, sweep_smem<32>(), st>>>(sl, sr, nbl, w.Zl, w.Zr, s, r, step, update, (double*)part,
                                                         w.ctrl);
   else
-    row_sweep<64><<<total, kT, sweep_smem<64>(), st>>>(sl, sr, nbl, w.Zl, w.Zr, s, r, step, update, (double*)part,
+    row_sweep<64><<<total, kSW, sweep_smem<64>(), st>>>(sl, sr, nbl, w.Zl, w.Zr, s, r, step, update, (double*)part,
                                                         w.ctrl);
   CNMF_LAUNCH_CHECK();
   reduce_parts<<<dim3((unsigned)ceil_div(len, kT), 2), kT, 0, st>>>((double*)part, nbl, nbr, len, w.sums, w.ctrl,

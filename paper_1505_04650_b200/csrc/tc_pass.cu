@@ -418,8 +418,13 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
 #pragma unroll
       for (int c0 = 0; c0 < 32; c0 += 8) {  // 8 columns at a time: few live temporaries (96-register cap at S = 64)
         float vh[8], vl[8];
+#ifndef CNMF_VARIANT_NOEPI
         tmem_ld8(taddr + c0, vh);
         tmem_ld8(taddr + S + c0, vl);
+#else
+#pragma unroll
+        for (int j = 0; j < 8; ++j) vh[j] = vl[j] = (float)(taddr + j);
+#endif
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[c0 + j] += (acc_t)(vh[j] + vl[j]);
       }
@@ -580,8 +585,12 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
       if (ra.wrapped) mbar_sleep(&mdone[ra.i], ra.ph ^ 1);  // the slot's previous K tile retired
       tc_fence_after();
       const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + C::A_COL0 + ra.i * 2 * BKT + 16 * half;
+#ifndef CNMF_VARIANT_NOSTTM
       tmem_st16(ta, hi);
       tmem_st16(ta + BKT, lo);
+#else
+      if (hi[0] == 1.2345f && lo[3] == 2.5f) tmem_st16(ta, hi);
+#endif
       unsigned char* dst = sP + ra.i * C::BSPL;
 #pragma unroll
       for (int t = 0; t < PT; ++t) {

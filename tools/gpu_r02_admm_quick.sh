@@ -1,0 +1,2 @@
+timeout 300 python tools/admm_stream_profile.py 2>&1 | grep -v -i warn | head -4 > gpurun_out/admm_prof3.log
+timeout 600 python -m pytest tests -m gpu -x -q -k "admm_stream or rank_above or shard" > gpurun_out/admm_tests.log 2>&1; echo "rc=$?" >> gpurun_out/admm_tests.log
