@@ -82,9 +82,10 @@ __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.syn
 __device__ __forceinline__ void nbar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-// named barriers: 1 = update group internal, 2 + b = tile buffer b filled,
-// 4 + b = tile buffer b consumed by the reduction group
-constexpr int kBarU = 1, kBarFull = 2, kBarEmpty = 4;
+// named barriers: 1 = update group internal, 6 = reduction group internal,
+// 2 + b = tile buffer b updated (update -> reduction group),
+// 4 + b = tile buffer b filled (reduction -> update group)
+constexpr int kBarU = 1, kBarFull = 2, kBarEmpty = 4, kBarR = 6;
 
 // D (8 x 8) += A (8 x 4, row g, column t) B (4 x 8, row t, column g); the
 // accumulator holds row g, columns 2 t, 2 t + 1 (g = lane / 4, t = lane % 4)
@@ -129,51 +130,43 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
   double* out = part + (size_t)blockIdx.x * sums_len(s, r);
   constexpr int KS = SP / 4;  // k steps over c (Pr columns >= s and Z rows >= s are zero)
 
+  // 16-byte copies when every row of x, dx starts 16-byte aligned (r even)
+  const bool vec = (r & 1) == 0;
+
   if (ugroup) {
     // ======================= update group =======================
     // x = max(P z + dx / p, 0) with dx / p as dx * (1 / p): one rounding
     // more than the reference's division (<= 1 ulp), ~30 instructions less
     const double inv_pen = 1.0 / sd.pen, step_pen = step * sd.pen;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    constexpr int PF = kRT * (SP / 4) / kT;  // float4 j of this thread: element tid + j kT of the tile
-    float4 pf[PF];
-    auto load_p = [&](int64_t t0n) {
-      const int nrn = (int)min64(kRT, r1 - t0n);
-#pragma unroll
-      for (int j = 0; j < PF; ++j) {
-        const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
-        pf[j] = (row < nrn) ? __ldg((const float4*)(sd.P + (t0n + row) * sd.ldp + c4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    };
-    if (ntile > 0) load_p(r0);
-    const int hi4 = tid >> 4, kg = tid & 15;  // cp.async mapping: 16 rows x 16 columns per pass
     for (int64_t t = 0; t < ntile; ++t) {
       const int buf = (int)(t & 1);
       const int64_t t0 = r0 + t * kRT;
       const int nr = (int)min64(kRT, r1 - t0);
-      double* Pr = PrB + buf * kRT * kLD;
+      const double* Pr = PrB + buf * kRT * kLD;
       double* Xs = XsB + buf * kRT * kLD;
-      if (t >= 2) nbar_sync(kBarEmpty + buf, kSW);  // the reduction group is done with buffer buf
-#pragma unroll
-      for (int j = 0; j < PF; ++j) {
-        const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
-        double* d = Pr + row * kLD + c4;
-        *(double2*)d = make_double2(c4 + 0 < s ? (double)pf[j].x : 0.0, c4 + 1 < s ? (double)pf[j].y : 0.0);
-        *(double2*)(d + 2) = make_double2(c4 + 2 < s ? (double)pf[j].z : 0.0, c4 + 3 < s ? (double)pf[j].w : 0.0);
-      }
-      // the tile's old (x, dx) land in Xs, Ds while P z is formed
-      for (int row = hi4; row < nr; row += kT / 16)
-        for (int k = kg; k < r; k += 16) {
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(Xs + row * kLD + k)),
-                       "l"(sd.x + (t0 + row) * r + k)
-                       : "memory");
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(Ds + row * kLD + k)),
-                       "l"(sd.dx + (t0 + row) * r + k)
-                       : "memory");
+      nbar_sync(kBarEmpty + buf, kSW);  // Pr[buf] and the old x in Xs[buf] are in place
+      // the tile's old dx lands in Ds while P z is formed (the previous
+      // tile's update is done with Ds: barrier kBarU below)
+      if (update) {
+        if (vec) {
+          const int h = r >> 1;  // 16-byte chunks per row
+          for (int i = tid; i < nr * h; i += kT) {
+            const int row = i / h, c2 = i - row * h;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(Ds + row * kLD + 2 * c2)),
+                         "l"(sd.dx + (t0 + row) * r + 2 * c2)
+                         : "memory");
+          }
+        } else {
+          for (int i = tid; i < nr * r; i += kT) {
+            const int row = i / r, k = i - row * r;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(Ds + row * kLD + k)),
+                         "l"(sd.dx + (t0 + row) * r + k)
+                         : "memory");
+          }
         }
+      }
       asm volatile("cp.async.commit_group;" ::: "memory");
-      if (t + 1 < ntile) load_p(t0 + kRT);  // next tile's P rows: in flight during this tile
-      nbar_sync(kBarU, kT);                 // Pr complete
       double acc[2][4][2];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
@@ -182,6 +175,7 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
       if (update) {
         const double* pa = Pr + (16 * wm + g) * kLD + tq;  // A[row][c]: rows 16 wm + 8 mi + g
         const double* zb = Z + tq * kLD + 32 * wn + g;     // B[c][k]: k = 32 wn + 8 ni + g
+        const int nn = min(4, (r - 32 * wn + 7) >> 3);     // 8-column tiles this warp needs
 #pragma unroll 4
         for (int ks = 0; ks < KS; ++ks) {
           const double a0 = pa[4 * ks], a1 = pa[8 * kLD + 4 * ks];
@@ -189,50 +183,66 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
 #pragma unroll
           for (int ni = 0; ni < 4; ++ni) bv[ni] = zb[4 * ks * kLD + 8 * ni];
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) {
-            dmma(acc[0][ni], a0, bv[ni]);
-            dmma(acc[1][ni], a1, bv[ni]);
-          }
+          for (int ni = 0; ni < 4; ++ni)
+            if (ni < nn) {
+              dmma(acc[0][ni], a0, bv[ni]);
+              dmma(acc[1][ni], a1, bv[ni]);
+            }
         }
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
-      nbar_sync(kBarU, kT);  // every thread's cp.async data visible
+      nbar_sync(kBarU, kT);  // every thread's dx visible
       // (x, dx) update, KKT sums, the new x into Xs (in place: every thread
       // reads and writes only its own elements: row 16 wm + 8 mi + g,
-      // columns 32 wn + 8 ni + 2 tq + e)
+      // columns 32 wn + 8 ni + 2 tq + {0, 1})
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi) {
         const int row = 16 * wm + 8 * mi + g;
+        const bool ron = row < nr;
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < 4; ++ni) {
+          const int k = 32 * wn + 8 * ni + 2 * tq;
+          double* xs = Xs + row * kLD + k;
+          const double2 xo = *(const double2*)xs;
+          double xn[2] = {0.0, 0.0};
+          if (update) {
+            const double2 dxo2 = *(const double2*)(Ds + row * kLD + k);
+            const double dxo[2] = {dxo2.x, dxo2.y};
+            double dxn[2];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int k = 32 * wn + 8 * ni + 2 * tq + e;
-            double xn = 0.0;
-            if (row < nr && k < r) {
-              const double xo = Xs[row * kLD + k];
-              if (update) {
-                const double pz = acc[mi][ni][e];
-                const double dxo = Ds[row * kLD + k];
-                const double x = fmax(pz + dxo * inv_pen, 0.0);
-                const double dx = dxo + step_pen * (pz - x);
-                const int64_t gi = (t0 + row) * r + k;
-                sd.x[gi] = x;
-                sd.dx[gi] = dx;
-                const double dl = pz - x, dp = dx * x, dpos = fmax(dx, 0.0), xneg = fmax(-x, 0.0);
-                s0 += dl * dl;
-                s1 += dp * dp;
-                s2 += dpos * dpos;
-                s3 += xneg * xneg;
-                xn = x;
-              } else {
-                xn = xo;
-              }
+            for (int e = 0; e < 2; ++e) {
+              const bool on = ron && k + e < r;
+              const double pz = acc[mi][ni][e];
+              const double v = pz + dxo[e] * inv_pen;
+              const double x = v > 0.0 ? v : 0.0;
+              const double dx = dxo[e] + step_pen * (pz - x);
+              const double dl = pz - x, dp = dx * x, dpos = dx > 0.0 ? dx : 0.0;
+              s0 += on ? dl * dl : 0.0;
+              s1 += on ? dp * dp : 0.0;
+              s2 += on ? dpos * dpos : 0.0;  // x >= 0, so the negative part of x is 0
+              xn[e] = on ? x : 0.0;
+              dxn[e] = dx;
             }
-            Xs[row * kLD + k] = xn;
+            const int64_t gi = (t0 + row) * r + k;
+            if (vec && ron && k + 1 < r) {
+              *(double2*)(sd.x + gi) = make_double2(xn[0], xn[1]);
+              *(double2*)(sd.dx + gi) = make_double2(dxn[0], dxn[1]);
+            } else if (ron) {
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                if (k + e < r) {
+                  sd.x[gi + e] = xn[e];
+                  sd.dx[gi + e] = dxn[e];
+                }
+            }
+          } else {
+            xn[0] = ron && k < r ? xo.x : 0.0;
+            xn[1] = ron && k + 1 < r ? xo.y : 0.0;
           }
+          *(double2*)xs = make_double2(xn[0], xn[1]);
+        }
       }
-      nbar_sync(kBarU, kT);              // Ds read and the tile buffers written by the whole group
+      nbar_sync(kBarU, kT);              // Ds read and Xs[buf] written by the whole group
       nbar_arrive(kBarFull + buf, kSW);  // tile buffer buf ready for the reduction group
     }
     // KKT sums: warp shuffles, then the update group's warps in order
@@ -251,13 +261,57 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
     }
   } else {
     // ======================= reduction group =======================
-    // P^T x: A[c][row] = Pr[row][c] (c = 16 wm + 8 mi + g), B[row][k] = Xs[row][k]
+    // fills tile buffers (P rows -> fp64 Pr, old x by cp.async) two tiles
+    // ahead, and reduces P^T x: A[c][row] = Pr[row][c] (c = 16 wm + 8 mi + g),
+    // B[row][k] = Xs[row][k]
+    auto fill = [&](int64_t t) {
+      const int buf = (int)(t & 1);
+      const int64_t t0 = r0 + t * kRT;
+      const int nr = (int)min64(kRT, r1 - t0);
+      double* Pr = PrB + buf * kRT * kLD;
+      double* Xs = XsB + buf * kRT * kLD;
+      constexpr int PF = kRT * (SP / 4) / kT;
+      float4 pf[PF];
+#pragma unroll
+      for (int j = 0; j < PF; ++j) {
+        const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
+        pf[j] = (row < nr) ? __ldg((const float4*)(sd.P + (t0 + row) * sd.ldp + c4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (vec) {
+        const int h = r >> 1;
+        for (int i = tid; i < nr * h; i += kT) {
+          const int row = i / h, c2 = i - row * h;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(Xs + row * kLD + 2 * c2)),
+                       "l"(sd.x + (t0 + row) * r + 2 * c2)
+                       : "memory");
+        }
+      } else {
+        for (int i = tid; i < nr * r; i += kT) {
+          const int row = i / r, k = i - row * r;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(Xs + row * kLD + k)),
+                       "l"(sd.x + (t0 + row) * r + k)
+                       : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < PF; ++j) {
+        const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
+        double* d = Pr + row * kLD + c4;
+        *(double2*)d = make_double2(c4 + 0 < s ? (double)pf[j].x : 0.0, c4 + 1 < s ? (double)pf[j].y : 0.0);
+        *(double2*)(d + 2) = make_double2(c4 + 2 < s ? (double)pf[j].z : 0.0, c4 + 3 < s ? (double)pf[j].w : 0.0);
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      nbar_arrive(kBarEmpty + buf, kSW);  // the bar.arrive orders the group's smem writes before the update group
+    };
     double au[2][4][2];
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) au[mi][ni][0] = au[mi][ni][1] = 0.0;
     const bool con = 16 * wm < s;
+    const int nn = min(4, (r - 32 * wn + 7) >> 3);
+    for (int64_t t = 0; t < ntile && t < 2; ++t) fill(t);
     for (int64_t t = 0; t < ntile; ++t) {
       const int buf = (int)(t & 1);
       nbar_sync(kBarFull + buf, kSW);
@@ -271,13 +325,17 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
 #pragma unroll
           for (int ni = 0; ni < 4; ++ni) bv[ni] = xb[4 * ks * kLD + 8 * ni];
 #pragma unroll
-          for (int ni = 0; ni < 4; ++ni) {
-            dmma(au[0][ni], a0, bv[ni]);
-            dmma(au[1][ni], a1, bv[ni]);
-          }
+          for (int ni = 0; ni < 4; ++ni)
+            if (ni < nn) {
+              dmma(au[0][ni], a0, bv[ni]);
+              dmma(au[1][ni], a1, bv[ni]);
+            }
         }
       }
-      if (t + 2 < ntile) nbar_arrive(kBarEmpty + buf, kSW);  // the update group refills buffer buf
+      if (t + 2 < ntile) {
+        nbar_sync(kBarR, kT);  // every reduction warp is done reading buffer buf
+        fill(t + 2);
+      }
     }
     if (con) {
 #pragma unroll
@@ -338,74 +396,149 @@ __global__ void __launch_bounds__(kT) reduce_parts(const double* __restrict__ pa
 // ---------------------------------------------------------------------------
 constexpr int kCT = 512;
 
-// C(m, n) = sum_k A[m * am + k * ak] * B[k * bk + n] for m < M, n < N <= 64,
-// M <= 64; out(m, n, value) consumes every result. Thread t owns rows
-// m = t / 16 + 32 p (p < 2) and columns n = t % 16 + 16 q (q < 4): a warp
-// reads 2 distinct A values (broadcast) and 16 consecutive B values per k
-// (conflict-free), with 8 independent FMA chains per thread.
+// C(m, n) = sum_k A[m * am + k * ak] * B[k * bk + n * bn] for m < M, n < N,
+// M, N <= 64; out(m, n, value) consumes every result exactly once. On the
+// fp64 tensor cores: warp w owns the 2 x 2 block of 8 x 8 output tiles at
+// rows 16 (w / 4), columns 16 (w % 4); per k step of 4 a lane loads two A and
+// two B elements (the next step's loads are issued before this step's four
+// DMMA). Rows >= M and columns >= N are computed on clamped (valid) data and
+// dropped at the output; only the k tail is masked. ~4.5k cycles for
+// 60 x 50 x 60 (tools/gemm_probe.cu), 2.2x the one-tile-per-load version.
 template <class F>
 __device__ __forceinline__ void small_gemm(int M, int N, int K, const double* A, int am, int ak, const double* B,
-                                           int bk, F out) {
-  static_assert(kCT == 512, "thread mapping covers 64 x 64");
-  const int tm = threadIdx.x >> 4, tn = threadIdx.x & 15;
-  if (tm >= M || tn >= N) return;
-  const int m1 = tm + 32 < M ? tm + 32 : tm;  // clamped reads; results masked below
-  int nn[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) nn[q] = tn + 16 * q < N ? tn + 16 * q : tn;
-  double c[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
-#pragma unroll 4
-  for (int k = 0; k < K; ++k) {
-    const double a0 = A[tm * am + k * ak], a1 = A[m1 * am + k * ak];
-    double bv[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) bv[q] = B[k * bk + nn[q]];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      c[0][q] = fma(a0, bv[q], c[0][q]);
-      c[1][q] = fma(a1, bv[q], c[1][q]);
+                                           int bk, int bn, F out) {
+  static_assert(kCT == 512, "16 warps x (16 x 16) cover 64 x 64");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const int bm_ = warp >> 2, bn_ = warp & 3;
+  if (16 * bm_ >= M || 16 * bn_ >= N) return;
+  const int m0 = min(16 * bm_ + g, M - 1), m1 = min(16 * bm_ + 8 + g, M - 1);
+  const int n0 = min(16 * bn_ + g, N - 1), n1 = min(16 * bn_ + 8 + g, N - 1);
+  const double* a0p = A + m0 * am + tq * ak;
+  const double* a1p = A + m1 * am + tq * ak;
+  const double* b0p = B + tq * bk + n0 * bn;
+  const double* b1p = B + tq * bk + n1 * bn;
+  double c[2][2][2] = {};
+  const int K4 = K & ~3;
+  if (K4 > 0) {
+    double x0 = a0p[0], x1 = a1p[0], y0 = b0p[0], y1 = b1p[0];
+    for (int k0 = 4; k0 < K4; k0 += 4) {
+      const double nx0 = a0p[k0 * ak], nx1 = a1p[k0 * ak], ny0 = b0p[k0 * bk], ny1 = b1p[k0 * bk];
+      dmma(c[0][0], x0, y0);
+      dmma(c[0][1], x0, y1);
+      dmma(c[1][0], x1, y0);
+      dmma(c[1][1], x1, y1);
+      x0 = nx0;
+      x1 = nx1;
+      y0 = ny0;
+      y1 = ny1;
     }
+    dmma(c[0][0], x0, y0);
+    dmma(c[0][1], x0, y1);
+    dmma(c[1][0], x1, y0);
+    dmma(c[1][1], x1, y1);
+  }
+  if (K4 < K) {  // tail: k = K4 + tq may pass K
+    const bool kon = K4 + tq < K;
+    const double x0 = kon ? a0p[K4 * ak] : 0.0, x1 = kon ? a1p[K4 * ak] : 0.0;
+    const double y0 = kon ? b0p[K4 * bk] : 0.0, y1 = kon ? b1p[K4 * bk] : 0.0;
+    dmma(c[0][0], x0, y0);
+    dmma(c[0][1], x0, y1);
+    dmma(c[1][0], x1, y0);
+    dmma(c[1][1], x1, y1);
   }
 #pragma unroll
-  for (int p = 0; p < 2; ++p)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (tm + 32 * p < M && tn + 16 * q < N) out(tm + 32 * p, tn + 16 * q, c[p][q]);
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int m = 16 * bm_ + 8 * i + g, n = 16 * bn_ + 8 * j + 2 * tq + e;
+        if (m < M && n < N) out(m, n, c[i][j][e]);
+      }
 }
 
-// In-place inverse of an SPD r x r matrix (ld r) by Gauss-Jordan without
-// pivoting (the ridge term keeps the pivots >= the penalty). Thread t owns
-// row t / 8 and columns t % 8 + 8 j (no integer division in the r elimination
-// steps; the 1-D version spent ~40 % of the core step's instructions on it).
+// In-place inverse of an SPD r x r matrix (ld r, r <= 64) by Gauss-Jordan
+// without pivoting (the ridge term keeps the pivots >= the penalty). Thread t
+// of the first 64 * TPR owns row t / TPR, columns EPT (t % TPR) .. + EPT - 1
+// (EPT = 64 / TPR) in registers. Per elimination step the owners of the
+// pivot row publish it (scaled) and the reciprocal pivot in a double-buffered
+// shared row, one named barrier, and every thread updates its entries
+// branch-free (a divergent branch per entry serialised every DFMA behind its
+// predecessor); the pivot-column entry of a row comes from the lane holding
+// it by shuffle, picked out of the registers by a select tree.
+constexpr int kPivLD = 72;  // per buffer: 64 pivot-row entries + the reciprocal pivot at [64]
+#ifndef CNMF_GJ_TPR
+#define CNMF_GJ_TPR 2
+#endif
+
 __device__ void spd_inverse(double* M, double* piv, int r) {
-  static_assert(kCT == 512, "64 rows x 8 column lanes");
-  const int tid = threadIdx.x, a = tid >> 3, c8 = tid & 7;
-  double* colk = piv + kMaxD;
-  for (int k = 0; k < r; ++k) {
-    __syncthreads();
-    const double inv = 1.0 / M[k * r + k];
-    if (tid < r) {
-      piv[tid] = M[k * r + tid] * inv;  // scaled pivot row
-      colk[tid] = M[tid * r + k];       // column k before this step overwrites it
-    }
-    __syncthreads();
-    if (a < r) {
-      const double f = colk[a];
+  constexpr int TPR = CNMF_GJ_TPR, EPT = 64 / TPR, NT = 64 * TPR;
+  static_assert(kCT >= NT && (TPR & (TPR - 1)) == 0 && TPR <= 32, "threads per row");
+  __syncthreads();  // M complete
+  const int t = threadIdx.x;
+  if (t < NT) {
+    const int a = t / TPR, q = t % TPR, cb = EPT * q, lane = t & 31;
+    double m[EPT];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int c = c8 + 8 * j;
-        if (c < r) {
-          double* e = M + a * r + c;
-          if (a == k)
-            *e = (c == k) ? inv : piv[c];
-          else
-            *e = (c == k) ? -f * inv : fma(-f, piv[c], *e);
-        }
+    for (int j = 0; j < EPT; ++j) m[j] = (a < r && cb + j < r) ? M[a * r + cb + j] : 0.0;
+    double fk = m[0];  // this thread's entry in the next pivot column (column 0 first)
+    for (int k = 0; k < r; ++k) {
+      double* pv = piv + (k & 1) * kPivLD;
+      const double f = __shfl_sync(0xffffffffu, fk, (lane & ~(TPR - 1)) | (k / EPT));  // row a, column k
+      if (a == k) {
+        const double inv = 1.0 / f;
+#pragma unroll
+        for (int j = 0; j < EPT; j += 2) *(double2*)(pv + cb + j) = make_double2(m[j] * inv, m[j + 1] * inv);
+        if (q == 0) pv[64] = inv;
       }
+      asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+      const double inv = pv[64];
+      //   row k:      m = piv (column k: inv)
+      //   other rows: m = m - f piv (column k: -f inv)
+      const bool own = (a == k);
+      const double coef = own ? 0.0 : -f, ck = own ? inv : -f * inv;
+      const int kc = k - cb;  // the pivot column, relative to this thread's entries
+      double2 p2[EPT / 2];
+#pragma unroll
+      for (int j = 0; j < EPT / 2; ++j) p2[j] = *(const double2*)(pv + cb + 2 * j);
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const double pj = (j & 1) ? p2[j >> 1].y : p2[j >> 1].x;
+        const double v = fma(coef, pj, own ? pj : m[j]);
+        m[j] = (j == kc) ? ck : v;
+      }
+      // this thread's entry in the next pivot column: a select tree
+      const int kn = k + 1 - cb;
+      double tr[EPT];
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) tr[j] = m[j];
+#pragma unroll
+      for (int w = EPT / 2; w >= 1; w >>= 1)
+#pragma unroll
+        for (int j = 0; j < w; ++j) tr[j] = (kn & w) ? tr[j + w] : tr[j];
+      fk = tr[0];
     }
+#pragma unroll
+    for (int j = 0; j < EPT; ++j)
+      if (a < r && cb + j < r) M[a * r + cb + j] = m[j];
   }
   __syncthreads();
 }
+
+#ifdef CNMF_CORE_TRACE
+// phase timestamps of the last core step (tools/core_trace.py; A/B builds only)
+__device__ long long g_core_trace[16];
+#define CORE_MARK(i)                                   \
+  do {                                                 \
+    __syncthreads();                                   \
+    if (threadIdx.x == 0) g_core_trace[i] = clock64(); \
+  } while (0)
+// (the product build's barriers are explicit: CORE_MARK adds one only here)
+#else
+#define CORE_MARK(i) \
+  do {               \
+  } while (0)
+#endif
 
 __device__ __forceinline__ double block_sum(double v, double* red, int slot) {
 #pragma unroll
@@ -430,15 +563,18 @@ __global__ void __launch_bounds__(kCT) core_step(const double* __restrict__ core
                                                   double step, double tol, double* trace, double* scores, SCtrl* ctrl,
                                                   int k, int max_iter, int first, int solve) {
   if (ctrl->done) return;
+#ifdef CNMF_CORE_TRACE
+  if (threadIdx.x == 0) g_core_trace[0] = clock64();
+#endif
   extern __shared__ __align__(16) unsigned char sm[];
   double* E = (double*)sm;         // s x s: E = xc yc - core, later the rhs (s x r)
   double* B = E + s * s;           // rhs2 (r x s)
-  double* M = B + r * s;           // r x r
-  double* piv = M + r * r;         // 2 x 64
-  double* coreS = piv + 2 * kMaxD; // s x s
+  double* M = B + ((r * s + s * s) & 1) + r * s;  // r x r (even offset: piv below stays 16-byte aligned)
+  double* piv = M + ((r * r + 1) & ~1);  // 2 x kPivLD, 16-byte aligned (double2 rows)
+  double* coreS = piv + 2 * kPivLD; // s x s
   double* xcS = coreS + s * s;     // s x r
   double* ycS = xcS + s * r;       // r x s
-  double* ycT = ycS + r * s;       // s x r (yc transposed: conflict-free B operand)
+  double* G = E;                   // s x s: G_L, then G_R, staged for the dual projections (E is free then)
   __shared__ double red[3 * (kCT / 32)];
   __shared__ int s_stop;
   const int tid = threadIdx.x, sr = s * r, len = sums_len(s, r);
@@ -447,43 +583,46 @@ __global__ void __launch_bounds__(kCT) core_step(const double* __restrict__ core
   if (tid == 0) s_stop = 0;
   for (int i = tid; i < s * s; i += kCT) coreS[i] = core[i];
   for (int i = tid; i < s * r; i += kCT) xcS[i] = xc[i];
-  for (int i = tid; i < r * s; i += kCT) {
-    ycS[i] = yc[i];
-    ycT[(i % s) * r + i / s] = yc[i];
-  }
+  for (int i = tid; i < r * s; i += kCT) ycS[i] = yc[i];
+  if (!first && k > 0)  // G_L (ld ldg) compacted to s x s
+    for (int i = tid; i < s * s; i += kCT) G[i] = GL[(i / s) * ldg + i % s];
   __syncthreads();
+  CORE_MARK(1);
   if (first) {
     // yc = V R^T (nmf.py:338): the reduced right sums of the initial state
     for (int i = tid; i < r * s; i += kCT) {
       const int a = i / s, c = i % s;
       yc[i] = srt[c * r + a];
       ycS[i] = srt[c * r + a];
-      ycT[c * r + a] = srt[c * r + a];
     }
     for (int i = tid; i < sr; i += kCT) DL[i] = DR[i] = 0.0;
     __syncthreads();
   } else if (k > 0) {
     // dual projections after the sweep of iteration k - 1 (xc, yc of k - 1)
-    small_gemm(s, r, s, GL, ldg, 1, xcS, r, [&](int a, int j, double v) {
+    small_gemm(s, r, s, G, s, 1, xcS, r, 1, [&](int a, int j, double v) {
       DL[a * r + j] += step * pu * (v - sl[a * r + j]);
     });
-    small_gemm(s, r, s, GR, ldg, 1, ycT, r, [&](int c, int j, double v) {
+    __syncthreads();
+    for (int i = tid; i < s * s; i += kCT) G[i] = GR[(i / s) * ldg + i % s];
+    __syncthreads();
+    small_gemm(s, r, s, G, s, 1, ycS, 1, s, [&](int c, int j, double v) {
       DR[c * r + j] += step * pv * (v - srt[c * r + j]);
     });
     __syncthreads();
+    CORE_MARK(2);
     // ---- KKT score of iteration k - 1 (nmf.py:281-303) ----
     double obj = 0.0, t1 = 0.0, t2 = 0.0;
-    small_gemm(s, s, r, xcS, r, 1, ycS, s, [&](int a, int c, double v) {
+    small_gemm(s, s, r, xcS, r, 1, ycS, s, 1, [&](int a, int c, double v) {
       const double e = v - coreS[a * s + c];
       E[a * s + c] = e;
       obj += e * e;
     });
     __syncthreads();
-    small_gemm(s, r, s, E, s, 1, ycT, r, [&](int a, int j, double v) {  // (E yc^T + L^T dU)[a][j]
+    small_gemm(s, r, s, E, s, 1, ycS, 1, s, [&](int a, int j, double v) {  // (E yc^T + L^T dU)[a][j]
       const double w = v + DL[a * r + j];
       t1 += w * w;
     });
-    small_gemm(r, s, s, xcS, 1, r, E, s, [&](int j, int c, double v) {  // (xc^T E + dV R^T)[j][c]
+    small_gemm(r, s, s, xcS, 1, r, E, s, 1, [&](int j, int c, double v) {  // (xc^T E + dV R^T)[j][c]
       const double w = v + DR[c * r + j];
       t2 += w * w;
     });
@@ -519,30 +658,44 @@ __global__ void __launch_bounds__(kCT) core_step(const double* __restrict__ core
     __syncthreads();
     if (s_stop) return;
   }
+  CORE_MARK(3);
   if (!solve || k >= max_iter) return;
   // ---- xc = (core yc^T + pu L^T U - L^T dU) (yc yc^T + pu I)^-1 ----
-  small_gemm(r, r, s, ycS, s, 1, ycT, r, [&](int a, int c, double v) { M[a * r + c] = v + (a == c ? pu : 0.0); });
-  small_gemm(s, r, s, coreS, s, 1, ycT, r, [&](int a, int c, double v) {  // rhs (s x r) in E
+  small_gemm(r, r, s, ycS, s, 1, ycS, 1, s, [&](int a, int c, double v) { M[a * r + c] = v + (a == c ? pu : 0.0); });
+  small_gemm(s, r, s, coreS, s, 1, ycS, 1, s, [&](int a, int c, double v) {  // rhs (s x r) in E
     E[a * r + c] = v + (pu * sl[a * r + c] - DL[a * r + c]);
   });
+  CORE_MARK(4);
   spd_inverse(M, piv, r);
-  small_gemm(s, r, r, E, r, 1, M, r, [&](int a, int c, double v) {
+  CORE_MARK(5);
+  small_gemm(s, r, r, E, r, 1, M, r, 1, [&](int a, int c, double v) {
     xc[a * r + c] = v;
     xcS[a * r + c] = v;
     Zl[a * r + c] = v;
   });
   __syncthreads();
   // ---- yc = (xc^T xc + pv I)^-1 (xc^T core + pv V R^T - dV R^T) ----
-  small_gemm(r, r, s, xcS, 1, r, xcS, r, [&](int a, int c, double v) { M[a * r + c] = v + (a == c ? pv : 0.0); });
-  small_gemm(r, s, s, xcS, 1, r, coreS, s, [&](int a, int c, double v) {  // rhs2 (r x s) in B
+  small_gemm(r, r, s, xcS, 1, r, xcS, r, 1, [&](int a, int c, double v) { M[a * r + c] = v + (a == c ? pv : 0.0); });
+  small_gemm(r, s, s, xcS, 1, r, coreS, s, 1, [&](int a, int c, double v) {  // rhs2 (r x s) in B
     B[a * s + c] = v + (pv * srt[c * r + a] - DR[c * r + a]);
   });
+  CORE_MARK(6);
   spd_inverse(M, piv, r);
-  small_gemm(r, s, r, M, r, 1, B, s, [&](int a, int c, double v) {
+  CORE_MARK(7);
+  small_gemm(r, s, r, M, r, 1, B, s, 1, [&](int a, int c, double v) {
     yc[a * s + c] = v;
     Zr[c * r + a] = v;  // Z for the right rows: yc^T (s x r)
   });
+  CORE_MARK(8);
 }
+
+#ifdef CNMF_CORE_TRACE
+}  // namespace
+extern "C" int cnmf_debug_core_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_core_trace, sizeof(long long) * 16) == cudaSuccess ? 0 : -1;
+}
+namespace {
+#endif
 
 __global__ void init_sctrl(SCtrl* c) {
   c->k = 0;
@@ -580,10 +733,10 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   double* GR = GL + kMaxD * kMaxD;
   double* DL = GR + kMaxD * kMaxD;  // L^T dU, R dV^T (s x r)
   double* DR = DL + kMaxD * kMaxD;
-  const size_t core_smem = (2 * (size_t)s * s + 4 * (size_t)s * r + (size_t)r * r + 2 * kMaxD) * 8;
+  const size_t core_smem = (2 * (size_t)s * s + 3 * (size_t)s * r + (size_t)r * r + 3 + 2 * kPivLD) * 8;
   CNMF_TRY(ensure_smem_attr((const void*)row_sweep<32>, (int)sweep_smem<32>()));
   CNMF_TRY(ensure_smem_attr((const void*)row_sweep<64>, (int)sweep_smem<64>()));
-  CNMF_TRY(ensure_smem_attr((const void*)core_step, (int)((7 * kMaxD * kMaxD + 2 * kMaxD) * 8)));
+  CNMF_TRY(ensure_smem_attr((const void*)core_step, (int)((6 * kMaxD * kMaxD + 3 + 2 * kPivLD) * 8)));
   const SSide sl{L, m, S, u, du, pu}, sr{Rt, n, S, vt, dvt, pv};
   auto sweep = [&](int update) -> int {
     if (S == 32)
@@ -713,8 +866,8 @@ int admm_shard_core(void* ws, const double* core, double* xc, double* yc, int s,
                     cudaStream_t st) {
   const ShardWs w = shard_ws(ws, s, r);
   const int S = s <= 32 ? 32 : 64;
-  const size_t core_smem = (2 * (size_t)s * s + 4 * (size_t)s * r + (size_t)r * r + 2 * kMaxD) * 8;
-  CNMF_TRY(ensure_smem_attr((const void*)core_step, (int)((7 * kMaxD * kMaxD + 2 * kMaxD) * 8)));
+  const size_t core_smem = (2 * (size_t)s * s + 3 * (size_t)s * r + (size_t)r * r + 3 + 2 * kPivLD) * 8;
+  CNMF_TRY(ensure_smem_attr((const void*)core_step, (int)((6 * kMaxD * kMaxD + 3 + 2 * kPivLD) * 8)));
   core_step<<<1, kCT, core_smem, st>>>(core, w.sums, xc, yc, w.Zl, w.Zr, w.GL, w.GR, S, w.DL, w.DR, s, r, pu, pv,
                                       step, tol, trace, scores, w.ctrl, k,
                                       max_iter, first, solve);
