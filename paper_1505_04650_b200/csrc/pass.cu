@@ -426,6 +426,8 @@ static bool use_tc(int S) {
   return g_pass_mode == 1 && (S == 32 || S == 64);
 }
 
+bool pass_uses_tc(int S) { return use_tc(S); }
+
 int pass_forward(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y,
                  cudaStream_t st) {
   if (use_tc(S)) return pass_forward_tc(A, m, n, lda, X, S, Y, st);

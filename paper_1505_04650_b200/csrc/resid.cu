@@ -8,8 +8,10 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "pass.cuh"
 
 namespace cnmf {
+int gram_tn_f64(const double* X, int64_t p, int a, const double* Y, int b, double* out, cudaStream_t st);
 namespace {
 
 constexpr int kRM = 64, kRN = 128, kRT = 256, kRMax = 64;
@@ -26,7 +28,8 @@ constexpr int kChunk = 16;
 
 __global__ void __launch_bounds__(kRT)
     resid_kernel(const float* __restrict__ A, int64_t m, int64_t n, int64_t lda, const float* __restrict__ xf,
-                 const float* __restrict__ yf, int r, double* __restrict__ out) {
+                 const float* __restrict__ yf, int r, double* __restrict__ out, const int* __restrict__ skip) {
+  if (skip != nullptr && *skip) return;  // the pass path's result stands
   extern __shared__ __align__(16) float rsm[];
   float(*Xs)[kRMax + 1] = (float(*)[kRMax + 1])rsm;               // kRM x (r + 1)
   float(*Ys)[kRN] = (float(*)[kRN])(rsm + kRM * (kRMax + 1));     // r x kRN
@@ -139,7 +142,8 @@ __global__ void __launch_bounds__(kRT)
 // (cols != null); yf (n x r) = Yt
 __global__ void factors_f32(const float* __restrict__ A, int64_t m, int64_t lda, const double* __restrict__ X,
                             const int64_t* __restrict__ cols, int64_t n, const double* __restrict__ Yt, int r,
-                            float* __restrict__ xf, float* __restrict__ yf) {
+                            float* __restrict__ xf, float* __restrict__ yf, const int* __restrict__ skip) {
+  if (skip != nullptr && *skip) return;
   const int64_t tot = (m + n) * r;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < m * r) {
@@ -153,17 +157,130 @@ __global__ void factors_f32(const float* __restrict__ A, int64_t m, int64_t lda,
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Pass path: ||A - X Y||^2 = ||A||^2 - 2 <A Y^T, X> + <X^T X, Y Y^T>, with
+// A Y^T and ||A||^2 from ONE tensor-core forward pass over A (the streaming
+// pass kernel, 3xTF32, the squares summed by its splitters) -- the direct
+// kernel is FP32-FFMA bound (2 m n r flops; 72 ms at configs[4]), the pass is
+// HBM bound. The expansion cancels: it is used only when the residual is
+// large enough that the pass's rounding (<= 1e-6 of <A Y^T, X>, estimated
+// conservatively; fp32-level products of nonnegative data) stays below 1e-4
+// of the residual; otherwise the combine kernel leaves the flag clear and the
+// direct kernel runs (graph-capturable: the decision stays on the device).
+// ---------------------------------------------------------------------------
+__global__ void yt_panel(const double* __restrict__ Yt, int64_t n, int r, int S, float* __restrict__ P) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * S; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / S;
+    const int k = (int)(i - row * S);
+    P[i] = k < r ? (float)Yt[row * r + k] : 0.f;
+  }
+}
+
+__global__ void gather_cols_f64(const float* __restrict__ A, int64_t m, int64_t lda, const int64_t* __restrict__ cols,
+                                int r, double* __restrict__ X) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m * r; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / r;
+    X[i] = (double)A[row * lda + cols[i - row * r]];
+  }
+}
+
+// acc[1] += sum_{i < m, k < r} T[i][k] X[i][k]
+__global__ void __launch_bounds__(256) dot_tx(const float* __restrict__ T, int64_t m, int S, const double* __restrict__ X,
+                                              int r, double* __restrict__ acc) {
+  __shared__ double red[8];
+  double v = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m * r; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / r;
+    v = fma((double)T[row * S + (i - row * r)], X[i], v);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    atomicAdd(&acc[1], t);
+  }
+}
+
+// acc = {||A||^2, <A Y^T, X>}, G1 = X^T X, G2 = Y Y^T (r x r): out and the
+// skip flag when the expansion is accurate enough, else zeroed out / flag 0
+__global__ void resid_combine(const double* __restrict__ acc, const double* __restrict__ G1,
+                              const double* __restrict__ G2, int r, double* __restrict__ out, int* __restrict__ skip) {
+  __shared__ double red[8];
+  double g = 0.0;
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) g = fma(G1[i], G2[i], g);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = g;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    const double a2 = acc[0], d = acc[1];
+    const double res = a2 - 2.0 * d + t;
+    const bool ok = res > 0.0 && 1e-6 * fabs(d) <= 1e-4 * res;
+    out[0] = ok ? res : 0.0;
+    out[1] = ok ? a2 : 0.0;
+    *skip = ok ? 1 : 0;
+  }
+}
+
+bool resid_pass_enabled(int64_t m, int64_t n, int r) {
+  const char* e = getenv("CNMF_RESID_PASS");  // "0": direct kernel only (A/B and tests)
+  const int mode = (e && e[0] == '0') ? 0 : 1;
+  // the pass path pays off where the direct kernel's 2 m n r flops exceed the
+  // pass's read of A (r >= 8) on matrices large enough to amortise its launches
+  return mode == 1 && r >= 8 && r <= 64 && (double)m * (double)n >= (double)(1 << 26) && pass_uses_tc(r <= 32 ? 32 : 64);
+}
+
 int residual_norms(const float* A, int64_t m, int64_t n, int64_t lda, const double* X, const int64_t* cols,
                    const double* Yt, int r, double* out, cudaStream_t st) {
   if (r < 1 || r > kRMax) return fail(CNMF_ERR_ARGUMENT, "residual_norms: 1 <= r <= 64");
   if ((X == nullptr) == (cols == nullptr)) return fail(CNMF_ERR_ARGUMENT, "give exactly one of X and cols");
-  CNMF_CUDA(cudaMemsetAsync(out, 0, 16, st));
+  const int* skip = nullptr;
+  if (resid_pass_enabled(m, n, r)) {
+    const int S = r <= 32 ? 32 : 64;
+    const size_t small = 64 + 2 * (size_t)r * r * 8;
+    const size_t need = small + (size_t)n * S * 4 + (size_t)m * S * 4 + (cols ? (size_t)m * r * 8 : 0) + 512;
+    void* scr = nullptr;
+    CNMF_TRY(device_scratch("resid-pass", need, &scr, st));
+    unsigned char* p = (unsigned char*)scr;
+    double* acc = (double*)p;          // [0] ||A||^2, [1] <A Y^T, X>
+    int* flag = (int*)(p + 32);
+    double* G1 = (double*)(p + 64);
+    double* G2 = G1 + (size_t)r * r;
+    float* P = (float*)(p + ((small + 255) & ~(size_t)255));
+    float* T = P + (size_t)n * S;
+    double* Xg = (double*)(T + (size_t)m * S);
+    CNMF_CUDA(cudaMemsetAsync(acc, 0, 16, st));
+    const unsigned g8 = (unsigned)(8 * device_sms());
+    yt_panel<<<g8, 256, 0, st>>>(Yt, n, r, S, P);
+    CNMF_LAUNCH_CHECK();
+    if (cols) {
+      gather_cols_f64<<<g8, 256, 0, st>>>(A, m, lda, cols, r, Xg);
+      CNMF_LAUNCH_CHECK();
+      X = Xg;
+    }
+    CNMF_TRY(pass_forward_sumsq_tc(A, m, n, lda, P, S, T, acc, st));
+    dot_tx<<<g8, 256, 0, st>>>(T, m, S, X, r, acc);
+    CNMF_LAUNCH_CHECK();
+    CNMF_TRY(gram_tn_f64(X, m, r, X, r, G1, st));
+    CNMF_TRY(gram_tn_f64(Yt, n, r, Yt, r, G2, st));
+    resid_combine<<<1, 256, 0, st>>>(acc, G1, G2, r, out, flag);
+    CNMF_LAUNCH_CHECK();
+    skip = flag;
+    if (cols) X = nullptr;
+  } else {
+    CNMF_CUDA(cudaMemsetAsync(out, 0, 16, st));
+  }
   void* scr = nullptr;
   CNMF_TRY(device_scratch("resid-factors", (size_t)(m + n) * r * 4 + 256, &scr, st));
   float* xf = (float*)scr;
   float* yf = xf + (size_t)m * r;
   factors_f32<<<(unsigned)std::min<int64_t>(ceil_div((m + n) * r, 256), 8 * device_sms()), 256, 0, st>>>(
-      A, m, lda, X, cols, n, Yt, r, xf, yf);
+      A, m, lda, X, cols, n, Yt, r, xf, yf, skip);
   CNMF_LAUNCH_CHECK();
   const int64_t units = ceil_div(n, kRN) * ceil_div(ceil_div(m, kRM), kChunk);
   constexpr size_t smem = (size_t)(kRM * (kRMax + 1) + kRMax * kRN) * 4;
@@ -171,7 +288,7 @@ int residual_norms(const float* A, int64_t m, int64_t n, int64_t lda, const doub
   int occ = 0;
   CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, resid_kernel, kRT, smem));
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)std::max(occ, 1) * device_sms()));
-  resid_kernel<<<grid, kRT, smem, st>>>(A, m, n, lda, xf, yf, r, out);
+  resid_kernel<<<grid, kRT, smem, st>>>(A, m, n, lda, xf, yf, r, out, skip);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }

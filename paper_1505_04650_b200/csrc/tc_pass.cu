@@ -219,6 +219,7 @@ struct PassSide {
   int64_t nblocks;  // 128-row output tiles
   int nt;           // K tiles per output tile
   int trans;
+  double* sumsq;    // forward side only, may be null: += sum of A^2 over the side's tiles
 };
 
 // The (side, output tile, K tile) walk of one CTA's units: [lo0, hi0) of
@@ -510,6 +511,7 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
     const int half = (warp - kWarpSplit0) >> 2; // K half of the A tile
     const int pc = warp - kWarpSplit0;          // 16-byte K chunk of the panel tile (k = 4 pc .. 4 pc + 3)
     const int row_in_tile = 32 * q + lane;
+    double sq_acc = 0.0;                        // sum of A^2 (residual pass only)
     constexpr int PT = S / 32;                  // panel columns per lane
     Ring<C::ST> r;
     Ring<C::AST> ra;
@@ -530,6 +532,12 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
           hi[4 * cc + 1] = v.y;
           hi[4 * cc + 2] = v.z;
           hi[4 * cc + 3] = v.w;
+        }
+        if ((w.p ? s1.sumsq : s0.sumsq) != nullptr) {  // ||A||_F^2 of the residual pass (zero fill adds 0)
+          float q2 = 0.f;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) q2 = fmaf(hi[k], hi[k], q2);
+          sq_acc += (double)q2;
         }
       } else {
         // A column = output row: gather 16 K values from the row-major tile
@@ -608,6 +616,11 @@ __global__ void __launch_bounds__(TcCfg<S>::THREADS, 1)
       ra.next();
       w.next(s0, s1);
     }
+    if (s0.sumsq != nullptr) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sq_acc += __shfl_xor_sync(0xffffffffu, sq_acc, o);
+      if (lane == 0) atomicAdd(s0.sumsq, sq_acc);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -624,6 +637,7 @@ struct SideArgs {
   const float* panel;  // X (n x S) for a forward side, W (m x S) for a transpose side
   float* out;
   int trans;
+  double* sumsq = nullptr;  // forward side: accumulate ||A||_F^2 (residual pass)
 };
 
 // Launch one or two sides over the same A.
@@ -631,7 +645,7 @@ template <int S>
 int launch_stream(const float* A, int64_t m, int64_t n, int64_t lda, const SideArgs* sa, int nsides, cudaStream_t st) {
   using C = TcCfg<S>;
   TmaDesc tA[2], tB[2];
-  PassSide sd[2] = {{nullptr, 0, 0, 1, 0}, {nullptr, 0, 0, 1, 0}};
+  PassSide sd[2] = {{nullptr, 0, 0, 1, 0, nullptr}, {nullptr, 0, 0, 1, 0, nullptr}};
   for (int i = 0; i < nsides; ++i) {
     const int64_t K = sa[i].trans ? m : n;  // panel rows
     const int64_t P = sa[i].trans ? n : m;  // output rows
@@ -640,7 +654,7 @@ int launch_stream(const float* A, int64_t m, int64_t n, int64_t lda, const SideA
     else
       CNMF_TRY(make_tma_2d(&tA[i], A, 4, m, n, lda, BMT, BKT, false));
     CNMF_TRY(make_tma_2d(&tB[i], sa[i].panel, 4, K, S, S, S, BKT, false));
-    sd[i] = PassSide{sa[i].out, P, ceil_div(P, BMT), (int)ceil_div(K, BKT), sa[i].trans};
+    sd[i] = PassSide{sa[i].out, P, ceil_div(P, BMT), (int)ceil_div(K, BKT), sa[i].trans, sa[i].trans ? nullptr : sa[i].sumsq};
   }
   if (nsides == 1) {
     tA[1] = tA[0];
@@ -712,6 +726,14 @@ int launch_any(const float* A, int64_t m, int64_t n, int64_t lda, const SideArgs
 
 int pass_forward_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y, cudaStream_t st) {
   const SideArgs sa{X, Y, 0};
+  return launch_any(A, m, n, lda, &sa, 1, S, st);
+}
+
+// Y = A X and sumsq += ||A||_F^2 in the same read of A (the residual pass)
+int pass_forward_sumsq_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y,
+                          double* sumsq, cudaStream_t st) {
+  SideArgs sa{X, Y, 0};
+  sa.sumsq = sumsq;
   return launch_any(A, m, n, lda, &sa, 1, S, st);
 }
 

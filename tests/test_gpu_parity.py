@@ -614,3 +614,31 @@ def test_fp64_snmf_config0_shape(sel):
     assert abs(res.rel_error_full - ref.rel_error_full) <= 1e-9 * ref.rel_error_full
     assert abs(res.rel_error_reduced - ref.rel_error_reduced) <= 1e-8 * max(ref.rel_error_reduced, 1e-12)
     assert np.abs(res.Y - ref.Y).max() <= 1e-8 * max(1.0, np.abs(ref.Y).max())
+
+
+@pytest.mark.parametrize("r,noise", [(50, 0.25), (20, 0.4), (50, 0.01)])
+def test_residual_pass_path(r, noise):
+    # ||A - X Y|| through one tensor-core forward pass (||A||^2 - 2 <A Y^T, X> +
+    # <X^T X, Y Y^T>) against an fp64 reference; small residuals (noise 0.01:
+    # rel ~ 1e-2, too much cancellation) must take the direct kernel
+    from paper_1505_04650_b200.nmf import _rel_error
+
+    m, n = 9000, 8000  # m n >= 2^26: the pass path is eligible
+    g = torch.Generator(device="cuda").manual_seed(r)
+    x = torch.rand(m, r, device="cuda", dtype=torch.float64, generator=g)
+    y = torch.rand(r, n, device="cuda", dtype=torch.float64, generator=g)
+    a = (x @ y) * (1.0 + noise * torch.randn(m, n, device="cuda", dtype=torch.float64, generator=g))
+    a32 = a.clamp_(min=0).float()
+    ref = float(torch.linalg.norm(a32.double() - x @ y) / torch.linalg.norm(a32.double()))
+    A = DeviceMatrix(a32)
+    vt = y.t().contiguous()
+    got = {}
+    for mode in ("1", "0"):
+        os.environ["CNMF_RESID_PASS"] = mode
+        try:
+            got[mode] = _rel_error(A, x, vt)
+        finally:
+            os.environ.pop("CNMF_RESID_PASS", None)
+    # the direct kernel forms X Y from fp32 factors in FP32 FMA: ~1e-5 relative
+    assert abs(got["0"] - ref) <= 2e-5 * ref, (got, ref)
+    assert abs(got["1"] - ref) <= 2e-5 * ref, (got, ref)
