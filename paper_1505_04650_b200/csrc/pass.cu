@@ -428,9 +428,24 @@ static bool use_tc(int S) {
 
 bool pass_uses_tc(int S) { return use_tc(S); }
 
+// streaming-pass kernel version on the tensor-core path: 2 = 256-row units
+// (csrc/tc_pass2.cu, default), 1 = 128-row units (csrc/tc_pass.cu); CNMF_PASS_V
+static int pass_version() {
+  const char* e = getenv("CNMF_PASS_V");
+  return (e && e[0] == '1') ? 1 : 2;
+}
+
+int pass_forward_sumsq(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y,
+                       double* sumsq, cudaStream_t st) {
+  if (!use_tc(S)) return fail(CNMF_ERR_ARGUMENT, "the residual pass needs the tensor-core pass");
+  return pass_version() == 2 ? pass_forward_sumsq_tc2(A, m, n, lda, X, S, Y, sumsq, st)
+                             : pass_forward_sumsq_tc(A, m, n, lda, X, S, Y, sumsq, st);
+}
+
 int pass_forward(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y,
                  cudaStream_t st) {
-  if (use_tc(S)) return pass_forward_tc(A, m, n, lda, X, S, Y, st);
+  if (use_tc(S))
+    return pass_version() == 2 ? pass_forward_tc2(A, m, n, lda, X, S, Y, st) : pass_forward_tc(A, m, n, lda, X, S, Y, st);
   switch (S) {
     case 32: return launch_forward<32>(A, m, n, lda, X, Y, st);
     case 64: return launch_forward<64>(A, m, n, lda, X, Y, st);
@@ -452,14 +467,18 @@ int pass_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* X,
     const char* e = getenv("CNMF_PAIR_PASS");
     paired = (e && e[0] == '0') ? 0 : 1;
   }
-  if (paired && use_tc(S) && 4.0 * (double)m * (double)n <= 4e9) return pass_pair_tc(A, m, n, lda, X, Y, W, Z, S, st);
+  if (paired && use_tc(S) && 4.0 * (double)m * (double)n <= 4e9)
+    return pass_version() == 2 ? pass_pair_tc2(A, m, n, lda, X, Y, W, Z, S, st)
+                               : pass_pair_tc(A, m, n, lda, X, Y, W, Z, S, st);
   CNMF_TRY(pass_forward(A, m, n, lda, X, S, Y, st));
   return pass_transpose(A, m, n, lda, W, S, Z, st);
 }
 
 int pass_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const float* W, int S, float* Z,
                    cudaStream_t st) {
-  if (use_tc(S)) return pass_transpose_tc(A, m, n, lda, W, S, Z, st);
+  if (use_tc(S))
+    return pass_version() == 2 ? pass_transpose_tc2(A, m, n, lda, W, S, Z, st)
+                               : pass_transpose_tc(A, m, n, lda, W, S, Z, st);
   switch (S) {
     case 32: return launch_transpose<32>(A, m, n, lda, W, Z, st);
     case 64: return launch_transpose<64>(A, m, n, lda, W, Z, st);

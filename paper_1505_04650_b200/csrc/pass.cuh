@@ -15,6 +15,16 @@ int pass_forward_tc(const float* A, int64_t m, int64_t n, int64_t lda, const flo
 int pass_forward_sumsq_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y,
                           double* sumsq, cudaStream_t st);
 bool pass_uses_tc(int S);
+int pass_forward_sumsq(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y,
+                       double* sumsq, cudaStream_t st);
+int pass_forward_tc2(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y,
+                     cudaStream_t st);
+int pass_forward_sumsq_tc2(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y,
+                           double* sumsq, cudaStream_t st);
+int pass_transpose_tc2(const float* A, int64_t m, int64_t n, int64_t lda, const float* W, int S, float* Z,
+                       cudaStream_t st);
+int pass_pair_tc2(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W,
+                  float* Z, int S, cudaStream_t st);
 int pass_transpose_tc(const float* A, int64_t m, int64_t n, int64_t lda, const float* W, int S, float* Z,
                       cudaStream_t st);
 // Y = A X and Z = A^T W in one launch (one A-read pipeline ramp per pair)

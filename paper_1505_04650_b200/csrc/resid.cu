@@ -263,7 +263,7 @@ int residual_norms(const float* A, int64_t m, int64_t n, int64_t lda, const doub
       CNMF_LAUNCH_CHECK();
       X = Xg;
     }
-    CNMF_TRY(pass_forward_sumsq_tc(A, m, n, lda, P, S, T, acc, st));
+    CNMF_TRY(pass_forward_sumsq(A, m, n, lda, P, S, T, acc, st));
     dot_tx<<<g8, 256, 0, st>>>(T, m, S, X, r, acc);
     CNMF_LAUNCH_CHECK();
     CNMF_TRY(gram_tn_f64(X, m, r, X, r, G1, st));

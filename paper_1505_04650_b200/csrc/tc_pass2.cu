@@ -1,0 +1,749 @@
+// Streaming passes over A on the 5th-generation tensor cores, version 2:
+// 256-row units (two 128-row TMEM sub-tiles share one split of the panel
+// tile) and one S-wide accumulator per sub-tile.
+//
+//   A X ~= A_hi X_hi + A_hi X_lo + A_lo X_hi   (3xTF32, v_hi = rn_tf32(v),
+//                                              v_lo = v - v_hi exact; the
+//                                              tensor core truncates v_lo)
+//
+// Forward pass  Y = A X   (M = rows of A, K = columns of A, N = S)
+// Transpose     Z = A^T W (M = columns of A, K = rows of A, N = S)
+//
+// What changed against tc_pass.cu (measured there with ncu at configs[4]'s
+// S = 64: ~3100 warp instructions and ~750 shared-memory wavefronts per
+// 16 KB tile, issue 62 % busy, no single pipe saturated):
+//   * a unit is 256 output rows x 32 k: the raw panel tile is TMA-loaded,
+//     split into the K-major SW128 [hi; lo] B operand and read by the
+//     tensor core for BOTH sub-tiles -- the panel load/split (8 + 8 + 16 KB
+//     of shared-memory traffic per unit at S = 64) is amortised over 32 KB
+//     of A instead of 16 KB;
+//   * the three products of a sub-tile accumulate into one S-wide TMEM
+//     accumulator (three N = S MMAs), so the epilogue drains S columns per
+//     row instead of 2S and adds no hi/lo halves;
+//   * the stage is released after the split arithmetic has consumed every
+//     loaded value (register dependence), so the generic-proxy reads are
+//     complete before the next TMA write without a proxy fence.
+// Warp roles (one CTA per SM): warp 0 TMA producer, warp 1 MMA issuer (one
+// elected thread), warps 2..9 splitters (lane quarter w & 3, K half of the
+// tile, both sub-tiles; panel K chunk w - 2), warps 10.. epilogue (lane
+// quarter, 32-column group; one row in each sub-tile per thread).
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
+#include "common.cuh"
+#include "pass.cuh"
+
+namespace cnmf {
+namespace {
+
+constexpr int BMT = 128;  // rows per sub-tile (TMEM lanes)
+constexpr int NSUB = 2;   // sub-tiles per unit: a unit is 256 output rows
+constexpr int BKT = 32;   // K per stage (one 128B swizzle atom of fp32)
+constexpr int NSPL = 8;   // splitter warps (2 per TMEM lane quarter; 8 panel K chunks)
+#ifndef CNMF_PASS_KB
+#define CNMF_PASS_KB 2
+#endif
+#ifdef CNMF_PASS_ACC64
+using acc_t = double;
+#else
+using acc_t = float;
+#endif
+#ifndef CNMF_PASS_NACC
+#define CNMF_PASS_NACC 2
+#endif
+#ifndef CNMF_PASS_AST64
+#define CNMF_PASS_AST64 4
+#endif
+
+// mbarrier wait with a suspend-time hint: a waiting warp sleeps in the
+// try_wait until the phase completes instead of re-polling (the epilogue and
+// producer warps spend most of a pass waiting; their polling loops were 15 %
+// of the issued instructions)
+__device__ __forceinline__ void mbar_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "elect.sync _|P, 0xffffffff;\n"
+      "selp.b32 %0, 1, 0, P;\n"
+      "}\n"
+      : "=r"(pred));
+  return pred;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 32 lanes x 8 consecutive fp32 columns per warp
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 32 lanes x 16 consecutive 32-bit columns per warp
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+
+// SM100 shared-memory matrix descriptor, 128B swizzle.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D fp32, A/B tf32, K-major A and B, M = 128.
+__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BMT >> 4) << 24);
+}
+
+// Round to the nearest tf32 value (10 explicit mantissa bits, ties away from
+// zero). The tensor core truncates the low 13 bits of an fp32 operand, so
+// both split halves are pre-rounded: hi = rn(v), lo = rn(v - hi) (v - hi is
+// exact in fp32), which keeps the split error unbiased and <= 2^-22 |v| --
+// truncating would bias every product of nonnegative data toward zero.
+__device__ __forceinline__ float tf32_rn(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Slot index + phase parity of a ring of N mbarrier-guarded buffers.
+template <int N>
+struct Ring {
+  int i = 0;
+  uint32_t ph = 0;
+  bool wrapped = false;  // every slot has been handed out at least once
+  __device__ __forceinline__ void next() {
+    if (++i == N) {
+      i = 0;
+      ph ^= 1;
+      wrapped = true;
+    }
+  }
+};
+
+
+// Accumulator layout: 2 = per sub-tile [A_hi X_hi | A_hi X_lo + A_lo X_hi]
+// (2S columns; the large and the small products accumulate apart in the
+// tensor core and are added in fp32 registers), 1 = one S-wide accumulator
+// for all three. KB = K tiles the tensor core accumulates before the
+// epilogue drains. Measured projector distances to the reference basis
+// (tests/test_gpu_fullsize.py; the reference's own band under one fp32
+// rounding of A in brackets):
+//   configs[1] shape 2000 x 1000 (S = 32, band 6.4e-5): tc_pass.cu 8.6e-5;
+//     here ACC 2 / KB 2: 1.24-1.29e-4, ACC 2 / KB 1: 7.5e-5 (3 % slower),
+//     ACC 1 / KB 2: 3.5e-4;
+//   configs[4] shape 4000 x 2000 (S = 64, band 4.3e-5): tc_pass.cu 5.8e-5,
+//     ACC 2 / KB 2: 6.2e-5, ACC 1 / KB 1: 6.6e-5, ACC 1 / KB 2: 1.3e-4.
+// At S = 64 two sub-tiles of 2S-wide accumulators fill half of TMEM, so
+// that configuration single-buffers them (NACC = 1); ACC 1 would keep two
+// buffers (4.13 vs 3.73 TB/s at 20000 x 100000) but doubles the error.
+#ifndef CNMF_PASS2_ACC32
+#define CNMF_PASS2_ACC32 2
+#endif
+#ifndef CNMF_PASS2_ACC64
+#define CNMF_PASS2_ACC64 2
+#endif
+#ifndef CNMF_PASS2_KB32
+#define CNMF_PASS2_KB32 1
+#endif
+#ifndef CNMF_PASS2_KB64
+#define CNMF_PASS2_KB64 2
+#endif
+
+template <int S>
+struct TcCfg2 {
+  static constexpr int ABYTES = NSUB * BMT * BKT * 4;  // 32 KB raw A (256 rows x 32 k)
+  static constexpr int BRAW = BKT * S * 4;             // raw fp32 panel tile [32 k][S]
+  static constexpr int STAGE = ABYTES + BRAW;
+  static constexpr int BSPL = BKT * 2 * S * 4;         // split K-major SW128 panel slot [hi; lo]
+  static constexpr int ACC = S == 64 ? CNMF_PASS2_ACC64 : CNMF_PASS2_ACC32;
+  static constexpr int AW = ACC * S;                   // accumulator columns per sub-tile
+  static constexpr int ACC_COLS = NSUB * AW;           // per accumulator buffer: sub-tile j at j AW
+  static constexpr int NACC = (ACC_COLS * 2 + NSUB * 2 * BKT * 2 <= 512) ? 2 : 1;  // buffers (1: S = 64, split)
+  static constexpr int ASLOT = NSUB * 2 * BKT;         // TMEM A ring slot: [sub-tile][hi | lo] x 32 k
+  static constexpr int A_COL0 = NACC * ACC_COLS;
+  static constexpr int AST = (512 - A_COL0) / ASLOT;   // TMEM A ring = split panel ring = MMA-done ring
+  static constexpr int ST = (227 * 1024 - 1024 - AST * BSPL) / STAGE;
+  static constexpr int KB = S == 64 ? CNMF_PASS2_KB64 : CNMF_PASS2_KB32;  // K tiles per tensor-core accumulation block
+  static constexpr int NEPI = 4 * (S / 32);
+  static constexpr int THREADS = 32 * (2 + NSPL + NEPI);
+  // registers: each SM sub-partition holds 16K of them for its ceil(warps / 4) warps
+  static constexpr int MAXREG = (16384 / (((THREADS / 32) + 3) / 4 * 32)) & ~7;
+  static constexpr size_t SMEM = (size_t)ST * STAGE + (size_t)AST * BSPL + 512;
+  static_assert(AST >= 2, "TMEM A ring");
+  static_assert(ST >= 3, "stage ring depth");
+  static_assert(SMEM <= 227 * 1024, "shared memory budget");
+  static_assert(A_COL0 + AST * ASLOT <= 512, "TMEM budget");
+};
+
+constexpr int kWarpTma = 0, kWarpMma = 1, kWarpSplit0 = 2, kWarpEpi0 = 2 + NSPL;
+
+struct PassSide {
+  float* out;
+  int64_t P;        // output rows
+  int64_t nblocks;  // 256-row output units
+  int nt;           // K tiles per output unit
+  int trans;
+  double* sumsq;    // forward side only, may be null: += sum of A^2 over the side's tiles
+};
+// The (side, output tile, K tile) walk of one CTA's units: [lo0, hi0) of
+// side 0, then [lo1, hi1) of side 1 (unit indices local to each side; plain
+// scalars, no indexed arrays, so nothing lands in local memory).
+struct Walk {
+  int p;
+  int64_t ob, u;
+  int kt;
+  int64_t lo0, hi0, lo1, hi1;
+  __device__ __forceinline__ void start(int64_t a0, int64_t a1, int64_t b0, int64_t b1, const PassSide& s0,
+                                        const PassSide& s1) {
+    lo0 = a0;
+    hi0 = a1;
+    lo1 = b0;
+    hi1 = b1;
+    p = lo0 < hi0 ? 0 : 1;
+    u = p ? lo1 : lo0;
+    const int nt = p ? s1.nt : s0.nt;
+    ob = u / nt;
+    kt = (int)(u - ob * nt);
+  }
+  __device__ __forceinline__ bool last() const { return u == (p ? hi1 : hi0) - 1; }  // last unit in range
+  __device__ __forceinline__ bool owned(int nt) const {                               // whole tile in range
+    const int64_t t0 = ob * nt;
+    return t0 >= (p ? lo1 : lo0) && t0 + nt <= (p ? hi1 : hi0);
+  }
+  // units left in the current output tile within this CTA's range
+  __device__ __forceinline__ int64_t tile_left(int nt) const {
+    const int64_t r = (p ? hi1 : hi0) - u, t = nt - kt;
+    return r < t ? r : t;
+  }
+  // advance by len units that stay inside the current tile (len <= tile_left)
+  __device__ __forceinline__ void skip(int len, const PassSide& s0, const PassSide& s1) {
+    u += len;
+    kt += len;
+    const int nt = p ? s1.nt : s0.nt;
+    if (p == 0 && u == hi0) {
+      p = 1;
+      u = lo1;
+      ob = u / s1.nt;
+      kt = (int)(u - ob * s1.nt);
+    } else if (kt == nt) {
+      kt = 0;
+      ++ob;
+    }
+  }
+  __device__ __forceinline__ void next(const PassSide& s0, const PassSide& s1) {
+    ++u;
+    if (p == 0 && u == hi0) {
+      p = 1;
+      u = lo1;
+      ob = u / s1.nt;
+      kt = (int)(u - ob * s1.nt);
+    } else if (++kt == (p ? s1.nt : s0.nt)) {
+      kt = 0;
+      ++ob;
+    }
+  }
+};
+
+// Split-K zeroing handshake (one slot of a per-device ring per launch).
+struct ZSync {
+  unsigned arrived, finished;
+};
+
+
+template <int S>
+__global__ void __maxnreg__(TcCfg2<S>::MAXREG)
+    stream_pass2(const __grid_constant__ TmaDesc tA0, const __grid_constant__ TmaDesc tB0,
+                 const __grid_constant__ TmaDesc tA1, const __grid_constant__ TmaDesc tB1, const PassSide s0,
+                 const PassSide s1, int whole, ZSync* __restrict__ zs) {
+  using C = TcCfg2<S>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* sP = smem + C::ST * C::STAGE;          // [AST][BSPL]
+  uint64_t* full = (uint64_t*)(sP + C::AST * C::BSPL);  // [ST] stage landed
+  uint64_t* empty = full + C::ST;                       // [ST] stage consumed by all splitters
+  uint64_t* afull = empty + C::ST;                      // [AST] split A in TMEM + split panel in SMEM
+  uint64_t* mdone = afull + C::AST;                     // [AST] MMAs of the slot's K tile retired
+  uint64_t* tfull = mdone + C::AST;                     // [NACC] accumulator ready
+  uint64_t* tempty = tfull + C::NACC;                   // [NACC] accumulator drained
+  uint32_t* tmem_slot = (uint32_t*)(tempty + C::NACC);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t U0 = s0.nblocks * s0.nt, U1 = s1.nblocks * s1.nt, G = gridDim.x, b = blockIdx.x;
+  int64_t u0, u1;
+  if (whole) {
+    const int64_t T = s0.nblocks + s1.nblocks;
+    const int64_t t0 = b * T / G, t1 = (b + 1) * T / G;
+    u0 = t0 <= s0.nblocks ? t0 * s0.nt : U0 + (t0 - s0.nblocks) * s1.nt;
+    u1 = t1 <= s0.nblocks ? t1 * s0.nt : U0 + (t1 - s0.nblocks) * s1.nt;
+  } else {
+    u0 = b * (U0 + U1) / G;
+    u1 = (b + 1) * (U0 + U1) / G;
+  }
+  const int64_t lo0 = u0 < U0 ? u0 : U0, hi0 = u1 < U0 ? u1 : U0;
+  const int64_t lo1 = u0 > U0 ? u0 - U0 : 0, hi1 = u1 > U0 ? u1 - U0 : 0;
+  const int64_t ntiles = (hi0 - lo0) + (hi1 - lo1);
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tA0);
+    prefetch_tmap(&tB0);
+    if (U1 > 0) {
+      prefetch_tmap(&tA1);
+      prefetch_tmap(&tB1);
+    }
+    for (int s = 0; s < C::ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NSPL);
+    }
+    for (int s = 0; s < C::AST; ++s) {
+      mbar_init(&afull[s], NSPL);
+      mbar_init(&mdone[s], 1);
+    }
+    for (int i = 0; i < C::NACC; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], C::NEPI);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kWarpMma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (zs != nullptr) {
+    for (int q = 0; q < 2; ++q) {
+      const PassSide& sd = q ? s1 : s0;
+      if (sd.nblocks == 0) continue;
+      const int64_t z0 = b * sd.P / G, z1 = (b + 1) * sd.P / G;
+      float4* o4 = reinterpret_cast<float4*>(sd.out + z0 * S);
+      for (int64_t i = threadIdx.x; i < (z1 - z0) * S / 4; i += blockDim.x) o4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (zs != nullptr && threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&zs->arrived, 1u);
+  }
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kWarpTma) {
+    // ---------------- TMA producer ----------------
+    if (elect_one()) {
+      Ring<C::ST> r;
+      Walk w;
+      w.start(lo0, hi0, lo1, hi1, s0, s1);
+      for (int64_t it = 0; it < ntiles; ++it) {
+        if (it >= C::ST) mbar_sleep(&empty[r.i], r.ph ^ 1);
+        unsigned char* dst = smem + r.i * C::STAGE;
+        mbar_arrive_expect_tx(&full[r.i], C::STAGE);
+        const PassSide& sd = w.p ? s1 : s0;
+        const TmaDesc* ta = w.p ? &tA1 : &tA0;
+        const TmaDesc* tb = w.p ? &tB1 : &tB0;
+        const int row0 = (int)(w.ob * (NSUB * BMT));
+        if (!sd.trans)  // A rows [row0, +256), cols [kt*32, +32): K-major SW128
+          tma_load_2d(dst, ta, &full[r.i], w.kt * BKT, row0);
+        else  // A rows [kt*32, +32) (K), cols [row0, +256) (M): row-major
+          tma_load_2d(dst, ta, &full[r.i], row0, w.kt * BKT);
+        tma_load_2d(dst + C::ABYTES, tb, &full[r.i], 0, w.kt * BKT);
+        r.next();
+        w.next(s0, s1);
+      }
+    }
+  } else if (warp >= kWarpEpi0) {
+    // ---------------- epilogue (one row per sub-tile x 32 columns per thread) ----------------
+    const int q = warp & 3;
+    const int cg = 32 * ((warp - kWarpEpi0) >> 2);
+    const int row_in_sub = 32 * q + lane;
+    Ring<C::NACC> racc;
+    float acc[NSUB][32];
+#pragma unroll
+    for (int j = 0; j < NSUB; ++j)
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[j][c] = 0.f;
+    Walk w;
+    w.start(lo0, hi0, lo1, hi1, s0, s1);
+    for (int64_t it = 0; it < ntiles;) {
+      const int nt = w.p ? s1.nt : s0.nt;
+      const int64_t left = w.tile_left(nt);
+      const int kb_left = C::KB - (w.kt % C::KB);
+      const int len = (int)(left < kb_left ? left : kb_left);
+      const bool tile_end = (len == left);
+      mbar_sleep(&tfull[racc.i], racc.ph);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + racc.i * C::ACC_COLS + cg;
+#pragma unroll
+      for (int j = 0; j < NSUB; ++j)
+#pragma unroll
+        for (int c0 = 0; c0 < 32; c0 += 8) {
+          float v[8];
+          tmem_ld8(taddr + j * C::AW + c0, v);
+          if constexpr (C::ACC == 2) {
+          float vl[8];
+          tmem_ld8(taddr + j * C::AW + S + c0, vl);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[j][c0 + e] += v[e] + vl[e];
+          } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[j][c0 + e] += v[e];
+          }
+        }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[racc.i]);
+      racc.next();
+      if (tile_end) {
+        const PassSide& sd = w.p ? s1 : s0;
+        const bool owned = w.owned(nt);
+        if (!owned && zs != nullptr) {
+          if (lane == 0) {
+            unsigned v;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&zs->arrived) : "memory");
+            } while (v < gridDim.x);
+          }
+          __syncwarp();
+        }
+#pragma unroll
+        for (int j = 0; j < NSUB; ++j) {
+          const int64_t row = w.ob * (NSUB * BMT) + j * BMT + row_in_sub;
+          if (row < sd.P) {
+            float* dst = sd.out + row * S + cg;
+            if (owned) {
+#pragma unroll
+              for (int c = 0; c < 32; c += 4)
+                *(float4*)(dst + c) = make_float4(acc[j][c], acc[j][c + 1], acc[j][c + 2], acc[j][c + 3]);
+            } else {
+#pragma unroll
+              for (int c = 0; c < 32; c += 4) red_add_v4(dst + c, acc[j][c], acc[j][c + 1], acc[j][c + 2], acc[j][c + 3]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc[j][c] = 0.f;
+        }
+      }
+      w.skip(len, s0, s1);
+      it += len;
+    }
+  } else if (warp == kWarpMma) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = idesc_tf32(S);
+    constexpr uint32_t idesc_cat = idesc_tf32(2 * S);
+    Ring<C::AST> ra;
+    Ring<C::NACC> racc;
+    Walk w;
+    w.start(lo0, hi0, lo1, hi1, s0, s1);
+    bool block_start = true;
+    for (int64_t it = 0; it < ntiles; ++it) {
+      const int nt = w.p ? s1.nt : s0.nt;
+      const bool tile_end = w.tile_left(nt) == 1;
+      const bool block_end = tile_end || ((w.kt + 1) % C::KB == 0);
+      if (block_start && racc.wrapped) mbar_sleep(&tempty[racc.i], racc.ph ^ 1);
+      mbar_sleep(&afull[ra.i], ra.ph);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sb = smem_u32(sP + ra.i * C::BSPL);  // K-major SW128 [hi (S rows); lo (S rows)]
+        const uint32_t aslot = tmem + C::A_COL0 + ra.i * C::ASLOT;
+        const uint32_t d0 = tmem + racc.i * C::ACC_COLS;
+#pragma unroll
+        for (int k = 0; k < BKT / 8; ++k) {
+          const uint64_t bhi = smem_desc(sb + 32 * k, 16, 1024);
+          const uint64_t blo = smem_desc(sb + S * 128 + 32 * k, 16, 1024);
+          const uint32_t acc0 = (block_start && k == 0) ? 0u : 1u;
+#pragma unroll
+          for (int j = 0; j < NSUB; ++j) {
+            const uint32_t ahi = aslot + j * 2 * BKT + 8 * k, alo = ahi + BKT, d = d0 + j * C::AW;
+#ifndef CNMF_VARIANT_NOMMA
+            if constexpr (C::ACC == 2) {
+              tc_mma_ts(d, ahi, bhi, idesc_cat, acc0);  // [A_hi X_hi | A_hi X_lo]   (B rows [hi; lo])
+              tc_mma_ts(d + S, alo, bhi, idesc, 1u);    //            + A_lo X_hi
+            } else {  // the small products first: they enter the block's accumulator before it grows
+              tc_mma_ts(d, ahi, blo, idesc, acc0);  // A_hi X_lo
+              tc_mma_ts(d, alo, bhi, idesc, 1u);    // + A_lo X_hi
+              tc_mma_ts(d, ahi, bhi, idesc, 1u);    // + A_hi X_hi
+            }
+#endif
+          }
+        }
+        tc_commit(&mdone[ra.i]);  // releases the TMEM A slot and the split panel slot
+        if (block_end) tc_commit(&tfull[racc.i]);
+      }
+      __syncwarp();
+      ra.next();
+      block_start = block_end;
+      if (block_end) racc.next();
+      w.next(s0, s1);
+    }
+  } else {
+    // ---------------- splitters (warps 2..9) ----------------
+    const int q = warp & 3;                      // TMEM lane quarter
+    const int half = (warp - kWarpSplit0) >> 2;  // K half of the A tile
+    const int pc = warp - kWarpSplit0;           // 16-byte K chunk of the panel tile
+    const int row_in_sub = 32 * q + lane;
+    double sq_acc = 0.0;
+    constexpr int PT = S / 32;
+    Ring<C::ST> r;
+    Ring<C::AST> ra;
+    Walk w;
+    w.start(lo0, hi0, lo1, hi1, s0, s1);
+    for (int64_t it = 0; it < ntiles; ++it) {
+      mbar_sleep(&full[r.i], r.ph);
+      if (ra.wrapped) mbar_sleep(&mdone[ra.i], ra.ph ^ 1);  // the TMEM slot's previous K tile retired
+      tc_fence_after();
+      const unsigned char* stage = smem + r.i * C::STAGE;
+      const bool trans = w.p ? s1.trans : s0.trans;
+      const bool sq = !trans && (w.p ? s1.sumsq : s0.sumsq) != nullptr;
+      // panel K chunk pc: rows k = 4 pc + jj, columns n = lane + 32 t
+      float ph[PT][4], pl[PT][4];
+      {
+        const float* raw = (const float*)(stage + C::ABYTES);
+#pragma unroll
+        for (int t = 0; t < PT; ++t)
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const float v = raw[(4 * pc + jj) * S + lane + 32 * t];
+            ph[t][jj] = tf32_rn(v);
+            pl[t][jj] = v - ph[t][jj];
+          }
+      }
+      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + C::A_COL0 + ra.i * C::ASLOT + 16 * half;
+      // A: sub-tile by sub-tile (load, split, store to TMEM); every loaded
+      // value is consumed before the stage is handed back to the producer
+#pragma unroll
+      for (int j = 0; j < NSUB; ++j) {
+        const int row = j * BMT + row_in_sub;  // row of the 256-row unit
+        float hv[16], lv[16];
+        if (!trans) {
+          const unsigned char* rowp = stage + row * 128;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int c = 4 * half + cc;
+            const float4 v = *(const float4*)(rowp + ((c ^ (row & 7)) << 4));
+            hv[4 * cc + 0] = v.x;
+            hv[4 * cc + 1] = v.y;
+            hv[4 * cc + 2] = v.z;
+            hv[4 * cc + 3] = v.w;
+          }
+        } else {
+          const float* raw = (const float*)stage + row;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) hv[k] = raw[(16 * half + k) * (NSUB * BMT)];
+        }
+        if (sq) {
+          float q2 = 0.f;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) q2 = fmaf(hv[k], hv[k], q2);
+          sq_acc += (double)q2;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float v = hv[k];
+          hv[k] = tf32_rn(v);
+          lv[k] = v - hv[k];
+        }
+        tmem_st16(ta + j * 2 * BKT, hv);
+        tmem_st16(ta + j * 2 * BKT + BKT, lv);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[r.i]);
+      unsigned char* dst = sP + ra.i * C::BSPL;
+#pragma unroll
+      for (int t = 0; t < PT; ++t) {
+        const int n = lane + 32 * t;
+        const uint32_t off = (uint32_t)n * 128 + ((pc ^ (n & 7)) << 4);
+        *(float4*)(dst + off) = make_float4(ph[t][0], ph[t][1], ph[t][2], ph[t][3]);
+        *(float4*)(dst + S * 128 + off) = make_float4(pl[t][0], pl[t][1], pl[t][2], pl[t][3]);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      fence_proxy_async();  // generic-proxy smem stores -> tensor-core (async proxy) reads
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&afull[ra.i]);
+      r.next();
+      ra.next();
+      w.next(s0, s1);
+    }
+    if (s0.sumsq != nullptr) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sq_acc += __shfl_xor_sync(0xffffffffu, sq_acc, o);
+      if (lane == 0) atomicAdd(s0.sumsq, sq_acc);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (zs != nullptr && threadIdx.x == 0 && atomicAdd(&zs->finished, 1u) == gridDim.x - 1) {
+    zs->arrived = 0u;
+    zs->finished = 0u;
+  }
+  if (warp == kWarpMma) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+struct SideArgs {
+  const float* panel;
+  float* out;
+  int trans;
+  double* sumsq = nullptr;
+};
+
+template <int S>
+int launch_stream2(const float* A, int64_t m, int64_t n, int64_t lda, const SideArgs* sa, int nsides, cudaStream_t st) {
+  using C = TcCfg2<S>;
+  TmaDesc tA[2], tB[2];
+  PassSide sd[2] = {{nullptr, 0, 0, 1, 0, nullptr}, {nullptr, 0, 0, 1, 0, nullptr}};
+  for (int i = 0; i < nsides; ++i) {
+    const int64_t K = sa[i].trans ? m : n;
+    const int64_t P = sa[i].trans ? n : m;
+    if (!sa[i].trans)
+      CNMF_TRY(make_tma_2d(&tA[i], A, 4, m, n, lda, BKT, NSUB * BMT, true));
+    else
+      CNMF_TRY(make_tma_2d(&tA[i], A, 4, m, n, lda, NSUB * BMT, BKT, false));
+    CNMF_TRY(make_tma_2d(&tB[i], sa[i].panel, 4, K, S, S, S, BKT, false));
+    sd[i] = PassSide{sa[i].out, P, ceil_div(P, NSUB * BMT), (int)ceil_div(K, BKT), sa[i].trans,
+                     sa[i].trans ? nullptr : sa[i].sumsq};
+  }
+  if (nsides == 1) {
+    tA[1] = tA[0];
+    tB[1] = tB[0];
+  }
+  const int64_t U = sd[0].nblocks * sd[0].nt + sd[1].nblocks * sd[1].nt;
+  const int64_t T = sd[0].nblocks + sd[1].nblocks;
+  CNMF_TRY(ensure_smem_attr((const void*)stream_pass2<S>, (int)C::SMEM));
+  static thread_local int occ_cache[64] = {};
+  int dev = 0;
+  CNMF_CUDA(cudaGetDevice(&dev));
+  int& occ = occ_cache[dev & 63];
+  if (occ == 0) {
+    CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_pass2<S>, C::THREADS, C::SMEM));
+    if (occ < 1) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, stream_pass2<S>);
+      return fail(CNMF_ERR_CUDA, "streaming pass kernel does not fit on an SM: regs " + std::to_string(fa.numRegs) +
+                                     " max threads " + std::to_string(fa.maxThreadsPerBlock) + " static smem " +
+                                     std::to_string(fa.sharedSizeBytes) + " max dyn smem " +
+                                     std::to_string(fa.maxDynamicSharedSizeBytes) + " threads " +
+                                     std::to_string(C::THREADS) + " smem " + std::to_string(C::SMEM));
+    }
+  }
+  const int64_t slots = (int64_t)device_sms() * occ;
+  const int whole = (nsides == 1 && T >= 16 * slots) ? 1 : 0;
+  const int64_t grid = std::min<int64_t>(slots, whole ? T : U);
+  ZSync* zs = nullptr;
+  if (!whole) {
+    void* ring = nullptr;
+    CNMF_TRY(device_scratch("pass-zsync", 64 * sizeof(ZSync), &ring, st));
+    zs = (ZSync*)ring + (device_ticket("pass-zsync") % 64);
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (pass_profiling()) {
+    CNMF_CUDA(cudaEventCreate(&e0));
+    CNMF_CUDA(cudaEventCreate(&e1));
+    CNMF_CUDA(cudaEventRecord(e0, st));
+  }
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3((unsigned)grid);
+  lc.blockDim = dim3(C::THREADS);
+  lc.dynamicSmemBytes = C::SMEM;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  CNMF_CUDA(cudaLaunchKernelEx(&lc, stream_pass2<S>, tA[0], tB[0], tA[1], tB[1], sd[0], sd[1], whole, zs));
+  CNMF_LAUNCH_CHECK();
+  if (e0) {
+    CNMF_CUDA(cudaEventRecord(e1, st));
+    pass_record(e0, e1, nsides * 4.0 * ((double)m * n + (double)n * S + (double)m * S));
+  }
+  return CNMF_OK;
+}
+
+int launch_any2(const float* A, int64_t m, int64_t n, int64_t lda, const SideArgs* sa, int nsides, int S,
+                cudaStream_t st) {
+  switch (S) {
+    case 32: return launch_stream2<32>(A, m, n, lda, sa, nsides, st);
+    case 64: return launch_stream2<64>(A, m, n, lda, sa, nsides, st);
+  }
+  return fail(CNMF_ERR_ARGUMENT, "tensor-core pass supports panel widths 32 and 64");
+}
+
+}  // namespace
+
+int pass_forward_tc2(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y,
+                     cudaStream_t st) {
+  const SideArgs sa{X, Y, 0};
+  return launch_any2(A, m, n, lda, &sa, 1, S, st);
+}
+
+int pass_forward_sumsq_tc2(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, int S, float* Y,
+                           double* sumsq, cudaStream_t st) {
+  SideArgs sa{X, Y, 0};
+  sa.sumsq = sumsq;
+  return launch_any2(A, m, n, lda, &sa, 1, S, st);
+}
+
+int pass_transpose_tc2(const float* A, int64_t m, int64_t n, int64_t lda, const float* W, int S, float* Z,
+                       cudaStream_t st) {
+  const SideArgs sa{W, Z, 1};
+  return launch_any2(A, m, n, lda, &sa, 1, S, st);
+}
+
+int pass_pair_tc2(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W,
+                  float* Z, int S, cudaStream_t st) {
+  const SideArgs sa[2] = {{X, Y, 0}, {W, Z, 1}};
+  return launch_any2(A, m, n, lda, sa, 2, S, st);
+}
+
+}  // namespace cnmf

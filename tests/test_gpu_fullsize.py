@@ -74,3 +74,33 @@ def test_snmf_config2_fullsize_picks(large, seed):
     assert (1 if returned else 0) in set(outcomes.tolist()) or outcomes.min() != outcomes.max()
     if returned:
         assert res.rel_error_full < 0.01
+
+
+FIX4 = os.path.join(ROOT, "tests", "golden", "reference_c4.npz")
+
+
+def classical_config4(m, n, seed):
+    """configs[4] generator at reduced size (tests/golden/make_golden_c4.py)."""
+    g = np.random.default_rng(seed)
+    x = g.uniform(size=(m, 50))
+    y = g.uniform(size=(50, n))
+    y *= g.uniform(size=(50, n)) >= 0.7
+    return np.maximum(x @ y + 0.01 * g.standard_normal((m, n)), 0.0)
+
+
+@pytest.mark.parametrize("m,n", [(4000, 2000), (12000, 6000)])
+def test_compress_config4_shape_full_subspace(m, n):
+    # S = 64 panels (r = 50, s = 60): the 256-row-unit pass kernel's wide
+    # configuration, against the reference's reorthogonalized basis
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    fx = np.load(FIX4)
+    a = classical_config4(m, n, seed=13).astype(np.float32)
+    q = C.structured_compress(a, C.CompressionConfig(r=50, r_ov=10, w=4, seed=3)).Q
+    key = f"c4_{m}x{n}"
+    ref = fx[key + "_q"].astype(np.float64)
+    band = float(fx[key + "_band"].max())
+    d = proj_dist(ref, q)
+    print(f"{key}: projector distance {d:.3e}, reference band {band:.3e}")
+    assert np.linalg.norm(q.T @ q - np.eye(60)) < 1e-5
+    assert d <= max(1e-4, 2.0 * band), (d, band)

@@ -10,7 +10,7 @@ from paper_1505_04650_b200.device import DeviceMatrix, stream, zeros
 
 lib = _lib.load()
 g = torch.Generator(device="cuda").manual_seed(0)
-M, S = 4096, 32
+M, S = 4096, int(os.environ.get("PA_S", "32"))
 for K in (256, 1024, 4096, 16384):
     a = torch.rand(M, K, device="cuda", generator=g)
     x = torch.randn(K, S, device="cuda", generator=g)

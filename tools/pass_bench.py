@@ -24,7 +24,9 @@ for impl in [int(x) for x in os.environ.get("IMPL", "1,0").split(",")]:
     for name, fn in (("forward", lambda: lib.cnmf_pass_forward(A.ptr, M, N, A.lda, X.data_ptr(), S, Y.data_ptr(), stream())),
                      ("transpose", lambda: lib.cnmf_pass_transpose(A.ptr, M, N, A.lda, W.data_ptr(), S, Z.data_ptr(), stream()))):
         for _ in range(3):
-            fn()
+            st_ = fn()
+            if st_ != 0:
+                raise SystemExit(f"status {st_}: {lib.cnmf_last_error()}")
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         lib.cnmf_set_pass_profiling(1)
