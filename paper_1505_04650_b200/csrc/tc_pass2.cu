@@ -216,7 +216,18 @@ struct TcCfg2 {
   static constexpr int ST = (227 * 1024 - 1024 - AST * BSPL) / STAGE;
   static constexpr int KB = S == 64 ? CNMF_PASS2_KB64 : CNMF_PASS2_KB32;  // K tiles per tensor-core accumulation block
   static constexpr int NEPI = 4 * (S / 32);
-  static constexpr int THREADS = 32 * (2 + NSPL + NEPI);
+  // warp roles: 0 TMA, 1 MMA, then NSPL splitters, then NEPI epilogue warps.
+  // S = 64 (18 warps) would cap every thread at 96 registers (16K registers
+  // per SM sub-partition, 5 warps each) and the epilogue's 64 running sums
+  // spilled (10 % of the instructions were spill traffic, ncu); there the
+  // roles are warpgroup-aligned instead -- warpgroup 0 = TMA, MMA and two
+  // idle warps, 1-2 splitters, 3-4 epilogue -- and setmaxnreg moves
+  // registers from warpgroup 0 to the epilogue.
+  static constexpr bool REBAL = (S == 64);
+  static constexpr int SPL0 = REBAL ? 4 : 2;
+  static constexpr int EPI0 = SPL0 + NSPL;
+  static constexpr int THREADS = 32 * (EPI0 + NEPI);
+  static constexpr int REG_LOW = 64, REG_EPI = 112;   // after setmaxnreg (REBAL only)
   // registers: each SM sub-partition holds 16K of them for its ceil(warps / 4) warps
   static constexpr int MAXREG = (16384 / (((THREADS / 32) + 3) / 4 * 32)) & ~7;
   static constexpr size_t SMEM = (size_t)ST * STAGE + (size_t)AST * BSPL + 512;
@@ -226,7 +237,7 @@ struct TcCfg2 {
   static_assert(A_COL0 + AST * ASLOT <= 512, "TMEM budget");
 };
 
-constexpr int kWarpTma = 0, kWarpMma = 1, kWarpSplit0 = 2, kWarpEpi0 = 2 + NSPL;
+constexpr int kWarpTma = 0, kWarpMma = 1;
 
 struct PassSide {
   float* out;
@@ -241,10 +252,10 @@ struct PassSide {
 // scalars, no indexed arrays, so nothing lands in local memory).
 struct Walk {
   int p;
-  int64_t ob, u;
+  int ob, u;
   int kt;
-  int64_t lo0, hi0, lo1, hi1;
-  __device__ __forceinline__ void start(int64_t a0, int64_t a1, int64_t b0, int64_t b1, const PassSide& s0,
+  int lo0, hi0, lo1, hi1;
+  __device__ __forceinline__ void start(int a0, int a1, int b0, int b1, const PassSide& s0,
                                         const PassSide& s1) {
     lo0 = a0;
     hi0 = a1;
@@ -258,12 +269,12 @@ struct Walk {
   }
   __device__ __forceinline__ bool last() const { return u == (p ? hi1 : hi0) - 1; }  // last unit in range
   __device__ __forceinline__ bool owned(int nt) const {                               // whole tile in range
-    const int64_t t0 = ob * nt;
+    const int t0 = ob * nt;
     return t0 >= (p ? lo1 : lo0) && t0 + nt <= (p ? hi1 : hi0);
   }
   // units left in the current output tile within this CTA's range
-  __device__ __forceinline__ int64_t tile_left(int nt) const {
-    const int64_t r = (p ? hi1 : hi0) - u, t = nt - kt;
+  __device__ __forceinline__ int tile_left(int nt) const {
+    const int r = (p ? hi1 : hi0) - u, t = nt - kt;
     return r < t ? r : t;
   }
   // advance by len units that stay inside the current tile (len <= tile_left)
@@ -302,7 +313,7 @@ struct ZSync {
 
 
 template <int S>
-__global__ void __maxnreg__(TcCfg2<S>::MAXREG)
+__global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
     stream_pass2(const __grid_constant__ TmaDesc tA0, const __grid_constant__ TmaDesc tB0,
                  const __grid_constant__ TmaDesc tA1, const __grid_constant__ TmaDesc tB1, const PassSide s0,
                  const PassSide s1, int whole, ZSync* __restrict__ zs) {
@@ -377,13 +388,19 @@ __global__ void __maxnreg__(TcCfg2<S>::MAXREG)
     atomicAdd(&zs->arrived, 1u);
   }
   const uint32_t tmem = *tmem_slot;
+  if constexpr (C::REBAL) {
+    if (warp < 4)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::REG_LOW));
+    else if (warp >= C::EPI0)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::REG_EPI));
+  }
 
   if (warp == kWarpTma) {
     // ---------------- TMA producer ----------------
     if (elect_one()) {
       Ring<C::ST> r;
       Walk w;
-      w.start(lo0, hi0, lo1, hi1, s0, s1);
+      w.start((int)lo0, (int)hi0, (int)lo1, (int)hi1, s0, s1);
       for (int64_t it = 0; it < ntiles; ++it) {
         if (it >= C::ST) mbar_sleep(&empty[r.i], r.ph ^ 1);
         unsigned char* dst = smem + r.i * C::STAGE;
@@ -401,10 +418,10 @@ __global__ void __maxnreg__(TcCfg2<S>::MAXREG)
         w.next(s0, s1);
       }
     }
-  } else if (warp >= kWarpEpi0) {
+  } else if (warp >= C::EPI0) {
     // ---------------- epilogue (one row per sub-tile x 32 columns per thread) ----------------
     const int q = warp & 3;
-    const int cg = 32 * ((warp - kWarpEpi0) >> 2);
+    const int cg = 32 * ((warp - C::EPI0) >> 2);
     const int row_in_sub = 32 * q + lane;
     Ring<C::NACC> racc;
     float acc[NSUB][32];
@@ -413,7 +430,7 @@ __global__ void __maxnreg__(TcCfg2<S>::MAXREG)
 #pragma unroll
       for (int c = 0; c < 32; ++c) acc[j][c] = 0.f;
     Walk w;
-    w.start(lo0, hi0, lo1, hi1, s0, s1);
+    w.start((int)lo0, (int)hi0, (int)lo1, (int)hi1, s0, s1);
     for (int64_t it = 0; it < ntiles;) {
       const int nt = w.p ? s1.nt : s0.nt;
       const int64_t left = w.tile_left(nt);
@@ -483,7 +500,7 @@ __global__ void __maxnreg__(TcCfg2<S>::MAXREG)
     Ring<C::AST> ra;
     Ring<C::NACC> racc;
     Walk w;
-    w.start(lo0, hi0, lo1, hi1, s0, s1);
+    w.start((int)lo0, (int)hi0, (int)lo1, (int)hi1, s0, s1);
     bool block_start = true;
     for (int64_t it = 0; it < ntiles; ++it) {
       const int nt = w.p ? s1.nt : s0.nt;
@@ -525,18 +542,18 @@ __global__ void __maxnreg__(TcCfg2<S>::MAXREG)
       if (block_end) racc.next();
       w.next(s0, s1);
     }
-  } else {
-    // ---------------- splitters (warps 2..9) ----------------
+  } else if (warp >= C::SPL0) {
+    // ---------------- splitters ----------------
     const int q = warp & 3;                      // TMEM lane quarter
-    const int half = (warp - kWarpSplit0) >> 2;  // K half of the A tile
-    const int pc = warp - kWarpSplit0;           // 16-byte K chunk of the panel tile
+    const int half = (warp - C::SPL0) >> 2;  // K half of the A tile
+    const int pc = warp - C::SPL0;           // 16-byte K chunk of the panel tile
     const int row_in_sub = 32 * q + lane;
     double sq_acc = 0.0;
     constexpr int PT = S / 32;
     Ring<C::ST> r;
     Ring<C::AST> ra;
     Walk w;
-    w.start(lo0, hi0, lo1, hi1, s0, s1);
+    w.start((int)lo0, (int)hi0, (int)lo1, (int)hi1, s0, s1);
     for (int64_t it = 0; it < ntiles; ++it) {
       mbar_sleep(&full[r.i], r.ph);
       if (ra.wrapped) mbar_sleep(&mdone[ra.i], ra.ph ^ 1);  // the TMEM slot's previous K tile retired
