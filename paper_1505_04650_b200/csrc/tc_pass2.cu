@@ -200,6 +200,16 @@ struct Ring {
 #define CNMF_PASS2_KB64 2
 #endif
 
+#ifndef REBAL_LOW
+#define REBAL_LOW 64
+#endif
+#ifndef REBAL_SPL
+#define REBAL_SPL 96
+#endif
+#ifndef REBAL_EPI
+#define REBAL_EPI 112
+#endif
+
 template <int S>
 struct TcCfg2 {
   static constexpr int ABYTES = NSUB * BMT * BKT * 4;  // 32 KB raw A (256 rows x 32 k)
@@ -227,7 +237,8 @@ struct TcCfg2 {
   static constexpr int SPL0 = REBAL ? 4 : 2;
   static constexpr int EPI0 = SPL0 + NSPL;
   static constexpr int THREADS = 32 * (EPI0 + NEPI);
-  static constexpr int REG_LOW = 64, REG_EPI = 112;   // after setmaxnreg (REBAL only)
+  static constexpr int REG_LOW = REBAL_LOW, REG_SPL = REBAL_SPL, REG_EPI = REBAL_EPI;  // after setmaxnreg (REBAL only)
+  static_assert(!REBAL || REG_LOW + 2 * REG_SPL + 2 * REG_EPI <= 5 * 96, "register file per sub-partition");
   // registers: each SM sub-partition holds 16K of them for its ceil(warps / 4) warps
   static constexpr int MAXREG = (16384 / (((THREADS / 32) + 3) / 4 * 32)) & ~7;
   static constexpr size_t SMEM = (size_t)ST * STAGE + (size_t)AST * BSPL + 512;
@@ -393,6 +404,8 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::REG_LOW));
     else if (warp >= C::EPI0)
       asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::REG_EPI));
+    else if (C::REG_SPL > 96)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::REG_SPL));
   }
 
   if (warp == kWarpTma) {
