@@ -172,32 +172,34 @@ struct Ring {
 };
 
 
-// Accumulator layout: 2 = per sub-tile [A_hi X_hi | A_hi X_lo + A_lo X_hi]
-// (2S columns; the large and the small products accumulate apart in the
-// tensor core and are added in fp32 registers), 1 = one S-wide accumulator
-// for all three. KB = K tiles the tensor core accumulates before the
-// epilogue drains. Measured projector distances to the reference basis
-// (tests/test_gpu_fullsize.py; the reference's own band under one fp32
-// rounding of A in brackets):
-//   configs[1] shape 2000 x 1000 (S = 32, band 6.4e-5): tc_pass.cu 8.6e-5;
-//     here ACC 2 / KB 2: 1.24-1.29e-4, ACC 2 / KB 1: 7.5e-5 (3 % slower),
-//     ACC 1 / KB 2: 3.5e-4;
-//   configs[4] shape 4000 x 2000 (S = 64, band 4.3e-5): tc_pass.cu 5.8e-5,
-//     ACC 2 / KB 2: 6.2e-5, ACC 1 / KB 1: 6.6e-5, ACC 1 / KB 2: 1.3e-4.
-// At S = 64 two sub-tiles of 2S-wide accumulators fill half of TMEM, so
-// that configuration single-buffers them (NACC = 1); ACC 1 would keep two
-// buffers (4.13 vs 3.73 TB/s at 20000 x 100000) but doubles the error.
+// Accumulator layout: 1 = one S-wide accumulator per sub-tile, fed per K
+// tile with the small products (A_hi X_lo, A_lo X_hi over all k steps)
+// first and the large ones (A_hi X_hi) on top; 2 = [A_hi X_hi | A_hi X_lo +
+// A_lo X_hi] (2S columns, large and small accumulate apart). KB = K tiles
+// the tensor core accumulates before the epilogue drains into fp32
+// registers. Measured (tools/pass_accuracy.py at K = 16384, S = 64: rms
+// error relative to |A||X|; projector distances to the reference basis,
+// tests/test_gpu_fullsize.py, the reference's own band under one fp32
+// rounding of A in brackets; 20000 x 100000 forward/transpose TB/s):
+//   tc_pass.cu (128-row units, split, KB 2): rms 2.6e-9; c1 2000 x 1000
+//     8.6e-5 [6.4e-5], c4 4000 x 2000 5.8e-5 [4.3e-5]; S=64 3.72/3.86
+//   ACC 1 / KB 1 (default): rms 2.2e-9; c1 7.0e-5, c4 5.3e-5;
+//     S=64 4.15/4.42, S=32 5.84/5.95
+//   ACC 2 / KB 2: rms 2.6e-9; c1 1.24-1.29e-4, c4 6.2e-5; S=64 3.73 (two
+//     2S-wide sub-tile accumulators fill half of TMEM: single-buffered)
+//   ACC 1 / KB 2: rms 4.6e-9; c4 1.2e-4 (over the 1e-4 bound)
+//   ACC 1 / KB 2 with the products interleaved per k step: rms 5.6e-9
 #ifndef CNMF_PASS2_ACC32
-#define CNMF_PASS2_ACC32 2
+#define CNMF_PASS2_ACC32 1
 #endif
 #ifndef CNMF_PASS2_ACC64
-#define CNMF_PASS2_ACC64 2
+#define CNMF_PASS2_ACC64 1
 #endif
 #ifndef CNMF_PASS2_KB32
 #define CNMF_PASS2_KB32 1
 #endif
 #ifndef CNMF_PASS2_KB64
-#define CNMF_PASS2_KB64 2
+#define CNMF_PASS2_KB64 1
 #endif
 
 #ifndef REBAL_LOW
@@ -527,25 +529,48 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
         const uint32_t aslot = tmem + C::A_COL0 + ra.i * C::ASLOT;
         const uint32_t d0 = tmem + racc.i * C::ACC_COLS;
 #pragma unroll
-        for (int k = 0; k < BKT / 8; ++k) {
-          const uint64_t bhi = smem_desc(sb + 32 * k, 16, 1024);
-          const uint64_t blo = smem_desc(sb + S * 128 + 32 * k, 16, 1024);
-          const uint32_t acc0 = (block_start && k == 0) ? 0u : 1u;
-#pragma unroll
-          for (int j = 0; j < NSUB; ++j) {
-            const uint32_t ahi = aslot + j * 2 * BKT + 8 * k, alo = ahi + BKT, d = d0 + j * C::AW;
 #ifndef CNMF_VARIANT_NOMMA
-            if constexpr (C::ACC == 2) {
+        if constexpr (C::ACC == 2) {
+#pragma unroll
+          for (int k = 0; k < BKT / 8; ++k) {
+            const uint64_t bhi = smem_desc(sb + 32 * k, 16, 1024);
+            const uint32_t acc0 = (block_start && k == 0) ? 0u : 1u;
+#pragma unroll
+            for (int j = 0; j < NSUB; ++j) {
+              const uint32_t ahi = aslot + j * 2 * BKT + 8 * k, alo = ahi + BKT, d = d0 + j * C::AW;
               tc_mma_ts(d, ahi, bhi, idesc_cat, acc0);  // [A_hi X_hi | A_hi X_lo]   (B rows [hi; lo])
               tc_mma_ts(d + S, alo, bhi, idesc, 1u);    //            + A_lo X_hi
-            } else {  // the small products first: they enter the block's accumulator before it grows
+            }
+          }
+        } else {
+          // one S-wide accumulator: the block's small products (A_hi X_lo,
+          // A_lo X_hi over all its k steps) accumulate first, from zero, and
+          // the large ones (A_hi X_hi) are added on top -- the tensor core's
+          // truncating fp32 accumulation then only rounds against the large
+          // partial sums as often as the split layout does
+#pragma unroll
+          for (int k = 0; k < BKT / 8; ++k) {
+            const uint64_t bhi = smem_desc(sb + 32 * k, 16, 1024);
+            const uint64_t blo = smem_desc(sb + S * 128 + 32 * k, 16, 1024);
+            const uint32_t acc0 = (block_start && k == 0) ? 0u : 1u;
+#pragma unroll
+            for (int j = 0; j < NSUB; ++j) {
+              const uint32_t ahi = aslot + j * 2 * BKT + 8 * k, alo = ahi + BKT, d = d0 + j * C::AW;
               tc_mma_ts(d, ahi, blo, idesc, acc0);  // A_hi X_lo
               tc_mma_ts(d, alo, bhi, idesc, 1u);    // + A_lo X_hi
-              tc_mma_ts(d, ahi, bhi, idesc, 1u);    // + A_hi X_hi
             }
-#endif
+          }
+#pragma unroll
+          for (int k = 0; k < BKT / 8; ++k) {
+            const uint64_t bhi = smem_desc(sb + 32 * k, 16, 1024);
+#pragma unroll
+            for (int j = 0; j < NSUB; ++j) {
+              const uint32_t ahi = aslot + j * 2 * BKT + 8 * k, d = d0 + j * C::AW;
+              tc_mma_ts(d, ahi, bhi, idesc, 1u);  // + A_hi X_hi
+            }
           }
         }
+#endif
         tc_commit(&mdone[ra.i]);  // releases the TMEM A slot and the split panel slot
         if (block_end) tc_commit(&tfull[racc.i]);
       }
