@@ -202,6 +202,28 @@ struct Ring {
 #define CNMF_PASS2_KB64 1
 #endif
 
+// TMA load with an L2 eviction policy (createpolicy): A is streamed once per
+// pass and must not push the panels out of L2 -- without the hint the
+// panel rows were re-read from DRAM, 101 GB per 80 GB pass at configs[4]
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const void* tmap, uint64_t* bar, int c0, int c1,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+      "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+
 #ifndef REBAL_LOW
 #define REBAL_LOW 64
 #endif
@@ -416,6 +438,7 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
       Ring<C::ST> r;
       Walk w;
       w.start((int)lo0, (int)hi0, (int)lo1, (int)hi1, s0, s1);
+      const uint64_t pol_a = l2_policy_evict_first(), pol_p = l2_policy_evict_last();
       for (int64_t it = 0; it < ntiles; ++it) {
         if (it >= C::ST) mbar_sleep(&empty[r.i], r.ph ^ 1);
         unsigned char* dst = smem + r.i * C::STAGE;
@@ -425,10 +448,10 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
         const TmaDesc* tb = w.p ? &tB1 : &tB0;
         const int row0 = (int)(w.ob * (NSUB * BMT));
         if (!sd.trans)  // A rows [row0, +256), cols [kt*32, +32): K-major SW128
-          tma_load_2d(dst, ta, &full[r.i], w.kt * BKT, row0);
+          tma_load_2d_hint(dst, ta, &full[r.i], w.kt * BKT, row0, pol_a);
         else  // A rows [kt*32, +32) (K), cols [row0, +256) (M): row-major
-          tma_load_2d(dst, ta, &full[r.i], row0, w.kt * BKT);
-        tma_load_2d(dst + C::ABYTES, tb, &full[r.i], 0, w.kt * BKT);
+          tma_load_2d_hint(dst, ta, &full[r.i], row0, w.kt * BKT, pol_a);
+        tma_load_2d_hint(dst + C::ABYTES, tb, &full[r.i], 0, w.kt * BKT, pol_p);
         r.next();
         w.next(s0, s1);
       }
