@@ -285,7 +285,12 @@ struct PassSide {
 // The (side, output tile, K tile) walk of one CTA's units: [lo0, hi0) of
 // side 0, then [lo1, hi1) of side 1 (unit indices local to each side; plain
 // scalars, no indexed arrays, so nothing lands in local memory).
-struct Walk {
+template <bool SINGLE>
+struct WalkT;
+
+// two sides: side 0's units, then side 1's
+template <>
+struct WalkT<false> {
   int p;
   int ob, u;
   int kt;
@@ -341,18 +346,61 @@ struct Walk {
   }
 };
 
+// one side (the common launch): no side switch, so the walk state and every
+// side-dependent operand fold to side 0 at compile time
+template <>
+struct WalkT<true> {
+  static constexpr int p = 0;
+  int ob, u, kt;
+  int lo0, hi0;
+  __device__ __forceinline__ void start(int a0, int a1, int, int, const PassSide& s0, const PassSide&) {
+    lo0 = a0;
+    hi0 = a1;
+    u = lo0;
+    ob = u / s0.nt;
+    kt = u - ob * s0.nt;
+  }
+  __device__ __forceinline__ bool owned(int nt) const {
+    const int t0 = ob * nt;
+    return t0 >= lo0 && t0 + nt <= hi0;
+  }
+  __device__ __forceinline__ int tile_left(int nt) const {
+    const int r = hi0 - u, t = nt - kt;
+    return r < t ? r : t;
+  }
+  __device__ __forceinline__ void skip(int len, const PassSide& s0, const PassSide&) {
+    u += len;
+    kt += len;
+    if (kt == s0.nt) {
+      kt = 0;
+      ++ob;
+    }
+  }
+  __device__ __forceinline__ void next(const PassSide& s0, const PassSide&) {
+    ++u;
+    if (++kt == s0.nt) {
+      kt = 0;
+      ++ob;
+    }
+  }
+};
+
 // Split-K zeroing handshake (one slot of a per-device ring per launch).
 struct ZSync {
   unsigned arrived, finished;
 };
 
 
-template <int S>
+// MODE 0: one forward side, 1: one transpose side, 2: two sides (paired),
+// 3: one forward side that also sums A^2 (the residual pass)
+template <int S, int MODE>
 __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
     stream_pass2(const __grid_constant__ TmaDesc tA0, const __grid_constant__ TmaDesc tB0,
                  const __grid_constant__ TmaDesc tA1, const __grid_constant__ TmaDesc tB1, const PassSide s0,
                  const PassSide s1, int whole, ZSync* __restrict__ zs) {
   using C = TcCfg2<S>;
+  constexpr bool SINGLE = MODE != 2;
+  using Walk = WalkT<SINGLE>;
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* sP = smem + C::ST * C::STAGE;          // [AST][BSPL]
   uint64_t* full = (uint64_t*)(sP + C::AST * C::BSPL);  // [ST] stage landed
@@ -447,7 +495,8 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
         const TmaDesc* ta = w.p ? &tA1 : &tA0;
         const TmaDesc* tb = w.p ? &tB1 : &tB0;
         const int row0 = (int)(w.ob * (NSUB * BMT));
-        if (!sd.trans)  // A rows [row0, +256), cols [kt*32, +32): K-major SW128
+        const bool trans = MODE == 1 || (MODE == 2 && sd.trans);
+        if (!trans)  // A rows [row0, +256), cols [kt*32, +32): K-major SW128
           tma_load_2d_hint(dst, ta, &full[r.i], w.kt * BKT, row0, pol_a);
         else  // A rows [kt*32, +32) (K), cols [row0, +256) (M): row-major
           tma_load_2d_hint(dst, ta, &full[r.i], row0, w.kt * BKT, pol_a);
@@ -620,8 +669,8 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
       if (ra.wrapped) mbar_sleep(&mdone[ra.i], ra.ph ^ 1);  // the TMEM slot's previous K tile retired
       tc_fence_after();
       const unsigned char* stage = smem + r.i * C::STAGE;
-      const bool trans = w.p ? s1.trans : s0.trans;
-      const bool sq = !trans && (w.p ? s1.sumsq : s0.sumsq) != nullptr;
+      const bool trans = MODE == 1 || (MODE == 2 && (w.p ? s1.trans : s0.trans));
+      constexpr bool sq = MODE == 3;
       // panel K chunk pc: rows k = 4 pc + jj, columns n = lane + 32 t
       float ph[PT][4], pl[PT][4];
       {
@@ -658,7 +707,7 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
 #pragma unroll
           for (int k = 0; k < 16; ++k) hv[k] = raw[(16 * half + k) * (NSUB * BMT)];
         }
-        if (sq) {
+        if constexpr (sq) {
           float q2 = 0.f;
 #pragma unroll
           for (int k = 0; k < 16; ++k) q2 = fmaf(hv[k], hv[k], q2);
@@ -692,7 +741,7 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
       ra.next();
       w.next(s0, s1);
     }
-    if (s0.sumsq != nullptr) {
+    if (MODE == 3) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sq_acc += __shfl_xor_sync(0xffffffffu, sq_acc, o);
       if (lane == 0) atomicAdd(s0.sumsq, sq_acc);
@@ -737,16 +786,18 @@ int launch_stream2(const float* A, int64_t m, int64_t n, int64_t lda, const Side
   }
   const int64_t U = sd[0].nblocks * sd[0].nt + sd[1].nblocks * sd[1].nt;
   const int64_t T = sd[0].nblocks + sd[1].nblocks;
-  CNMF_TRY(ensure_smem_attr((const void*)stream_pass2<S>, (int)C::SMEM));
+  const int mode = nsides == 2 ? 2 : sa[0].trans ? 1 : sa[0].sumsq ? 3 : 0;
+  auto kern = mode == 0 ? stream_pass2<S, 0> : mode == 1 ? stream_pass2<S, 1> : mode == 2 ? stream_pass2<S, 2> : stream_pass2<S, 3>;
+  CNMF_TRY(ensure_smem_attr((const void*)kern, (int)C::SMEM));
   static thread_local int occ_cache[64] = {};
   int dev = 0;
   CNMF_CUDA(cudaGetDevice(&dev));
   int& occ = occ_cache[dev & 63];
   if (occ == 0) {
-    CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stream_pass2<S>, C::THREADS, C::SMEM));
+    CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM));
     if (occ < 1) {
       cudaFuncAttributes fa{};
-      cudaFuncGetAttributes(&fa, stream_pass2<S>);
+      cudaFuncGetAttributes(&fa, kern);
       return fail(CNMF_ERR_CUDA, "streaming pass kernel does not fit on an SM: regs " + std::to_string(fa.numRegs) +
                                      " max threads " + std::to_string(fa.maxThreadsPerBlock) + " static smem " +
                                      std::to_string(fa.sharedSizeBytes) + " max dyn smem " +
@@ -779,7 +830,7 @@ int launch_stream2(const float* A, int64_t m, int64_t n, int64_t lda, const Side
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  CNMF_CUDA(cudaLaunchKernelEx(&lc, stream_pass2<S>, tA[0], tB[0], tA[1], tB[1], sd[0], sd[1], whole, zs));
+  CNMF_CUDA(cudaLaunchKernelEx(&lc, kern, tA[0], tB[0], tA[1], tB[1], sd[0], sd[1], whole, zs));
   CNMF_LAUNCH_CHECK();
   if (e0) {
     CNMF_CUDA(cudaEventRecord(e1, st));
