@@ -512,8 +512,9 @@ def run_ours(args):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                 "traffic": TRAFFIC.get(cid), "traffic_unit": "dram bytes read+written per launch (ncu --set full)",
                 "algorithmic_bytes_per_launch": pass_bytes,
-                "kernel": f"stream_pass<{S}> (tcgen05 3xTF32, TMA-fed; one or two sides per launch), CUDA events "
-                          "on the launch stream around every pass of one compression",
+                "kernel": f"stream_pass2<{S}> (csrc/tc_pass2.cu: tcgen05 3xTF32, TMA-fed, 256-row units; one or "
+                          "two sides per launch), CUDA events on the launch stream around every pass of one "
+                          "compression",
                 "launches": pl.value, "avg_launch_ms": pass_avg_ms, "peak_source": peak_src,
                 "share_of_step": pms.value / ms_per_step if ms_per_step else None}
 
@@ -565,22 +566,24 @@ def run_ours(args):
 
 
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-# kernel at the configuration's size (ncu --set full; profiles/)
-TRAFFIC = {}
+# kernel at the configuration's size (ncu --set full of the bench command;
+# profiles/r02_cfg4_pass_ncu_full.txt, profiles/r02_cfg1_pass_ncu_full.txt)
+TRAFFIC = {4: 80.9e9, 1: 353.4e6}
 
 
 def admm_roofline(m, n, s, r, ms_per_iter):
-    """The ADMM iteration against the fp64 pipe: per iteration the row updates
-    form P z (2 (m+n) s r flops) and the reduced sums P^T x, P^T dx
-    (4 (m+n) s r), and stream U, dU, V^T, dV^T (read + write, fp64) plus the
-    fp32 bases."""
-    flops = 6.0 * (m + n) * s * r
+    """The ADMM iteration against the fp64 tensor pipe: per iteration the row
+    sweep forms P z (2 (m+n) s r flops) and the reduced sums P^T x
+    (2 (m+n) s r; P^T dx follows from the dual recurrence), and streams U, dU,
+    V^T, dV^T (read + write, fp64) plus the fp32 bases; the core step's
+    s x s / r x r work is O(s^3) and does not scale with m + n."""
+    flops = 4.0 * (m + n) * s * r
     bytes_ = 32.0 * (m + n) * r + 4.0 * (m + n) * (32 if s <= 32 else 64)
-    fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12  # 64 fp64 FMA / SM / cycle at 1965 MHz (nominal)
+    fp64_peak = 37.2  # DMMA m8n8k4 measured on B200 (tools/dmma_probe.cu: 37.1-37.2 TFLOP/s; DFMA 33.9)
     t = ms_per_iter * 1e-3
     return {"bound": "fp64", "achieved": flops / t / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",
             "frac": flops / t / 1e12 / fp64_peak, "bytes_per_iter": bytes_, "hbm_gbs": bytes_ / t / 1e9,
-            "ms_per_iter": ms_per_iter, "peak_source": "nominal fp64 rate (no measured fp64 peak in MEASURED_PEAKS)"}
+            "ms_per_iter": ms_per_iter, "peak_source": "measured DMMA rate (tools/dmma_probe.cu)"}
 
 
 def e2e_run(args, cid, host, c0, ncols, comm, ops, pj, abytes):

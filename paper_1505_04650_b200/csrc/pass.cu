@@ -463,11 +463,14 @@ int pass_forward(const float* A, int64_t m, int64_t n, int64_t lda, const float*
 int pass_pair(const float* A, int64_t m, int64_t n, int64_t lda, const float* X, float* Y, const float* W, float* Z,
               int S, cudaStream_t st) {
   static int paired = -1;
+  static double max_bytes = 4e9;
   if (paired < 0) {
     const char* e = getenv("CNMF_PAIR_PASS");
     paired = (e && e[0] == '0') ? 0 : 1;
+    const char* g = getenv("CNMF_PAIR_MAX_GB");  // A/B: the size limit of the paired launch
+    if (g) max_bytes = atof(g) * 1e9;
   }
-  if (paired && use_tc(S) && 4.0 * (double)m * (double)n <= 4e9)
+  if (paired && use_tc(S) && 4.0 * (double)m * (double)n <= max_bytes)
     return pass_version() == 2 ? pass_pair_tc2(A, m, n, lda, X, Y, W, Z, S, st)
                                : pass_pair_tc(A, m, n, lda, X, Y, W, Z, S, st);
   CNMF_TRY(pass_forward(A, m, n, lda, X, S, Y, st));

@@ -1,0 +1,52 @@
+"""One-page summary of an ncu --set full report (per captured kernel): time,
+DRAM bytes, throughputs, pipe utilisation, stall reasons, spills."""
+import csv
+import subprocess
+import sys
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("sm__cycles_elapsed.avg.per_second", "SM clock"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active", "tcgen05 pipe active %"),
+    ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", "DMMA pipe active %"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active %"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem LSU wavefronts %"),
+    ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem TC wavefronts %"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("sass__inst_executed_register_spilling", "spill instructions"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+]
+
+
+def main(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units = rows[0], rows[1]
+    idx = {h: i for i, h in enumerate(hdr)}
+    for row in rows[2:]:
+        print(f"== {row[idx['Kernel Name']][:90]}")
+        for k, name in KEYS:
+            if k in idx and row[idx[k]] not in ("", "n/a"):
+                print(f"  {name:28s} {row[idx[k]]} {units[idx[k]]}")
+        st = []
+        for h in hdr:
+            if h.startswith("smsp__average_warps_issue_stalled") and h.endswith("_per_issue_active.ratio"):
+                try:
+                    v = float(row[idx[h]])
+                except ValueError:
+                    continue
+                if v >= 0.2:
+                    st.append((v, h[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+        print("  stalls (warps per issue):   " + ", ".join(f"{n} {v:.2f}" for v, n in sorted(st, reverse=True)))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
