@@ -385,11 +385,110 @@ struct WalkT<true> {
   }
 };
 
-// Split-K zeroing handshake (one slot of a per-device ring per launch).
-struct ZSync {
-  unsigned arrived, finished;
+
+
+
+template <int S>
+constexpr int NEPI_OF() { return 4 * (S / 32); }
+
+// Split-K tile (its units span the CTA boundaries bf .. bl): every
+// contributor parks its partial in its own slot, the last to arrive sums
+// the slots in CTA order and stores -- bit-reproducible, no zeroing of the
+// output and no grid-wide wait. A CTA contributes to at most two split tiles
+// (its first and its last), so the slots are [2 x grid]: slot 2c for CTA c's
+// first tile, 2c + 1 for its last. Out of line: the hot epilogue loop keeps
+// its registers. Unit indices fit 32 bits (checked by the launcher).
+struct SplitTile {
+  int bf, bl, tg;
 };
 
+__device__ __forceinline__ int splitk_slot(int c, int tg, int U0, int Ut, int nb0, int nt0, int nt1, int G) {
+  const int v = (int)((unsigned)c * (unsigned)Ut / (unsigned)G);  // CTA c's first unit
+  const int t = v < U0 ? v / nt0 : nb0 + (v - U0) / nt1;
+  return 2 * c + (t == tg ? 0 : 1);
+}
+
+// this CTA's slot for the split tile (ob of side p); the partial is stored by
+// the caller (inline: the running sums stay in registers)
+__device__ __forceinline__ float* splitk_mine(SplitTile& st, int U0, int Ut, int nb0, int nt0, int nt1, int p, int ob,
+                                              int nt, int G, int b, float* sk_slots, int tile_floats) {
+  const int t_lo = (p ? U0 : 0) + ob * nt, t_hi = t_lo + nt - 1;
+  st.bf = (int)(((unsigned)(t_lo + 1) * (unsigned)G - 1u) / (unsigned)Ut);
+  st.bl = (int)(((unsigned)(t_hi + 1) * (unsigned)G - 1u) / (unsigned)Ut);
+  st.tg = (p ? nb0 : 0) + ob;
+  return sk_slots + (size_t)splitk_slot(b, st.tg, U0, Ut, nb0, nt0, nt1, G) * tile_floats;
+}
+
+template <int S, int NEPI>
+__device__ __noinline__ void splitk_tile(SplitTile st, const PassSide& sd, int U0, int Ut, int nb0, int nt0, int nt1,
+                                         int ob, int G, int row_in_sub, int cg, bool leader,
+                                         float* __restrict__ sk_slots, unsigned* __restrict__ sk_cnt) {
+  const int bf = st.bf, bl = st.bl, tg = st.tg;
+  auto slot_of = [&](int c) { return splitk_slot(c, tg, U0, Ut, nb0, nt0, nt1, G); };
+  __threadfence();
+  asm volatile("bar.sync 2, %0;" ::"n"(NEPI * 32) : "memory");
+  __shared__ int s_last;
+  if (leader) {
+    unsigned* cnt = sk_cnt + slot_of(bf);
+    const unsigned old = atomicAdd(cnt, 1u);
+    const int last = old == (unsigned)(bl - bf);
+    if (last) *cnt = 0u;  // ready for the next launch
+    __threadfence();
+    s_last = last;
+  }
+  asm volatile("bar.sync 2, %0;" ::"n"(NEPI * 32) : "memory");
+  if (!s_last) return;
+#pragma unroll
+  for (int j = 0; j < NSUB; ++j) {
+    float tot[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) tot[c] = 0.f;
+    // contributors in CTA order, two slots' loads in flight at a time
+    const size_t off = (size_t)(j * BMT + row_in_sub) * S + cg;
+    int k = bf;
+    for (; k + 1 <= bl; k += 2) {
+      const float* s0p = sk_slots + (size_t)slot_of(k) * (NSUB * BMT * S) + off;
+      const float* s1p = sk_slots + (size_t)slot_of(k + 1) * (NSUB * BMT * S) + off;
+      float4 va[8], vb[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        va[c] = __ldcg((const float4*)(s0p + 4 * c));
+        vb[c] = __ldcg((const float4*)(s1p + 4 * c));
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        tot[4 * c] += va[c].x;
+        tot[4 * c + 1] += va[c].y;
+        tot[4 * c + 2] += va[c].z;
+        tot[4 * c + 3] += va[c].w;
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        tot[4 * c] += vb[c].x;
+        tot[4 * c + 1] += vb[c].y;
+        tot[4 * c + 2] += vb[c].z;
+        tot[4 * c + 3] += vb[c].w;
+      }
+    }
+    if (k <= bl) {
+      const float* s0p = sk_slots + (size_t)slot_of(k) * (NSUB * BMT * S) + off;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 v = __ldcg((const float4*)(s0p + 4 * c));
+        tot[4 * c] += v.x;
+        tot[4 * c + 1] += v.y;
+        tot[4 * c + 2] += v.z;
+        tot[4 * c + 3] += v.w;
+      }
+    }
+    const int64_t row = (int64_t)ob * (NSUB * BMT) + j * BMT + row_in_sub;
+    if (row < sd.P) {
+      float* dst = sd.out + row * S + cg;
+#pragma unroll
+      for (int c = 0; c < 32; c += 4) *(float4*)(dst + c) = make_float4(tot[c], tot[c + 1], tot[c + 2], tot[c + 3]);
+    }
+  }
+}
 
 // MODE 0: one forward side, 1: one transpose side, 2: two sides (paired),
 // 3: one forward side that also sums A^2 (the residual pass)
@@ -397,7 +496,7 @@ template <int S, int MODE>
 __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
     stream_pass2(const __grid_constant__ TmaDesc tA0, const __grid_constant__ TmaDesc tB0,
                  const __grid_constant__ TmaDesc tA1, const __grid_constant__ TmaDesc tB1, const PassSide s0,
-                 const PassSide s1, int whole, ZSync* __restrict__ zs) {
+                 const PassSide s1, int whole, float* __restrict__ sk_slots, unsigned* __restrict__ sk_cnt) {
   using C = TcCfg2<S>;
   constexpr bool SINGLE = MODE != 2;
   using Walk = WalkT<SINGLE>;
@@ -454,22 +553,9 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (zs != nullptr) {
-    for (int q = 0; q < 2; ++q) {
-      const PassSide& sd = q ? s1 : s0;
-      if (sd.nblocks == 0) continue;
-      const int64_t z0 = b * sd.P / G, z1 = (b + 1) * sd.P / G;
-      float4* o4 = reinterpret_cast<float4*>(sd.out + z0 * S);
-      for (int64_t i = threadIdx.x; i < (z1 - z0) * S / 4; i += blockDim.x) o4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (zs != nullptr && threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(&zs->arrived, 1u);
-  }
   const uint32_t tmem = *tmem_slot;
   if constexpr (C::REBAL) {
     if (warp < 4)
@@ -549,33 +635,35 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
       racc.next();
       if (tile_end) {
         const PassSide& sd = w.p ? s1 : s0;
-        const bool owned = w.owned(nt);
-        if (!owned && zs != nullptr) {
-          if (lane == 0) {
-            unsigned v;
-            do {
-              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&zs->arrived) : "memory");
-            } while (v < gridDim.x);
-          }
-          __syncwarp();
-        }
+        if (w.owned(nt)) {
 #pragma unroll
-        for (int j = 0; j < NSUB; ++j) {
-          const int64_t row = w.ob * (NSUB * BMT) + j * BMT + row_in_sub;
-          if (row < sd.P) {
-            float* dst = sd.out + row * S + cg;
-            if (owned) {
+          for (int j = 0; j < NSUB; ++j) {
+            const int64_t row = w.ob * (NSUB * BMT) + j * BMT + row_in_sub;
+            if (row < sd.P) {
+              float* dst = sd.out + row * S + cg;
 #pragma unroll
               for (int c = 0; c < 32; c += 4)
                 *(float4*)(dst + c) = make_float4(acc[j][c], acc[j][c + 1], acc[j][c + 2], acc[j][c + 3]);
-            } else {
-#pragma unroll
-              for (int c = 0; c < 32; c += 4) red_add_v4(dst + c, acc[j][c], acc[j][c + 1], acc[j][c + 2], acc[j][c + 3]);
             }
           }
+        } else {
+          SplitTile stile;
+          float* mine = splitk_mine(stile, (int)U0, (int)(U0 + U1), (int)s0.nblocks, s0.nt, s1.nt, w.p, w.ob, nt,
+                                    (int)G, (int)b, sk_slots, NSUB * BMT * S);
+#pragma unroll
+          for (int j = 0; j < NSUB; ++j) {
+            float* dst = mine + (j * BMT + row_in_sub) * S + cg;
+#pragma unroll
+            for (int c = 0; c < 32; c += 4)
+              __stcg((float4*)(dst + c), make_float4(acc[j][c], acc[j][c + 1], acc[j][c + 2], acc[j][c + 3]));
+          }
+          splitk_tile<S, NEPI_OF<S>()>(stile, sd, (int)U0, (int)(U0 + U1), (int)s0.nblocks, s0.nt, s1.nt, w.ob,
+                                      (int)G, row_in_sub, cg, warp == C::EPI0 && lane == 0, sk_slots, sk_cnt);
+        }
+#pragma unroll
+        for (int j = 0; j < NSUB; ++j)
 #pragma unroll
           for (int c = 0; c < 32; ++c) acc[j][c] = 0.f;
-        }
       }
       w.skip(len, s0, s1);
       it += len;
@@ -672,8 +760,8 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
       const bool trans = MODE == 1 || (MODE == 2 && (w.p ? s1.trans : s0.trans));
       constexpr bool sq = MODE == 3;
       // panel K chunk pc: rows k = 4 pc + jj, columns n = lane + 32 t
-      float ph[PT][4], pl[PT][4];
       {
+        float ph[PT][4], pl[PT][4];
         const float* raw = (const float*)(stage + C::ABYTES);
 #pragma unroll
         for (int t = 0; t < PT; ++t)
@@ -683,6 +771,14 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
             ph[t][jj] = tf32_rn(v);
             pl[t][jj] = v - ph[t][jj];
           }
+        unsigned char* dst = sP + ra.i * C::BSPL;  // the slot is free (mdone above)
+#pragma unroll
+        for (int t = 0; t < PT; ++t) {
+          const int n = lane + 32 * t;
+          const uint32_t off = (uint32_t)n * 128 + ((pc ^ (n & 7)) << 4);
+          *(float4*)(dst + off) = make_float4(ph[t][0], ph[t][1], ph[t][2], ph[t][3]);
+          *(float4*)(dst + S * 128 + off) = make_float4(pl[t][0], pl[t][1], pl[t][2], pl[t][3]);
+        }
       }
       const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + C::A_COL0 + ra.i * C::ASLOT + 16 * half;
       // A: sub-tile by sub-tile (load, split, store to TMEM); every loaded
@@ -722,16 +818,14 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
         tmem_st16(ta + j * 2 * BKT, hv);
         tmem_st16(ta + j * 2 * BKT + BKT, lv);
       }
+      // every value loaded from the stage has now been consumed by an
+      // instruction that cannot issue before its load returned (the panel
+      // STS above, the A tcgen05.st): only then is the stage handed back to
+      // the TMA producer. (Releasing it while the panel split could still be
+      // scheduled after the arrive let the next TMA overwrite panel rows in
+      // flight: ~2 % wrong tiles in 34 of 200 launches, tools/stress_splitk.py.)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[r.i]);
-      unsigned char* dst = sP + ra.i * C::BSPL;
-#pragma unroll
-      for (int t = 0; t < PT; ++t) {
-        const int n = lane + 32 * t;
-        const uint32_t off = (uint32_t)n * 128 + ((pc ^ (n & 7)) << 4);
-        *(float4*)(dst + off) = make_float4(ph[t][0], ph[t][1], ph[t][2], ph[t][3]);
-        *(float4*)(dst + S * 128 + off) = make_float4(pl[t][0], pl[t][1], pl[t][2], pl[t][3]);
-      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       fence_proxy_async();  // generic-proxy smem stores -> tensor-core (async proxy) reads
       tc_fence_before();
@@ -750,12 +844,10 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (zs != nullptr && threadIdx.x == 0 && atomicAdd(&zs->finished, 1u) == gridDim.x - 1) {
-    zs->arrived = 0u;
-    zs->finished = 0u;
-  }
   if (warp == kWarpMma) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
+
+constexpr int kSplitKCtas = 256;  // >= the SM count of the device (148 on B200)
 
 struct SideArgs {
   const float* panel;
@@ -808,11 +900,20 @@ int launch_stream2(const float* A, int64_t m, int64_t n, int64_t lda, const Side
   const int64_t slots = (int64_t)device_sms() * occ;
   const int whole = (nsides == 1 && T >= 16 * slots) ? 1 : 0;
   const int64_t grid = std::min<int64_t>(slots, whole ? T : U);
-  ZSync* zs = nullptr;
+  // split-K slots and arrival counters (fixed size: two slots per CTA; the
+  // counters return to zero after every launch). One set per device, shared
+  // by the launches of a stream; launches on concurrent streams would need
+  // their own set (not done: the library enqueues passes on one stream).
+  float* sk_slots = nullptr;
+  unsigned* sk_cnt = nullptr;
   if (!whole) {
-    void* ring = nullptr;
-    CNMF_TRY(device_scratch("pass-zsync", 64 * sizeof(ZSync), &ring, st));
-    zs = (ZSync*)ring + (device_ticket("pass-zsync") % 64);
+    const size_t slots = 2 * (size_t)kSplitKCtas;
+    if (grid > kSplitKCtas) return fail(CNMF_ERR_CUDA, "split-K slots: grid larger than the device's SM count");
+    if ((double)U * (double)grid >= 2147483647.0) return fail(CNMF_ERR_ARGUMENT, "split-K pass: too many units");
+    void* p = nullptr;
+    CNMF_TRY(device_scratch("pass2-splitk", slots * (NSUB * BMT * 64 * 4) + slots * 4, &p, st));
+    sk_slots = (float*)p;
+    sk_cnt = (unsigned*)(sk_slots + slots * (NSUB * BMT * 64));
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (pass_profiling()) {
@@ -830,7 +931,7 @@ int launch_stream2(const float* A, int64_t m, int64_t n, int64_t lda, const Side
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
-  CNMF_CUDA(cudaLaunchKernelEx(&lc, kern, tA[0], tB[0], tA[1], tB[1], sd[0], sd[1], whole, zs));
+  CNMF_CUDA(cudaLaunchKernelEx(&lc, kern, tA[0], tB[0], tA[1], tB[1], sd[0], sd[1], whole, sk_slots, sk_cnt));
   CNMF_LAUNCH_CHECK();
   if (e0) {
     CNMF_CUDA(cudaEventRecord(e1, st));

@@ -411,6 +411,34 @@ def test_passes_split_k_repeated(m, n):
         assert ((z.double() - zref).abs().max() / zref.abs().max()).item() < 1e-5
 
 
+@pytest.mark.parametrize("m,n,S", [(4000, 3000, 32), (5000, 3000, 32), (3000, 4000, 64), (10000, 5000, 32),
+                                   (2600, 1300, 64)])
+def test_passes_bit_reproducible(m, n, S):
+    # split-K tiles are reduced in CTA order by the last contributor
+    # (csrc/tc_pass2.cu): repeated launches -- single and paired -- give
+    # bit-identical outputs
+    g = torch.Generator(device="cuda").manual_seed(3 * m + n)
+    a = torch.rand(m, n, device="cuda", generator=g)
+    A = DeviceMatrix(a)
+    x = torch.randn(n, S, device="cuda", generator=g)
+    w = torch.randn(m, S, device="cuda", generator=g)
+    lib = _lib.load()
+    outs = []
+    for _ in range(40):
+        y, z, y2, z2 = zeros((m, S)), zeros((n, S)), zeros((m, S)), zeros((n, S))
+        assert lib.cnmf_pass_forward(A.ptr, m, n, A.lda, x.data_ptr(), S, y.data_ptr(), stream()) == 0
+        assert lib.cnmf_pass_transpose(A.ptr, m, n, A.lda, w.data_ptr(), S, z.data_ptr(), stream()) == 0
+        assert lib.cnmf_pass_pair(A.ptr, m, n, A.lda, x.data_ptr(), y2.data_ptr(), w.data_ptr(), z2.data_ptr(), S,
+                                  stream()) == 0
+        torch.cuda.synchronize()
+        outs.append((y, z, y2, z2))
+    yref = a.double() @ x.double()
+    assert ((outs[0][0].double() - yref).abs().max() / yref.abs().max()).item() < 1e-5
+    for o in outs[1:]:
+        for u, v in zip(o, outs[0]):
+            assert torch.equal(u, v)
+
+
 @pytest.mark.parametrize("m,n,s", [(10000, 5000, 30), (4000, 3000, 30), (3000, 4000, 30), (300, 200, 30),
                                    (2500, 1300, 60)])
 def test_paired_pass_matches_separate(m, n, s):
