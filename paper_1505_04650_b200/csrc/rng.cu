@@ -15,9 +15,13 @@
 //       the entry itself) and prefix-sums the corrected counts;
 //   k3  one warp per segment decodes again from its true entry and writes its
 //       variates at the scanned offset.
-// Any segment whose chain does not merge inside its first window flags the
-// stream, which is then decoded by one warp sequentially (never observed; kept
-// for exactness).
+// Any segment whose chain does not merge inside its first window, or a stream
+// whose segments end before its last variate, flags the stream, which is then
+// decoded by one warp sequentially. The segments cover the stream's variate
+// count plus a 5 % margin of raw positions: with 2 % one 4096 x 60 chunk of
+// configs[4]'s right test matrix (child_seed(5, "right-basis")) ran short and
+// its serial decode took 10 ms (tools/zig_probe.py); the streams are the same
+// either way.
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -463,7 +467,10 @@ static Layout make_layout(uint64_t seed, int64_t rows, int64_t cols, int64_t chu
   L.nchunks = ceil_div(rows, L.chunk_rows);
   L.key = seed;
   auto seg = [](int64_t count, int32_t* seglen, int32_t* nseg) {
-    const int64_t need = (int64_t)(count * 1.02) + 4 * kWin;
+#ifndef CNMF_ZIG_MARGIN
+#define CNMF_ZIG_MARGIN 1.05
+#endif
+    const int64_t need = (int64_t)(count * CNMF_ZIG_MARGIN) + 4 * kWin;
     int64_t len = kWin;  // one window per segment: 4x the warps of 4-window segments (latency-bound walk)
     while (ceil_div(need, len) > 1024) len *= 2;
     *seglen = (int32_t)len;
