@@ -26,6 +26,10 @@ __global__ void k_inv(double* Mg, int r, long long* cyc) {
   long long t0 = clock64();
   spd_inverse(M, piv, r);
   long long t1 = clock64();
+#ifdef TWICE
+  spd_inverse(M, piv, r);  // inverse of the inverse
+  spd_inverse(M, piv, r);
+#endif
   for (int i = threadIdx.x; i < r * r; i += blockDim.x) Mg[i] = M[i];
   if (threadIdx.x == 0) *cyc = t1 - t0;
 }
