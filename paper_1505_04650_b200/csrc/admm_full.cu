@@ -385,7 +385,9 @@ __global__ void __launch_bounds__(kThreads) full_right(FullArgs a, int init) {
       double gg = 0.0;
       for (int i = 0; i < r; ++i)
         for (int l = 0; l < r; ++l) gg = fma(a.mats->Gx[i * kR + l], a.mats->Gy[i * kR + l], gg);
-      a.trace[c->k] = c->nA2 - 2.0 * acc[3] + gg;
+      // the expansion cancels for well-fitted data (absolute error ~1e-7 ||A||^2,
+      // DESIGN.md): a squared norm is never negative
+      a.trace[c->k] = fmax(c->nA2 - 2.0 * acc[3] + gg, 0.0);
       c->part[2] = sqrt(acc[4]);
       c->part[3] = sqrt(acc[5]);
       c->part[4] = sqrt(acc[6]);
