@@ -22,10 +22,12 @@ namespace {
 constexpr int kQMax = 64;
 
 struct WarpScratch {
-  double* L;    // lower factor (row-major, odd stride ld), insertion order
+  double* L;    // lower factor, packed by rows (entry (i, j), j <= i, at i (i + 1) / 2 + j), insertion order
   int* order;   // passive indices in insertion order
-  int ld;
+  int ld;       // unused (packed storage: half the shared memory per warp, twice the warps per SM)
 };
+
+__device__ __forceinline__ int tri(int i, int j) { return ((i * (i + 1)) >> 1) + j; }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -50,12 +52,12 @@ __device__ bool chol_add(const double* G, int q, WarpScratch ws, int p, int a, d
   }
   // forward substitution L y = b (column-oriented)
   for (int j = 0; j < p; ++j) {
-    const double yj = vget(b, j) / ws.L[j * ws.ld + j];
+    const double yj = vget(b, j) / ws.L[tri(j, j)];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int i = lane + 32 * h;
       if (i == j) b[h] = yj;
-      else if (i > j && i < p) b[h] -= ws.L[i * ws.ld + j] * yj;
+      else if (i > j && i < p) b[h] -= ws.L[tri(i, j)] * yj;
     }
   }
   double yy = 0.0;
@@ -64,7 +66,7 @@ __device__ bool chol_add(const double* G, int q, WarpScratch ws, int p, int a, d
     const int i = lane + 32 * h;
     if (i < p) {
       yy += b[h] * b[h];
-      ws.L[p * ws.ld + i] = b[h];
+      ws.L[tri(p, i)] = b[h];
     }
   }
   yy = warp_sum(yy);
@@ -73,7 +75,7 @@ __device__ bool chol_add(const double* G, int q, WarpScratch ws, int p, int a, d
   __syncwarp();
   if (!(d > 1e-13 * fabs(gaa)) || !isfinite(d)) return false;
   if (lane == 0) {
-    ws.L[p * ws.ld + p] = sqrt(d);
+    ws.L[tri(p, p)] = sqrt(d);
     ws.order[p] = a;
   }
   __syncwarp();
@@ -102,22 +104,22 @@ __device__ void chol_solve(const double (&t)[2], int q, WarpScratch ws, int p, d
   }
   // forward L u = t_P
   for (int j = 0; j < p; ++j) {
-    const double uj = vget(w, j) / ws.L[j * ws.ld + j];
+    const double uj = vget(w, j) / ws.L[tri(j, j)];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int i = lane + 32 * h;
       if (i == j) w[h] = uj;
-      else if (i > j && i < p) w[h] -= ws.L[i * ws.ld + j] * uj;
+      else if (i > j && i < p) w[h] -= ws.L[tri(i, j)] * uj;
     }
   }
   // backward L^T v = u
   for (int j = p - 1; j >= 0; --j) {
-    const double vj = vget(w, j) / ws.L[j * ws.ld + j];
+    const double vj = vget(w, j) / ws.L[tri(j, j)];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int i = lane + 32 * h;
       if (i == j) w[h] = vj;
-      else if (i < j) w[h] -= ws.L[j * ws.ld + i] * vj;
+      else if (i < j) w[h] -= ws.L[tri(j, i)] * vj;
     }
   }
   // scatter back to index space: z[order[i]] = w[i]
@@ -130,18 +132,25 @@ __device__ void chol_solve(const double (&t)[2], int q, WarpScratch ws, int p, d
   }
 }
 
+// H0 (optional, k x q0 with q0 < q): a feasible start -- the solution of the
+// same targets over the first q0 design columns (XRAY's previous refit: the
+// picks grow by appending). Its support becomes the initial passive set and
+// the iteration proceeds from it exactly as from any feasible iterate; the
+// minimiser is unique when the design has full column rank, so only the
+// exchange path (not the answer) changes.
 __global__ void nnls_kernel(const double* __restrict__ gram_g, const double* __restrict__ target, int64_t k, int q,
                             double tol, int cap, double ridge, double* __restrict__ H,
-                            unsigned long long* __restrict__ n_capped) {
+                            unsigned long long* __restrict__ n_capped, const double* __restrict__ H0, int q0) {
   extern __shared__ double smem[];
   double* G = smem;  // q x q
   const int wpb = blockDim.x / 32;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < q * q; i += blockDim.x) G[i] = gram_g[i];
   WarpScratch ws;
-  ws.ld = q | 1;
-  ws.L = G + q * q + (size_t)warp * q * ws.ld;
-  ws.order = (int*)(G + q * q + (size_t)wpb * q * ws.ld) + warp * kQMax;
+  const int tsz = (q * (q + 1) / 2 + 1) & ~1;  // packed factor, 16-byte multiple
+  ws.ld = 0;
+  ws.L = G + q * q + (size_t)warp * tsz;
+  ws.order = (int*)(G + q * q + (size_t)wpb * tsz) + warp * kQMax;
   __syncthreads();
 
   for (int64_t col = (int64_t)blockIdx.x * wpb + warp; col < k; col += (int64_t)gridDim.x * wpb) {
@@ -158,7 +167,30 @@ __global__ void nnls_kernel(const double* __restrict__ gram_g, const double* __r
     bool capped = false;
     bool factored = true;  // factor of order[0..p) is valid
     bool ridged = false;
+    bool warm = false;     // run the feasibility loop on the start before the first entering index
+    if (H0 != nullptr) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = lane + 32 * e;
+        h[e] = (i < q0) ? fmax(H0[col * q0 + i], 0.0) : 0.0;
+      }
+      pas = (uint64_t)__ballot_sync(0xffffffffu, h[0] > 0.0) |
+            ((uint64_t)__ballot_sync(0xffffffffu, h[1] > 0.0) << 32);
+      p = __popcll(pas);
+      if (p > 0) {
+        if (lane == 0) {
+          int np = 0;
+          for (int i = 0; i < q; ++i)
+            if ((pas >> i) & 1ull) ws.order[np++] = i;
+        }
+        __syncwarp();
+        ridged = !chol_rebuild(G, q, ws, p, 0.0);
+        if (ridged) chol_rebuild(G, q, ws, p, ridge);
+        warm = true;
+      }
+    }
     for (;;) {
+      if (!warm) {
       // entering index: first argmax of grad over the active set
       double bv = -DBL_MAX;
       int bi = q;
@@ -199,6 +231,8 @@ __global__ void nnls_kernel(const double* __restrict__ gram_g, const double* __r
         if (ridged) chol_rebuild(G, q, ws, p, ridge);
         factored = true;
       }
+      }  // !warm
+      warm = false;
       for (;;) {
         double z[2];
         chol_solve(t, q, ws, p, z);
@@ -303,7 +337,7 @@ __global__ void nnls_kernel(const double* __restrict__ gram_g, const double* __r
 }  // namespace
 
 int nnls_gram(const double* gram, const double* target, int64_t k, int q, double tol, int max_exchanges, double* H,
-              int64_t* n_capped, cudaStream_t st) {
+              int64_t* n_capped, cudaStream_t st, const double* H0, int q0) {
   if (q < 1 || q > kQMax) return fail(CNMF_ERR_ARGUMENT, "nnls: 1 <= q <= 64 required");
   if (!(tol > 0)) return fail(CNMF_ERR_ARGUMENT, "tol must be positive");
   if (k == 0) return CNMF_OK;
@@ -316,9 +350,9 @@ int nnls_gram(const double* gram, const double* target, int64_t k, int q, double
   for (int i = 0; i < q; ++i) tr += hg[i * q + i];
   delete[] hg;
   const double ridge = 1e-12 * tr;
-  const int ldl = q | 1;
-  const size_t per_warp = (size_t)q * ldl * 8 + kQMax * 4;
-  int wpb = (int)std::min<size_t>(16, (200 * 1024 - (size_t)q * q * 8) / per_warp);
+  const size_t tsz = (size_t)((q * (q + 1) / 2 + 1) & ~1);
+  const size_t per_warp = tsz * 8 + kQMax * 4;
+  int wpb = (int)std::min<size_t>(32, (220 * 1024 - (size_t)q * q * 8) / per_warp);
   wpb = std::max(1, wpb);
   const size_t smem = (size_t)q * q * 8 + (size_t)wpb * per_warp;
   static bool attr = false;
@@ -331,7 +365,8 @@ int nnls_gram(const double* gram, const double* target, int64_t k, int q, double
   CNMF_CUDA(cudaMallocAsync((void**)&d_cap, 8, st));
   CNMF_CUDA(cudaMemsetAsync(d_cap, 0, 8, st));
   const int64_t blocks = std::min<int64_t>(ceil_div(k, wpb), 16 * kNumSMs);
-  nnls_kernel<<<(unsigned)blocks, 32 * wpb, smem, st>>>(gram, target, k, q, tol, cap, ridge, H, d_cap);
+  nnls_kernel<<<(unsigned)blocks, 32 * wpb, smem, st>>>(gram, target, k, q, tol, cap, ridge, H, d_cap,
+                                                        (H0 != nullptr && q0 > 0 && q0 < q) ? H0 : nullptr, q0);
   CNMF_LAUNCH_CHECK();
   unsigned long long hcap = 0;
   CNMF_CUDA(cudaMemcpyAsync(&hcap, d_cap, 8, cudaMemcpyDeviceToHost, st));

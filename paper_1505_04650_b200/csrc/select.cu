@@ -20,7 +20,8 @@
 
 namespace cnmf {
 
-int nnls_gram(const double*, const double*, int64_t, int, double, int, double*, int64_t*, cudaStream_t);
+int nnls_gram(const double*, const double*, int64_t, int, double, int, double*, int64_t*, cudaStream_t,
+              const double* H0 = nullptr, int q0 = 0);
 
 namespace {
 
@@ -480,7 +481,8 @@ int panel_to_f64(const float* src, int64_t rows, int S, double* dst, int64_t ld,
 // NNLS coefficients of every column over the picked columns (snmf.py:129-137).
 // Ht: n x k (coefficients transposed). scratch: k*k + n*k doubles.
 int right_factor(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_picks, int k, double tol,
-                 double* Ht, double* scratch, int64_t* n_capped, cudaStream_t st) {
+                 double* Ht, double* scratch, int64_t* n_capped, cudaStream_t st, const double* H0 = nullptr,
+                 int q0 = 0) {
   double* gram = scratch;
   double* target = scratch + (size_t)k * k;
   const size_t sm = (size_t)k * s * 8;
@@ -491,7 +493,7 @@ int right_factor(const double* W, int64_t n, int s, int64_t ld, const int64_t* d
   }
   gather_gram<<<sel_grid(n), kSelThreads, sm, st>>>(W, n, s, ld, W, d_picks, k, gram, target);
   CNMF_LAUNCH_CHECK();
-  return nnls_gram(gram, target, n, k, tol, 0, Ht, n_capped, st);
+  return nnls_gram(gram, target, n, k, tol, 0, Ht, n_capped, st, H0, q0);
 }
 
 // residual norms ||W - W[:, picks] H||^2 and ||W||^2 into tot[0..1] (device)
@@ -509,6 +511,12 @@ int refit_norms(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_
   return CNMF_OK;
 }
 
+// CNMF_XRAY_WARM=0: every refit from h = 0 like the reference (A/B)
+static bool xray_warm() {
+  const char* e = getenv("CNMF_XRAY_WARM");
+  return !(e && e[0] == '0');
+}
+
 // XRAY (snmf.py:74-126). W: n x ld fp64 (the reduced matrix, transposed);
 // mass: device s-vector; picks_host receives the picks.
 int select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const double* mass, double nnls_tol,
@@ -519,7 +527,7 @@ int select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const doub
   const unsigned agrid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kSelThreads), 4 * kNumSMs));
   // buffers
   size_t bytes = (size_t)n * ld * 8 /*R*/ + (size_t)n * 8 * 3 /*sq, denom, score*/ + (size_t)n * 2 /*flags*/ +
-                 (size_t)64 * 64 * 8 + (size_t)n * 64 * 8 * 2 /*target, H*/ + 4096 * 16 + 64 * 8 + 1024;
+                 (size_t)64 * 64 * 8 + (size_t)n * 64 * 8 * 3 /*target, H, previous H*/ + 4096 * 16 + 64 * 8 + 1024;
   char* buf = nullptr;
   keep_pool();
   CNMF_CUDA(cudaMallocAsync((void**)&buf, bytes, st));
@@ -537,6 +545,7 @@ int select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const doub
   uint8_t* scorable = (uint8_t*)take((size_t)n);
   double* scratch = (double*)take((size_t)64 * 64 * 8 + (size_t)n * 64 * 8);
   double* Ht = (double*)take((size_t)n * 64 * 8);
+  double* Hprev = (double*)take((size_t)n * 64 * 8);
   double* blk_v = (double*)take(4096 * 8);
   int64_t* blk_i = (int64_t*)take(4096 * 8);
   int64_t* d_picks = (int64_t*)take(64 * 8);
@@ -605,8 +614,12 @@ int select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const doub
     const uint8_t one = 1;
     CNMF_CUDA(cudaMemcpyAsync(picked + i, &one, 1, cudaMemcpyHostToDevice, st));
     int64_t capped = 0;
-    CNMF_TRY(right_factor(W, n, s, ld, d_picks, (int)hp.size(), nnls_tol, Ht, scratch, &capped, st));
+    // warm start from the previous refit (the picks only grew by one): the
+    // same unique minimiser, a fraction of the exchanges (tools/xray_profile.py)
+    CNMF_TRY(right_factor(W, n, s, ld, d_picks, (int)hp.size(), nnls_tol, Ht, scratch, &capped, st,
+                          hp.size() > 1 && xray_warm() ? Hprev : nullptr, (int)hp.size() - 1));
     CNMF_TRY(refit_norms(W, n, s, ld, d_picks, (int)hp.size(), Ht, R, sq, nullptr, st));
+    std::swap(Ht, Hprev);  // Hprev = this refit
   }
   CNMF_CUDA(cudaStreamSynchronize(st));
   CNMF_CUDA(cudaFreeAsync(buf, st));
