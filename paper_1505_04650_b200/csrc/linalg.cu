@@ -52,12 +52,7 @@ __global__ void init_info(int* info) {
 int chol_inv(const double* G, int s, int S, double* T, double* R, int* info, int pass_id, cudaStream_t st) {
   // s <= 32: 256-thread register-tile factorisation (chol_tile32), else the block version
   const size_t smem = std::max(((size_t)s * s + 2 * (size_t)s) * 8, (size_t)(32 * 33 + 128) * 8);
-  static bool attr = false;
-  if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (128 * 128 + 256) * 8));
-    attr = true;
-  }
+  CNMF_TRY(ensure_smem_attr((const void*)chol_inv_kernel, (128 * 128 + 256) * 8));
   chol_inv_kernel<<<1, s <= 32 ? 256 : 512, smem, st>>>(G, s, S, T, R, info, pass_id);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;

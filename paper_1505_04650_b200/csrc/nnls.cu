@@ -355,11 +355,7 @@ int nnls_gram(const double* gram, const double* target, int64_t k, int q, double
   int wpb = (int)std::min<size_t>(32, (220 * 1024 - (size_t)q * q * 8) / per_warp);
   wpb = std::max(1, wpb);
   const size_t smem = (size_t)q * q * 8 + (size_t)wpb * per_warp;
-  static bool attr = false;
-  if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(nnls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
+  CNMF_TRY(ensure_smem_attr((const void*)nnls_kernel, 227 * 1024));
   unsigned long long* d_cap = nullptr;
   keep_pool();
   CNMF_CUDA(cudaMallocAsync((void**)&d_cap, 8, st));

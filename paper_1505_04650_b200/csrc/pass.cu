@@ -337,11 +337,7 @@ int launch_forward(const float* A, int64_t m, int64_t n, int64_t lda, const floa
   const int64_t grid = std::min<int64_t>(kNumSMs, whole ? mb : mb * nkt);
   if (!whole) CNMF_CUDA(cudaMemsetAsync(Y, 0, (size_t)m * S * 4, st));
   constexpr size_t smem = fwd_smem<S>();
-  static bool attr = false;
-  if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(fwd_ffma<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  CNMF_TRY(ensure_smem_attr((const void*)fwd_ffma<S>, (int)smem));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (pass_profiling()) {
     CNMF_CUDA(cudaEventCreate(&e0));
@@ -369,11 +365,7 @@ int launch_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const fl
   const int64_t grid = std::min<int64_t>(kNumSMs, whole ? nb : nb * nrt);
   if (!whole) CNMF_CUDA(cudaMemsetAsync(Z, 0, (size_t)n * S * 4, st));
   constexpr size_t smem = trn_smem<S>();
-  static bool attr = false;
-  if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(trn_ffma<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  CNMF_TRY(ensure_smem_attr((const void*)trn_ffma<S>, (int)smem));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (pass_profiling()) {
     CNMF_CUDA(cudaEventCreate(&e0));
@@ -392,11 +384,7 @@ int launch_transpose(const float* A, int64_t m, int64_t n, int64_t lda, const fl
 template <int S>
 int launch_apply(float* P, int64_t rows, const double* T, cudaStream_t st) {
   constexpr size_t smem = (size_t)(S * S + 2 * 64 * S) * 4;
-  static bool attr = false;
-  if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(apply_panel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  CNMF_TRY(ensure_smem_attr((const void*)apply_panel<S>, (int)smem));
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 64), 2 * kNumSMs));
   apply_panel<S><<<grid, kThreads, smem, st>>>(P, rows, T);
   CNMF_LAUNCH_CHECK();

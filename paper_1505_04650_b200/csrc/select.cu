@@ -486,11 +486,7 @@ int right_factor(const double* W, int64_t n, int s, int64_t ld, const int64_t* d
   double* gram = scratch;
   double* target = scratch + (size_t)k * k;
   const size_t sm = (size_t)k * s * 8;
-  static bool attr = false;
-  if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(gather_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  CNMF_TRY(ensure_smem_attr((const void*)gather_gram, 200 * 1024));
   gather_gram<<<sel_grid(n), kSelThreads, sm, st>>>(W, n, s, ld, W, d_picks, k, gram, target);
   CNMF_LAUNCH_CHECK();
   return nnls_gram(gram, target, n, k, tol, 0, Ht, n_capped, st, H0, q0);
@@ -499,11 +495,7 @@ int right_factor(const double* W, int64_t n, int s, int64_t ld, const int64_t* d
 // residual norms ||W - W[:, picks] H||^2 and ||W||^2 into tot[0..1] (device)
 int refit_norms(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_picks, int k, const double* Ht,
                 double* R, double* sq_out, double* tot, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    CNMF_CUDA(cudaFuncSetAttribute(refit_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
+  CNMF_TRY(ensure_smem_attr((const void*)refit_residual, 200 * 1024));
   if (tot) CNMF_CUDA(cudaMemsetAsync(tot, 0, 16, st));
   refit_residual<<<sel_grid(n), kSelThreads, (size_t)k * s * 8, st>>>(W, n, s, ld, W, d_picks, k, Ht, R, sq_out,
                                                                       tot);

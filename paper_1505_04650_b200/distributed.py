@@ -44,6 +44,11 @@ from .errors import ConvergenceError, RankDeficiencyError, UndefinedMetricError
 from .rng import child_seed
 
 
+class _Done:
+    def wait(self):
+        return True
+
+
 def column_shard(n, world, rank):
     """Contiguous balanced column range (c0, n_i) of `rank`."""
     base, extra = divmod(int(n), int(world))
@@ -64,6 +69,14 @@ class Comm:
         if self.world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
+
+    def allreduce_async(self, t):
+        """Start a SUM all-reduce of `t` in place; the handle's wait() makes
+        the caller's stream wait for it (NCCL runs it on its own stream, so a
+        kernel enqueued before wait() overlaps the transfer)."""
+        if self.world > 1:
+            return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        return _Done()
 
     def allreduce_max(self, t):
         if self.world > 1:
@@ -319,11 +332,53 @@ def range_finder(ops, comm, A, m, n, c0, cfg, side):
     return P
 
 
+def range_finders_interleaved(ops, comm, A, m, n, c0, lcfg, rcfg):
+    """Both range finders of nmf_admm, interleaved step by step (the sharded
+    counterpart of cnmf_compress_pair_async): at every power step one chain
+    needs a forward pass (partial sum, all-reduced) and the other a transpose
+    pass (local). The forward pass is enqueued first, its all-reduce is
+    started asynchronously, and the transpose pass runs on the GPU while the
+    NCCL transfer is in flight; the replicated / sharded orthonormalisations
+    follow. Same arithmetic as two range_finder calls (each chain's sequence
+    of passes and orthonormalisations is unchanged), so the bases agree
+    bit for bit. Returns (Q replicated m x S, this rank's rows of R^T)."""
+    if lcfg.w != rcfg.w or lcfg.basis_cols != rcfg.basis_cols:
+        return (range_finder(ops, comm, A, m, n, c0, lcfg, 0), range_finder(ops, comm, A, m, n, c0, rcfg, 1))
+    s = lcfg.basis_cols
+    S = ops.panel_ld(s)
+    ops.begin(s)
+    # step 0: left Y = sum_i A_i Omega_i (forward), right P = A_i^T Omega' (transpose)
+    Y = ops.forward(A, ops.omega_rows(child_seed(lcfg.seed, "omega"), c0, A.n, s, S), S)
+    h = comm.allreduce_async(Y)
+    P = ops.transpose(A, ops.omega_rows(child_seed(rcfg.seed, "omega"), 0, m, s, S), S)
+    h.wait()
+    ops.orthonormalize(Y, s)
+    P = orthonormalize_sharded(ops, comm, P, s, S)
+    for _ in range(lcfg.w):
+        # left: Z = A^T Y (transpose), right: Y' = A P (forward, all-reduced)
+        Yr = ops.forward(A, P, S)
+        h = comm.allreduce_async(Yr)
+        Z = ops.transpose(A, Y, S)
+        h.wait()
+        ops.orthonormalize(Yr, s)
+        Z = orthonormalize_sharded(ops, comm, Z, s, S)
+        # left: Y = A Z (forward, all-reduced), right: P = A^T Y' (transpose)
+        Y = ops.forward(A, Z, S)
+        h = comm.allreduce_async(Y)
+        P = ops.transpose(A, Yr, S)
+        h.wait()
+        ops.orthonormalize(Y, s)
+        P = orthonormalize_sharded(ops, comm, P, s, S)
+    ops.end()
+    return Y, P
+
+
 def compressed_problem(ops, comm, A, m, n, c0, cfg):
     """Left basis (replicated), local rows of the right basis, and the core
     L^T A R^T (nmf.py:120-135, 327-332)."""
-    left = range_finder(ops, comm, A, m, n, c0, replace(cfg, seed=child_seed(cfg.seed, "left-basis")), 0)
-    right = range_finder(ops, comm, A, m, n, c0, replace(cfg, seed=child_seed(cfg.seed, "right-basis")), 1)
+    left, right = range_finders_interleaved(ops, comm, A, m, n, c0,
+                                            replace(cfg, seed=child_seed(cfg.seed, "left-basis")),
+                                            replace(cfg, seed=child_seed(cfg.seed, "right-basis")))
     S = left.shape[1]
     core = comm.allreduce(ops.cross(ops.transpose(A, left, S), right, S))
     s = cfg.basis_cols

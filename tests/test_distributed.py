@@ -221,6 +221,16 @@ def _jobs(rank, world, a, a_sep):
     L = D.range_finder(ops, comm, A, m, n, c0, cfg, 0)
     R = comm.allgather_rows(D.range_finder(ops, comm, A, m, n, c0, cfg, 1), counts)
     res["bases"] = (L[:, : cfg.basis_cols].numpy(), R[:, : cfg.basis_cols].numpy())
+    # the interleaved pair (forward pass's all-reduce overlapped with the other
+    # chain's transpose) against the two sequential finders, same seeds
+    from dataclasses import replace
+    lcfg = replace(cfg, seed=O.child_seed(11, "left-basis"))
+    rcfg = replace(cfg, seed=O.child_seed(11, "right-basis"))
+    Li, Ri = D.range_finders_interleaved(ops, comm, A, m, n, c0, lcfg, rcfg)
+    Ls = D.range_finder(ops, comm, A, m, n, c0, lcfg, 0)
+    Rs = D.range_finder(ops, comm, A, m, n, c0, rcfg, 1)
+    res["interleaved"] = (Li.numpy(), Ls.numpy(), comm.allgather_rows(Ri, counts).numpy(),
+                          comm.allgather_rows(Rs, counts).numpy())
     u, vt_local, it, _, rel = D.nmf_admm(A, m, n, c0, 4, CompressionConfig(r=4, r_ov=6, w=2, seed=11), comm, ops,
                                          max_iter=60, tol=1e-4)
     res["admm"] = (u.numpy(), comm.allgather_rows(vt_local, counts).numpy(), it, rel)
@@ -301,6 +311,12 @@ def test_sharded_bases_match_oracle(mat, sharded):
     assert O.projector_distance(R, O.row_basis(mat, cfg)) < 1e-10
     # identical columns (same canonical signs), not only the same span
     np.testing.assert_allclose(L, O.range_basis(mat, cfg), atol=1e-9)
+
+
+def test_interleaved_range_finders_equal_sequential(sharded):
+    Li, Ls, Ri, Rs = sharded["interleaved"]
+    np.testing.assert_array_equal(Li, Ls)
+    np.testing.assert_array_equal(Ri, Rs)
 
 
 def test_sharded_admm_matches_oracle(mat, sharded):
