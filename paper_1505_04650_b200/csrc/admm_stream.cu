@@ -18,6 +18,8 @@
 // U, dU, V, dV read and written (fp64) + L, R read (fp32).
 #include <algorithm>
 #include <cmath>
+#include <mutex>
+#include <string>
 
 #include "common.cuh"
 
@@ -203,7 +205,6 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
         for (int ni = 0; ni < 4; ++ni) {
           const int k = 32 * wn + 8 * ni + 2 * tq;
           double* xs = Xs + row * kLD + k;
-          const double2 xo = *(const double2*)xs;
           double xn[2] = {0.0, 0.0};
           if (update) {
             const double2 dxo2 = *(const double2*)(Ds + row * kLD + k);
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
                 }
             }
           } else {
+            const double2 xo = *(const double2*)xs;
             xn[0] = ron && k < r ? xo.x : 0.0;
             xn[1] = ron && k + 1 < r ? xo.y : 0.0;
           }
@@ -277,7 +279,10 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
         const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
         pf[j] = (row < nr) ? __ldg((const float4*)(sd.P + (t0 + row) * sd.ldp + c4)) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      if (vec) {
+      // the old x is needed only by the start-up sweep (update = 0: P^T x of
+      // the initial splits); an update sweep overwrites every entry of Xs
+      if (update) {
+      } else if (vec) {
         const int h = r >> 1;
         for (int i = tid; i < nr * h; i += kT) {
           const int row = i / h, c2 = i - row * h;
@@ -365,28 +370,40 @@ int sweep_blocks(int sms) {
   return occ * sms;
 }
 
-// fixed-order sums of the block partials of each side: sums[side][e]
+// fixed-order sums of the block partials of each side: sums[side][e]. A block
+// covers kRE elements x kRS segments of the side's blocks; a segment is summed
+// in block order and the segments are combined in segment order, so the
+// result does not depend on scheduling.
+constexpr int kRS = 4, kRE = kT / kRS;
 __global__ void __launch_bounds__(kT) reduce_parts(const double* __restrict__ part, int nbl, int nbr, int len,
                                                     double* __restrict__ sums, const SCtrl* ctrl, int update) {
   if (update && ctrl->done) return;
-  const int e = blockIdx.x * kT + threadIdx.x;
+  __shared__ double seg[kRS][kRE];
+  const int el = threadIdx.x % kRE, sg = threadIdx.x / kRE;
+  const int e = blockIdx.x * kRE + el;
   const int side = blockIdx.y;
-  if (e >= len) return;
   const int b0 = side ? nbl : 0, nb = side ? nbr : nbl;
   const int sr = (len - 4) / 2;
-  if (e >= sr && e < 2 * sr) {  // the dual projections come from the core step's recurrence
-    sums[side * len + e] = 0.0;
-    return;
-  }
+  const bool dual = e >= sr && e < 2 * sr;  // the dual projections come from the core step's recurrence
   double acc = 0.0;
-  for (int j0 = 0; j0 < nb; j0 += 8) {
-    double v[8];
+  if (e < len && !dual) {
+    const int per = (nb + kRS - 1) / kRS, j1 = min(nb, (sg + 1) * per);
+    for (int j0 = sg * per; j0 < j1; j0 += 8) {
+      double v[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = (j0 + j < nb) ? part[(size_t)(b0 + j0 + j) * len + e] : 0.0;
+      for (int j = 0; j < 8; ++j) v[j] = (j0 + j < j1) ? part[(size_t)(b0 + j0 + j) * len + e] : 0.0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc += v[j];
+      for (int j = 0; j < 8; ++j) acc += v[j];
+    }
   }
-  sums[side * len + e] = acc;
+  seg[sg][el] = acc;
+  __syncthreads();
+  if (sg == 0 && e < len) {
+    double t = seg[0][el];
+#pragma unroll
+    for (int j = 1; j < kRS; ++j) t += seg[j][el];
+    sums[side * len + e] = dual ? 0.0 : t;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -701,6 +718,191 @@ extern "C" int cnmf_debug_core_trace(long long* out) {
 namespace {
 #endif
 
+// ---------------------------------------------------------------------------
+// Single-GPU driver: the core step split so that only what the next sweep
+// needs sits between two sweeps (the column-sharded driver below keeps the
+// one-kernel core_step, its sums being all-reduced by the host in between).
+//
+//   core_x(k)  2 CTAs after the sweeps of iteration k - 1:
+//     CTA 0    xc_k = (P1 + pu L^T U - L^T dU) Minv: one product, Minv =
+//              (yc yc^T + pu I)^-1, P1 = core yc^T and G_L xc_{k-1} having
+//              been prepared by core_y(k - 1) while the sweeps ran;
+//     CTA 1    KKT score of iteration k - 1 and the stopping rule;
+//   core_y(k)  1 CTA on a side stream, concurrent with the left sweep of
+//              iteration k (which needs xc_k only): yc_k, then Minv, P1,
+//              G_L xc_k, G_R yc_k^T for core_x(k + 1);
+//   left sweep(k) -> right sweep(k) (after core_y(k)) -> reduce.
+// xc_k is published in scratch (xcn, Zl) and copied to the caller's xc by
+// core_y(k), which runs only when the score CTA did not stop the run, so xc,
+// yc stay those of the last completed iteration. L^T dU and R dV^T are
+// double-buffered by the parity of k (iteration k reads k - 1's, writes its
+// own), so recomputing an iteration's core_x on resume is idempotent.
+// ---------------------------------------------------------------------------
+struct CoreBufs {
+  double *Zl, *Zr;    // s x r operands of the sweeps: xc, yc^T
+  double *GL, *GR;    // ldg x ldg Gram matrices of the panels
+  double *DL, *DR;    // [2][kMaxD * kMaxD]: L^T dU, R dV^T (s x r) by iteration parity
+  double *Minv;       // r x r
+  double *P1;         // s x r: core yc^T
+  double *GLx, *GRy;  // s x r: G_L xc, G_R yc^T
+  double *xcn;        // s x r: xc of the iteration being swept
+};
+constexpr int kCoreBufDoubles = 13 * kMaxD * kMaxD;
+
+__global__ void __launch_bounds__(kCT) core_x(const double* __restrict__ core, const double* __restrict__ sums,
+                                               const double* __restrict__ xc, const double* __restrict__ yc,
+                                               CoreBufs cb, int s, int r, double pu, double pv, double step,
+                                               double tol, double* trace, double* scores, SCtrl* ctrl, int k,
+                                               int max_iter, int solve) {
+  if (ctrl->done) return;
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ double red[3 * (kCT / 32)];
+  const int tid = threadIdx.x, sr = s * r, len = sums_len(s, r);
+  const double* sl = sums;         // left: L^T U | - | sums
+  const double* srt = sums + len;  // right: R V^T (as s x r) | - | sums
+  const double* DLo = cb.DL + ((k + 1) & 1) * kMaxD * kMaxD;
+  const double* DRo = cb.DR + ((k + 1) & 1) * kMaxD * kMaxD;
+  double* DLn = cb.DL + (k & 1) * kMaxD * kMaxD;
+  double* DRn = cb.DR + (k & 1) * kMaxD * kMaxD;
+  if (blockIdx.x == 0) {
+    // ---- xc = (core yc^T + pu L^T U - L^T dU) (yc yc^T + pu I)^-1 (nmf.py:342-343) ----
+    if (!solve || k >= max_iter) return;
+    double* rhs = (double*)sm;  // s x r
+    double* Mi = rhs + sr;      // r x r
+    for (int i = tid; i < r * r; i += kCT) Mi[i] = cb.Minv[i];
+    for (int i = tid; i < sr; i += kCT) {
+      const double dl = k > 0 ? DLo[i] + step * pu * (cb.GLx[i] - sl[i]) : 0.0;
+      DLn[i] = dl;
+      rhs[i] = cb.P1[i] + (pu * sl[i] - dl);
+    }
+    __syncthreads();
+    small_gemm(s, r, r, rhs, r, 1, Mi, r, 1, [&](int a, int c, double v) {
+      cb.xcn[a * r + c] = v;
+      cb.Zl[a * r + c] = v;
+    });
+    return;
+  }
+  // ---- KKT score of iteration k - 1 (nmf.py:281-303) and the stopping rule ----
+  if (k == 0) return;
+  double* E = (double*)sm;      // s x s: xc yc - core
+  double* coreS = E + s * s;    // s x s
+  double* xcS = coreS + s * s;  // s x r
+  double* ycS = xcS + sr;       // r x s
+  for (int i = tid; i < s * s; i += kCT) coreS[i] = core[i];
+  for (int i = tid; i < sr; i += kCT) {
+    xcS[i] = xc[i];
+    ycS[i] = yc[i];
+    DRn[i] = DRo[i] + step * pv * (cb.GRy[i] - srt[i]);
+  }
+  __syncthreads();
+  double obj = 0.0, t1 = 0.0, t2 = 0.0;
+  small_gemm(s, s, r, xcS, r, 1, ycS, s, 1, [&](int a, int c, double v) {
+    const double e = v - coreS[a * s + c];
+    E[a * s + c] = e;
+    obj += e * e;
+  });
+  __syncthreads();
+  small_gemm(s, r, s, E, s, 1, ycS, 1, s, [&](int a, int j, double v) {  // (E yc^T + L^T dU)[a][j]
+    const double w = v + (DLo[a * r + j] + step * pu * (cb.GLx[a * r + j] - sl[a * r + j]));
+    t1 += w * w;
+  });
+  small_gemm(r, s, s, xcS, 1, r, E, s, 1, [&](int j, int c, double v) {  // (xc^T E + dV R^T)[j][c]
+    const double w = v + DRn[c * r + j];
+    t2 += w * w;
+  });
+  block_sum(t1, red, 0);
+  block_sum(t2, red, 1);
+  block_sum(obj, red, 2);
+  __syncthreads();
+  if (tid == 0) {
+    double a1 = 0, a2 = 0, ob = 0;
+    for (int w = 0; w < kCT / 32; ++w) {
+      a1 += red[w];
+      a2 += red[(kCT / 32) + w];
+      ob += red[2 * (kCT / 32) + w];
+    }
+    const double sc = fmax(fmax(fmax(sqrt(a1), sqrt(a2)), fmax(sqrt(sl[2 * sr]), sqrt(srt[2 * sr]))),
+                           fmax(sqrt(sl[2 * sr + 1] + sl[2 * sr + 2] + sl[2 * sr + 3]),
+                                sqrt(srt[2 * sr + 1] + srt[2 * sr + 2] + srt[2 * sr + 3])));
+    const int it = k - 1;
+    trace[it] = ob;
+    scores[it] = sc;
+    ctrl->k = k;
+    if (sc < tol || k >= max_iter) {
+      ctrl->done = 1;
+      ctrl->iters = k;
+    } else if (it >= 50 && sc > 10.0 * scores[it - 50]) {
+      ctrl->diverged = it;
+      ctrl->done = 1;
+      ctrl->iters = k;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCT) core_y(const double* __restrict__ core, const double* __restrict__ sums,
+                                               double* __restrict__ xc, double* __restrict__ yc, CoreBufs cb, int ldg,
+                                               int s, int r, double pu, double pv, const SCtrl* ctrl, int k,
+                                               int first) {
+  if (ctrl->done) return;
+  extern __shared__ __align__(16) unsigned char sm[];
+  double* G = (double*)sm;         // s x s: G_L, then G_R
+  double* B = G + s * s;           // rhs2 (r x s)
+  double* M = B + ((r * s + s * s) & 1) + r * s;  // r x r (even offset: piv below stays 16-byte aligned)
+  double* piv = M + ((r * r + 1) & ~1);
+  double* coreS = piv + kPivDoubles;  // s x s
+  double* xcS = coreS + s * s;        // s x r
+  double* ycS = xcS + s * r;          // r x s
+  const int tid = threadIdx.x, sr = s * r, len = sums_len(s, r);
+  const double* srt = sums + len;
+  for (int i = tid; i < s * s; i += kCT) {
+    coreS[i] = core[i];
+    G[i] = cb.GL[(i / s) * ldg + i % s];
+  }
+  if (first) {
+    // yc = V R^T (nmf.py:338): the reduced right sums of the initial state;
+    // dU = dV = 0
+    for (int i = tid; i < sr; i += kCT) {
+      const int a = i / s, c = i % s;
+      const double v = srt[c * r + a];
+      yc[i] = v;
+      ycS[i] = v;
+      cb.Zr[c * r + a] = v;
+      xcS[i] = xc[i];
+    }
+    for (int i = tid; i < 2 * kMaxD * kMaxD; i += kCT) cb.DL[i] = cb.DR[i] = 0.0;
+    __syncthreads();
+  } else {
+    const double* DRn = cb.DR + (k & 1) * kMaxD * kMaxD;
+    for (int i = tid; i < sr; i += kCT) {
+      const double v = cb.xcn[i];
+      xc[i] = v;
+      xcS[i] = v;
+    }
+    __syncthreads();
+    // ---- yc = (xc^T xc + pv I)^-1 (xc^T core + pv V R^T - dV R^T) (nmf.py:344-345) ----
+    small_gemm(r, r, s, xcS, 1, r, xcS, r, 1, [&](int a, int c, double v) { M[a * r + c] = v + (a == c ? pv : 0.0); });
+    small_gemm(r, s, s, xcS, 1, r, coreS, s, 1, [&](int a, int c, double v) {  // rhs2 (r x s) in B
+      B[a * s + c] = v + (pv * srt[c * r + a] - DRn[c * r + a]);
+    });
+    spd_inverse(M, piv, r);
+    small_gemm(r, s, r, M, r, 1, B, s, 1, [&](int a, int c, double v) {
+      yc[a * s + c] = v;
+      ycS[a * s + c] = v;
+      cb.Zr[c * r + a] = v;  // Z for the right rows: yc^T (s x r)
+    });
+    __syncthreads();
+  }
+  // ---- for core_x(k + 1), while the sweeps run ----
+  small_gemm(s, r, s, G, s, 1, xcS, r, 1, [&](int a, int j, double v) { cb.GLx[a * r + j] = v; });
+  small_gemm(r, r, s, ycS, s, 1, ycS, 1, s, [&](int a, int c, double v) { M[a * r + c] = v + (a == c ? pu : 0.0); });
+  small_gemm(s, r, s, coreS, s, 1, ycS, 1, s, [&](int a, int c, double v) { cb.P1[a * r + c] = v; });
+  __syncthreads();
+  for (int i = tid; i < s * s; i += kCT) G[i] = cb.GR[(i / s) * ldg + i % s];
+  spd_inverse(M, piv, r);  // (barriers on entry and exit)
+  for (int i = tid; i < r * r; i += kCT) cb.Minv[i] = M[i];
+  small_gemm(s, r, s, G, s, 1, ycS, 1, s, [&](int c, int j, double v) { cb.GRy[c * r + j] = v; });
+}
+
 __global__ void init_sctrl(SCtrl* c) {
   c->k = 0;
   c->done = 0;
@@ -710,45 +912,75 @@ __global__ void init_sctrl(SCtrl* c) {
 
 }  // namespace
 
+namespace {
+// side stream and fork / join events of the streaming driver, one set per device
+int stream_side(cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  static cudaEvent_t forks[64] = {}, joins[64] = {};
+  int dev = 0;
+  CNMF_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(CNMF_ERR_CUDA, "device index out of range");
+  std::lock_guard<std::mutex> lk(mu);
+  if (streams[dev] == nullptr) {
+    CNMF_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+    CNMF_CUDA(cudaEventCreateWithFlags(&forks[dev], cudaEventDisableTiming));
+    CNMF_CUDA(cudaEventCreateWithFlags(&joins[dev], cudaEventDisableTiming));
+  }
+  *side = streams[dev];
+  *fork = forks[dev];
+  *join = joins[dev];
+  return CNMF_OK;
+}
+}  // namespace
+
 int admm_stream_run(const double* core, const float* L, int64_t m, const float* Rt, int64_t n, int s, int r, double* u,
                     double* du, double* vt, double* dvt, double* xc, double* yc, double pu, double pv, double step,
                     int max_iter, double tol, double* trace, double* scores, int* iterations, void* ws, int resume,
                     int step_limit, cudaStream_t st) {
   const int S = s <= 32 ? 32 : 64;
   SCtrl* ctrl = (SCtrl*)ws;
-  int dev = 0, sms = 0;
-  CNMF_CUDA(cudaGetDevice(&dev));
-  CNMF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // row blocks: as many as are resident at once, split between the sides by row count
+  const int sms = device_sms();
+  // row blocks: as many as are resident at once. The start-up sweep splits
+  // them between the sides by row count; an iteration sweeps the left rows on
+  // all but two SMs (core_y runs beside it), then the right rows on all.
   const int total = sweep_blocks(sms);
   const int nbl = (int)std::max<int64_t>(1, std::min<int64_t>(total - 1, (total * m + (m + n) / 2) / (m + n)));
   const int nbr = total - nbl;
+  const int gl = std::max(1, total - 2), gr = total;
   const int len = sums_len(s, r);
-  // library scratch: block partials, reduced sums, Z operands
-  const size_t need = ((size_t)total * len + 2 * (size_t)len + 6 * kMaxD * kMaxD) * 8;
+  // library scratch: block partials, reduced sums, the core kernels' buffers
+  const size_t need = ((size_t)(gl + gr) * len + 2 * (size_t)len + kCoreBufDoubles) * 8;
   void* scr = nullptr;
   CNMF_TRY(device_scratch("admm-stream", need, &scr, st));
   double* scratch = (double*)scr;
   double* part = scratch;
-  double* sums = part + (size_t)total * len;
-  double* Zl = sums + 2 * len;
-  double* Zr = Zl + kMaxD * kMaxD;
-  double* GL = Zr + kMaxD * kMaxD;  // L^T L and R R^T (S x S), for the dual-projection recurrence
-  double* GR = GL + kMaxD * kMaxD;
-  double* DL = GR + kMaxD * kMaxD;  // L^T dU, R dV^T (s x r)
-  double* DR = DL + kMaxD * kMaxD;
-  const size_t core_smem = (2 * (size_t)s * s + 3 * (size_t)s * r + (size_t)r * r + 3 + kPivDoubles) * 8;
+  double* sums = part + (size_t)(gl + gr) * len;
+  double* cbp = sums + 2 * len;
+  constexpr int D2 = kMaxD * kMaxD;
+  const CoreBufs cb{cbp,          cbp + D2,     cbp + 2 * D2,  cbp + 3 * D2,  cbp + 4 * D2, cbp + 6 * D2,
+                    cbp + 8 * D2, cbp + 9 * D2, cbp + 10 * D2, cbp + 11 * D2, cbp + 12 * D2};
+  const size_t corey_smem = (2 * (size_t)s * s + 3 * (size_t)s * r + (size_t)r * r + 3 + kPivDoubles) * 8;
+  const size_t corex_smem = (2 * (size_t)s * s + 2 * (size_t)s * r + (size_t)r * r) * 8;
   CNMF_TRY(ensure_smem_attr((const void*)row_sweep<32>, (int)sweep_smem<32>()));
   CNMF_TRY(ensure_smem_attr((const void*)row_sweep<64>, (int)sweep_smem<64>()));
-  CNMF_TRY(ensure_smem_attr((const void*)core_step, (int)((6 * kMaxD * kMaxD + 3 + kPivDoubles) * 8)));
+  CNMF_TRY(ensure_smem_attr((const void*)core_y, (int)((6 * D2 + 3 + kPivDoubles) * 8)));
+  CNMF_TRY(ensure_smem_attr((const void*)core_x, (int)(5 * D2 * 8)));
+  cudaStream_t side;
+  cudaEvent_t fork, join;
+  CNMF_TRY(stream_side(&side, &fork, &join));
   const SSide sl{L, m, S, u, du, pu}, sr{Rt, n, S, vt, dvt, pv};
-  auto sweep = [&](int update) -> int {
+  // grid blocks, the first nl of them on the left rows, partials from part + off
+  auto sweep = [&](int grid, int nl, size_t off, int update) -> int {
     if (S == 32)
-      row_sweep<32><<<total, kSW, sweep_smem<32>(), st>>>(sl, sr, nbl, Zl, Zr, s, r, step, update, part, ctrl);
+      row_sweep<32><<<grid, kSW, sweep_smem<32>(), st>>>(sl, sr, nl, cb.Zl, cb.Zr, s, r, step, update, part + off, ctrl);
     else
-      row_sweep<64><<<total, kSW, sweep_smem<64>(), st>>>(sl, sr, nbl, Zl, Zr, s, r, step, update, part, ctrl);
+      row_sweep<64><<<grid, kSW, sweep_smem<64>(), st>>>(sl, sr, nl, cb.Zl, cb.Zr, s, r, step, update, part + off, ctrl);
     CNMF_LAUNCH_CHECK();
-    reduce_parts<<<dim3((unsigned)ceil_div(len, kT), 2), kT, 0, st>>>(part, nbl, nbr, len, sums, ctrl, update);
+    return CNMF_OK;
+  };
+  auto reduce = [&](int nl, int nr, int update) -> int {
+    reduce_parts<<<dim3((unsigned)ceil_div(len, kRE), 2), kT, 0, st>>>(part, nl, nr, len, sums, ctrl, update);
     CNMF_LAUNCH_CHECK();
     return CNMF_OK;
   };
@@ -756,11 +988,14 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   if (!resume) {
     init_sctrl<<<1, 1, 0, st>>>(ctrl);
     CNMF_LAUNCH_CHECK();
-    CNMF_TRY(panel_cross(L, L, m, S, GL, st));
-    CNMF_TRY(panel_cross(Rt, Rt, n, S, GR, st));
+    CNMF_TRY(panel_cross(L, L, m, S, cb.GL, st));
+    CNMF_TRY(panel_cross(Rt, Rt, n, S, cb.GR, st));
     CNMF_CUDA(cudaMemsetAsync(du, 0, (size_t)m * r * 8, st));
     CNMF_CUDA(cudaMemsetAsync(dvt, 0, (size_t)n * r * 8, st));
-    CNMF_TRY(sweep(0));  // L^T U and V R^T of the start
+    CNMF_TRY(sweep(total, nbl, 0, 0));  // L^T U and V R^T of the start
+    CNMF_TRY(reduce(nbl, nbr, 0));
+    core_y<<<1, kCT, corey_smem, st>>>(core, sums, xc, yc, cb, S, s, r, pu, pv, ctrl, 0, 1);
+    CNMF_LAUNCH_CHECK();
   } else {
     SCtrl h;
     CNMF_CUDA(cudaMemcpyAsync(&h, ctrl, sizeof h, cudaMemcpyDeviceToHost, st));
@@ -773,16 +1008,24 @@ int admm_stream_run(const double* core, const float* L, int64_t m, const float* 
   }
   const int k1 = step_limit > 0 ? std::min(max_iter, k0 + step_limit) : max_iter;
   for (int k = k0; k < k1; ++k) {
-    core_step<<<1, kCT, core_smem, st>>>(core, sums, xc, yc, Zl, Zr, GL, GR, S, DL, DR, s, r, pu, pv, step, tol,
-                                        trace, scores, ctrl, k,
-                                        max_iter, k == 0 && !resume, 1);
+    core_x<<<2, kCT, corex_smem, st>>>(core, sums, xc, yc, cb, s, r, pu, pv, step, tol, trace, scores, ctrl, k,
+                                       max_iter, 1);
     CNMF_LAUNCH_CHECK();
-    CNMF_TRY(sweep(1));
+    CNMF_CUDA(cudaEventRecord(fork, st));
+    CNMF_CUDA(cudaStreamWaitEvent(side, fork, 0));
+    core_y<<<1, kCT, corey_smem, side>>>(core, sums, xc, yc, cb, S, s, r, pu, pv, ctrl, k, 0);
+    const cudaError_t ey = cudaGetLastError();
+    CNMF_CUDA(cudaEventRecord(join, side));
+    const int rl = ey == cudaSuccess ? sweep(gl, gl, 0, 1) : CNMF_OK;  // left rows: needs xc_k only
+    CNMF_CUDA(cudaStreamWaitEvent(st, join, 0));                       // always join the side stream
+    if (ey != cudaSuccess) return fail(CNMF_ERR_CUDA, std::string("core_y launch: ") + cudaGetErrorString(ey));
+    CNMF_TRY(rl);
+    CNMF_TRY(sweep(gr, 0, (size_t)gl * len, 1));  // right rows: yc_k
+    CNMF_TRY(reduce(gl, gr, 1));
   }
   // score of the last swept iteration (and the stop decision)
-  core_step<<<1, kCT, core_smem, st>>>(core, sums, xc, yc, Zl, Zr, GL, GR, S, DL, DR, s, r, pu, pv, step, tol, trace,
-                                      scores, ctrl, k1,
-                                      max_iter, 0, 0);
+  core_x<<<2, kCT, corex_smem, st>>>(core, sums, xc, yc, cb, s, r, pu, pv, step, tol, trace, scores, ctrl, k1, max_iter,
+                                     0);
   CNMF_LAUNCH_CHECK();
   SCtrl h;
   CNMF_CUDA(cudaMemcpyAsync(&h, ctrl, sizeof h, cudaMemcpyDeviceToHost, st));
@@ -859,7 +1102,7 @@ int admm_shard_sweep(void* ws, const float* L, int64_t m, const float* Rt, int64
     row_sweep<64><<<total, kSW, sweep_smem<64>(), st>>>(sl, sr, nbl, w.Zl, w.Zr, s, r, step, update, (double*)part,
                                                         w.ctrl);
   CNMF_LAUNCH_CHECK();
-  reduce_parts<<<dim3((unsigned)ceil_div(len, kT), 2), kT, 0, st>>>((double*)part, nbl, nbr, len, w.sums, w.ctrl,
+  reduce_parts<<<dim3((unsigned)ceil_div(len, kRE), 2), kT, 0, st>>>((double*)part, nbl, nbr, len, w.sums, w.ctrl,
                                                                     update);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;

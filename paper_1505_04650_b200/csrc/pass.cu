@@ -497,7 +497,7 @@ namespace {
 template <int S>
 __global__ void __launch_bounds__(256)
     panel_cross_kernel(const float* __restrict__ P1, const float* __restrict__ P2, int64_t rows,
-                       double* __restrict__ out) {
+                       double* __restrict__ out) {  // out: [gridDim.x][S * S] block partials
   constexpr int TR = S > 64 ? 32 : 64, NB = S / 4, NBLK = NB * NB, BPT = (NBLK + 255) / 256;
   __shared__ __align__(16) float s1[TR * S];
   __shared__ __align__(16) float s2[TR * S];
@@ -546,15 +546,40 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) atomicAdd(out + (4 * bi + a) * S + 4 * bj + b, g[q][a * 4 + b]);
+      for (int b = 0; b < 4; ++b) out[(size_t)blockIdx.x * S * S + (4 * bi + a) * S + 4 * bj + b] = g[q][a * 4 + b];
   }
+}
+
+// out[e] = sum over blocks of part[block][e], four block segments summed in
+// block order and combined in segment order (bit-reproducible)
+__global__ void __launch_bounds__(256) cross_reduce(const double* __restrict__ part, int nb, int len,
+                                                    double* __restrict__ out) {
+  __shared__ double seg[4][64];
+  const int el = threadIdx.x & 63, sg = threadIdx.x >> 6, e = blockIdx.x * 64 + el;
+  double acc = 0.0;
+  if (e < len) {
+    const int per = (nb + 3) / 4, j1 = min(nb, (sg + 1) * per);
+    for (int j0 = sg * per; j0 < j1; j0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (j0 + j < j1) ? part[(size_t)(j0 + j) * len + e] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += v[j];
+    }
+  }
+  seg[sg][el] = acc;
+  __syncthreads();
+  if (sg == 0 && e < len) out[e] = ((seg[0][el] + seg[1][el]) + seg[2][el]) + seg[3][el];
 }
 
 template <int S>
 int launch_cross(const float* P1, const float* P2, int64_t rows, double* out, cudaStream_t st) {
-  CNMF_CUDA(cudaMemsetAsync(out, 0, (size_t)S * S * 8, st));
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 64), 2 * kNumSMs));
-  panel_cross_kernel<S><<<grid, 256, 0, st>>>(P1, P2, rows, out);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 64), 2 * device_sms()));
+  void* part = nullptr;  // per-block partials (every block writes all S x S entries)
+  CNMF_TRY(device_scratch("panel-cross", (size_t)2 * device_sms() * 128 * 128 * 8, &part, st));
+  panel_cross_kernel<S><<<grid, 256, 0, st>>>(P1, P2, rows, (double*)part);
+  CNMF_LAUNCH_CHECK();
+  cross_reduce<<<S * S / 64, 256, 0, st>>>((const double*)part, (int)grid, S * S, out);
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }

@@ -499,6 +499,49 @@ def test_admm_stream_matches_persistent():
     assert np.allclose(t0, t1, rtol=1e-8)
 
 
+def test_admm_stream_resume_and_tol_stop():
+    # the streaming driver (core_x / core_y split, csrc/admm_stream.cu):
+    # (1) one iteration per call (resume = 1, step_limit = 1: the on_iteration
+    # path) ends in the same state as a single call; (2) a tolerance stop
+    # happens at the persistent kernel's iteration with its xc, yc
+    from paper_1505_04650_b200.nmf import compressed_problem, run_admm
+
+    a = O.dense_lowrank(1500, 900, 20, 0.01, seed=2).astype(np.float32)
+    A = DeviceMatrix(torch.from_numpy(a).cuda())
+    cfg = C.adjust_config(C.CompressionConfig(r=20, r_ov=10, w=4, seed=5), 1500, 900)
+    left, right, core = compressed_problem(A, cfg)
+    run = lambda **kw: run_admm(core, left.panel, 1500, right.panel, 900, cfg, 20, **kw)
+    os.environ["CNMF_ADMM_STREAM"] = "1"
+    try:
+        u0, v0, i0, t0 = run(max_iter=30, tol=0.0)
+        seen = []
+        u1, v1, i1, t1 = run(max_iter=30, tol=0.0,
+                             on_iteration=lambda k, u, du, vt, dvt, xc, yc: seen.append((k, xc.clone(), yc.clone())))
+    finally:
+        os.environ.pop("CNMF_ADMM_STREAM", None)
+    torch.cuda.synchronize()
+    assert i0 == i1 == 30 and [k for k, _, _ in seen] == list(range(30))
+    assert torch.equal(u0, u1) and torch.equal(v0, v1) and t0 == t1  # bit-reproducible, resumed or not
+    # a tolerance the persistent kernel crosses mid-run: the streaming driver
+    # stops at the same iteration with the same state
+    tol, itp = None, None
+    for cand in 10.0 ** np.arange(6, -3, -0.5):
+        up, vp, itp, _ = run(max_iter=200, tol=float(cand))
+        if 3 < itp < 200:
+            tol = float(cand)
+            break
+    assert tol is not None
+    os.environ["CNMF_ADMM_STREAM"] = "1"
+    try:
+        us, vs, its, _ = run(max_iter=200, tol=tol)
+    finally:
+        os.environ.pop("CNMF_ADMM_STREAM", None)
+    torch.cuda.synchronize()
+    assert its == itp, (its, itp, tol)
+    assert (us - up).abs().max().item() <= 1e-6 * up.abs().max().item()
+    assert (vs - vp).abs().max().item() <= 1e-6 * vp.abs().max().item()
+
+
 def test_admm_rank_above_32_matches_oracle():
     # r > 32 with s > 32 (the shape class of configs[4], r = 50) runs on the
     # streaming iteration; parity with the oracle at a size it finishes fast
