@@ -21,7 +21,8 @@
 namespace cnmf {
 
 int nnls_gram(const double*, const double*, int64_t, int, double, int, double*, int64_t*, cudaStream_t,
-              const double* H0 = nullptr, int q0 = 0);
+              const double* H0 = nullptr, int q0 = 0, double* fstate = nullptr, size_t fstride = 0);
+size_t nnls_state_stride(int qmax);
 
 namespace {
 
@@ -482,14 +483,14 @@ int panel_to_f64(const float* src, int64_t rows, int S, double* dst, int64_t ld,
 // Ht: n x k (coefficients transposed). scratch: k*k + n*k doubles.
 int right_factor(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_picks, int k, double tol,
                  double* Ht, double* scratch, int64_t* n_capped, cudaStream_t st, const double* H0 = nullptr,
-                 int q0 = 0) {
+                 int q0 = 0, double* fstate = nullptr, size_t fstride = 0) {
   double* gram = scratch;
   double* target = scratch + (size_t)k * k;
   const size_t sm = (size_t)k * s * 8;
   CNMF_TRY(ensure_smem_attr((const void*)gather_gram, 200 * 1024));
   gather_gram<<<sel_grid(n), kSelThreads, sm, st>>>(W, n, s, ld, W, d_picks, k, gram, target);
   CNMF_LAUNCH_CHECK();
-  return nnls_gram(gram, target, n, k, tol, 0, Ht, n_capped, st, H0, q0);
+  return nnls_gram(gram, target, n, k, tol, 0, Ht, n_capped, st, H0, q0, fstate, fstride);
 }
 
 // residual norms ||W - W[:, picks] H||^2 and ||W||^2 into tot[0..1] (device)
@@ -520,9 +521,23 @@ int select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const doub
   // buffers
   size_t bytes = (size_t)n * ld * 8 /*R*/ + (size_t)n * 8 * 3 /*sq, denom, score*/ + (size_t)n * 2 /*flags*/ +
                  (size_t)64 * 64 * 8 + (size_t)n * 64 * 8 * 3 /*target, H, previous H*/ + 4096 * 16 + 64 * 8 + 1024;
+  // per-column Cholesky factors of the NNLS passive sets, kept from one
+  // refit to the next (the picks grow by appending, so a column's factor
+  // stays valid): n x (33 + r (r + 1) / 2) doubles, 2.1 GB at configs[3];
+  // skipped (factors rebuilt per refit) when it would not fit comfortably
+  // (CNMF_XRAY_FACTORS=0 disables it)
+  const size_t fstride = nnls_state_stride(r);
+  size_t fbytes = (size_t)n * fstride * 8;
+  {
+    size_t free_b = 0, total_b = 0;
+    const char* e = getenv("CNMF_XRAY_FACTORS");
+    if ((e && e[0] == '0') || !xray_warm() || cudaMemGetInfo(&free_b, &total_b) != cudaSuccess ||
+        fbytes + bytes > free_b / 2)
+      fbytes = 0;
+  }
   char* buf = nullptr;
   keep_pool();
-  CNMF_CUDA(cudaMallocAsync((void**)&buf, bytes, st));
+  CNMF_CUDA(cudaMallocAsync((void**)&buf, bytes + fbytes + 256, st));
   char* p = buf;
   auto take = [&](size_t b) {
     char* q = p;
@@ -541,6 +556,7 @@ int select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const doub
   double* blk_v = (double*)take(4096 * 8);
   int64_t* blk_i = (int64_t*)take(4096 * 8);
   int64_t* d_picks = (int64_t*)take(64 * 8);
+  double* fstate = fbytes ? (double*)take(fbytes) : nullptr;
   CNMF_CUDA(cudaMemsetAsync(picked, 0, n, st));
   // denominators and the scorable mask (snmf.py:103-104)
   col_mass<<<grid, kSelThreads, 0, st>>>(W, n, s, ld, mass, denom);
@@ -609,7 +625,7 @@ int select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const doub
     // warm start from the previous refit (the picks only grew by one): the
     // same unique minimiser, a fraction of the exchanges (tools/xray_profile.py)
     CNMF_TRY(right_factor(W, n, s, ld, d_picks, (int)hp.size(), nnls_tol, Ht, scratch, &capped, st,
-                          hp.size() > 1 && xray_warm() ? Hprev : nullptr, (int)hp.size() - 1));
+                          hp.size() > 1 && xray_warm() ? Hprev : nullptr, (int)hp.size() - 1, fstate, fstride));
     CNMF_TRY(refit_norms(W, n, s, ld, d_picks, (int)hp.size(), Ht, R, sq, nullptr, st));
     std::swap(Ht, Hprev);  // Hprev = this refit
   }

@@ -26,6 +26,9 @@ for e in prof.events():
         k = e.name.replace("(anonymous namespace)", "")[:60]
         agg[k][0] += 1
         agg[k][1] += e.time_range.end - e.time_range.start
-print("picks", list(picks)[:12])
+print("picks", [int(x) for x in list(picks)[:12]])
+nn = [e.time_range.end - e.time_range.start for e in prof.events()
+      if e.device_type == torch.autograd.DeviceType.CUDA and "nnls_kernel" in e.name]
+print("nnls us per refit:", " ".join(f"{t:.0f}" for t in nn))
 for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:6]:
     print(f"{t/1e3:10.2f} ms {c:5d} launches {t / c:9.1f} us avg  {k}")
