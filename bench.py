@@ -577,11 +577,12 @@ TRAFFIC = {4: 80.9e9, 1: 353.4e6}
 def admm_roofline(m, n, s, r, ms_per_iter):
     """The ADMM iteration against the fp64 tensor pipe: per iteration the row
     sweep forms P z (2 (m+n) s r flops) and the reduced sums P^T x
-    (2 (m+n) s r; P^T dx follows from the dual recurrence), and streams U, dU,
-    V^T, dV^T (read + write, fp64) plus the fp32 bases; the core step's
-    s x s / r x r work is O(s^3) and does not scale with m + n."""
+    (2 (m+n) s r; P^T dx follows from the dual recurrence), and streams dU,
+    dV^T (read + write) and U, V^T (write only: the update never reads the
+    old x), fp64, plus the fp32 bases; the core step's s x s / r x r work is
+    O(s^3) and does not scale with m + n."""
     flops = 4.0 * (m + n) * s * r
-    bytes_ = 32.0 * (m + n) * r + 4.0 * (m + n) * (32 if s <= 32 else 64)
+    bytes_ = 24.0 * (m + n) * r + 4.0 * (m + n) * (32 if s <= 32 else 64)
     fp64_peak = 37.2  # DMMA m8n8k4 measured on B200 (tools/dmma_probe.cu: 37.1-37.2 TFLOP/s; DFMA 33.9)
     t = ms_per_iter * 1e-3
     return {"bound": "fp64", "achieved": flops / t / 1e12, "peak": fp64_peak, "unit": "TFLOP/s",

@@ -37,6 +37,8 @@ int select_spa(double*, int64_t, int, int64_t, int, int64_t*, int*, void*, size_
 int select_xray(const double*, int64_t, int, int64_t, int, const double*, double, int64_t*, int*, cudaStream_t);
 int right_factor(const double*, int64_t, int, int64_t, const int64_t*, int, double, double*, double*, int64_t*,
                  cudaStream_t, const double* H0 = nullptr, int q0 = 0, double* fstate = nullptr, size_t fstride = 0);
+int right_factor_after_selection(const double*, int64_t, int, int64_t, const int64_t*, int, double, double*, double*,
+                                 int64_t*, cudaStream_t);
 int refit_norms(const double*, int64_t, int, int64_t, const int64_t*, int, const double*, double*, double*, double*,
                 cudaStream_t);
 int nnls_gram(const double*, const double*, int64_t, int, double, int, double*, int64_t*, cudaStream_t,
@@ -227,7 +229,7 @@ int cnmf_right_factor(const double* W, int64_t n, int s, int64_t ld, const int64
   keep_pool();
   double* scratch = nullptr;
   CNMF_CUDA(cudaMallocAsync((void**)&scratch, ((size_t)k * k + (size_t)n * k) * 8, st));
-  int rc = right_factor(W, n, s, ld, d_picks, k, tol, Ht, scratch, n_capped, st);
+  int rc = right_factor_after_selection(W, n, s, ld, d_picks, k, tol, Ht, scratch, n_capped, st);
   cudaFreeAsync(scratch, st);
   return rc;
 }

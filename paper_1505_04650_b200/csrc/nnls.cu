@@ -236,9 +236,9 @@ __device__ __noinline__ double2 nnls_gradient(const double* G, int q, double t0,
   return make_double2(g0, g1);
 }
 
-// H0 (optional, k x q0 with q0 < q): a feasible start -- the solution of the
+// H0 (optional, k x q0 with q0 <= q): a feasible start -- the solution of the
 // same targets over the first q0 design columns (XRAY's previous refit: the
-// picks grow by appending). Its support becomes the initial passive set and
+// picks grow by appending; q0 = q: the right factor after a selection). Its support becomes the initial passive set and
 // the iteration proceeds from it exactly as from any feasible iterate; the
 // minimiser is unique when the design has full column rank, so only the
 // exchange path (not the answer) changes.
@@ -537,7 +537,7 @@ int nnls_gram(const double* gram, const double* target, int64_t k, int q, double
   CNMF_CUDA(cudaMemsetAsync(d_cap, 0, 16, st));
   const int64_t blocks = std::min<int64_t>(ceil_div(k, wpb), 2 * device_sms());
   nnls_kernel<<<(unsigned)blocks, 32 * wpb, smem, st>>>(gram, target, k, q, tol, cap, ridge, H, d_cap,
-                                                        (H0 != nullptr && q0 > 0 && q0 < q) ? H0 : nullptr, q0,
+                                                        (H0 != nullptr && q0 > 0 && q0 <= q) ? H0 : nullptr, q0,
                                                         fstate, fstride, d_cap + 1);
   CNMF_LAUNCH_CHECK();
   unsigned long long hcap = 0;

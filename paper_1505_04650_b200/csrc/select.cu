@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -504,6 +506,24 @@ int refit_norms(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_
   return CNMF_OK;
 }
 
+// The last XRAY run's final refit per device: the right factor that follows
+// a selection (snmf.py:129-137 after snmf.py:74-126) is the same NNLS problem
+// as XRAY's last refit, so it can start from that solution and only has to
+// confirm the KKT conditions (configs[3]: 63 ms from h = 0, ~4 ms from here).
+// A start only: the active-set iteration runs to the same tolerance on the
+// caller's data whatever the cache holds, so a stale entry costs time, not
+// correctness.
+struct XrayLast {
+  const double* W = nullptr;
+  int64_t n = 0, ld = 0;
+  int s = 0, k = 0;
+  double tol = 0.0;
+  std::vector<int64_t> picks;
+  const double* H = nullptr;  // n x k (library scratch "xray-last-H")
+};
+static std::mutex g_xray_last_mu;
+static std::map<int, XrayLast> g_xray_last;
+
 // CNMF_XRAY_WARM=0: every refit from h = 0 like the reference (A/B)
 static bool xray_warm() {
   const char* e = getenv("CNMF_XRAY_WARM");
@@ -629,11 +649,50 @@ int select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const doub
     CNMF_TRY(refit_norms(W, n, s, ld, d_picks, (int)hp.size(), Ht, R, sq, nullptr, st));
     std::swap(Ht, Hprev);  // Hprev = this refit
   }
+  if (status == CNMF_OK && (int)hp.size() == r && xray_warm()) {
+    // keep the final refit (Hprev after the swap) for the right factor
+    void* keep = nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        device_scratch("xray-last-H", (size_t)n * r * 8, &keep, st) == CNMF_OK &&
+        cudaMemcpyAsync(keep, Hprev, (size_t)n * r * 8, cudaMemcpyDeviceToDevice, st) == cudaSuccess) {
+      std::lock_guard<std::mutex> lk(g_xray_last_mu);
+      XrayLast& e = g_xray_last[dev];
+      e.W = W;
+      e.n = n;
+      e.ld = ld;
+      e.s = s;
+      e.k = r;
+      e.tol = nnls_tol;
+      e.picks = hp;
+      e.H = (const double*)keep;
+    }
+  }
   CNMF_CUDA(cudaStreamSynchronize(st));
   CNMF_CUDA(cudaFreeAsync(buf, st));
   for (size_t a = 0; a < hp.size(); ++a) picks_host[a] = hp[a];
   *n_picks = (int)hp.size();
   return status;
+}
+
+// right_factor started from the last XRAY refit when it solved this very
+// problem (same reduced matrix, picks in the same order, tolerance)
+int right_factor_after_selection(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_picks, int k,
+                                 double tol, double* Ht, double* scratch, int64_t* n_capped, cudaStream_t st) {
+  const double* H0 = nullptr;
+  int dev = 0;
+  if (xray_warm() && cudaGetDevice(&dev) == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_xray_last_mu);
+    auto it = g_xray_last.find(dev);
+    if (it != g_xray_last.end() && it->second.W == W && it->second.n == n && it->second.ld == ld &&
+        it->second.s == s && it->second.k == k && it->second.tol == tol) {
+      std::vector<int64_t> hp(k);
+      CNMF_CUDA(cudaMemcpyAsync(hp.data(), d_picks, (size_t)k * 8, cudaMemcpyDeviceToHost, st));
+      CNMF_CUDA(cudaStreamSynchronize(st));
+      if (hp == it->second.picks) H0 = it->second.H;
+    }
+  }
+  return right_factor(W, n, s, ld, d_picks, k, tol, Ht, scratch, n_capped, st, H0, H0 ? k : 0);
 }
 
 }  // namespace cnmf
