@@ -178,8 +178,9 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
         const double* pa = Pr + (16 * wm + g) * kLD + tq;  // A[row][c]: rows 16 wm + 8 mi + g
         const double* zb = Z + tq * kLD + 32 * wn + g;     // B[c][k]: k = 32 wn + 8 ni + g
         const int nn = min(4, (r - 32 * wn + 7) >> 3);     // 8-column tiles this warp needs
+        const int ksn = min(KS, (s + 3) >> 2);  // k steps that hold columns c < s
 #pragma unroll 4
-        for (int ks = 0; ks < KS; ++ks) {
+        for (int ks = 0; ks < ksn; ++ks) {
           const double a0 = pa[4 * ks], a1 = pa[8 * kLD + 4 * ks];
           double bv[4];
 #pragma unroll
@@ -266,19 +267,26 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
     // fills tile buffers (P rows -> fp64 Pr, old x by cp.async) two tiles
     // ahead, and reduces P^T x: A[c][row] = Pr[row][c] (c = 16 wm + 8 mi + g),
     // B[row][k] = Xs[row][k]
-    auto fill = [&](int64_t t) {
-      const int buf = (int)(t & 1);
+    // a tile's panel rows are fetched into registers (fill_load) before the
+    // reduction of the tile two back, whose buffer they go to, and stored
+    // after it (fill_store): the loads' HBM latency hides under the DMMAs
+    constexpr int PF = kRT * (SP / 4) / kT;
+    float4 pf[PF];
+    auto fill_load = [&](int64_t t) {
       const int64_t t0 = r0 + t * kRT;
       const int nr = (int)min64(kRT, r1 - t0);
-      double* Pr = PrB + buf * kRT * kLD;
-      double* Xs = XsB + buf * kRT * kLD;
-      constexpr int PF = kRT * (SP / 4) / kT;
-      float4 pf[PF];
 #pragma unroll
       for (int j = 0; j < PF; ++j) {
         const int i = tid + j * kT, row = i / (SP / 4), c4 = 4 * (i % (SP / 4));
         pf[j] = (row < nr) ? __ldg((const float4*)(sd.P + (t0 + row) * sd.ldp + c4)) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+    };
+    auto fill_store = [&](int64_t t) {
+      const int buf = (int)(t & 1);
+      const int64_t t0 = r0 + t * kRT;
+      const int nr = (int)min64(kRT, r1 - t0);
+      double* Pr = PrB + buf * kRT * kLD;
+      double* Xs = XsB + buf * kRT * kLD;
       // the old x is needed only by the start-up sweep (update = 0: P^T x of
       // the initial splits); an update sweep overwrites every entry of Xs
       if (update) {
@@ -316,9 +324,13 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
       for (int ni = 0; ni < 4; ++ni) au[mi][ni][0] = au[mi][ni][1] = 0.0;
     const bool con = 16 * wm < s;
     const int nn = min(4, (r - 32 * wn + 7) >> 3);
-    for (int64_t t = 0; t < ntile && t < 2; ++t) fill(t);
+    for (int64_t t = 0; t < ntile && t < 2; ++t) {
+      fill_load(t);
+      fill_store(t);
+    }
     for (int64_t t = 0; t < ntile; ++t) {
       const int buf = (int)(t & 1);
+      if (t + 2 < ntile) fill_load(t + 2);
       nbar_sync(kBarFull + buf, kSW);
       if (con) {
         const double* pa = PrB + buf * kRT * kLD + tq * kLD + 16 * wm + g;
@@ -339,7 +351,7 @@ __global__ void __launch_bounds__(kSW, 1) row_sweep(SSide L, SSide R, int nbl, c
       }
       if (t + 2 < ntile) {
         nbar_sync(kBarR, kT);  // every reduction warp is done reading buffer buf
-        fill(t + 2);
+        fill_store(t + 2);
       }
     }
     if (con) {

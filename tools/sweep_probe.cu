@@ -9,10 +9,12 @@
 #include <vector>
 
 int main() {
-  const int s = 30, S = 32, reps = 40;
-  const int64_t rows[2] = {10000, 5000};
+  // SW_S / SW_ROWS0 / SW_ROWS1: basis width and panel heights (default configs[1]; configs[4]: 60 200000 100000)
+  const int s = getenv("SW_S") ? atoi(getenv("SW_S")) : 30, S = s <= 32 ? 32 : 64, reps = 40;
+  const int64_t rows[2] = {getenv("SW_ROWS0") ? atoll(getenv("SW_ROWS0")) : 10000,
+                           getenv("SW_ROWS1") ? atoll(getenv("SW_ROWS1")) : 5000};
   cnmf::SweepPanel p[2];
-  std::vector<float> h(10000 * S);
+  std::vector<float> h((size_t)rows[0] * S);
   srand(3);
   for (size_t i = 0; i < h.size(); ++i) h[i] = (i % S) < (size_t)s ? rand() / (float)RAND_MAX - 0.5f : 0.f;
   for (int k = 0; k < 2; ++k) {
@@ -47,9 +49,9 @@ int main() {
     unsigned long long t[512][12];
     cudaMemcpyFromSymbol(t, cnmf::g_sw_t, sizeof t);
     unsigned long long t0 = ~0ull;
-    const int nbk = np == 2 ? 236 : 157;
+    const int nbk = 296;
     for (int b = 0; b < nbk; ++b) t0 = t[b][0] < t0 ? t[b][0] : t0;
-    auto mx = [&](int k) { unsigned long long m = 0; for (int b = 0; b < nbk; ++b) if (t[b][k] > m && t[b][k] < t0 + 1000000) m = t[b][k]; return (m - t0) * 1e-3; };
+    auto mx = [&](int k) { unsigned long long m = 0; for (int b = 0; b < nbk; ++b) if (t[b][k] > m && t[b][k] < t0 + 100000000) m = t[b][k]; return (m - t0) * 1e-3; };
     auto mn = [&](int k) { unsigned long long m = ~0ull; for (int b = 0; b < nbk; ++b) if (t[b][k] >= t0 && t[b][k] < m) m = t[b][k]; return (m - t0) * 1e-3; };
     printf("  tile loaded max %.2f | gram computed max %.2f\n", mx(8), mx(9));
     printf("  start spread %.2f | gram done max %.2f | partial stored max %.2f | reducers done max %.2f | final reduce %.2f..%.2f | factor done %.2f | T seen min %.2f max %.2f | apply done max %.2f us\n",
