@@ -451,15 +451,25 @@ def run_ours(args):
             ev[0].record(st)
             compress()
             ev[1].record(st)
-            if ws == 1:
-                res = C.snmf(A.t if prec == "fp64" else A, r, selector=c["sel"],
-                             cfg=C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED), precision=prec)
-            else:
-                res = D.snmf(ops, comm, A, m, n, c0, r, selector=c["sel"],
-                             cfg=C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED))
+            try:
+                if ws == 1:
+                    res = C.snmf(A.t if prec == "fp64" else A, r, selector=c["sel"],
+                                 cfg=C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED), precision=prec)
+                else:
+                    res = D.snmf(ops, comm, A, m, n, c0, r, selector=c["sel"],
+                                 cfg=C.CompressionConfig(r=r, r_ov=R_OV, w=c["q"], seed=SEED))
+                info["picks"] = [int(k) for k in res.K]
+            except C.ConvergenceError as e:
+                # the reference's NNLS exchange cap (nnls.py:83-105): with its
+                # absolute tolerance 1e-10 on gradients of size ~1e6
+                # (configs[2]) rounding decides whether it trips -- the
+                # reference itself raises on 4 of 10 fp32-sized perturbations
+                # (profiles/r02_config2_reference_sensitivity.txt). The job
+                # ends here, as the reference's does; the picks are complete.
+                info["job_ended_by"] = "ConvergenceError: " + str(e)
+                info["picks"] = [int(k) for k in getattr(e, "picks", [])]
             ev[2].record(st)
             ev[3].record(st)
-            info["picks"] = [int(k) for k in res.K]
             return 0
 
     for _ in range(args.warmup):
@@ -537,6 +547,8 @@ def run_ours(args):
         line["roofline_admm"] = admm_roofline(m, n, cfg.basis_cols, r, admm_ms / max(it_avg, 1))
     else:
         line["picks_true"] = len(set(info.get("picks", [])) & set(truth or [])) if truth else None
+        if info.get("job_ended_by"):
+            line["job_ended_by"] = info["job_ended_by"]
 
     # ---- end to end through the public API with host buffers ----
     host = None
@@ -612,10 +624,15 @@ def e2e_run(args, cid, host, c0, ncols, comm, ops, pj, abytes):
                                             tol=TOL)
             uh, vh = u.cpu(), vt.cpu()
             return uh.numel() * 8 + vh.numel() * 8 + 8 * len(tr), rel
-        if ws == 1:
-            res = C.snmf(host, r, selector=c["sel"], cfg=pub, precision=c.get("precision", "fp32"))
-        else:
-            res = D.snmf(ops, comm, DeviceMatrix(host), m, n, c0, r, selector=c["sel"], cfg=pub, host_out=True)
+        try:
+            if ws == 1:
+                res = C.snmf(host, r, selector=c["sel"], cfg=pub, precision=c.get("precision", "fp32"))
+            else:
+                res = D.snmf(ops, comm, DeviceMatrix(host), m, n, c0, r, selector=c["sel"], cfg=pub, host_out=True)
+        except C.ConvergenceError as e:  # the reference's exchange cap (see run_ours): .best is the result
+            import numpy as np
+
+            return int(np.asarray(e.best).nbytes), None
         return res.Y.nbytes + res.K.nbytes, res.rel_error_full
 
     call()  # warm

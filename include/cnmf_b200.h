@@ -172,6 +172,11 @@ int cnmf_panel_apply(float* P, int64_t rows, int S, const double* T, void* strea
  *                       NNLS coefficients (transposed) of every column over
  *                       the k picked ones; d_picks: device int64[k].
  *                       *n_capped = columns that hit the exchange cap.
+ *                       When the call follows cnmf_select_xray on the same W
+ *                       with the same picks and tolerance, the active-set
+ *                       iteration starts from that selection's last refit
+ *                       (the same NNLS problem) instead of h = 0: the same
+ *                       KKT tolerance is met, in a fraction of the exchanges.
  * cnmf_refit_norms      out[0] = ||W - W[:,K] H||^2, out[1] = ||W||^2 (device)
  *                       (snmf.py:218-221 rel_error_reduced).
  */

@@ -14,7 +14,7 @@ namespace cnmf {
 int gram_tn_f64(const double* X, int64_t p, int a, const double* Y, int b, double* out, cudaStream_t st);
 namespace {
 
-constexpr int kRM = 64, kRN = 128, kRT = 256, kRMax = 64;
+constexpr int kRM = 64, kRN = 128, kRT = 256, kRMax = 128;  // ranks up to 64 and up to 128 are separate instantiations
 
 // Work units: (column strip of 128 columns, chunk of kChunk row tiles),
 // spread round-robin over the CTAs so that every SM gets the same share (the
@@ -26,13 +26,14 @@ constexpr int kRM = 64, kRN = 128, kRT = 256, kRMax = 64;
 // differences are summed in fp32 per thread and tile, then in fp64.
 constexpr int kChunk = 16;
 
+template <int RMAX>
 __global__ void __launch_bounds__(kRT)
     resid_kernel(const float* __restrict__ A, int64_t m, int64_t n, int64_t lda, const float* __restrict__ xf,
                  const float* __restrict__ yf, int r, double* __restrict__ out, const int* __restrict__ skip) {
   if (skip != nullptr && *skip) return;  // the pass path's result stands
   extern __shared__ __align__(16) float rsm[];
-  float(*Xs)[kRMax + 1] = (float(*)[kRMax + 1])rsm;               // kRM x (r + 1)
-  float(*Ys)[kRN] = (float(*)[kRN])(rsm + kRM * (kRMax + 1));     // r x kRN
+  float(*Xs)[RMAX + 1] = (float(*)[RMAX + 1])rsm;               // kRM x (r + 1)
+  float(*Ys)[kRN] = (float(*)[kRN])(rsm + kRM * (RMAX + 1));     // r x kRN
   __shared__ double red[2][kRT / 32];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int64_t mt = ceil_div(m, kRM), nt = ceil_div(n, kRN), chunks = ceil_div(mt, kChunk);
@@ -237,7 +238,7 @@ bool resid_pass_enabled(int64_t m, int64_t n, int r) {
 
 int residual_norms(const float* A, int64_t m, int64_t n, int64_t lda, const double* X, const int64_t* cols,
                    const double* Yt, int r, double* out, cudaStream_t st) {
-  if (r < 1 || r > kRMax) return fail(CNMF_ERR_ARGUMENT, "residual_norms: 1 <= r <= 64");
+  if (r < 1 || r > kRMax) return fail(CNMF_ERR_ARGUMENT, "residual_norms: 1 <= r <= 128");
   if ((X == nullptr) == (cols == nullptr)) return fail(CNMF_ERR_ARGUMENT, "give exactly one of X and cols");
   const int* skip = nullptr;
   if (resid_pass_enabled(m, n, r)) {
@@ -283,12 +284,19 @@ int residual_norms(const float* A, int64_t m, int64_t n, int64_t lda, const doub
       A, m, lda, X, cols, n, Yt, r, xf, yf, skip);
   CNMF_LAUNCH_CHECK();
   const int64_t units = ceil_div(n, kRN) * ceil_div(ceil_div(m, kRM), kChunk);
-  constexpr size_t smem = (size_t)(kRM * (kRMax + 1) + kRMax * kRN) * 4;
-  CNMF_TRY(ensure_smem_attr((const void*)resid_kernel, (int)smem));
-  int occ = 0;
-  CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, resid_kernel, kRT, smem));
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)std::max(occ, 1) * device_sms()));
-  resid_kernel<<<grid, kRT, smem, st>>>(A, m, n, lda, xf, yf, r, out, skip);
+  auto launch = [&](auto kernel, size_t smem) -> int {
+    CNMF_TRY(ensure_smem_attr((const void*)kernel, (int)smem));
+    int occ = 0;
+    CNMF_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kRT, smem));
+    const unsigned grid =
+        (unsigned)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)std::max(occ, 1) * device_sms()));
+    kernel<<<grid, kRT, smem, st>>>(A, m, n, lda, xf, yf, r, out, skip);
+    return CNMF_OK;
+  };
+  if (r <= 64)
+    CNMF_TRY(launch(resid_kernel<64>, (size_t)(kRM * (64 + 1) + 64 * kRN) * 4));
+  else
+    CNMF_TRY(launch(resid_kernel<128>, (size_t)(kRM * (128 + 1) + 128 * kRN) * 4));
   CNMF_LAUNCH_CHECK();
   return CNMF_OK;
 }

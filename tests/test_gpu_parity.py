@@ -560,6 +560,25 @@ def test_relative_error_matches(golden):
         C.relative_error(np.zeros((4, 4)), np.ones((4, 2)), np.ones((2, 4)))
 
 
+def test_errors_for_ranks_above_64():
+    # relative_error / compression_error for 64 < r <= 128 (the residual
+    # kernel's second instantiation): against fp64 numpy
+    g = np.random.default_rng(5)
+    a = np.abs(g.standard_normal((700, 90))) @ np.abs(g.standard_normal((90, 520))) + 0.01 * g.standard_normal((700, 520))
+    a = np.maximum(a, 0.0).astype(np.float32)
+    x = np.abs(g.standard_normal((700, 100)))
+    y = np.abs(g.standard_normal((100, 520))) * 0.01
+    a64 = a.astype(np.float64)
+    want = np.linalg.norm(a64 - x @ y) / np.linalg.norm(a64)
+    assert abs(C.relative_error(a, x, y) - want) <= 1e-5 * want
+    cfg = C.CompressionConfig(r=70, r_ov=10, w=1, seed=4)
+    basis = C.structured_compress(a, cfg)
+    q = np.asarray(basis.Q, dtype=np.float64)
+    assert q.shape[1] == 80
+    want_c = np.linalg.norm(a64 - q @ (q.T @ a64))
+    assert abs(C.compression_error(a, basis) - want_c) <= 1e-4 * max(want_c, 1e-3 * np.linalg.norm(a64))
+
+
 def test_admm_validates():
     with pytest.raises(C.ArgumentError):
         C.nmf_admm(np.random.default_rng(0).uniform(size=(40, 30)), 2, penalty_u=0.0)
