@@ -319,8 +319,28 @@ def test_xray_config3_shape_small():
     a32 = a.astype(np.float32)
     res = C.snmf(a32, 40, selector="xray", cfg=C.CompressionConfig(r=40, r_ov=10, w=4, seed=6))
     ref = O.snmf(a32.astype(np.float64), 40, selector="xray", cfg=O.Config(40, 10, 4, 6))
-    assert np.array_equal(np.sort(res.K), np.sort(ref.K))
+    assert np.array_equal(res.K, ref.K)  # pick order included
     assert sorted(res.K.tolist()) == truth.tolist()
+
+
+def test_xray_pick_order_and_right_factor_on_the_oracle_reduction(monkeypatch):
+    # the selection and NNLS kernels in isolation: on the ORACLE's reduced
+    # matrix (fp64, configs[3]-like: s = 50, r = 40) the device's XRAY picks
+    # equal the oracle's INCLUDING their order, whatever the NNLS start (warm
+    # refits with kept factors, warm without, cold like the reference), and the
+    # right factor (started from the selection's last refit when one exists)
+    # is the oracle's minimiser
+    a, truth = O.near_separable(1200, 1500, 40, 1.0, 0.01, seed=31)
+    ref = O.snmf(a, 40, selector="xray", cfg=O.Config(40, 10, 4, 6))
+    assert sorted(ref.K.tolist()) == truth.tolist()
+    for warm, factors in (("1", "1"), ("1", "0"), ("0", "1")):
+        monkeypatch.setenv("CNMF_XRAY_WARM", warm)
+        monkeypatch.setenv("CNMF_XRAY_FACTORS", factors)
+        picks = C.select_columns_xray(ref.reduced, 40, mass=ref.mass)
+        assert np.array_equal(picks, ref.K), (warm, factors)
+        y = C.snmf_right_factor(ref.reduced, picks)
+        assert y.min() >= 0.0
+        assert np.abs(y - ref.Y).max() <= 1e-8 * max(1.0, np.abs(ref.Y).max()), (warm, factors)
 
 
 # ---------------------------------------------------------------- ADMM ----
