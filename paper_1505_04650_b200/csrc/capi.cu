@@ -36,13 +36,14 @@ int panel_to_f64(const float*, int64_t, int, double*, int64_t, cudaStream_t);
 int select_spa(double*, int64_t, int, int64_t, int, int64_t*, int*, void*, size_t, cudaStream_t);
 int select_xray(const double*, int64_t, int, int64_t, int, const double*, double, int64_t*, int*, cudaStream_t);
 int right_factor(const double*, int64_t, int, int64_t, const int64_t*, int, double, double*, double*, int64_t*,
-                 cudaStream_t, const double* H0 = nullptr, int q0 = 0, double* fstate = nullptr, size_t fstride = 0);
+                 cudaStream_t, const double* H0 = nullptr, int q0 = 0, double* fstate = nullptr, size_t fstride = 0,
+                 int tld = 0);
 int right_factor_after_selection(const double*, int64_t, int, int64_t, const int64_t*, int, double, double*, double*,
                                  int64_t*, cudaStream_t);
 int refit_norms(const double*, int64_t, int, int64_t, const int64_t*, int, const double*, double*, double*, double*,
                 cudaStream_t);
 int nnls_gram(const double*, const double*, int64_t, int, double, int, double*, int64_t*, cudaStream_t,
-              const double* H0 = nullptr, int q0 = 0, double* fstate = nullptr, size_t fstride = 0);
+              const double* H0 = nullptr, int q0 = 0, double* fstate = nullptr, size_t fstride = 0, int tld = 0);
 size_t nnls_state_stride(int qmax);
 int residual_norms(const float*, int64_t, int64_t, int64_t, const double*, const int64_t*, const double*, int,
                    double*, cudaStream_t);

@@ -245,7 +245,7 @@ __device__ __noinline__ double2 nnls_gradient(const double* G, int q, double t0,
 __global__ void __launch_bounds__(1024) nnls_kernel(const double* __restrict__ gram_g, const double* __restrict__ target, int64_t k, int q,
                             double tol, int cap, double ridge, double* __restrict__ H,
                             unsigned long long* __restrict__ n_capped, const double* __restrict__ H0, int q0,
-                            double* __restrict__ fstate, size_t fstride, unsigned long long* next_col) {
+                            double* __restrict__ fstate, size_t fstride, unsigned long long* next_col, int tld) {
   extern __shared__ double smem[];
   double* G = smem;  // q x q
   const int wpb = blockDim.x / 32;
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(1024) nnls_kernel(const double* __restrict__ g
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int i = lane + 32 * e;
-      t[e] = (i < q) ? target[col * q + i] : 0.0;
+      t[e] = (i < q) ? target[col * tld + i] : 0.0;
       h[e] = 0.0;
       grad[e] = t[e];
     }
@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(1024) nnls_kernel(const double* __restrict__ g
 size_t nnls_state_stride(int qmax) { return (size_t)kStateHead + (size_t)((qmax * (qmax + 1) / 2 + 1) & ~1); }
 
 int nnls_gram(const double* gram, const double* target, int64_t k, int q, double tol, int max_exchanges, double* H,
-              int64_t* n_capped, cudaStream_t st, const double* H0, int q0, double* fstate, size_t fstride) {
+              int64_t* n_capped, cudaStream_t st, const double* H0, int q0, double* fstate, size_t fstride, int tld) {
   if (q < 1 || q > kQMax) return fail(CNMF_ERR_ARGUMENT, "nnls: 1 <= q <= 64 required");
   if (!(tol > 0)) return fail(CNMF_ERR_ARGUMENT, "tol must be positive");
   if (k == 0) return CNMF_OK;
@@ -538,7 +538,7 @@ int nnls_gram(const double* gram, const double* target, int64_t k, int q, double
   const int64_t blocks = std::min<int64_t>(ceil_div(k, wpb), 2 * device_sms());
   nnls_kernel<<<(unsigned)blocks, 32 * wpb, smem, st>>>(gram, target, k, q, tol, cap, ridge, H, d_cap,
                                                         (H0 != nullptr && q0 > 0 && q0 <= q) ? H0 : nullptr, q0,
-                                                        fstate, fstride, d_cap + 1);
+                                                        fstate, fstride, d_cap + 1, tld > 0 ? tld : q);
   CNMF_LAUNCH_CHECK();
   unsigned long long hcap = 0;
   CNMF_CUDA(cudaMemcpyAsync(&hcap, d_cap, 8, cudaMemcpyDeviceToHost, st));

@@ -23,7 +23,7 @@
 namespace cnmf {
 
 int nnls_gram(const double*, const double*, int64_t, int, double, int, double*, int64_t*, cudaStream_t,
-              const double* H0 = nullptr, int q0 = 0, double* fstate = nullptr, size_t fstride = 0);
+              const double* H0 = nullptr, int q0 = 0, double* fstate = nullptr, size_t fstride = 0, int tld = 0);
 size_t nnls_state_stride(int qmax);
 
 namespace {
@@ -154,7 +154,10 @@ __global__ void f32_to_f64_panel(const float* __restrict__ src, int64_t rows, in
 // gram[a][b] = W_{p_a} . W_{p_b};  target[c][k] = W_c . W_{p_k}
 __global__ void __launch_bounds__(kSelThreads)
     gather_gram(const double* __restrict__ W, int64_t n, int s, int64_t ld, const double* __restrict__ Wp,
-                const int64_t* __restrict__ picks, int k, double* __restrict__ gram, double* __restrict__ target) {
+                const int64_t* __restrict__ picks, int k, double* __restrict__ gram, double* __restrict__ target,
+                int a0, int tld) {
+  // target columns [a0, k) are (re)computed, row stride tld: XRAY keeps the
+  // targets of earlier picks (the picks grow by appending) and passes a0 = k - 1
   extern __shared__ double sc[];  // k x s picked columns: rows picks[a] of Wp (Wp = W, or a gathered copy)
   for (int i = threadIdx.x; i < k * s; i += blockDim.x) {
     const int a = i / s, j = i % s;
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(kSelThreads)
       const int i = lane + 32 * q;
       x[q] = (i < s) ? W[c * ld + i] : 0.0;
     }
-    for (int a = 0; a < k; ++a) {
+    for (int a = a0; a < k; ++a) {
       double d = 0.0;
 #pragma unroll
       for (int q = 0; q < kMaxS / 32; ++q) {
@@ -184,7 +187,7 @@ __global__ void __launch_bounds__(kSelThreads)
         if (i < s) d += sc[a * s + i] * x[q];
       }
       d = wsum(d);
-      if (lane == 0) target[c * k + a] = d;
+      if (lane == 0) target[c * tld + a] = d;
     }
   }
 }
@@ -459,7 +462,7 @@ int right_factor_given(const double* W, int64_t n, int s, int64_t ld, const doub
   double* gram = (double*)scr;
   double* target = gram + (size_t)k * k;
   CNMF_TRY(ensure_smem_attr((const void*)gather_gram, 200 * 1024));
-  gather_gram<<<sel_grid(n), kSelThreads, (size_t)k * s * 8, st>>>(W, n, s, ld, P, nullptr, k, gram, target);
+  gather_gram<<<sel_grid(n), kSelThreads, (size_t)k * s * 8, st>>>(W, n, s, ld, P, nullptr, k, gram, target, 0, k);
   CNMF_LAUNCH_CHECK();
   return nnls_gram(gram, target, n, k, tol, 0, Ht, n_capped, st);
 }
@@ -485,14 +488,17 @@ int panel_to_f64(const float* src, int64_t rows, int S, double* dst, int64_t ld,
 // Ht: n x k (coefficients transposed). scratch: k*k + n*k doubles.
 int right_factor(const double* W, int64_t n, int s, int64_t ld, const int64_t* d_picks, int k, double tol,
                  double* Ht, double* scratch, int64_t* n_capped, cudaStream_t st, const double* H0 = nullptr,
-                 int q0 = 0, double* fstate = nullptr, size_t fstride = 0) {
+                 int q0 = 0, double* fstate = nullptr, size_t fstride = 0, int tld = 0) {
+  // tld > 0 (XRAY): the targets live at a fixed place in scratch with row
+  // stride tld and those of the first k - 1 picks are already there
   double* gram = scratch;
-  double* target = scratch + (size_t)k * k;
+  double* target = scratch + (tld > 0 ? (size_t)64 * 64 : (size_t)k * k);
   const size_t sm = (size_t)k * s * 8;
   CNMF_TRY(ensure_smem_attr((const void*)gather_gram, 200 * 1024));
-  gather_gram<<<sel_grid(n), kSelThreads, sm, st>>>(W, n, s, ld, W, d_picks, k, gram, target);
+  gather_gram<<<sel_grid(n), kSelThreads, sm, st>>>(W, n, s, ld, W, d_picks, k, gram, target, tld > 0 ? k - 1 : 0,
+                                                    tld > 0 ? tld : k);
   CNMF_LAUNCH_CHECK();
-  return nnls_gram(gram, target, n, k, tol, 0, Ht, n_capped, st, H0, q0, fstate, fstride);
+  return nnls_gram(gram, target, n, k, tol, 0, Ht, n_capped, st, H0, q0, fstate, fstride, tld);
 }
 
 // residual norms ||W - W[:, picks] H||^2 and ||W||^2 into tot[0..1] (device)
@@ -645,7 +651,7 @@ int select_xray(const double* W, int64_t n, int s, int64_t ld, int r, const doub
     // warm start from the previous refit (the picks only grew by one): the
     // same unique minimiser, a fraction of the exchanges (tools/xray_profile.py)
     CNMF_TRY(right_factor(W, n, s, ld, d_picks, (int)hp.size(), nnls_tol, Ht, scratch, &capped, st,
-                          hp.size() > 1 && xray_warm() ? Hprev : nullptr, (int)hp.size() - 1, fstate, fstride));
+                          hp.size() > 1 && xray_warm() ? Hprev : nullptr, (int)hp.size() - 1, fstate, fstride, r));
     CNMF_TRY(refit_norms(W, n, s, ld, d_picks, (int)hp.size(), Ht, R, sq, nullptr, st));
     std::swap(Ht, Hprev);  // Hprev = this refit
   }
