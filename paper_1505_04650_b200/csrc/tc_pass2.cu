@@ -109,6 +109,37 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 16 / 32 consecutive fp32 columns per warp: one TMEM round trip
+// for what eight x8 loads (each followed by its own wait) fetched
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
+      "[%16];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 // 32 lanes x 16 consecutive 32-bit columns per warp
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
   asm volatile(
@@ -613,22 +644,41 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
       mbar_sleep(&tfull[racc.i], racc.ph);
       tc_fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + racc.i * C::ACC_COLS + cg;
+#ifndef CNMF_PASS2_LDW
+#define CNMF_PASS2_LDW 8  // columns per TMEM drain load; 16 and 32 measured within +-3 % (tools/gpu_r02_ldw.sh): the drain is not the limiter
+#endif
 #pragma unroll
-      for (int j = 0; j < NSUB; ++j)
+      for (int j = 0; j < NSUB; ++j) {
+        if constexpr (C::ACC == 2 || CNMF_PASS2_LDW == 8) {
 #pragma unroll
-        for (int c0 = 0; c0 < 32; c0 += 8) {
-          float v[8];
-          tmem_ld8(taddr + j * C::AW + c0, v);
-          if constexpr (C::ACC == 2) {
-          float vl[8];
-          tmem_ld8(taddr + j * C::AW + S + c0, vl);
+          for (int c0 = 0; c0 < 32; c0 += 8) {
+            float v[8];
+            tmem_ld8(taddr + j * C::AW + c0, v);
+            if constexpr (C::ACC == 2) {
+              float vl[8];
+              tmem_ld8(taddr + j * C::AW + S + c0, vl);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) acc[j][c0 + e] += v[e] + vl[e];
-          } else {
+              for (int e = 0; e < 8; ++e) acc[j][c0 + e] += v[e] + vl[e];
+            } else {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) acc[j][c0 + e] += v[e];
+              for (int e = 0; e < 8; ++e) acc[j][c0 + e] += v[e];
+            }
           }
+        } else if constexpr (CNMF_PASS2_LDW == 16) {
+#pragma unroll
+          for (int c0 = 0; c0 < 32; c0 += 16) {
+            float v[16];
+            tmem_ld16(taddr + j * C::AW + c0, v);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[j][c0 + e] += v[e];
+          }
+        } else {
+          float v[32];
+          tmem_ld32(taddr + j * C::AW, v);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) acc[j][e] += v[e];
         }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[racc.i]);

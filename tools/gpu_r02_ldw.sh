@@ -1,0 +1,10 @@
+# A/B: TMEM drain load width of the pass epilogue (8 / 16 / 32 columns per tcgen05.ld)
+for v in ldw8 default ldw32; do
+  if [ $v = default ]; then unset CNMF_LIB_PATH; else export CNMF_LIB_PATH=$PWD/varlibs/$v.so; fi
+  echo "== $v"
+  IMPL=1 REPS=20 timeout 300 python tools/pass_bench.py 20000 100000 64 2>&1 | grep -v -i warn | tail -2
+  IMPL=1 REPS=20 timeout 300 python tools/pass_bench.py 20000 100000 32 2>&1 | grep -v -i warn | tail -2
+done
+unset CNMF_LIB_PATH
+timeout 900 python -m pytest tests -m gpu -x -q -k "pass or bit_reproducible or compress" 2>&1 | tail -3
+CNMF_LIB_PATH=$PWD/varlibs/ldw32.so timeout 900 python -m pytest tests -m gpu -x -q -k "pass or bit_reproducible or compress" 2>&1 | tail -3
