@@ -2,7 +2,7 @@
 //
 // Reference: nmf.py:53-75 relative_error (blocked over A's rows) and
 // snmf.py:223-230 (full-space error of A[:, K] Y). The product X Y is never
-// materialised: each 64 x 128 tile of A is read once (coalesced float4),
+// materialised: each 128 x 128 tile of A is read once (coalesced float4),
 // the matching rank-r product is formed in registers from shared-memory
 // slices of X and Y, and squared differences are accumulated in fp64.
 #include <algorithm>
@@ -14,36 +14,75 @@ namespace cnmf {
 int gram_tn_f64(const double* X, int64_t p, int a, const double* Y, int b, double* out, cudaStream_t st);
 namespace {
 
-constexpr int kRM = 64, kRN = 128, kRT = 256, kRMax = 128;  // ranks up to 64 and up to 128 are separate instantiations
+constexpr int kRM = 128, kRN = 128, kRT = 256, kRMax = 128;  // ranks up to 64 and up to 128 are separate instantiations
 
 // Work units: (column strip of 128 columns, chunk of kChunk row tiles),
-// spread round-robin over the CTAs so that every SM gets the same share (the
-// previous strips-per-CTA split left a third of the GPU idle for the last
-// strip at configs[4]). X and Y arrive pre-converted to fp32 (xf: m x r,
-// yf: n x r); a CTA keeps its strip's Y slice in shared memory across the
-// chunk's row tiles and issues the loads of a tile of A before forming X Y
-// for it, so the DRAM latency of A overlaps the rank-r products. Squared
-// differences are summed in fp32 per thread and tile, then in fp64.
+// spread round-robin over the CTAs so that every SM gets the same share. X
+// and Y arrive pre-converted to fp32 (xf: m x r, yf: n x r). A CTA keeps its
+// strip's Y slice in shared memory across the chunk's row tiles (k-major:
+// Ys[k][column]) and stages each tile's X rows k-major too (Xs[k][row]), so
+// that a thread's 8 x 8 block of X Y costs four 128-bit shared loads per 64
+// FMAs (the round-1/2 kernel's 4 x 8 blocks took six loads per 32 and were
+// bound by shared-memory bandwidth: 26 TFLOP/s). A is read once, straight
+// into registers, after the products (two CTAs per SM overlap one's loads
+// with the other's FMAs). Squared differences are summed in fp32 per thread
+// and tile, then in fp64.
 constexpr int kChunk = 16;
+constexpr int kRLD = 132;
+static_assert(kRM == kRN && kRLD >= kRM && kRLD % 4 == 0, "slice layout");
 
 template <int RMAX>
-__global__ void __launch_bounds__(kRT)
+__global__ void __launch_bounds__(kRT, 1)
     resid_kernel(const float* __restrict__ A, int64_t m, int64_t n, int64_t lda, const float* __restrict__ xf,
                  const float* __restrict__ yf, int r, double* __restrict__ out, const int* __restrict__ skip) {
   if (skip != nullptr && *skip) return;  // the pass path's result stands
   extern __shared__ __align__(16) float rsm[];
-  float(*Xs)[RMAX + 1] = (float(*)[RMAX + 1])rsm;               // kRM x (r + 1)
-  float(*Ys)[kRN] = (float(*)[kRN])(rsm + kRM * (RMAX + 1));     // r x kRN
+  // k-major slices with a row stride of 132 floats: the staging stores (a warp
+  // writes 32 consecutive k of one row / column) then hit 8 banks instead of 1
+  float(*Xs)[kRLD] = (float(*)[kRLD])rsm;                  // r x kRM
+  float(*Ys)[kRLD] = (float(*)[kRLD])(rsm + RMAX * kRLD);  // r x kRN
   __shared__ double red[2][kRT / 32];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const int64_t mt = ceil_div(m, kRM), nt = ceil_div(n, kRN), chunks = ceil_div(mt, kChunk);
   const int64_t units = nt * chunks;
   double res = 0.0, ref = 0.0;
   const bool vec = (lda & 3) == 0;
+  // a tile's rows of X are one contiguous run of kRM * r floats of xf; thread
+  // t takes elements t, t + 256, ...: (row, k) of element e advance by
+  // (256 / r, 256 % r) per step -- no division in the loops
+  constexpr int NX = kRM * RMAX / kRT;
+  const int q256 = kRT / r, m256 = kRT - q256 * r;
+  const int rr0 = tid / r, k0 = tid - rr0 * r;
+  const int nx = kRM * r;
+  float xn[NX];
+  auto x_fetch = [&](int64_t r0) {  // the tile at row r0 -> registers
+    const int64_t lim = min64((int64_t)nx, (m - r0) * r);
+    const float* src = xf + r0 * r;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      const int i = tid + j * kRT;
+      xn[j] = (i < lim) ? src[i] : 0.f;
+    }
+  };
+  auto x_store = [&]() {  // registers -> Xs (k-major)
+    int rr = rr0, k = k0;
+#pragma unroll
+    for (int j = 0; j < NX; ++j) {
+      if (tid + j * kRT < nx) Xs[k][rr] = xn[j];
+      rr += q256;
+      k += m256;
+      if (k >= r) {
+        k -= r;
+        ++rr;
+      }
+    }
+  };
   int64_t cur_strip = -1;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     const int64_t strip = u / chunks, ch = u - strip * chunks;
     const int64_t c0 = strip * kRN;
+    const int64_t rt0 = ch * kChunk, rt1 = min64(mt, (ch + 1) * kChunk);
+    x_fetch(rt0 * kRM);
     if (strip != cur_strip) {
       __syncthreads();
       for (int i = tid; i < kRN * r; i += kRT) {
@@ -53,18 +92,24 @@ __global__ void __launch_bounds__(kRT)
       }
       cur_strip = strip;
     }
-    const int64_t rt1 = min64(mt, (ch + 1) * kChunk);
-    for (int64_t rt = ch * kChunk; rt < rt1; ++rt) {
+    for (int64_t rt = rt0; rt < rt1; ++rt) {
       const int64_t r0 = rt * kRM;
-      // this thread's 4 rows x 8 columns of the A tile, loaded first
-      float a[4][8];
+      const int nrow = (int)min64(kRM, m - r0);
+      __syncthreads();  // the previous tile's products are done with Xs
+      x_store();
+      __syncthreads();
+      if (rt + 1 < rt1) x_fetch(r0 + kRM);  // the next tile's X rows, in flight during the products
+      // this thread's block of A: rows 8 ty .. + 7, columns 4 tx .. + 3 and
+      // 64 + 4 tx .. + 3, loaded first (in flight during the products too)
+      float a[8][8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t row = r0 + 4 * ty + i;
+      for (int i = 0; i < 8; ++i) {
+        const int64_t row = r0 + 8 * ty + i;
+        const bool rok = 8 * ty + i < nrow;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int64_t col = c0 + 64 * h + 4 * tx;
-          if (row < m && col + 3 < n && vec) {
+          if (rok && col + 3 < n && vec) {
             const float4 v = __ldcs((const float4*)(A + row * lda + col));
             a[i][4 * h] = v.x;
             a[i][4 * h + 1] = v.y;
@@ -72,48 +117,38 @@ __global__ void __launch_bounds__(kRT)
             a[i][4 * h + 3] = v.w;
           } else {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) a[i][4 * h + q] = (row < m && col + q < n) ? A[row * lda + col + q] : 0.f;
+            for (int q = 0; q < 4; ++q) a[i][4 * h + q] = (rok && col + q < n) ? A[row * lda + col + q] : 0.f;
           }
         }
       }
-      __syncthreads();
-      const int nrow = (int)min64(kRM, m - r0);
-      for (int i = tid; i < nrow * r; i += kRT) {  // contiguous fp32 rows of X
-        const int rr = i / r, k = i - rr * r;
-        Xs[rr][k] = xf[(r0 + rr) * r + k];
-      }
-      __syncthreads();
-      float acc[4][8];
+      float acc[8][8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 #pragma unroll 2
       for (int k = 0; k < r; ++k) {
+        const float4 x0 = *(const float4*)&Xs[k][8 * ty];
+        const float4 x1 = *(const float4*)&Xs[k][8 * ty + 4];
         const float4 y0 = *(const float4*)&Ys[k][4 * tx];
         const float4 y1 = *(const float4*)&Ys[k][64 + 4 * tx];
+        const float xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
         const float ys[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float xv = Xs[4 * ty + i][k];
+        for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(xv, ys[j], acc[i][j]);
-        }
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(xs[i], ys[j], acc[i][j]);
       }
+      // rows >= nrow and columns >= n hold a = 0 and X Y = 0 (zero-filled slices)
       float tr = 0.f, tf = 0.f;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const bool rok = 4 * ty + i < nrow;
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int64_t col = c0 + 64 * (j >> 2) + 4 * tx + (j & 3);
-          if (rok && col < n) {
-            const float d = a[i][j] - acc[i][j];
-            tr = fmaf(d, d, tr);
-            tf = fmaf(a[i][j], a[i][j], tf);
-          }
+          const float d = a[i][j] - acc[i][j];
+          tr = fmaf(d, d, tr);
+          tf = fmaf(a[i][j], a[i][j], tf);
         }
-      }
       res += (double)tr;
       ref += (double)tf;
     }
@@ -260,8 +295,8 @@ int residual_norms(const float* A, int64_t m, int64_t n, int64_t lda, const doub
       CNMF_LAUNCH_CHECK();
       return CNMF_OK;
     };
-    if (r <= 64) return launch(resid_kernel<64>, (size_t)(kRM * (64 + 1) + 64 * kRN) * 4);
-    return launch(resid_kernel<128>, (size_t)(kRM * (128 + 1) + 128 * kRN) * 4);
+    if (r <= 64) return launch(resid_kernel<64>, (size_t)(2 * 64 * kRLD) * 4);
+    return launch(resid_kernel<128>, (size_t)(2 * 128 * kRLD) * 4);
   };
   if (try_pass) {
     // The expansion below is only accepted for relative residuals above ~0.1
