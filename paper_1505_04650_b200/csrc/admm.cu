@@ -130,6 +130,15 @@ __device__ __forceinline__ void sstamp(int slot) {
 
 __device__ __forceinline__ double ld(const double* p) { return __ldcg(p); }
 
+// D (8 x 8) += A (8 x 4, row g, column t) B (4 x 8, row t, column g) on the
+// fp64 tensor cores; the accumulator holds row g, columns 2 t, 2 t + 1
+// (g = lane / 4, t = lane % 4)
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
 __device__ __forceinline__ double wsum(double v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -742,7 +751,130 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
           for (int rr = 0; rr < nr; ++rr) g[t] = fma(sm.Pt[rr * (SP + 2) + j], sm.Pt[rr * (SP + 2) + l], g[t]);
       }
     }
-    if (mode == 1) {
+    if (RES && mode == 1) {
+      // Resident slice: both products on the fp64 tensor cores (DMMA m8n8k4).
+      // lx = P X (nr x r, K = s): warp w owns the 8-row tiles w, w + 8, ...,
+      // all r / 8 column tiles of each; then u = max(lx + d/pen, 0),
+      // d += step*pen*(lx - u) (nmf.py:354-357) on the accumulator fragments.
+      const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+      constexpr int NT = RP / 8, KS = SP / 4, NW = kThreads / 32;
+      const int nmt = (nr + 7) >> 3, nnt = min(NT, (r + 7) >> 3);
+      for (int mt0 = warp; mt0 < nmt; mt0 += 2 * NW) {
+        // two row tiles (mt0, mt0 + 8) at a time: 2 x r / 8 independent accumulators
+        double dd[2][NT][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) dd[h][ni][0] = dd[h][ni][1] = 0.0;
+        const bool two = mt0 + NW < nmt;
+        int rrs[2];
+        const double* pa[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          rrs[h] = 8 * (mt0 + h * NW) + g;  // rows >= nr compute on the last row and are dropped
+          pa[h] = sm.Pt + min(rrs[h], nr - 1) * (SP + 2) + tq;
+        }
+        const double* xb = sm.X + tq * LR + g;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const double a0 = pa[0][4 * ks], a1 = pa[1][4 * ks];
+          double bv[NT];
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) bv[ni] = xb[4 * ks * LR + 8 * ni];
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni)
+            if (ni < nnt) {
+              dmma(dd[0][ni], a0, bv[ni]);
+              if (two) dmma(dd[1][ni], a1, bv[ni]);
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int rr = rrs[h];
+          if (rr >= nr || (h == 1 && !two)) continue;
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int b = 8 * ni + 2 * tq + e;
+              if (b >= r) continue;
+              const int i = rr * r + b;
+              const double lx = dd[h][ni][e];
+              const double d0 = Dr[i];
+              const double u = fmax(lx + d0 * invpen, 0.0);
+              const double d1 = d0 + sp_ * (lx - u);
+              Uw[i] = u;
+              Dw[i] = d1;
+              const double fe = lx - u;
+              feas += fe * fe;
+              const double du = d1 * u;
+              comp += du * du + (d1 > 0.0 ? d1 * d1 : 0.0);  // u >= 0: neg(u) = 0
+            }
+        }
+      }
+      __syncthreads();
+      sstamp(4);
+      // L^T U (s x r, K = the slice's rows): warp w takes k steps w % 4, w % 4 + 4,
+      // ... and the row-tile half w / 4 (SP / 16 row tiles x all column tiles:
+      // independent accumulators, short chains); the four K partials meet in
+      // shared memory and one atomic per entry goes to the grid sums
+      static_assert(kThreads == 256 && SP % 16 == 0, "8 warps: 4 K slices x 2 row-tile halves");
+      constexpr int MH = SP / 16;  // row tiles per half
+      {
+        const int kq = warp & 3, half = warp >> 2;
+        const int nkt = (nr + 3) >> 2;
+        double dt[MH][NT][2];
+#pragma unroll
+        for (int mi = 0; mi < MH; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) dt[mi][ni][0] = dt[mi][ni][1] = 0.0;
+        const double* pa = sm.Pt + tq * (SP + 2) + 8 * MH * half + g;  // A[c][row] = Pt[row][c]
+        for (int ks = kq; ks < nkt; ks += 4) {
+          const int ra = 4 * ks + tq;
+          const bool ron = ra < nr;
+          double av[MH], bv[NT];
+#pragma unroll
+          for (int mi = 0; mi < MH; ++mi) av[mi] = ron ? pa[4 * ks * (SP + 2) + 8 * mi] : 0.0;
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) bv[ni] = (ron && 8 * ni + g < r) ? Uw[ra * r + 8 * ni + g] : 0.0;
+#pragma unroll
+          for (int mi = 0; mi < MH; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NT; ++ni)
+              if (ni < nnt) dmma(dt[mi][ni], av[mi], bv[ni]);
+        }
+        if constexpr (4 * SP * RP <= kThreads * 16) {
+          // partial kq of entry (c, b) at fold[kq][c * RP + b]
+          double* fd = sm.fold + kq * (SP * RP);
+#pragma unroll
+          for (int mi = 0; mi < MH; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                fd[(8 * (MH * half + mi) + g) * RP + 8 * ni + 2 * tq + e] = dt[mi][ni][e];
+        } else {
+          // (the fold buffer holds 4 partials only up to 32 x 32: larger cores add them atomically)
+#pragma unroll
+          for (int mi = 0; mi < MH; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int j = 8 * (MH * half + mi) + g, b = 8 * ni + 2 * tq + e;
+                if (j < s && b < r) atomicAdd(&accU[j * kMax + b], dt[mi][ni][e]);
+              }
+        }
+      }
+      if constexpr (4 * SP * RP <= kThreads * 16) {
+        __syncthreads();
+        for (int i = tid; i < s * r; i += kThreads) {
+          const int j = i / r, b = i - j * r;
+          const double* f0 = sm.fold + j * RP + b;
+          atomicAdd(&accU[j * kMax + b], (f0[0] + f0[SP * RP]) + (f0[2 * SP * RP] + f0[3 * SP * RP]));
+        }
+      }
+    } else if (mode == 1) {
       // lx = P X ; u = max(lx + d/pen, 0) ; d += step*pen*(lx - u)   (nmf.py:354-357)
       // 16 threads across b (BJ values each), 16 row groups of BR rows
       constexpr int BJ = RP / 16, BR = (8 / BJ) > 0 ? 8 / BJ : 1;
@@ -797,7 +929,7 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
       __syncthreads();
       sstamp(4);
     }
-    if (own) {
+    if (own && !(RES && mode == 1)) {
       for (int rr = grp; rr < nr; rr += GROUPS) {
         double pv[4], uv[4];
 #pragma unroll
@@ -828,7 +960,8 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
   // lanes of a warp (consecutive blocks) touch consecutive words -- the
   // block-major layout put all 32 lanes on one bank (32-way conflicts)
   double* fold = sm.fold;  // GROUPS x NBLK x 16 <= kThreads x 16 doubles
-  if (GROUPS > 1) {
+  const bool folded = !(RES && mode == 1);  // the DMMA path added its tiles to the grid sums already
+  if (GROUPS > 1 && folded) {
     __syncthreads();
     if (own)
 #pragma unroll
@@ -837,7 +970,7 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
         for (int y = 0; y < 4; ++y) fold[(x * 4 + y) * (GROUPS * NBLK) + grp * NBLK + myb] = au[x][y];
     __syncthreads();
   }
-  if (own && grp == 0) {
+  if (own && grp == 0 && folded) {
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
