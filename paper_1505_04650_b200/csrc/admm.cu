@@ -775,19 +775,43 @@ __device__ void split_side(const Side& a, const Smem<SP, RP>& sm, bool right, in
           pa[h] = sm.Pt + min(rrs[h], nr - 1) * (SP + 2) + tq;
         }
         const double* xb = sm.X + tq * LR + g;
+        // even and odd k steps accumulate separately: a dependent DMMA waits
+        // ~300 cycles for its predecessor, so the chains are kept short and
+        // 4 x r / 8 of them are in flight per warp
+        double de[2][NT][2];
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) de[h][ni][0] = de[h][ni][1] = 0.0;
+        static_assert(KS % 2 == 0, "k steps in pairs");
+#pragma unroll
+        for (int ks = 0; ks < KS; ks += 2) {
           const double a0 = pa[0][4 * ks], a1 = pa[1][4 * ks];
-          double bv[NT];
+          const double a2 = pa[0][4 * ks + 4], a3 = pa[1][4 * ks + 4];
+          double bv[NT], bw[NT];
 #pragma unroll
-          for (int ni = 0; ni < NT; ++ni) bv[ni] = xb[4 * ks * LR + 8 * ni];
+          for (int ni = 0; ni < NT; ++ni) {
+            bv[ni] = xb[4 * ks * LR + 8 * ni];
+            bw[ni] = xb[(4 * ks + 4) * LR + 8 * ni];
+          }
 #pragma unroll
           for (int ni = 0; ni < NT; ++ni)
             if (ni < nnt) {
               dmma(dd[0][ni], a0, bv[ni]);
-              if (two) dmma(dd[1][ni], a1, bv[ni]);
+              dmma(de[0][ni], a2, bw[ni]);
+              if (two) {
+                dmma(dd[1][ni], a1, bv[ni]);
+                dmma(de[1][ni], a3, bw[ni]);
+              }
             }
         }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) {
+            dd[h][ni][0] += de[h][ni][0];
+            dd[h][ni][1] += de[h][ni][1];
+          }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int rr = rrs[h];
