@@ -767,7 +767,9 @@ __global__ void __launch_bounds__(TcCfg2<S>::THREADS, 1)
             for (int j = 0; j < NSUB; ++j) {
               const uint32_t ahi = aslot + j * 2 * BKT + 8 * k, alo = ahi + BKT, d = d0 + j * C::AW;
               tc_mma_ts(d, ahi, blo, idesc, acc0);  // A_hi X_lo
+#ifndef CNMF_VARIANT_2PROD  // (timing probe: two of the three products)
               tc_mma_ts(d, alo, bhi, idesc, 1u);    // + A_lo X_hi
+#endif
             }
           }
 #pragma unroll
