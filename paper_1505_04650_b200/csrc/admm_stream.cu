@@ -5,17 +5,21 @@
 // Reference: nmf.py:306-377 (the loop), nmf.py:281-303 (KKT score); the same
 // arithmetic as oracle/cnmf_oracle.py admm_compressed.
 //
-// One iteration = three launches, all state in HBM:
-//   core_step  (1 block)   KKT score of the previous iteration from the
+// All state in HBM; the kernels of one iteration:
+//   core step              KKT score of the previous iteration from the
 //                          reduced sums, convergence / divergence rule, then
 //                          xc = (core yc^T + pu L^T U - L^T dU)(yc yc^T + pu I)^-1
 //                          yc = (xc^T xc + pv I)^-1 (xc^T core + pv V R^T - dV R^T)
-//   row_sweep  (grid)      every row of both sides: x = max(P z + dx / p, 0),
+//   row_sweep  (grid)      every row of a side: x = max(P z + dx / p, 0),
 //                          dx += step p (P z - x), and the block partials of
-//                          P^T x, P^T dx and the four KKT sums
-//   reduce     (grid)      fixed-order sums of the block partials
-// so every reduction is deterministic. Streaming bytes per iteration:
-// U, dU, V, dV read and written (fp64) + L, R read (fp32).
+//                          P^T x and the four KKT sums
+//   reduce_parts (grid)    fixed-order sums of the block partials
+// so every reduction is deterministic. On one GPU (admm_stream_run) the core
+// step is split into core_x (xc + the score, between two sweeps) and core_y
+// (yc + the next iteration's operands, concurrent with the left sweep); the
+// column-sharded driver (admm_shard_*) runs it as one kernel, core_step,
+// between the host's all-reduces. Streaming bytes per iteration: dU, dV read
+// and written, U, V written (fp64) + L, R read (fp32).
 #include <algorithm>
 #include <cmath>
 #include <mutex>
