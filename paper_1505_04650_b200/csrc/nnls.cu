@@ -11,6 +11,15 @@
 // by one row per entering index (O(p^2) per exchange instead of O(p^3)).
 // Singular passive systems fall back to the reference's ridge
 // 1e-12 * trace(C^T C).
+//
+// The factor lives packed in shared memory with reciprocal diagonals (every
+// substitution step multiplies); a removal rebuilds it by a left-looking
+// column Cholesky (O(p) dependent steps, bit-identical to p row insertions).
+// XRAY's refits are warm: a column starts from its previous solution, and,
+// when the caller keeps per-column factor states (fstate), from its previous
+// factor too -- then neither a rebuild nor the first passive-set solve is
+// needed. Columns are handed to the warps one at a time (their exchange
+// counts vary by an order of magnitude).
 #include <algorithm>
 #include <cfloat>
 #include <cstdio>
