@@ -91,9 +91,11 @@ def _require_feasible(cfg, m, n):
         raise InfeasibleRankError(f"basis width {s} exceeds min(m, n) = {min(m, n)}; adjust_config first")
 
 
-def _compress(a, cfg, side, check=True):
+def _compress(a, cfg, side, check=True, host_basis=True):
     """Device range finder. check=False enqueues without synchronising; the
-    caller must then call ``basis.check()`` before trusting the result."""
+    caller must then call ``basis.check()`` before trusting the result.
+    host_basis=False keeps Q on the device even for a host input (callers
+    that only use the panel, e.g. snmf)."""
     A = DeviceMatrix(a)
     _require_feasible(cfg, A.m, A.n)
     s = cfg.basis_cols
@@ -107,7 +109,7 @@ def _compress(a, cfg, side, check=True):
     _lib.call(name, A.ptr, A.m, A.n, A.lda, s, cfg.w, cfg.seed & MASK64, side, q.data_ptr(), ws.data_ptr(), nbytes,
               stream())
     view = q[:, :s]
-    Q = view.double().cpu().numpy() if (A.on_host and check) else view
+    Q = view.double().cpu().numpy() if (A.on_host and check and host_basis) else view
     basis = CompressionBasis(Q=Q, kind="structured", config=cfg, panel=q)
     basis._ws = ws
     basis._dims = (A.m, A.n, s)

@@ -147,7 +147,7 @@ def _graphs_enabled():
     return os.environ.get("CNMF_GRAPHS", "1") != "0"
 
 
-def compressed_problem(A, cfg, check=True, graph=None):
+def compressed_problem(A, cfg, check=True, graph=None, host_bases=True):
     """Bases and core for the compressed ADMM (nmf.py:120-135, 327-332),
     enqueued back to back (replayed as one CUDA graph unless graph=False or
     CNMF_GRAPHS=0); one status check at the end."""
@@ -181,7 +181,10 @@ def compressed_problem(A, cfg, check=True, graph=None):
     if check:
         _check(left)
         _check(right)
-    if A.on_host:
+    if A.on_host and host_bases:
+        # host copies of the bases for callers that asked for them (nmf_admm
+        # does not return them: at configs[4] the two copies were 144 MB of
+        # pageable D2H, 60 ms of the end-to-end call)
         left.Q = left.panel[:, :s].double().cpu().numpy()
         right.Q = right.panel[:, :s].double().cpu().numpy()
     return left, right, core[:s, :s].contiguous()
@@ -197,7 +200,7 @@ def nmf_admm(a, r, compressed=True, cfg=None, penalty_u=1.0, penalty_v=1.0, step
     if not compressed:
         return _nmf_admm_full(A, r, cfg, penalty_u, penalty_v, step_scale, max_iter, tol, on_iteration)
     cfg = _resolve_config(r, cfg, m, n)
-    left, right, core = compressed_problem(A, cfg)
+    left, right, core = compressed_problem(A, cfg, host_bases=False)
 
     def snapshot(k, u, du, vt, dvt, xc, yc):
         st = AdmmState(xc=out(xc.clone(), A.on_host), yc=out(yc.clone(), A.on_host), u=out(u.clone(), A.on_host),

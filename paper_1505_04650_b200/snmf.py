@@ -171,7 +171,7 @@ def snmf(a, r, selector="spa", reduction="compressed", cfg=None, nnls_tol=1e-10,
         if cfg is None:
             cfg = CompressionConfig(r=r, r_ov=10, w=0, seed=0)
         cfg = adjust_config(cfg, m, n)
-        basis, _ = _compress(A, cfg, 0)
+        basis, _ = _compress(A, cfg, 0, host_basis=False)
         q = basis.panel
     elif reduction == "qr" and n > m:
         # full QR reduction of a fat matrix (snmf.py:140-151): Q is square
