@@ -19,7 +19,7 @@ import torch
 
 from . import _lib
 from .compress import CompressionConfig, _check, _compress_pair, adjust_config
-from .device import MASK64, DeviceMatrix, as_device64, out, stream, zeros
+from .device import MASK64, DeviceMatrix, as_device64, host_result, out, out_into, stream, zeros
 from .errors import ArgumentError, DivergenceError, UndefinedMetricError
 from .rng import Rng, child_seed
 
@@ -200,7 +200,15 @@ def nmf_admm(a, r, compressed=True, cfg=None, penalty_u=1.0, penalty_v=1.0, step
     if not compressed:
         return _nmf_admm_full(A, r, cfg, penalty_u, penalty_v, step_scale, max_iter, tol, on_iteration)
     cfg = _resolve_config(r, cfg, m, n)
-    left, right, core = compressed_problem(A, cfg, host_bases=False)
+    if A.on_host:
+        # enqueue the compression, then allocate and touch the host arrays of
+        # the factors while the GPU works, and only then wait for its status
+        left, right, core = compressed_problem(A, cfg, check=False, host_bases=False)
+        xh, yh = host_result((m, r)), host_result((r, n))
+        _check(left)
+        _check(right)
+    else:
+        left, right, core = compressed_problem(A, cfg, host_bases=False)
 
     def snapshot(k, u, du, vt, dvt, xc, yc):
         st = AdmmState(xc=out(xc.clone(), A.on_host), yc=out(yc.clone(), A.on_host), u=out(u.clone(), A.on_host),
@@ -212,8 +220,10 @@ def nmf_admm(a, r, compressed=True, cfg=None, penalty_u=1.0, penalty_v=1.0, step
     u, vt, iters, trace = run_admm(core, left.panel, m, right.panel, n, cfg, r, penalty_u, penalty_v, step_scale,
                                    max_iter, tol, snapshot if on_iteration is not None else None)
     rel = _rel_error(A, u, vt)
-    return FactorPair(X=out(u, A.on_host), Y=out(vt.t().contiguous(), A.on_host), iterations=iters,
-                      objective_trace=trace, rel_error=rel)
+    if A.on_host:
+        return FactorPair(X=out_into(u, xh), Y=out_into(vt.t(), yh), iterations=iters, objective_trace=trace,
+                          rel_error=rel)
+    return FactorPair(X=u, Y=vt.t().contiguous(), iterations=iters, objective_trace=trace, rel_error=rel)
 
 
 def _nmf_admm_full(A, r, cfg, penalty_u, penalty_v, step_scale, max_iter, tol, on_iteration):
