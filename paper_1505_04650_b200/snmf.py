@@ -15,8 +15,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .compress import CompressionConfig, _compress, _compress_f64, _precision, adjust_config
-from .device import DeviceMatrix, as_device64, out, panel_ld, stream, zeros
+from .compress import CompressionConfig, _check, _compress, _compress_f64, _precision, adjust_config
+from .device import DeviceMatrix, as_device64, host_result, out, out_into, panel_ld, stream, zeros
 from .errors import ArgumentError, ConvergenceError, RankDeficiencyError, UndefinedMetricError
 
 
@@ -167,11 +167,19 @@ def snmf(a, r, selector="spa", reduction="compressed", cfg=None, nnls_tol=1e-10,
         raise ArgumentError(f"rank {r} out of range for a {m}x{n} matrix")
     if selector not in ("spa", "xray"):
         raise ArgumentError(f"unknown selector {selector!r}")
+    yh = None
     if reduction == "compressed":
         if cfg is None:
             cfg = CompressionConfig(r=r, r_ov=10, w=0, seed=0)
         cfg = adjust_config(cfg, m, n)
-        basis, _ = _compress(A, cfg, 0, host_basis=False)
+        if A.on_host:
+            # enqueue the range finder, touch the host array of Y while the
+            # GPU works (device.host_result), then wait for its status
+            basis, _ = _compress(A, cfg, 0, check=False, host_basis=False)
+            yh = host_result((r, n))
+            _check(basis)
+        else:
+            basis, _ = _compress(A, cfg, 0, host_basis=False)
         q = basis.panel
     elif reduction == "qr" and n > m:
         # full QR reduction of a fat matrix (snmf.py:140-151): Q is square
@@ -221,7 +229,7 @@ def snmf(a, r, selector="spa", reduction="compressed", cfg=None, nnls_tol=1e-10,
     _lib.call("cnmf_residual_norms", A.ptr, m, n, A.lda, None, d_picks.data_ptr(), Ht.data_ptr(), len(picks),
               full.data_ptr(), stream())
     res_f, ref_f = full.tolist()
-    Y = out(Ht.t().contiguous(), A.on_host)
+    Y = out_into(Ht.t(), yh) if yh is not None else out(Ht.t().contiguous(), A.on_host)
     return SnmfResult(K=picks, Y=Y, rel_error_reduced=float(np.sqrt(max(res_red, 0.0) / ref_red)),
                       rel_error_full=float(np.sqrt(max(res_f, 0.0) / ref_f)) if ref_f else 0.0)
 
