@@ -583,7 +583,9 @@ def run_ours(args):
 # dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
 # kernel at the configuration's size (ncu --set full of the bench command;
 # profiles/r02_cfg4_pass_ncu_full.txt, profiles/r02_cfg1_pass_ncu_full.txt)
-TRAFFIC = {4: 80.9e9, 1: 353.4e6}
+# configs[4]: forward launches 80.81 GB, transpose launches 86.52 GB; 9 forward
+# and 10 transpose passes per compression -> 83.8 GB per launch on average
+TRAFFIC = {4: 83.8e9, 1: 353.4e6}
 
 
 def admm_roofline(m, n, s, r, ms_per_iter):
